@@ -1,0 +1,174 @@
+/*
+ * include/p2p.h -- C ABI v1 of libp2p, the B200-native (sm_100a) MLFMA near-field (P2P) operator with
+ * the data-redundancy layout of arXiv 2511.21535 ("Modeling the Effect of Data Redundancy on Speedup in
+ * MLFMA Near-Field Computation").
+ *
+ * Citations: P:Lnnn = PAPER.md line nnn (section / equation / table named), S:Lnnn = SPEC.md line nnn,
+ * DESIGN.md §3 C<k> = the numbered reading of a silent / garbled / ambiguous passage.
+ *
+ * The operator (§1: "direct particle-to-particle interactions within neighboring cells, forming a
+ * stencil-like computation"): particles are binned into leaf boxes, Morton-sorted, given E2 neighbour
+ * lists (27-box stencil in 3D, §5.2; 9-box in 2D, §5.1), then each target box's
+ * neighbour sources are gathered into ONE contiguous redundant buffer (§1.1, §5.2.1
+ * "duplicated data enables threads to access contiguous blocks") and every target accumulates its
+ * direct interactions against that buffer.  Two pair kernels:
+ *   P2P_GRAVITY      softened 1/r (PhotoNs-2.0-like; form fixed by S:L253, DESIGN C1-C3):
+ *                    phi_i = -sum_{j!=i} m_j (r^2+eps^2)^{-1/2},  a_i = sum_j m_j d_ij (r^2+eps^2)^{-3/2}
+ *   P2P_HELMHOLTZ2D  the DBIM-MLFMA pattern table ("all 9t^2 neighboring patterns ... loaded
+ *                    into shared memory"): y_i = sum_s sum_j P[i][s t + j] x_j, P from
+ *                    G(r) = (i/4) H0^(1)(k r) (DESIGN C15), complex.
+ *
+ * Pipeline of calls (SPEC's build_uniform_tree + e2_neighbors = p2p_plan_create,
+ * pack_redundant = p2p_restructure, run_p2p_redundant / run_p2p_indexing = p2p_eval):
+ *   p2p_plan_create -> p2p_restructure -> p2p_eval(P2P_REDUNDANT)  (-> p2p_eval ...) -> p2p_destroy
+ *
+ * General conventions
+ *  - Every function returns p2p_status (nothing throws across the ABI); p2p_last_error() gives a
+ *    thread-local message naming the violated invariant (SPEC style).
+ *  - Pointers marked "device" must be CUDA device (or managed) memory of the current device; host
+ *    pointers there are rejected with P2P_ERR_INVALID_ARGUMENT.  Pointers marked "host" are plain host
+ *    memory.  The caller owns every buffer it passes; the plan owns every internal buffer.
+ *  - All device work is stream-ordered on cfg->stream (a cudaStream_t, NULL = legacy default stream).
+ *    p2p_plan_create performs exactly ONE host synchronisation (to learn the box / neighbour / buffer
+ *    sizes); every other compute call only enqueues.  Asynchronous kernel faults surface as
+ *    P2P_ERR_CUDA at the next call or the caller's own synchronisation; CUDA / NCCL errors are sticky
+ *    and leave the plan unusable (destroy it).
+ *  - Outputs are always OVERWRITTEN (never accumulated), in the caller's INPUT order (DESIGN C12).
+ *  - Determinism: outputs are bitwise reproducible for a fixed input and config; P2P_REDUNDANT and
+ *    P2P_INDEXED_BITWISE are bitwise equal; P2P_INDEXED agrees with them within tolerance.
+ */
+#ifndef P2P_H_
+#define P2P_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define P2P_ABI_VERSION 1
+
+typedef struct p2p_plan p2p_plan; /* opaque */
+typedef struct p2p_comm p2p_comm; /* opaque; wraps an ncclComm_t owned by the library */
+
+typedef enum {
+    P2P_OK = 0,
+    P2P_ERR_INVALID_ARGUMENT = 1, /* NULL / host pointer where device required, n < 0, h <= 0, eps <= 0,
+                                     dim/kernel mismatch, periodic dim with nbox < 3, nbox < 1 */
+    P2P_ERR_OUT_OF_DOMAIN = 2,    /* a position outside [lo, lo + nbox*h) in some dim (never clamped);
+                                     p2p_last_error names the first offending input index */
+    P2P_ERR_OUT_OF_MEMORY = 3,
+    P2P_ERR_CUDA = 4,             /* sticky */
+    P2P_ERR_NCCL = 5,             /* sticky */
+    P2P_ERR_BAD_STATE = 6,        /* eval(REDUNDANT) before restructure / after set_charges, ... */
+    P2P_ERR_UNSUPPORTED = 7       /* key overflow (> 1024 boxes per dim in 3D, > 2^32 keys in 2D),
+                                     Helmholtz input that is not a regular t-per-box lattice,
+                                     n_local >= 2^31 */
+} p2p_status;
+
+typedef enum { P2P_GRAVITY = 0, P2P_HELMHOLTZ2D = 1 } p2p_kernel;
+
+/* Working precision: fp32 = fp32 storage, accumulation and outputs; fp64 = fp64 throughout.  Binning,
+ * keys and the rebase of redundant records are always computed in fp64 IEEE arithmetic (C6, C11). */
+typedef enum { P2P_FP32 = 0, P2P_FP64 = 1 } p2p_precision;
+
+typedef enum {
+    P2P_REDUNDANT = 0,      /* stream the restructured per-target-box buffer red[] (the paper's redundant
+                               layout, §5.2.1; DBIM: the zero-padded im2col Xg, §5.1.2) */
+    P2P_INDEXED = 1,        /* non-redundant baseline (§5.2.1 "Particle indices are first loaded,
+                               followed by data access"): neighbour segments of the Morton-sorted
+                               records, located through the neighbour CSR, staged on the fly */
+    P2P_INDEXED_BITWISE = 2 /* test configuration of INDEXED: stages bit-identical copies of red[]
+                               records, so its outputs equal P2P_REDUNDANT bit for bit */
+} p2p_layout;
+
+typedef struct {
+    int32_t dim;                /* 3 for P2P_GRAVITY, 2 for P2P_HELMHOLTZ2D */
+    p2p_kernel kernel;
+    p2p_precision precision;
+    double box_size;            /* h > 0: leaf box edge */
+    double lo[3];               /* domain origin; the domain is lo + [0, nbox*h) per dim */
+    int32_t nbox[3];            /* boxes per dim (>= 1; >= 3 where periodic); unused dims ignored */
+    uint32_t periodic_mask;     /* bit d set => periodic in dim d (gravity only; DBIM is open, C5) */
+    double softening;           /* gravity: eps > 0 (C2) */
+    double wavenumber;          /* helmholtz: k > 0 (C15 uses k = 2 pi / (10 Delta)) */
+    int32_t points_per_box;     /* helmholtz: t, a perfect square; sample spacing Delta = h / sqrt(t) */
+    void *stream;               /* cudaStream_t */
+    p2p_comm *comm;             /* NULL => single GPU; else every rank calls collectively */
+} p2p_config;
+
+/* Build the plan: bin (a1), Morton keys, stable radix sort (a2), permute into Morton-ordered records
+ * (a3), box-offset scan (a4), neighbour CSR + redundant offsets + work items (a5).  Copies what it needs
+ * from the inputs into plan-owned storage; the inputs may be reused once the stream passes this point.
+ *   positions : device, [n_local][dim] row-major, float (FP32) or double (FP64)
+ *   charges   : device, gravity: [n_local] masses (same type as positions);
+ *               helmholtz: [n_local] complex (re, im) pairs of that type
+ *   out       : host, receives the plan (NULL on failure)
+ * One host synchronisation. */
+p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *positions, const void *charges,
+                           p2p_plan **out);
+
+/* a6: build the redundant buffer (gravity: red[R] records {x,y,z,m} rebased to the target box origin,
+ * C11; helmholtz: Xg[B][9][t], zero segments for missing neighbours, C10).  Enqueue only. */
+p2p_status p2p_restructure(p2p_plan *plan);
+
+/* a7/a8 + a9: evaluate every target and scatter to input order.
+ *   potential : device, gravity [n_local] real; helmholtz [n_local] complex (re, im)
+ *   field     : device, gravity [n_local][3] real (the acceleration, C1) or NULL; helmholtz: must be NULL
+ * P2P_REDUNDANT requires a preceding p2p_restructure (else P2P_ERR_BAD_STATE).  Enqueue only. */
+p2p_status p2p_eval(p2p_plan *plan, p2p_layout layout, void *potential, void *field);
+
+/* Replace the charges, keeping the geometry (DBIM reuses its geometry across iterations).
+ * charges: device, same layout as in p2p_plan_create, INPUT order.  Invalidates red[] (restructure
+ * again before eval(REDUNDANT)).  Enqueue only. */
+p2p_status p2p_set_charges(p2p_plan *plan, const void *charges);
+
+/* Free every plan-owned buffer (stream-ordered).  NULL-safe. */
+void p2p_destroy(p2p_plan *plan);
+
+/* ---- introspection for bit-exact parity (copy-out only; never hands out internal pointers) ---- */
+typedef enum {
+    P2P_ARR_PERM = 0,        /* u32 [n_local]   perm[p] = input index of sorted slot p */
+    P2P_ARR_SORTED_KEYS = 1, /* u32 [n_local]   Morton keys in sorted order (helmholtz: box*t + subcell) */
+    P2P_ARR_BOX_KEYS = 2,    /* u32 [n_boxes]   ascending Morton keys of the non-empty boxes */
+    P2P_ARR_BOX_START = 3,   /* u32 [n_boxes+1] first sorted slot of each box, last = n_local */
+    P2P_ARR_NBR_OFF = 4,     /* u32 [n_boxes+1] neighbour CSR offsets (helmholtz: 9 b) */
+    P2P_ARR_NBR_BOX = 5,     /* u32 [n_nbr]     neighbour box index (helmholtz: 0xffffffff = missing) */
+    P2P_ARR_NBR_SLOT = 6,    /* u8  [n_nbr]     stencil slot 0..26 (2D 0..8), ascending per box */
+    P2P_ARR_RED_OFF = 7,     /* u64 [n_boxes+1] first record of each box's redundant run */
+    P2P_ARR_RED = 8          /* gravity: [n_red][4] float/double; helmholtz: [n_boxes][9][t] complex */
+} p2p_array;
+
+typedef struct {
+    int64_t n_local;   /* particles on this rank */
+    int64_t n_boxes;   /* B: non-empty boxes */
+    int64_t n_nbr;     /* neighbour CSR entries */
+    int64_t n_red;     /* R: redundant records (helmholtz: 9 t B) */
+    int64_t n_pairs;   /* I: pair interactions evaluated (gravity incl. i = j; helmholtz non-padded), C19 */
+    int64_t n_items;   /* eval work items */
+    int32_t key_bits;  /* Morton key width */
+    int32_t sort_passes;
+} p2p_info;
+
+/* Both synchronise the plan's stream. `bytes` must equal the array's exact size. */
+p2p_status p2p_get_info(const p2p_plan *plan, p2p_info *out);
+p2p_status p2p_copy_out(const p2p_plan *plan, p2p_array which, void *host_dst, size_t bytes);
+
+/* ---- multi-GPU: NCCL communicator owned by the library ----
+ * The 128 id bytes are produced on rank 0 by p2p_comm_unique_id and broadcast by the caller (e.g. over
+ * a torch.distributed process group); every rank then calls p2p_comm_create collectively. */
+p2p_status p2p_comm_unique_id(void *id_out /* host, 128 bytes */);
+p2p_status p2p_comm_create(int nranks, int rank, const void *id /* host, 128 bytes */, p2p_comm **out);
+void p2p_comm_destroy(p2p_comm *comm);
+
+/* ---- diagnostics ---- */
+const char *p2p_status_string(p2p_status s);
+const char *p2p_last_error(void);        /* thread-local detail of the last failing call on this thread */
+uint64_t p2p_kernel_launch_count(void);   /* number of libp2p kernels launched by this process so far */
+int p2p_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* P2P_H_ */

@@ -57,6 +57,7 @@ def lib():
                 "orc_gravity_red": (None, [i32, i64, p, p, dbl, p, p, u32, p, p, p, p, p, p, p, p]),
                 "orc_gravity_eval_redundant": (None, [i32, i64, p, dbl, p, p, p, p, p, p, p, p, p, p, dbl, p, p]),
                 "orc_gravity_eval_indexed": (None, [i64, p, p, dbl, p, u32, p, p, p, p, p, p, dbl, p, p]),
+                "orc_gravity_eval_indexed_boxes": (None, [i64, p, p, p, dbl, p, u32, p, p, p, p, p, p, dbl, p, p]),
                 "orc_gravity_brute": (i64, [i64, p, p, dbl, p, p, u32, dbl, p, p]),
                 "orc_helm_weight": (None, [dbl, dbl, dbl, p, p]),
                 "orc_helm_table": (None, [i32, dbl, dbl, p]),
@@ -199,6 +200,26 @@ class GravityPlan:
                                        _p(self.nbr_off), _p(self.nbr_box), _p(self.nbr_slot), float(self.inp.eps),
                                        _p(phi), _p(field))
         return phi, field
+
+
+    def eval_indexed_boxes(self, boxes):
+        """plain definition (mode ii) for the targets of the listed boxes only; returns (phi, field) arrays of
+        full length N with NaN outside the listed boxes"""
+        n = self.pos.shape[0]
+        phi = np.full(n, np.nan)
+        field = np.full((n, 3), np.nan)
+        sel = np.ascontiguousarray(np.asarray(boxes, dtype=np.uint32))
+        lib().orc_gravity_eval_indexed_boxes(sel.shape[0], _p(sel), _p(self.pos), _p(self.mass), float(self.inp.h),
+                                             _p(self.nbox), int(self.inp.periodic), _p(self.perm), _p(self.bkey),
+                                             _p(self.bstart), _p(self.nbr_off), _p(self.nbr_box), _p(self.nbr_slot),
+                                             float(self.inp.eps), _p(phi), _p(field))
+        return phi, field
+
+    def pairs_of_boxes(self, boxes) -> int:
+        boxes = np.asarray(boxes, dtype=np.int64)
+        nb = np.diff(self.bstart.astype(np.int64))
+        nsrc = np.diff(self.red_off.astype(np.int64))
+        return int((nb[boxes] * nsrc[boxes]).sum())
 
 
 def gravity_brute(inp):

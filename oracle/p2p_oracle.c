@@ -332,46 +332,68 @@ void orc_gravity_eval_redundant(int prec, int64_t B, const double *pos, double h
 /* a7 + a9, oracle mode (ii) "indexed order" = the plain definition: loop over the neighbour CSR and */
 /* the raw records, d = (x_j + S) - x_i computed in fp64 from the (promoted) input positions.        */
 /* --------------------------------------------------------------------------------------------- */
+static void eval_indexed_box(int64_t b, int nb, const double *pos, const double *mass, double h,
+                             const int32_t *nbox, uint32_t periodic, const uint32_t *perm, const uint32_t *bkey,
+                             const uint32_t *bstart, const uint32_t *nbr_off, const uint32_t *nbr_box,
+                             const uint8_t *nbr_slot, double eps2, double *phi, double *field)
+{
+    int32_t c[3];
+    orc_demorton(3, nb, bkey[b], c);
+    for (uint32_t p = bstart[b]; p < bstart[b + 1]; ++p) {
+        uint32_t i = perm[p];
+        const double *xi = &pos[3 * (int64_t)i];
+        double ph = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
+        for (uint32_t e = nbr_off[b]; e < nbr_off[b + 1]; ++e) {
+            double S[3];
+            slot_shift(nbr_slot[e], c, nbox, periodic, h, S);
+            uint32_t k = nbr_box[e];
+            for (uint32_t q = bstart[k]; q < bstart[k + 1]; ++q) {
+                uint32_t j = perm[q];
+                const double *xj = &pos[3 * (int64_t)j];
+                double dx = (xj[0] + S[0]) - xi[0];
+                double dy = (xj[1] + S[1]) - xi[1];
+                double dz = (xj[2] + S[2]) - xi[2];
+                double r2 = dx * dx + dy * dy + dz * dz + eps2;
+                double rinv = 1.0 / sqrt(r2);
+                double mr3 = mass[j] * rinv * rinv * rinv;
+                if (j != i) ph -= mass[j] * rinv;
+                ax += mr3 * dx;
+                ay += mr3 * dy;
+                az += mr3 * dz;
+            }
+        }
+        phi[i] = ph;
+        field[3 * (int64_t)i + 0] = ax;
+        field[3 * (int64_t)i + 1] = ay;
+        field[3 * (int64_t)i + 2] = az;
+    }
+}
+
 void orc_gravity_eval_indexed(int64_t B, const double *pos, const double *mass, double h, const int32_t *nbox,
                               uint32_t periodic, const uint32_t *perm, const uint32_t *bkey,
                               const uint32_t *bstart, const uint32_t *nbr_off, const uint32_t *nbr_box,
                               const uint8_t *nbr_slot, double eps, double *phi, double *field)
 {
     int nb = orc_bits_per_dim(3, nbox);
-    double eps2 = eps * eps;
 #pragma omp parallel for schedule(dynamic, 16)
-    for (int64_t b = 0; b < B; ++b) {
-        int32_t c[3];
-        orc_demorton(3, nb, bkey[b], c);
-        for (uint32_t p = bstart[b]; p < bstart[b + 1]; ++p) {
-            uint32_t i = perm[p];
-            const double *xi = &pos[3 * (int64_t)i];
-            double ph = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
-            for (uint32_t e = nbr_off[b]; e < nbr_off[b + 1]; ++e) {
-                double S[3];
-                slot_shift(nbr_slot[e], c, nbox, periodic, h, S);
-                uint32_t k = nbr_box[e];
-                for (uint32_t q = bstart[k]; q < bstart[k + 1]; ++q) {
-                    uint32_t j = perm[q];
-                    const double *xj = &pos[3 * (int64_t)j];
-                    double dx = (xj[0] + S[0]) - xi[0];
-                    double dy = (xj[1] + S[1]) - xi[1];
-                    double dz = (xj[2] + S[2]) - xi[2];
-                    double r2 = dx * dx + dy * dy + dz * dz + eps2;
-                    double rinv = 1.0 / sqrt(r2);
-                    double mr3 = mass[j] * rinv * rinv * rinv;
-                    if (j != i) ph -= mass[j] * rinv;
-                    ax += mr3 * dx;
-                    ay += mr3 * dy;
-                    az += mr3 * dz;
-                }
-            }
-            phi[i] = ph;
-            field[3 * (int64_t)i + 0] = ax;
-            field[3 * (int64_t)i + 1] = ay;
-            field[3 * (int64_t)i + 2] = az;
-        }
-    }
+    for (int64_t b = 0; b < B; ++b)
+        eval_indexed_box(b, nb, pos, mass, h, nbox, periodic, perm, bkey, bstart, nbr_off, nbr_box, nbr_slot,
+                         eps * eps, phi, field);
+}
+
+/* The same plain definition restricted to a list of target boxes (bounded CPU-baseline samples and sampled
+ * parity checks at full size); outputs of targets outside the listed boxes are left untouched. */
+void orc_gravity_eval_indexed_boxes(int64_t nsel, const uint32_t *sel, const double *pos, const double *mass,
+                                    double h, const int32_t *nbox, uint32_t periodic, const uint32_t *perm,
+                                    const uint32_t *bkey, const uint32_t *bstart, const uint32_t *nbr_off,
+                                    const uint32_t *nbr_box, const uint8_t *nbr_slot, double eps, double *phi,
+                                    double *field)
+{
+    int nb = orc_bits_per_dim(3, nbox);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t q = 0; q < nsel; ++q)
+        eval_indexed_box((int64_t)sel[q], nb, pos, mass, h, nbox, periodic, perm, bkey, bstart, nbr_off, nbr_box,
+                         nbr_slot, eps * eps, phi, field);
 }
 
 /* --------------------------------------------------------------------------------------------- */

@@ -1,0 +1,308 @@
+"""paper_2511_21535_b200 -- B200-native (sm_100a) MLFMA near-field (P2P) operator with the data-redundancy layout
+of arXiv 2511.21535.
+
+This module is the thin Python binding over the C ABI of libp2p.so (include/p2p.h): argument marshalling only --
+every step of the path (binning, Morton keys, radix sort, box scan, neighbour lists, restructure, evaluation,
+scatter) runs in the library's CUDA kernels.  PyTorch supplies device memory, streams and process groups.  There
+is NO CPU fallback: if libp2p.so is missing or no CUDA device is present the calls raise.
+
+Functions with the C names (p2p_plan_create, p2p_restructure, p2p_eval, p2p_set_charges, p2p_destroy,
+p2p_get_info, p2p_copy_out, p2p_comm_*, p2p_status_string, p2p_last_error, p2p_kernel_launch_count) take raw
+pointers / ints exactly like the ABI; `Plan` and `nearfield` are conveniences over them taking torch tensors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libp2p.so")
+
+# ---- enums (include/p2p.h) ----
+P2P_OK, P2P_ERR_INVALID_ARGUMENT, P2P_ERR_OUT_OF_DOMAIN, P2P_ERR_OUT_OF_MEMORY, P2P_ERR_CUDA, P2P_ERR_NCCL, \
+    P2P_ERR_BAD_STATE, P2P_ERR_UNSUPPORTED = range(8)
+P2P_GRAVITY, P2P_HELMHOLTZ2D = 0, 1
+P2P_FP32, P2P_FP64 = 0, 1
+P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE = 0, 1, 2
+(P2P_ARR_PERM, P2P_ARR_SORTED_KEYS, P2P_ARR_BOX_KEYS, P2P_ARR_BOX_START, P2P_ARR_NBR_OFF, P2P_ARR_NBR_BOX,
+ P2P_ARR_NBR_SLOT, P2P_ARR_RED_OFF, P2P_ARR_RED) = range(9)
+
+LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise": P2P_INDEXED_BITWISE}
+
+EXPORTED = ["p2p_plan_create", "p2p_restructure", "p2p_eval", "p2p_set_charges", "p2p_destroy", "p2p_get_info",
+            "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy", "p2p_status_string",
+            "p2p_last_error", "p2p_kernel_launch_count", "p2p_abi_version"]
+
+
+class P2PConfig(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("kernel", C.c_int), ("precision", C.c_int), ("box_size", C.c_double),
+                ("lo", C.c_double * 3), ("nbox", C.c_int32 * 3), ("periodic_mask", C.c_uint32),
+                ("softening", C.c_double), ("wavenumber", C.c_double), ("points_per_box", C.c_int32),
+                ("stream", C.c_void_p), ("comm", C.c_void_p)]
+
+
+class P2PInfo(C.Structure):
+    _fields_ = [("n_local", C.c_int64), ("n_boxes", C.c_int64), ("n_nbr", C.c_int64), ("n_red", C.c_int64),
+                ("n_pairs", C.c_int64), ("n_items", C.c_int64), ("key_bits", C.c_int32),
+                ("sort_passes", C.c_int32)]
+
+
+class P2PError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_status_name(status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libp2p.so (fails loudly when it has not been built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        p, i64, u64 = C.c_void_p, C.c_int64, C.c_uint64
+        sig = {
+            "p2p_plan_create": (C.c_int, [C.POINTER(P2PConfig), i64, p, p, C.POINTER(C.c_void_p)]),
+            "p2p_restructure": (C.c_int, [p]),
+            "p2p_eval": (C.c_int, [p, C.c_int, p, p]),
+            "p2p_set_charges": (C.c_int, [p, p]),
+            "p2p_destroy": (None, [p]),
+            "p2p_get_info": (C.c_int, [p, C.POINTER(P2PInfo)]),
+            "p2p_copy_out": (C.c_int, [p, C.c_int, p, C.c_size_t]),
+            "p2p_comm_unique_id": (C.c_int, [p]),
+            "p2p_comm_create": (C.c_int, [C.c_int, C.c_int, p, C.POINTER(C.c_void_p)]),
+            "p2p_comm_destroy": (None, [p]),
+            "p2p_status_string": (C.c_char_p, [C.c_int]),
+            "p2p_last_error": (C.c_char_p, []),
+            "p2p_kernel_launch_count": (u64, []),
+            "p2p_abi_version": (C.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _status_name(s: int) -> str:
+    try:
+        return lib().p2p_status_string(int(s)).decode()
+    except Exception:  # noqa: BLE001 -- only used to format an error message
+        return f"status {s}"
+
+
+def _check(s: int):
+    if s != P2P_OK:
+        raise P2PError(s, lib().p2p_last_error().decode())
+
+
+# ---- ABI-shaped functions (raw pointers) ----
+def p2p_plan_create(cfg: P2PConfig, n_local: int, positions: int, charges: int) -> int:
+    out = C.c_void_p()
+    _check(lib().p2p_plan_create(C.byref(cfg), int(n_local), C.c_void_p(positions), C.c_void_p(charges),
+                                 C.byref(out)))
+    return out.value
+
+
+def p2p_restructure(plan: int):
+    _check(lib().p2p_restructure(C.c_void_p(plan)))
+
+
+def p2p_eval(plan: int, layout: int, potential: int, field: int | None):
+    _check(lib().p2p_eval(C.c_void_p(plan), int(layout), C.c_void_p(potential), C.c_void_p(field or None)))
+
+
+def p2p_set_charges(plan: int, charges: int):
+    _check(lib().p2p_set_charges(C.c_void_p(plan), C.c_void_p(charges)))
+
+
+def p2p_destroy(plan: int):
+    lib().p2p_destroy(C.c_void_p(plan))
+
+
+def p2p_get_info(plan: int) -> P2PInfo:
+    info = P2PInfo()
+    _check(lib().p2p_get_info(C.c_void_p(plan), C.byref(info)))
+    return info
+
+
+def p2p_copy_out(plan: int, which: int, dst: np.ndarray):
+    _check(lib().p2p_copy_out(C.c_void_p(plan), int(which), dst.ctypes.data_as(C.c_void_p), dst.nbytes))
+
+
+def p2p_comm_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(lib().p2p_comm_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def p2p_comm_create(nranks: int, rank: int, uid: bytes) -> int:
+    out = C.c_void_p()
+    buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+    _check(lib().p2p_comm_create(int(nranks), int(rank), C.cast(buf, C.c_void_p), C.byref(out)))
+    return out.value
+
+
+def p2p_comm_destroy(comm: int):
+    lib().p2p_comm_destroy(C.c_void_p(comm))
+
+
+def p2p_status_string(s: int) -> str:
+    return lib().p2p_status_string(int(s)).decode()
+
+
+def p2p_last_error() -> str:
+    return lib().p2p_last_error().decode()
+
+
+def p2p_kernel_launch_count() -> int:
+    return int(lib().p2p_kernel_launch_count())
+
+
+def p2p_abi_version() -> int:
+    return int(lib().p2p_abi_version())
+
+
+# ---- torch conveniences ----
+def make_config(kernel: int, precision: int, h: float, lo, nbox, periodic: int = 0, eps: float = 0.0,
+                k: float = 0.0, t: int = 0, stream=None) -> P2PConfig:
+    cfg = P2PConfig()
+    cfg.dim = 3 if kernel == P2P_GRAVITY else 2
+    cfg.kernel = kernel
+    cfg.precision = precision
+    cfg.box_size = float(h)
+    lo = list(lo) + [0.0] * (3 - len(lo))
+    nb = list(nbox) + [1] * (3 - len(nbox))
+    for d in range(3):
+        cfg.lo[d] = float(lo[d])
+        cfg.nbox[d] = int(nb[d])
+    cfg.periodic_mask = int(periodic)
+    cfg.softening = float(eps)
+    cfg.wavenumber = float(k)
+    cfg.points_per_box = int(t)
+    cfg.stream = stream
+    cfg.comm = None
+    return cfg
+
+
+def _stream_handle(stream) -> int | None:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Plan:
+    """RAII wrapper of a p2p_plan over torch CUDA tensors (positions [N][dim], charges [N] real or [N][2] complex)."""
+
+    def __init__(self, kernel: int, positions, charges, h: float, lo, nbox, periodic: int = 0, eps: float = 0.0,
+                 k: float = 0.0, t: int = 0, stream=None):
+        import torch
+        assert positions.is_cuda and charges.is_cuda, "positions / charges must be CUDA tensors"
+        positions = positions.contiguous()
+        charges = charges.contiguous()
+        prec = P2P_FP64 if positions.dtype == torch.float64 else P2P_FP32
+        self.kernel, self.precision = kernel, prec
+        self.dtype = positions.dtype
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self.cfg = make_config(kernel, prec, h, lo, nbox, periodic, eps, k, t, self.stream.cuda_stream)
+        self.n = int(positions.shape[0])
+        self._handle = p2p_plan_create(self.cfg, self.n, positions.data_ptr(), charges.data_ptr())
+        self.info = p2p_get_info(self._handle)
+
+    @property
+    def handle(self) -> int:
+        if not self._handle:
+            raise P2PError(P2P_ERR_BAD_STATE, "plan destroyed")
+        return self._handle
+
+    def restructure(self):
+        p2p_restructure(self.handle)
+
+    def set_charges(self, charges):
+        p2p_set_charges(self.handle, charges.contiguous().data_ptr())
+
+    def eval(self, layout: int = P2P_REDUNDANT, potential=None, field=None, want_field: bool = True):
+        import torch
+        dev = torch.device("cuda", torch.cuda.current_device())
+        if self.kernel == P2P_GRAVITY:
+            if potential is None:
+                potential = torch.empty(self.n, dtype=self.dtype, device=dev)
+            if field is None and want_field:
+                field = torch.empty((self.n, 3), dtype=self.dtype, device=dev)
+            p2p_eval(self.handle, layout, potential.data_ptr(), field.data_ptr() if field is not None else None)
+            return potential, field
+        if potential is None:
+            potential = torch.empty((self.n, 2), dtype=self.dtype, device=dev)
+        p2p_eval(self.handle, layout, potential.data_ptr(), None)
+        return potential
+
+    def copy_out(self, which: int) -> np.ndarray:
+        i = self.info
+        f64 = self.precision == P2P_FP64
+        if which == P2P_ARR_PERM or which == P2P_ARR_SORTED_KEYS:
+            a = np.empty(i.n_local, np.uint32)
+        elif which == P2P_ARR_BOX_KEYS:
+            a = np.empty(i.n_boxes, np.uint32)
+        elif which in (P2P_ARR_BOX_START, P2P_ARR_NBR_OFF):
+            a = np.empty(i.n_boxes + 1, np.uint32)
+        elif which == P2P_ARR_NBR_BOX:
+            a = np.empty(i.n_nbr, np.uint32)
+        elif which == P2P_ARR_NBR_SLOT:
+            a = np.empty(i.n_nbr, np.uint8)
+        elif which == P2P_ARR_RED_OFF:
+            a = np.empty(i.n_boxes + 1, np.uint64)
+        elif which == P2P_ARR_RED:
+            if self.kernel == P2P_GRAVITY:
+                a = np.empty((i.n_red, 4), np.float64 if f64 else np.float32)
+            else:
+                a = np.empty(i.n_red, np.complex128 if f64 else np.complex64)
+        else:
+            raise ValueError(which)
+        if i.n_local == 0:
+            return a[:0] if a.ndim == 1 else a
+        p2p_copy_out(self.handle, which, a)
+        return a
+
+    def close(self):
+        if self._handle:
+            p2p_destroy(self._handle)
+            self._handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+
+def nearfield(kernel: int, positions, charges, h: float, lo, nbox, periodic: int = 0, eps: float = 0.0,
+              k: float = 0.0, t: int = 0, layout: int = P2P_REDUNDANT):
+    """One-shot public API: plan -> restructure -> eval -> destroy.  Accepts host (CPU) or device tensors; host
+    inputs are copied to the device and the results back to the host (the end-to-end path bench.py times)."""
+    import torch
+    host = not positions.is_cuda
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pos_d = positions.to(dev, non_blocking=True) if host else positions
+    q_d = charges.to(dev, non_blocking=True) if host else charges
+    with Plan(kernel, pos_d, q_d, h, lo, nbox, periodic, eps, k, t) as plan:
+        if layout == P2P_REDUNDANT:
+            plan.restructure()
+        out = plan.eval(layout)
+    if not host:
+        return out
+    if kernel == P2P_GRAVITY:
+        return out[0].to("cpu", non_blocking=False), out[1].to("cpu", non_blocking=False)
+    return out.to("cpu", non_blocking=False)

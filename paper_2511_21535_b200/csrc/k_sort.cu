@@ -1,0 +1,219 @@
+// k_sort.cu -- hand-written stable LSD radix sort of (u32 key, u32 value) pairs for sm_100a
+// (SURVEY §8a-a2 "Morton-key radix sort"; BASELINE north_star forbids a library sort on the path).
+//
+// Design (Onesweep-style, one read + one write of the pairs per 8-bit digit):
+//   k_radix_hist      one pass over the keys builds the 256-bin histogram of EVERY digit at once
+//   k_radix_hist_scan exclusive scan of each digit histogram -> global digit offsets
+//   k_radix_pass      per digit: each CTA takes the next 4096-key tile (tile ids handed out by an atomic
+//                     counter in launch order, so look-back never waits on an unscheduled tile), ranks its
+//                     keys stably with warp-level match (__match_any_sync) in input order, publishes its
+//                     per-digit counts, decoupled look-back over earlier tiles for the exclusive prefix,
+//                     stages the tile in shared memory in digit order and writes each digit run
+//                     contiguously (coalesced) to its global position.
+// Stability: within a tile keys are ranked in (warp, item, lane) order, which is input order; tiles are
+// ordered by id = input order.  HBM traffic per pass: 8 B read + 8 B write per pair (+ look-back words).
+#include "plan.hpp"
+
+namespace p2p {
+
+namespace {
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys per tile
+constexpr uint32_t FLAG_AGG = 1u << 30;
+constexpr uint32_t FLAG_INC = 2u << 30;
+constexpr uint32_t VAL_MASK = (1u << 30) - 1u;
+
+__global__ void __launch_bounds__(256) k_radix_hist(const uint32_t *__restrict__ keys, uint32_t n, int passes,
+                                                    uint32_t *__restrict__ hist) {
+    __shared__ uint32_t sh[4][256];
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t k = keys[i];
+        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+        uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
+    }
+}
+
+// block-wide exclusive scan of one value per thread (256 threads)
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *warp_tot /*[8]*/, uint32_t *total) {
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    uint32_t add = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < RS_WARPS; ++i) {
+        uint32_t t = warp_tot[i];
+        add += (i < (int)w) ? t : 0u;
+        tot += t;
+    }
+    __syncthreads();
+    if (total) *total = tot;
+    return x - v + add;
+}
+
+__global__ void __launch_bounds__(256) k_radix_hist_scan(uint32_t *hist) {
+    __shared__ uint32_t wt[RS_WARPS];
+    uint32_t *h = hist + blockIdx.x * 256;
+    uint32_t v = h[threadIdx.x];
+    uint32_t e = block_excl_scan256(v, wt, nullptr);
+    h[threadIdx.x] = e;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile(uint32_t *p, uint32_t v) {
+    asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_radix_pass(const uint32_t *__restrict__ kin,
+                                                           const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
+                                                           uint32_t *__restrict__ vout, uint32_t n, int shift,
+                                                           const uint32_t *__restrict__ digit_off,
+                                                           uint32_t *status, uint32_t *tile_ctr) {
+    __shared__ uint32_t s_whist[RS_WARPS][256];
+    __shared__ uint32_t s_tdig[256];
+    __shared__ uint32_t s_goff[256];
+    __shared__ uint32_t s_keys[RS_TILE];
+    __shared__ uint32_t s_vals[RS_TILE];
+    __shared__ uint32_t s_wt[RS_WARPS];
+    __shared__ uint32_t s_tile;
+
+    const unsigned tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) (&s_whist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t base = tile * RS_TILE;
+    const uint32_t seg = base + w * 32 * RS_ITEMS;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+
+    uint32_t k[RS_ITEMS], v[RS_ITEMS], r[RS_ITEMS];
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; ++i) {
+        uint32_t idx = seg + i * 32 + lane;
+        bool ok = idx < n;
+        k[i] = ok ? kin[idx] : 0u;
+        v[i] = ok ? vin[idx] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; ++i) {
+        uint32_t idx = seg + i * 32 + lane;
+        bool ok = idx < n;
+        uint32_t mask = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            uint32_t d = (k[i] >> shift) & 255u;
+            uint32_t peers = __match_any_sync(mask, d);
+            uint32_t cnt = s_whist[w][d];
+            r[i] = cnt + __popc(peers & lt_mask);
+            __syncwarp(mask);
+            if (lane == (uint32_t)(__ffs(peers) - 1)) s_whist[w][d] = cnt + __popc(peers);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // per digit: exclusive prefix across warps, tile count, tile-local digit start, look-back
+    {
+        const uint32_t d = tid;
+        uint32_t sum = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS_WARPS; ++ww) {
+            uint32_t c = s_whist[ww][d];
+            s_whist[ww][d] = sum;
+            sum += c;
+        }
+        uint32_t *my = status + (size_t)tile * 256 + d;
+        if (tile == 0) st_volatile(my, FLAG_INC | sum);
+        else st_volatile(my, FLAG_AGG | sum);
+        uint32_t excl = 0;
+        if (tile > 0) {
+            int64_t t = (int64_t)tile - 1;
+            while (true) {
+                uint32_t s = ld_volatile(status + (size_t)t * 256 + d);
+                uint32_t f = s & ~VAL_MASK;
+                if (f == 0) continue;  // predecessor not published yet: spin
+                excl += s & VAL_MASK;
+                if (f == FLAG_INC) break;
+                --t;
+            }
+            st_volatile(my, FLAG_INC | (excl + sum));
+        }
+        s_goff[d] = digit_off[d] + excl;
+        s_tdig[d] = block_excl_scan256(sum, s_wt, nullptr);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; ++i) {
+        uint32_t idx = seg + i * 32 + lane;
+        if (idx < n) {
+            uint32_t d = (k[i] >> shift) & 255u;
+            uint32_t pos = s_tdig[d] + s_whist[w][d] + r[i];
+            s_keys[pos] = k[i];
+            s_vals[pos] = v[i];
+        }
+    }
+    __syncthreads();
+    const uint32_t tile_n = min((uint32_t)RS_TILE, n - base);
+    for (uint32_t j = tid; j < tile_n; j += RS_THREADS) {
+        uint32_t key = s_keys[j];
+        uint32_t d = (key >> shift) & 255u;
+        uint32_t dst = s_goff[d] + (j - s_tdig[d]);
+        kout[dst] = key;
+        vout[dst] = s_vals[j];
+    }
+}
+
+__global__ void k_copy_u32(const uint32_t *__restrict__ a, uint32_t *__restrict__ b, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = a[i];
+}
+}  // namespace
+
+cudaError_t radix_sort_pairs(uint32_t *kin, uint32_t *vin, uint32_t *kalt, uint32_t *valt, uint32_t n, int passes,
+                             DevCounters *ctr, cudaStream_t st, uint32_t **kout, uint32_t **vout) {
+    *kout = kin;
+    *vout = vin;
+    if (n == 0 || passes == 0) return cudaSuccess;
+    const uint32_t ntiles = div_up(n, RS_TILE);
+    uint32_t *hist = nullptr, *status = nullptr;
+    cudaError_t e;
+    size_t hist_bytes = (size_t)passes * 256 * sizeof(uint32_t);
+    size_t status_bytes = (size_t)passes * ntiles * 256 * sizeof(uint32_t);
+    if ((e = dalloc((void **)&hist, hist_bytes, st)) != cudaSuccess) return e;
+    if ((e = dalloc((void **)&status, status_bytes, st)) != cudaSuccess) return e;
+    cudaMemsetAsync(hist, 0, hist_bytes, st);
+    cudaMemsetAsync(status, 0, status_bytes, st);
+    cudaMemsetAsync(ctr->sort_tile_ctr, 0, sizeof(ctr->sort_tile_ctr), st);
+    unsigned hg = std::min<unsigned>(div_up(n, 256 * 8), 148 * 8);
+    P2P_LAUNCH(k_radix_hist, hg, 256, 0, st, kin, n, passes, hist);
+    P2P_LAUNCH(k_radix_hist_scan, passes, 256, 0, st, hist);
+    uint32_t *a_k = kin, *a_v = vin, *b_k = kalt, *b_v = valt;
+    for (int p = 0; p < passes; ++p) {
+        P2P_LAUNCH(k_radix_pass, ntiles, RS_THREADS, 0, st, a_k, a_v, b_k, b_v, n, 8 * p, hist + 256 * p,
+                   status + (size_t)p * ntiles * 256, &ctr->sort_tile_ctr[p]);
+        std::swap(a_k, b_k);
+        std::swap(a_v, b_v);
+    }
+    dfree(hist, st);
+    dfree(status, st);
+    *kout = a_k;
+    *vout = a_v;
+    return cudaGetLastError();
+}
+
+}  // namespace p2p

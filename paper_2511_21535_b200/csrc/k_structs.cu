@@ -1,0 +1,431 @@
+// k_structs.cu -- method steps a1..a5 on the device:
+//   a1 bin + Morton key (fp64 IEEE binning, DESIGN C6/C7), a2 stable radix sort (k_sort.cu),
+//   a3 permute into Morton-ordered AoS records, a4 box-offset scan (run heads -> compact box table),
+//   a5 neighbour CSR (ascending stencil slot, C10) + redundant offsets red_off + eval work items.
+// Bit-exactness with the oracle: every fp64 operation that decides an integer (box index, sub-cell) is an
+// explicit IEEE intrinsic (__dsub_rn, __ddiv_rn, __fma_rn) so no contraction or reassociation can change
+// a rounding.
+#include <algorithm>
+
+#include "plan.hpp"
+#include "scan.cuh"
+
+namespace p2p {
+
+// ------------------------------------------------------------------------------------------------
+// eval work items: a box's targets are split into ceil(n_b / ITEM_TMAX) chunks, more if the chunk cost
+// n_t * R_b exceeds ITEM_COSTCAP interactions (bounds the tail of the dynamic work queue on clustered
+// inputs).  Chunks are balanced: chunk c = [n_b c / nch, n_b (c+1) / nch).
+// ITEM_TMAX = 32 lanes x K targets per lane (eval register blocking: K = 4 fp32, 2 fp64)
+constexpr uint64_t ITEM_COSTCAP = 1ull << 17;
+
+__device__ __forceinline__ uint32_t item_chunks(uint32_t nb_b, uint64_t nsrc, uint32_t tmax) {
+    uint64_t a = (nb_b + tmax - 1) / tmax;
+    uint64_t c = ((uint64_t)nb_b * nsrc + ITEM_COSTCAP - 1) / ITEM_COSTCAP;
+    uint64_t m = a > c ? a : c;
+    if (m > nb_b) m = nb_b;
+    if (m < 1) m = 1;
+    return (uint32_t)m;
+}
+
+// ------------------------------------------------------------------------------------------------ a1
+template <typename T>
+__global__ void k_bin_gravity(const T *__restrict__ pos, uint32_t n, Geom g, uint32_t *__restrict__ key,
+                              uint32_t *__restrict__ idx, DevCounters *ctr) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t c[3];
+        bool bad = false;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double x = (double)pos[3 * (size_t)i + d];
+            double f = floor(__ddiv_rn(__dsub_rn(x, g.lo[d]), g.h));
+            if (!(f >= 0.0 && f < (double)g.nbox[d])) {
+                bad = true;
+                f = 0.0;
+            }
+            c[d] = (uint32_t)f;
+        }
+        if (bad) atomicMin(&ctr->err_index, (unsigned long long)i);
+        key[i] = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
+        idx[i] = i;
+    }
+}
+
+// Helmholtz: key = morton2(box) * t + subcell, subcell = sy*st + sx, s_d = floor((x_d - o_d)/Delta),
+// o_d = fma(ib_d, h, lo_d), Delta = h / st (DESIGN C8)
+template <typename T>
+__global__ void k_bin_helmholtz(const T *__restrict__ pos, uint32_t n, Geom g, int st, double delta, uint32_t t,
+                                uint32_t *__restrict__ key, uint32_t *__restrict__ idx, DevCounters *ctr) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t c[2], s[2];
+        bool bad = false, irr = false;
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            double x = (double)pos[2 * (size_t)i + d];
+            double f = floor(__ddiv_rn(__dsub_rn(x, g.lo[d]), g.h));
+            if (!(f >= 0.0 && f < (double)g.nbox[d])) {
+                bad = true;
+                f = 0.0;
+            }
+            c[d] = (uint32_t)f;
+            double o = __fma_rn((double)c[d], g.h, g.lo[d]);
+            double sf = floor(__ddiv_rn(__dsub_rn(x, o), delta));
+            if (!(sf >= 0.0 && sf < (double)st)) {
+                irr = true;
+                sf = 0.0;
+            }
+            s[d] = (uint32_t)sf;
+        }
+        if (bad) atomicMin(&ctr->err_index, (unsigned long long)i);
+        if (irr && !bad) atomicOr(&ctr->irregular, 1u);
+        key[i] = (spread2(c[0]) | (spread2(c[1]) << 1)) * t + (s[1] * (uint32_t)st + s[0]);
+        idx[i] = i;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------ a3
+template <typename T, typename V4>
+__global__ void k_permute_gravity(const T *__restrict__ pos, const T *__restrict__ q, const uint32_t *__restrict__ perm,
+                                  uint32_t n, V4 *__restrict__ rec) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        uint32_t i = perm[p];
+        V4 r;
+        r.x = pos[3 * (size_t)i + 0];
+        r.y = pos[3 * (size_t)i + 1];
+        r.z = pos[3 * (size_t)i + 2];
+        r.w = q[i];
+        rec[p] = r;
+    }
+}
+
+template <typename C2>
+__global__ void k_permute_complex(const C2 *__restrict__ x, const uint32_t *__restrict__ perm, uint32_t n,
+                                  C2 *__restrict__ xs) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) xs[p] = x[perm[p]];
+}
+
+// ------------------------------------------------------------------------------------------------ a4
+struct HeadGet {
+    const uint32_t *skey;
+    uint32_t div;
+    __device__ uint32_t operator()(uint64_t p) const {
+        return (p == 0 || skey[p] / div != skey[p - 1] / div) ? 1u : 0u;
+    }
+};
+struct HeadPut {
+    const uint32_t *skey;
+    uint32_t div;
+    uint32_t *bkey, *bstart, *box_of;
+    uint32_t n;
+    __device__ void operator()(uint64_t p, uint32_t e, uint32_t v) const {
+        if (v) {
+            uint32_t bk = skey[p] / div;
+            bkey[e] = bk;
+            bstart[e] = (uint32_t)p;
+            box_of[bk] = e;
+        }
+        if (p == n - 1) bstart[e + v] = n;
+    }
+};
+
+// ------------------------------------------------------------------------------------------------ a5
+__device__ __forceinline__ bool stencil_nbr(const Geom &g, const uint32_t c[3], int slot, uint32_t nc[3]) {
+    const int dd[3] = {slot % 3 - 1, (slot / 3) % 3 - 1, slot / 9 - 1};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        int v = (int)c[d] + dd[d];
+        if (v < 0 || v >= g.nbox[d]) {
+            if (!((g.periodic >> d) & 1u)) return false;
+            v = v < 0 ? v + g.nbox[d] : v - g.nbox[d];
+        }
+        nc[d] = (uint32_t)v;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void decode3(uint32_t key, uint32_t c[3]) {
+    c[0] = compact3(key);
+    c[1] = compact3(key >> 1);
+    c[2] = compact3(key >> 2);
+}
+
+__global__ void k_nbr_count(Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
+                            const uint32_t *__restrict__ box_of, DevCounters *ctr, uint32_t *__restrict__ nbr_cnt,
+                            uint64_t *__restrict__ red_cnt, uint32_t *__restrict__ item_cnt, uint32_t tmax) {
+    const uint32_t B = ctr->B;
+    uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long pairs = 0;
+    if (b < B) {
+        uint32_t c[3];
+        decode3(bkey[b], c);
+        uint32_t cnt = 0;
+        uint64_t nsrc = 0;
+        for (int slot = 0; slot < 27; ++slot) {
+            uint32_t nc[3];
+            if (!stencil_nbr(g, c, slot, nc)) continue;
+            uint32_t nk = spread3(nc[0]) | (spread3(nc[1]) << 1) | (spread3(nc[2]) << 2);
+            uint32_t k = box_of[nk];
+            if (k < B && bkey[k] == nk) {
+                ++cnt;
+                nsrc += bstart[k + 1] - bstart[k];
+            }
+        }
+        uint32_t nb_b = bstart[b + 1] - bstart[b];
+        nbr_cnt[b] = cnt;
+        red_cnt[b] = nsrc;
+        item_cnt[b] = item_chunks(nb_b, nsrc, tmax);
+        pairs = (unsigned long long)nb_b * nsrc;
+    }
+    // warp-aggregated pair count
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    if ((threadIdx.x & 31u) == 0 && pairs) atomicAdd(&ctr->I, pairs);
+}
+
+__global__ void k_nbr_fill(Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
+                           const uint32_t *__restrict__ box_of, const DevCounters *ctr,
+                           const uint32_t *__restrict__ nbr_off, const uint32_t *__restrict__ item_off,
+                           const uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ nbr_box,
+                           uint8_t *__restrict__ nbr_slot, Item *__restrict__ items) {
+    const uint32_t B = ctr->B;
+    uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    uint32_t c[3];
+    decode3(bkey[b], c);
+    uint32_t e = nbr_off[b];
+    for (int slot = 0; slot < 27; ++slot) {
+        uint32_t nc[3];
+        if (!stencil_nbr(g, c, slot, nc)) continue;
+        uint32_t nk = spread3(nc[0]) | (spread3(nc[1]) << 1) | (spread3(nc[2]) << 2);
+        uint32_t k = box_of[nk];
+        if (k < B && bkey[k] == nk) {
+            nbr_box[e] = k;
+            nbr_slot[e] = (uint8_t)slot;
+            ++e;
+        }
+    }
+    const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
+    const uint32_t nch = item_cnt[b], it = item_off[b];
+    for (uint32_t ci = 0; ci < nch; ++ci) {
+        uint32_t a = (uint32_t)(((uint64_t)nb_b * ci) / nch), z = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
+        items[it + ci] = Item{b, s0 + a, z - a};
+    }
+}
+
+// Helmholtz: 9-slot table, missing -> 0xffffffff (C10); boxes must be full (t samples, distinct sub-cells)
+__global__ void k_helm_check(const uint32_t *__restrict__ skey, uint32_t n, DevCounters *ctr) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x + 1; p < n; p += gridDim.x * blockDim.x)
+        if (skey[p] == skey[p - 1]) atomicOr(&ctr->irregular, 1u);
+}
+
+__global__ void k_helm_nbr(const Geom g, uint32_t t, const uint32_t *__restrict__ bkey,
+                           const uint32_t *__restrict__ bstart, const uint32_t *__restrict__ box_of,
+                           DevCounters *ctr, uint32_t *__restrict__ nbr_off, uint32_t *__restrict__ nbr9,
+                           uint8_t *__restrict__ nbr_slot) {
+    const uint32_t B = ctr->B;
+    uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long pairs = 0;
+    if (b < B) {
+        if (bstart[b + 1] - bstart[b] != t) atomicOr(&ctr->irregular, 1u);
+        uint32_t key = bkey[b];
+        int cx = (int)compact2(key), cy = (int)compact2(key >> 1);
+        uint32_t present = 0;
+        for (int s = 0; s < 9; ++s) {
+            int nx = cx + s % 3 - 1, ny = cy + s / 3 - 1;
+            uint32_t k = 0xffffffffu;
+            if (nx >= 0 && nx < g.nbox[0] && ny >= 0 && ny < g.nbox[1]) {
+                uint32_t nk = spread2((uint32_t)nx) | (spread2((uint32_t)ny) << 1);
+                uint32_t kk = box_of[nk];
+                if (kk < B && bkey[kk] == nk) k = kk;
+            }
+            nbr9[9 * (size_t)b + s] = k;
+            nbr_slot[9 * (size_t)b + s] = (uint8_t)s;
+            present += (k != 0xffffffffu);
+        }
+        nbr_off[b] = 9 * b;
+        if (b == B - 1) nbr_off[B] = 9 * B;
+        pairs = (unsigned long long)t * t * present;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    if ((threadIdx.x & 31u) == 0 && pairs) atomicAdd(&ctr->I, pairs);
+}
+
+// ------------------------------------------------------------------------------------------------
+// scan functors over plain arrays
+template <typename T>
+struct ArrGet {
+    const T *a;
+    __device__ T operator()(uint64_t i) const { return a[i]; }
+};
+template <typename T>
+struct OffPut {
+    T *off;
+    const uint32_t *nptr;
+    __device__ void operator()(uint64_t i, T e, T v) const {
+        off[i] = e;
+        if (i == (uint64_t)*nptr - 1) off[i + 1] = e + v;
+    }
+};
+
+static unsigned grid_for(uint64_t n, int threads, int num_sms) {
+    uint64_t g = (n + threads - 1) / threads;
+    uint64_t cap = (uint64_t)num_sms * 16;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, cap));
+}
+
+// ------------------------------------------------------------------------------------------------
+p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q) {
+    cudaStream_t st = P->stream;
+    const uint32_t n = (uint32_t)P->n;
+    const bool f64 = P->cfg.precision == P2P_FP64;
+    uint32_t *key = nullptr, *idx = nullptr, *kalt = nullptr, *valt = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&key, sizeof(uint32_t) * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&idx, sizeof(uint32_t) * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&kalt, sizeof(uint32_t) * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&valt, sizeof(uint32_t) * n, st));
+    const unsigned gb = grid_for(n, 256, P->num_sms);
+    if (f64) P2P_LAUNCH(k_bin_gravity<double>, gb, 256, 0, st, (const double *)pos, n, P->geom, key, idx, P->ctr);
+    else P2P_LAUNCH(k_bin_gravity<float>, gb, 256, 0, st, (const float *)pos, n, P->geom, key, idx, P->ctr);
+    uint32_t *sk, *sv;
+    P2P_CUDA_TRY(radix_sort_pairs(key, idx, kalt, valt, n, P->passes, P->ctr, st, &sk, &sv));
+    // keep sorted keys / perm in plan-owned buffers, free the others
+    P->skey = sk;
+    P->perm = sv;
+    dfree(sk == key ? kalt : key, st);
+    dfree(sv == idx ? valt : idx, st);
+    // a3
+    const size_t rec_bytes = (f64 ? sizeof(double4) : sizeof(float4)) * (size_t)n;
+    P2P_CUDA_TRY(dalloc(&P->rec, rec_bytes, st));
+    if (f64)
+        P2P_LAUNCH((k_permute_gravity<double, double4>), gb, 256, 0, st, (const double *)pos, (const double *)q,
+                   P->perm, n, (double4 *)P->rec);
+    else
+        P2P_LAUNCH((k_permute_gravity<float, float4>), gb, 256, 0, st, (const float *)pos, (const float *)q, P->perm,
+                   n, (float4 *)P->rec);
+    // a4
+    const uint64_t keyspace = 1ull << P->key_bits;
+    const uint64_t bcap = std::min<uint64_t>(n, keyspace);
+    P2P_CUDA_TRY(dalloc((void **)&P->bkey, sizeof(uint32_t) * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->bstart, sizeof(uint32_t) * (bcap + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->box_of, sizeof(uint32_t) * keyspace, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, 1u}, HeadPut{P->skey, 1u, P->bkey, P->bstart, P->box_of, n},
+                                       nullptr, n, &P->ctr->B, st));
+    // a5
+    uint32_t *nbr_cnt = nullptr, *item_cnt = nullptr;
+    uint64_t *red_cnt = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&nbr_cnt, sizeof(uint32_t) * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&item_cnt, sizeof(uint32_t) * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&red_cnt, sizeof(uint64_t) * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_off, sizeof(uint32_t) * (bcap + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->red_off, sizeof(uint64_t) * (bcap + 1), st));
+    uint32_t *item_off = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&item_off, sizeof(uint32_t) * (bcap + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_box, sizeof(uint32_t) * 27 * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, sizeof(uint8_t) * 27 * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->items, sizeof(Item) * n, st));
+    const unsigned gbx = div_up(bcap, 256);
+    const uint32_t tmax = f64 ? 64u : 128u;  // 32 lanes x K (K = 2 fp64, 4 fp32; k_eval_gravity.cu)
+    P2P_LAUNCH(k_nbr_count, gbx, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, nbr_cnt, red_cnt,
+               item_cnt, tmax);
+    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{nbr_cnt}, OffPut<uint32_t>{P->nbr_off, &P->ctr->B},
+                                       &P->ctr->B, bcap, &P->ctr->n_nbr, st));
+    P2P_CUDA_TRY(device_scan<unsigned long long>(ArrGet<unsigned long long>{(const unsigned long long *)red_cnt},
+                                                 OffPut<unsigned long long>{(unsigned long long *)P->red_off, &P->ctr->B},
+                                                 &P->ctr->B, bcap, &P->ctr->R, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{item_cnt}, OffPut<uint32_t>{item_off, &P->ctr->B}, &P->ctr->B,
+                                       bcap, &P->ctr->n_items, st));
+    P2P_LAUNCH(k_nbr_fill, gbx, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, P->nbr_off, item_off,
+               item_cnt, P->nbr_box, P->nbr_slot, P->items);
+    dfree(nbr_cnt, st);
+    dfree(item_cnt, st);
+    dfree(red_cnt, st);
+    dfree(item_off, st);
+    P2P_CUDA_TRY(cudaGetLastError());
+    return P2P_OK;
+}
+
+template <typename T, typename V4>
+__global__ void k_set_mass(const T *__restrict__ q, const uint32_t *__restrict__ perm, uint32_t n,
+                           V4 *__restrict__ rec) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) rec[p].w = q[perm[p]];
+}
+
+p2p_status set_charges_gravity(p2p_plan *P, const void *q) {
+    // masses are the .w field of the Morton-sorted records: re-gather them in sorted order
+    cudaStream_t st = P->stream;
+    const uint32_t n = (uint32_t)P->n;
+    const unsigned gb = grid_for(n, 256, P->num_sms);
+    if (P->cfg.precision == P2P_FP64)
+        P2P_LAUNCH((k_set_mass<double, double4>), gb, 256, 0, st, (const double *)q, P->perm, n, (double4 *)P->rec);
+    else
+        P2P_LAUNCH((k_set_mass<float, float4>), gb, 256, 0, st, (const float *)q, P->perm, n, (float4 *)P->rec);
+    P2P_CUDA_TRY(cudaGetLastError());
+    return P2P_OK;
+}
+
+p2p_status build_helmholtz_structs(p2p_plan *P, const void *pos, const void *q) {
+    cudaStream_t st = P->stream;
+    const uint32_t n = (uint32_t)P->n;
+    const bool f64 = P->cfg.precision == P2P_FP64;
+    const uint32_t t = (uint32_t)P->cfg.points_per_box;
+    int stt = 0;
+    while (stt * stt < (int)t) ++stt;
+    const double delta = P->cfg.box_size / (double)stt;
+    uint32_t *key = nullptr, *idx = nullptr, *kalt = nullptr, *valt = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&key, sizeof(uint32_t) * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&idx, sizeof(uint32_t) * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&kalt, sizeof(uint32_t) * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&valt, sizeof(uint32_t) * n, st));
+    const unsigned gb = grid_for(n, 256, P->num_sms);
+    if (f64)
+        P2P_LAUNCH(k_bin_helmholtz<double>, gb, 256, 0, st, (const double *)pos, n, P->geom, stt, delta, t, key, idx,
+                   P->ctr);
+    else
+        P2P_LAUNCH(k_bin_helmholtz<float>, gb, 256, 0, st, (const float *)pos, n, P->geom, stt, delta, t, key, idx,
+                   P->ctr);
+    uint32_t *sk, *sv;
+    P2P_CUDA_TRY(radix_sort_pairs(key, idx, kalt, valt, n, P->passes, P->ctr, st, &sk, &sv));
+    P->skey = sk;
+    P->perm = sv;
+    dfree(sk == key ? kalt : key, st);
+    dfree(sv == idx ? valt : idx, st);
+    P2P_LAUNCH(k_helm_check, gb, 256, 0, st, P->skey, n, P->ctr);
+    // a3: complex unknowns in sorted order
+    const size_t cbytes = (f64 ? sizeof(double2) : sizeof(float2)) * (size_t)n;
+    P2P_CUDA_TRY(dalloc(&P->rec, cbytes, st));
+    if (f64)
+        P2P_LAUNCH(k_permute_complex<double2>, gb, 256, 0, st, (const double2 *)q, P->perm, n, (double2 *)P->rec);
+    else
+        P2P_LAUNCH(k_permute_complex<float2>, gb, 256, 0, st, (const float2 *)q, P->perm, n, (float2 *)P->rec);
+    // a4: boxes = runs of key / t
+    const uint64_t keyspace = 1ull << (2 * P->nb);
+    const uint64_t bcap = std::min<uint64_t>(n, keyspace);
+    P2P_CUDA_TRY(dalloc((void **)&P->bkey, sizeof(uint32_t) * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->bstart, sizeof(uint32_t) * (bcap + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->box_of, sizeof(uint32_t) * keyspace, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, t}, HeadPut{P->skey, t, P->bkey, P->bstart, P->box_of, n},
+                                       nullptr, n, &P->ctr->B, st));
+    // a5: 9 slots per box
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_off, sizeof(uint32_t) * (bcap + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_box, sizeof(uint32_t) * 9 * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, sizeof(uint8_t) * 9 * bcap, st));
+    P2P_LAUNCH(k_helm_nbr, div_up(bcap, 256), 256, 0, st, P->geom, t, P->bkey, P->bstart, P->box_of, P->ctr,
+               P->nbr_off, P->nbr_box, P->nbr_slot);
+    P2P_CUDA_TRY(cudaGetLastError());
+    return P2P_OK;
+}
+
+p2p_status set_charges_helmholtz(p2p_plan *P, const void *q) {
+    cudaStream_t st = P->stream;
+    const uint32_t n = (uint32_t)P->n;
+    const unsigned gb = grid_for(n, 256, P->num_sms);
+    if (P->cfg.precision == P2P_FP64)
+        P2P_LAUNCH(k_permute_complex<double2>, gb, 256, 0, st, (const double2 *)q, P->perm, n, (double2 *)P->rec);
+    else
+        P2P_LAUNCH(k_permute_complex<float2>, gb, 256, 0, st, (const float2 *)q, P->perm, n, (float2 *)P->rec);
+    P2P_CUDA_TRY(cudaGetLastError());
+    return P2P_OK;
+}
+
+}  // namespace p2p

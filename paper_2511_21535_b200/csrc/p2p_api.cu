@@ -1,0 +1,343 @@
+// p2p_api.cu -- the C ABI of libp2p (include/p2p.h): argument validation, plan life cycle, error plumbing.
+// Every step of the path runs in this library's kernels (k_*.cu); this file only orchestrates.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "plan.hpp"
+
+namespace p2p {
+
+static thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+static bool g_pool_configured = false;
+
+cudaError_t dalloc(void **p, size_t bytes, cudaStream_t st) {
+    *p = nullptr;
+    if (bytes == 0) bytes = 16;
+    if (!g_pool_configured) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;  // keep freed blocks for reuse: plan create/destroy per step stays cheap
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        g_pool_configured = true;
+    }
+    return cudaMallocAsync(p, bytes, st);
+}
+
+void dfree(void *p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+static bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static p2p_status fail(p2p_status s, const std::string &msg) {
+    set_error(msg);
+    return s;
+}
+
+// entry guard: sticky state, async errors from earlier work
+static p2p_status enter(p2p_plan *P) {
+    if (!P) return fail(P2P_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (P->sticky != P2P_OK) return fail(P->sticky, "plan is unusable after an earlier CUDA/NCCL error");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != P->device) cudaSetDevice(P->device);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        P->sticky = P2P_ERR_CUDA;
+        return fail(P2P_ERR_CUDA, std::string("asynchronous CUDA error: ") + cudaGetErrorString(e));
+    }
+    return P2P_OK;
+}
+
+static p2p_status mark(p2p_plan *P, p2p_status s) {
+    if (s == P2P_ERR_CUDA || s == P2P_ERR_NCCL) P->sticky = s;
+    return s;
+}
+
+static void free_plan_buffers(p2p_plan *P) {
+    cudaStream_t st = P->stream;
+    void *bufs[] = {P->rec, P->skey, P->perm, P->bkey, P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot,
+                    P->red_off, P->box_of, P->items, P->red, P->table, P->ctr};
+    for (void *b : bufs) dfree(b, st);
+}
+
+}  // namespace p2p
+
+using namespace p2p;
+
+extern "C" {
+
+int p2p_abi_version(void) { return P2P_ABI_VERSION; }
+
+uint64_t p2p_kernel_launch_count(void) { return g_launches.load(); }
+
+const char *p2p_last_error(void) { return g_err.c_str(); }
+
+const char *p2p_status_string(p2p_status s) {
+    switch (s) {
+    case P2P_OK: return "P2P_OK";
+    case P2P_ERR_INVALID_ARGUMENT: return "P2P_ERR_INVALID_ARGUMENT";
+    case P2P_ERR_OUT_OF_DOMAIN: return "P2P_ERR_OUT_OF_DOMAIN";
+    case P2P_ERR_OUT_OF_MEMORY: return "P2P_ERR_OUT_OF_MEMORY";
+    case P2P_ERR_CUDA: return "P2P_ERR_CUDA";
+    case P2P_ERR_NCCL: return "P2P_ERR_NCCL";
+    case P2P_ERR_BAD_STATE: return "P2P_ERR_BAD_STATE";
+    case P2P_ERR_UNSUPPORTED: return "P2P_ERR_UNSUPPORTED";
+    }
+    return "P2P_ERR_UNKNOWN";
+}
+
+p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *positions, const void *charges,
+                           p2p_plan **out) {
+    if (!out) return fail(P2P_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!cfg) return fail(P2P_ERR_INVALID_ARGUMENT, "cfg is NULL");
+    if (n_local < 0) return fail(P2P_ERR_INVALID_ARGUMENT, "n_local < 0");
+    if (n_local >= (int64_t)1 << 31) return fail(P2P_ERR_UNSUPPORTED, "n_local >= 2^31 (u32 indices)");
+    const bool grav = cfg->kernel == P2P_GRAVITY;
+    if (!grav && cfg->kernel != P2P_HELMHOLTZ2D) return fail(P2P_ERR_INVALID_ARGUMENT, "unknown kernel");
+    if (cfg->precision != P2P_FP32 && cfg->precision != P2P_FP64)
+        return fail(P2P_ERR_INVALID_ARGUMENT, "unknown precision");
+    if ((grav && cfg->dim != 3) || (!grav && cfg->dim != 2))
+        return fail(P2P_ERR_INVALID_ARGUMENT, "dim does not match the kernel (gravity: 3, helmholtz: 2)");
+    if (!(cfg->box_size > 0.0) || !std::isfinite(cfg->box_size))
+        return fail(P2P_ERR_INVALID_ARGUMENT, "box_size h must be > 0");
+    for (int d = 0; d < cfg->dim; ++d) {
+        if (cfg->nbox[d] < 1) return fail(P2P_ERR_INVALID_ARGUMENT, "nbox[d] must be >= 1");
+        if (((cfg->periodic_mask >> d) & 1u) && cfg->nbox[d] < 3)
+            return fail(P2P_ERR_INVALID_ARGUMENT, "a periodic dimension needs nbox >= 3 (27 distinct images, C5)");
+        if (!std::isfinite(cfg->lo[d])) return fail(P2P_ERR_INVALID_ARGUMENT, "lo must be finite");
+    }
+    if (grav && !(cfg->softening > 0.0)) return fail(P2P_ERR_INVALID_ARGUMENT, "softening eps must be > 0 (C2)");
+    if (!grav) {
+        if (cfg->periodic_mask & 3u) return fail(P2P_ERR_INVALID_ARGUMENT, "helmholtz domain is open (C5)");
+        if (!(cfg->wavenumber > 0.0)) return fail(P2P_ERR_INVALID_ARGUMENT, "wavenumber k must be > 0");
+        int t = cfg->points_per_box, st = 0;
+        while (st * st < t) ++st;
+        if (t < 1 || st * st != t) return fail(P2P_ERR_INVALID_ARGUMENT, "points_per_box t must be a perfect square");
+    }
+    if (cfg->comm) return fail(P2P_ERR_UNSUPPORTED, "multi-GPU plans are not available in this build");
+    if (n_local > 0 && (!is_device_ptr(positions) || !is_device_ptr(charges)))
+        return fail(P2P_ERR_INVALID_ARGUMENT, "positions / charges must be device pointers");
+
+    p2p_plan *P = new p2p_plan();
+    P->cfg = *cfg;
+    P->stream = (cudaStream_t)cfg->stream;
+    cudaGetDevice(&P->device);
+    cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device);
+    P->n = n_local;
+    // geometry
+    Geom &g = P->geom;
+    g.h = cfg->box_size;
+    int32_t mx = 1;
+    for (int d = 0; d < 3; ++d) {
+        const bool used = d < cfg->dim;
+        g.lo[d] = used ? cfg->lo[d] : 0.0;
+        g.nbox[d] = used ? cfg->nbox[d] : 1;
+        g.L[d] = (double)g.nbox[d] * g.h;  // IEEE product (C5)
+        if (g.nbox[d] > mx) mx = g.nbox[d];
+    }
+    g.periodic = grav ? (cfg->periodic_mask & 7u) : 0u;
+    int nb = 0;
+    while ((1 << nb) < mx) ++nb;
+    g.nb = nb;
+    g.eps2 = cfg->softening * cfg->softening;
+    P->nb = nb;
+    if (grav) {
+        if (nb > 10) {
+            delete P;
+            return fail(P2P_ERR_UNSUPPORTED, "more than 1024 boxes per dim (u32 Morton keys, C7)");
+        }
+        P->key_bits = 3 * nb;
+    } else {
+        if (nb > 16) {
+            delete P;
+            return fail(P2P_ERR_UNSUPPORTED, "more than 65536 boxes per dim");
+        }
+        uint64_t kmax = ((uint64_t)1 << (2 * nb)) * (uint64_t)cfg->points_per_box;
+        int kb = 0;
+        while (((uint64_t)1 << kb) < kmax) ++kb;
+        if (kb > 32) {
+            delete P;
+            return fail(P2P_ERR_UNSUPPORTED, "helmholtz key (box * t + subcell) exceeds 32 bits");
+        }
+        P->key_bits = kb;
+    }
+    P->passes = (P->key_bits + 7) / 8;
+
+    cudaStream_t st = P->stream;
+    auto bail = [&](p2p_status s) {
+        free_plan_buffers(P);
+        cudaStreamSynchronize(st);
+        delete P;
+        return s;
+    };
+    if (dalloc((void **)&P->ctr, sizeof(DevCounters), st) != cudaSuccess)
+        return bail(fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate counters"));
+    cudaMemsetAsync(P->ctr, 0, sizeof(DevCounters), st);
+    cudaMemsetAsync(&P->ctr->err_index, 0xff, sizeof(unsigned long long), st);
+    if (n_local == 0) {
+        cudaStreamSynchronize(st);
+        *out = P;
+        return P2P_OK;
+    }
+    p2p_status s = grav ? build_gravity_structs(P, positions, charges) : build_helmholtz_structs(P, positions, charges);
+    if (s != P2P_OK) return bail(s);
+    // the ONE host synchronisation: sizes for the redundant buffer and launch geometry
+    DevCounters h;
+    cudaError_t e = cudaMemcpyAsync(&h, P->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return bail(fail(P2P_ERR_CUDA, std::string("CUDA error in plan build: ") + cudaGetErrorString(e)));
+    if (h.err_index != ~0ull) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "position of input particle %llu is outside the domain [lo, lo + nbox*h) (C6)",
+                 (unsigned long long)h.err_index);
+        return bail(fail(P2P_ERR_OUT_OF_DOMAIN, buf));
+    }
+    if (h.irregular) return bail(fail(P2P_ERR_UNSUPPORTED, "helmholtz input is not a regular t-per-box lattice (C8)"));
+    P->B = h.B;
+    P->I = (int64_t)h.I;
+    if (grav) {
+        P->n_nbr = h.n_nbr;
+        P->R = (int64_t)h.R;
+        P->n_items = h.n_items;
+        const size_t rec_sz = cfg->precision == P2P_FP64 ? sizeof(double4) : sizeof(float4);
+        if (dalloc(&P->red, rec_sz * (size_t)std::max<int64_t>(P->R, 1), st) != cudaSuccess)
+            return bail(fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate the redundant buffer"));
+    } else {
+        const int64_t t = cfg->points_per_box;
+        P->n_nbr = 9 * P->B;
+        P->R = 9 * t * P->B;
+        P->n_items = P->B;
+        const size_t c_sz = cfg->precision == P2P_FP64 ? sizeof(double2) : sizeof(float2);
+        if (dalloc(&P->red, c_sz * (size_t)std::max<int64_t>(P->R, 1), st) != cudaSuccess)
+            return bail(fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate the im2col buffer"));
+        s = helmholtz_table(P);
+        if (s != P2P_OK) return bail(s);
+    }
+    *out = P;
+    return P2P_OK;
+}
+
+p2p_status p2p_restructure(p2p_plan *P) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (P->n == 0) {
+        P->red_valid = true;
+        return P2P_OK;
+    }
+    s = P->cfg.kernel == P2P_GRAVITY ? restructure_gravity(P) : restructure_helmholtz(P);
+    if (s == P2P_OK) P->red_valid = true;
+    return mark(P, s);
+}
+
+p2p_status p2p_eval(p2p_plan *P, p2p_layout layout, void *potential, void *field) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (layout != P2P_REDUNDANT && layout != P2P_INDEXED && layout != P2P_INDEXED_BITWISE)
+        return fail(P2P_ERR_INVALID_ARGUMENT, "unknown layout");
+    if (layout == P2P_REDUNDANT && !P->red_valid)
+        return fail(P2P_ERR_BAD_STATE, "eval(P2P_REDUNDANT) needs p2p_restructure first (and after set_charges)");
+    if (P->n == 0) return P2P_OK;
+    if (!is_device_ptr(potential)) return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
+    if (P->cfg.kernel == P2P_GRAVITY) {
+        if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
+        return mark(P, eval_gravity(P, layout, potential, field));
+    }
+    if (field) return fail(P2P_ERR_INVALID_ARGUMENT, "helmholtz has no field output (pass NULL)");
+    return mark(P, eval_helmholtz(P, layout, potential));
+}
+
+p2p_status p2p_set_charges(p2p_plan *P, const void *charges) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (P->n == 0) return P2P_OK;
+    if (!is_device_ptr(charges)) return fail(P2P_ERR_INVALID_ARGUMENT, "charges must be a device pointer");
+    P->red_valid = false;
+    s = P->cfg.kernel == P2P_GRAVITY ? set_charges_gravity(P, charges) : set_charges_helmholtz(P, charges);
+    return mark(P, s);
+}
+
+void p2p_destroy(p2p_plan *P) {
+    if (!P) return;
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != P->device) cudaSetDevice(P->device);
+    free_plan_buffers(P);
+    delete P;
+}
+
+p2p_status p2p_get_info(const p2p_plan *P, p2p_info *out) {
+    if (!P || !out) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (P->sticky != P2P_OK) return fail(P->sticky, "plan is unusable after an earlier error");
+    cudaError_t e = cudaStreamSynchronize(P->stream);
+    if (e != cudaSuccess) return fail(P2P_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+    out->n_local = P->n;
+    out->n_boxes = P->B;
+    out->n_nbr = P->n_nbr;
+    out->n_red = P->R;
+    out->n_pairs = P->I;
+    out->n_items = P->n_items;
+    out->key_bits = P->key_bits;
+    out->sort_passes = P->passes;
+    return P2P_OK;
+}
+
+p2p_status p2p_copy_out(const p2p_plan *P, p2p_array which, void *host_dst, size_t bytes) {
+    if (!P || (!host_dst && bytes)) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (P->sticky != P2P_OK) return fail(P->sticky, "plan is unusable after an earlier error");
+    const bool grav = P->cfg.kernel == P2P_GRAVITY;
+    const bool f64 = P->cfg.precision == P2P_FP64;
+    const void *src = nullptr;
+    size_t need = 0;
+    switch (which) {
+    case P2P_ARR_PERM: src = P->perm; need = 4 * (size_t)P->n; break;
+    case P2P_ARR_SORTED_KEYS: src = P->skey; need = 4 * (size_t)P->n; break;
+    case P2P_ARR_BOX_KEYS: src = P->bkey; need = 4 * (size_t)P->B; break;
+    case P2P_ARR_BOX_START: src = P->bstart; need = 4 * (size_t)(P->B + 1); break;
+    case P2P_ARR_NBR_OFF: src = P->nbr_off; need = 4 * (size_t)(P->B + 1); break;
+    case P2P_ARR_NBR_BOX: src = P->nbr_box; need = 4 * (size_t)P->n_nbr; break;
+    case P2P_ARR_NBR_SLOT: src = P->nbr_slot; need = (size_t)P->n_nbr; break;
+    case P2P_ARR_RED_OFF:
+        if (!grav) return fail(P2P_ERR_UNSUPPORTED, "helmholtz runs have fixed stride 9t (no red_off array)");
+        src = P->red_off; need = 8 * (size_t)(P->B + 1); break;
+    case P2P_ARR_RED:
+        if (!P->red_valid) return fail(P2P_ERR_BAD_STATE, "the redundant buffer is not built (call p2p_restructure)");
+        src = P->red;
+        need = (size_t)P->R * (grav ? (f64 ? 32 : 16) : (f64 ? 16 : 8));
+        break;
+    default: return fail(P2P_ERR_INVALID_ARGUMENT, "unknown array");
+    }
+    if (P->n == 0) need = 0;
+    if (bytes != need) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "bytes = %zu but the array holds %zu bytes", bytes, need);
+        return fail(P2P_ERR_INVALID_ARGUMENT, buf);
+    }
+    if (need == 0) return P2P_OK;
+    cudaError_t e = cudaStreamSynchronize(P->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(host_dst, src, need, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(P2P_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+    return P2P_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// plan.hpp -- the opaque p2p_plan object and the internal kernel entry points of libp2p.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "p2p.h"
+
+namespace p2p {
+
+// device-resident counters written by the structure kernels; read back ONCE at the end of plan_create
+struct DevCounters {
+    unsigned long long err_index;  // min out-of-domain input index (init ~0ull)
+    unsigned int irregular;        // helmholtz: non-regular lattice detected
+    unsigned int B;                // non-empty boxes
+    unsigned int n_nbr;            // CSR entries
+    unsigned int n_items;          // eval work items
+    unsigned long long R;          // redundant records
+    unsigned long long I;          // pair interactions
+    unsigned int item_head;        // eval work queue head (reset before every eval)
+    unsigned int sort_tile_ctr[4]; // onesweep tile counters, one per pass
+    unsigned int pad[3];
+};
+
+// eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
+struct Item {
+    uint32_t box;
+    uint32_t t0;
+    uint32_t nt;
+};
+
+// gravity geometry passed by value to kernels
+struct Geom {
+    double lo[3];
+    double h;
+    double L[3];          // periodic lengths nbox_d * h (IEEE product, C5)
+    int32_t nbox[3];
+    uint32_t periodic;
+    int32_t nb;           // Morton bits per dim
+    double eps2;          // eps^2 (fp64)
+};
+
+}  // namespace p2p
+
+struct p2p_plan {
+    p2p_config cfg;
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    int num_sms = 148;
+    int64_t n = 0;
+    int key_bits = 0, passes = 0, nb = 0;
+    p2p::Geom geom{};
+    // sizes (host copies, valid after plan_create)
+    int64_t B = 0, n_nbr = 0, R = 0, I = 0, n_items = 0;
+    // device buffers
+    void *rec = nullptr;        // gravity: float4/double4 {x,y,z,m} Morton-sorted; helmholtz: complex xs
+    uint32_t *skey = nullptr, *perm = nullptr, *bkey = nullptr, *bstart = nullptr;
+    uint32_t *nbr_off = nullptr, *nbr_box = nullptr;
+    uint8_t *nbr_slot = nullptr;
+    uint64_t *red_off = nullptr;
+    uint32_t *box_of = nullptr;  // dense Morton-key -> box lookup (validated by bkey, never cleared)
+    p2p::Item *items = nullptr;
+    void *red = nullptr;         // gravity red[R] records; helmholtz Xg[B][9][t]
+    void *table = nullptr;       // helmholtz pattern table P[t][9t] complex
+    p2p::DevCounters *ctr = nullptr;
+    bool red_valid = false;
+    p2p_status sticky = P2P_OK;
+    int eval_blocks[3] = {0, 0, 0};
+};
+
+namespace p2p {
+
+// k_sort.cu: stable LSD radix sort of (key, value) pairs, `passes` 8-bit digits.  On return the sorted
+// pairs are in (*kout, *vout) which point to either the in or the alt buffers.
+cudaError_t radix_sort_pairs(uint32_t *kin, uint32_t *vin, uint32_t *kalt, uint32_t *valt, uint32_t n, int passes,
+                             DevCounters *ctr, cudaStream_t st, uint32_t **kout, uint32_t **vout);
+
+// k_structs.cu
+p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q);
+p2p_status build_helmholtz_structs(p2p_plan *P, const void *pos, const void *q);
+p2p_status set_charges_gravity(p2p_plan *P, const void *q);
+p2p_status set_charges_helmholtz(p2p_plan *P, const void *q);
+
+// k_restructure.cu
+p2p_status restructure_gravity(p2p_plan *P);
+p2p_status restructure_helmholtz(p2p_plan *P);
+
+// k_eval_gravity.cu / k_helmholtz.cu
+p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field);
+p2p_status eval_helmholtz(p2p_plan *P, p2p_layout layout, void *y);
+p2p_status helmholtz_table(p2p_plan *P);
+
+// allocation helpers (stream-ordered, pooled)
+cudaError_t dalloc(void **p, size_t bytes, cudaStream_t st);
+void dfree(void *p, cudaStream_t st);
+
+}  // namespace p2p

@@ -1,0 +1,178 @@
+"""GPU parity of the gravity path (-m gpu): the CUDA library through its C ABI vs the fp64 oracle.
+
+Bars (BASELINE north_star): sort order, box table, neighbour lists and redundant buffers bit-exact; potentials
+and fields within relative L2 1e-5 (fp32) / 1e-12 (fp64) of the oracle's plain definition (mode ii);
+P2P_REDUNDANT == P2P_INDEXED_BITWISE bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+import p2p_inputs as G
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float32: 1e-5, np.float64: 1e-12}
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2511_21535_b200 as P
+    return P
+
+
+def gpu_plan(P, inp):
+    pos = torch.from_numpy(inp.pos).cuda()
+    m = torch.from_numpy(inp.mass).cuda()
+    return P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps)
+
+
+def check_structs(P, plan, gp):
+    assert plan.info.n_boxes == gp.B and plan.info.n_nbr == gp.n_nbr
+    assert plan.info.n_red == gp.R and plan.info.n_pairs == gp.I
+    assert np.array_equal(plan.copy_out(P.P2P_ARR_SORTED_KEYS), gp.skey)
+    assert np.array_equal(plan.copy_out(P.P2P_ARR_PERM), gp.perm)
+    assert np.array_equal(plan.copy_out(P.P2P_ARR_BOX_KEYS), gp.bkey)
+    assert np.array_equal(plan.copy_out(P.P2P_ARR_BOX_START), gp.bstart)
+    assert np.array_equal(plan.copy_out(P.P2P_ARR_NBR_OFF), gp.nbr_off)
+    assert np.array_equal(plan.copy_out(P.P2P_ARR_NBR_BOX), gp.nbr_box)
+    assert np.array_equal(plan.copy_out(P.P2P_ARR_NBR_SLOT), gp.nbr_slot)
+    assert np.array_equal(plan.copy_out(P.P2P_ARR_RED_OFF), gp.red_off)
+
+
+def run_all_layouts(P, plan):
+    plan.restructure()
+    out = {}
+    for name, lay in P.LAYOUTS.items():
+        phi, f = plan.eval(lay)
+        torch.cuda.synchronize()
+        out[name] = (phi.cpu().numpy(), f.cpu().numpy())
+    return out
+
+
+def check_case(P, inp, structs=True):
+    dt = inp.pos.dtype.type
+    gp = oracle.GravityPlan(inp)
+    ref_phi, ref_f = gp.eval_indexed()
+    with gpu_plan(P, inp) as plan:
+        if structs:
+            check_structs(P, plan, gp)
+        out = run_all_layouts(P, plan)
+        if structs:
+            red = plan.copy_out(P.P2P_ARR_RED)
+            assert red.tobytes() == gp.red.tobytes()     # bit-exact redundant buffer
+    for name, (phi, f) in out.items():
+        assert oracle.rel_l2(phi, ref_phi) <= TOL[dt], name
+        assert oracle.rel_l2(f, ref_f) <= TOL[dt], name
+    # REDUNDANT and INDEXED_BITWISE stage identical bits -> identical outputs
+    assert out["redundant"][0].tobytes() == out["indexed_bitwise"][0].tobytes()
+    assert out["redundant"][1].tobytes() == out["indexed_bitwise"][1].tobytes()
+    return out
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_c1(P, dtype):
+    check_case(P, G.uniform_per_box(4, 16, seed=0, dtype=dtype))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_ragged_random_boundaries(P, seed):
+    rng = np.random.default_rng(200 + seed)
+    per = [0b111, 0, 0b010, 0b101, 0b111, 0b011, 0b111, 0][seed]
+    nbox = tuple(int(v) for v in rng.integers(3, 9, size=3))
+    dt = np.float64 if seed % 2 else np.float32
+    inp = G.random_gravity(int(rng.integers(100, 3000)), 0, seed=seed, dtype=dt, periodic=per, nbox=nbox, h=0.13,
+                           lo=(-0.4, 0.25, 2.0))
+    check_case(P, inp)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_plummer_clustered(P, dtype):
+    # dense clustered boxes: > 128 targets per box (several work items), runs longer than one pipeline stage
+    check_case(P, G.plummer(20000, 8, seed=1, dtype=dtype))
+
+
+def test_hundred_c1_scenarios(P):
+    """>= 100 seeded C1-sized scenarios (S:L590 acceptance criterion 1), structures + values"""
+    for seed in range(100):
+        inp = G.uniform_per_box(4, 16, seed=seed) if seed % 2 == 0 else G.random_gravity(1024, 4, seed=seed)
+        check_case(P, inp, structs=(seed % 10 == 0))
+
+
+def test_edge_cases(P):
+    # single particle, all particles in one box, one box per dim, empty input
+    one = G.GravityInput(np.array([[0.1, 0.2, 0.3]], np.float32), np.array([0.5], np.float32), (0, 0, 0), 0.25,
+                         (4, 4, 4), 0b111, 1e-3)
+    out = check_case(P, one)
+    assert out["redundant"][0][0] == 0.0 and np.all(out["redundant"][1] == 0.0)
+    rng = np.random.default_rng(0)
+    box = G.GravityInput((0.5 + 0.2 * rng.random((700, 3))).astype(np.float32),
+                         rng.uniform(0.5, 1.5, 700).astype(np.float32) / 700, (0, 0, 0), 1.0, (1, 1, 1), 0, 1e-2)
+    check_case(P, box)
+    empty = G.GravityInput(np.zeros((0, 3), np.float32), np.zeros(0, np.float32), (0, 0, 0), 0.25, (4, 4, 4), 0b111,
+                           1e-3)
+    with gpu_plan(P, empty) as plan:
+        assert plan.info.n_boxes == 0
+        plan.restructure()
+        phi, f = plan.eval(P.P2P_REDUNDANT)
+        assert phi.numel() == 0
+
+
+def test_errors(P):
+    inp = G.uniform_per_box(4, 2, seed=0)
+    bad = inp.pos.copy()
+    bad[17, 1] = 1.0                     # x = lo + n h is outside the domain (C6)
+    with pytest.raises(P.P2PError) as e:
+        gpu_plan(P, G.GravityInput(bad, inp.mass, inp.lo, inp.h, inp.nbox, inp.periodic, inp.eps))
+    assert e.value.status == P.P2P_ERR_OUT_OF_DOMAIN and "17" in str(e.value)
+    with gpu_plan(P, inp) as plan:
+        with pytest.raises(P.P2PError) as e:
+            plan.eval(P.P2P_REDUNDANT)   # before restructure
+        assert e.value.status == P.P2P_ERR_BAD_STATE
+        plan.restructure()
+        plan.eval(P.P2P_REDUNDANT)
+        plan.set_charges(torch.from_numpy(inp.mass * 2).cuda())
+        with pytest.raises(P.P2PError) as e:
+            plan.eval(P.P2P_REDUNDANT)   # red[] invalidated by set_charges
+        assert e.value.status == P.P2P_ERR_BAD_STATE
+    # host pointers rejected
+    cfg = P.make_config(P.P2P_GRAVITY, P.P2P_FP32, inp.h, inp.lo, inp.nbox, inp.periodic, eps=1e-3)
+    with pytest.raises(P.P2PError) as e:
+        P.p2p_plan_create(cfg, inp.n, inp.pos.ctypes.data, inp.mass.ctypes.data)
+    assert e.value.status == P.P2P_ERR_INVALID_ARGUMENT
+
+
+def test_set_charges_reuses_geometry(P):
+    inp = G.uniform_per_box(5, 8, seed=3)
+    m2 = (inp.mass * np.float32(1.7)).astype(np.float32)
+    ref = oracle.GravityPlan(G.GravityInput(inp.pos, m2, inp.lo, inp.h, inp.nbox, inp.periodic, inp.eps))
+    rphi, rf = ref.eval_indexed()
+    with gpu_plan(P, inp) as plan:
+        plan.set_charges(torch.from_numpy(m2).cuda())
+        plan.restructure()
+        for lay in P.LAYOUTS.values():
+            phi, f = plan.eval(lay)
+            assert oracle.rel_l2(phi.cpu().numpy(), rphi) < 1e-5
+            assert oracle.rel_l2(f.cpu().numpy(), rf) < 1e-5
+
+
+def test_determinism(P):
+    inp = G.plummer(30000, 16, seed=7)
+    res = []
+    for _ in range(2):
+        with gpu_plan(P, inp) as plan:
+            res.append(run_all_layouts(P, plan))
+    for name in res[0]:
+        assert res[0][name][0].tobytes() == res[1][name][0].tobytes()
+        assert res[0][name][1].tobytes() == res[1][name][1].tobytes()
+
+
+def test_nearfield_host_api(P):
+    inp = G.uniform_per_box(6, 8, seed=11)
+    phi, f = P.nearfield(P.P2P_GRAVITY, torch.from_numpy(inp.pos), torch.from_numpy(inp.mass), inp.h, inp.lo,
+                         inp.nbox, inp.periodic, eps=inp.eps)
+    assert not phi.is_cuda
+    rphi, rf = oracle.GravityPlan(inp).eval_indexed()
+    assert oracle.rel_l2(phi.numpy(), rphi) < 1e-5 and oracle.rel_l2(f.numpy(), rf) < 1e-5

@@ -1,0 +1,82 @@
+"""GPU parity of the Helmholtz (DBIM-like) path (-m gpu): structures bit-exact, y within 1e-5 (complex64) /
+1e-12 (complex128) of the oracle, REDUNDANT (im2col Xg) == INDEXED bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+import p2p_inputs as G
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2511_21535_b200 as P
+    return P
+
+
+def gpu_plan(P, inp, f64=False):
+    rdt = torch.float64 if f64 else torch.float32
+    pos = torch.from_numpy(inp.pos.astype(np.float64 if f64 else np.float32)).cuda()
+    x = np.ascontiguousarray(inp.x.astype(np.complex128 if f64 else np.complex64))
+    xr = torch.from_numpy(x.view(np.float64 if f64 else np.float32).reshape(-1, 2)).cuda().to(rdt)
+    return P.Plan(P.P2P_HELMHOLTZ2D, pos, xr, inp.h, inp.lo, inp.nbox, 0, k=inp.k, t=inp.t)
+
+
+def to_c(y):
+    a = y.cpu().numpy()
+    return a[:, 0] + 1j * a[:, 1]
+
+
+@pytest.mark.parametrize("t,n,holes,f64", [(16, 8, None, False), (64, 6, None, False), (4, 5, [(1, 2)], False),
+                                           (1, 7, None, False), (16, 6, [(0, 0), (3, 3)], True), (9, 4, None, True)])
+def test_helmholtz_parity(P, t, n, holes, f64):
+    inp = G.dbim_lattice(n, t, seed=t + n, holes=holes)
+    hp = oracle.HelmholtzPlan(inp)
+    ref = hp.eval_table()
+    assert oracle.rel_l2(ref, oracle.helm_dense(inp)) < 1e-13
+    with gpu_plan(P, inp, f64) as plan:
+        assert plan.info.n_boxes == hp.B
+        assert plan.info.n_pairs == hp.n_pairs
+        assert np.array_equal(plan.copy_out(P.P2P_ARR_PERM), hp.perm)
+        assert np.array_equal(plan.copy_out(P.P2P_ARR_SORTED_KEYS), hp.skey)
+        assert np.array_equal(plan.copy_out(P.P2P_ARR_BOX_KEYS), hp.bkey)
+        assert np.array_equal(plan.copy_out(P.P2P_ARR_BOX_START), hp.bstart)
+        assert np.array_equal(plan.copy_out(P.P2P_ARR_NBR_BOX), hp.nbr9.ravel())
+        plan.restructure()
+        Xg = plan.copy_out(P.P2P_ARR_RED).reshape(hp.B, 9, t)
+        assert np.array_equal(Xg, hp.xg().astype(Xg.dtype))   # zero-padded im2col, bit copies
+        y_red = to_c(plan.eval(P.P2P_REDUNDANT))
+        y_idx = to_c(plan.eval(P.P2P_INDEXED))
+    tol = 1e-12 if f64 else 1e-5
+    assert oracle.rel_l2(y_red, ref) <= tol
+    assert oracle.rel_l2(y_idx, ref) <= tol
+    assert np.array_equal(y_red, y_idx)
+
+
+def test_irregular_rejected(P):
+    inp = G.dbim_lattice(3, 4, seed=0)
+    pos = inp.pos.copy()
+    pos[0] = pos[1]
+    bad = G.HelmholtzInput(pos, inp.x, inp.lo, inp.h, inp.nbox, inp.t, inp.delta, inp.k)
+    with pytest.raises(P.P2PError) as e:
+        gpu_plan(P, bad)
+    assert e.value.status == P.P2P_ERR_UNSUPPORTED
+
+
+def test_set_charges_dbim_iterations(P):
+    """DBIM reuses the geometry across iterations: new unknowns, same plan"""
+    inp = G.dbim_lattice(8, 16, seed=1)
+    rng = np.random.default_rng(5)
+    with gpu_plan(P, inp) as plan:
+        for it in range(3):
+            x = ((rng.normal(size=inp.n) + 1j * rng.normal(size=inp.n)) / np.sqrt(2)).astype(np.complex64)
+            plan.set_charges(torch.from_numpy(x.view(np.float32).reshape(-1, 2)).cuda())
+            plan.restructure()
+            y = to_c(plan.eval(P.P2P_REDUNDANT))
+            ref = oracle.HelmholtzPlan(G.HelmholtzInput(inp.pos, x, inp.lo, inp.h, inp.nbox, inp.t, inp.delta,
+                                                        inp.k)).eval_table()
+            assert oracle.rel_l2(y, ref) < 1e-5
