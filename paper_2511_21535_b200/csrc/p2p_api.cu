@@ -2,7 +2,9 @@
 // Every step of the path runs in this library's kernels (k_*.cu); this file only orchestrates.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -17,6 +19,24 @@ std::atomic<uint64_t> g_launches{0};
 void set_error(const std::string &msg) { g_err = msg; }
 
 static bool g_pool_configured = false;
+
+// P2P_TRACE=1: host-side phase timestamps of p2p_plan_create on stderr (diagnostics only)
+static bool trace_on() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("P2P_TRACE");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+struct Tracer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void at(const char *what) {
+        if (!trace_on()) return;
+        auto us = std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count();
+        fprintf(stderr, "[p2p trace] %-28s %8lld us\n", what, (long long)us);
+    }
+};
 
 cudaError_t dalloc(void **p, size_t bytes, cudaStream_t st) {
     *p = nullptr;
@@ -139,6 +159,7 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
     if (n_local > 0 && (!is_device_ptr(positions) || !is_device_ptr(charges)))
         return fail(P2P_ERR_INVALID_ARGUMENT, "positions / charges must be device pointers");
 
+    Tracer tr;
     p2p_plan *P = new p2p_plan();
     P->cfg = *cfg;
     P->stream = (cudaStream_t)cfg->stream;
@@ -200,13 +221,16 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
         *out = P;
         return P2P_OK;
     }
+    tr.at("validated+counters");
     p2p_status s = grav ? build_gravity_structs(P, positions, charges) : build_helmholtz_structs(P, positions, charges);
     if (s != P2P_OK) return bail(s);
+    tr.at("structs enqueued");
     // the ONE host synchronisation: sizes for the redundant buffer and launch geometry
     DevCounters h;
     cudaError_t e = cudaMemcpyAsync(&h, P->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return bail(fail(P2P_ERR_CUDA, std::string("CUDA error in plan build: ") + cudaGetErrorString(e)));
+    tr.at("synchronised");
     if (h.err_index != ~0ull) {
         char buf[160];
         snprintf(buf, sizeof buf, "position of input particle %llu is outside the domain [lo, lo + nbox*h) (C6)",
@@ -234,6 +258,7 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
         s = helmholtz_table(P);
         if (s != P2P_OK) return bail(s);
     }
+    tr.at("red allocated");
     *out = P;
     return P2P_OK;
 }
