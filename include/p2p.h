@@ -109,6 +109,15 @@ typedef struct {
 p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *positions, const void *charges,
                            p2p_plan **out);
 
+/* Rebuild a1..a5 of an existing GRAVITY plan for new positions / charges (a PhotoNs-like time step: the
+ * particles moved, the tree is rebuilt every step, §4, §5.2.3 item 1).  Same config; n_local may
+ * change (buffers grow stream-ordered if n_local exceeds the capacity).  Fully ASYNCHRONOUS: no host
+ * synchronisation and, in steady state, no allocation -- box / neighbour / buffer counts stay on the device
+ * (the redundant buffer is sized for the worst case R <= 27 n_local).  Input errors detected on the device
+ * (P2P_ERR_OUT_OF_DOMAIN) are reported by the next synchronising call (p2p_get_info / p2p_copy_out); results
+ * computed in between are undefined.  Invalidates red[] (restructure again).  Helmholtz: P2P_ERR_UNSUPPORTED. */
+p2p_status p2p_plan_update(p2p_plan *plan, int64_t n_local, const void *positions, const void *charges);
+
 /* a6: build the redundant buffer (gravity: red[R] records {x,y,z,m} rebased to the target box origin,
  * C11; helmholtz: Xg[B][9][t], zero segments for missing neighbours, C10).  Enqueue only. */
 p2p_status p2p_restructure(p2p_plan *plan);

@@ -69,6 +69,7 @@ def lib() -> C.CDLL:
         p, i64, u64 = C.c_void_p, C.c_int64, C.c_uint64
         sig = {
             "p2p_plan_create": (C.c_int, [C.POINTER(P2PConfig), i64, p, p, C.POINTER(C.c_void_p)]),
+            "p2p_plan_update": (C.c_int, [p, i64, p, p]),
             "p2p_restructure": (C.c_int, [p]),
             "p2p_eval": (C.c_int, [p, C.c_int, p, p]),
             "p2p_set_charges": (C.c_int, [p, p]),
@@ -109,6 +110,10 @@ def p2p_plan_create(cfg: P2PConfig, n_local: int, positions: int, charges: int) 
     _check(lib().p2p_plan_create(C.byref(cfg), int(n_local), C.c_void_p(positions), C.c_void_p(charges),
                                  C.byref(out)))
     return out.value
+
+
+def p2p_plan_update(plan: int, n_local: int, positions: int, charges: int):
+    _check(lib().p2p_plan_update(C.c_void_p(plan), int(n_local), C.c_void_p(positions), C.c_void_p(charges)))
 
 
 def p2p_restructure(plan: int):
@@ -214,13 +219,34 @@ class Plan:
         self.cfg = make_config(kernel, prec, h, lo, nbox, periodic, eps, k, t, self.stream.cuda_stream)
         self.n = int(positions.shape[0])
         self._handle = p2p_plan_create(self.cfg, self.n, positions.data_ptr(), charges.data_ptr())
-        self.info = p2p_get_info(self._handle)
+        self._info = p2p_get_info(self._handle)
+
+    @property
+    def info(self) -> P2PInfo:
+        """sizes of the current structures (synchronises once after an asynchronous update())"""
+        if self._info is None:
+            self._info = p2p_get_info(self.handle)
+        return self._info
 
     @property
     def handle(self) -> int:
         if not self._handle:
             raise P2PError(P2P_ERR_BAD_STATE, "plan destroyed")
         return self._handle
+
+    def update(self, positions, charges):
+        """a PhotoNs-like time step: rebuild a1..a5 for moved particles, asynchronously (no host sync); the
+        sizes in self.info refresh lazily (refresh_info() synchronises and reports input errors)."""
+        positions = positions.contiguous()
+        charges = charges.contiguous()
+        self.n = int(positions.shape[0])
+        p2p_plan_update(self.handle, self.n, positions.data_ptr(), charges.data_ptr())
+        self._keep = (positions, charges)
+        self._info = None
+
+    def refresh_info(self):
+        self._info = p2p_get_info(self.handle)
+        return self._info
 
     def restructure(self):
         p2p_restructure(self.handle)
@@ -244,7 +270,7 @@ class Plan:
         return potential
 
     def copy_out(self, which: int) -> np.ndarray:
-        i = self.info
+        i = self.refresh_info()
         f64 = self.precision == P2P_FP64
         if which == P2P_ARR_PERM or which == P2P_ARR_SORTED_KEYS:
             a = np.empty(i.n_local, np.uint32)

@@ -8,22 +8,28 @@
 //                        (cp.async.bulk, SASS UBLKCP) per chunk of the run.
 //   P2P_INDEXED          non-redundant baseline (§5.2.1): the <= 27 neighbour segments of the
 //                        Morton-sorted records rec[], located through the CSR, one bulk copy per segment piece;
-//                        absolute fp32 coordinates, periodic images applied as exact +-L shifts.
+//                        absolute coordinates, periodic images applied as exact -L shifts.
 //   P2P_INDEXED_BITWISE  as INDEXED, then each staged record is rebased in shared memory exactly like a red[]
 //                        record, so the arithmetic and the outputs equal P2P_REDUNDANT bit for bit.
 //
 // B200 design (the paper's GTX 1050 thread-per-particle kernel is prior art, not the blueprint):
-//   * persistent CTAs (EV_WARPS warps each); every warp pulls work items (box, target chunk) from a global
-//     atomic queue and runs its own 2-stage producer/consumer pipeline: while it computes chunk c from one
-//     shared-memory stage, the bulk copy of chunk c+1 (possibly the next item's first chunk) lands in the
-//     other stage, completion tracked by an mbarrier with expect_tx.
+//   * persistent CTAs (EV_WARPS warps each); every warp pulls work items (box, <= 32-target chunk) from a
+//     global atomic queue (index fetched one item ahead) and runs its own 2-stage producer/consumer pipeline:
+//     while it computes chunk c from one shared-memory stage, the bulk copies of chunk c+1 -- or of the next
+//     item's first chunk AND its targets -- land in the other stage (mbarrier + expect_tx completion).
 //   * targets live in registers: lane (g, s) holds K targets (group g) and walks the staged sources
-//     j = s, s+S, ... (S = floor(32/G) source splits, G = ceil(n_t/K) groups), so a box of any occupancy keeps
-//     (almost) all 32 lanes busy; the S partial sums are combined by a fixed shuffle tree (deterministic).
-//   * inner loop per (source, target): 3 FADD + 3 FFMA + MUFU.RSQ + FMUL + FADD + 2 FMUL + 3 FFMA = 13 FP32-pipe
-//     instructions + 1 MUFU (fp32) -> the FP32 pipe is the roofline.  The self pair
-//     (d = 0, r^2 = eps^2) is evaluated like any other and its potential term subtracted bit-exactly after
-//     the loop (DESIGN C3).
+//     j = s, s+S, ... (S source splits, G groups; S, G precomputed per item by k_nbr_fill), so boxes of any
+//     occupancy keep (almost) all 32 lanes busy; the S partial sums are combined by a fixed shuffle tree
+//     (deterministic).
+//   * fp32: targets are paired and the pair math is issued as packed FP32x2 instructions (FADD2 / FMUL2 /
+//     FFMA2, sm_100a; the source component is a broadcast scalar operand), so the 13 FP32-pipe lane-ops of an
+//     interaction cost only 6.5 issue slots + 1 MUFU.RSQ: the kernel is bound by the FP32 pipe
+//     (128 lane-ops/clk/SM), not by instruction issue.  The rounding of every operation is the same as the
+//     scalar formula (fma.rn.f32x2 == two fma.rn.f32).
+//   * the self pair (d = 0, r^2 = eps^2) is evaluated like any other and its potential term subtracted
+//     bit-exactly after the loop (DESIGN C3).
+#include <type_traits>
+
 #include "plan.hpp"
 
 namespace p2p {
@@ -34,7 +40,42 @@ template <> struct V4T<float> { using type = float4; };
 template <> struct V4T<double> { using type = double4; };
 
 constexpr int EV_WARPS = 4;              // warps per CTA
-constexpr int EV_STAGE_BYTES = 4096;     // one pipeline stage per warp (256 fp32 / 128 fp64 records)
+constexpr int EV_STAGE_BYTES = 4096;     // source records per pipeline stage per warp (256 fp32 / 128 fp64)
+constexpr int EV_TGT = 32;               // max targets per item (ITEM_TMAX in k_structs.cu)
+
+// ceil(2^20 / S) for S = 0..32: x / S == (x * M20[S]) >> 20 exactly for x < 2^11 (no integer division)
+__constant__ uint32_t c_m20[33] = {0,       1048576, 524288, 349526, 262144, 209716, 174763, 149797, 131072,
+                                   116509,  104858,  95326,  87382,  80660,  74899,  69906,  65536,  61681,
+                                   58255,   55189,   52429,  49933,  47663,  45591,  43691,  41944,  40330,
+                                   38837,   37450,   36158,  34953,  33826,  32768};
+
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float a, float b) {
+    u64 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(u64 v, float &a, float &b) { asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
 
 template <typename T>
 struct EvalArgs {
@@ -46,25 +87,11 @@ struct EvalArgs {
     const uint64_t *red_off;
     const uint32_t *perm;
     const Item *items;
-    uint32_t n_items;
+    const uint32_t *n_items;   // device-side count (valid without a host sync after p2p_plan_update)
     unsigned int *item_head;
     T *phi;
     T *field;
 };
-
-template <typename T>
-__device__ __forceinline__ T rinv_of(T r2);
-template <>
-__device__ __forceinline__ float rinv_of<float>(float r2) { return rsqrt_ftz(r2); }
-template <>
-__device__ __forceinline__ double rinv_of<double>(double r2) { return 1.0 / sqrt(r2); }
-
-template <typename T>
-__device__ __forceinline__ T fma_(T a, T b, T c);
-template <>
-__device__ __forceinline__ float fma_<float>(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-template <>
-__device__ __forceinline__ double fma_<double>(double a, double b, double c) { return __fma_rn(a, b, c); }
 
 // image shift of stencil slot seen from box c (DESIGN C5)
 __device__ __forceinline__ double slot_shift(const Geom &g, const uint32_t c[3], int slot, int d) {
@@ -82,17 +109,136 @@ __device__ __forceinline__ double frame_shift(const Geom &g, const uint32_t c[3]
     return (((g.periodic >> d) & 1u) && (int)c[d] == g.nbox[d] - 1) ? -g.L[d] : 0.0;
 }
 
+// ---- per-lane target block + accumulators --------------------------------------------------------
+template <typename T, int K>
+struct Tgt;
+
+// fp32: K targets as K/2 packed pairs (float2 + the sm_100 packed intrinsics __fadd2_rn / __fmul2_rn /
+// __ffma2_rn -> SASS FADD2 / FMUL2 / FFMA2; the broadcast source component becomes a scalar operand)
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
+
+template <int K>
+struct Tgt<float, K> {
+    static constexpr int P = K / 2;
+    float2 tx[P], ty[P], tz[P], ap[P], ax[P], ay[P], az[P];
+    __device__ __forceinline__ void set(int k, float x, float y, float z) {
+        const int p = k >> 1;
+        if (k & 1) { tx[p].y = x; ty[p].y = y; tz[p].y = z; }
+        else { tx[p].x = x; ty[p].x = y; tz[p].x = z; }
+    }
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int p = 0; p < P; ++p) tx[p] = ty[p] = tz[p] = ap[p] = ax[p] = ay[p] = az[p] = make_float2(0.f, 0.f);
+    }
+    __device__ __forceinline__ void interact(const float4 &s, float2 E) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const float2 dx = __fadd2_rn(bc(s.x), neg2(tx[p]));
+            const float2 dy = __fadd2_rn(bc(s.y), neg2(ty[p]));
+            const float2 dz = __fadd2_rn(bc(s.z), neg2(tz[p]));
+            float2 r2 = __ffma2_rn(dx, dx, E);
+            r2 = __ffma2_rn(dy, dy, r2);
+            r2 = __ffma2_rn(dz, dz, r2);
+            const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+            const float2 mri = __fmul2_rn(bc(s.w), ri);
+            ap[p] = __fadd2_rn(ap[p], mri);
+            const float2 m3 = __fmul2_rn(__fmul2_rn(mri, ri), ri);
+            ax[p] = __ffma2_rn(m3, dx, ax[p]);
+            ay[p] = __ffma2_rn(m3, dy, ay[p]);
+            az[p] = __ffma2_rn(m3, dz, az[p]);
+        }
+    }
+    __device__ __forceinline__ void reduce(uint32_t S, uint32_t sl) {
+        for (uint32_t off = 1; off < S; off <<= 1) {
+            const bool take = sl + off < S;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                float2 v[4] = {ap[p], ax[p], ay[p], az[p]};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    v[q].x = __shfl_down_sync(0xffffffffu, v[q].x, off);
+                    v[q].y = __shfl_down_sync(0xffffffffu, v[q].y, off);
+                }
+                if (take) {
+                    ap[p] = __fadd2_rn(ap[p], v[0]);
+                    ax[p] = __fadd2_rn(ax[p], v[1]);
+                    ay[p] = __fadd2_rn(ay[p], v[2]);
+                    az[p] = __fadd2_rn(az[p], v[3]);
+                }
+            }
+        }
+    }
+    __device__ __forceinline__ void get(int k, float &p_, float &x, float &y, float &z) const {
+        const int p = k >> 1;
+        p_ = (k & 1) ? ap[p].y : ap[p].x;
+        x = (k & 1) ? ax[p].y : ax[p].x;
+        y = (k & 1) ? ay[p].y : ay[p].x;
+        z = (k & 1) ? az[p].y : az[p].x;
+    }
+    static __device__ __forceinline__ float self_rinv(float eps2) { return rsqrt_ftz(__fmaf_rn(0.f, 0.f, eps2)); }
+    static __device__ __forceinline__ float2 eps_pack(float e2) { return make_float2(e2, e2); }
+};
+
+// fp64: scalar
+template <int K>
+struct Tgt<double, K> {
+    double tx[K], ty[K], tz[K], ap[K], ax[K], ay[K], az[K];
+    __device__ __forceinline__ void set(int k, double x, double y, double z) {
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if (q == k) { tx[q] = x; ty[q] = y; tz[q] = z; }
+    }
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int k = 0; k < K; ++k) tx[k] = ty[k] = tz[k] = ap[k] = ax[k] = ay[k] = az[k] = 0.0;
+    }
+    __device__ __forceinline__ void interact(const double4 &s, double E) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const double dx = s.x - tx[k], dy = s.y - ty[k], dz = s.z - tz[k];
+            double r2 = __fma_rn(dx, dx, E);
+            r2 = __fma_rn(dy, dy, r2);
+            r2 = __fma_rn(dz, dz, r2);
+            const double ri = 1.0 / sqrt(r2);
+            const double mri = s.w * ri;
+            ap[k] += mri;
+            const double m3 = mri * ri * ri;
+            ax[k] = __fma_rn(m3, dx, ax[k]);
+            ay[k] = __fma_rn(m3, dy, ay[k]);
+            az[k] = __fma_rn(m3, dz, az[k]);
+        }
+    }
+    __device__ __forceinline__ void reduce(uint32_t S, uint32_t sl) {
+        for (uint32_t off = 1; off < S; off <<= 1) {
+            const bool take = sl + off < S;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const double v0 = __shfl_down_sync(0xffffffffu, ap[k], off), v1 = __shfl_down_sync(0xffffffffu, ax[k], off);
+                const double v2 = __shfl_down_sync(0xffffffffu, ay[k], off), v3 = __shfl_down_sync(0xffffffffu, az[k], off);
+                if (take) { ap[k] += v0; ax[k] += v1; ay[k] += v2; az[k] += v3; }
+            }
+        }
+    }
+    __device__ __forceinline__ void get(int k, double &p_, double &x, double &y, double &z) const {
+        p_ = ap[k]; x = ax[k]; y = ay[k]; z = az[k];
+    }
+    static __device__ __forceinline__ double self_rinv(double eps2) { return 1.0 / sqrt(__fma_rn(0.0, 0.0, eps2)); }
+    static __device__ __forceinline__ double eps_pack(double e2) { return e2; }
+};
+
 template <typename T, int LAYOUT, int K>
 __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T> a) {
     using V4 = typename V4T<T>::type;
     constexpr int CH = EV_STAGE_BYTES / (int)sizeof(V4);
+    constexpr int STAGE_RECS = CH + EV_TGT;  // source chunk + the item's targets
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[EV_WARPS][2];
 
     const int w = threadIdx.x >> 5;
     const unsigned lane = threadIdx.x & 31u;
-    V4 *stage_base = reinterpret_cast<V4 *>(smem_raw + (size_t)w * 2 * EV_STAGE_BYTES);
+    V4 *stage_base = reinterpret_cast<V4 *>(smem_raw) + (size_t)w * 2 * STAGE_RECS;
     uint64_t *bar = bars[w];
     if (lane == 0) {
         mbar_init(&bar[0], 1);
@@ -102,9 +248,11 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
     __syncwarp();
 
     const T eps2 = (T)a.g.eps2;
+    const auto E = Tgt<T, K>::eps_pack(eps2);
+    const uint32_t n_items = *a.n_items;
 
     // ---------------- producer state (item whose chunks are being copied in) ----------------
-    uint32_t p_item, p_box = 0, p_R = 0, p_nch = 0;
+    uint32_t p_box = 0, p_t0 = 0, p_meta = 0, p_key = 0, p_R = 0, p_nch = 0;
     uint64_t p_base = 0;
     uint32_t p_src = 0, p_st = 0, p_cnt = 0, p_slot = 0, p_ne = 0;  // INDEXED: lane = segment
 
@@ -116,6 +264,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
     auto load_item = [&](uint32_t idx) {
         const Item it = a.items[idx];
         p_box = it.box;
+        p_t0 = it.t0;
+        p_meta = it.meta;
+        p_key = a.bkey[p_box];
         if (LAYOUT == P2P_REDUNDANT) {
             p_base = a.red_off[p_box];
             p_R = (uint32_t)(a.red_off[p_box + 1] - p_base);
@@ -140,13 +291,15 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
         }
         p_nch = (p_R + CH - 1) / CH;
     };
+    // copy chunk `chunk` of the producer item into stage s (+ the item's targets when chunk == 0)
     auto issue = [&](uint32_t chunk, int s) {
         const uint32_t c0 = chunk * CH;
         const uint32_t cnt = min((uint32_t)CH, p_R - c0);
-        V4 *dst = stage_base + s * CH;
+        const uint32_t nt = p_meta & 0xffu;
+        V4 *dst = stage_base + s * STAGE_RECS;
         if (lane == 0) {
             fence_proxy_async_smem();  // order earlier generic smem accesses of this stage before the async write
-            mbar_arrive_expect_tx(&bar[s], cnt * (uint32_t)sizeof(V4));
+            mbar_arrive_expect_tx(&bar[s], (cnt + (chunk == 0 ? nt : 0u)) * (uint32_t)sizeof(V4));
         }
         __syncwarp();
         if (LAYOUT == P2P_REDUNDANT) {
@@ -156,22 +309,22 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
             if (lane < p_ne && ov1 > ov0)
                 bulk_g2s(dst + (ov0 - c0), a.rec + p_src + (ov0 - p_st), (ov1 - ov0) * (uint32_t)sizeof(V4), &bar[s]);
         }
+        if (chunk == 0 && lane == 31) bulk_g2s(dst + CH, a.rec + p_t0, nt * (uint32_t)sizeof(V4), &bar[s]);
     };
 
-    p_item = fetch();
-    if (p_item >= a.n_items) return;
-    load_item(p_item);
+    uint32_t cur = fetch();
+    if (cur >= n_items) return;
+    uint32_t nxt = fetch();  // one item ahead: the atomic's latency overlaps the current item
+    load_item(cur);
     issue(0, 0);
     int s = 0;
     uint32_t phases = 0u;  // bit s = parity of stage s's mbarrier
 
     while (true) {
         // ---------------- adopt the producer's item as the current (consumer) item ----------------
-        const Item it = a.items[p_item];
-        const uint32_t c_box = p_box, c_R = p_R, c_nch = p_nch;
+        const uint32_t c_t0 = p_t0, c_meta = p_meta, c_R = p_R, c_nch = p_nch;
         const uint32_t c_st = p_st, c_cnt = p_cnt, c_slot = p_slot, c_ne = p_ne;
-        const uint32_t key = a.bkey[c_box];
-        const uint32_t cc[3] = {compact3(key), compact3(key >> 1), compact3(key >> 2)};
+        const uint32_t cc[3] = {compact3(p_key), compact3(p_key >> 1), compact3(p_key >> 2)};
         double org[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d)
@@ -182,54 +335,57 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
             for (int d = 0; d < 3; ++d)
                 needs_fix |= ((a.g.periodic >> d) & 1u) && (cc[d] == 0 || (int)cc[d] == a.g.nbox[d] - 1);
         }
-
-        // lane layout: G groups of K targets, S source splits
-        const uint32_t nt = it.nt;
-        const uint32_t G = (nt + K - 1) / K;
-        const uint32_t S = max(1u, 32u / G);
-        const uint32_t g = lane / S, sl = lane - g * S;
+        // lane layout (precomputed by k_nbr_fill): G groups of K targets x S source splits
+        const uint32_t nt = c_meta & 0xffu, S = (c_meta >> 8) & 0xffu, G = (c_meta >> 16) & 0xffu;
+        const uint32_t m20 = c_m20[S];
+        const uint32_t g = (lane * m20) >> 20, sl = lane - g * S;
         const bool active = g < G;
 
-        T tx[K], ty[K], tz[K], ap[K], ax[K], ay[K], az[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t ti = g * K + k;
-            T x = 0, y = 0, z = 0;
-            if (active && ti < nt) {
-                const V4 r = a.rec[it.t0 + ti];
-                if (LAYOUT == P2P_INDEXED) {
-                    x = r.x + (T)org[0];
-                    y = r.y + (T)org[1];
-                    z = r.z + (T)org[2];
-                } else {
-                    x = (T)__dsub_rn((double)r.x, org[0]);
-                    y = (T)__dsub_rn((double)r.y, org[1]);
-                    z = (T)__dsub_rn((double)r.z, org[2]);
-                }
-            }
-            tx[k] = x; ty[k] = y; tz[k] = z;
-            ap[k] = 0; ax[k] = 0; ay[k] = 0; az[k] = 0;
-        }
+        Tgt<T, K> tg;
+        tg.zero();
+        T tm[K];
 
         bool have_next = true;
         for (uint32_t c = 0; c < c_nch; ++c) {
-            // prefetch the next chunk into the other stage
+            // prefetch the next chunk (or the next item's first chunk + targets) into the other stage
             if (c + 1 < c_nch) {
                 issue(c + 1, s ^ 1);
+            } else if (nxt < n_items) {
+                load_item(nxt);
+                issue(0, s ^ 1);
+                cur = nxt;
+                nxt = fetch();
             } else {
-                p_item = fetch();
-                if (p_item < a.n_items) {
-                    load_item(p_item);
-                    issue(0, s ^ 1);
-                } else {
-                    have_next = false;
-                }
+                have_next = false;
             }
             mbar_wait(&bar[s], (phases >> s) & 1u);
             phases ^= 1u << s;
-            V4 *stg = stage_base + s * CH;
+            V4 *stg = stage_base + s * STAGE_RECS;
             const uint32_t c0 = c * CH;
             const uint32_t cnt = min((uint32_t)CH, c_R - c0);
+
+            if (c == 0) {  // targets landed with the first chunk
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const uint32_t ti = g * K + k;
+                    T x = 0, y = 0, z = 0, m = 0;
+                    if (active && ti < nt) {
+                        const V4 r = stg[CH + ti];
+                        m = r.w;
+                        if (LAYOUT == P2P_INDEXED) {
+                            x = r.x + (T)org[0];
+                            y = r.y + (T)org[1];
+                            z = r.z + (T)org[2];
+                        } else {
+                            x = (T)__dsub_rn((double)r.x, org[0]);
+                            y = (T)__dsub_rn((double)r.y, org[1]);
+                            z = (T)__dsub_rn((double)r.z, org[2]);
+                        }
+                    }
+                    tg.set(k, x, y, z);
+                    tm[k] = m;
+                }
+            }
 
             // ---- layout fix-ups of the staged raw records (INDEXED variants only) ----
             if (LAYOUT == P2P_INDEXED_BITWISE || (LAYOUT == P2P_INDEXED && needs_fix)) {
@@ -263,58 +419,41 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
 
             // ---- the hot loop: staged sources x register targets ----
             if (active && sl < cnt) {
-                const uint32_t nj = (cnt - 1 - sl) / S + 1;
+                // two sources per iteration with one remainder step: the accumulators stay in the same
+                // registers (no IMAD.MOV copies, which would occupy the FMA-heavy pipe the FFMA2s run on), and
+                // the addresses advance by pointer increments (ALU pipe) instead of IMAD
+                const uint32_t nj = (((cnt - 1 - sl) * m20) >> 20) + 1;
                 const V4 *sp = stg + sl;
-#pragma unroll 2
-                for (uint32_t q = 0; q < nj; ++q) {
-                    const V4 src = sp[q * S];
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const T dx = src.x - tx[k];
-                        const T dy = src.y - ty[k];
-                        const T dz = src.z - tz[k];
-                        T r2 = fma_(dx, dx, eps2);
-                        r2 = fma_(dy, dy, r2);
-                        r2 = fma_(dz, dz, r2);
-                        const T ri = rinv_of<T>(r2);
-                        const T mri = src.w * ri;
-                        ap[k] += mri;
-                        const T mri3 = mri * ri * ri;
-                        ax[k] = fma_(mri3, dx, ax[k]);
-                        ay[k] = fma_(mri3, dy, ay[k]);
-                        az[k] = fma_(mri3, dz, az[k]);
-                    }
+                const V4 *const end2 = sp + (size_t)(nj & ~1u) * S;
+#pragma unroll 1
+                for (; sp != end2; sp += 2 * S) {
+                    const V4 s0 = sp[0], s1 = sp[S];
+                    tg.interact(s0, E);
+                    tg.interact(s1, E);
                 }
+                if (nj & 1u) tg.interact(sp[0], E);
             }
             __syncwarp();
             s ^= 1;
         }
 
         // ---- combine the S source splits of each group (fixed shuffle tree -> deterministic) ----
-        for (uint32_t off = 1; off < S; off <<= 1) {
-            const bool take = sl + off < S;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                T v0 = __shfl_down_sync(FULL, ap[k], off), v1 = __shfl_down_sync(FULL, ax[k], off);
-                T v2 = __shfl_down_sync(FULL, ay[k], off), v3 = __shfl_down_sync(FULL, az[k], off);
-                if (take) { ap[k] += v0; ax[k] += v1; ay[k] += v2; az[k] += v3; }
-            }
-        }
+        tg.reduce(S, sl);
         // ---- a9: scatter to input order; remove the self potential term (DESIGN C3) ----
         if (active && sl == 0) {
+            const T rs = Tgt<T, K>::self_rinv(eps2);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const uint32_t ti = g * K + k;
                 if (ti < nt) {
-                    const uint32_t p = it.t0 + ti;
-                    const uint32_t i = a.perm[p];
-                    const T m = a.rec[p].w;
-                    const T self = m * rinv_of<T>(fma_((T)0, (T)0, eps2));
-                    a.phi[i] = -(ap[k] - self);
+                    const uint32_t i = a.perm[c_t0 + ti];
+                    T pot, fx, fy, fz;
+                    tg.get(k, pot, fx, fy, fz);
+                    a.phi[i] = -(pot - tm[k] * rs);
                     if (a.field) {
-                        a.field[3 * (size_t)i + 0] = ax[k];
-                        a.field[3 * (size_t)i + 1] = ay[k];
-                        a.field[3 * (size_t)i + 2] = az[k];
+                        a.field[3 * (size_t)i + 0] = fx;
+                        a.field[3 * (size_t)i + 1] = fy;
+                        a.field[3 * (size_t)i + 2] = fz;
                     }
                 }
             }
@@ -327,7 +466,7 @@ template <typename T, int LAYOUT, int K>
 p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
     using V4 = typename V4T<T>::type;
     auto kern = k_eval_gravity<T, LAYOUT, K>;
-    const int smem = EV_WARPS * 2 * EV_STAGE_BYTES;
+    const int smem = EV_WARPS * 2 * (EV_STAGE_BYTES + EV_TGT * (int)sizeof(V4));
     if (P->eval_blocks[slot] == 0) {
         P2P_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int per_sm = 0;
@@ -346,12 +485,13 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
     a.red_off = P->red_off;
     a.perm = P->perm;
     a.items = P->items;
-    a.n_items = (uint32_t)P->n_items;
+    a.n_items = &P->ctr->n_items;
     a.item_head = &P->ctr->item_head;
     a.phi = (T *)phi;
     a.field = (T *)field;
+    const int64_t nit = P->sizes_known ? P->n_items : P->cap;
     const unsigned grid =
-        (unsigned)std::min<int64_t>(P->eval_blocks[slot], std::max<int64_t>(1, (P->n_items + EV_WARPS - 1) / EV_WARPS));
+        (unsigned)std::min<int64_t>(P->eval_blocks[slot], std::max<int64_t>(1, (nit + EV_WARPS - 1) / EV_WARPS));
     P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->item_head, 0, sizeof(unsigned int), P->stream));
     P2P_LAUNCH(kern, grid, EV_WARPS * 32, smem, P->stream, a);
     P2P_CUDA_TRY(cudaGetLastError());
@@ -360,16 +500,18 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
 }  // namespace
 
 p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
-    if (P->n_items == 0) return P2P_OK;
+    if (P->sizes_known && P->n_items == 0) return P2P_OK;
     const bool f64 = P->cfg.precision == P2P_FP64;
     switch (layout) {
     case P2P_REDUNDANT:
-        return f64 ? launch<double, P2P_REDUNDANT, 2>(P, phi, field, 0) : launch<float, P2P_REDUNDANT, 4>(P, phi, field, 0);
+        return f64 ? launch<double, P2P_REDUNDANT, EVAL_K_F64>(P, phi, field, 0)
+                   : launch<float, P2P_REDUNDANT, EVAL_K_F32>(P, phi, field, 0);
     case P2P_INDEXED:
-        return f64 ? launch<double, P2P_INDEXED, 2>(P, phi, field, 1) : launch<float, P2P_INDEXED, 4>(P, phi, field, 1);
+        return f64 ? launch<double, P2P_INDEXED, EVAL_K_F64>(P, phi, field, 1)
+                   : launch<float, P2P_INDEXED, EVAL_K_F32>(P, phi, field, 1);
     case P2P_INDEXED_BITWISE:
-        return f64 ? launch<double, P2P_INDEXED_BITWISE, 2>(P, phi, field, 2)
-                   : launch<float, P2P_INDEXED_BITWISE, 4>(P, phi, field, 2);
+        return f64 ? launch<double, P2P_INDEXED_BITWISE, EVAL_K_F64>(P, phi, field, 2)
+                   : launch<float, P2P_INDEXED_BITWISE, EVAL_K_F32>(P, phi, field, 2);
     }
     return P2P_ERR_INVALID_ARGUMENT;
 }

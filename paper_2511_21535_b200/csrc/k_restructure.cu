@@ -37,9 +37,11 @@ __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const
                                                              const uint32_t *__restrict__ nbr_off,
                                                              const uint32_t *__restrict__ nbr_box,
                                                              const uint8_t *__restrict__ nbr_slot,
-                                                             const uint64_t *__restrict__ red_off, uint32_t B,
+                                                             const uint64_t *__restrict__ red_off,
+                                                             const DevCounters *__restrict__ ctr,
                                                              typename V4T<T>::type *__restrict__ red) {
     using V4 = typename V4T<T>::type;
+    const uint32_t B = ctr->B;  // device-side count: no host sync needed after an async p2p_plan_update
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nwarps) {
@@ -110,15 +112,15 @@ __global__ void k_restructure_helmholtz(const C2 *__restrict__ xs, const uint32_
 }  // namespace
 
 p2p_status restructure_gravity(p2p_plan *P) {
-    if (P->B == 0) return P2P_OK;
-    const unsigned blocks = div_up((uint64_t)P->B * 32, 256);
-    const unsigned grid = std::min<unsigned>(blocks, (unsigned)P->num_sms * 16);
+    if (P->sizes_known && P->B == 0) return P2P_OK;
+    const uint64_t nb = P->sizes_known ? (uint64_t)P->B : (uint64_t)P->bcap;
+    const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(div_up(nb * 32, 256), (unsigned)P->num_sms * 16));
     if (P->cfg.precision == P2P_FP64)
         P2P_LAUNCH(k_restructure_gravity<double>, grid, 256, 0, P->stream, P->geom, (const double4 *)P->rec, P->bkey,
-                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, (uint32_t)P->B, (double4 *)P->red);
+                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->ctr, (double4 *)P->red);
     else
         P2P_LAUNCH(k_restructure_gravity<float>, grid, 256, 0, P->stream, P->geom, (const float4 *)P->rec, P->bkey,
-                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, (uint32_t)P->B, (float4 *)P->red);
+                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->ctr, (float4 *)P->red);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }

@@ -184,20 +184,17 @@ __global__ void k_copy_u32(const uint32_t *__restrict__ a, uint32_t *__restrict_
 }
 }  // namespace
 
+size_t radix_status_words(uint64_t n, int passes) { return (size_t)passes * div_up(n, RS_TILE) * 256; }
+
 cudaError_t radix_sort_pairs(uint32_t *kin, uint32_t *vin, uint32_t *kalt, uint32_t *valt, uint32_t n, int passes,
-                             DevCounters *ctr, cudaStream_t st, uint32_t **kout, uint32_t **vout) {
+                             DevCounters *ctr, uint32_t *hist, uint32_t *status, cudaStream_t st, uint32_t **kout,
+                             uint32_t **vout) {
     *kout = kin;
     *vout = vin;
     if (n == 0 || passes == 0) return cudaSuccess;
     const uint32_t ntiles = div_up(n, RS_TILE);
-    uint32_t *hist = nullptr, *status = nullptr;
-    cudaError_t e;
-    size_t hist_bytes = (size_t)passes * 256 * sizeof(uint32_t);
-    size_t status_bytes = (size_t)passes * ntiles * 256 * sizeof(uint32_t);
-    if ((e = dalloc((void **)&hist, hist_bytes, st)) != cudaSuccess) return e;
-    if ((e = dalloc((void **)&status, status_bytes, st)) != cudaSuccess) return e;
-    cudaMemsetAsync(hist, 0, hist_bytes, st);
-    cudaMemsetAsync(status, 0, status_bytes, st);
+    cudaMemsetAsync(hist, 0, (size_t)passes * 256 * sizeof(uint32_t), st);
+    cudaMemsetAsync(status, 0, radix_status_words(n, passes) * sizeof(uint32_t), st);
     cudaMemsetAsync(ctr->sort_tile_ctr, 0, sizeof(ctr->sort_tile_ctr), st);
     unsigned hg = std::min<unsigned>(div_up(n, 256 * 8), 148 * 8);
     P2P_LAUNCH(k_radix_hist, hg, 256, 0, st, kin, n, passes, hist);
@@ -209,8 +206,6 @@ cudaError_t radix_sort_pairs(uint32_t *kin, uint32_t *vin, uint32_t *kalt, uint3
         std::swap(a_k, b_k);
         std::swap(a_v, b_v);
     }
-    dfree(hist, st);
-    dfree(status, st);
     *kout = a_k;
     *vout = a_v;
     return cudaGetLastError();

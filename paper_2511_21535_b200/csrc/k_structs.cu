@@ -16,7 +16,7 @@ namespace p2p {
 // eval work items: a box's targets are split into ceil(n_b / ITEM_TMAX) chunks, more if the chunk cost
 // n_t * R_b exceeds ITEM_COSTCAP interactions (bounds the tail of the dynamic work queue on clustered
 // inputs).  Chunks are balanced: chunk c = [n_b c / nch, n_b (c+1) / nch).
-// ITEM_TMAX = 32 lanes x K targets per lane (eval register blocking: K = 4 fp32, 2 fp64)
+// ITEM_TMAX (plan.hpp): at most 32 targets per item -> G <= 8 groups of K = 4 (fp32), >= 28 busy lanes
 constexpr uint64_t ITEM_COSTCAP = 1ull << 17;
 
 __device__ __forceinline__ uint32_t item_chunks(uint32_t nb_b, uint64_t nsrc, uint32_t tmax) {
@@ -149,66 +149,78 @@ __device__ __forceinline__ void decode3(uint32_t key, uint32_t c[3]) {
     c[2] = compact3(key >> 2);
 }
 
-__global__ void k_nbr_count(Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
-                            const uint32_t *__restrict__ box_of, DevCounters *ctr, uint32_t *__restrict__ nbr_cnt,
-                            uint64_t *__restrict__ red_cnt, uint32_t *__restrict__ item_cnt, uint32_t tmax) {
-    const uint32_t B = ctr->B;
-    uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long pairs = 0;
-    if (b < B) {
-        uint32_t c[3];
-        decode3(bkey[b], c);
-        uint32_t cnt = 0;
-        uint64_t nsrc = 0;
-        for (int slot = 0; slot < 27; ++slot) {
-            uint32_t nc[3];
-            if (!stencil_nbr(g, c, slot, nc)) continue;
-            uint32_t nk = spread3(nc[0]) | (spread3(nc[1]) << 1) | (spread3(nc[2]) << 2);
-            uint32_t k = box_of[nk];
-            if (k < B && bkey[k] == nk) {
-                ++cnt;
-                nsrc += bstart[k + 1] - bstart[k];
-            }
-        }
-        uint32_t nb_b = bstart[b + 1] - bstart[b];
-        nbr_cnt[b] = cnt;
-        red_cnt[b] = nsrc;
-        item_cnt[b] = item_chunks(nb_b, nsrc, tmax);
-        pairs = (unsigned long long)nb_b * nsrc;
-    }
-    // warp-aggregated pair count
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
-    if ((threadIdx.x & 31u) == 0 && pairs) atomicAdd(&ctr->I, pairs);
+// one warp per target box, lane = stencil slot (27 of 32 lanes): parallel box_of lookups, ballot-compacted
+// output in ascending slot order (C10)
+__device__ __forceinline__ bool lane_nbr(const Geom &g, const uint32_t c[3], unsigned lane, uint32_t B,
+                                         const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ box_of,
+                                         uint32_t &k) {
+    uint32_t nc[3];
+    if (lane >= 27 || !stencil_nbr(g, c, (int)lane, nc)) return false;
+    const uint32_t nk = spread3(nc[0]) | (spread3(nc[1]) << 1) | (spread3(nc[2]) << 2);
+    k = box_of[nk];
+    return k < B && bkey[k] == nk;
 }
 
-__global__ void k_nbr_fill(Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
-                           const uint32_t *__restrict__ box_of, const DevCounters *ctr,
-                           const uint32_t *__restrict__ nbr_off, const uint32_t *__restrict__ item_off,
-                           const uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ nbr_box,
-                           uint8_t *__restrict__ nbr_slot, Item *__restrict__ items) {
+__global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__restrict__ bkey,
+                                                   const uint32_t *__restrict__ bstart,
+                                                   const uint32_t *__restrict__ box_of, DevCounters *ctr,
+                                                   uint32_t *__restrict__ nbr_cnt, uint64_t *__restrict__ red_cnt,
+                                                   uint32_t *__restrict__ item_cnt, uint32_t tmax) {
     const uint32_t B = ctr->B;
-    uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B) return;
-    uint32_t c[3];
-    decode3(bkey[b], c);
-    uint32_t e = nbr_off[b];
-    for (int slot = 0; slot < 27; ++slot) {
-        uint32_t nc[3];
-        if (!stencil_nbr(g, c, slot, nc)) continue;
-        uint32_t nk = spread3(nc[0]) | (spread3(nc[1]) << 1) | (spread3(nc[2]) << 2);
-        uint32_t k = box_of[nk];
-        if (k < B && bkey[k] == nk) {
-            nbr_box[e] = k;
-            nbr_slot[e] = (uint8_t)slot;
-            ++e;
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long pairs = 0;
+    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nwarps) {
+        uint32_t c[3];
+        decode3(bkey[b], c);
+        uint32_t k = 0;
+        const bool ok = lane_nbr(g, c, lane, B, bkey, box_of, k);
+        uint32_t nk = ok ? bstart[k + 1] - bstart[k] : 0u;
+        const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, ok));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nk += __shfl_xor_sync(0xffffffffu, nk, o);
+        if (lane == 0) {
+            const uint32_t nb_b = bstart[b + 1] - bstart[b];
+            nbr_cnt[b] = cnt;
+            red_cnt[b] = nk;
+            item_cnt[b] = item_chunks(nb_b, nk, tmax);
+            pairs += (unsigned long long)nb_b * nk;
         }
     }
-    const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
-    const uint32_t nch = item_cnt[b], it = item_off[b];
-    for (uint32_t ci = 0; ci < nch; ++ci) {
-        uint32_t a = (uint32_t)(((uint64_t)nb_b * ci) / nch), z = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
-        items[it + ci] = Item{b, s0 + a, z - a};
+    if (lane == 0 && pairs) atomicAdd(&ctr->I, pairs);
+}
+
+__global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__restrict__ bkey,
+                                                  const uint32_t *__restrict__ bstart,
+                                                  const uint32_t *__restrict__ box_of, const DevCounters *ctr,
+                                                  const uint32_t *__restrict__ nbr_off,
+                                                  const uint32_t *__restrict__ item_off,
+                                                  const uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ nbr_box,
+                                                  uint8_t *__restrict__ nbr_slot, Item *__restrict__ items,
+                                                  uint32_t K) {
+    const uint32_t B = ctr->B;
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nwarps) {
+        uint32_t c[3];
+        decode3(bkey[b], c);
+        uint32_t k = 0;
+        const bool ok = lane_nbr(g, c, lane, B, bkey, box_of, k);
+        const uint32_t m = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            const uint32_t e = nbr_off[b] + __popc(m & ((1u << lane) - 1u));
+            nbr_box[e] = k;
+            nbr_slot[e] = (uint8_t)lane;
+        }
+        const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
+        const uint32_t nch = item_cnt[b], it = item_off[b];
+        for (uint32_t ci = lane; ci < nch; ci += 32) {
+            const uint32_t a0 = (uint32_t)(((uint64_t)nb_b * ci) / nch);
+            const uint32_t z0 = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
+            // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
+            const uint32_t nt = z0 - a0, G = (nt + K - 1) / K, S = 32u / G;
+            items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16)};
+        }
     }
 }
 
@@ -275,28 +287,82 @@ static unsigned grid_for(uint64_t n, int threads, int num_sms) {
 }
 
 // ------------------------------------------------------------------------------------------------
+static unsigned warp_grid(uint64_t nwork, int num_sms) {
+    // one warp per work unit, 8 warps per block, at most 16 resident blocks per SM (grid-stride beyond)
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(div_up(nwork, 8), (uint64_t)num_sms * 16));
+}
+
+void free_capacity(p2p_plan *P) {
+    cudaStream_t st = P->stream;
+    void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
+                    P->s_nbr_cnt, P->s_item_cnt, P->s_item_off, P->s_red_cnt, P->rec, P->bkey, P->bstart,
+                    P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items};
+    for (void *b : bufs) dfree(b, st);
+    P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
+    P->s_partials = nullptr;
+    P->s_nbr_cnt = P->s_item_cnt = P->s_item_off = nullptr;
+    P->s_red_cnt = nullptr;
+    P->rec = nullptr;
+    P->bkey = P->bstart = P->nbr_off = P->nbr_box = P->box_of = nullptr;
+    P->nbr_slot = nullptr;
+    P->red_off = nullptr;
+    P->items = nullptr;
+    P->skey = P->perm = nullptr;
+    P->cap = P->bcap = 0;
+}
+
+// every buffer whose size depends on N (or on the box capacity min(N, key space)), allocated once
+p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
+    cudaStream_t st = P->stream;
+    const bool grav = P->cfg.kernel == P2P_GRAVITY;
+    const bool f64 = P->cfg.precision == P2P_FP64;
+    const uint64_t n = (uint64_t)std::max<int64_t>(cap, 1);
+    const uint64_t keyspace = grav ? (1ull << P->key_bits) : (1ull << (2 * P->nb));
+    const uint64_t bcap = std::min<uint64_t>(n, keyspace);
+    const int nslot = grav ? 27 : 9;
+    P->cap = cap;
+    P->bcap = (int64_t)bcap;
+    P2P_CUDA_TRY(dalloc((void **)&P->s_key, 4 * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->s_idx, 4 * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->s_kalt, 4 * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->s_valt, 4 * n, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->s_hist, 4 * 4 * 256, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->s_status, 4 * std::max<size_t>(1, radix_status_words(n, std::max(1, P->passes))), st));
+    P2P_CUDA_TRY(dalloc(&P->s_partials, scan_partials_bytes(std::max(n, bcap)), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->bkey, 4 * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->bstart, 4 * (bcap + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->box_of, 4 * keyspace, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_off, 4 * (bcap + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_box, 4 * nslot * bcap, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, (size_t)nslot * bcap, st));
+    if (grav) {
+        P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_nbr_cnt, 4 * bcap, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_item_cnt, 4 * bcap, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_item_off, 4 * (bcap + 1), st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_red_cnt, 8 * bcap, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->red_off, 8 * (bcap + 1), st));
+        P2P_CUDA_TRY(dalloc((void **)&P->items, sizeof(Item) * n, st));
+    } else {
+        P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double2) : sizeof(float2)) * n, st));
+    }
+    return P2P_OK;
+}
+
 p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q) {
     cudaStream_t st = P->stream;
     const uint32_t n = (uint32_t)P->n;
     const bool f64 = P->cfg.precision == P2P_FP64;
-    uint32_t *key = nullptr, *idx = nullptr, *kalt = nullptr, *valt = nullptr;
-    P2P_CUDA_TRY(dalloc((void **)&key, sizeof(uint32_t) * n, st));
-    P2P_CUDA_TRY(dalloc((void **)&idx, sizeof(uint32_t) * n, st));
-    P2P_CUDA_TRY(dalloc((void **)&kalt, sizeof(uint32_t) * n, st));
-    P2P_CUDA_TRY(dalloc((void **)&valt, sizeof(uint32_t) * n, st));
     const unsigned gb = grid_for(n, 256, P->num_sms);
-    if (f64) P2P_LAUNCH(k_bin_gravity<double>, gb, 256, 0, st, (const double *)pos, n, P->geom, key, idx, P->ctr);
-    else P2P_LAUNCH(k_bin_gravity<float>, gb, 256, 0, st, (const float *)pos, n, P->geom, key, idx, P->ctr);
-    uint32_t *sk, *sv;
-    P2P_CUDA_TRY(radix_sort_pairs(key, idx, kalt, valt, n, P->passes, P->ctr, st, &sk, &sv));
-    // keep sorted keys / perm in plan-owned buffers, free the others
-    P->skey = sk;
-    P->perm = sv;
-    dfree(sk == key ? kalt : key, st);
-    dfree(sv == idx ? valt : idx, st);
+    // a1
+    if (f64)
+        P2P_LAUNCH(k_bin_gravity<double>, gb, 256, 0, st, (const double *)pos, n, P->geom, P->s_key, P->s_idx, P->ctr);
+    else
+        P2P_LAUNCH(k_bin_gravity<float>, gb, 256, 0, st, (const float *)pos, n, P->geom, P->s_key, P->s_idx, P->ctr);
+    // a2
+    P2P_CUDA_TRY(radix_sort_pairs(P->s_key, P->s_idx, P->s_kalt, P->s_valt, n, P->passes, P->ctr, P->s_hist,
+                                  P->s_status, st, &P->skey, &P->perm));
     // a3
-    const size_t rec_bytes = (f64 ? sizeof(double4) : sizeof(float4)) * (size_t)n;
-    P2P_CUDA_TRY(dalloc(&P->rec, rec_bytes, st));
     if (f64)
         P2P_LAUNCH((k_permute_gravity<double, double4>), gb, 256, 0, st, (const double *)pos, (const double *)q,
                    P->perm, n, (double4 *)P->rec);
@@ -304,43 +370,25 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q) {
         P2P_LAUNCH((k_permute_gravity<float, float4>), gb, 256, 0, st, (const float *)pos, (const float *)q, P->perm,
                    n, (float4 *)P->rec);
     // a4
-    const uint64_t keyspace = 1ull << P->key_bits;
-    const uint64_t bcap = std::min<uint64_t>(n, keyspace);
-    P2P_CUDA_TRY(dalloc((void **)&P->bkey, sizeof(uint32_t) * bcap, st));
-    P2P_CUDA_TRY(dalloc((void **)&P->bstart, sizeof(uint32_t) * (bcap + 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&P->box_of, sizeof(uint32_t) * keyspace, st));
     P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, 1u}, HeadPut{P->skey, 1u, P->bkey, P->bstart, P->box_of, n},
-                                       nullptr, n, &P->ctr->B, st));
+                                       nullptr, n, &P->ctr->B, P->s_partials, st));
     // a5
-    uint32_t *nbr_cnt = nullptr, *item_cnt = nullptr;
-    uint64_t *red_cnt = nullptr;
-    P2P_CUDA_TRY(dalloc((void **)&nbr_cnt, sizeof(uint32_t) * bcap, st));
-    P2P_CUDA_TRY(dalloc((void **)&item_cnt, sizeof(uint32_t) * bcap, st));
-    P2P_CUDA_TRY(dalloc((void **)&red_cnt, sizeof(uint64_t) * bcap, st));
-    P2P_CUDA_TRY(dalloc((void **)&P->nbr_off, sizeof(uint32_t) * (bcap + 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&P->red_off, sizeof(uint64_t) * (bcap + 1), st));
-    uint32_t *item_off = nullptr;
-    P2P_CUDA_TRY(dalloc((void **)&item_off, sizeof(uint32_t) * (bcap + 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&P->nbr_box, sizeof(uint32_t) * 27 * bcap, st));
-    P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, sizeof(uint8_t) * 27 * bcap, st));
-    P2P_CUDA_TRY(dalloc((void **)&P->items, sizeof(Item) * n, st));
-    const unsigned gbx = div_up(bcap, 256);
-    const uint32_t tmax = f64 ? 64u : 128u;  // 32 lanes x K (K = 2 fp64, 4 fp32; k_eval_gravity.cu)
-    P2P_LAUNCH(k_nbr_count, gbx, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, nbr_cnt, red_cnt,
-               item_cnt, tmax);
-    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{nbr_cnt}, OffPut<uint32_t>{P->nbr_off, &P->ctr->B},
-                                       &P->ctr->B, bcap, &P->ctr->n_nbr, st));
-    P2P_CUDA_TRY(device_scan<unsigned long long>(ArrGet<unsigned long long>{(const unsigned long long *)red_cnt},
-                                                 OffPut<unsigned long long>{(unsigned long long *)P->red_off, &P->ctr->B},
-                                                 &P->ctr->B, bcap, &P->ctr->R, st));
-    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{item_cnt}, OffPut<uint32_t>{item_off, &P->ctr->B}, &P->ctr->B,
-                                       bcap, &P->ctr->n_items, st));
-    P2P_LAUNCH(k_nbr_fill, gbx, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, P->nbr_off, item_off,
-               item_cnt, P->nbr_box, P->nbr_slot, P->items);
-    dfree(nbr_cnt, st);
-    dfree(item_cnt, st);
-    dfree(red_cnt, st);
-    dfree(item_off, st);
+    const uint64_t bcap = (uint64_t)P->bcap;
+    const unsigned gw = warp_grid(bcap, P->num_sms);
+    const uint32_t tmax = ITEM_TMAX;
+    P2P_LAUNCH(k_nbr_count, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, P->s_nbr_cnt,
+               P->s_red_cnt, P->s_item_cnt, tmax);
+    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_nbr_cnt}, OffPut<uint32_t>{P->nbr_off, &P->ctr->B},
+                                       &P->ctr->B, bcap, &P->ctr->n_nbr, P->s_partials, st));
+    P2P_CUDA_TRY(device_scan<unsigned long long>(
+        ArrGet<unsigned long long>{(const unsigned long long *)P->s_red_cnt},
+        OffPut<unsigned long long>{(unsigned long long *)P->red_off, &P->ctr->B}, &P->ctr->B, bcap, &P->ctr->R,
+        P->s_partials, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_item_cnt}, OffPut<uint32_t>{P->s_item_off, &P->ctr->B},
+                                       &P->ctr->B, bcap, &P->ctr->n_items, P->s_partials, st));
+    P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, P->nbr_off,
+               P->s_item_off, P->s_item_cnt, P->nbr_box, P->nbr_slot, P->items,
+               (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }
@@ -372,45 +420,26 @@ p2p_status build_helmholtz_structs(p2p_plan *P, const void *pos, const void *q) 
     int stt = 0;
     while (stt * stt < (int)t) ++stt;
     const double delta = P->cfg.box_size / (double)stt;
-    uint32_t *key = nullptr, *idx = nullptr, *kalt = nullptr, *valt = nullptr;
-    P2P_CUDA_TRY(dalloc((void **)&key, sizeof(uint32_t) * n, st));
-    P2P_CUDA_TRY(dalloc((void **)&idx, sizeof(uint32_t) * n, st));
-    P2P_CUDA_TRY(dalloc((void **)&kalt, sizeof(uint32_t) * n, st));
-    P2P_CUDA_TRY(dalloc((void **)&valt, sizeof(uint32_t) * n, st));
     const unsigned gb = grid_for(n, 256, P->num_sms);
     if (f64)
-        P2P_LAUNCH(k_bin_helmholtz<double>, gb, 256, 0, st, (const double *)pos, n, P->geom, stt, delta, t, key, idx,
-                   P->ctr);
+        P2P_LAUNCH(k_bin_helmholtz<double>, gb, 256, 0, st, (const double *)pos, n, P->geom, stt, delta, t, P->s_key,
+                   P->s_idx, P->ctr);
     else
-        P2P_LAUNCH(k_bin_helmholtz<float>, gb, 256, 0, st, (const float *)pos, n, P->geom, stt, delta, t, key, idx,
-                   P->ctr);
-    uint32_t *sk, *sv;
-    P2P_CUDA_TRY(radix_sort_pairs(key, idx, kalt, valt, n, P->passes, P->ctr, st, &sk, &sv));
-    P->skey = sk;
-    P->perm = sv;
-    dfree(sk == key ? kalt : key, st);
-    dfree(sv == idx ? valt : idx, st);
+        P2P_LAUNCH(k_bin_helmholtz<float>, gb, 256, 0, st, (const float *)pos, n, P->geom, stt, delta, t, P->s_key,
+                   P->s_idx, P->ctr);
+    P2P_CUDA_TRY(radix_sort_pairs(P->s_key, P->s_idx, P->s_kalt, P->s_valt, n, P->passes, P->ctr, P->s_hist,
+                                  P->s_status, st, &P->skey, &P->perm));
     P2P_LAUNCH(k_helm_check, gb, 256, 0, st, P->skey, n, P->ctr);
     // a3: complex unknowns in sorted order
-    const size_t cbytes = (f64 ? sizeof(double2) : sizeof(float2)) * (size_t)n;
-    P2P_CUDA_TRY(dalloc(&P->rec, cbytes, st));
     if (f64)
         P2P_LAUNCH(k_permute_complex<double2>, gb, 256, 0, st, (const double2 *)q, P->perm, n, (double2 *)P->rec);
     else
         P2P_LAUNCH(k_permute_complex<float2>, gb, 256, 0, st, (const float2 *)q, P->perm, n, (float2 *)P->rec);
     // a4: boxes = runs of key / t
-    const uint64_t keyspace = 1ull << (2 * P->nb);
-    const uint64_t bcap = std::min<uint64_t>(n, keyspace);
-    P2P_CUDA_TRY(dalloc((void **)&P->bkey, sizeof(uint32_t) * bcap, st));
-    P2P_CUDA_TRY(dalloc((void **)&P->bstart, sizeof(uint32_t) * (bcap + 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&P->box_of, sizeof(uint32_t) * keyspace, st));
     P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, t}, HeadPut{P->skey, t, P->bkey, P->bstart, P->box_of, n},
-                                       nullptr, n, &P->ctr->B, st));
+                                       nullptr, n, &P->ctr->B, P->s_partials, st));
     // a5: 9 slots per box
-    P2P_CUDA_TRY(dalloc((void **)&P->nbr_off, sizeof(uint32_t) * (bcap + 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&P->nbr_box, sizeof(uint32_t) * 9 * bcap, st));
-    P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, sizeof(uint8_t) * 9 * bcap, st));
-    P2P_LAUNCH(k_helm_nbr, div_up(bcap, 256), 256, 0, st, P->geom, t, P->bkey, P->bstart, P->box_of, P->ctr,
+    P2P_LAUNCH(k_helm_nbr, div_up(P->bcap, 256), 256, 0, st, P->geom, t, P->bkey, P->bstart, P->box_of, P->ctr,
                P->nbr_off, P->nbr_box, P->nbr_slot);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;

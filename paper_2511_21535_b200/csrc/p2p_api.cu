@@ -95,9 +95,38 @@ static p2p_status mark(p2p_plan *P, p2p_status s) {
 
 static void free_plan_buffers(p2p_plan *P) {
     cudaStream_t st = P->stream;
-    void *bufs[] = {P->rec, P->skey, P->perm, P->bkey, P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot,
-                    P->red_off, P->box_of, P->items, P->red, P->table, P->ctr};
+    free_capacity(P);
+    void *bufs[] = {P->red, P->table, P->ctr};
     for (void *b : bufs) dfree(b, st);
+    P->red = P->table = nullptr;
+    P->ctr = nullptr;
+}
+
+// host copies of the device-side sizes after an asynchronous p2p_plan_update (synchronises the stream)
+static p2p_status resolve_sizes(p2p_plan *P) {
+    if (P->sizes_known) return P2P_OK;
+    DevCounters h;
+    cudaError_t e = cudaMemcpyAsync(&h, P->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, P->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+    if (e != cudaSuccess) {
+        P->sticky = P2P_ERR_CUDA;
+        return fail(P2P_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+    }
+    if (h.err_index != ~0ull) {
+        char buf[200];
+        snprintf(buf, sizeof buf,
+                 "position of input particle %llu is outside the domain [lo, lo + nbox*h) (C6); the plan holds "
+                 "no valid structures until the next successful p2p_plan_update",
+                 (unsigned long long)h.err_index);
+        return fail(P2P_ERR_OUT_OF_DOMAIN, buf);
+    }
+    P->B = h.B;
+    P->n_nbr = h.n_nbr;
+    P->R = (int64_t)h.R;
+    P->I = (int64_t)h.I;
+    P->n_items = h.n_items;
+    P->sizes_known = true;
+    return P2P_OK;
 }
 
 }  // namespace p2p
@@ -218,10 +247,12 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
     cudaMemsetAsync(&P->ctr->err_index, 0xff, sizeof(unsigned long long), st);
     if (n_local == 0) {
         cudaStreamSynchronize(st);
+        P->sizes_known = true;
         *out = P;
         return P2P_OK;
     }
     tr.at("validated+counters");
+    if (alloc_capacity(P, n_local) != P2P_OK) return bail(fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate plan buffers"));
     p2p_status s = grav ? build_gravity_structs(P, positions, charges) : build_helmholtz_structs(P, positions, charges);
     if (s != P2P_OK) return bail(s);
     tr.at("structs enqueued");
@@ -247,6 +278,7 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
         const size_t rec_sz = cfg->precision == P2P_FP64 ? sizeof(double4) : sizeof(float4);
         if (dalloc(&P->red, rec_sz * (size_t)std::max<int64_t>(P->R, 1), st) != cudaSuccess)
             return bail(fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate the redundant buffer"));
+        P->red_cap = std::max<int64_t>(P->R, 1);
     } else {
         const int64_t t = cfg->points_per_box;
         P->n_nbr = 9 * P->B;
@@ -259,8 +291,52 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
         if (s != P2P_OK) return bail(s);
     }
     tr.at("red allocated");
+    P->sizes_known = true;
     *out = P;
     return P2P_OK;
+}
+
+p2p_status p2p_plan_update(p2p_plan *P, int64_t n_local, const void *positions, const void *charges) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (P->cfg.kernel != P2P_GRAVITY)
+        return fail(P2P_ERR_UNSUPPORTED, "p2p_plan_update is for gravity plans (DBIM geometry is fixed: use set_charges)");
+    if (n_local < 0) return fail(P2P_ERR_INVALID_ARGUMENT, "n_local < 0");
+    if (n_local >= (int64_t)1 << 31) return fail(P2P_ERR_UNSUPPORTED, "n_local >= 2^31 (u32 indices)");
+    if (n_local > 0 && (!is_device_ptr(positions) || !is_device_ptr(charges)))
+        return fail(P2P_ERR_INVALID_ARGUMENT, "positions / charges must be device pointers");
+    cudaStream_t st = P->stream;
+    if (n_local > P->cap) {  // grow (stream-ordered; steady-state time steps never get here)
+        free_capacity(P);
+        if (alloc_capacity(P, n_local) != P2P_OK) {
+            P->sticky = P2P_ERR_OUT_OF_MEMORY;
+            return fail(P2P_ERR_OUT_OF_MEMORY, "cannot grow plan buffers");
+        }
+    }
+    // worst case R <= 27 N (each record is one of <= 27 images of a particle) -> no host sync needed
+    const int64_t red_need = std::max<int64_t>(27 * n_local, 1);
+    if (P->red_cap < red_need) {
+        dfree(P->red, st);
+        const size_t rec_sz = P->cfg.precision == P2P_FP64 ? sizeof(double4) : sizeof(float4);
+        if (dalloc(&P->red, rec_sz * (size_t)red_need, st) != cudaSuccess) {
+            P->red = nullptr;
+            P->red_cap = 0;
+            P->sticky = P2P_ERR_OUT_OF_MEMORY;
+            return fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate the redundant buffer");
+        }
+        P->red_cap = red_need;
+    }
+    P->n = n_local;
+    P->sizes_known = false;
+    P->red_valid = false;
+    cudaMemsetAsync(P->ctr, 0, sizeof(DevCounters), st);
+    cudaMemsetAsync(&P->ctr->err_index, 0xff, sizeof(unsigned long long), st);
+    if (n_local == 0) {
+        P->sizes_known = true;
+        P->B = P->n_nbr = P->R = P->I = P->n_items = 0;
+        return P2P_OK;
+    }
+    return mark(P, build_gravity_structs(P, positions, charges));
 }
 
 p2p_status p2p_restructure(p2p_plan *P) {
@@ -311,9 +387,12 @@ void p2p_destroy(p2p_plan *P) {
     delete P;
 }
 
-p2p_status p2p_get_info(const p2p_plan *P, p2p_info *out) {
-    if (!P || !out) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+p2p_status p2p_get_info(const p2p_plan *Pc, p2p_info *out) {
+    if (!Pc || !out) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+    p2p_plan *P = const_cast<p2p_plan *>(Pc);  // resolves the lazily synchronised host copies of the sizes
     if (P->sticky != P2P_OK) return fail(P->sticky, "plan is unusable after an earlier error");
+    p2p_status rs = resolve_sizes(P);
+    if (rs != P2P_OK) return rs;
     cudaError_t e = cudaStreamSynchronize(P->stream);
     if (e != cudaSuccess) return fail(P2P_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
     out->n_local = P->n;
@@ -327,9 +406,12 @@ p2p_status p2p_get_info(const p2p_plan *P, p2p_info *out) {
     return P2P_OK;
 }
 
-p2p_status p2p_copy_out(const p2p_plan *P, p2p_array which, void *host_dst, size_t bytes) {
-    if (!P || (!host_dst && bytes)) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+p2p_status p2p_copy_out(const p2p_plan *Pc, p2p_array which, void *host_dst, size_t bytes) {
+    if (!Pc || (!host_dst && bytes)) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+    p2p_plan *P = const_cast<p2p_plan *>(Pc);
     if (P->sticky != P2P_OK) return fail(P->sticky, "plan is unusable after an earlier error");
+    p2p_status rs = resolve_sizes(P);
+    if (rs != P2P_OK) return rs;
     const bool grav = P->cfg.kernel == P2P_GRAVITY;
     const bool f64 = P->cfg.precision == P2P_FP64;
     const void *src = nullptr;

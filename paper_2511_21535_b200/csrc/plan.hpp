@@ -23,11 +23,15 @@ struct DevCounters {
 };
 
 // eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
+// meta = n_t | S << 8 | G << 16: the warp lane layout (G groups of K targets x S source splits, G*S <= 32)
 struct Item {
     uint32_t box;
     uint32_t t0;
-    uint32_t nt;
+    uint32_t meta;
 };
+constexpr int EVAL_K_F32 = 4;    // targets per lane in k_eval_gravity (fp32: two packed FP32x2 pairs)
+constexpr int EVAL_K_F64 = 2;
+constexpr uint32_t ITEM_TMAX = 32;  // max targets per work item (lane utilisation)
 
 // gravity geometry passed by value to kernels
 struct Geom {
@@ -63,6 +67,14 @@ struct p2p_plan {
     void *red = nullptr;         // gravity red[R] records; helmholtz Xg[B][9][t]
     void *table = nullptr;       // helmholtz pattern table P[t][9t] complex
     p2p::DevCounters *ctr = nullptr;
+    // capacity-sized scratch, allocated once per plan (p2p_plan_update reuses it: no allocation, no sync)
+    int64_t cap = 0, bcap = 0, red_cap = 0;
+    uint32_t *s_key = nullptr, *s_idx = nullptr, *s_kalt = nullptr, *s_valt = nullptr;
+    uint32_t *s_hist = nullptr, *s_status = nullptr;
+    void *s_partials = nullptr;
+    uint32_t *s_nbr_cnt = nullptr, *s_item_cnt = nullptr, *s_item_off = nullptr;
+    uint64_t *s_red_cnt = nullptr;
+    bool sizes_known = false;  // host copies of B, n_nbr, R, I, n_items valid (false after an async update)
     bool red_valid = false;
     p2p_status sticky = P2P_OK;
     int eval_blocks[3] = {0, 0, 0};
@@ -72,10 +84,15 @@ namespace p2p {
 
 // k_sort.cu: stable LSD radix sort of (key, value) pairs, `passes` 8-bit digits.  On return the sorted
 // pairs are in (*kout, *vout) which point to either the in or the alt buffers.
+// hist: [4][256] u32, status: [passes][ceil(n/4096)][256] u32 scratch (plan-owned)
 cudaError_t radix_sort_pairs(uint32_t *kin, uint32_t *vin, uint32_t *kalt, uint32_t *valt, uint32_t n, int passes,
-                             DevCounters *ctr, cudaStream_t st, uint32_t **kout, uint32_t **vout);
+                             DevCounters *ctr, uint32_t *hist, uint32_t *status, cudaStream_t st, uint32_t **kout,
+                             uint32_t **vout);
+size_t radix_status_words(uint64_t n, int passes);
 
 // k_structs.cu
+p2p_status alloc_capacity(p2p_plan *P, int64_t cap);   // all N-/B-sized buffers + scratch
+void free_capacity(p2p_plan *P);
 p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q);
 p2p_status build_helmholtz_structs(p2p_plan *P, const void *pos, const void *q);
 p2p_status set_charges_gravity(p2p_plan *P, const void *q);

@@ -101,20 +101,21 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_down(Get get, Put put, cons
 }
 
 // run the three phases; `ncap` = capacity (launch size), `nptr` = optional device count
+// scratch: >= scan_partials_bytes(ncap) bytes (plan-owned, reused by consecutive scans on one stream)
+static inline size_t scan_partials_bytes(uint64_t ncap) { return 8 * (size_t)div_up(ncap, SC_TILE) + 8; }
+
 template <typename T, typename Get, typename Put>
-cudaError_t device_scan(Get get, Put put, const uint32_t *nptr, uint64_t ncap, T *total_out, cudaStream_t st) {
+cudaError_t device_scan(Get get, Put put, const uint32_t *nptr, uint64_t ncap, T *total_out, void *scratch,
+                        cudaStream_t st) {
     if (ncap == 0) {
         if (total_out) cudaMemsetAsync(total_out, 0, sizeof(T), st);
         return cudaGetLastError();
     }
     const unsigned nblk = div_up(ncap, SC_TILE);
-    T *partials = nullptr;
-    cudaError_t e = dalloc((void **)&partials, sizeof(T) * nblk, st);
-    if (e != cudaSuccess) return e;
+    T *partials = (T *)scratch;
     P2P_LAUNCH((k_scan_reduce<T, Get>), nblk, SC_THREADS, 0, st, get, nptr, ncap, partials);
     P2P_LAUNCH((k_scan_partials<T>), 1, SC_THREADS, 0, st, partials, nblk, total_out);
     P2P_LAUNCH((k_scan_down<T, Get, Put>), nblk, SC_THREADS, 0, st, get, put, nptr, ncap, partials);
-    dfree(partials, st);
     return cudaGetLastError();
 }
 

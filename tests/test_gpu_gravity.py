@@ -176,3 +176,35 @@ def test_nearfield_host_api(P):
     assert not phi.is_cuda
     rphi, rf = oracle.GravityPlan(inp).eval_indexed()
     assert oracle.rel_l2(phi.numpy(), rphi) < 1e-5 and oracle.rel_l2(f.numpy(), rf) < 1e-5
+
+
+def test_plan_update_time_steps(P):
+    """p2p_plan_update: asynchronous rebuild for moved particles (PhotoNs time step, P:L197); N may shrink or grow;
+    structures and values equal a fresh oracle build of the new input"""
+    a = G.plummer(5000, 6, seed=1)
+    seq = [G.plummer(4000, 6, seed=2), G.uniform_per_box(6, 8, seed=3), G.plummer(9000, 6, seed=4)]
+    with gpu_plan(P, a) as plan:
+        for inp in seq:
+            plan.update(torch.from_numpy(inp.pos).cuda(), torch.from_numpy(inp.mass).cuda())
+            plan.restructure()
+            phi, f = plan.eval(P.P2P_REDUNDANT)
+            gp = oracle.GravityPlan(inp)
+            check_structs(P, plan, gp)
+            assert plan.copy_out(P.P2P_ARR_RED).tobytes() == gp.red.tobytes()
+            rphi, rf = gp.eval_indexed()
+            assert oracle.rel_l2(phi.cpu().numpy(), rphi) < 1e-5 and oracle.rel_l2(f.cpu().numpy(), rf) < 1e-5
+            phi2, f2 = plan.eval(P.P2P_INDEXED)
+            assert oracle.rel_l2(phi2.cpu().numpy(), rphi) < 1e-5 and oracle.rel_l2(f2.cpu().numpy(), rf) < 1e-5
+
+
+def test_plan_update_reports_out_of_domain(P):
+    inp = G.uniform_per_box(4, 4, seed=0)
+    bad = inp.pos.copy()
+    bad[5, 2] = -0.01
+    with gpu_plan(P, inp) as plan:
+        plan.update(torch.from_numpy(bad).cuda(), torch.from_numpy(inp.mass).cuda())   # asynchronous: no error yet
+        with pytest.raises(P.P2PError) as e:
+            plan.refresh_info()
+        assert e.value.status == P.P2P_ERR_OUT_OF_DOMAIN and "5" in str(e.value)
+        plan.update(torch.from_numpy(inp.pos).cuda(), torch.from_numpy(inp.mass).cuda())
+        assert plan.refresh_info().n_boxes == 64
