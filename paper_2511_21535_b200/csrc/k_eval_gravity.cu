@@ -89,6 +89,9 @@ struct EvalArgs {
     const Item *items;
     const uint32_t *n_items;   // device-side count (valid without a host sync after p2p_plan_update)
     unsigned int *item_head;
+    const uint32_t *n_small;   // small-box targets (thread-per-target path)
+    unsigned int *small_head;
+    const uint32_t *small_tgt, *small_box;
     T *phi;
     T *field;
 };
@@ -227,6 +230,131 @@ struct Tgt<double, K> {
     static __device__ __forceinline__ double eps_pack(double e2) { return e2; }
 };
 
+// ---- thread-per-target path for the targets of small boxes (n_b <= SMALL_NT) ----------------------------
+// One lane = one target; the lane walks its box's source sequence in run order (REDUNDANT: the contiguous
+// red[] run through the read-only L1 path; INDEXED: the CSR segments of rec[]), so there is no per-item
+// staging, no source split and no reduction -- the per-item overhead that dominates tiny boxes disappears.
+// Lanes of one warp are consecutive targets in Morton order, so lanes of the same box read the same
+// addresses (one L1 wavefront).  Same formula and rounding sequence as Tgt::interact.
+__device__ __forceinline__ float4 ldro(const float4 *p) { return __ldg(p); }
+__device__ __forceinline__ double4 ldro(const double4 *p) {
+    const double2 a = __ldg(reinterpret_cast<const double2 *>(p)), b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+template <typename T>
+__device__ __forceinline__ void interact1(const typename V4T<T>::type &s, T tx, T ty, T tz, T e2, T &ap, T &ax,
+                                          T &ay, T &az) {
+    if constexpr (std::is_same<T, float>::value) {
+        const float dx = __fsub_rn(s.x, tx), dy = __fsub_rn(s.y, ty), dz = __fsub_rn(s.z, tz);
+        float r2 = __fmaf_rn(dx, dx, e2);
+        r2 = __fmaf_rn(dy, dy, r2);
+        r2 = __fmaf_rn(dz, dz, r2);
+        const float ri = rsqrt_ftz(r2);
+        const float mri = __fmul_rn(s.w, ri);
+        ap = __fadd_rn(ap, mri);
+        const float m3 = __fmul_rn(__fmul_rn(mri, ri), ri);
+        ax = __fmaf_rn(m3, dx, ax);
+        ay = __fmaf_rn(m3, dy, ay);
+        az = __fmaf_rn(m3, dz, az);
+    } else {
+        const double dx = __dsub_rn(s.x, tx), dy = __dsub_rn(s.y, ty), dz = __dsub_rn(s.z, tz);
+        double r2 = __fma_rn(dx, dx, e2);
+        r2 = __fma_rn(dy, dy, r2);
+        r2 = __fma_rn(dz, dz, r2);
+        const double ri = 1.0 / sqrt(r2);
+        const double mri = __dmul_rn(s.w, ri);
+        ap = __dadd_rn(ap, mri);
+        const double m3 = __dmul_rn(__dmul_rn(mri, ri), ri);
+        ax = __fma_rn(m3, dx, ax);
+        ay = __fma_rn(m3, dy, ay);
+        az = __fma_rn(m3, dz, az);
+    }
+}
+
+template <typename T, int LAYOUT>
+__device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane) {
+    using V4 = typename V4T<T>::type;
+    const uint32_t n_small = *a.n_small;
+    const T eps2 = (T)a.g.eps2;
+    while (true) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(a.small_head, 32u);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= n_small) break;
+        const uint32_t i = base + lane;
+        if (i < n_small) {
+        const uint32_t p = a.small_tgt[i], b = a.small_box[i];
+        const uint32_t key = a.bkey[b];
+        const uint32_t cc[3] = {compact3(key), compact3(key >> 1), compact3(key >> 2)};
+        double org[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+            org[d] = (LAYOUT == P2P_INDEXED) ? frame_shift(a.g, cc, d) : __fma_rn((double)cc[d], a.g.h, a.g.lo[d]);
+        const V4 t = a.rec[p];
+        T tx, ty, tz;
+        if (LAYOUT == P2P_INDEXED) {
+            tx = t.x + (T)org[0];
+            ty = t.y + (T)org[1];
+            tz = t.z + (T)org[2];
+        } else {
+            tx = (T)__dsub_rn((double)t.x, org[0]);
+            ty = (T)__dsub_rn((double)t.y, org[1]);
+            tz = (T)__dsub_rn((double)t.z, org[2]);
+        }
+        T ap = 0, ax = 0, ay = 0, az = 0;
+        if (LAYOUT == P2P_REDUNDANT) {
+            const uint64_t r0 = a.red_off[b], r1 = a.red_off[b + 1];
+            const V4 *run = a.red + r0;
+            const uint32_t R = (uint32_t)(r1 - r0);
+            uint32_t j = 0;
+#pragma unroll 1
+            for (; j + 2 <= R; j += 2) {
+                const V4 s0 = ldro(run + j), s1 = ldro(run + j + 1);
+                interact1<T>(s0, tx, ty, tz, eps2, ap, ax, ay, az);
+                interact1<T>(s1, tx, ty, tz, eps2, ap, ax, ay, az);
+            }
+            if (j < R) interact1<T>(ldro(run + j), tx, ty, tz, eps2, ap, ax, ay, az);
+        } else {
+            const uint32_t e0 = a.nbr_off[b], e1 = a.nbr_off[b + 1];
+            for (uint32_t e = e0; e < e1; ++e) {
+                const uint32_t k = a.nbr_box[e];
+                const int slot = a.nbr_slot[e];
+                const double S0 = slot_shift(a.g, cc, slot, 0), S1 = slot_shift(a.g, cc, slot, 1),
+                             S2 = slot_shift(a.g, cc, slot, 2);
+                const uint32_t q0 = a.bstart[k], q1 = a.bstart[k + 1];
+                if (LAYOUT == P2P_INDEXED) {
+                    const T h0 = (T)(S0 + org[0]), h1 = (T)(S1 + org[1]), h2 = (T)(S2 + org[2]);
+#pragma unroll 2
+                    for (uint32_t q = q0; q < q1; ++q) {
+                        V4 s = ldro(a.rec + q);
+                        s.x += h0;
+                        s.y += h1;
+                        s.z += h2;
+                        interact1<T>(s, tx, ty, tz, eps2, ap, ax, ay, az);
+                    }
+                } else {
+                    for (uint32_t q = q0; q < q1; ++q) {
+                        V4 s = ldro(a.rec + q);
+                        s.x = (T)__dsub_rn(__dadd_rn((double)s.x, S0), org[0]);
+                        s.y = (T)__dsub_rn(__dadd_rn((double)s.y, S1), org[1]);
+                        s.z = (T)__dsub_rn(__dadd_rn((double)s.z, S2), org[2]);
+                        interact1<T>(s, tx, ty, tz, eps2, ap, ax, ay, az);
+                    }
+                }
+            }
+        }
+        const uint32_t idx = a.perm[p];
+        a.phi[idx] = -(ap - t.w * Tgt<T, 2>::self_rinv(eps2));
+        if (a.field) {
+            a.field[3 * (size_t)idx + 0] = ax;
+            a.field[3 * (size_t)idx + 1] = ay;
+            a.field[3 * (size_t)idx + 2] = az;
+        }
+        }
+    }
+}
+
 template <typename T, int LAYOUT, int K>
 __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T> a) {
     using V4 = typename V4T<T>::type;
@@ -313,7 +441,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
     };
 
     uint32_t cur = fetch();
-    if (cur >= n_items) return;
+    if (cur < n_items) {
     uint32_t nxt = fetch();  // one item ahead: the atomic's latency overlaps the current item
     load_item(cur);
     issue(0, 0);
@@ -460,6 +588,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
         }
         if (!have_next) break;
     }
+    }
+    // the small boxes' targets, thread per target (fills the tail of the item queue)
+    small_phase<T, LAYOUT>(a, lane);
 }
 
 template <typename T, int LAYOUT, int K>
@@ -487,12 +618,17 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
     a.items = P->items;
     a.n_items = &P->ctr->n_items;
     a.item_head = &P->ctr->item_head;
+    a.n_small = &P->ctr->n_small;
+    a.small_head = &P->ctr->small_head;
+    a.small_tgt = P->small_tgt;
+    a.small_box = P->small_box;
     a.phi = (T *)phi;
     a.field = (T *)field;
-    const int64_t nit = P->sizes_known ? P->n_items : P->cap;
+    const int64_t nit = P->sizes_known ? P->n_items + (P->n + 31) / 32 : P->cap;
     const unsigned grid =
         (unsigned)std::min<int64_t>(P->eval_blocks[slot], std::max<int64_t>(1, (nit + EV_WARPS - 1) / EV_WARPS));
     P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->item_head, 0, sizeof(unsigned int), P->stream));
+    P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->small_head, 0, sizeof(unsigned int), P->stream));
     P2P_LAUNCH(kern, grid, EV_WARPS * 32, smem, P->stream, a);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
@@ -500,7 +636,7 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
 }  // namespace
 
 p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
-    if (P->sizes_known && P->n_items == 0) return P2P_OK;
+    if (P->sizes_known && P->n == 0) return P2P_OK;
     const bool f64 = P->cfg.precision == P2P_FP64;
     switch (layout) {
     case P2P_REDUNDANT:

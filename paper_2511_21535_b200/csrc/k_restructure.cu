@@ -51,12 +51,19 @@ __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const
         const double o1 = __fma_rn((double)c[1], g.h, g.lo[1]);
         const double o2 = __fma_rn((double)c[2], g.h, g.lo[2]);
         const uint32_t e0 = nbr_off[b], ne = nbr_off[b + 1] - e0;
-        uint32_t src = 0, cnt = 0, slot = 0;
+        // lane e < ne holds segment e: source start, length, and the image code of its slot
+        // (2 bits per dim: 1 = +L, 2 = -L, computed once per segment instead of once per record)
+        uint32_t src = 0, cnt = 0, code = 0;
         if (lane < ne) {
             const uint32_t k = nbr_box[e0 + lane];
             src = bstart[k];
             cnt = bstart[k + 1] - src;
-            slot = nbr_slot[e0 + lane];
+            const int slot = nbr_slot[e0 + lane];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double S = slot_shift(g, c, slot, d);
+                code |= (S > 0.0 ? 1u : (S < 0.0 ? 2u : 0u)) << (2 * d);
+            }
         }
         uint32_t incl = cnt;
 #pragma unroll
@@ -67,25 +74,28 @@ __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const
         const uint32_t st = incl - cnt;
         const uint32_t Rb = __shfl_sync(0xffffffffu, incl, 31);
         V4 *__restrict__ out = red + red_off[b];
+        const bool seg = lane < ne;
         for (uint32_t r0 = 0; r0 < Rb; r0 += 32) {
+            // segment of record r0 + lane without a search (segments are non-empty and contiguous):
+            //   segments starting before r0 (ballot) - 1  +  segment starts in [r0, r0 + lane] (OR-reduced mask)
+            const uint32_t before = __popc(__ballot_sync(0xffffffffu, seg && st < r0));
+            const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
+            const uint32_t starts = __reduce_or_sync(0xffffffffu, in_win);
+            const uint32_t le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+            const uint32_t e = before - 1u + __popc(starts & le);
+            const uint32_t e_src = __shfl_sync(0xffffffffu, src, e & 31u);
+            const uint32_t e_st = __shfl_sync(0xffffffffu, st, e & 31u);
+            const uint32_t e_code = __shfl_sync(0xffffffffu, code, e & 31u);
             const uint32_t r = r0 + lane;
-            // largest segment e < ne with st_e <= r
-            uint32_t e = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint32_t cand = e + step;
-                const uint32_t sc = __shfl_sync(0xffffffffu, st, cand & 31u);
-                if (cand < ne && sc <= r) e = cand;
-            }
-            const uint32_t e_src = __shfl_sync(0xffffffffu, src, e);
-            const uint32_t e_st = __shfl_sync(0xffffffffu, st, e);
-            const int e_slot = (int)__shfl_sync(0xffffffffu, slot, e);
             if (r < Rb) {
                 const V4 x = rec[e_src + (r - e_st)];
+                const double S0 = (e_code & 1u) ? g.L[0] : ((e_code & 2u) ? -g.L[0] : 0.0);
+                const double S1 = (e_code & 4u) ? g.L[1] : ((e_code & 8u) ? -g.L[1] : 0.0);
+                const double S2 = (e_code & 16u) ? g.L[2] : ((e_code & 32u) ? -g.L[2] : 0.0);
                 V4 v;
-                v.x = (T)__dsub_rn(__dadd_rn((double)x.x, slot_shift(g, c, e_slot, 0)), o0);
-                v.y = (T)__dsub_rn(__dadd_rn((double)x.y, slot_shift(g, c, e_slot, 1)), o1);
-                v.z = (T)__dsub_rn(__dadd_rn((double)x.z, slot_shift(g, c, e_slot, 2)), o2);
+                v.x = (T)__dsub_rn(__dadd_rn((double)x.x, S0), o0);
+                v.y = (T)__dsub_rn(__dadd_rn((double)x.y, S1), o1);
+                v.z = (T)__dsub_rn(__dadd_rn((double)x.z, S2), o2);
                 v.w = x.w;
                 out[r] = v;
             }

@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
                                                    const uint32_t *__restrict__ bstart,
                                                    const uint32_t *__restrict__ box_of, DevCounters *ctr,
                                                    uint32_t *__restrict__ nbr_cnt, uint64_t *__restrict__ red_cnt,
-                                                   uint32_t *__restrict__ item_cnt, uint32_t tmax) {
+                                                   uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ small_cnt,
+                                                   uint32_t tmax) {
     const uint32_t B = ctr->B;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -183,7 +184,10 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
             const uint32_t nb_b = bstart[b + 1] - bstart[b];
             nbr_cnt[b] = cnt;
             red_cnt[b] = nk;
-            item_cnt[b] = item_chunks(nb_b, nk, tmax);
+            // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
+            const bool small = nb_b <= SMALL_NT && nk <= SMALL_R;
+            item_cnt[b] = small ? 0u : item_chunks(nb_b, nk, tmax);
+            small_cnt[b] = small ? nb_b : 0u;
             pairs += (unsigned long long)nb_b * nk;
         }
     }
@@ -197,6 +201,8 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
                                                   const uint32_t *__restrict__ item_off,
                                                   const uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ nbr_box,
                                                   uint8_t *__restrict__ nbr_slot, Item *__restrict__ items,
+                                                  const uint32_t *__restrict__ small_off,
+                                                  uint32_t *__restrict__ small_tgt, uint32_t *__restrict__ small_box,
                                                   uint32_t K) {
     const uint32_t B = ctr->B;
     const unsigned lane = threadIdx.x & 31u;
@@ -213,6 +219,13 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
             nbr_slot[e] = (uint8_t)lane;
         }
         const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
+        if (item_cnt[b] == 0) {  // small box (k_nbr_count): thread-per-target path
+            if (lane < nb_b) {
+                small_tgt[small_off[b] + lane] = s0 + lane;
+                small_box[small_off[b] + lane] = b;
+            }
+            continue;
+        }
         const uint32_t nch = item_cnt[b], it = item_off[b];
         for (uint32_t ci = lane; ci < nch; ci += 32) {
             const uint32_t a0 = (uint32_t)(((uint64_t)nb_b * ci) / nch);
@@ -295,12 +308,14 @@ static unsigned warp_grid(uint64_t nwork, int num_sms) {
 void free_capacity(p2p_plan *P) {
     cudaStream_t st = P->stream;
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
-                    P->s_nbr_cnt, P->s_item_cnt, P->s_item_off, P->s_red_cnt, P->rec, P->bkey, P->bstart,
+                    P->s_nbr_cnt, P->s_item_cnt, P->s_item_off, P->s_red_cnt, P->s_small_cnt, P->s_small_off,
+                    P->small_tgt, P->small_box, P->rec, P->bkey, P->bstart,
                     P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
     P->s_nbr_cnt = P->s_item_cnt = P->s_item_off = nullptr;
+    P->s_small_cnt = P->s_small_off = P->small_tgt = P->small_box = nullptr;
     P->s_red_cnt = nullptr;
     P->rec = nullptr;
     P->bkey = P->bstart = P->nbr_off = P->nbr_box = P->box_of = nullptr;
@@ -340,6 +355,10 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
         P2P_CUDA_TRY(dalloc((void **)&P->s_nbr_cnt, 4 * bcap, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_item_cnt, 4 * bcap, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_item_off, 4 * (bcap + 1), st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_small_cnt, 4 * bcap, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_small_off, 4 * (bcap + 1), st));
+        P2P_CUDA_TRY(dalloc((void **)&P->small_tgt, 4 * n, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->small_box, 4 * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_red_cnt, 8 * bcap, st));
         P2P_CUDA_TRY(dalloc((void **)&P->red_off, 8 * (bcap + 1), st));
         P2P_CUDA_TRY(dalloc((void **)&P->items, sizeof(Item) * n, st));
@@ -377,7 +396,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q) {
     const unsigned gw = warp_grid(bcap, P->num_sms);
     const uint32_t tmax = ITEM_TMAX;
     P2P_LAUNCH(k_nbr_count, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, P->s_nbr_cnt,
-               P->s_red_cnt, P->s_item_cnt, tmax);
+               P->s_red_cnt, P->s_item_cnt, P->s_small_cnt, tmax);
     P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_nbr_cnt}, OffPut<uint32_t>{P->nbr_off, &P->ctr->B},
                                        &P->ctr->B, bcap, &P->ctr->n_nbr, P->s_partials, st));
     P2P_CUDA_TRY(device_scan<unsigned long long>(
@@ -386,8 +405,11 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q) {
         P->s_partials, st));
     P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_item_cnt}, OffPut<uint32_t>{P->s_item_off, &P->ctr->B},
                                        &P->ctr->B, bcap, &P->ctr->n_items, P->s_partials, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_small_cnt}, OffPut<uint32_t>{P->s_small_off, &P->ctr->B},
+                                       &P->ctr->B, bcap, &P->ctr->n_small, P->s_partials, st));
     P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, P->nbr_off,
-               P->s_item_off, P->s_item_cnt, P->nbr_box, P->nbr_slot, P->items,
+               P->s_item_off, P->s_item_cnt, P->nbr_box, P->nbr_slot, P->items, P->s_small_off, P->small_tgt,
+               P->small_box,
                (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;

@@ -19,7 +19,9 @@ struct DevCounters {
     unsigned long long I;          // pair interactions
     unsigned int item_head;        // eval work queue head (reset before every eval)
     unsigned int sort_tile_ctr[4]; // onesweep tile counters, one per pass
-    unsigned int pad[3];
+    unsigned int n_small;          // targets of small boxes (thread-per-target path of the eval)
+    unsigned int small_head;       // eval small-target queue head (reset before every eval)
+    unsigned int pad[1];
 };
 
 // eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
@@ -32,6 +34,10 @@ struct Item {
 constexpr int EVAL_K_F32 = 4;    // targets per lane in k_eval_gravity (fp32: two packed FP32x2 pairs)
 constexpr int EVAL_K_F64 = 2;
 constexpr uint32_t ITEM_TMAX = 32;  // max targets per work item (lane utilisation)
+// boxes with <= SMALL_NT targets and <= SMALL_R sources take the eval's thread-per-target path (no work item):
+// their per-item overhead would exceed their work, and their runs are short enough for L1-latency-bound loads
+constexpr uint32_t SMALL_NT = 8;
+constexpr uint32_t SMALL_R = 128;
 
 // gravity geometry passed by value to kernels
 struct Geom {
@@ -73,6 +79,8 @@ struct p2p_plan {
     uint32_t *s_hist = nullptr, *s_status = nullptr;
     void *s_partials = nullptr;
     uint32_t *s_nbr_cnt = nullptr, *s_item_cnt = nullptr, *s_item_off = nullptr;
+    uint32_t *s_small_cnt = nullptr, *s_small_off = nullptr;
+    uint32_t *small_tgt = nullptr, *small_box = nullptr;  // sorted target index / its box, small boxes only
     uint64_t *s_red_cnt = nullptr;
     bool sizes_known = false;  // host copies of B, n_nbr, R, I, n_items valid (false after an async update)
     bool red_valid = false;
