@@ -75,29 +75,44 @@ __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const
         const uint32_t Rb = __shfl_sync(0xffffffffu, incl, 31);
         V4 *__restrict__ out = red + red_off[b];
         const bool seg = lane < ne;
-        for (uint32_t r0 = 0; r0 < Rb; r0 += 32) {
-            // segment of record r0 + lane without a search (segments are non-empty and contiguous):
-            //   segments starting before r0 (ballot) - 1  +  segment starts in [r0, r0 + lane] (OR-reduced mask)
-            const uint32_t before = __popc(__ballot_sync(0xffffffffu, seg && st < r0));
-            const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
-            const uint32_t starts = __reduce_or_sync(0xffffffffu, in_win);
-            const uint32_t le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-            const uint32_t e = before - 1u + __popc(starts & le);
-            const uint32_t e_src = __shfl_sync(0xffffffffu, src, e & 31u);
-            const uint32_t e_st = __shfl_sync(0xffffffffu, st, e & 31u);
-            const uint32_t e_code = __shfl_sync(0xffffffffu, code, e & 31u);
-            const uint32_t r = r0 + lane;
-            if (r < Rb) {
-                const V4 x = rec[e_src + (r - e_st)];
-                const double S0 = (e_code & 1u) ? g.L[0] : ((e_code & 2u) ? -g.L[0] : 0.0);
-                const double S1 = (e_code & 4u) ? g.L[1] : ((e_code & 8u) ? -g.L[1] : 0.0);
-                const double S2 = (e_code & 16u) ? g.L[2] : ((e_code & 32u) ? -g.L[2] : 0.0);
-                V4 v;
-                v.x = (T)__dsub_rn(__dadd_rn((double)x.x, S0), o0);
-                v.y = (T)__dsub_rn(__dadd_rn((double)x.y, S1), o1);
-                v.z = (T)__dsub_rn(__dadd_rn((double)x.z, S2), o2);
-                v.w = x.w;
-                out[r] = v;
+        const uint32_t le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+        // UNR windows of 32 records per iteration: all loads issued before the first store (memory-level
+        // parallelism: the kernel is latency-bound otherwise)
+        constexpr int UNR = 4;
+        for (uint32_t rb = 0; rb < Rb; rb += 32 * UNR) {
+            V4 x[UNR];
+            uint32_t xcode[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t r0 = rb + 32u * u;
+                if (r0 >= Rb) break;  // warp-uniform: short runs skip the empty windows
+                // segment of record r0 + lane without a search (segments are non-empty and contiguous):
+                // segments starting before r0 (ballot) - 1 + segment starts in [r0, r0 + lane] (OR-reduced mask)
+                const uint32_t before = __popc(__ballot_sync(0xffffffffu, seg && st < r0));
+                const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
+                const uint32_t starts = __reduce_or_sync(0xffffffffu, in_win);
+                const uint32_t e = (before - 1u + __popc(starts & le)) & 31u;
+                const uint32_t e_src = __shfl_sync(0xffffffffu, src, e);
+                const uint32_t e_st = __shfl_sync(0xffffffffu, st, e);
+                xcode[u] = __shfl_sync(0xffffffffu, code, e);
+                const uint32_t r = r0 + lane;
+                if (r < Rb) x[u] = rec[e_src + (r - e_st)];
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t r = rb + 32u * u + lane;
+                if (r < Rb) {
+                    const uint32_t cd = xcode[u];
+                    const double S0 = (cd & 1u) ? g.L[0] : ((cd & 2u) ? -g.L[0] : 0.0);
+                    const double S1 = (cd & 4u) ? g.L[1] : ((cd & 8u) ? -g.L[1] : 0.0);
+                    const double S2 = (cd & 16u) ? g.L[2] : ((cd & 32u) ? -g.L[2] : 0.0);
+                    V4 v;
+                    v.x = (T)__dsub_rn(__dadd_rn((double)x[u].x, S0), o0);
+                    v.y = (T)__dsub_rn(__dadd_rn((double)x[u].y, S1), o1);
+                    v.z = (T)__dsub_rn(__dadd_rn((double)x[u].z, S2), o2);
+                    v.w = x[u].w;
+                    out[r] = v;
+                }
             }
         }
     }

@@ -171,24 +171,38 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     unsigned long long pairs = 0;
-    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nwarps) {
-        uint32_t c[3];
-        decode3(bkey[b], c);
-        uint32_t k = 0;
-        const bool ok = lane_nbr(g, c, lane, B, bkey, box_of, k);
-        uint32_t nk = ok ? bstart[k + 1] - bstart[k] : 0u;
-        const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, ok));
+    // NB boxes per warp iteration: their dependent lookups (box_of -> bkey -> bstart) are in flight together
+    constexpr int NB = 4;
+    for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NB; b0 < B; b0 += nwarps * NB) {
+        bool ok[NB];
+        uint32_t k[NB];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nk += __shfl_xor_sync(0xffffffffu, nk, o);
-        if (lane == 0) {
-            const uint32_t nb_b = bstart[b + 1] - bstart[b];
-            nbr_cnt[b] = cnt;
-            red_cnt[b] = nk;
-            // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
-            const bool small = nb_b <= SMALL_NT && nk <= SMALL_R;
-            item_cnt[b] = small ? 0u : item_chunks(nb_b, nk, tmax);
-            small_cnt[b] = small ? nb_b : 0u;
-            pairs += (unsigned long long)nb_b * nk;
+        for (int u = 0; u < NB; ++u) {
+            ok[u] = false;
+            k[u] = 0;
+            if (b0 + u < B) {
+                uint32_t c[3];
+                decode3(bkey[b0 + u], c);
+                ok[u] = lane_nbr(g, c, lane, B, bkey, box_of, k[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const uint32_t b = b0 + u;
+            uint32_t nk = ok[u] ? bstart[k[u] + 1] - bstart[k[u]] : 0u;
+            const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, ok[u]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nk += __shfl_xor_sync(0xffffffffu, nk, o);
+            if (lane == 0 && b < B) {
+                const uint32_t nb_b = bstart[b + 1] - bstart[b];
+                nbr_cnt[b] = cnt;
+                red_cnt[b] = nk;
+                // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
+                const bool small = nb_b <= SMALL_NT && nk <= SMALL_R;
+                item_cnt[b] = small ? 0u : item_chunks(nb_b, nk, tmax);
+                small_cnt[b] = small ? nb_b : 0u;
+                pairs += (unsigned long long)nb_b * nk;
+            }
         }
     }
     if (lane == 0 && pairs) atomicAdd(&ctr->I, pairs);
@@ -207,32 +221,47 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
     const uint32_t B = ctr->B;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nwarps) {
-        uint32_t c[3];
-        decode3(bkey[b], c);
-        uint32_t k = 0;
-        const bool ok = lane_nbr(g, c, lane, B, bkey, box_of, k);
-        const uint32_t m = __ballot_sync(0xffffffffu, ok);
-        if (ok) {
-            const uint32_t e = nbr_off[b] + __popc(m & ((1u << lane) - 1u));
-            nbr_box[e] = k;
-            nbr_slot[e] = (uint8_t)lane;
-        }
-        const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
-        if (item_cnt[b] == 0) {  // small box (k_nbr_count): thread-per-target path
-            if (lane < nb_b) {
-                small_tgt[small_off[b] + lane] = s0 + lane;
-                small_box[small_off[b] + lane] = b;
+    constexpr int NB = 4;  // boxes per warp iteration (memory-level parallelism, as in k_nbr_count)
+    for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NB; b0 < B; b0 += nwarps * NB) {
+        bool ok[NB];
+        uint32_t k[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            ok[u] = false;
+            k[u] = 0;
+            if (b0 + u < B) {
+                uint32_t c[3];
+                decode3(bkey[b0 + u], c);
+                ok[u] = lane_nbr(g, c, lane, B, bkey, box_of, k[u]);
             }
-            continue;
         }
-        const uint32_t nch = item_cnt[b], it = item_off[b];
-        for (uint32_t ci = lane; ci < nch; ci += 32) {
-            const uint32_t a0 = (uint32_t)(((uint64_t)nb_b * ci) / nch);
-            const uint32_t z0 = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
-            // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
-            const uint32_t nt = z0 - a0, G = (nt + K - 1) / K, S = 32u / G;
-            items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16)};
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const uint32_t b = b0 + u;
+            const uint32_t m = __ballot_sync(0xffffffffu, ok[u]);
+            if (b >= B) continue;
+            if (ok[u]) {
+                const uint32_t e = nbr_off[b] + __popc(m & ((1u << lane) - 1u));
+                nbr_box[e] = k[u];
+                nbr_slot[e] = (uint8_t)lane;
+            }
+            const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
+            const uint32_t nch = item_cnt[b];
+            if (nch == 0) {  // small box (k_nbr_count): thread-per-target path
+                if (lane < nb_b) {
+                    small_tgt[small_off[b] + lane] = s0 + lane;
+                    small_box[small_off[b] + lane] = b;
+                }
+                continue;
+            }
+            const uint32_t it = item_off[b];
+            for (uint32_t ci = lane; ci < nch; ci += 32) {
+                const uint32_t a0 = (uint32_t)(((uint64_t)nb_b * ci) / nch);
+                const uint32_t z0 = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
+                // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
+                const uint32_t nt = z0 - a0, G = (nt + K - 1) / K, S = 32u / G;
+                items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16)};
+            }
         }
     }
 }
@@ -302,7 +331,7 @@ static unsigned grid_for(uint64_t n, int threads, int num_sms) {
 // ------------------------------------------------------------------------------------------------
 static unsigned warp_grid(uint64_t nwork, int num_sms) {
     // one warp per work unit, 8 warps per block, at most 16 resident blocks per SM (grid-stride beyond)
-    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(div_up(nwork, 8), (uint64_t)num_sms * 16));
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(div_up(nwork, 8), (uint64_t)num_sms * 8));  // one full-occupancy wave
 }
 
 void free_capacity(p2p_plan *P) {
