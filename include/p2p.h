@@ -171,6 +171,31 @@ p2p_status p2p_comm_unique_id(void *id_out /* host, 128 bytes */);
 p2p_status p2p_comm_create(int nranks, int rank, const void *id /* host, 128 bytes */, p2p_comm **out);
 void p2p_comm_destroy(p2p_comm *comm);
 
+/* Multi-GPU plan semantics (cfg->comm != NULL; gravity only).  Every rank calls p2p_plan_create / p2p_eval
+ * collectively with ITS OWN input slice (any distribution).  The ranks repartition the particles into
+ * contiguous Morton ranges of boxes, balanced by particle count on a coarse supercell histogram
+ * (p2p_partition_splitters), exchange whole halo boxes, and each rank evaluates the targets of its range;
+ * p2p_eval returns every result to the rank and input slot it came from.  Results are bitwise identical to a
+ * 1-GPU plan over the rank-major concatenation of the slices.  p2p_get_info / p2p_copy_out describe the rank's
+ * LOCAL plan (owned + halo particles; halo boxes have empty neighbour lists and runs).  p2p_plan_update and
+ * p2p_set_charges return P2P_ERR_UNSUPPORTED for multi-GPU plans (re-create the plan). */
+
+/* The count-balanced splitters of SURVEY §8e / DESIGN C20, as computed inside the collective plan build
+ * (exported for testing the host logic): hist[nbins] = global particle counts per supercell (supercell =
+ * key >> shift); rank r gets keys [splitters[r], splitters[r+1]), splitters[0] = 0, splitters[nranks] =
+ * 2^key_bits; splitter r = (first supercell whose exclusive prefix count >= r * total / nranks) << shift.
+ *   hist: host, [nbins] u64;  splitters_out: host, [nranks + 1] u32 */
+p2p_status p2p_partition_splitters(const uint64_t *hist, int64_t nbins, int shift, int key_bits, int nranks,
+                                   uint32_t *splitters_out);
+
+/* In-process "loopback" communicators: nranks emulated ranks = nranks host threads of ONE process sharing one
+ * device; the collectives become device-to-device copies + a host barrier.  Used to run the whole multi-GPU
+ * algorithm on a single GPU (tests: bit-identity against the 1-GPU plan). */
+typedef struct p2p_loopback_group p2p_loopback_group;
+p2p_status p2p_loopback_group_create(int nranks, p2p_loopback_group **out);
+void p2p_loopback_group_destroy(p2p_loopback_group *group);
+p2p_status p2p_comm_create_loopback(p2p_loopback_group *group, int rank, p2p_comm **out);
+
 /* ---- diagnostics ---- */
 const char *p2p_status_string(p2p_status s);
 const char *p2p_last_error(void);        /* thread-local detail of the last failing call on this thread */

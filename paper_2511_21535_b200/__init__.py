@@ -31,9 +31,11 @@ P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE = 0, 1, 2
 
 LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise": P2P_INDEXED_BITWISE}
 
-EXPORTED = ["p2p_plan_create", "p2p_restructure", "p2p_eval", "p2p_set_charges", "p2p_destroy", "p2p_get_info",
-            "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy", "p2p_status_string",
-            "p2p_last_error", "p2p_kernel_launch_count", "p2p_abi_version"]
+EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_restructure", "p2p_eval", "p2p_set_charges", "p2p_destroy",
+            "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
+            "p2p_partition_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
+            "p2p_comm_create_loopback", "p2p_status_string", "p2p_last_error", "p2p_kernel_launch_count",
+            "p2p_abi_version"]
 
 
 class P2PConfig(C.Structure):
@@ -83,6 +85,10 @@ def lib() -> C.CDLL:
             "p2p_last_error": (C.c_char_p, []),
             "p2p_kernel_launch_count": (u64, []),
             "p2p_abi_version": (C.c_int, []),
+            "p2p_partition_splitters": (C.c_int, [p, i64, C.c_int, C.c_int, C.c_int, p]),
+            "p2p_loopback_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+            "p2p_loopback_group_destroy": (None, [p]),
+            "p2p_comm_create_loopback": (C.c_int, [p, C.c_int, C.POINTER(C.c_void_p)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -159,6 +165,30 @@ def p2p_comm_destroy(comm: int):
     lib().p2p_comm_destroy(C.c_void_p(comm))
 
 
+def p2p_partition_splitters(hist: np.ndarray, shift: int, key_bits: int, nranks: int) -> np.ndarray:
+    h = np.ascontiguousarray(np.asarray(hist, dtype=np.uint64))
+    out = np.zeros(nranks + 1, np.uint32)
+    _check(lib().p2p_partition_splitters(h.ctypes.data_as(C.c_void_p), h.shape[0], int(shift), int(key_bits),
+                                         int(nranks), out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def p2p_loopback_group_create(nranks: int) -> int:
+    out = C.c_void_p()
+    _check(lib().p2p_loopback_group_create(int(nranks), C.byref(out)))
+    return out.value
+
+
+def p2p_loopback_group_destroy(group: int):
+    lib().p2p_loopback_group_destroy(C.c_void_p(group))
+
+
+def p2p_comm_create_loopback(group: int, rank: int) -> int:
+    out = C.c_void_p()
+    _check(lib().p2p_comm_create_loopback(C.c_void_p(group), int(rank), C.byref(out)))
+    return out.value
+
+
 def p2p_status_string(s: int) -> str:
     return lib().p2p_status_string(int(s)).decode()
 
@@ -207,7 +237,7 @@ class Plan:
     """RAII wrapper of a p2p_plan over torch CUDA tensors (positions [N][dim], charges [N] real or [N][2] complex)."""
 
     def __init__(self, kernel: int, positions, charges, h: float, lo, nbox, periodic: int = 0, eps: float = 0.0,
-                 k: float = 0.0, t: int = 0, stream=None):
+                 k: float = 0.0, t: int = 0, stream=None, comm: int | None = None):
         import torch
         assert positions.is_cuda and charges.is_cuda, "positions / charges must be CUDA tensors"
         positions = positions.contiguous()
@@ -217,6 +247,7 @@ class Plan:
         self.dtype = positions.dtype
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self.cfg = make_config(kernel, prec, h, lo, nbox, periodic, eps, k, t, self.stream.cuda_stream)
+        self.cfg.comm = comm
         self.n = int(positions.shape[0])
         self._handle = p2p_plan_create(self.cfg, self.n, positions.data_ptr(), charges.data_ptr())
         self._info = p2p_get_info(self._handle)

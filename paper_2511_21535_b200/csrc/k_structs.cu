@@ -29,15 +29,16 @@ __device__ __forceinline__ uint32_t item_chunks(uint32_t nb_b, uint64_t nsrc, ui
 }
 
 // ------------------------------------------------------------------------------------------------ a1
+// positions at pos[i * ps + d] (ps = 3: the caller's [N][3] array; ps = 4: {x,y,z,m} records)
 template <typename T>
-__global__ void k_bin_gravity(const T *__restrict__ pos, uint32_t n, Geom g, uint32_t *__restrict__ key,
+__global__ void k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geom g, uint32_t *__restrict__ key,
                               uint32_t *__restrict__ idx, DevCounters *ctr) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         uint32_t c[3];
         bool bad = false;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            double x = (double)pos[3 * (size_t)i + d];
+            double x = (double)pos[(size_t)ps * i + d];
             double f = floor(__ddiv_rn(__dsub_rn(x, g.lo[d]), g.h));
             if (!(f >= 0.0 && f < (double)g.nbox[d])) {
                 bad = true;
@@ -85,15 +86,15 @@ __global__ void k_bin_helmholtz(const T *__restrict__ pos, uint32_t n, Geom g, i
 
 // ------------------------------------------------------------------------------------------------ a3
 template <typename T, typename V4>
-__global__ void k_permute_gravity(const T *__restrict__ pos, const T *__restrict__ q, const uint32_t *__restrict__ perm,
-                                  uint32_t n, V4 *__restrict__ rec) {
+__global__ void k_permute_gravity(const T *__restrict__ pos, int ps, const T *__restrict__ q, int qs,
+                                  const uint32_t *__restrict__ perm, uint32_t n, V4 *__restrict__ rec) {
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
         uint32_t i = perm[p];
         V4 r;
-        r.x = pos[3 * (size_t)i + 0];
-        r.y = pos[3 * (size_t)i + 1];
-        r.z = pos[3 * (size_t)i + 2];
-        r.w = q[i];
+        r.x = pos[(size_t)ps * i + 0];
+        r.y = pos[(size_t)ps * i + 1];
+        r.z = pos[(size_t)ps * i + 2];
+        r.w = q[(size_t)qs * i];
         rec[p] = r;
     }
 }
@@ -181,9 +182,11 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
             ok[u] = false;
             k[u] = 0;
             if (b0 + u < B) {
+                const uint32_t key = bkey[b0 + u];
                 uint32_t c[3];
-                decode3(bkey[b0 + u], c);
-                ok[u] = lane_nbr(g, c, lane, B, bkey, box_of, k[u]);
+                decode3(key, c);
+                // non-target (multi-GPU halo) boxes get no neighbour list and no work
+                if (key >= g.tkey_lo && key <= g.tkey_hi) ok[u] = lane_nbr(g, c, lane, B, bkey, box_of, k[u]);
             }
         }
 #pragma unroll
@@ -194,12 +197,14 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) nk += __shfl_xor_sync(0xffffffffu, nk, o);
             if (lane == 0 && b < B) {
-                const uint32_t nb_b = bstart[b + 1] - bstart[b];
+                const uint32_t key = bkey[b];
+                const bool target = key >= g.tkey_lo && key <= g.tkey_hi;
+                const uint32_t nb_b = target ? bstart[b + 1] - bstart[b] : 0u;
                 nbr_cnt[b] = cnt;
                 red_cnt[b] = nk;
                 // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
                 const bool small = nb_b <= SMALL_NT && nk <= SMALL_R;
-                item_cnt[b] = small ? 0u : item_chunks(nb_b, nk, tmax);
+                item_cnt[b] = (small || !target) ? 0u : item_chunks(nb_b, nk, tmax);
                 small_cnt[b] = small ? nb_b : 0u;
                 pairs += (unsigned long long)nb_b * nk;
             }
@@ -230,9 +235,11 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
             ok[u] = false;
             k[u] = 0;
             if (b0 + u < B) {
+                const uint32_t key = bkey[b0 + u];
                 uint32_t c[3];
-                decode3(bkey[b0 + u], c);
-                ok[u] = lane_nbr(g, c, lane, B, bkey, box_of, k[u]);
+                decode3(key, c);
+                // non-target (multi-GPU halo) boxes get no neighbour list and no work
+                if (key >= g.tkey_lo && key <= g.tkey_hi) ok[u] = lane_nbr(g, c, lane, B, bkey, box_of, k[u]);
             }
         }
 #pragma unroll
@@ -245,6 +252,8 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
                 nbr_box[e] = k[u];
                 nbr_slot[e] = (uint8_t)lane;
             }
+            const uint32_t key = bkey[b];
+            if (key < g.tkey_lo || key > g.tkey_hi) continue;  // halo box: source only
             const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
             const uint32_t nch = item_cnt[b];
             if (nch == 0) {  // small box (k_nbr_count): thread-per-target path
@@ -397,26 +406,35 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     return P2P_OK;
 }
 
-p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q) {
+p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, const void *rec_in) {
     cudaStream_t st = P->stream;
     const uint32_t n = (uint32_t)P->n;
     const bool f64 = P->cfg.precision == P2P_FP64;
     const unsigned gb = grid_for(n, 256, P->num_sms);
+    // AoS record input (multi-GPU local plan): positions at stride 4, masses = the .w component
+    const size_t tsz = f64 ? sizeof(double) : sizeof(float);
+    const int ps = rec_in ? 4 : 3, qs = rec_in ? 4 : 1;
+    if (rec_in) {
+        pos = rec_in;
+        q = (const char *)rec_in + 3 * tsz;
+    }
     // a1
     if (f64)
-        P2P_LAUNCH(k_bin_gravity<double>, gb, 256, 0, st, (const double *)pos, n, P->geom, P->s_key, P->s_idx, P->ctr);
+        P2P_LAUNCH(k_bin_gravity<double>, gb, 256, 0, st, (const double *)pos, ps, n, P->geom, P->s_key, P->s_idx,
+                   P->ctr);
     else
-        P2P_LAUNCH(k_bin_gravity<float>, gb, 256, 0, st, (const float *)pos, n, P->geom, P->s_key, P->s_idx, P->ctr);
+        P2P_LAUNCH(k_bin_gravity<float>, gb, 256, 0, st, (const float *)pos, ps, n, P->geom, P->s_key, P->s_idx,
+                   P->ctr);
     // a2
     P2P_CUDA_TRY(radix_sort_pairs(P->s_key, P->s_idx, P->s_kalt, P->s_valt, n, P->passes, P->ctr, P->s_hist,
                                   P->s_status, st, &P->skey, &P->perm));
     // a3
     if (f64)
-        P2P_LAUNCH((k_permute_gravity<double, double4>), gb, 256, 0, st, (const double *)pos, (const double *)q,
-                   P->perm, n, (double4 *)P->rec);
+        P2P_LAUNCH((k_permute_gravity<double, double4>), gb, 256, 0, st, (const double *)pos, ps, (const double *)q,
+                   qs, P->perm, n, (double4 *)P->rec);
     else
-        P2P_LAUNCH((k_permute_gravity<float, float4>), gb, 256, 0, st, (const float *)pos, (const float *)q, P->perm,
-                   n, (float4 *)P->rec);
+        P2P_LAUNCH((k_permute_gravity<float, float4>), gb, 256, 0, st, (const float *)pos, ps, (const float *)q, qs,
+                   P->perm, n, (float4 *)P->rec);
     // a4
     P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, 1u}, HeadPut{P->skey, 1u, P->bkey, P->bstart, P->box_of, n},
                                        nullptr, n, &P->ctr->B, P->s_partials, st));

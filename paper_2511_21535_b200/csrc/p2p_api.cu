@@ -96,6 +96,7 @@ static p2p_status mark(p2p_plan *P, p2p_status s) {
 static void free_plan_buffers(p2p_plan *P) {
     cudaStream_t st = P->stream;
     free_capacity(P);
+    free_distributed(P);
     void *bufs[] = {P->red, P->table, P->ctr};
     for (void *b : bufs) dfree(b, st);
     P->red = P->table = nullptr;
@@ -184,7 +185,8 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
         while (st * st < t) ++st;
         if (t < 1 || st * st != t) return fail(P2P_ERR_INVALID_ARGUMENT, "points_per_box t must be a perfect square");
     }
-    if (cfg->comm) return fail(P2P_ERR_UNSUPPORTED, "multi-GPU plans are not available in this build");
+    if (cfg->comm && !grav) return fail(P2P_ERR_UNSUPPORTED, "multi-GPU plans are gravity plans (DBIM is 1-GPU)");
+    if (cfg->comm && !cfg->comm->impl) return fail(P2P_ERR_INVALID_ARGUMENT, "comm is not initialised");
     if (n_local > 0 && (!is_device_ptr(positions) || !is_device_ptr(charges)))
         return fail(P2P_ERR_INVALID_ARGUMENT, "positions / charges must be device pointers");
 
@@ -245,16 +247,35 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
         return bail(fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate counters"));
     cudaMemsetAsync(P->ctr, 0, sizeof(DevCounters), st);
     cudaMemsetAsync(&P->ctr->err_index, 0xff, sizeof(unsigned long long), st);
-    if (n_local == 0) {
-        cudaStreamSynchronize(st);
-        P->sizes_known = true;
-        *out = P;
-        return P2P_OK;
+    g.tkey_lo = 0u;  // single GPU: every box is a target box
+    g.tkey_hi = 0xffffffffu;
+    p2p_status s = P2P_OK;
+    if (cfg->comm) {
+        // multi-GPU: collective build (repartition + halo), then the local plan over [owned ; halo] (k_dist.cu)
+        P->comm = cfg->comm->impl;
+        P->n_in = n_local;
+        s = build_distributed(P, positions, charges);
+        if (s != P2P_OK) return bail(s);
+        if (P->n == 0) {
+            cudaStreamSynchronize(st);
+            P->sizes_known = true;
+            *out = P;
+            return P2P_OK;
+        }
+    } else {
+        P->n_in = n_local;
+        if (n_local == 0) {
+            cudaStreamSynchronize(st);
+            P->sizes_known = true;
+            *out = P;
+            return P2P_OK;
+        }
+        tr.at("validated+counters");
+        if (alloc_capacity(P, n_local) != P2P_OK)
+            return bail(fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate plan buffers"));
+        s = grav ? build_gravity_structs(P, positions, charges) : build_helmholtz_structs(P, positions, charges);
+        if (s != P2P_OK) return bail(s);
     }
-    tr.at("validated+counters");
-    if (alloc_capacity(P, n_local) != P2P_OK) return bail(fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate plan buffers"));
-    p2p_status s = grav ? build_gravity_structs(P, positions, charges) : build_helmholtz_structs(P, positions, charges);
-    if (s != P2P_OK) return bail(s);
     tr.at("structs enqueued");
     // the ONE host synchronisation: sizes for the redundant buffer and launch geometry
     DevCounters h;
@@ -301,6 +322,7 @@ p2p_status p2p_plan_update(p2p_plan *P, int64_t n_local, const void *positions, 
     if (s != P2P_OK) return s;
     if (P->cfg.kernel != P2P_GRAVITY)
         return fail(P2P_ERR_UNSUPPORTED, "p2p_plan_update is for gravity plans (DBIM geometry is fixed: use set_charges)");
+    if (P->comm) return fail(P2P_ERR_UNSUPPORTED, "multi-GPU plans are rebuilt with p2p_plan_create (collective)");
     if (n_local < 0) return fail(P2P_ERR_INVALID_ARGUMENT, "n_local < 0");
     if (n_local >= (int64_t)1 << 31) return fail(P2P_ERR_UNSUPPORTED, "n_local >= 2^31 (u32 indices)");
     if (n_local > 0 && (!is_device_ptr(positions) || !is_device_ptr(charges)))
@@ -358,6 +380,12 @@ p2p_status p2p_eval(p2p_plan *P, p2p_layout layout, void *potential, void *field
         return fail(P2P_ERR_INVALID_ARGUMENT, "unknown layout");
     if (layout == P2P_REDUNDANT && !P->red_valid)
         return fail(P2P_ERR_BAD_STATE, "eval(P2P_REDUNDANT) needs p2p_restructure first (and after set_charges)");
+    if (P->comm) {  // collective: every rank calls, even with no particles
+        if (P->n_in > 0 && !is_device_ptr(potential))
+            return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
+        if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
+        return mark(P, eval_distributed(P, layout, potential, field));
+    }
     if (P->n == 0) return P2P_OK;
     if (!is_device_ptr(potential)) return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
     if (P->cfg.kernel == P2P_GRAVITY) {
@@ -371,6 +399,7 @@ p2p_status p2p_eval(p2p_plan *P, p2p_layout layout, void *potential, void *field
 p2p_status p2p_set_charges(p2p_plan *P, const void *charges) {
     p2p_status s = enter(P);
     if (s != P2P_OK) return s;
+    if (P->comm) return fail(P2P_ERR_UNSUPPORTED, "multi-GPU plans: charges move with the repartition (re-create)");
     if (P->n == 0) return P2P_OK;
     if (!is_device_ptr(charges)) return fail(P2P_ERR_INVALID_ARGUMENT, "charges must be a device pointer");
     P->red_valid = false;

@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
+#include "comm.hpp"
 #include "common.cuh"
 #include "p2p.h"
 
@@ -48,6 +51,7 @@ struct Geom {
     uint32_t periodic;
     int32_t nb;           // Morton bits per dim
     double eps2;          // eps^2 (fp64)
+    uint32_t tkey_lo, tkey_hi;  // target boxes: keys in [tkey_lo, tkey_hi] (multi-GPU: this rank's Morton range)
 };
 
 }  // namespace p2p
@@ -83,6 +87,14 @@ struct p2p_plan {
     uint32_t *small_tgt = nullptr, *small_box = nullptr;  // sorted target index / its box, small boxes only
     uint64_t *s_red_cnt = nullptr;
     bool sizes_known = false;  // host copies of B, n_nbr, R, I, n_items valid (false after an async update)
+    // ---- multi-GPU: this rank owns the target boxes of one contiguous Morton range ----
+    p2p::CommBase *comm = nullptr;
+    int64_t n_in = 0;          // caller's particles on this rank (outputs are for these, in their input order)
+    int64_t n_own = 0;         // owned (target) particles after the repartition; local plan n = n_own + halo
+    uint32_t *perm_send = nullptr;          // input index of the i-th particle sent in the repartition
+    std::vector<int64_t> rp_scnt, rp_soff, rp_rcnt, rp_roff;  // repartition counts / offsets (elements)
+    std::vector<uint32_t> splitters;        // G + 1 key boundaries of the rank ranges
+    void *phi_loc = nullptr, *field_loc = nullptr, *res_own = nullptr, *res_back = nullptr;
     bool red_valid = false;
     p2p_status sticky = P2P_OK;
     int eval_blocks[3] = {0, 0, 0};
@@ -101,7 +113,8 @@ size_t radix_status_words(uint64_t n, int passes);
 // k_structs.cu
 p2p_status alloc_capacity(p2p_plan *P, int64_t cap);   // all N-/B-sized buffers + scratch
 void free_capacity(p2p_plan *P);
-p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q);
+// pos/q: SoA caller arrays; or, if rec_in != nullptr, AoS {x,y,z,m} records (multi-GPU local plans)
+p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, const void *rec_in = nullptr);
 p2p_status build_helmholtz_structs(p2p_plan *P, const void *pos, const void *q);
 p2p_status set_charges_gravity(p2p_plan *P, const void *q);
 p2p_status set_charges_helmholtz(p2p_plan *P, const void *q);
@@ -112,6 +125,11 @@ p2p_status restructure_helmholtz(p2p_plan *P);
 
 // k_eval_gravity.cu / k_helmholtz.cu
 p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field);
+
+// k_dist.cu: the distributed (multi-GPU) plan build and result return
+p2p_status build_distributed(p2p_plan *P, const void *pos, const void *q);
+p2p_status eval_distributed(p2p_plan *P, p2p_layout layout, void *phi, void *field);
+void free_distributed(p2p_plan *P);
 p2p_status eval_helmholtz(p2p_plan *P, p2p_layout layout, void *y);
 p2p_status helmholtz_table(p2p_plan *P);
 
