@@ -160,21 +160,40 @@ def ours(args, rank, world, local):
     phi = torch.empty(N, dtype=torch.float32, device=dev)
     field = torch.empty((N, 3), dtype=torch.float32, device=dev)
 
-    # one persistent plan = the simulation's setup (allocations); every step rebuilds a1..a5 from the
-    # positions with p2p_plan_update (asynchronous: no host sync, no allocation), then a6, a7+a9
-    splan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps, stream=stream)
+    comm = None
+    if world > 1:
+        # NCCL communicator owned by libp2p; rank 0's unique id is broadcast over the torch process group
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(P.p2p_comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        comm = P.p2p_comm_create(world, rank, bytes(idt.cpu().numpy().tobytes()))
+
+    # 1 GPU: one persistent plan = the simulation's setup (allocations); every step rebuilds a1..a5 from the
+    # positions with p2p_plan_update (asynchronous: no host sync, no allocation), then a6, a7+a9.
+    # N GPUs: every step is the collective build (a1..a5 + histogram all-reduce + repartition + halo exchange
+    # over NCCL), a6, a7+a9 and the reverse all-to-all-v of the results.
+    splan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps, stream=stream,
+                   comm=comm)
+    holder = {"plan": splan}
 
     def step(events=None):
         ev = events
         if ev:
             ev[0].record(stream)
-        splan.update(pos, m)
+        if comm is None:
+            splan.update(pos, m)
+            plan = holder["plan"]
+        else:
+            holder["plan"].close()
+            plan = holder["plan"] = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps,
+                                           stream=stream, comm=comm)
         if ev:
             ev[1].record(stream)
-        splan.restructure()
+        plan.restructure()
         if ev:
             ev[2].record(stream)
-        splan.eval(P.P2P_REDUNDANT, phi, field)
+        plan.eval(P.P2P_REDUNDANT, phi, field)
         if ev:
             ev[3].record(stream)
 
@@ -188,7 +207,7 @@ def ours(args, rank, world, local):
         step()
         l2_flush()
     barrier()
-    I = int(splan.refresh_info().n_pairs)
+    I = int(holder["plan"].refresh_info().n_pairs)
 
     # ---- timed region: K full steps, L2 flushed between steps (outside the events) ----
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
@@ -217,7 +236,7 @@ def ours(args, rank, world, local):
     value = I_all / (ms_step * 1e-3)
 
     # ---- kernel-only phases on a persistent plan (same stream, L2 flushed before each launch) ----
-    plan = splan
+    plan = holder["plan"]
     plan.restructure()
 
     def timed(fn, reps):
@@ -270,7 +289,9 @@ def ours(args, rank, world, local):
         "dtype": "f32",
         "data": "synthetic (seeded numpy PCG64 Plummer tiles; BASELINE configs[4] per-GPU tile)",
         "config": {"workload": wdesc, "N_per_gpu": N, "boxes_per_gpu": B, "pairs_per_gpu_per_step": I,
-                   "red_records_per_gpu": R, "parallelism": f"dp{world} (one Plummer tile per GPU)",
+                   "red_records_per_gpu": R, "parallelism": (f"morton-range sharding over {world} GPUs: NCCL histogram all-reduce + all-to-all-v "
+                                   f"repartition + halo exchange (one Plummer tile per GPU)") if world > 1
+                   else "1 GPU",
                    "l2": "inputs+red buffer > L2 and 512 MB L2 flush between timed steps",
                    "step": "p2p_plan_update(a1-a5) + p2p_restructure(a6) + p2p_eval REDUNDANT(a7,a9); plan created once"},
         "roofline": {"bound": "alu", "kernel": "k_eval_gravity<float,REDUNDANT,4>", "achieved": achieved / 1e9,
@@ -299,7 +320,8 @@ def ours(args, rank, world, local):
         def e2e_once():
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            ph, fl = P.nearfield(P.P2P_GRAVITY, pos_h, m_h, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps)
+            ph, fl = P.nearfield(P.P2P_GRAVITY, pos_h, m_h, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps,
+                                 comm=comm)
             b.record(stream)
             b.synchronize()
             return a.elapsed_time(b)
@@ -315,6 +337,9 @@ def ours(args, rank, world, local):
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(inp, budget_s=12.0)
+    holder["plan"].close()
+    if comm is not None:
+        P.p2p_comm_destroy(comm)
     if dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -346,7 +346,7 @@ class Plan:
 
 
 def nearfield(kernel: int, positions, charges, h: float, lo, nbox, periodic: int = 0, eps: float = 0.0,
-              k: float = 0.0, t: int = 0, layout: int = P2P_REDUNDANT):
+              k: float = 0.0, t: int = 0, layout: int = P2P_REDUNDANT, comm: int | None = None):
     """One-shot public API: plan -> restructure -> eval -> destroy.  Accepts host (CPU) or device tensors; host
     inputs are copied to the device and the results back to the host (the end-to-end path bench.py times)."""
     import torch
@@ -354,7 +354,7 @@ def nearfield(kernel: int, positions, charges, h: float, lo, nbox, periodic: int
     dev = torch.device("cuda", torch.cuda.current_device())
     pos_d = positions.to(dev, non_blocking=True) if host else positions
     q_d = charges.to(dev, non_blocking=True) if host else charges
-    with Plan(kernel, pos_d, q_d, h, lo, nbox, periodic, eps, k, t) as plan:
+    with Plan(kernel, pos_d, q_d, h, lo, nbox, periodic, eps, k, t, comm=comm) as plan:
         if layout == P2P_REDUNDANT:
             plan.restructure()
         out = plan.eval(layout)

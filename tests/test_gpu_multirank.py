@@ -117,6 +117,25 @@ def test_multirank_bitwise_equals_single_gpu(P, case):
     assert oracle.rel_l2(phi, rphi) <= tol
 
 
+def test_nccl_communicator_single_rank(P):
+    """the NCCL backend itself (1 rank on the box's one GPU: all-reduce, grouped send/recv to self)"""
+    inp = G.plummer(20000, 16, seed=21)
+    uid = P.p2p_comm_unique_id()
+    comm = P.p2p_comm_create(1, 0, uid)
+    try:
+        pos = torch.from_numpy(inp.pos).cuda()
+        m = torch.from_numpy(inp.mass).cuda()
+        with P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps, comm=comm) as plan:
+            plan.restructure()
+            phi, f = plan.eval(P.P2P_REDUNDANT)
+            phi, f = phi.cpu().numpy(), f.cpu().numpy()
+    finally:
+        P.p2p_comm_destroy(comm)
+    ref, _ = single(P, inp, [P.P2P_REDUNDANT])
+    assert phi.tobytes() == ref[P.P2P_REDUNDANT][0].tobytes()
+    assert f.tobytes() == ref[P.P2P_REDUNDANT][1].tobytes()
+
+
 def test_multirank_rank_with_no_particles(P):
     inp = G.uniform_per_box(4, 4, seed=3)
     out, infos = run_ranks(P, inp, [np.arange(inp.n), np.arange(0)], [P.P2P_REDUNDANT])
