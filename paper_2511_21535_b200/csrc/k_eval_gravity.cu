@@ -236,6 +236,24 @@ struct Tgt<double, K> {
 // staging, no source split and no reduction -- the per-item overhead that dominates tiny boxes disappears.
 // Lanes of one warp are consecutive targets in Morton order, so lanes of the same box read the same
 // addresses (one L1 wavefront).  Same formula and rounding sequence as Tgt::interact.
+// shared-memory record load from a 32-bit shared address
+template <typename V4>
+__device__ __forceinline__ V4 lds_rec(uint32_t a);
+template <>
+__device__ __forceinline__ float4 lds_rec<float4>(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+                 : "memory");
+    return v;
+}
+template <>
+__device__ __forceinline__ double4 lds_rec<double4>(uint32_t a) {
+    double4 v;
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2+16];" : "=d"(v.z), "=d"(v.w) : "r"(a) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ float4 ldro(const float4 *p) { return __ldg(p); }
 __device__ __forceinline__ double4 ldro(const double4 *p) {
     const double2 a = __ldg(reinterpret_cast<const double2 *>(p)), b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
@@ -284,25 +302,31 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
         if (base >= n_small) break;
         const uint32_t i = base + lane;
         if (i < n_small) {
+        // lane = a PAIR of targets of one small box (the second may not exist: b_end), so the pair math is the
+        // same packed FP32x2 code as the item path (Tgt<T,2>), one broadcast source per step
         const uint32_t p = a.small_tgt[i], b = a.small_box[i];
+        const uint32_t b_end = a.bstart[b + 1];
+        const bool two = p + 1 < b_end;
         const uint32_t key = a.bkey[b];
         const uint32_t cc[3] = {compact3(key), compact3(key >> 1), compact3(key >> 2)};
         double org[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d)
             org[d] = (LAYOUT == P2P_INDEXED) ? frame_shift(a.g, cc, d) : __fma_rn((double)cc[d], a.g.h, a.g.lo[d]);
-        const V4 t = a.rec[p];
-        T tx, ty, tz;
-        if (LAYOUT == P2P_INDEXED) {
-            tx = t.x + (T)org[0];
-            ty = t.y + (T)org[1];
-            tz = t.z + (T)org[2];
-        } else {
-            tx = (T)__dsub_rn((double)t.x, org[0]);
-            ty = (T)__dsub_rn((double)t.y, org[1]);
-            tz = (T)__dsub_rn((double)t.z, org[2]);
+        Tgt<T, 2> tg;
+        tg.zero();
+        T tm[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const V4 t = a.rec[(k == 1 && two) ? p + 1 : p];
+            tm[k] = t.w;
+            if (LAYOUT == P2P_INDEXED)
+                tg.set(k, t.x + (T)org[0], t.y + (T)org[1], t.z + (T)org[2]);
+            else
+                tg.set(k, (T)__dsub_rn((double)t.x, org[0]), (T)__dsub_rn((double)t.y, org[1]),
+                       (T)__dsub_rn((double)t.z, org[2]));
         }
-        T ap = 0, ax = 0, ay = 0, az = 0;
+        const auto E = Tgt<T, 2>::eps_pack(eps2);
         if (LAYOUT == P2P_REDUNDANT) {
             const uint64_t r0 = a.red_off[b], r1 = a.red_off[b + 1];
             const V4 *run = a.red + r0;
@@ -311,10 +335,10 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
 #pragma unroll 1
             for (; j + 2 <= R; j += 2) {
                 const V4 s0 = ldro(run + j), s1 = ldro(run + j + 1);
-                interact1<T>(s0, tx, ty, tz, eps2, ap, ax, ay, az);
-                interact1<T>(s1, tx, ty, tz, eps2, ap, ax, ay, az);
+                tg.interact(s0, E);
+                tg.interact(s1, E);
             }
-            if (j < R) interact1<T>(ldro(run + j), tx, ty, tz, eps2, ap, ax, ay, az);
+            if (j < R) tg.interact(ldro(run + j), E);
         } else {
             const uint32_t e0 = a.nbr_off[b], e1 = a.nbr_off[b + 1];
             for (uint32_t e = e0; e < e1; ++e) {
@@ -331,7 +355,7 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
                         s.x += h0;
                         s.y += h1;
                         s.z += h2;
-                        interact1<T>(s, tx, ty, tz, eps2, ap, ax, ay, az);
+                        tg.interact(s, E);
                     }
                 } else {
                     for (uint32_t q = q0; q < q1; ++q) {
@@ -339,17 +363,24 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
                         s.x = (T)__dsub_rn(__dadd_rn((double)s.x, S0), org[0]);
                         s.y = (T)__dsub_rn(__dadd_rn((double)s.y, S1), org[1]);
                         s.z = (T)__dsub_rn(__dadd_rn((double)s.z, S2), org[2]);
-                        interact1<T>(s, tx, ty, tz, eps2, ap, ax, ay, az);
+                        tg.interact(s, E);
                     }
                 }
             }
         }
-        const uint32_t idx = a.perm[p];
-        a.phi[idx] = -(ap - t.w * Tgt<T, 2>::self_rinv(eps2));
-        if (a.field) {
-            a.field[3 * (size_t)idx + 0] = ax;
-            a.field[3 * (size_t)idx + 1] = ay;
-            a.field[3 * (size_t)idx + 2] = az;
+        const T rs = Tgt<T, 2>::self_rinv(eps2);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (k == 1 && !two) break;
+            T pot, fx, fy, fz;
+            tg.get(k, pot, fx, fy, fz);
+            const uint32_t idx = a.perm[p + k];
+            a.phi[idx] = -(pot - tm[k] * rs);
+            if (a.field) {
+                a.field[3 * (size_t)idx + 0] = fx;
+                a.field[3 * (size_t)idx + 1] = fy;
+                a.field[3 * (size_t)idx + 2] = fz;
+            }
         }
         }
     }
@@ -551,15 +582,17 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
                 // registers (no IMAD.MOV copies, which would occupy the FMA-heavy pipe the FFMA2s run on), and
                 // the addresses advance by pointer increments (ALU pipe) instead of IMAD
                 const uint32_t nj = (((cnt - 1 - sl) * m20) >> 20) + 1;
-                const V4 *sp = stg + sl;
-                const V4 *const end2 = sp + (size_t)(nj & ~1u) * S;
+                // 32-bit shared-memory byte addresses advanced with IADD (ALU pipe), not IMAD (FMA-heavy pipe)
+                const uint32_t stride = S * (uint32_t)sizeof(V4);
+                uint32_t sa = smem_u32(stg + sl);
+                const uint32_t end2 = sa + (nj & ~1u) * stride;
 #pragma unroll 1
-                for (; sp != end2; sp += 2 * S) {
-                    const V4 s0 = sp[0], s1 = sp[S];
+                for (; sa != end2; sa += 2 * stride) {
+                    const V4 s0 = lds_rec<V4>(sa), s1 = lds_rec<V4>(sa + stride);
                     tg.interact(s0, E);
                     tg.interact(s1, E);
                 }
-                if (nj & 1u) tg.interact(sp[0], E);
+                if (nj & 1u) tg.interact(lds_rec<V4>(sa), E);
             }
             __syncwarp();
             s ^= 1;

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
                 // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
                 const bool small = nb_b <= SMALL_NT && nk <= SMALL_R;
                 item_cnt[b] = (small || !target) ? 0u : item_chunks(nb_b, nk, tmax);
-                small_cnt[b] = small ? nb_b : 0u;
+                small_cnt[b] = small ? (nb_b + 1) / 2 : 0u;  // target PAIRS (eval small path)
                 pairs += (unsigned long long)nb_b * nk;
             }
         }
@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
             const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
             const uint32_t nch = item_cnt[b];
             if (nch == 0) {  // small box (k_nbr_count): thread-per-target path
-                if (lane < nb_b) {
-                    small_tgt[small_off[b] + lane] = s0 + lane;
+                if (lane < (nb_b + 1) / 2) {  // one entry per target pair
+                    small_tgt[small_off[b] + lane] = s0 + 2 * lane;
                     small_box[small_off[b] + lane] = b;
                 }
                 continue;
