@@ -1,0 +1,62 @@
+"""Helmholtz (DBIM-like, BASELINE configs[1]) timing: plan (one-off geometry), restructure (im2col Xg), eval
+REDUNDANT / INDEXED, as pair-interactions (complex MACs) per second and the FP32-pipe roofline (4 FFMA per
+complex MAC: peak = n_SM * 128 * f_max / 4).  Prints one JSON line per workload.
+usage: python scripts/bench_helmholtz.py [c2a|c2b ...]"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import p2p_inputs as G  # noqa: E402
+import paper_2511_21535_b200 as P  # noqa: E402
+
+
+def timed(fn, stream, reps=10):
+    flush = torch.empty(128 * 2**20, dtype=torch.float32, device="cuda")
+    ts = []
+    for _ in range(reps + 3):
+        flush.add_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts[3:]))
+
+
+def main():
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"sm_max_mhz": 1965.0, "hbm_gbs": 6650.0}
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    for wl in (sys.argv[1:] or ["c2a", "c2b"]):
+        inp = G.config(wl)
+        stream = torch.cuda.current_stream()
+        xr = torch.from_numpy(inp.x.view(np.float32).reshape(-1, 2)).cuda()
+        pos = torch.from_numpy(inp.pos).cuda()
+        y = torch.empty((inp.n, 2), dtype=torch.float32, device="cuda")
+        with P.Plan(P.P2P_HELMHOLTZ2D, pos, xr, inp.h, inp.lo, inp.nbox, 0, k=inp.k, t=inp.t) as plan:
+            t_rest = timed(plan.restructure, stream)
+            t_red = timed(lambda: plan.eval(P.P2P_REDUNDANT, y), stream)
+            t_idx = timed(lambda: plan.eval(P.P2P_INDEXED, y), stream)
+            info = plan.info
+        I = int(info.n_pairs)
+        peak = nsm * 128 * peaks["sm_max_mhz"] * 1e6 / 4
+        xg_bytes = int(info.n_red) * 8
+        out = {"workload": wl, "N": inp.n, "t": inp.t, "boxes": int(info.n_boxes), "pairs": I,
+               "restructure_ms": t_rest, "eval_redundant_ms": t_red, "eval_indexed_ms": t_idx,
+               "eval_pairs_per_s": I / (t_red * 1e-3), "eval_frac_fp32": I / (t_red * 1e-3) / peak,
+               "restructure_plus_eval_pairs_per_s": I / ((t_rest + t_red) * 1e-3),
+               "indexed_pairs_per_s": I / (t_idx * 1e-3),
+               "restructure_hbm_frac": (xg_bytes + inp.n * 8) / (t_rest * 1e-3) / (peaks["hbm_gbs"] * 1e9),
+               "peak_basis": f"{nsm} SM x 128 FP32 lanes x {peaks['sm_max_mhz']} MHz / 4 FFMA per complex MAC"}
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
