@@ -159,6 +159,101 @@ __global__ void k_eval_helm_generic(const typename C2T<T>::type *__restrict__ Pt
     }
 }
 
+// fp32 kernel with packed FP32x2 complex MACs: acc = (re, im); per complex MAC (a+ib)(c+id):
+//   acc = fma2((a, a), (c, d), acc); acc = fma2((-b, b), (d, c), acc)      -> 2 FFMA2 (4 lane-ops)
+// so the FP32 work issues in half the slots.  Shared tiles hold X as (c, d, d, c) and P as (a, a, -b, b) float4
+// so one LDS.128 yields both operand pairs.  Warp tile 32 boxes x 16 outputs, lane = (box group bg, output
+// group og), boxes bg + 8r / outputs og + 4r' interleaved (conflict-free LDS.128); CTA = 8 warps.
+// Rounding sequence per component identical to k_eval_helm_tiled (same two fmas in the same order).
+constexpr int HF_KT = 8;
+
+template <int LAYOUT, int TT>
+__global__ void __launch_bounds__(256) k_eval_helm_f2(const float2 *__restrict__ Pt, const float2 *__restrict__ Xg,
+                                                       const float2 *__restrict__ xs, const uint32_t *__restrict__ nbr9,
+                                                       const uint32_t *__restrict__ bstart,
+                                                       const uint32_t *__restrict__ perm, uint32_t B,
+                                                       float2 *__restrict__ y) {
+    constexpr int WO = TT / 16, WB = 8 / WO, BM = 32 * WB, KK = 9 * TT;
+    constexpr int RB = 4, RO = 4;
+    __shared__ float4 Xs[BM][HF_KT + 1];
+    __shared__ float4 Ps[TT][HF_KT + 1];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int wb = w / WO, wo = w % WO;
+    const int bg = lane >> 2, og = lane & 3;
+    const uint32_t b0 = blockIdx.x * BM;
+    float2 acc[RB][RO];
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+#pragma unroll
+        for (int j = 0; j < RO; ++j) acc[i][j] = make_float2(0.f, 0.f);
+
+    // register double buffering: the global loads of chunk m0 + KT are issued before chunk m0 is computed
+    constexpr int XE = BM * HF_KT / 256, PE = (TT * HF_KT + 255) / 256;
+    float2 xr[XE], pr[PE];
+    auto gload = [&](int m0) {
+#pragma unroll
+        for (int q = 0; q < XE; ++q) {
+            const int e = tid + 256 * q, bi = e / HF_KT, kk = e % HF_KT;
+            const uint32_t b = b0 + bi;
+            float2 v = make_float2(0.f, 0.f);
+            if (b < B) {
+                const int m = m0 + kk;
+                if (LAYOUT == P2P_REDUNDANT) {
+                    v = Xg[(size_t)b * KK + m];
+                } else {
+                    const uint32_t k = nbr9[(size_t)b * 9 + m / TT];
+                    if (k != 0xffffffffu) v = xs[bstart[k] + m % TT];
+                }
+            }
+            xr[q] = v;
+        }
+#pragma unroll
+        for (int q = 0; q < PE; ++q) {
+            const int e = tid + 256 * q;
+            if (e < TT * HF_KT) pr[q] = Pt[(size_t)(e / HF_KT) * KK + m0 + e % HF_KT];
+        }
+    };
+    gload(0);
+    for (int m0 = 0; m0 < KK; m0 += HF_KT) {
+#pragma unroll
+        for (int q = 0; q < XE; ++q) {
+            const int e = tid + 256 * q;
+            Xs[e / HF_KT][e % HF_KT] = make_float4(xr[q].x, xr[q].y, xr[q].y, xr[q].x);
+        }
+#pragma unroll
+        for (int q = 0; q < PE; ++q) {
+            const int e = tid + 256 * q;
+            if (e < TT * HF_KT) Ps[e / HF_KT][e % HF_KT] = make_float4(pr[q].x, pr[q].x, -pr[q].y, pr[q].y);
+        }
+        __syncthreads();
+        if (m0 + HF_KT < KK) gload(m0 + HF_KT);
+#pragma unroll
+        for (int kk = 0; kk < HF_KT; ++kk) {
+            float4 xv[RB], pv[RO];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) xv[r] = Xs[wb * 32 + bg + 8 * r][kk];
+#pragma unroll
+            for (int r = 0; r < RO; ++r) pv[r] = Ps[wo * 16 + og + 4 * r][kk];
+#pragma unroll
+            for (int i = 0; i < RB; ++i)
+#pragma unroll
+                for (int j = 0; j < RO; ++j) {
+                    acc[i][j] = __ffma2_rn(make_float2(pv[j].x, pv[j].y), make_float2(xv[i].x, xv[i].y), acc[i][j]);
+                    acc[i][j] = __ffma2_rn(make_float2(pv[j].z, pv[j].w), make_float2(xv[i].z, xv[i].w), acc[i][j]);
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+        const uint32_t b = b0 + wb * 32 + bg + 8 * i;
+        if (b >= B) continue;
+        const uint32_t s0 = bstart[b];
+#pragma unroll
+        for (int j = 0; j < RO; ++j) y[perm[s0 + wo * 16 + og + 4 * j]] = acc[i][j];
+    }
+}
+
 template <typename T, int LAYOUT>
 p2p_status launch_helm(p2p_plan *P, void *y) {
     using C2 = typename C2T<T>::type;
@@ -167,14 +262,12 @@ p2p_status launch_helm(p2p_plan *P, void *y) {
     bool done = false;
     if constexpr (sizeof(T) == 4) {
         if (t == 16) {
-            constexpr int TO = 16 / 4, BM = (HZ_THREADS / TO) * 4;
-            P2P_LAUNCH((k_eval_helm_tiled<T, LAYOUT, 16, 4, 4>), div_up(B, BM), HZ_THREADS, 0, P->stream, Pt, Xg, xs,
-                       P->nbr_box, P->bstart, P->perm, B, (C2 *)y);
+            P2P_LAUNCH((k_eval_helm_f2<LAYOUT, 16>), div_up(B, 256), 256, 0, P->stream, (const float2 *)Pt,
+                       (const float2 *)Xg, (const float2 *)xs, P->nbr_box, P->bstart, P->perm, B, (float2 *)y);
             done = true;
         } else if (t == 64) {
-            constexpr int TO = 64 / 4, BM = (HZ_THREADS / TO) * 4;
-            P2P_LAUNCH((k_eval_helm_tiled<T, LAYOUT, 64, 4, 4>), div_up(B, BM), HZ_THREADS, 0, P->stream, Pt, Xg, xs,
-                       P->nbr_box, P->bstart, P->perm, B, (C2 *)y);
+            P2P_LAUNCH((k_eval_helm_f2<LAYOUT, 64>), div_up(B, 64), 256, 0, P->stream, (const float2 *)Pt,
+                       (const float2 *)Xg, (const float2 *)xs, P->nbr_box, P->bstart, P->perm, B, (float2 *)y);
             done = true;
         }
     }
