@@ -415,20 +415,30 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
     uint64_t p_base = 0;
     uint32_t p_src = 0, p_st = 0, p_cnt = 0, p_slot = 0, p_ne = 0;  // INDEXED: lane = segment
 
-    auto fetch = [&]() -> uint32_t {
-        uint32_t v = 0;
-        if (lane == 0) v = atomicAdd(a.item_head, 1u);
-        return __shfl_sync(FULL, v, 0);
+    // work-queue pipeline, one item ahead at every level: the atomicAdd for item n+2 is issued while item n
+    // computes (consumed by shfl one item later), and item n+1's 32-byte Item record is already in registers
+    // when its first chunk is issued -- no dependent load on the per-item critical path (REDUNDANT)
+    uint32_t pend = 0;  // lane 0: result of the last issued atomicAdd
+    uint4 q0 = make_uint4(0, 0, 0, 0), q1 = make_uint4(0, 0, 0, 0);  // prefetched raw Item
+    auto fetch_issue = [&]() {
+        if (lane == 0) pend = atomicAdd(a.item_head, 1u);
     };
-    auto load_item = [&](uint32_t idx) {
-        const Item it = a.items[idx];
-        p_box = it.box;
-        p_t0 = it.t0;
-        p_meta = it.meta;
-        p_key = a.bkey[p_box];
+    auto fetch_take = [&]() -> uint32_t { return __shfl_sync(FULL, pend, 0); };
+    auto prefetch = [&](uint32_t idx) {
+        if (idx < n_items) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(a.items + idx);
+            q0 = __ldg(src);
+            q1 = __ldg(src + 1);
+        }
+    };
+    auto load_item = [&]() {
+        p_box = q0.x;
+        p_t0 = q0.y;
+        p_meta = q0.z;
+        p_key = q0.w;
         if (LAYOUT == P2P_REDUNDANT) {
-            p_base = a.red_off[p_box];
-            p_R = (uint32_t)(a.red_off[p_box + 1] - p_base);
+            p_base = (uint64_t)q1.x | ((uint64_t)q1.y << 32);
+            p_R = q1.z;
         } else {
             const uint32_t e0 = a.nbr_off[p_box];
             p_ne = a.nbr_off[p_box + 1] - e0;
@@ -471,11 +481,16 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
         if (chunk == 0 && lane == 31) bulk_g2s(dst + CH, a.rec + p_t0, nt * (uint32_t)sizeof(V4), &bar[s]);
     };
 
-    uint32_t cur = fetch();
-    if (cur < n_items) {
-    uint32_t nxt = fetch();  // one item ahead: the atomic's latency overlaps the current item
-    load_item(cur);
+    fetch_issue();
+    const uint32_t first = fetch_take();
+    if (first < n_items) {
+    prefetch(first);
+    fetch_issue();
+    load_item();
     issue(0, 0);
+    uint32_t nxt = fetch_take();
+    prefetch(nxt);
+    fetch_issue();
     int s = 0;
     uint32_t phases = 0u;  // bit s = parity of stage s's mbarrier
 
@@ -510,10 +525,11 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
             if (c + 1 < c_nch) {
                 issue(c + 1, s ^ 1);
             } else if (nxt < n_items) {
-                load_item(nxt);
+                load_item();
                 issue(0, s ^ 1);
-                cur = nxt;
-                nxt = fetch();
+                nxt = fetch_take();
+                prefetch(nxt);
+                fetch_issue();
             } else {
                 have_next = false;
             }

@@ -85,17 +85,30 @@ __global__ void k_bin_helmholtz(const T *__restrict__ pos, uint32_t n, Geom g, i
 }
 
 // ------------------------------------------------------------------------------------------------ a3
+// random gather (input order is arbitrary): 4 particles per thread iteration, all loads issued before the
+// stores (memory-level parallelism for the latency-bound gather)
 template <typename T, typename V4>
 __global__ void k_permute_gravity(const T *__restrict__ pos, int ps, const T *__restrict__ q, int qs,
                                   const uint32_t *__restrict__ perm, uint32_t n, V4 *__restrict__ rec) {
-    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-        uint32_t i = perm[p];
-        V4 r;
-        r.x = pos[(size_t)ps * i + 0];
-        r.y = pos[(size_t)ps * i + 1];
-        r.z = pos[(size_t)ps * i + 2];
-        r.w = q[(size_t)qs * i];
-        rec[p] = r;
+    constexpr int U = 4;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += U * stride) {
+        uint32_t i[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) i[u] = p0 + u * stride < n ? perm[p0 + u * stride] : 0u;
+        V4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (p0 + u * stride < n) {
+                r[u].x = pos[(size_t)ps * i[u] + 0];
+                r[u].y = pos[(size_t)ps * i[u] + 1];
+                r[u].z = pos[(size_t)ps * i[u] + 2];
+                r[u].w = q[(size_t)qs * i[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (p0 + u * stride < n) rec[p0 + u * stride] = r[u];
     }
 }
 
@@ -118,12 +131,14 @@ struct HeadPut {
     uint32_t div;
     uint32_t *bkey, *bstart, *box_of;
     uint32_t n;
+    uint32_t *occ = nullptr;  // optional occupancy bitmap of the key space (gravity)
     __device__ void operator()(uint64_t p, uint32_t e, uint32_t v) const {
         if (v) {
             uint32_t bk = skey[p] / div;
             bkey[e] = bk;
             bstart[e] = (uint32_t)p;
             box_of[bk] = e;
+            if (occ) atomicOr(&occ[bk >> 5], 1u << (bk & 31u));
         }
         if (p == n - 1) bstart[e + v] = n;
     }
@@ -152,19 +167,24 @@ __device__ __forceinline__ void decode3(uint32_t key, uint32_t c[3]) {
 
 // one warp per target box, lane = stencil slot (27 of 32 lanes): parallel box_of lookups, ballot-compacted
 // output in ascending slot order (C10)
-__device__ __forceinline__ bool lane_nbr(const Geom &g, const uint32_t c[3], unsigned lane, uint32_t B,
-                                         const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ box_of,
+// Emptiness is answered by the 2^key_bits-bit occupancy bitmap (2 MB for 256^3 boxes: L2/L1-resident), so
+// the common case of clustered inputs -- an empty neighbour -- costs one cached load; only non-empty neighbours
+// read the dense key -> box table (always valid for set bits: no validation load needed).
+__device__ __forceinline__ bool lane_nbr(const Geom &g, const uint32_t c[3], unsigned lane,
+                                         const uint32_t *__restrict__ occ, const uint32_t *__restrict__ box_of,
                                          uint32_t &k) {
     uint32_t nc[3];
     if (lane >= 27 || !stencil_nbr(g, c, (int)lane, nc)) return false;
     const uint32_t nk = spread3(nc[0]) | (spread3(nc[1]) << 1) | (spread3(nc[2]) << 2);
+    if (!((__ldg(&occ[nk >> 5]) >> (nk & 31u)) & 1u)) return false;
     k = box_of[nk];
-    return k < B && bkey[k] == nk;
+    return true;
 }
 
 __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__restrict__ bkey,
                                                    const uint32_t *__restrict__ bstart,
-                                                   const uint32_t *__restrict__ box_of, DevCounters *ctr,
+                                                   const uint32_t *__restrict__ box_of,
+                                                   const uint32_t *__restrict__ occ, DevCounters *ctr,
                                                    uint32_t *__restrict__ nbr_cnt, uint64_t *__restrict__ red_cnt,
                                                    uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ small_cnt,
                                                    uint32_t tmax) {
@@ -186,7 +206,7 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
                 uint32_t c[3];
                 decode3(key, c);
                 // non-target (multi-GPU halo) boxes get no neighbour list and no work
-                if (key >= g.tkey_lo && key <= g.tkey_hi) ok[u] = lane_nbr(g, c, lane, B, bkey, box_of, k[u]);
+                if (key >= g.tkey_lo && key <= g.tkey_hi) ok[u] = lane_nbr(g, c, lane, occ, box_of, k[u]);
             }
         }
 #pragma unroll
@@ -215,14 +235,15 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
 
 __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__restrict__ bkey,
                                                   const uint32_t *__restrict__ bstart,
-                                                  const uint32_t *__restrict__ box_of, const DevCounters *ctr,
+                                                  const uint32_t *__restrict__ box_of,
+                                                  const uint32_t *__restrict__ occ, const DevCounters *ctr,
                                                   const uint32_t *__restrict__ nbr_off,
                                                   const uint32_t *__restrict__ item_off,
                                                   const uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ nbr_box,
                                                   uint8_t *__restrict__ nbr_slot, Item *__restrict__ items,
                                                   const uint32_t *__restrict__ small_off,
                                                   uint32_t *__restrict__ small_tgt, uint32_t *__restrict__ small_box,
-                                                  uint32_t K) {
+                                                  const unsigned long long *__restrict__ red_off, uint32_t K) {
     const uint32_t B = ctr->B;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -239,7 +260,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
                 uint32_t c[3];
                 decode3(key, c);
                 // non-target (multi-GPU halo) boxes get no neighbour list and no work
-                if (key >= g.tkey_lo && key <= g.tkey_hi) ok[u] = lane_nbr(g, c, lane, B, bkey, box_of, k[u]);
+                if (key >= g.tkey_lo && key <= g.tkey_hi) ok[u] = lane_nbr(g, c, lane, occ, box_of, k[u]);
             }
         }
 #pragma unroll
@@ -264,12 +285,14 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
                 continue;
             }
             const uint32_t it = item_off[b];
+            const unsigned long long rb = red_off[b];
+            const uint32_t Rb = (uint32_t)(red_off[b + 1] - rb);
             for (uint32_t ci = lane; ci < nch; ci += 32) {
                 const uint32_t a0 = (uint32_t)(((uint64_t)nb_b * ci) / nch);
                 const uint32_t z0 = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
                 // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
                 const uint32_t nt = z0 - a0, G = (nt + K - 1) / K, S = 32u / G;
-                items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16)};
+                items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16), key, rb, Rb, 0u};
             }
         }
     }
@@ -348,7 +371,7 @@ void free_capacity(p2p_plan *P) {
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
                     P->s_nbr_cnt, P->s_item_cnt, P->s_item_off, P->s_red_cnt, P->s_small_cnt, P->s_small_off,
                     P->small_tgt, P->small_box, P->rec, P->bkey, P->bstart,
-                    P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items};
+                    P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
@@ -356,7 +379,7 @@ void free_capacity(p2p_plan *P) {
     P->s_small_cnt = P->s_small_off = P->small_tgt = P->small_box = nullptr;
     P->s_red_cnt = nullptr;
     P->rec = nullptr;
-    P->bkey = P->bstart = P->nbr_off = P->nbr_box = P->box_of = nullptr;
+    P->bkey = P->bstart = P->nbr_off = P->nbr_box = P->box_of = P->occ = nullptr;
     P->nbr_slot = nullptr;
     P->red_off = nullptr;
     P->items = nullptr;
@@ -385,6 +408,7 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     P2P_CUDA_TRY(dalloc((void **)&P->bkey, 4 * bcap, st));
     P2P_CUDA_TRY(dalloc((void **)&P->bstart, 4 * (bcap + 1), st));
     P2P_CUDA_TRY(dalloc((void **)&P->box_of, 4 * keyspace, st));
+    P2P_CUDA_TRY(dalloc((void **)&P->occ, 4 * std::max<uint64_t>(1, keyspace / 32), st));
     P2P_CUDA_TRY(dalloc((void **)&P->nbr_off, 4 * (bcap + 1), st));
     P2P_CUDA_TRY(dalloc((void **)&P->nbr_box, 4 * nslot * bcap, st));
     P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, (size_t)nslot * bcap, st));
@@ -436,13 +460,16 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
         P2P_LAUNCH((k_permute_gravity<float, float4>), gb, 256, 0, st, (const float *)pos, ps, (const float *)q, qs,
                    P->perm, n, (float4 *)P->rec);
     // a4
-    P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, 1u}, HeadPut{P->skey, 1u, P->bkey, P->bstart, P->box_of, n},
-                                       nullptr, n, &P->ctr->B, P->s_partials, st));
+    const uint64_t occ_words = std::max<uint64_t>(1, (1ull << P->key_bits) / 32);
+    P2P_CUDA_TRY(cudaMemsetAsync(P->occ, 0, 4 * occ_words, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, 1u},
+                                       HeadPut{P->skey, 1u, P->bkey, P->bstart, P->box_of, n, P->occ}, nullptr, n,
+                                       &P->ctr->B, P->s_partials, st));
     // a5
     const uint64_t bcap = (uint64_t)P->bcap;
     const unsigned gw = warp_grid(bcap, P->num_sms);
     const uint32_t tmax = ITEM_TMAX;
-    P2P_LAUNCH(k_nbr_count, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, P->s_nbr_cnt,
+    P2P_LAUNCH(k_nbr_count, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->occ, P->ctr, P->s_nbr_cnt,
                P->s_red_cnt, P->s_item_cnt, P->s_small_cnt, tmax);
     P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_nbr_cnt}, OffPut<uint32_t>{P->nbr_off, &P->ctr->B},
                                        &P->ctr->B, bcap, &P->ctr->n_nbr, P->s_partials, st));
@@ -454,9 +481,9 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
                                        &P->ctr->B, bcap, &P->ctr->n_items, P->s_partials, st));
     P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_small_cnt}, OffPut<uint32_t>{P->s_small_off, &P->ctr->B},
                                        &P->ctr->B, bcap, &P->ctr->n_small, P->s_partials, st));
-    P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->ctr, P->nbr_off,
+    P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->occ, P->ctr, P->nbr_off,
                P->s_item_off, P->s_item_cnt, P->nbr_box, P->nbr_slot, P->items, P->s_small_off, P->small_tgt,
-               P->small_box,
+               P->small_box, (const unsigned long long *)P->red_off,
                (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;

@@ -29,10 +29,16 @@ struct DevCounters {
 
 // eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
 // meta = n_t | S << 8 | G << 16: the warp lane layout (G groups of K targets x S source splits, G*S <= 32)
-struct Item {
+// key / red_base / R duplicate the box's Morton key and redundant run so the eval's one-item-ahead prefetch is a
+// single 32-byte load (no dependent loads on the critical path of tiny items)
+struct __align__(16) Item {
     uint32_t box;
     uint32_t t0;
     uint32_t meta;
+    uint32_t key;
+    unsigned long long red_base;
+    uint32_t R;
+    uint32_t pad;
 };
 constexpr int EVAL_K_F32 = 4;    // targets per lane in k_eval_gravity (fp32: two packed FP32x2 pairs)
 constexpr int EVAL_K_F64 = 2;
@@ -72,7 +78,8 @@ struct p2p_plan {
     uint32_t *nbr_off = nullptr, *nbr_box = nullptr;
     uint8_t *nbr_slot = nullptr;
     uint64_t *red_off = nullptr;
-    uint32_t *box_of = nullptr;  // dense Morton-key -> box lookup (validated by bkey, never cleared)
+    uint32_t *box_of = nullptr;  // dense Morton-key -> box lookup (gravity: valid where occ has the bit set)
+    uint32_t *occ = nullptr;     // gravity: occupancy bitmap of the key space (cleared every build)
     p2p::Item *items = nullptr;
     void *red = nullptr;         // gravity red[R] records; helmholtz Xg[B][9][t]
     void *table = nullptr;       // helmholtz pattern table P[t][9t] complex
