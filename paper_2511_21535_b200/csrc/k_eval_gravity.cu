@@ -172,6 +172,60 @@ struct Tgt<float, K> {
             }
         }
     }
+    // Transpose-reduce of the S source splits of a group (K = 4: 16 values per lane, f = 4 q + k with q = 0
+    // potential, 1..3 field, k = target): each level exchanges HALF of the remaining values with the partner
+    // split and keeps the other half, so log2(S) levels cost 8 + 4 + 2 + 1 shuffles instead of 16 per level.
+    // A non-power-of-two S first folds its tail splits [Sp, S) onto [0, S - Sp).  Afterwards split sl < Sp
+    // holds the cnt = 16 >> min(lg, 4) consecutive values f0 .. f0 + cnt - 1 in v[]; `own` marks the lanes
+    // whose values are final and unique.  Fixed exchange pattern -> deterministic.
+    template <int H>
+    static __device__ __forceinline__ void tr_level(float2 (&w)[8], uint32_t sl, uint32_t gbase, uint32_t o) {
+        const bool up = (sl & o) != 0u;
+        const uint32_t src = (gbase + (sl ^ o)) & 31u;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            const float2 snd = up ? w[i] : w[i + H];
+            const float2 kp = up ? w[i + H] : w[i];
+            const float2 r = make_float2(__shfl_sync(0xffffffffu, snd.x, src), __shfl_sync(0xffffffffu, snd.y, src));
+            w[i] = __fadd2_rn(kp, r);
+        }
+    }
+    __device__ __forceinline__ void treduce(uint32_t S, uint32_t sl, uint32_t gbase, float (&v)[4], uint32_t &f0,
+                                            uint32_t &cnt, bool &own) const {
+        static_assert(K == 4, "transpose-reduce is written for K = 4");
+        float2 w[8] = {ap[0], ap[1], ax[0], ax[1], ay[0], ay[1], az[0], az[1]};
+        uint32_t Sp = S;
+        if (S & (S - 1u)) {
+            Sp = 1u << (31 - __clz(S));
+            const uint32_t src = (gbase + sl + Sp) & 31u;
+            const bool take = sl + Sp < S;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float2 r = make_float2(__shfl_sync(0xffffffffu, w[i].x, src),
+                                             __shfl_sync(0xffffffffu, w[i].y, src));
+                if (take) w[i] = __fadd2_rn(w[i], r);
+            }
+        }
+        const uint32_t lg = 31u - __clz(Sp);  // S >= 4 (G <= 8) -> lg in 2..5
+        tr_level<4>(w, sl, gbase, Sp >> 1);
+        tr_level<2>(w, sl, gbase, Sp >> 2);
+        if (lg >= 3) tr_level<1>(w, sl, gbase, Sp >> 3);
+        if (lg >= 4) {
+            const uint32_t o = Sp >> 4;
+            const bool up = (sl & o) != 0u;
+            const float snd = up ? w[0].x : w[0].y, kp = up ? w[0].y : w[0].x;
+            w[0].x = kp + __shfl_sync(0xffffffffu, snd, (gbase + (sl ^ o)) & 31u);
+        }
+        if (lg == 5) w[0].x += __shfl_xor_sync(0xffffffffu, w[0].x, 1);
+        const uint32_t Lh = lg < 4u ? lg : 4u;
+        cnt = 16u >> Lh;
+        f0 = (sl >> (lg - Lh)) * cnt;
+        own = sl < Sp && (lg < 5u || (sl & 1u) == 0u);
+        v[0] = w[0].x;
+        v[1] = w[0].y;
+        v[2] = w[1].x;
+        v[3] = w[1].y;
+    }
     __device__ __forceinline__ void get(int k, float &p_, float &x, float &y, float &z) const {
         const int p = k >> 1;
         p_ = (k & 1) ? ap[p].y : ap[p].x;
@@ -411,7 +465,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
     const uint32_t n_items = *a.n_items;
 
     // ---------------- producer state (item whose chunks are being copied in) ----------------
-    uint32_t p_box = 0, p_t0 = 0, p_meta = 0, p_key = 0, p_R = 0, p_nch = 0;
+    uint32_t p_box = 0, p_t0 = 0, p_meta = 0, p_key = 0, p_R = 0, p_nch = 0, p_tofs = 0;
     uint64_t p_base = 0;
     uint32_t p_src = 0, p_st = 0, p_cnt = 0, p_slot = 0, p_ne = 0;  // INDEXED: lane = segment
 
@@ -439,6 +493,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
         if (LAYOUT == P2P_REDUNDANT) {
             p_base = (uint64_t)q1.x | ((uint64_t)q1.y << 32);
             p_R = q1.z;
+            p_tofs = q1.w;
         } else {
             const uint32_t e0 = a.nbr_off[p_box];
             p_ne = a.nbr_off[p_box + 1] - e0;
@@ -478,7 +533,10 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
             if (lane < p_ne && ov1 > ov0)
                 bulk_g2s(dst + (ov0 - c0), a.rec + p_src + (ov0 - p_st), (ov1 - ov0) * (uint32_t)sizeof(V4), &bar[s]);
         }
-        if (chunk == 0 && lane == 31) bulk_g2s(dst + CH, a.rec + p_t0, nt * (uint32_t)sizeof(V4), &bar[s]);
+        // targets: REDUNDANT takes them already rebased from the box's own segment of its run
+        if (chunk == 0 && lane == 31)
+            bulk_g2s(dst + CH, LAYOUT == P2P_REDUNDANT ? a.red + p_base + p_tofs : a.rec + p_t0,
+                     nt * (uint32_t)sizeof(V4), &bar[s]);
     };
 
     fetch_issue();
@@ -551,10 +609,14 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
                             x = r.x + (T)org[0];
                             y = r.y + (T)org[1];
                             z = r.z + (T)org[2];
-                        } else {
-                            x = (T)__dsub_rn((double)r.x, org[0]);
-                            y = (T)__dsub_rn((double)r.y, org[1]);
-                            z = (T)__dsub_rn((double)r.z, org[2]);
+                        } else if (LAYOUT == P2P_REDUNDANT) {
+                            x = r.x;
+                            y = r.y;
+                            z = r.z;
+                        } else {  // INDEXED_BITWISE: k_restructure's formula with S = 0
+                            x = (T)__dsub_rn(__dadd_rn((double)r.x, 0.0), org[0]);
+                            y = (T)__dsub_rn(__dadd_rn((double)r.y, 0.0), org[1]);
+                            z = (T)__dsub_rn(__dadd_rn((double)r.z, 0.0), org[2]);
                         }
                     }
                     tg.set(k, x, y, z);
@@ -614,9 +676,31 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
             s ^= 1;
         }
 
-        // ---- combine the S source splits of each group (fixed shuffle tree -> deterministic) ----
-        tg.reduce(S, sl);
+        // ---- combine the S source splits of each group (fixed shuffle pattern -> deterministic) and
         // ---- a9: scatter to input order; remove the self potential term (DESIGN C3) ----
+        if constexpr (sizeof(T) == 4) {
+            float v[4];
+            uint32_t f0, vcnt;
+            bool own;
+            tg.treduce(S, sl, g * S, v, f0, vcnt, own);
+            if (active && own) {
+                const T rs = Tgt<T, K>::self_rinv(eps2);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t f = f0 + j, q = f >> 2, k = f & 3u, ti = g * K + k;
+                    if ((uint32_t)j < vcnt && ti < nt) {
+                        const uint32_t i = a.perm[c_t0 + ti];
+                        if (q == 0) {
+                            const T mk = k == 0 ? tm[0] : (k == 1 ? tm[1] : (k == 2 ? tm[2] : tm[3]));
+                            a.phi[i] = -(v[j] - mk * rs);
+                        } else if (a.field) {
+                            a.field[3 * (size_t)i + (q - 1)] = v[j];
+                        }
+                    }
+                }
+            }
+        } else {
+        tg.reduce(S, sl);
         if (active && sl == 0) {
             const T rs = Tgt<T, K>::self_rinv(eps2);
 #pragma unroll
@@ -634,6 +718,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
                     }
                 }
             }
+        }
         }
         if (!have_next) break;
     }

@@ -268,6 +268,9 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
             const uint32_t b = b0 + u;
             const uint32_t m = __ballot_sync(0xffffffffu, ok[u]);
             if (b >= B) continue;
+            // records of the slots before the centre (13) = offset of the box's own segment in its run
+            const uint32_t pre = (ok[u] && lane < 13) ? bstart[k[u] + 1] - bstart[k[u]] : 0u;
+            const uint32_t cen = __reduce_add_sync(0xffffffffu, pre);
             if (ok[u]) {
                 const uint32_t e = nbr_off[b] + __popc(m & ((1u << lane) - 1u));
                 nbr_box[e] = k[u];
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
                 const uint32_t z0 = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
                 // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
                 const uint32_t nt = z0 - a0, G = (nt + K - 1) / K, S = 32u / G;
-                items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16), key, rb, Rb, 0u};
+                items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16), key, rb, Rb, cen + a0};
             }
         }
     }

@@ -30,7 +30,9 @@ struct DevCounters {
 // eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
 // meta = n_t | S << 8 | G << 16: the warp lane layout (G groups of K targets x S source splits, G*S <= 32)
 // key / red_base / R duplicate the box's Morton key and redundant run so the eval's one-item-ahead prefetch is a
-// single 32-byte load (no dependent loads on the critical path of tiny items)
+// single 32-byte load (no dependent loads on the critical path of tiny items).  tofs = offset of the item's
+// first target inside the run (the box's own slot-13 segment + the item's target offset): the REDUNDANT eval
+// stages its targets already rebased from red[] instead of re-deriving them in fp64.
 struct __align__(16) Item {
     uint32_t box;
     uint32_t t0;
@@ -38,7 +40,7 @@ struct __align__(16) Item {
     uint32_t key;
     unsigned long long red_base;
     uint32_t R;
-    uint32_t pad;
+    uint32_t tofs;
 };
 constexpr int EVAL_K_F32 = 4;    // targets per lane in k_eval_gravity (fp32: two packed FP32x2 pairs)
 constexpr int EVAL_K_F64 = 2;
