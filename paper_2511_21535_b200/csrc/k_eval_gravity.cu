@@ -146,7 +146,7 @@ struct Tgt<float, K> {
             const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
             const float2 mri = __fmul2_rn(bc(s.w), ri);
             ap[p] = __fadd2_rn(ap[p], mri);
-            const float2 m3 = __fmul2_rn(__fmul2_rn(mri, ri), ri);
+            const float2 m3 = __fmul2_rn(mri, __fmul2_rn(ri, ri));  // ri*ri in parallel with m*ri: one FMUL shorter chain
             ax[p] = __ffma2_rn(m3, dx, ax[p]);
             ay[p] = __ffma2_rn(m3, dy, ay[p]);
             az[p] = __ffma2_rn(m3, dz, az[p]);
@@ -260,7 +260,7 @@ struct Tgt<double, K> {
             const double ri = 1.0 / sqrt(r2);
             const double mri = s.w * ri;
             ap[k] += mri;
-            const double m3 = mri * ri * ri;
+            const double m3 = mri * (ri * ri);
             ax[k] = __fma_rn(m3, dx, ax[k]);
             ay[k] = __fma_rn(m3, dy, ay[k]);
             az[k] = __fma_rn(m3, dz, az[k]);
@@ -325,7 +325,7 @@ __device__ __forceinline__ void interact1(const typename V4T<T>::type &s, T tx, 
         const float ri = rsqrt_ftz(r2);
         const float mri = __fmul_rn(s.w, ri);
         ap = __fadd_rn(ap, mri);
-        const float m3 = __fmul_rn(__fmul_rn(mri, ri), ri);
+        const float m3 = __fmul_rn(mri, __fmul_rn(ri, ri));
         ax = __fmaf_rn(m3, dx, ax);
         ay = __fmaf_rn(m3, dy, ay);
         az = __fmaf_rn(m3, dz, az);
@@ -337,7 +337,7 @@ __device__ __forceinline__ void interact1(const typename V4T<T>::type &s, T tx, 
         const double ri = 1.0 / sqrt(r2);
         const double mri = __dmul_rn(s.w, ri);
         ap = __dadd_rn(ap, mri);
-        const double m3 = __dmul_rn(__dmul_rn(mri, ri), ri);
+        const double m3 = __dmul_rn(mri, __dmul_rn(ri, ri));
         ax = __fma_rn(m3, dx, ax);
         ay = __fma_rn(m3, dy, ay);
         az = __fma_rn(m3, dz, az);
