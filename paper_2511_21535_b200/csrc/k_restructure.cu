@@ -6,8 +6,13 @@
 // records into ONE contiguous run red[red_off[b] ..), rebased to b's origin in fp64 with a single
 // rounding to the working precision (DESIGN C11):
 //     red = { fl_p(((double)x_j + S_x) - o_bx), ..y.., ..z.., m_j },  o_bd = fma(ib_d, h, lo_d)
-// One warp per box; the warp's 32 lanes cover the run's records contiguously (coalesced 16 B stores), each
-// lane finding its source segment by a shuffle binary search over the <= 27 segment starts held in lanes.
+// One warp per CHUNK of 32 consecutive CSR entries (not per box): the entries' segments are consecutive in
+// red[] (CSR order = run order, and runs of consecutive boxes are adjacent), so a chunk is one contiguous output
+// range even when it spans several small boxes.  k_nbr_fill records each chunk's owner box and output start.
+// Three dependent load levels per chunk (entry -> segment / owner box -> records) instead of four per box, and
+// no per-box idle lanes: the Plummer workloads' median box has R ~ 20 records.  The 32 lanes cover the range
+// contiguously (coalesced 16 B stores), each lane finding its segment from a ballot / OR-reduce over the
+// segment starts held in lanes.
 // Bound: HBM -- writes 16 R bytes (fp32), reads 16 N_src bytes compulsory (repeats hit L2 in Morton order).
 //
 // Helmholtz: Xg[b][s][j] = xs[bstart[nbr9[b][s]] + j] or 0 (zero-padded im2col, DESIGN C10), one thread
@@ -37,79 +42,115 @@ __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const
                                                              const uint32_t *__restrict__ nbr_off,
                                                              const uint32_t *__restrict__ nbr_box,
                                                              const uint8_t *__restrict__ nbr_slot,
-                                                             const uint64_t *__restrict__ red_off,
+                                                             const uint32_t *__restrict__ chunk_box,
+                                                             const unsigned long long *__restrict__ chunk_out,
                                                              const DevCounters *__restrict__ ctr,
                                                              typename V4T<T>::type *__restrict__ red) {
     using V4 = typename V4T<T>::type;
-    const uint32_t B = ctr->B;  // device-side count: no host sync needed after an async p2p_plan_update
+    constexpr unsigned FULL = 0xffffffffu;
+    // device-side counts: no host sync needed after an asynchronous p2p_plan_update
+    const uint32_t B = ctr->B, n_nbr = ctr->n_nbr;
+    const uint32_t nchunk = (n_nbr + 31u) >> 5;
     const unsigned lane = threadIdx.x & 31u;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nwarps) {
-        const uint32_t key = bkey[b];
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const double L0 = g.L[0], L1 = g.L[1], L2 = g.L[2];
+    for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunk; ch += nw) {
+        // ---- level 1: the chunk head and lane e's CSR entry ----
+        const uint32_t e = (ch << 5) + lane;
+        const bool seg = e < n_nbr;
+        const uint32_t b0 = chunk_box[ch];
+        const unsigned long long gout = chunk_out[ch];
+        uint32_t k = 0, slot = 13;
+        if (seg) {
+            k = nbr_box[e];
+            slot = nbr_slot[e];
+        }
+        // ---- level 2: boxes b0 .. b0 + 31 (CSR starts, keys) and lane e's source segment ----
+        const uint32_t bl = b0 + lane;
+        uint32_t boff = 0xffffffffu, keyl = 0;
+        if (bl < B) {
+            boff = nbr_off[bl];
+            keyl = bkey[bl];
+        }
+        uint32_t src = 0, cnt = 0;
+        if (seg) {
+            src = bstart[k];
+            cnt = bstart[k + 1] - src;
+        }
+        // owner of entry e: the largest i with nbr_off[b0 + i] <= e (non-decreasing in i; every target box owns
+        // >= 1 entry, so the chunk's <= 32 entries belong to boxes b0 .. b0 + 31)
+        uint32_t i = 0;
+#pragma unroll
+        for (uint32_t step = 16; step > 0; step >>= 1) {
+            const uint32_t t = __shfl_sync(FULL, boff, i + step);
+            if (t <= e) i += step;
+        }
+        const uint32_t key = __shfl_sync(FULL, keyl, i);
         const uint32_t c[3] = {compact3(key), compact3(key >> 1), compact3(key >> 2)};
         const double o0 = __fma_rn((double)c[0], g.h, g.lo[0]);
         const double o1 = __fma_rn((double)c[1], g.h, g.lo[1]);
         const double o2 = __fma_rn((double)c[2], g.h, g.lo[2]);
-        const uint32_t e0 = nbr_off[b], ne = nbr_off[b + 1] - e0;
-        // lane e < ne holds segment e: source start, length, and the image code of its slot
-        // (2 bits per dim: 1 = +L, 2 = -L, computed once per segment instead of once per record)
-        uint32_t src = 0, cnt = 0, code = 0;
-        if (lane < ne) {
-            const uint32_t k = nbr_box[e0 + lane];
-            src = bstart[k];
-            cnt = bstart[k + 1] - src;
-            const int slot = nbr_slot[e0 + lane];
+        // image code of the entry's slot (2 bits per dim: 1 = +L, 2 = -L), once per segment
+        uint32_t code = 0;
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const double S = slot_shift(g, c, slot, d);
-                code |= (S > 0.0 ? 1u : (S < 0.0 ? 2u : 0u)) << (2 * d);
-            }
+        for (int d = 0; d < 3; ++d) {
+            const double S = slot_shift(g, c, (int)slot, d);
+            code |= (S > 0.0 ? 1u : (S < 0.0 ? 2u : 0u)) << (2 * d);
         }
+        // segments of consecutive CSR entries are consecutive in red[]: one contiguous output range per chunk
         uint32_t incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
             if (lane >= (unsigned)o) incl += y;
         }
         const uint32_t st = incl - cnt;
-        const uint32_t Rb = __shfl_sync(0xffffffffu, incl, 31);
-        V4 *__restrict__ out = red + red_off[b];
-        const bool seg = lane < ne;
-        const uint32_t le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-        // UNR windows of 32 records per iteration: all loads issued before the first store (memory-level
-        // parallelism: the kernel is latency-bound otherwise)
+        const uint32_t Rc = __shfl_sync(FULL, incl, 31);
+        V4 *__restrict__ out = red + gout;
+        const uint32_t le = lane == 31 ? FULL : ((2u << lane) - 1u);
+        // ---- level 3: UNR windows of 32 records per iteration, all loads issued before the first store ----
+        // chunks without any periodic image (all but the boundary layers) skip the shift selection: adding the
+        // +0.0 shift keeps the oracle's rounding sequence (and its -0 -> +0 behaviour) exactly
+        const bool wrap = __any_sync(FULL, seg && code != 0u);
         constexpr int UNR = 4;
-        for (uint32_t rb = 0; rb < Rb; rb += 32 * UNR) {
+        for (uint32_t rb = 0; rb < Rc; rb += 32 * UNR) {
             V4 x[UNR];
-            uint32_t xcode[UNR];
+            uint32_t xe[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 const uint32_t r0 = rb + 32u * u;
-                if (r0 >= Rb) break;  // warp-uniform: short runs skip the empty windows
+                if (r0 >= Rc) break;  // warp-uniform: short ranges skip the empty windows
                 // segment of record r0 + lane without a search (segments are non-empty and contiguous):
                 // segments starting before r0 (ballot) - 1 + segment starts in [r0, r0 + lane] (OR-reduced mask)
-                const uint32_t before = __popc(__ballot_sync(0xffffffffu, seg && st < r0));
+                const uint32_t before = __popc(__ballot_sync(FULL, seg && st < r0));
                 const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
-                const uint32_t starts = __reduce_or_sync(0xffffffffu, in_win);
-                const uint32_t e = (before - 1u + __popc(starts & le)) & 31u;
-                const uint32_t e_src = __shfl_sync(0xffffffffu, src, e);
-                const uint32_t e_st = __shfl_sync(0xffffffffu, st, e);
-                xcode[u] = __shfl_sync(0xffffffffu, code, e);
+                const uint32_t starts = __reduce_or_sync(FULL, in_win);
+                xe[u] = (before - 1u + __popc(starts & le)) & 31u;
+                const uint32_t e_src = __shfl_sync(FULL, src, xe[u]);
+                const uint32_t e_st = __shfl_sync(FULL, st, xe[u]);
                 const uint32_t r = r0 + lane;
-                if (r < Rb) x[u] = rec[e_src + (r - e_st)];
+                if (r < Rc) x[u] = rec[e_src + (r - e_st)];
             }
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
-                const uint32_t r = rb + 32u * u + lane;
-                if (r < Rb) {
-                    const uint32_t cd = xcode[u];
-                    const double S0 = (cd & 1u) ? g.L[0] : ((cd & 2u) ? -g.L[0] : 0.0);
-                    const double S1 = (cd & 4u) ? g.L[1] : ((cd & 8u) ? -g.L[1] : 0.0);
-                    const double S2 = (cd & 16u) ? g.L[2] : ((cd & 32u) ? -g.L[2] : 0.0);
+                const uint32_t r0 = rb + 32u * u;
+                if (r0 >= Rc) break;
+                const double eo0 = __shfl_sync(FULL, o0, xe[u]);
+                const double eo1 = __shfl_sync(FULL, o1, xe[u]);
+                const double eo2 = __shfl_sync(FULL, o2, xe[u]);
+                double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+                if (wrap) {
+                    const uint32_t cd = __shfl_sync(FULL, code, xe[u]);
+                    S0 = (cd & 1u) ? L0 : ((cd & 2u) ? -L0 : 0.0);
+                    S1 = (cd & 4u) ? L1 : ((cd & 8u) ? -L1 : 0.0);
+                    S2 = (cd & 16u) ? L2 : ((cd & 32u) ? -L2 : 0.0);
+                }
+                const uint32_t r = r0 + lane;
+                if (r < Rc) {
                     V4 v;
-                    v.x = (T)__dsub_rn(__dadd_rn((double)x[u].x, S0), o0);
-                    v.y = (T)__dsub_rn(__dadd_rn((double)x[u].y, S1), o1);
-                    v.z = (T)__dsub_rn(__dadd_rn((double)x[u].z, S2), o2);
+                    v.x = (T)__dsub_rn(__dadd_rn((double)x[u].x, S0), eo0);
+                    v.y = (T)__dsub_rn(__dadd_rn((double)x[u].y, S1), eo1);
+                    v.z = (T)__dsub_rn(__dadd_rn((double)x[u].z, S2), eo2);
                     v.w = x[u].w;
                     out[r] = v;
                 }
@@ -137,15 +178,18 @@ __global__ void k_restructure_helmholtz(const C2 *__restrict__ xs, const uint32_
 }  // namespace
 
 p2p_status restructure_gravity(p2p_plan *P) {
-    if (P->sizes_known && P->B == 0) return P2P_OK;
-    const uint64_t nb = P->sizes_known ? (uint64_t)P->B : (uint64_t)P->bcap;
-    const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(div_up(nb * 32, 256), (unsigned)P->num_sms * 16));
+    if (P->sizes_known && (P->B == 0 || P->n_nbr == 0)) return P2P_OK;
+    // one warp per chunk of 32 CSR entries; the chunk count is device-side after an asynchronous update
+    const uint64_t nchunk = div_up(P->sizes_known ? (uint64_t)P->n_nbr : 27ull * (uint64_t)P->bcap, 32);
+    const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(div_up(nchunk * 32, 256), (unsigned)P->num_sms * 16));
     if (P->cfg.precision == P2P_FP64)
         P2P_LAUNCH(k_restructure_gravity<double>, grid, 256, 0, P->stream, P->geom, (const double4 *)P->rec, P->bkey,
-                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->ctr, (double4 *)P->red);
+                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
+                   (double4 *)P->red);
     else
         P2P_LAUNCH(k_restructure_gravity<float>, grid, 256, 0, P->stream, P->geom, (const float4 *)P->rec, P->bkey,
-                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->ctr, (float4 *)P->red);
+                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
+                   (float4 *)P->red);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }

@@ -243,7 +243,9 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
                                                   uint8_t *__restrict__ nbr_slot, Item *__restrict__ items,
                                                   const uint32_t *__restrict__ small_off,
                                                   uint32_t *__restrict__ small_tgt, uint32_t *__restrict__ small_box,
-                                                  const unsigned long long *__restrict__ red_off, uint32_t K) {
+                                                  const unsigned long long *__restrict__ red_off,
+                                                  uint32_t *__restrict__ chunk_box,
+                                                  unsigned long long *__restrict__ chunk_out, uint32_t K) {
     const uint32_t B = ctr->B;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -268,13 +270,24 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
             const uint32_t b = b0 + u;
             const uint32_t m = __ballot_sync(0xffffffffu, ok[u]);
             if (b >= B) continue;
+            // segment lengths in slot (= CSR) order; exclusive prefix = segment offset inside the box's run
+            const uint32_t cnt_l = ok[u] ? bstart[k[u] + 1] - bstart[k[u]] : 0u;
+            uint32_t incl = cnt_l;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (unsigned)o) incl += y;
+            }
             // records of the slots before the centre (13) = offset of the box's own segment in its run
-            const uint32_t pre = (ok[u] && lane < 13) ? bstart[k[u] + 1] - bstart[k[u]] : 0u;
-            const uint32_t cen = __reduce_add_sync(0xffffffffu, pre);
+            const uint32_t cen = __shfl_sync(0xffffffffu, incl - cnt_l, 13);
             if (ok[u]) {
                 const uint32_t e = nbr_off[b] + __popc(m & ((1u << lane) - 1u));
                 nbr_box[e] = k[u];
                 nbr_slot[e] = (uint8_t)lane;
+                if ((e & 31u) == 0u) {  // head of a restructure chunk
+                    chunk_box[e >> 5] = b;
+                    chunk_out[e >> 5] = red_off[b] + (incl - cnt_l);
+                }
             }
             const uint32_t key = bkey[b];
             if (key < g.tkey_lo || key > g.tkey_hi) continue;  // halo box: source only
@@ -373,13 +386,14 @@ void free_capacity(p2p_plan *P) {
     cudaStream_t st = P->stream;
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
                     P->s_nbr_cnt, P->s_item_cnt, P->s_item_off, P->s_red_cnt, P->s_small_cnt, P->s_small_off,
-                    P->small_tgt, P->small_box, P->rec, P->bkey, P->bstart,
+                    P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, P->rec, P->bkey, P->bstart,
                     P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
     P->s_nbr_cnt = P->s_item_cnt = P->s_item_off = nullptr;
-    P->s_small_cnt = P->s_small_off = P->small_tgt = P->small_box = nullptr;
+    P->s_small_cnt = P->s_small_off = P->small_tgt = P->small_box = P->chunk_box = nullptr;
+    P->chunk_out = nullptr;
     P->s_red_cnt = nullptr;
     P->rec = nullptr;
     P->bkey = P->bstart = P->nbr_off = P->nbr_box = P->box_of = P->occ = nullptr;
@@ -427,6 +441,9 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
         P2P_CUDA_TRY(dalloc((void **)&P->s_red_cnt, 8 * bcap, st));
         P2P_CUDA_TRY(dalloc((void **)&P->red_off, 8 * (bcap + 1), st));
         P2P_CUDA_TRY(dalloc((void **)&P->items, sizeof(Item) * n, st));
+        const uint64_t nchunk = div_up((uint64_t)nslot * bcap, 32) + 1;
+        P2P_CUDA_TRY(dalloc((void **)&P->chunk_box, 4 * nchunk, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->chunk_out, 8 * nchunk, st));
     } else {
         P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double2) : sizeof(float2)) * n, st));
     }
@@ -486,7 +503,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
                                        &P->ctr->B, bcap, &P->ctr->n_small, P->s_partials, st));
     P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->occ, P->ctr, P->nbr_off,
                P->s_item_off, P->s_item_cnt, P->nbr_box, P->nbr_slot, P->items, P->s_small_off, P->small_tgt,
-               P->small_box, (const unsigned long long *)P->red_off,
+               P->small_box, (const unsigned long long *)P->red_off, P->chunk_box, P->chunk_out,
                (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;

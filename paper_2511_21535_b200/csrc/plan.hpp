@@ -94,6 +94,10 @@ struct p2p_plan {
     uint32_t *s_nbr_cnt = nullptr, *s_item_cnt = nullptr, *s_item_off = nullptr;
     uint32_t *s_small_cnt = nullptr, *s_small_off = nullptr;
     uint32_t *small_tgt = nullptr, *small_box = nullptr;  // sorted target index / its box, small boxes only
+    // restructure chunks: every 32 consecutive CSR entries e = 32 c .. 32 c + 31 form one chunk; their redundant
+    // segments are one contiguous range of red[] starting at chunk_out[c]; chunk_box[c] = box owning entry 32 c
+    uint32_t *chunk_box = nullptr;
+    unsigned long long *chunk_out = nullptr;
     uint64_t *s_red_cnt = nullptr;
     bool sizes_known = false;  // host copies of B, n_nbr, R, I, n_items valid (false after an async update)
     // ---- multi-GPU: this rank owns the target boxes of one contiguous Morton range ----
