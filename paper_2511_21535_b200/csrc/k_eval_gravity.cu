@@ -386,13 +386,17 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
             const V4 *run = a.red + r0;
             const uint32_t R = (uint32_t)(r1 - r0);
             uint32_t j = 0;
+            // four loads in flight per lane (the path is L1/L2-latency bound, not FP32 bound)
 #pragma unroll 1
-            for (; j + 2 <= R; j += 2) {
-                const V4 s0 = ldro(run + j), s1 = ldro(run + j + 1);
+            for (; j + 4 <= R; j += 4) {
+                const V4 s0 = ldro(run + j), s1 = ldro(run + j + 1), s2 = ldro(run + j + 2), s3 = ldro(run + j + 3);
                 tg.interact(s0, E);
                 tg.interact(s1, E);
+                tg.interact(s2, E);
+                tg.interact(s3, E);
             }
-            if (j < R) tg.interact(ldro(run + j), E);
+#pragma unroll 1
+            for (; j < R; ++j) tg.interact(ldro(run + j), E);
         } else {
             const uint32_t e0 = a.nbr_off[b], e1 = a.nbr_off[b + 1];
             for (uint32_t e = e0; e < e1; ++e) {
