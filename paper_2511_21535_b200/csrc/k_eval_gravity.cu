@@ -42,6 +42,7 @@ template <> struct V4T<double> { using type = double4; };
 constexpr int EV_WARPS = 4;              // warps per CTA
 constexpr int EV_STAGE_BYTES = 4096;     // source records per pipeline stage per warp (256 fp32 / 128 fp64)
 constexpr int EV_TGT = 32;               // max targets per item (ITEM_TMAX in k_structs.cu)
+constexpr int EV_BATCH = 2;              // work items claimed per queue atomic
 
 // ceil(2^20 / S) for S = 0..32: x / S == (x * M20[S]) >> 20 exactly for x < 2^11 (no integer division)
 __constant__ uint32_t c_m20[33] = {0,       1048576, 524288, 349526, 262144, 209716, 174763, 149797, 131072,
@@ -473,15 +474,21 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
     uint64_t p_base = 0;
     uint32_t p_src = 0, p_st = 0, p_cnt = 0, p_slot = 0, p_ne = 0;  // INDEXED: lane = segment
 
-    // work-queue pipeline, one item ahead at every level: the atomicAdd for item n+2 is issued while item n
-    // computes (consumed by shfl one item later), and item n+1's 32-byte Item record is already in registers
-    // when its first chunk is issued -- no dependent load on the per-item critical path (REDUNDANT)
+    // work-queue pipeline: each atomicAdd claims EV_BATCH consecutive items (fewer atomics on the one queue
+    // counter) and its result is consumed by shfl a whole batch later; item n+1's 32-byte Item record is already
+    // in registers when its first chunk is issued -- no dependent load on the per-item critical path (REDUNDANT)
     uint32_t pend = 0;  // lane 0: result of the last issued atomicAdd
+    uint32_t nb_idx = 0, nb_left = 0;
     uint4 q0 = make_uint4(0, 0, 0, 0), q1 = make_uint4(0, 0, 0, 0);  // prefetched raw Item
-    auto fetch_issue = [&]() {
-        if (lane == 0) pend = atomicAdd(a.item_head, 1u);
+    auto next_index = [&]() -> uint32_t {
+        if (nb_left == 0) {
+            nb_idx = __shfl_sync(FULL, pend, 0);
+            nb_left = EV_BATCH;
+            if (lane == 0) pend = atomicAdd(a.item_head, (uint32_t)EV_BATCH);
+        }
+        --nb_left;
+        return nb_idx++;
     };
-    auto fetch_take = [&]() -> uint32_t { return __shfl_sync(FULL, pend, 0); };
     auto prefetch = [&](uint32_t idx) {
         if (idx < n_items) {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.items + idx);
@@ -543,16 +550,14 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
                      nt * (uint32_t)sizeof(V4), &bar[s]);
     };
 
-    fetch_issue();
-    const uint32_t first = fetch_take();
+    if (lane == 0) pend = atomicAdd(a.item_head, (uint32_t)EV_BATCH);
+    const uint32_t first = next_index();
     if (first < n_items) {
     prefetch(first);
-    fetch_issue();
     load_item();
     issue(0, 0);
-    uint32_t nxt = fetch_take();
+    uint32_t nxt = next_index();
     prefetch(nxt);
-    fetch_issue();
     int s = 0;
     uint32_t phases = 0u;  // bit s = parity of stage s's mbarrier
 
@@ -589,9 +594,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
             } else if (nxt < n_items) {
                 load_item();
                 issue(0, s ^ 1);
-                nxt = fetch_take();
+                nxt = next_index();
                 prefetch(nxt);
-                fetch_issue();
             } else {
                 have_next = false;
             }
