@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
                                                    const uint32_t *__restrict__ occ, DevCounters *ctr,
                                                    uint32_t *__restrict__ nbr_cnt, uint64_t *__restrict__ red_cnt,
                                                    uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ small_cnt,
-                                                   uint32_t tmax) {
+                                                   uint32_t *__restrict__ slot_box, uint32_t tmax) {
     const uint32_t B = ctr->B;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
             const uint32_t b = b0 + u;
+            if (b < B && lane < 27) slot_box[27 * (size_t)b + lane] = ok[u] ? k[u] : 0xffffffffu;
             uint32_t nk = ok[u] ? bstart[k[u] + 1] - bstart[k[u]] : 0u;
             const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, ok[u]));
 #pragma unroll
@@ -235,8 +236,7 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
 
 __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__restrict__ bkey,
                                                   const uint32_t *__restrict__ bstart,
-                                                  const uint32_t *__restrict__ box_of,
-                                                  const uint32_t *__restrict__ occ, const DevCounters *ctr,
+                                                  const uint32_t *__restrict__ slot_box, const DevCounters *ctr,
                                                   const uint32_t *__restrict__ nbr_off,
                                                   const uint32_t *__restrict__ item_off,
                                                   const uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ nbr_box,
@@ -255,15 +255,9 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
         uint32_t k[NB];
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
-            ok[u] = false;
-            k[u] = 0;
-            if (b0 + u < B) {
-                const uint32_t key = bkey[b0 + u];
-                uint32_t c[3];
-                decode3(key, c);
-                // non-target (multi-GPU halo) boxes get no neighbour list and no work
-                if (key >= g.tkey_lo && key <= g.tkey_hi) ok[u] = lane_nbr(g, c, lane, occ, box_of, k[u]);
-            }
+            // k_nbr_count's slot table (halo boxes: all ~0u, no neighbour list and no work)
+            k[u] = (b0 + u < B && lane < 27) ? slot_box[27 * (size_t)(b0 + u) + lane] : 0xffffffffu;
+            ok[u] = k[u] != 0xffffffffu;
         }
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
@@ -386,12 +380,13 @@ void free_capacity(p2p_plan *P) {
     cudaStream_t st = P->stream;
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
                     P->s_nbr_cnt, P->s_item_cnt, P->s_item_off, P->s_red_cnt, P->s_small_cnt, P->s_small_off,
+                    P->s_slot_box,
                     P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, P->rec, P->bkey, P->bstart,
                     P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
-    P->s_nbr_cnt = P->s_item_cnt = P->s_item_off = nullptr;
+    P->s_nbr_cnt = P->s_item_cnt = P->s_item_off = P->s_slot_box = nullptr;
     P->s_small_cnt = P->s_small_off = P->small_tgt = P->small_box = P->chunk_box = nullptr;
     P->chunk_out = nullptr;
     P->s_red_cnt = nullptr;
@@ -432,6 +427,7 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     if (grav) {
         P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_nbr_cnt, 4 * bcap, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_slot_box, 4 * 27 * bcap, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_item_cnt, 4 * bcap, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_item_off, 4 * (bcap + 1), st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_small_cnt, 4 * bcap, st));
@@ -490,7 +486,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     const unsigned gw = warp_grid(bcap, P->num_sms);
     const uint32_t tmax = ITEM_TMAX;
     P2P_LAUNCH(k_nbr_count, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->occ, P->ctr, P->s_nbr_cnt,
-               P->s_red_cnt, P->s_item_cnt, P->s_small_cnt, tmax);
+               P->s_red_cnt, P->s_item_cnt, P->s_small_cnt, P->s_slot_box, tmax);
     P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_nbr_cnt}, OffPut<uint32_t>{P->nbr_off, &P->ctr->B},
                                        &P->ctr->B, bcap, &P->ctr->n_nbr, P->s_partials, st));
     P2P_CUDA_TRY(device_scan<unsigned long long>(
@@ -501,7 +497,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
                                        &P->ctr->B, bcap, &P->ctr->n_items, P->s_partials, st));
     P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_small_cnt}, OffPut<uint32_t>{P->s_small_off, &P->ctr->B},
                                        &P->ctr->B, bcap, &P->ctr->n_small, P->s_partials, st));
-    P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->occ, P->ctr, P->nbr_off,
+    P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->s_slot_box, P->ctr, P->nbr_off,
                P->s_item_off, P->s_item_cnt, P->nbr_box, P->nbr_slot, P->items, P->s_small_off, P->small_tgt,
                P->small_box, (const unsigned long long *)P->red_off, P->chunk_box, P->chunk_out,
                (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));

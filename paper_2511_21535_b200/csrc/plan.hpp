@@ -92,6 +92,7 @@ struct p2p_plan {
     uint32_t *s_hist = nullptr, *s_status = nullptr;
     void *s_partials = nullptr;
     uint32_t *s_nbr_cnt = nullptr, *s_item_cnt = nullptr, *s_item_off = nullptr;
+    uint32_t *s_slot_box = nullptr;  // [27 B] k_nbr_count -> k_nbr_fill: neighbour box per stencil slot (~0u: none)
     uint32_t *s_small_cnt = nullptr, *s_small_off = nullptr;
     uint32_t *small_tgt = nullptr, *small_box = nullptr;  // sorted target index / its box, small boxes only
     // restructure chunks: every 32 consecutive CSR entries e = 32 c .. 32 c + 31 form one chunk; their redundant
