@@ -137,7 +137,7 @@ struct HeadPut {
             uint32_t bk = skey[p] / div;
             bkey[e] = bk;
             bstart[e] = (uint32_t)p;
-            box_of[bk] = e;
+            if (box_of) box_of[bk] = e;
             if (occ) atomicOr(&occ[bk >> 5], 1u << (bk & 31u));
         }
         if (p == n - 1) bstart[e + v] = n;
@@ -145,82 +145,106 @@ struct HeadPut {
 };
 
 // ------------------------------------------------------------------------------------------------ a5
-__device__ __forceinline__ bool stencil_nbr(const Geom &g, const uint32_t c[3], int slot, uint32_t nc[3]) {
-    const int dd[3] = {slot % 3 - 1, (slot / 3) % 3 - 1, slot / 9 - 1};
+// Neighbour keys by Morton arithmetic (no decode / re-encode): lane = stencil slot with offsets dd in {-1,0,1}^3;
+// a +-1 step in dimension d is a masked add / subtract on that dimension's interleaved bits, the periodic wrap
+// (C5) replaces the bits by 0 or by nbox_d - 1.  Slots in ascending order (C10): slot = (dx+1) + 3 (dy+1) + 9 (dz+1).
+struct MortonStencil {
+    uint32_t M[3], top[3];  // dimension-d bit mask of the key space, bits of coordinate nbox_d - 1
+    int dd[3];
+    bool live;
+};
+__device__ __forceinline__ MortonStencil make_stencil(const Geom &g, unsigned lane) {
+    MortonStencil s;
+    s.live = lane < 27;
+    const uint32_t full = spread3((1u << g.nb) - 1u);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        int v = (int)c[d] + dd[d];
-        if (v < 0 || v >= g.nbox[d]) {
-            if (!((g.periodic >> d) & 1u)) return false;
-            v = v < 0 ? v + g.nbox[d] : v - g.nbox[d];
+        s.M[d] = full << d;
+        s.top[d] = spread3((uint32_t)(g.nbox[d] - 1)) << d;
+    }
+    s.dd[0] = (int)(lane % 3) - 1;
+    s.dd[1] = (int)((lane / 3) % 3) - 1;
+    s.dd[2] = (int)(lane / 9) - 1;
+    return s;
+}
+__device__ __forceinline__ bool morton_nbr(const Geom &g, const MortonStencil &s, uint32_t key, uint32_t &nk) {
+    if (!s.live) return false;
+    nk = key;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const uint32_t M = s.M[d], kd = key & M;
+        if (s.dd[d] > 0) {
+            if (kd == s.top[d]) {
+                if (!((g.periodic >> d) & 1u)) return false;
+                nk &= ~M;
+            } else {
+                nk = (((nk | ~M) + (1u << d)) & M) | (nk & ~M);
+            }
+        } else if (s.dd[d] < 0) {
+            if (kd == 0u) {
+                if (!((g.periodic >> d) & 1u)) return false;
+                nk = (nk & ~M) | s.top[d];
+            } else {
+                nk = (((nk & M) - (1u << d)) & M) | (nk & ~M);
+            }
         }
-        nc[d] = (uint32_t)v;
     }
     return true;
 }
 
-__device__ __forceinline__ void decode3(uint32_t key, uint32_t c[3]) {
-    c[0] = compact3(key);
-    c[1] = compact3(key >> 1);
-    c[2] = compact3(key >> 2);
+// dense key -> {box, n_b} table for the gravity neighbour search (valid where the occupancy bit is set)
+__global__ void k_boxinfo(const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
+                          const DevCounters *__restrict__ ctr, uint2 *__restrict__ boxinfo) {
+    const uint32_t B = ctr->B;
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x)
+        boxinfo[bkey[b]] = make_uint2(b, bstart[b + 1] - bstart[b]);
 }
 
-// one warp per target box, lane = stencil slot (27 of 32 lanes): parallel box_of lookups, ballot-compacted
-// output in ascending slot order (C10)
-// Emptiness is answered by the 2^key_bits-bit occupancy bitmap (2 MB for 256^3 boxes: L2/L1-resident), so
-// the common case of clustered inputs -- an empty neighbour -- costs one cached load; only non-empty neighbours
-// read the dense key -> box table (always valid for set bits: no validation load needed).
-__device__ __forceinline__ bool lane_nbr(const Geom &g, const uint32_t c[3], unsigned lane,
-                                         const uint32_t *__restrict__ occ, const uint32_t *__restrict__ box_of,
-                                         uint32_t &k) {
-    uint32_t nc[3];
-    if (lane >= 27 || !stencil_nbr(g, c, (int)lane, nc)) return false;
-    const uint32_t nk = spread3(nc[0]) | (spread3(nc[1]) << 1) | (spread3(nc[2]) << 2);
-    if (!((__ldg(&occ[nk >> 5]) >> (nk & 31u)) & 1u)) return false;
-    k = box_of[nk];
-    return true;
-}
-
+// a5 (count pass): lane = stencil slot.  Two dependent load levels per box: the box key, then the neighbour's
+// occupancy word and its {box, n} entry, issued together (a stale entry of an empty key is ignored).  The
+// per-slot result goes to a slot table that k_nbr_fill reads back instead of repeating the search.
 __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__restrict__ bkey,
-                                                   const uint32_t *__restrict__ bstart,
-                                                   const uint32_t *__restrict__ box_of,
+                                                   const uint2 *__restrict__ boxinfo,
                                                    const uint32_t *__restrict__ occ, DevCounters *ctr,
                                                    uint32_t *__restrict__ nbr_cnt, uint64_t *__restrict__ red_cnt,
                                                    uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ small_cnt,
-                                                   uint32_t *__restrict__ slot_box, uint32_t tmax) {
+                                                   uint2 *__restrict__ slot_tab, uint32_t tmax) {
     const uint32_t B = ctr->B;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const MortonStencil stc = make_stencil(g, lane);
     unsigned long long pairs = 0;
-    // NB boxes per warp iteration: their dependent lookups (box_of -> bkey -> bstart) are in flight together
-    constexpr int NB = 4;
+    constexpr int NB = 4;  // boxes per warp iteration: their lookups are in flight together
     for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NB; b0 < B; b0 += nwarps * NB) {
         bool ok[NB];
-        uint32_t k[NB];
+        uint32_t kk[NB], cn[NB], key[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) key[u] = b0 + u < B ? bkey[b0 + u] : 0u;
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
             ok[u] = false;
-            k[u] = 0;
-            if (b0 + u < B) {
-                const uint32_t key = bkey[b0 + u];
-                uint32_t c[3];
-                decode3(key, c);
-                // non-target (multi-GPU halo) boxes get no neighbour list and no work
-                if (key >= g.tkey_lo && key <= g.tkey_hi) ok[u] = lane_nbr(g, c, lane, occ, box_of, k[u]);
+            kk[u] = 0;
+            cn[u] = 0;
+            uint32_t nk;
+            // non-target (multi-GPU halo) boxes get no neighbour list and no work
+            if (b0 + u < B && key[u] >= g.tkey_lo && key[u] <= g.tkey_hi && morton_nbr(g, stc, key[u], nk)) {
+                const uint32_t w = __ldg(&occ[nk >> 5]);
+                const uint2 inf = boxinfo[nk];
+                ok[u] = (w >> (nk & 31u)) & 1u;
+                kk[u] = inf.x;
+                cn[u] = inf.y;
             }
         }
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
             const uint32_t b = b0 + u;
-            if (b < B && lane < 27) slot_box[27 * (size_t)b + lane] = ok[u] ? k[u] : 0xffffffffu;
-            uint32_t nk = ok[u] ? bstart[k[u] + 1] - bstart[k[u]] : 0u;
+            if (b < B && lane < 27) slot_tab[27 * (size_t)b + lane] = ok[u] ? make_uint2(kk[u], cn[u]) : make_uint2(~0u, 0u);
+            const uint32_t nk = __reduce_add_sync(0xffffffffu, ok[u] ? cn[u] : 0u);
             const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, ok[u]));
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) nk += __shfl_xor_sync(0xffffffffu, nk, o);
+            const uint32_t own = __shfl_sync(0xffffffffu, ok[u] ? cn[u] : 0u, 13);  // centre slot = the box itself
             if (lane == 0 && b < B) {
-                const uint32_t key = bkey[b];
-                const bool target = key >= g.tkey_lo && key <= g.tkey_hi;
-                const uint32_t nb_b = target ? bstart[b + 1] - bstart[b] : 0u;
+                const bool target = key[u] >= g.tkey_lo && key[u] <= g.tkey_hi;
+                const uint32_t nb_b = target ? own : 0u;
                 nbr_cnt[b] = cnt;
                 red_cnt[b] = nk;
                 // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
@@ -236,7 +260,7 @@ __global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__res
 
 __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__restrict__ bkey,
                                                   const uint32_t *__restrict__ bstart,
-                                                  const uint32_t *__restrict__ slot_box, const DevCounters *ctr,
+                                                  const uint2 *__restrict__ slot_tab, const DevCounters *ctr,
                                                   const uint32_t *__restrict__ nbr_off,
                                                   const uint32_t *__restrict__ item_off,
                                                   const uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ nbr_box,
@@ -252,11 +276,13 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
     constexpr int NB = 4;  // boxes per warp iteration (memory-level parallelism, as in k_nbr_count)
     for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NB; b0 < B; b0 += nwarps * NB) {
         bool ok[NB];
-        uint32_t k[NB];
+        uint32_t k[NB], cn[NB];
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
             // k_nbr_count's slot table (halo boxes: all ~0u, no neighbour list and no work)
-            k[u] = (b0 + u < B && lane < 27) ? slot_box[27 * (size_t)(b0 + u) + lane] : 0xffffffffu;
+            const uint2 t = (b0 + u < B && lane < 27) ? slot_tab[27 * (size_t)(b0 + u) + lane] : make_uint2(~0u, 0u);
+            k[u] = t.x;
+            cn[u] = t.y;
             ok[u] = k[u] != 0xffffffffu;
         }
 #pragma unroll
@@ -265,7 +291,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
             const uint32_t m = __ballot_sync(0xffffffffu, ok[u]);
             if (b >= B) continue;
             // segment lengths in slot (= CSR) order; exclusive prefix = segment offset inside the box's run
-            const uint32_t cnt_l = ok[u] ? bstart[k[u] + 1] - bstart[k[u]] : 0u;
+            const uint32_t cnt_l = ok[u] ? cn[u] : 0u;
             uint32_t incl = cnt_l;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -380,13 +406,15 @@ void free_capacity(p2p_plan *P) {
     cudaStream_t st = P->stream;
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
                     P->s_nbr_cnt, P->s_item_cnt, P->s_item_off, P->s_red_cnt, P->s_small_cnt, P->s_small_off,
-                    P->s_slot_box,
+                    P->s_slot_tab, P->boxinfo,
                     P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, P->rec, P->bkey, P->bstart,
                     P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
-    P->s_nbr_cnt = P->s_item_cnt = P->s_item_off = P->s_slot_box = nullptr;
+    P->s_nbr_cnt = P->s_item_cnt = P->s_item_off = nullptr;
+    P->s_slot_tab = nullptr;
+    P->boxinfo = nullptr;
     P->s_small_cnt = P->s_small_off = P->small_tgt = P->small_box = P->chunk_box = nullptr;
     P->chunk_out = nullptr;
     P->s_red_cnt = nullptr;
@@ -419,7 +447,7 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     P2P_CUDA_TRY(dalloc(&P->s_partials, scan_partials_bytes(std::max(n, bcap)), st));
     P2P_CUDA_TRY(dalloc((void **)&P->bkey, 4 * bcap, st));
     P2P_CUDA_TRY(dalloc((void **)&P->bstart, 4 * (bcap + 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&P->box_of, 4 * keyspace, st));
+    if (!grav) P2P_CUDA_TRY(dalloc((void **)&P->box_of, 4 * keyspace, st));
     P2P_CUDA_TRY(dalloc((void **)&P->occ, 4 * std::max<uint64_t>(1, keyspace / 32), st));
     P2P_CUDA_TRY(dalloc((void **)&P->nbr_off, 4 * (bcap + 1), st));
     P2P_CUDA_TRY(dalloc((void **)&P->nbr_box, 4 * nslot * bcap, st));
@@ -427,7 +455,8 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     if (grav) {
         P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_nbr_cnt, 4 * bcap, st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_slot_box, 4 * 27 * bcap, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_slot_tab, sizeof(uint2) * 27 * bcap, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->boxinfo, sizeof(uint2) * keyspace, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_item_cnt, 4 * bcap, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_item_off, 4 * (bcap + 1), st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_small_cnt, 4 * bcap, st));
@@ -479,14 +508,16 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     const uint64_t occ_words = std::max<uint64_t>(1, (1ull << P->key_bits) / 32);
     P2P_CUDA_TRY(cudaMemsetAsync(P->occ, 0, 4 * occ_words, st));
     P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, 1u},
-                                       HeadPut{P->skey, 1u, P->bkey, P->bstart, P->box_of, n, P->occ}, nullptr, n,
+                                       HeadPut{P->skey, 1u, P->bkey, P->bstart, nullptr, n, P->occ}, nullptr, n,
                                        &P->ctr->B, P->s_partials, st));
     // a5
     const uint64_t bcap = (uint64_t)P->bcap;
     const unsigned gw = warp_grid(bcap, P->num_sms);
     const uint32_t tmax = ITEM_TMAX;
-    P2P_LAUNCH(k_nbr_count, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->box_of, P->occ, P->ctr, P->s_nbr_cnt,
-               P->s_red_cnt, P->s_item_cnt, P->s_small_cnt, P->s_slot_box, tmax);
+    P2P_LAUNCH(k_boxinfo, std::max<unsigned>(1, std::min<unsigned>(div_up(bcap, 256), (unsigned)P->num_sms * 8)), 256,
+               0, st, P->bkey, P->bstart, P->ctr, P->boxinfo);
+    P2P_LAUNCH(k_nbr_count, gw, 256, 0, st, P->geom, P->bkey, P->boxinfo, P->occ, P->ctr, P->s_nbr_cnt,
+               P->s_red_cnt, P->s_item_cnt, P->s_small_cnt, P->s_slot_tab, tmax);
     P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_nbr_cnt}, OffPut<uint32_t>{P->nbr_off, &P->ctr->B},
                                        &P->ctr->B, bcap, &P->ctr->n_nbr, P->s_partials, st));
     P2P_CUDA_TRY(device_scan<unsigned long long>(
@@ -497,7 +528,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
                                        &P->ctr->B, bcap, &P->ctr->n_items, P->s_partials, st));
     P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_small_cnt}, OffPut<uint32_t>{P->s_small_off, &P->ctr->B},
                                        &P->ctr->B, bcap, &P->ctr->n_small, P->s_partials, st));
-    P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->s_slot_box, P->ctr, P->nbr_off,
+    P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->s_slot_tab, P->ctr, P->nbr_off,
                P->s_item_off, P->s_item_cnt, P->nbr_box, P->nbr_slot, P->items, P->s_small_off, P->small_tgt,
                P->small_box, (const unsigned long long *)P->red_off, P->chunk_box, P->chunk_out,
                (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));

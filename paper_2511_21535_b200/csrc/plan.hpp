@@ -80,7 +80,7 @@ struct p2p_plan {
     uint32_t *nbr_off = nullptr, *nbr_box = nullptr;
     uint8_t *nbr_slot = nullptr;
     uint64_t *red_off = nullptr;
-    uint32_t *box_of = nullptr;  // dense Morton-key -> box lookup (gravity: valid where occ has the bit set)
+    uint32_t *box_of = nullptr;  // Helmholtz: dense Morton-key -> box lookup
     uint32_t *occ = nullptr;     // gravity: occupancy bitmap of the key space (cleared every build)
     p2p::Item *items = nullptr;
     void *red = nullptr;         // gravity red[R] records; helmholtz Xg[B][9][t]
@@ -92,7 +92,8 @@ struct p2p_plan {
     uint32_t *s_hist = nullptr, *s_status = nullptr;
     void *s_partials = nullptr;
     uint32_t *s_nbr_cnt = nullptr, *s_item_cnt = nullptr, *s_item_off = nullptr;
-    uint32_t *s_slot_box = nullptr;  // [27 B] k_nbr_count -> k_nbr_fill: neighbour box per stencil slot (~0u: none)
+    uint2 *s_slot_tab = nullptr;  // [27 B] k_nbr_count -> k_nbr_fill: {neighbour box, n_k} per stencil slot (x = ~0u: none)
+    uint2 *boxinfo = nullptr;     // gravity: dense Morton key -> {box, n_b} (valid where occ has the bit set)
     uint32_t *s_small_cnt = nullptr, *s_small_off = nullptr;
     uint32_t *small_tgt = nullptr, *small_box = nullptr;  // sorted target index / its box, small boxes only
     // restructure chunks: every 32 consecutive CSR entries e = 32 c .. 32 c + 31 form one chunk; their redundant
