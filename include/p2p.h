@@ -118,6 +118,20 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
  * computed in between are undefined.  Invalidates red[] (restructure again).  Helmholtz: P2P_ERR_UNSUPPORTED. */
 p2p_status p2p_plan_update(p2p_plan *plan, int64_t n_local, const void *positions, const void *charges);
 
+/* Host-buffer variants of p2p_plan_update / p2p_eval: the end-to-end path of a time-stepping code whose
+ * particle data live in host memory.  p2p_plan_update_host copies the inputs into plan-owned device staging
+ * (cudaMemcpyAsync on the plan's stream: asynchronous for page-locked host memory, the caller keeps the host
+ * buffers alive until the stream passes the copy) and runs p2p_plan_update on it.  p2p_eval_host evaluates
+ * into plan-owned device results, copies them to the host buffers and returns after the copy completed (ONE
+ * stream synchronisation): the host results are valid on return.
+ *   positions_host : host, [n_local][3] (the plan's precision);  charges_host : host, [n_local] masses
+ *   potential_host : host, [n_local];  field_host : host, [n_local][3] or NULL
+ * Device pointers are rejected (P2P_ERR_INVALID_ARGUMENT: use the device entry points).  Gravity, single-GPU
+ * plans only (else P2P_ERR_UNSUPPORTED).  Staging grows on demand (the first call per size allocates). */
+p2p_status p2p_plan_update_host(p2p_plan *plan, int64_t n_local, const void *positions_host,
+                                const void *charges_host);
+p2p_status p2p_eval_host(p2p_plan *plan, p2p_layout layout, void *potential_host, void *field_host);
+
 /* a6: build the redundant buffer (gravity: red[R] records {x,y,z,m} rebased to the target box origin,
  * C11; helmholtz: Xg[B][9][t], zero segments for missing neighbours, C10).  Enqueue only. */
 p2p_status p2p_restructure(p2p_plan *plan);

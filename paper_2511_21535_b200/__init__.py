@@ -31,7 +31,8 @@ P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE = 0, 1, 2
 
 LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise": P2P_INDEXED_BITWISE}
 
-EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_restructure", "p2p_eval", "p2p_set_charges", "p2p_destroy",
+EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure", "p2p_eval",
+            "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
             "p2p_partition_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
             "p2p_comm_create_loopback", "p2p_status_string", "p2p_last_error", "p2p_kernel_launch_count",
@@ -72,6 +73,8 @@ def lib() -> C.CDLL:
         sig = {
             "p2p_plan_create": (C.c_int, [C.POINTER(P2PConfig), i64, p, p, C.POINTER(C.c_void_p)]),
             "p2p_plan_update": (C.c_int, [p, i64, p, p]),
+            "p2p_plan_update_host": (C.c_int, [p, i64, p, p]),
+            "p2p_eval_host": (C.c_int, [p, C.c_int, p, p]),
             "p2p_restructure": (C.c_int, [p]),
             "p2p_eval": (C.c_int, [p, C.c_int, p, p]),
             "p2p_set_charges": (C.c_int, [p, p]),
@@ -110,6 +113,20 @@ def _check(s: int):
         raise P2PError(s, lib().p2p_last_error().decode())
 
 
+def _host_array(a, dtype):
+    """a contiguous host array of the plan's dtype (torch CPU tensor kept as is, numpy converted)"""
+    import torch
+    if isinstance(a, np.ndarray):
+        a = torch.from_numpy(np.ascontiguousarray(a))
+    if a.is_cuda:
+        raise P2PError(P2P_ERR_INVALID_ARGUMENT, "host array expected (use update / eval for device tensors)")
+    return a.to(dtype).contiguous()
+
+
+def _host_ptr(a) -> int:
+    return a.data_ptr()
+
+
 # ---- ABI-shaped functions (raw pointers) ----
 def p2p_plan_create(cfg: P2PConfig, n_local: int, positions: int, charges: int) -> int:
     out = C.c_void_p()
@@ -120,6 +137,16 @@ def p2p_plan_create(cfg: P2PConfig, n_local: int, positions: int, charges: int) 
 
 def p2p_plan_update(plan: int, n_local: int, positions: int, charges: int):
     _check(lib().p2p_plan_update(C.c_void_p(plan), int(n_local), C.c_void_p(positions), C.c_void_p(charges)))
+
+
+def p2p_plan_update_host(plan: int, n_local: int, positions_host: int, charges_host: int):
+    _check(lib().p2p_plan_update_host(C.c_void_p(plan), int(n_local), C.c_void_p(positions_host),
+                                      C.c_void_p(charges_host)))
+
+
+def p2p_eval_host(plan: int, layout: int, potential_host: int, field_host: int | None):
+    _check(lib().p2p_eval_host(C.c_void_p(plan), int(layout), C.c_void_p(potential_host),
+                               C.c_void_p(field_host or None)))
 
 
 def p2p_restructure(plan: int):
@@ -274,6 +301,27 @@ class Plan:
         p2p_plan_update(self.handle, self.n, positions.data_ptr(), charges.data_ptr())
         self._keep = (positions, charges)
         self._info = None
+
+    def update_host(self, positions, charges):
+        """update() from HOST arrays (numpy or CPU tensors; page-locked memory makes the copy asynchronous):
+        the library copies them to the device on the plan's stream (p2p_plan_update_host).  The arrays must stay
+        alive until the stream passes the copy."""
+        positions = _host_array(positions, self.dtype)
+        charges = _host_array(charges, self.dtype)
+        self.n = int(positions.shape[0])
+        p2p_plan_update_host(self.handle, self.n, _host_ptr(positions), _host_ptr(charges))
+        self._keep = (positions, charges)
+        self._info = None
+
+    def eval_host(self, layout: int = P2P_REDUNDANT, potential=None, field=None, want_field: bool = True):
+        """eval() into HOST arrays (p2p_eval_host: device results copied back, valid on return)"""
+        import torch
+        if potential is None:
+            potential = torch.empty(self.n, dtype=self.dtype, pin_memory=True)
+        if field is None and want_field:
+            field = torch.empty((self.n, 3), dtype=self.dtype, pin_memory=True)
+        p2p_eval_host(self.handle, layout, _host_ptr(potential), _host_ptr(field) if field is not None else None)
+        return potential, field
 
     def refresh_info(self):
         self._info = p2p_get_info(self.handle)

@@ -97,9 +97,10 @@ static void free_plan_buffers(p2p_plan *P) {
     cudaStream_t st = P->stream;
     free_capacity(P);
     free_distributed(P);
-    void *bufs[] = {P->red, P->table, P->ctr};
+    void *bufs[] = {P->red, P->table, P->ctr, P->stage_in, P->stage_out};
     for (void *b : bufs) dfree(b, st);
-    P->red = P->table = nullptr;
+    P->red = P->table = P->stage_in = P->stage_out = nullptr;
+    P->stage_in_cap = P->stage_out_cap = 0;
     P->ctr = nullptr;
 }
 
@@ -359,6 +360,65 @@ p2p_status p2p_plan_update(p2p_plan *P, int64_t n_local, const void *positions, 
         return P2P_OK;
     }
     return mark(P, build_gravity_structs(P, positions, charges));
+}
+
+// ---- host-buffer entry points: the library stages the copies on the plan's stream ----
+static bool grow_stage(p2p_plan *P, void **buf, int64_t *cap, int64_t need_bytes) {
+    if (*cap >= need_bytes) return true;
+    dfree(*buf, P->stream);
+    *buf = nullptr;
+    *cap = 0;
+    if (dalloc(buf, (size_t)need_bytes, P->stream) != cudaSuccess) {
+        *buf = nullptr;
+        return false;
+    }
+    *cap = need_bytes;
+    return true;
+}
+
+p2p_status p2p_plan_update_host(p2p_plan *P, int64_t n_local, const void *positions_host, const void *charges_host) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (P->cfg.kernel != P2P_GRAVITY || P->comm)
+        return fail(P2P_ERR_UNSUPPORTED, "p2p_plan_update_host: single-GPU gravity plans only");
+    if (n_local < 0) return fail(P2P_ERR_INVALID_ARGUMENT, "n_local < 0");
+    if (n_local > 0 && (!positions_host || !charges_host)) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_local > 0 && (is_device_ptr(positions_host) || is_device_ptr(charges_host)))
+        return fail(P2P_ERR_INVALID_ARGUMENT, "positions / charges must be host pointers (use p2p_plan_update)");
+    const size_t tsz = P->cfg.precision == P2P_FP64 ? sizeof(double) : sizeof(float);
+    const size_t pb = 3 * tsz * (size_t)n_local, qb = tsz * (size_t)n_local;
+    if (!grow_stage(P, &P->stage_in, &P->stage_in_cap, (int64_t)std::max<size_t>(pb + qb, 1)))
+        return fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate the input staging buffer");
+    char *d = (char *)P->stage_in;
+    if (n_local > 0) {
+        cudaError_t e = cudaMemcpyAsync(d, positions_host, pb, cudaMemcpyHostToDevice, P->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d + pb, charges_host, qb, cudaMemcpyHostToDevice, P->stream);
+        if (e != cudaSuccess) return fail(P2P_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+    }
+    return p2p_plan_update(P, n_local, d, d + pb);
+}
+
+p2p_status p2p_eval_host(p2p_plan *P, p2p_layout layout, void *potential_host, void *field_host) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (P->cfg.kernel != P2P_GRAVITY || P->comm)
+        return fail(P2P_ERR_UNSUPPORTED, "p2p_eval_host: single-GPU gravity plans only");
+    if (P->n > 0 && !potential_host) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL potential");
+    if ((potential_host && is_device_ptr(potential_host)) || (field_host && is_device_ptr(field_host)))
+        return fail(P2P_ERR_INVALID_ARGUMENT, "potential / field must be host pointers (use p2p_eval)");
+    const size_t tsz = P->cfg.precision == P2P_FP64 ? sizeof(double) : sizeof(float);
+    const size_t ob = tsz * (size_t)P->n, fb = field_host ? 3 * tsz * (size_t)P->n : 0;
+    if (!grow_stage(P, &P->stage_out, &P->stage_out_cap, (int64_t)std::max<size_t>(ob + fb, 1)))
+        return fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate the output staging buffer");
+    char *d = (char *)P->stage_out;
+    s = p2p_eval(P, layout, d, field_host ? d + ob : nullptr);
+    if (s != P2P_OK) return s;
+    cudaError_t e = cudaSuccess;
+    if (ob) e = cudaMemcpyAsync(potential_host, d, ob, cudaMemcpyDeviceToHost, P->stream);
+    if (e == cudaSuccess && fb) e = cudaMemcpyAsync(field_host, d + ob, fb, cudaMemcpyDeviceToHost, P->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+    if (e != cudaSuccess) return fail(P2P_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+    return P2P_OK;
 }
 
 p2p_status p2p_restructure(p2p_plan *P) {

@@ -88,6 +88,9 @@ struct p2p_plan {
     p2p::DevCounters *ctr = nullptr;
     // capacity-sized scratch, allocated once per plan (p2p_plan_update reuses it: no allocation, no sync)
     int64_t cap = 0, bcap = 0, red_cap = 0;
+    // host-buffer entry points (p2p_plan_update_host / p2p_eval_host): plan-owned device staging
+    void *stage_in = nullptr, *stage_out = nullptr;
+    int64_t stage_in_cap = 0, stage_out_cap = 0;
     uint32_t *s_key = nullptr, *s_idx = nullptr, *s_kalt = nullptr, *s_valt = nullptr;
     uint32_t *s_hist = nullptr, *s_status = nullptr;
     void *s_partials = nullptr;

@@ -208,3 +208,34 @@ def test_plan_update_reports_out_of_domain(P):
         assert e.value.status == P.P2P_ERR_OUT_OF_DOMAIN and "5" in str(e.value)
         plan.update(torch.from_numpy(inp.pos).cuda(), torch.from_numpy(inp.mass).cuda())
         assert plan.refresh_info().n_boxes == 64
+
+
+def test_host_buffer_entry_points(P):
+    """p2p_plan_update_host / p2p_eval_host (the bench's e2e path): the library's own H2D / D2H copies give the
+    same bits as the device entry points, and the values match the oracle"""
+    a = G.plummer(6000, 6, seed=21)
+    seq = [G.plummer(7000, 6, seed=22), G.uniform_per_box(6, 5, seed=23)]   # same geometry as a
+    with gpu_plan(P, a) as plan:
+        for inp in seq:
+            pos_h = torch.from_numpy(inp.pos).pin_memory()
+            m_h = torch.from_numpy(inp.mass).pin_memory()
+            plan.update_host(pos_h, m_h)
+            plan.restructure()
+            phi_h, f_h = plan.eval_host(P.P2P_REDUNDANT)
+            assert not phi_h.is_cuda and not f_h.is_cuda
+            plan.update(pos_h.cuda(), m_h.cuda())
+            plan.restructure()
+            phi_d, f_d = plan.eval(P.P2P_REDUNDANT)
+            torch.cuda.synchronize()
+            assert phi_h.numpy().tobytes() == phi_d.cpu().numpy().tobytes()
+            assert f_h.numpy().tobytes() == f_d.cpu().numpy().tobytes()
+            rphi, rf = oracle.GravityPlan(inp).eval_indexed()
+            assert oracle.rel_l2(phi_h.numpy(), rphi) < 1e-5 and oracle.rel_l2(f_h.numpy(), rf) < 1e-5
+            # numpy inputs (pageable) work too; device pointers are rejected
+            plan.update_host(inp.pos, inp.mass)
+            plan.restructure()
+            phi2, _ = plan.eval_host(P.P2P_REDUNDANT, want_field=False)
+            assert phi2.numpy().tobytes() == phi_h.numpy().tobytes()
+        with pytest.raises(P.P2PError) as e:
+            P.p2p_eval_host(plan.handle, P.P2P_REDUNDANT, phi_d.data_ptr(), None)
+        assert e.value.status == P.P2P_ERR_INVALID_ARGUMENT
