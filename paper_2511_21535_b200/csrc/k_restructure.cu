@@ -54,17 +54,29 @@ __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const double L0 = g.L[0], L1 = g.L[1], L2 = g.L[2];
-    for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunk; ch += nw) {
-        // ---- level 1: the chunk head and lane e's CSR entry ----
+    // level 1 of a chunk: its head and lane e's CSR entry -- loaded one chunk ahead (software pipeline)
+    uint32_t n_b0 = 0, n_k = 0, n_slot = 13;
+    unsigned long long n_gout = 0;
+    auto load1 = [&](uint32_t c) {
+        if (c < nchunk) {
+            n_b0 = chunk_box[c];
+            n_gout = chunk_out[c];
+            const uint32_t ee = (c << 5) + lane;
+            if (ee < n_nbr) {
+                n_k = nbr_box[ee];
+                n_slot = nbr_slot[ee];
+            }
+        }
+    };
+    uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    load1(ch);
+    for (; ch < nchunk; ch += nw) {
         const uint32_t e = (ch << 5) + lane;
         const bool seg = e < n_nbr;
-        const uint32_t b0 = chunk_box[ch];
-        const unsigned long long gout = chunk_out[ch];
-        uint32_t k = 0, slot = 13;
-        if (seg) {
-            k = nbr_box[e];
-            slot = nbr_slot[e];
-        }
+        const uint32_t b0 = n_b0;
+        const unsigned long long gout = n_gout;
+        const uint32_t k = seg ? n_k : 0u, slot = seg ? n_slot : 13u;
+        load1(ch + nw);
         // ---- level 2: boxes b0 .. b0 + 31 (CSR starts, keys) and lane e's source segment ----
         const uint32_t bl = b0 + lane;
         uint32_t boff = 0xffffffffu, keyl = 0;
