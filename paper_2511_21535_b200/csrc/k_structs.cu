@@ -200,129 +200,238 @@ __global__ void k_boxinfo(const uint32_t *__restrict__ bkey, const uint32_t *__r
         boxinfo[bkey[b]] = make_uint2(b, bstart[b + 1] - bstart[b]);
 }
 
-// a5 (count pass): lane = stencil slot.  Two dependent load levels per box: the box key, then the neighbour's
-// occupancy word and its {box, n} entry, issued together (a stale entry of an empty key is ignored).  The
-// per-slot result goes to a slot table that k_nbr_fill reads back instead of repeating the search.
-__global__ void __launch_bounds__(256) k_nbr_count(Geom g, const uint32_t *__restrict__ bkey,
-                                                   const uint2 *__restrict__ boxinfo,
-                                                   const uint32_t *__restrict__ occ, DevCounters *ctr,
-                                                   uint32_t *__restrict__ nbr_cnt, uint64_t *__restrict__ red_cnt,
-                                                   uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ small_cnt,
-                                                   uint2 *__restrict__ slot_tab, uint32_t tmax) {
-    const uint32_t B = ctr->B;
-    const unsigned lane = threadIdx.x & 31u;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const MortonStencil stc = make_stencil(g, lane);
-    unsigned long long pairs = 0;
-    constexpr int NB = 4;  // boxes per warp iteration: their lookups are in flight together
-    for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NB; b0 < B; b0 += nwarps * NB) {
-        bool ok[NB];
-        uint32_t kk[NB], cn[NB], key[NB];
-#pragma unroll
-        for (int u = 0; u < NB; ++u) key[u] = b0 + u < B ? bkey[b0 + u] : 0u;
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            ok[u] = false;
-            kk[u] = 0;
-            cn[u] = 0;
-            uint32_t nk;
-            // non-target (multi-GPU halo) boxes get no neighbour list and no work
-            if (b0 + u < B && key[u] >= g.tkey_lo && key[u] <= g.tkey_hi && morton_nbr(g, stc, key[u], nk)) {
-                const uint32_t w = __ldg(&occ[nk >> 5]);
-                const uint2 inf = boxinfo[nk];
-                ok[u] = (w >> (nk & 31u)) & 1u;
-                kk[u] = inf.x;
-                cn[u] = inf.y;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            const uint32_t b = b0 + u;
-            if (b < B && lane < 27) slot_tab[27 * (size_t)b + lane] = ok[u] ? make_uint2(kk[u], cn[u]) : make_uint2(~0u, 0u);
-            const uint32_t nk = __reduce_add_sync(0xffffffffu, ok[u] ? cn[u] : 0u);
-            const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, ok[u]));
-            const uint32_t own = __shfl_sync(0xffffffffu, ok[u] ? cn[u] : 0u, 13);  // centre slot = the box itself
-            if (lane == 0 && b < B) {
-                const bool target = key[u] >= g.tkey_lo && key[u] <= g.tkey_hi;
-                const uint32_t nb_b = target ? own : 0u;
-                nbr_cnt[b] = cnt;
-                red_cnt[b] = nk;
-                // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
-                const bool small = nb_b <= SMALL_NT && nk <= SMALL_R;
-                item_cnt[b] = (small || !target) ? 0u : item_chunks(nb_b, nk, tmax);
-                small_cnt[b] = small ? (nb_b + 1) / 2 : 0u;  // target PAIRS (eval small path)
-                pairs += (unsigned long long)nb_b * nk;
-            }
-        }
-    }
-    if (lane == 0 && pairs) atomicAdd(&ctr->I, pairs);
+// a5, one pass: neighbour search, the four exclusive scans (CSR offsets, redundant offsets, work items, small
+// target pairs) and all writes of the CSR / items / small lists / restructure chunk heads.
+// One warp per tile of 32 consecutive boxes; tiles are claimed from an atomic counter in launch order, so the
+// decoupled look-back (NbTileStatus) only ever waits on tiles that are already running.
+//   phase A  lane = stencil slot, 4 boxes in flight: neighbour key by Morton arithmetic, then the occupancy
+//            word and the {box, n} entry together (a stale entry of an empty key is ignored); per-slot results
+//            to shared memory, per-box totals to lane i
+//   phase B  warp scans of the per-box totals, look-back for the tile's exclusive prefix, nbr_off / red_off
+//   phase C  lane = stencil slot again, per box: ballot-compacted CSR in ascending slot order (C10), the
+//            restructure chunk heads, the eval work items or small-target entries
+constexpr int NBB_WARPS = 4;
+constexpr int NBB_TILE = 32;
+
+__device__ __forceinline__ unsigned long long ld_vol64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_vol64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__restrict__ bkey,
-                                                  const uint32_t *__restrict__ bstart,
-                                                  const uint2 *__restrict__ slot_tab, const DevCounters *ctr,
-                                                  const uint32_t *__restrict__ nbr_off,
-                                                  const uint32_t *__restrict__ item_off,
-                                                  const uint32_t *__restrict__ item_cnt, uint32_t *__restrict__ nbr_box,
-                                                  uint8_t *__restrict__ nbr_slot, Item *__restrict__ items,
-                                                  const uint32_t *__restrict__ small_off,
-                                                  uint32_t *__restrict__ small_tgt, uint32_t *__restrict__ small_box,
-                                                  const unsigned long long *__restrict__ red_off,
-                                                  uint32_t *__restrict__ chunk_box,
-                                                  unsigned long long *__restrict__ chunk_out, uint32_t K) {
+__global__ void __launch_bounds__(NBB_WARPS * 32) k_nbr_build(
+    Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart, const uint2 *__restrict__ boxinfo,
+    const uint32_t *__restrict__ occ, DevCounters *ctr, NbTileStatus *status, uint32_t *__restrict__ nbr_off,
+    unsigned long long *__restrict__ red_off, uint32_t *__restrict__ nbr_box, uint8_t *__restrict__ nbr_slot,
+    Item *__restrict__ items, uint32_t *__restrict__ small_tgt, uint32_t *__restrict__ small_box,
+    uint32_t *__restrict__ chunk_box, unsigned long long *__restrict__ chunk_out, uint32_t K, uint32_t tmax) {
+    __shared__ uint32_t s_k[NBB_WARPS][NBB_TILE][27];
+    __shared__ uint32_t s_c[NBB_WARPS][NBB_TILE][27];
+    constexpr unsigned FULL = 0xffffffffu;
     const uint32_t B = ctr->B;
-    const unsigned lane = threadIdx.x & 31u;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    constexpr int NB = 4;  // boxes per warp iteration (memory-level parallelism, as in k_nbr_count)
-    for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NB; b0 < B; b0 += nwarps * NB) {
-        bool ok[NB];
-        uint32_t k[NB], cn[NB];
+    const uint32_t ntiles = (B + NBB_TILE - 1) / NBB_TILE;
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const MortonStencil stc = make_stencil(g, lane);
+    unsigned long long pairs = 0;
+    while (true) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(&ctr->nbr_tile, 1u);
+        t = __shfl_sync(FULL, t, 0);
+        if (t >= ntiles) break;
+        const uint32_t tb = t * NBB_TILE;
+        // lane i: box tb + i
+        const uint32_t mb = tb + lane;
+        const bool have = mb < B;
+        const uint32_t mkey = have ? bkey[mb] : 0u;
+        const uint32_t ms0 = have ? bstart[mb] : 0u;
+        const bool mtarget = have && mkey >= g.tkey_lo && mkey <= g.tkey_hi;  // halo boxes: source only
+        uint32_t my_nbr = 0, my_item = 0, my_small = 0, my_nb = 0;
+        unsigned long long my_red = 0;
+
+        // ---- phase A ----
+        constexpr int NB = 4;
+        for (int i0 = 0; i0 < NBB_TILE; i0 += NB) {
+            if (tb + i0 >= B) break;  // warp-uniform
+            bool ok[NB];
+            uint32_t kk[NB], cn[NB];
 #pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            // k_nbr_count's slot table (halo boxes: all ~0u, no neighbour list and no work)
-            const uint2 t = (b0 + u < B && lane < 27) ? slot_tab[27 * (size_t)(b0 + u) + lane] : make_uint2(~0u, 0u);
-            k[u] = t.x;
-            cn[u] = t.y;
-            ok[u] = k[u] != 0xffffffffu;
+            for (int u = 0; u < NB; ++u) {
+                const int i = i0 + u;
+                const uint32_t key = __shfl_sync(FULL, mkey, i);
+                const bool tgt = __shfl_sync(FULL, (uint32_t)mtarget, i) != 0u;
+                ok[u] = false;
+                kk[u] = 0;
+                cn[u] = 0;
+                uint32_t nk;
+                if (tgt && morton_nbr(g, stc, key, nk)) {
+                    const uint32_t wd = __ldg(&occ[nk >> 5]);
+                    const uint2 inf = boxinfo[nk];
+                    ok[u] = (wd >> (nk & 31u)) & 1u;
+                    kk[u] = inf.x;
+                    cn[u] = inf.y;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                const int i = i0 + u;
+                if (lane < 27) {
+                    s_k[w][i][lane] = ok[u] ? kk[u] : 0xffffffffu;
+                    s_c[w][i][lane] = ok[u] ? cn[u] : 0u;
+                }
+                const uint32_t nk = __reduce_add_sync(FULL, ok[u] ? cn[u] : 0u);
+                const uint32_t cnt = __popc(__ballot_sync(FULL, ok[u]));
+                const uint32_t own = __shfl_sync(FULL, ok[u] ? cn[u] : 0u, 13);  // centre slot = the box itself
+                if (lane == (unsigned)i && have) {
+                    my_nbr = cnt;
+                    my_red = nk;
+                    my_nb = mtarget ? own : 0u;
+                    // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
+                    const bool small = my_nb <= SMALL_NT && nk <= SMALL_R;
+                    my_item = (small || !mtarget) ? 0u : item_chunks(my_nb, nk, tmax);
+                    my_small = (small && mtarget) ? (my_nb + 1) / 2 : 0u;  // target PAIRS
+                    pairs += (unsigned long long)my_nb * nk;
+                }
+            }
         }
+        __syncwarp();
+
+        // ---- phase B: tile scans + decoupled look-back ----
+        uint32_t in_nbr = my_nbr, in_item = my_item, in_small = my_small;
+        unsigned long long in_red = my_red;
 #pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            const uint32_t b = b0 + u;
-            const uint32_t m = __ballot_sync(0xffffffffu, ok[u]);
-            if (b >= B) continue;
-            // segment lengths in slot (= CSR) order; exclusive prefix = segment offset inside the box's run
-            const uint32_t cnt_l = ok[u] ? cn[u] : 0u;
-            uint32_t incl = cnt_l;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t a = __shfl_up_sync(FULL, in_nbr, o), b2 = __shfl_up_sync(FULL, in_item, o),
+                           c = __shfl_up_sync(FULL, in_small, o);
+            const unsigned long long d = __shfl_up_sync(FULL, in_red, o);
+            if (lane >= (unsigned)o) {
+                in_nbr += a;
+                in_item += b2;
+                in_small += c;
+                in_red += d;
+            }
+        }
+        unsigned long long p_nbr = 0, p_red = 0, p_is = 0;  // tile prefix (items | small << 32)
+        const unsigned long long a_nbr = __shfl_sync(FULL, (unsigned long long)in_nbr, 31);
+        const unsigned long long a_red = __shfl_sync(FULL, in_red, 31);
+        const unsigned long long a_is = __shfl_sync(FULL, (unsigned long long)in_item | ((unsigned long long)in_small << 32), 31);
+        NbTileStatus *me = status + t;
+        if (t == 0) {
+            if (lane == 0) {
+                st_vol64(&me->inc[0], a_nbr);
+                st_vol64(&me->inc[1], a_red);
+                st_vol64(&me->inc[2], a_is);
+                __threadfence();
+                st_vol64(&me->flag, 2ull);
+            }
+        } else {
+            if (lane == 0) {
+                st_vol64(&me->agg[0], a_nbr);
+                st_vol64(&me->agg[1], a_red);
+                st_vol64(&me->agg[2], a_is);
+                __threadfence();
+                st_vol64(&me->flag, 1ull);
+            }
+            // warp-parallel look-back: lane j inspects tile base - j; a window of 32 predecessors per step
+            for (int64_t base = (int64_t)t - 1;;) {
+                const int64_t q = base - (int64_t)lane;
+                unsigned long long f = 2ull;  // tiles before 0 act as an inclusive zero
+                if (q >= 0) {
+                    do {
+                        f = ld_vol64(&status[q].flag);
+                    } while (f == 0ull);
+                }
+                __threadfence();
+                const uint32_t incm = __ballot_sync(FULL, f == 2ull);
+                const int jstop = incm ? __ffs(incm) - 1 : 31;  // nearest inclusive predecessor in the window
+                unsigned long long v0 = 0, v1 = 0, v2 = 0;
+                if ((int)lane <= jstop && q >= 0) {
+                    const unsigned long long *v = f == 2ull ? status[q].inc : status[q].agg;
+                    v0 = ld_vol64(&v[0]);
+                    v1 = ld_vol64(&v[1]);
+                    v2 = ld_vol64(&v[2]);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    v0 += __shfl_xor_sync(FULL, v0, o);
+                    v1 += __shfl_xor_sync(FULL, v1, o);
+                    v2 += __shfl_xor_sync(FULL, v2, o);
+                }
+                p_nbr += v0;
+                p_red += v1;
+                p_is += v2;
+                if (incm) break;
+                base -= 32;
+            }
+            if (lane == 0) {
+                st_vol64(&me->inc[0], p_nbr + a_nbr);
+                st_vol64(&me->inc[1], p_red + a_red);
+                st_vol64(&me->inc[2], p_is + a_is);
+                __threadfence();
+                st_vol64(&me->flag, 2ull);
+            }
+        }
+        const uint32_t o_nbr = (uint32_t)p_nbr + in_nbr - my_nbr;
+        const unsigned long long o_red = p_red + in_red - my_red;
+        const uint32_t o_item = (uint32_t)p_is + in_item - my_item;
+        const uint32_t o_small = (uint32_t)(p_is >> 32) + in_small - my_small;
+        if (have) {
+            nbr_off[mb] = o_nbr;
+            red_off[mb] = o_red;
+        }
+        if (mb == B - 1) {  // the last box closes the offsets and publishes the totals
+            nbr_off[B] = o_nbr + my_nbr;
+            red_off[B] = o_red + my_red;
+            ctr->n_nbr = o_nbr + my_nbr;
+            ctr->R = o_red + my_red;
+            ctr->n_items = o_item + my_item;
+            ctr->n_small = o_small + my_small;
+        }
+
+        // ---- phase C: CSR, chunk heads, items / small entries (lane = stencil slot) ----
+        for (int i = 0; i < NBB_TILE; ++i) {
+            const uint32_t b = tb + i;
+            if (b >= B) break;  // warp-uniform
+            const uint32_t k = lane < 27 ? s_k[w][i][lane] : 0xffffffffu;
+            const uint32_t cl = lane < 27 ? s_c[w][i][lane] : 0u;
+            const bool ok = k != 0xffffffffu;
+            const uint32_t m = __ballot_sync(FULL, ok);
+            const uint32_t e0 = __shfl_sync(FULL, o_nbr, i);
+            const unsigned long long rb = __shfl_sync(FULL, o_red, i);
+            uint32_t incl = cl;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                const uint32_t y = __shfl_up_sync(FULL, incl, o);
                 if (lane >= (unsigned)o) incl += y;
             }
             // records of the slots before the centre (13) = offset of the box's own segment in its run
-            const uint32_t cen = __shfl_sync(0xffffffffu, incl - cnt_l, 13);
-            if (ok[u]) {
-                const uint32_t e = nbr_off[b] + __popc(m & ((1u << lane) - 1u));
-                nbr_box[e] = k[u];
+            const uint32_t cen = __shfl_sync(FULL, incl - cl, 13);
+            if (ok) {
+                const uint32_t e = e0 + __popc(m & ((1u << lane) - 1u));
+                nbr_box[e] = k;
                 nbr_slot[e] = (uint8_t)lane;
                 if ((e & 31u) == 0u) {  // head of a restructure chunk
                     chunk_box[e >> 5] = b;
-                    chunk_out[e >> 5] = red_off[b] + (incl - cnt_l);
+                    chunk_out[e >> 5] = rb + (incl - cl);
                 }
             }
-            const uint32_t key = bkey[b];
-            if (key < g.tkey_lo || key > g.tkey_hi) continue;  // halo box: source only
-            const uint32_t s0 = bstart[b], nb_b = bstart[b + 1] - s0;
-            const uint32_t nch = item_cnt[b];
-            if (nch == 0) {  // small box (k_nbr_count): thread-per-target path
-                if (lane < (nb_b + 1) / 2) {  // one entry per target pair
-                    small_tgt[small_off[b] + lane] = s0 + 2 * lane;
-                    small_box[small_off[b] + lane] = b;
+            const bool tgt = __shfl_sync(FULL, (uint32_t)mtarget, i) != 0u;
+            if (!tgt) continue;
+            const uint32_t s0 = __shfl_sync(FULL, ms0, i), nb_b = __shfl_sync(FULL, my_nb, i);
+            const uint32_t nch = __shfl_sync(FULL, my_item, i);
+            if (nch == 0) {  // small box: thread-per-target path, one entry per target pair
+                const uint32_t so = __shfl_sync(FULL, o_small, i);
+                if (lane < (nb_b + 1) / 2) {
+                    small_tgt[so + lane] = s0 + 2 * lane;
+                    small_box[so + lane] = b;
                 }
                 continue;
             }
-            const uint32_t it = item_off[b];
-            const unsigned long long rb = red_off[b];
-            const uint32_t Rb = (uint32_t)(red_off[b + 1] - rb);
+            const uint32_t it = __shfl_sync(FULL, o_item, i);
+            const uint32_t key = __shfl_sync(FULL, mkey, i);
+            const uint32_t Rb = (uint32_t)__shfl_sync(FULL, my_red, i);
             for (uint32_t ci = lane; ci < nch; ci += 32) {
                 const uint32_t a0 = (uint32_t)(((uint64_t)nb_b * ci) / nch);
                 const uint32_t z0 = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
@@ -331,10 +440,13 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Geom g, const uint32_t *__rest
                 items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16), key, rb, Rb, cen + a0};
             }
         }
+        __syncwarp();  // phase C's shared-memory reads before the next tile's phase A writes
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(FULL, pairs, o);
+    if (lane == 0 && pairs) atomicAdd(&ctr->I, pairs);
 }
 
-// Helmholtz: 9-slot table, missing -> 0xffffffff (C10); boxes must be full (t samples, distinct sub-cells)
 __global__ void k_helm_check(const uint32_t *__restrict__ skey, uint32_t n, DevCounters *ctr) {
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x + 1; p < n; p += gridDim.x * blockDim.x)
         if (skey[p] == skey[p - 1]) atomicOr(&ctr->irregular, 1u);
@@ -373,51 +485,25 @@ __global__ void k_helm_nbr(const Geom g, uint32_t t, const uint32_t *__restrict_
     if ((threadIdx.x & 31u) == 0 && pairs) atomicAdd(&ctr->I, pairs);
 }
 
-// ------------------------------------------------------------------------------------------------
-// scan functors over plain arrays
-template <typename T>
-struct ArrGet {
-    const T *a;
-    __device__ T operator()(uint64_t i) const { return a[i]; }
-};
-template <typename T>
-struct OffPut {
-    T *off;
-    const uint32_t *nptr;
-    __device__ void operator()(uint64_t i, T e, T v) const {
-        off[i] = e;
-        if (i == (uint64_t)*nptr - 1) off[i + 1] = e + v;
-    }
-};
-
 static unsigned grid_for(uint64_t n, int threads, int num_sms) {
     uint64_t g = (n + threads - 1) / threads;
     uint64_t cap = (uint64_t)num_sms * 16;
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, cap));
 }
 
-// ------------------------------------------------------------------------------------------------
-static unsigned warp_grid(uint64_t nwork, int num_sms) {
-    // one warp per work unit, 8 warps per block, at most 16 resident blocks per SM (grid-stride beyond)
-    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(div_up(nwork, 8), (uint64_t)num_sms * 8));  // one full-occupancy wave
-}
-
 void free_capacity(p2p_plan *P) {
     cudaStream_t st = P->stream;
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
-                    P->s_nbr_cnt, P->s_item_cnt, P->s_item_off, P->s_red_cnt, P->s_small_cnt, P->s_small_off,
-                    P->s_slot_tab, P->boxinfo,
+                    P->s_nb_status, P->boxinfo,
                     P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, P->rec, P->bkey, P->bstart,
                     P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
-    P->s_nbr_cnt = P->s_item_cnt = P->s_item_off = nullptr;
-    P->s_slot_tab = nullptr;
+    P->s_nb_status = nullptr;
     P->boxinfo = nullptr;
-    P->s_small_cnt = P->s_small_off = P->small_tgt = P->small_box = P->chunk_box = nullptr;
+    P->small_tgt = P->small_box = P->chunk_box = nullptr;
     P->chunk_out = nullptr;
-    P->s_red_cnt = nullptr;
     P->rec = nullptr;
     P->bkey = P->bstart = P->nbr_off = P->nbr_box = P->box_of = P->occ = nullptr;
     P->nbr_slot = nullptr;
@@ -454,16 +540,10 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, (size_t)nslot * bcap, st));
     if (grav) {
         P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_nbr_cnt, 4 * bcap, st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_slot_tab, sizeof(uint2) * 27 * bcap, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_nb_status, sizeof(NbTileStatus) * div_up(bcap, NBB_TILE), st));
         P2P_CUDA_TRY(dalloc((void **)&P->boxinfo, sizeof(uint2) * keyspace, st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_item_cnt, 4 * bcap, st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_item_off, 4 * (bcap + 1), st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_small_cnt, 4 * bcap, st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_small_off, 4 * (bcap + 1), st));
         P2P_CUDA_TRY(dalloc((void **)&P->small_tgt, 4 * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->small_box, 4 * n, st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_red_cnt, 8 * bcap, st));
         P2P_CUDA_TRY(dalloc((void **)&P->red_off, 8 * (bcap + 1), st));
         P2P_CUDA_TRY(dalloc((void **)&P->items, sizeof(Item) * n, st));
         const uint64_t nchunk = div_up((uint64_t)nslot * bcap, 32) + 1;
@@ -512,26 +592,16 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
                                        &P->ctr->B, P->s_partials, st));
     // a5
     const uint64_t bcap = (uint64_t)P->bcap;
-    const unsigned gw = warp_grid(bcap, P->num_sms);
-    const uint32_t tmax = ITEM_TMAX;
+    const uint64_t ntile_cap = div_up(bcap, NBB_TILE);
     P2P_LAUNCH(k_boxinfo, std::max<unsigned>(1, std::min<unsigned>(div_up(bcap, 256), (unsigned)P->num_sms * 8)), 256,
                0, st, P->bkey, P->bstart, P->ctr, P->boxinfo);
-    P2P_LAUNCH(k_nbr_count, gw, 256, 0, st, P->geom, P->bkey, P->boxinfo, P->occ, P->ctr, P->s_nbr_cnt,
-               P->s_red_cnt, P->s_item_cnt, P->s_small_cnt, P->s_slot_tab, tmax);
-    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_nbr_cnt}, OffPut<uint32_t>{P->nbr_off, &P->ctr->B},
-                                       &P->ctr->B, bcap, &P->ctr->n_nbr, P->s_partials, st));
-    P2P_CUDA_TRY(device_scan<unsigned long long>(
-        ArrGet<unsigned long long>{(const unsigned long long *)P->s_red_cnt},
-        OffPut<unsigned long long>{(unsigned long long *)P->red_off, &P->ctr->B}, &P->ctr->B, bcap, &P->ctr->R,
-        P->s_partials, st));
-    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_item_cnt}, OffPut<uint32_t>{P->s_item_off, &P->ctr->B},
-                                       &P->ctr->B, bcap, &P->ctr->n_items, P->s_partials, st));
-    P2P_CUDA_TRY(device_scan<uint32_t>(ArrGet<uint32_t>{P->s_small_cnt}, OffPut<uint32_t>{P->s_small_off, &P->ctr->B},
-                                       &P->ctr->B, bcap, &P->ctr->n_small, P->s_partials, st));
-    P2P_LAUNCH(k_nbr_fill, gw, 256, 0, st, P->geom, P->bkey, P->bstart, P->s_slot_tab, P->ctr, P->nbr_off,
-               P->s_item_off, P->s_item_cnt, P->nbr_box, P->nbr_slot, P->items, P->s_small_off, P->small_tgt,
-               P->small_box, (const unsigned long long *)P->red_off, P->chunk_box, P->chunk_out,
-               (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));
+    P2P_CUDA_TRY(cudaMemsetAsync(P->s_nb_status, 0, sizeof(NbTileStatus) * ntile_cap, st));
+    P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->nbr_tile, 0, sizeof(unsigned int), st));
+    P2P_LAUNCH(k_nbr_build, std::max<unsigned>(1, std::min<unsigned>(div_up(ntile_cap, NBB_WARPS), (unsigned)P->num_sms * 8)),
+               NBB_WARPS * 32, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, P->s_nb_status,
+               P->nbr_off, (unsigned long long *)P->red_off, P->nbr_box, P->nbr_slot, P->items, P->small_tgt,
+               P->small_box, P->chunk_box, P->chunk_out, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32),
+               (uint32_t)ITEM_TMAX);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }

@@ -24,7 +24,16 @@ struct DevCounters {
     unsigned int sort_tile_ctr[4]; // onesweep tile counters, one per pass
     unsigned int n_small;          // targets of small boxes (thread-per-target path of the eval)
     unsigned int small_head;       // eval small-target queue head (reset before every eval)
-    unsigned int pad[1];
+    unsigned int nbr_tile;         // k_nbr_build look-back tile counter (reset before every build)
+};
+
+// k_nbr_build decoupled look-back status of one 32-box tile: the flag word is written last (1 = aggregate,
+// 2 = inclusive prefix), each in its own slot so a reader never sees a half-updated value set.
+// Values: {CSR entries, redundant records, work items, small target pairs}.
+struct NbTileStatus {
+    unsigned long long flag;
+    unsigned long long agg[3];  // [0] n_nbr, [1] R, [2] items | small << 32
+    unsigned long long inc[3];
 };
 
 // eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
@@ -94,16 +103,13 @@ struct p2p_plan {
     uint32_t *s_key = nullptr, *s_idx = nullptr, *s_kalt = nullptr, *s_valt = nullptr;
     uint32_t *s_hist = nullptr, *s_status = nullptr;
     void *s_partials = nullptr;
-    uint32_t *s_nbr_cnt = nullptr, *s_item_cnt = nullptr, *s_item_off = nullptr;
-    uint2 *s_slot_tab = nullptr;  // [27 B] k_nbr_count -> k_nbr_fill: {neighbour box, n_k} per stencil slot (x = ~0u: none)
+    p2p::NbTileStatus *s_nb_status = nullptr;  // [ceil(B / 32)] k_nbr_build look-back words
     uint2 *boxinfo = nullptr;     // gravity: dense Morton key -> {box, n_b} (valid where occ has the bit set)
-    uint32_t *s_small_cnt = nullptr, *s_small_off = nullptr;
     uint32_t *small_tgt = nullptr, *small_box = nullptr;  // sorted target index / its box, small boxes only
     // restructure chunks: every 32 consecutive CSR entries e = 32 c .. 32 c + 31 form one chunk; their redundant
     // segments are one contiguous range of red[] starting at chunk_out[c]; chunk_box[c] = box owning entry 32 c
     uint32_t *chunk_box = nullptr;
     unsigned long long *chunk_out = nullptr;
-    uint64_t *s_red_cnt = nullptr;
     bool sizes_known = false;  // host copies of B, n_nbr, R, I, n_items valid (false after an async update)
     // ---- multi-GPU: this rank owns the target boxes of one contiguous Morton range ----
     p2p::CommBase *comm = nullptr;
