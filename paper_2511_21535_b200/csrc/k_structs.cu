@@ -313,70 +313,51 @@ __global__ void __launch_bounds__(NBB_WARPS * 32) k_nbr_build(
                 in_red += d;
             }
         }
-        unsigned long long p_nbr = 0, p_red = 0, p_is = 0;  // tile prefix (items | small << 32)
-        const unsigned long long a_nbr = __shfl_sync(FULL, (unsigned long long)in_nbr, 31);
-        const unsigned long long a_red = __shfl_sync(FULL, in_red, 31);
-        const unsigned long long a_is = __shfl_sync(FULL, (unsigned long long)in_item | ((unsigned long long)in_small << 32), 31);
+        // tile aggregates (lane 31's inclusive values); items | small << 31 share one word
+        constexpr unsigned long long VMASK = (1ull << 62) - 1ull, F_AGG = 1ull << 62, F_INC = 2ull << 62;
+        unsigned long long agg[3];
+        agg[0] = __shfl_sync(FULL, (unsigned long long)in_nbr, 31);
+        agg[1] = __shfl_sync(FULL, in_red, 31);
+        agg[2] = __shfl_sync(FULL, (unsigned long long)in_item | ((unsigned long long)in_small << 31), 31);
+        unsigned long long pre[3] = {0ull, 0ull, 0ull};
         NbTileStatus *me = status + t;
+        const unsigned long long my_agg = lane == 0 ? agg[0] : (lane == 1 ? agg[1] : agg[2]);
         if (t == 0) {
-            if (lane == 0) {
-                st_vol64(&me->inc[0], a_nbr);
-                st_vol64(&me->inc[1], a_red);
-                st_vol64(&me->inc[2], a_is);
-                __threadfence();
-                st_vol64(&me->flag, 2ull);
-            }
+            if (lane < 3) st_vol64(&me->w[lane], F_INC | my_agg);
         } else {
-            if (lane == 0) {
-                st_vol64(&me->agg[0], a_nbr);
-                st_vol64(&me->agg[1], a_red);
-                st_vol64(&me->agg[2], a_is);
-                __threadfence();
-                st_vol64(&me->flag, 1ull);
-            }
-            // warp-parallel look-back: lane j inspects tile base - j; a window of 32 predecessors per step
-            for (int64_t base = (int64_t)t - 1;;) {
-                const int64_t q = base - (int64_t)lane;
-                unsigned long long f = 2ull;  // tiles before 0 act as an inclusive zero
-                if (q >= 0) {
-                    do {
-                        f = ld_vol64(&status[q].flag);
-                    } while (f == 0ull);
-                }
-                __threadfence();
-                const uint32_t incm = __ballot_sync(FULL, f == 2ull);
-                const int jstop = incm ? __ffs(incm) - 1 : 31;  // nearest inclusive predecessor in the window
-                unsigned long long v0 = 0, v1 = 0, v2 = 0;
-                if ((int)lane <= jstop && q >= 0) {
-                    const unsigned long long *v = f == 2ull ? status[q].inc : status[q].agg;
-                    v0 = ld_vol64(&v[0]);
-                    v1 = ld_vol64(&v[1]);
-                    v2 = ld_vol64(&v[2]);
-                }
+            if (lane < 3) st_vol64(&me->w[lane], F_AGG | my_agg);
+            // warp-parallel look-back, per word: lane j inspects tile base - j (a window of 32 predecessors per
+            // step) until the nearest inclusive prefix
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    v0 += __shfl_xor_sync(FULL, v0, o);
-                    v1 += __shfl_xor_sync(FULL, v1, o);
-                    v2 += __shfl_xor_sync(FULL, v2, o);
+            for (int wd = 0; wd < 3; ++wd) {
+                for (int64_t base = (int64_t)t - 1;;) {
+                    const int64_t q = base - (int64_t)lane;
+                    unsigned long long x = F_INC;  // tiles before 0 act as an inclusive zero
+                    if (q >= 0) {
+                        do {
+                            x = ld_vol64(&status[q].w[wd]);
+                        } while ((x >> 62) == 0ull);
+                    }
+                    const uint32_t incm = __ballot_sync(FULL, (x >> 62) == 2ull);
+                    const int jstop = incm ? __ffs(incm) - 1 : 31;  // nearest inclusive predecessor
+                    unsigned long long v = (int)lane <= jstop ? (x & VMASK) : 0ull;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+                    pre[wd] += v;
+                    if (incm) break;
+                    base -= 32;
                 }
-                p_nbr += v0;
-                p_red += v1;
-                p_is += v2;
-                if (incm) break;
-                base -= 32;
             }
-            if (lane == 0) {
-                st_vol64(&me->inc[0], p_nbr + a_nbr);
-                st_vol64(&me->inc[1], p_red + a_red);
-                st_vol64(&me->inc[2], p_is + a_is);
-                __threadfence();
-                st_vol64(&me->flag, 2ull);
+            if (lane < 3) {
+                const unsigned long long mine = (lane == 0 ? pre[0] : (lane == 1 ? pre[1] : pre[2])) + my_agg;
+                st_vol64(&me->w[lane], F_INC | mine);
             }
         }
+        const unsigned long long p_nbr = pre[0], p_red = pre[1], p_is = pre[2];
         const uint32_t o_nbr = (uint32_t)p_nbr + in_nbr - my_nbr;
         const unsigned long long o_red = p_red + in_red - my_red;
-        const uint32_t o_item = (uint32_t)p_is + in_item - my_item;
-        const uint32_t o_small = (uint32_t)(p_is >> 32) + in_small - my_small;
+        const uint32_t o_item = (uint32_t)(p_is & 0x7fffffffull) + in_item - my_item;
+        const uint32_t o_small = (uint32_t)(p_is >> 31) + in_small - my_small;
         if (have) {
             nbr_off[mb] = o_nbr;
             red_off[mb] = o_red;

@@ -27,15 +27,12 @@ struct DevCounters {
     unsigned int nbr_tile;         // k_nbr_build look-back tile counter (reset before every build)
 };
 
-// k_nbr_build decoupled look-back status of one 32-box tile: the flag word is written last (1 = aggregate,
-// 2 = inclusive prefix), each in its own slot so a reader never sees a half-updated value set.
-// Values: {CSR entries, redundant records, work items, small target pairs}.
+// k_nbr_build decoupled look-back status of one 32-box tile: three self-describing 64-bit words (no fences
+// needed: each is stored and loaded whole), word = flag << 62 | value, flag 1 = tile aggregate, 2 = inclusive
+// prefix.  Values: [0] CSR entries, [1] redundant records, [2] work items | small target pairs << 31.
 struct NbTileStatus {
-    unsigned long long flag;
-    unsigned long long agg[3];  // [0] n_nbr, [1] R, [2] items | small << 32
-    unsigned long long inc[3];
+    unsigned long long w[3];
 };
-
 // eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
 // meta = n_t | S << 8 | G << 16: the warp lane layout (G groups of K targets x S source splits, G*S <= 32)
 // key / red_base / R duplicate the box's Morton key and redundant run so the eval's one-item-ahead prefetch is a
