@@ -309,6 +309,43 @@ __device__ __forceinline__ double4 lds_rec<double4>(uint32_t a) {
     return v;
 }
 
+// shared-memory record load at a compile-time byte offset from a 32-bit shared address
+template <int OFF>
+__device__ __forceinline__ float4 lds_rec_off(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4+%5];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a), "n"(OFF) : "memory");
+    return v;
+}
+
+// the eval hot loop: nj sources at shared addresses sa, sa + ST, sa + 2 ST, ... (ST = S records), two per
+// iteration with one remainder step; the accumulators stay in the same registers (no IMAD.MOV copies on the
+// FMA-heavy pipe the FFMA2s run on)
+template <typename T, int K, int SS, typename TG, typename EP>
+__device__ __forceinline__ void hot_loop(TG &tg, uint32_t sa, uint32_t nj, const EP &E) {
+    constexpr int ST = SS * 16;
+    const uint32_t end2 = sa + (nj & ~1u) * (uint32_t)ST;
+#pragma unroll 1
+    for (; sa != end2; sa += 2 * ST) {
+        const float4 s0 = lds_rec<float4>(sa), s1 = lds_rec_off<ST>(sa);
+        tg.interact(s0, E);
+        tg.interact(s1, E);
+    }
+    if (nj & 1u) tg.interact(lds_rec<float4>(sa), E);
+}
+template <typename T, int K, typename TG, typename EP>
+__device__ __forceinline__ void hot_loop_rt(TG &tg, uint32_t sa, uint32_t nj, uint32_t stride, const EP &E) {
+    using V4 = typename V4T<T>::type;
+    const uint32_t end2 = sa + (nj & ~1u) * stride;
+#pragma unroll 1
+    for (; sa != end2; sa += 2 * stride) {
+        const V4 s0 = lds_rec<V4>(sa), s1 = lds_rec<V4>(sa + stride);
+        tg.interact(s0, E);
+        tg.interact(s1, E);
+    }
+    if (nj & 1u) tg.interact(lds_rec<V4>(sa), E);
+}
+
 __device__ __forceinline__ float4 ldro(const float4 *p) { return __ldg(p); }
 __device__ __forceinline__ double4 ldro(const double4 *p) {
     const double2 a = __ldg(reinterpret_cast<const double2 *>(p)), b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
@@ -446,7 +483,7 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
 }
 
 template <typename T, int LAYOUT, int K>
-__global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T> a) {
+__global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P_REDUNDANT ? 5 : 4) : 1) k_eval_gravity(const EvalArgs<T> a) {
     using V4 = typename V4T<T>::type;
     constexpr int CH = EV_STAGE_BYTES / (int)sizeof(V4);
     constexpr int STAGE_RECS = CH + EV_TGT;  // source chunk + the item's targets
@@ -668,17 +705,22 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k_eval_gravity(const EvalArgs<T
                 // registers (no IMAD.MOV copies, which would occupy the FMA-heavy pipe the FFMA2s run on), and
                 // the addresses advance by pointer increments (ALU pipe) instead of IMAD
                 const uint32_t nj = (((cnt - 1 - sl) * m20) >> 20) + 1;
-                // 32-bit shared-memory byte addresses advanced with IADD (ALU pipe), not IMAD (FMA-heavy pipe)
-                const uint32_t stride = S * (uint32_t)sizeof(V4);
-                uint32_t sa = smem_u32(stg + sl);
-                const uint32_t end2 = sa + (nj & ~1u) * stride;
-#pragma unroll 1
-                for (; sa != end2; sa += 2 * stride) {
-                    const V4 s0 = lds_rec<V4>(sa), s1 = lds_rec<V4>(sa + stride);
-                    tg.interact(s0, E);
-                    tg.interact(s1, E);
+                const uint32_t sa = smem_u32(stg + sl);
+                // the split stride S as a compile-time constant: the second source of an iteration is an
+                // immediate-offset LDS and the pointer advances once per two sources
+                if constexpr (sizeof(T) == 4) {
+                    switch (S) {
+                    case 32: hot_loop<T, K, 32>(tg, sa, nj, E); break;
+                    case 16: hot_loop<T, K, 16>(tg, sa, nj, E); break;
+                    case 10: hot_loop<T, K, 10>(tg, sa, nj, E); break;
+                    case 8: hot_loop<T, K, 8>(tg, sa, nj, E); break;
+                    case 6: hot_loop<T, K, 6>(tg, sa, nj, E); break;
+                    case 5: hot_loop<T, K, 5>(tg, sa, nj, E); break;
+                    default: hot_loop<T, K, 4>(tg, sa, nj, E); break;  // S >= 4 always (G <= 8)
+                    }
+                } else {
+                    hot_loop_rt<T, K>(tg, sa, nj, S * (uint32_t)sizeof(V4), E);
                 }
-                if (nj & 1u) tg.interact(lds_rec<V4>(sa), E);
             }
             __syncwarp();
             s ^= 1;
