@@ -324,14 +324,18 @@ __device__ __forceinline__ float4 lds_rec_off(uint32_t a) {
 template <typename T, int K, int SS, typename TG, typename EP>
 __device__ __forceinline__ void hot_loop(TG &tg, uint32_t sa, uint32_t nj, const EP &E) {
     constexpr int ST = SS * 16;
-    const uint32_t end2 = sa + (nj & ~1u) * (uint32_t)ST;
+    const uint32_t end4 = sa + (nj & ~3u) * (uint32_t)ST;
 #pragma unroll 1
-    for (; sa != end2; sa += 2 * ST) {
-        const float4 s0 = lds_rec<float4>(sa), s1 = lds_rec_off<ST>(sa);
+    for (; sa != end4; sa += 4 * ST) {
+        const float4 s0 = lds_rec<float4>(sa), s1 = lds_rec_off<ST>(sa), s2 = lds_rec_off<2 * ST>(sa),
+                     s3 = lds_rec_off<3 * ST>(sa);
         tg.interact(s0, E);
         tg.interact(s1, E);
+        tg.interact(s2, E);
+        tg.interact(s3, E);
     }
-    if (nj & 1u) tg.interact(lds_rec<float4>(sa), E);
+#pragma unroll 1
+    for (uint32_t r = nj & 3u; r; --r, sa += ST) tg.interact(lds_rec<float4>(sa), E);
 }
 template <typename T, int K, typename TG, typename EP>
 __device__ __forceinline__ void hot_loop_rt(TG &tg, uint32_t sa, uint32_t nj, uint32_t stride, const EP &E) {
