@@ -591,6 +591,11 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
                      nt * (uint32_t)sizeof(V4), &bar[s]);
     };
 
+    // the small boxes' targets (thread per target, L1/L2-latency bound) are taken first by one warp of every
+    // CTA, so their latency hides behind the FP32-bound item work of the CTA's other warps (run last by all
+    // warps, they would form a latency-bound tail)
+    const bool small_first = w == EV_WARPS - 1;
+    if (small_first) small_phase<T, LAYOUT>(a, lane);
     if (lane == 0) pend = atomicAdd(a.item_head, (uint32_t)EV_BATCH);
     const uint32_t first = next_index();
     if (first < n_items) {
@@ -777,8 +782,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
         if (!have_next) break;
     }
     }
-    // the small boxes' targets, thread per target (fills the tail of the item queue)
-    small_phase<T, LAYOUT>(a, lane);
+    // the remaining small boxes' targets, if any (fills the tail of the item queue)
+    if (!small_first) small_phase<T, LAYOUT>(a, lane);
 }
 
 template <typename T, int LAYOUT, int K>
