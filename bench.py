@@ -169,10 +169,10 @@ def ours(args, rank, world, local):
         dist.broadcast(idt, 0)
         comm = P.p2p_comm_create(world, rank, bytes(idt.cpu().numpy().tobytes()))
 
-    # 1 GPU: one persistent plan = the simulation's setup (allocations); every step rebuilds a1..a5 from the
-    # positions with p2p_plan_update (asynchronous: no host sync, no allocation), then a6, a7+a9.
-    # N GPUs: every step is the collective build (a1..a5 + histogram all-reduce + repartition + halo exchange
-    # over NCCL), a6, a7+a9 and the reverse all-to-all-v of the results.
+    # one persistent plan = the simulation's setup (allocations); every step rebuilds a1..a5 from the positions
+    # with p2p_plan_update (1 GPU: asynchronous, no host sync, no allocation), then a6, a7+a9.
+    # N GPUs: the update is collective (histogram all-reduce + repartition + halo exchange over NCCL, whose
+    # sizes need host syncs, then a1..a5 on the plan's buffers), a6, a7+a9 and the reverse all-to-all-v.
     splan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps, stream=stream,
                    comm=comm)
     holder = {"plan": splan}
@@ -181,13 +181,8 @@ def ours(args, rank, world, local):
         ev = events
         if ev:
             ev[0].record(stream)
-        if comm is None:
-            splan.update(pos, m)
-            plan = holder["plan"]
-        else:
-            holder["plan"].close()
-            plan = holder["plan"] = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps,
-                                           stream=stream, comm=comm)
+        splan.update(pos, m)   # N > 1: collective (repartition + halo exchange over NCCL, then a1..a5)
+        plan = holder["plan"]
         if ev:
             ev[1].record(stream)
         plan.restructure()

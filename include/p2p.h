@@ -115,7 +115,10 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
  * synchronisation and, in steady state, no allocation -- box / neighbour / buffer counts stay on the device
  * (the redundant buffer is sized for the worst case R <= 27 n_local).  Input errors detected on the device
  * (P2P_ERR_OUT_OF_DOMAIN) are reported by the next synchronising call (p2p_get_info / p2p_copy_out); results
- * computed in between are undefined.  Invalidates red[] (restructure again).  Helmholtz: P2P_ERR_UNSUPPORTED. */
+ * computed in between are undefined.  Invalidates red[] (restructure again).  Helmholtz: P2P_ERR_UNSUPPORTED.
+ * Multi-GPU plans (cfg->comm): COLLECTIVE, every rank calls with its new input slice; the repartition and halo
+ * exchange run again (their sizes need host synchronisations for the NCCL counts), the local structures reuse
+ * the plan's buffers as above. */
 p2p_status p2p_plan_update(p2p_plan *plan, int64_t n_local, const void *positions, const void *charges);
 
 /* Host-buffer variants of p2p_plan_update / p2p_eval: the end-to-end path of a time-stepping code whose
@@ -191,8 +194,9 @@ void p2p_comm_destroy(p2p_comm *comm);
  * (p2p_partition_splitters), exchange whole halo boxes, and each rank evaluates the targets of its range;
  * p2p_eval returns every result to the rank and input slot it came from.  Results are bitwise identical to a
  * 1-GPU plan over the rank-major concatenation of the slices.  p2p_get_info / p2p_copy_out describe the rank's
- * LOCAL plan (owned + halo particles; halo boxes have empty neighbour lists and runs).  p2p_plan_update and
- * p2p_set_charges return P2P_ERR_UNSUPPORTED for multi-GPU plans (re-create the plan). */
+ * LOCAL plan (owned + halo particles; halo boxes have empty neighbour lists and runs).  p2p_plan_update is
+ * collective too (a new time step: the partition is recomputed); p2p_set_charges and the host-buffer entry
+ * points return P2P_ERR_UNSUPPORTED for multi-GPU plans. */
 
 /* The count-balanced splitters of SURVEY §8e / DESIGN C20, as computed inside the collective plan build
  * (exported for testing the host logic): hist[nbins] = global particle counts per supercell (supercell =

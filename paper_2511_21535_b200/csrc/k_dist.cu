@@ -56,6 +56,11 @@ __global__ void k_sc_hist(const uint32_t *__restrict__ key, uint32_t n, int shif
         atomicAdd(&hist[key[i] >> shift], 1ull);
 }
 
+// hist[nbins] = 1 if this rank saw an out-of-domain input (summed over ranks by the all-reduce)
+__global__ void k_err_flag(const unsigned long long *err, unsigned long long *flag) {
+    *flag = *err != ~0ull ? 1ull : 0ull;
+}
+
 __device__ __forceinline__ int owner_of(uint32_t key, const uint32_t *spl, int G) {
     int lo = 0, hi = G - 1;  // largest r with spl[r] <= key
     while (lo < hi) {
@@ -227,6 +232,7 @@ struct Tmp {  // stream-ordered temporaries of the build
 template <typename T>
 p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
     using V4 = typename V4T<T>::type;
+    free_distributed(P);  // a previous build's exchange buffers (p2p_plan_update on a collective plan)
     CommBase *C = P->comm;
     const int G = C->nranks, me = C->rank;
     cudaStream_t st = P->stream;
@@ -253,15 +259,13 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
     P2P_CUDA_TRY(tmp.get(&hist, 8 * (nbins + 1)));
     P2P_CUDA_TRY(cudaMemsetAsync(hist, 0, 8 * (nbins + 1), st));
     if (n_in) P2P_LAUNCH(k_sc_hist, gb, 256, 0, st, key, n_in, shift, hist);
-    unsigned long long herr = ~0ull;
-    P2P_CUDA_TRY(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, st));
-    P2P_CUDA_TRY(cudaStreamSynchronize(st));
-    const unsigned long long bad_rank = herr != ~0ull ? 1ull : 0ull;
-    P2P_CUDA_TRY(cudaMemcpyAsync(hist + nbins, &bad_rank, 8, cudaMemcpyHostToDevice, st));
+    P2P_LAUNCH(k_err_flag, 1, 1, 0, st, err, hist + nbins);
     p2p_status s = C->allreduce_sum_u64(hist, nbins + 1, st);
     if (s != P2P_OK) return s;
     std::vector<unsigned long long> h(nbins + 1);
+    unsigned long long herr = ~0ull;
     P2P_CUDA_TRY(cudaMemcpyAsync(h.data(), hist, 8 * (nbins + 1), cudaMemcpyDeviceToHost, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, st));
     P2P_CUDA_TRY(cudaStreamSynchronize(st));
     if (h[nbins]) {  // every rank bails out consistently
         if (herr != ~0ull) {
@@ -403,18 +407,21 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
         if (s != P2P_OK) return s;
     }
     // ---- 7. the local plan over [owned ; halo], targets = this rank's Morton range ----
+    // capacity buffers persist across p2p_plan_update calls (grow only); the temporaries above are released
+    // stream-ordered (cudaFreeAsync), after every collective that reads them has completed on this stream
     P->n = n_own + n_halo;
     if (P->n == 0) return P2P_OK;
-    s = alloc_capacity(P, P->n);
-    if (s != P2P_OK) return s;
+    if (P->n > P->cap) {
+        free_capacity(P);
+        s = alloc_capacity(P, P->n);
+        if (s != P2P_OK) return s;
+    }
     s = build_gravity_structs(P, nullptr, nullptr, local);
     if (s != P2P_OK) return s;
     P2P_CUDA_TRY(dalloc(&P->phi_loc, sizeof(T) * std::max<int64_t>(n_own, 1), st));
     P2P_CUDA_TRY(dalloc(&P->field_loc, 3 * sizeof(T) * std::max<int64_t>(n_own, 1), st));
     P2P_CUDA_TRY(dalloc(&P->res_own, sizeof(V4) * std::max<int64_t>(n_own, 1), st));
     P2P_CUDA_TRY(dalloc(&P->res_back, sizeof(V4) * nn, st));
-    // keep the temporaries alive until the stream passes them (the caller synchronises right after)
-    P2P_CUDA_TRY(cudaStreamSynchronize(st));
     return P2P_OK;
 }
 

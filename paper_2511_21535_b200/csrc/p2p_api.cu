@@ -323,12 +323,39 @@ p2p_status p2p_plan_update(p2p_plan *P, int64_t n_local, const void *positions, 
     if (s != P2P_OK) return s;
     if (P->cfg.kernel != P2P_GRAVITY)
         return fail(P2P_ERR_UNSUPPORTED, "p2p_plan_update is for gravity plans (DBIM geometry is fixed: use set_charges)");
-    if (P->comm) return fail(P2P_ERR_UNSUPPORTED, "multi-GPU plans are rebuilt with p2p_plan_create (collective)");
     if (n_local < 0) return fail(P2P_ERR_INVALID_ARGUMENT, "n_local < 0");
     if (n_local >= (int64_t)1 << 31) return fail(P2P_ERR_UNSUPPORTED, "n_local >= 2^31 (u32 indices)");
     if (n_local > 0 && (!is_device_ptr(positions) || !is_device_ptr(charges)))
         return fail(P2P_ERR_INVALID_ARGUMENT, "positions / charges must be device pointers");
     cudaStream_t st = P->stream;
+    if (P->comm) {
+        // collective rebuild (every rank calls): the exchange sizes need the host (NCCL counts), the local
+        // structures reuse the plan's capacity buffers and stay device-side like the single-GPU update
+        P->n_in = n_local;
+        P->sizes_known = false;
+        P->red_valid = false;
+        cudaMemsetAsync(P->ctr, 0, sizeof(DevCounters), st);
+        cudaMemsetAsync(&P->ctr->err_index, 0xff, sizeof(unsigned long long), st);
+        p2p_status bs = build_distributed(P, positions, charges);
+        if (bs != P2P_OK) return mark(P, bs);
+        const int64_t need = std::max<int64_t>(27 * P->n, 1);
+        if (P->red_cap < need) {
+            dfree(P->red, st);
+            const size_t rec_sz = P->cfg.precision == P2P_FP64 ? sizeof(double4) : sizeof(float4);
+            if (dalloc(&P->red, rec_sz * (size_t)need, st) != cudaSuccess) {
+                P->red = nullptr;
+                P->red_cap = 0;
+                P->sticky = P2P_ERR_OUT_OF_MEMORY;
+                return fail(P2P_ERR_OUT_OF_MEMORY, "cannot allocate the redundant buffer");
+            }
+            P->red_cap = need;
+        }
+        if (P->n == 0) {
+            P->sizes_known = true;
+            P->B = P->n_nbr = P->R = P->I = P->n_items = 0;
+        }
+        return P2P_OK;
+    }
     if (n_local > P->cap) {  // grow (stream-ordered; steady-state time steps never get here)
         free_capacity(P);
         if (alloc_capacity(P, n_local) != P2P_OK) {

@@ -142,3 +142,58 @@ def test_multirank_rank_with_no_particles(P):
     ref, _ = single(P, inp, [P.P2P_REDUNDANT])
     assert out[0][P.P2P_REDUNDANT][0].tobytes() == ref[P.P2P_REDUNDANT][0].tobytes()
     assert out[1][P.P2P_REDUNDANT][0].size == 0
+
+
+@pytest.mark.parametrize("nr", [2, 3])
+def test_multirank_plan_update_time_steps(P, nr):
+    """p2p_plan_update on a collective plan (a new time step on every rank, the partition recomputed, the plan's
+    buffers reused; N per rank changes between steps): bitwise equal to a 1-GPU plan of each step's input"""
+    steps = [G.plummer(9000, 8, seed=31), G.plummer(12000, 8, seed=32), G.uniform_per_box(8, 3, seed=33)]
+    lay = P.P2P_REDUNDANT
+    grp = P.p2p_loopback_group_create(nr)
+    comms = [P.p2p_comm_create_loopback(grp, r) for r in range(nr)]
+    rng = np.random.default_rng(5)
+    cuts = []
+    for inp in steps:
+        c = np.sort(rng.choice(np.arange(1, inp.n), size=nr - 1, replace=False))
+        cuts.append([0, *c.tolist(), inp.n])
+    out = [[None] * nr for _ in steps]
+    errs = []
+
+    def rank_main(r):
+        try:
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                plan = None
+                for k, inp in enumerate(steps):
+                    sl = slice(cuts[k][r], cuts[k][r + 1])
+                    pos = torch.from_numpy(np.ascontiguousarray(inp.pos[sl])).cuda()
+                    m = torch.from_numpy(np.ascontiguousarray(inp.mass[sl])).cuda()
+                    if plan is None:
+                        plan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps,
+                                      stream=stream, comm=comms[r])
+                    else:
+                        plan.update(pos, m)
+                    plan.restructure()
+                    phi, f = plan.eval(lay)
+                    stream.synchronize()
+                    out[k][r] = (phi.cpu().numpy(), f.cpu().numpy())
+                plan.close()
+        except Exception as e:  # noqa: BLE001 -- surfaced below
+            errs.append((r, e))
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(nr)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for c in comms:
+        P.p2p_comm_destroy(c)
+    P.p2p_loopback_group_destroy(grp)
+    assert not errs, errs
+    for k, inp in enumerate(steps):
+        ref, _ = single(P, inp, [lay])
+        phi = np.concatenate([out[k][r][0] for r in range(nr)])
+        f = np.concatenate([out[k][r][1] for r in range(nr)])
+        assert phi.tobytes() == ref[lay][0].tobytes(), k
+        assert f.tobytes() == ref[lay][1].tobytes(), k
