@@ -50,34 +50,6 @@ __constant__ uint32_t c_m20[33] = {0,       1048576, 524288, 349526, 262144, 209
                                    58255,   55189,   52429,  49933,  47663,  45591,  43691,  41944,  40330,
                                    38837,   37450,   36158,  34953,  33826,  32768};
 
-typedef unsigned long long u64;
-__device__ __forceinline__ u64 pk2(float a, float b) {
-    u64 r;
-    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void upk2(u64 v, float &a, float &b) { asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
-__device__ __forceinline__ u64 add2(u64 a, u64 b) {
-    u64 d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
-    u64 d;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-    u64 d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
-    u64 d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-
 template <typename T>
 struct EvalArgs {
     Geom g;
@@ -153,32 +125,13 @@ struct Tgt<float, K> {
             az[p] = __ffma2_rn(m3, dz, az[p]);
         }
     }
-    __device__ __forceinline__ void reduce(uint32_t S, uint32_t sl) {
-        for (uint32_t off = 1; off < S; off <<= 1) {
-            const bool take = sl + off < S;
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                float2 v[4] = {ap[p], ax[p], ay[p], az[p]};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    v[q].x = __shfl_down_sync(0xffffffffu, v[q].x, off);
-                    v[q].y = __shfl_down_sync(0xffffffffu, v[q].y, off);
-                }
-                if (take) {
-                    ap[p] = __fadd2_rn(ap[p], v[0]);
-                    ax[p] = __fadd2_rn(ax[p], v[1]);
-                    ay[p] = __fadd2_rn(ay[p], v[2]);
-                    az[p] = __fadd2_rn(az[p], v[3]);
-                }
-            }
-        }
-    }
     // Transpose-reduce of the S source splits of a group (K = 4: 16 values per lane, f = 4 q + k with q = 0
     // potential, 1..3 field, k = target): each level exchanges HALF of the remaining values with the partner
     // split and keeps the other half, so log2(S) levels cost 8 + 4 + 2 + 1 shuffles instead of 16 per level.
     // A non-power-of-two S first folds its tail splits [Sp, S) onto [0, S - Sp).  Afterwards split sl < Sp
-    // holds the cnt = 16 >> min(lg, 4) consecutive values f0 .. f0 + cnt - 1 in v[]; `own` marks the lanes
-    // whose values are final and unique.  Fixed exchange pattern -> deterministic.
+    // (lg = log2 Sp, Lh = min(lg, 4)) holds the cnt = 16 >> Lh consecutive values f0 .. f0 + cnt - 1 in v[],
+    // f0 = (sl >> (lg - Lh)) * cnt; for lg = 5 only the even splits' values are unique.  Fixed exchange pattern
+    // -> deterministic.
     template <int H>
     static __device__ __forceinline__ void tr_level(float2 (&w)[8], uint32_t sl, uint32_t gbase, uint32_t o) {
         const bool up = (sl & o) != 0u;
@@ -191,8 +144,7 @@ struct Tgt<float, K> {
             w[i] = __fadd2_rn(kp, r);
         }
     }
-    __device__ __forceinline__ void treduce(uint32_t S, uint32_t sl, uint32_t gbase, float (&v)[4], uint32_t &f0,
-                                            uint32_t &cnt, bool &own) const {
+    __device__ __forceinline__ void treduce(uint32_t S, uint32_t sl, uint32_t gbase, float (&v)[4]) const {
         static_assert(K == 4, "transpose-reduce is written for K = 4");
         float2 w[8] = {ap[0], ap[1], ax[0], ax[1], ay[0], ay[1], az[0], az[1]};
         uint32_t Sp = S;
@@ -218,10 +170,6 @@ struct Tgt<float, K> {
             w[0].x = kp + __shfl_sync(0xffffffffu, snd, (gbase + (sl ^ o)) & 31u);
         }
         if (lg == 5) w[0].x += __shfl_xor_sync(0xffffffffu, w[0].x, 1);
-        const uint32_t Lh = lg < 4u ? lg : 4u;
-        cnt = 16u >> Lh;
-        f0 = (sl >> (lg - Lh)) * cnt;
-        own = sl < Sp && (lg < 5u || (sl & 1u) == 0u);
         v[0] = w[0].x;
         v[1] = w[0].y;
         v[2] = w[1].x;
@@ -354,36 +302,6 @@ __device__ __forceinline__ float4 ldro(const float4 *p) { return __ldg(p); }
 __device__ __forceinline__ double4 ldro(const double4 *p) {
     const double2 a = __ldg(reinterpret_cast<const double2 *>(p)), b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
     return make_double4(a.x, a.y, b.x, b.y);
-}
-
-template <typename T>
-__device__ __forceinline__ void interact1(const typename V4T<T>::type &s, T tx, T ty, T tz, T e2, T &ap, T &ax,
-                                          T &ay, T &az) {
-    if constexpr (std::is_same<T, float>::value) {
-        const float dx = __fsub_rn(s.x, tx), dy = __fsub_rn(s.y, ty), dz = __fsub_rn(s.z, tz);
-        float r2 = __fmaf_rn(dx, dx, e2);
-        r2 = __fmaf_rn(dy, dy, r2);
-        r2 = __fmaf_rn(dz, dz, r2);
-        const float ri = rsqrt_ftz(r2);
-        const float mri = __fmul_rn(s.w, ri);
-        ap = __fadd_rn(ap, mri);
-        const float m3 = __fmul_rn(mri, __fmul_rn(ri, ri));
-        ax = __fmaf_rn(m3, dx, ax);
-        ay = __fmaf_rn(m3, dy, ay);
-        az = __fmaf_rn(m3, dz, az);
-    } else {
-        const double dx = __dsub_rn(s.x, tx), dy = __dsub_rn(s.y, ty), dz = __dsub_rn(s.z, tz);
-        double r2 = __fma_rn(dx, dx, e2);
-        r2 = __fma_rn(dy, dy, r2);
-        r2 = __fma_rn(dz, dz, r2);
-        const double ri = 1.0 / sqrt(r2);
-        const double mri = __dmul_rn(s.w, ri);
-        ap = __dadd_rn(ap, mri);
-        const double m3 = __dmul_rn(mri, __dmul_rn(ri, ri));
-        ax = __fma_rn(m3, dx, ax);
-        ay = __fma_rn(m3, dy, ay);
-        az = __fma_rn(m3, dz, az);
-    }
 }
 
 template <typename T, int LAYOUT>
@@ -739,9 +657,11 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
         // ---- a9: scatter to input order; remove the self potential term (DESIGN C3) ----
         if constexpr (sizeof(T) == 4) {
             float v[4];
-            uint32_t f0, vcnt;
-            bool own;
-            tg.treduce(S, sl, g * S, v, f0, vcnt, own);
+            tg.treduce(S, sl, g * S, v);
+            // the lane's values after the transpose-reduce (see Tgt::treduce): f0 .. f0 + vcnt - 1
+            const uint32_t lg = 31u - __clz(S);  // log2 of the power-of-two part of S
+            const uint32_t Lh = lg < 4u ? lg : 4u, vcnt = 16u >> Lh, f0 = (sl >> (lg - Lh)) * vcnt;
+            const bool own = sl < (1u << lg) && (lg < 5u || (sl & 1u) == 0u);
             if (active && own) {
                 const T rs = Tgt<T, K>::self_rinv(eps2);
 #pragma unroll
