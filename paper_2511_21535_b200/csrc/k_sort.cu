@@ -5,9 +5,10 @@
 //   k_radix_hist      one pass over the keys builds the 256-bin histogram of EVERY digit at once
 //   k_radix_hist_scan exclusive scan of each digit histogram -> global digit offsets
 //   k_radix_pass      per digit: each CTA takes the next 4096-key tile (tile ids handed out by an atomic
-//                     counter in launch order, so look-back never waits on an unscheduled tile), ranks its
-//                     keys stably with warp-level match (__match_any_sync) in input order, publishes its
-//                     per-digit counts, decoupled look-back over earlier tiles for the exclusive prefix,
+//                     counter in launch order, so look-back never waits on an unscheduled tile), counts its
+//                     digits, publishes them and resolves its exclusive prefix by decoupled look-back over
+//                     earlier tiles (before the ranking: the inclusive prefixes propagate at look-back speed),
+//                     ranks its keys stably with warp-level match (__match_any_sync) in input order,
 //                     stages the tile in shared memory in digit order and writes each digit run
 //                     contiguously (coalesced) to its global position.
 // Stability: within a tile keys are ranked in (warp, item, lane) order, which is input order; tiles are
@@ -93,10 +94,12 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_pass(const uint32_t *__res
     __shared__ uint32_t s_vals[RS_TILE];
     __shared__ uint32_t s_wt[RS_WARPS];
     __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_thist[256];
 
     const unsigned tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
     for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) (&s_whist[0][0])[i] = 0;
+    s_thist[tid] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint32_t base = tile * RS_TILE;
@@ -110,6 +113,36 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_pass(const uint32_t *__res
         bool ok = idx < n;
         k[i] = ok ? kin[idx] : 0u;
         v[i] = ok ? vin[idx] : 0u;
+    }
+    // the tile's digit counts first (shared-memory atomics), published as the tile aggregate BEFORE the
+    // ranking: successors looking back find it early, and this tile's own look-back (after the ranking) mostly
+    // finds its predecessors already resolved
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; ++i)
+        if (seg + i * 32 + lane < n) atomicAdd(&s_thist[(k[i] >> shift) & 255u], 1u);
+    __syncthreads();
+    // per digit: publish the aggregate, look back for the exclusive prefix, publish the inclusive prefix --
+    // all BEFORE the ranking, so the chain of inclusive prefixes across tiles advances at look-back speed and the
+    // ranking work stays off it
+    {
+        const uint32_t d = tid, cnt = s_thist[d];
+        uint32_t *my = status + (size_t)tile * 256 + d;
+        uint32_t excl = 0;
+        if (tile == 0) {
+            st_volatile(my, FLAG_INC | cnt);
+        } else {
+            st_volatile(my, FLAG_AGG | cnt);
+            for (int64_t t = (int64_t)tile - 1;;) {
+                const uint32_t sv = ld_volatile(status + (size_t)t * 256 + d);
+                const uint32_t f = sv & ~VAL_MASK;
+                if (f == 0) continue;  // predecessor not published yet: spin
+                excl += sv & VAL_MASK;
+                if (f == FLAG_INC) break;
+                --t;
+            }
+            st_volatile(my, FLAG_INC | (excl + cnt));
+        }
+        s_goff[d] = digit_off[d] + excl;
     }
 #pragma unroll
     for (int i = 0; i < RS_ITEMS; ++i) {
@@ -128,7 +161,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_pass(const uint32_t *__res
     }
     __syncthreads();
 
-    // per digit: exclusive prefix across warps, tile count, tile-local digit start, look-back
+    // per digit: exclusive prefix across warps, tile-local digit start
     {
         const uint32_t d = tid;
         uint32_t sum = 0;
@@ -138,23 +171,6 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_pass(const uint32_t *__res
             s_whist[ww][d] = sum;
             sum += c;
         }
-        uint32_t *my = status + (size_t)tile * 256 + d;
-        if (tile == 0) st_volatile(my, FLAG_INC | sum);
-        else st_volatile(my, FLAG_AGG | sum);
-        uint32_t excl = 0;
-        if (tile > 0) {
-            int64_t t = (int64_t)tile - 1;
-            while (true) {
-                uint32_t s = ld_volatile(status + (size_t)t * 256 + d);
-                uint32_t f = s & ~VAL_MASK;
-                if (f == 0) continue;  // predecessor not published yet: spin
-                excl += s & VAL_MASK;
-                if (f == FLAG_INC) break;
-                --t;
-            }
-            st_volatile(my, FLAG_INC | (excl + sum));
-        }
-        s_goff[d] = digit_off[d] + excl;
         s_tdig[d] = block_excl_scan256(sum, s_wt, nullptr);
     }
     __syncthreads();
