@@ -17,6 +17,8 @@
 //
 // Helmholtz: Xg[b][s][j] = xs[bstart[nbr9[b][s]] + j] or 0 (zero-padded im2col, DESIGN C10), one thread
 // per element, fully coalesced.
+#include <cmath>
+
 #include "plan.hpp"
 
 namespace p2p {
@@ -35,7 +37,7 @@ __device__ __forceinline__ double slot_shift(const Geom &g, const uint32_t c[3],
     return 0.0;
 }
 
-template <typename T>
+template <typename T, bool EXACT32>
 __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const typename V4T<T>::type *__restrict__ rec,
                                                              const uint32_t *__restrict__ bkey,
                                                              const uint32_t *__restrict__ bstart,
@@ -124,6 +126,13 @@ __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const
         // chunks without any periodic image (all but the boundary layers) skip the shift selection: adding the
         // +0.0 shift keeps the oracle's rounding sequence (and its -0 -> +0 behaviour) exactly
         const bool wrap = __any_sync(FULL, seg && code != 0u);
+        // fp32 fast path (C11 unchanged bit for bit): with no periodic shift and every owner origin exactly an
+        // fp32 value, fl32(fl64(x + 0) - o) == fl32(fl32(x + 0) - o) -- a single subtraction of two fp32
+        // operands rounded through fp64 (53 >= 2*24 + 2 bits) rounds like the direct fp32 subtraction -- so the
+        // conversions and fp64 operations (6 F2F on the XU pipe per record) drop out
+        // (EXACT32: the host verified that every box origin of the grid is an fp32 value)
+        const float f0o = (float)o0, f1o = (float)o1, f2o = (float)o2;
+        const bool fast32 = EXACT32 && !wrap;
         constexpr int UNR = 4;
         for (uint32_t rb = 0; rb < Rc; rb += 32 * UNR) {
             V4 x[UNR];
@@ -142,6 +151,26 @@ __global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const
                 const uint32_t e_st = __shfl_sync(FULL, st, xe[u]);
                 const uint32_t r = r0 + lane;
                 if (r < Rc) x[u] = rec[e_src + (r - e_st)];
+            }
+            if (fast32) {
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const uint32_t r0 = rb + 32u * u;
+                    if (r0 >= Rc) break;
+                    const float eo0 = __shfl_sync(FULL, f0o, xe[u]);
+                    const float eo1 = __shfl_sync(FULL, f1o, xe[u]);
+                    const float eo2 = __shfl_sync(FULL, f2o, xe[u]);
+                    const uint32_t r = r0 + lane;
+                    if (r < Rc) {
+                        V4 v;
+                        v.x = (T)__fsub_rn(__fadd_rn((float)x[u].x, 0.0f), eo0);
+                        v.y = (T)__fsub_rn(__fadd_rn((float)x[u].y, 0.0f), eo1);
+                        v.z = (T)__fsub_rn(__fadd_rn((float)x[u].z, 0.0f), eo2);
+                        v.w = x[u].w;
+                        out[r] = v;
+                    }
+                }
+                continue;
             }
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
@@ -189,18 +218,32 @@ __global__ void k_restructure_helmholtz(const C2 *__restrict__ xs, const uint32_
 }
 }  // namespace
 
+// every box origin o_d = fma(c, h, lo_d), c < nbox_d, is exactly an fp32 value (the restructure's fp32 path)
+static bool origins_exact_fp32(const Geom &g) {
+    for (int d = 0; d < 3; ++d)
+        for (int c = 0; c < g.nbox[d]; ++c) {
+            const double o = std::fma((double)c, g.h, g.lo[d]);
+            if ((double)(float)o != o) return false;
+        }
+    return true;
+}
+
 p2p_status restructure_gravity(p2p_plan *P) {
     if (P->sizes_known && (P->B == 0 || P->n_nbr == 0)) return P2P_OK;
     // one warp per chunk of 32 CSR entries; the chunk count is device-side after an asynchronous update
     const uint64_t nchunk = div_up(P->sizes_known ? (uint64_t)P->n_nbr : 27ull * (uint64_t)P->bcap, 32);
     const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(div_up(nchunk * 32, 256), (unsigned)P->num_sms * 16));
     if (P->cfg.precision == P2P_FP64)
-        P2P_LAUNCH(k_restructure_gravity<double>, grid, 256, 0, P->stream, P->geom, (const double4 *)P->rec, P->bkey,
-                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
+        P2P_LAUNCH((k_restructure_gravity<double, false>), grid, 256, 0, P->stream, P->geom, (const double4 *)P->rec,
+                   P->bkey, P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
                    (double4 *)P->red);
+    else if (origins_exact_fp32(P->geom))
+        P2P_LAUNCH((k_restructure_gravity<float, true>), grid, 256, 0, P->stream, P->geom, (const float4 *)P->rec,
+                   P->bkey, P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
+                   (float4 *)P->red);
     else
-        P2P_LAUNCH(k_restructure_gravity<float>, grid, 256, 0, P->stream, P->geom, (const float4 *)P->rec, P->bkey,
-                   P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
+        P2P_LAUNCH((k_restructure_gravity<float, false>), grid, 256, 0, P->stream, P->geom, (const float4 *)P->rec,
+                   P->bkey, P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
                    (float4 *)P->red);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
