@@ -1,0 +1,334 @@
+// k_helm_tc.cu -- method step a8 (§5.1) on the 5th-generation tensor cores: Y = Xg P^T as ONE
+// real GEMM, fp32-accurate through 3xTF32 ("a 3xTF32 tensor-core variant of Y = X P^T under
+// the 1e-5 tolerance").
+//
+// Real form.  Xg[b] (9t complex, interleaved re/im) is a real row of K = 18t floats as stored -- the restructure
+// output is the A operand without any copy.  The pattern table becomes a real N x K matrix W (N = 2t):
+//   row i      (Re y_i):  W[i][2c] =  Re P[i][c],  W[i][2c+1]   = -Im P[i][c]
+//   row t + i  (Im y_i):  W[t+i][2c] = Im P[i][c],  W[t+i][2c+1] =  Re P[i][c]
+// so D[b][n] = sum_k Xg[b][k] W[n][k] holds Re y in columns < t and Im y in columns >= t.
+//
+// 3xTF32.  x = hi(x) + lo(x) with hi(x) = x rounded to the nearest TF32 value (low 13 mantissa bits zero, so the
+// tensor core reads it exactly) and lo(x) = x - hi(x) (exact in fp32, |lo| <= 2^-11 |x|); D = Xhi Whi + Xhi Wlo +
+// Xlo Whi, the dropped Xlo Wlo term and the TF32 reading of the lo parts are ~2^-22 relative per product.  W's parts are built once on the host (plan create); X is split
+// in shared memory after each TMA load (hi in place, lo into a second buffer with the same swizzled offsets).
+//
+// Kernel: one CTA per 128 boxes (M = 128), all N = 2t outputs in one TMEM accumulator (N fp32 columns).
+//   warp 4, one lane      TMA producer: 2D tensor loads (128-byte swizzle) of the X tile and both W tiles of
+//                         each 32-float K slice into a 3-stage ring (mbarrier full / empty)
+//   warps 0..3            split X of the landed slice; thread 0 then issues 4 K-steps x 3 tcgen05.mma
+//                         (kind::tf32, M = 128, N = 2t, K = 8, both operands K-major from shared memory
+//                         descriptors) and commits them to the stage's empty barrier
+//   epilogue (warps 0-3)  tcgen05.ld of the accumulator rows (TMEM lane = box), scatter to input order
+#include <cuda.h>
+
+#include <cstring>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace p2p {
+
+namespace {
+constexpr int TC_BM = 128;        // boxes per CTA (MMA M, TMEM lanes)
+constexpr int TC_BK = 32;         // floats per K slice = one 128-byte swizzle row
+constexpr int TC_STAGES = 3;
+constexpr int TC_THREADS = 160;   // 4 compute warps + 1 producer warp
+// TMEM accumulators (K slices round-robin, summed in fp32 at the end): as many as fit the 512 TMEM columns, at
+// most 8 -- the tensor core's internal fp32 accumulation loses ~2^-23 of the running sum per step (measured: one
+// accumulator 7.8e-6, four 2.0e-6 relative L2 at t = 64 vs the fp64 oracle)
+template <int N>
+constexpr int tc_nacc() { return (N < 32 ? 32 : N) * 8 <= 512 ? 8 : 512 / (N < 32 ? 32 : N); }
+
+__device__ __forceinline__ uint32_t cvta_smem(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// the nearest TF32 value (ties away from zero on the magnitude bits): |x - hi| <= 2^-11 |x|, and x - hi is exact
+// in fp32; finite inputs of this path never reach the exponent limit
+__device__ __forceinline__ float tf32_rn(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart (SBO), sm_100 version 1
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024u >> 4) << 32) |
+           ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(map), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int T>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_helm_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWhi,
+              const __grid_constant__ CUtensorMap tmWlo, const uint32_t *__restrict__ bstart,
+              const uint32_t *__restrict__ perm, uint32_t B, float2 *__restrict__ y) {
+    constexpr int N = 2 * T, K = 18 * T, NKT = K / TC_BK;
+    constexpr uint32_t X_BYTES = TC_BM * TC_BK * 4, W_BYTES = N * TC_BK * 4;
+    constexpr uint32_t STAGE_BYTES = 2 * X_BYTES + 2 * W_BYTES;  // X (hi in place), X lo, W hi, W lo
+    // NACC accumulators (K slices round-robin), summed in fp32 in the epilogue: the tensor core's fp32
+    // accumulation error grows with the number of accumulation steps into one accumulator
+    constexpr int NACC = tc_nacc<N>();
+    constexpr uint32_t TMEM_COLS = (N < 32 ? 32 : N) * NACC;
+    // instruction descriptor: D fp32, A/B TF32, both K-major, N >> 3, M >> 4
+    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+                               ((uint32_t)(TC_BM >> 4) << 24);
+    static_assert(K % TC_BK == 0 && N % 16 == 0 && N <= 256, "unsupported t");
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], accum;
+    __shared__ uint32_t tmem_base;
+    // 1024-byte alignment of the stage ring (128-byte swizzle atoms)
+    const uint32_t ring = (cvta_smem(smem_raw) + 1023u) & ~1023u;
+    unsigned char *ring_gen = smem_raw + (ring - cvta_smem(smem_raw));
+
+    const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    const uint32_t m0 = blockIdx.x * TC_BM;
+    if (tid == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&accum, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {  // TMEM accumulator: N fp32 columns x 128 lanes
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cvta_smem(&tmem_base)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            for (int kt = 0; kt < NKT; ++kt) {
+                const int s = kt % TC_STAGES;
+                if (kt >= TC_STAGES) mbar_wait(&empty[s], (uint32_t)((kt / TC_STAGES - 1) & 1));
+                const uint32_t st = ring + s * STAGE_BYTES;
+                mbar_arrive_expect_tx(&full[s], X_BYTES + 2 * W_BYTES);
+                tma_load_2d(st, &tmX, kt * TC_BK, (int)m0, cvta_smem(&full[s]));
+                tma_load_2d(st + 2 * X_BYTES, &tmWhi, kt * TC_BK, 0, cvta_smem(&full[s]));
+                tma_load_2d(st + 2 * X_BYTES + W_BYTES, &tmWlo, kt * TC_BK, 0, cvta_smem(&full[s]));
+            }
+        }
+    } else {
+        // ---------------- split X, issue the MMAs ----------------
+        for (int kt = 0; kt < NKT; ++kt) {
+            const int s = kt % TC_STAGES;
+            mbar_wait(&full[s], (uint32_t)((kt / TC_STAGES) & 1));
+            const uint32_t st = ring + s * STAGE_BYTES;
+            float4 *xh = reinterpret_cast<float4 *>(ring_gen + s * STAGE_BYTES);
+            float4 *xl = reinterpret_cast<float4 *>(ring_gen + s * STAGE_BYTES + X_BYTES);
+#pragma unroll
+            for (int q = 0; q < (int)(X_BYTES / 16 / 128); ++q) {
+                const int i = (int)tid + 128 * q;
+                float4 v = xh[i], h, l;
+                h.x = tf32_rn(v.x);
+                h.y = tf32_rn(v.y);
+                h.z = tf32_rn(v.z);
+                h.w = tf32_rn(v.w);
+                l.x = __fsub_rn(v.x, h.x);
+                l.y = __fsub_rn(v.y, h.y);
+                l.z = __fsub_rn(v.z, h.z);
+                l.w = __fsub_rn(v.w, h.w);
+                xh[i] = h;
+                xl[i] = l;
+            }
+            // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (tid == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a_hi = st, a_lo = st + X_BYTES, b_hi = st + 2 * X_BYTES, b_lo = b_hi + W_BYTES;
+#pragma unroll
+                for (int k = 0; k < TC_BK / 8; ++k) {  // 4 K-steps of 8 TF32 (32 bytes) inside the swizzled row
+                    const uint32_t off = k * 32;
+                    const uint32_t d = tmem + (uint32_t)((kt % NACC) * (N < 32 ? 32 : N));
+                    const uint32_t acc0 = (kt >= NACC || k > 0) ? 1u : 0u;
+                    mma_tf32(d, sdesc_sw128(a_hi + off), sdesc_sw128(b_hi + off), IDESC, acc0);
+                    mma_tf32(d, sdesc_sw128(a_hi + off), sdesc_sw128(b_lo + off), IDESC, 1u);
+                    mma_tf32(d, sdesc_sw128(a_lo + off), sdesc_sw128(b_hi + off), IDESC, 1u);
+                }
+                mma_commit(cvta_smem(&empty[s]));  // the stage is free once these MMAs have read it
+                if (kt == NKT - 1) mma_commit(cvta_smem(&accum));
+            }
+        }
+        // ---------------- epilogue: TMEM -> registers -> y in input order ----------------
+        mbar_wait(&accum, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t b = m0 + warp * 32 + lane;          // this thread's TMEM lane = box
+        const uint32_t lane_addr = tmem + ((warp * 32u) << 16);
+        const uint32_t s0 = b < B ? bstart[b] : 0u;
+        constexpr uint32_t AST = N < 32 ? 32 : N;  // columns per accumulator
+        if constexpr (T < 32) {  // t = 16: Re in columns 0..15, Im in 16..31 of one 32-column load
+            float v[32];
+            tmem_ld32(lane_addr, v);
+#pragma unroll
+            for (int a = 1; a < NACC; ++a) {
+                float w[32];
+                tmem_ld32(lane_addr + a * AST, w);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] += w[i];
+            }
+            if (b < B) {
+#pragma unroll
+                for (int i = 0; i < T; ++i) y[perm[s0 + i]] = make_float2(v[i], v[T + i]);
+            }
+        } else {
+#pragma unroll
+            for (int c0 = 0; c0 < T; c0 += 32) {  // outputs c0 .. c0 + 31
+                float re[32], im[32];
+                tmem_ld32(lane_addr + c0, re);
+                tmem_ld32(lane_addr + T + c0, im);
+#pragma unroll
+                for (int a = 1; a < NACC; ++a) {
+                    float w[32];
+                    tmem_ld32(lane_addr + a * AST + c0, w);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) re[i] += w[i];
+                    tmem_ld32(lane_addr + a * AST + T + c0, w);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) im[i] += w[i];
+                }
+                if (b < B) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) y[perm[s0 + c0 + i]] = make_float2(re[i], im[i]);
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+// 2D fp32 tensor [rows][cols] row-major, box [box_rows][32 floats], 128-byte swizzle
+bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)TC_BK, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int T>
+p2p_status launch_tc(p2p_plan *P, void *y) {
+    constexpr int N = 2 * T, K = 18 * T;
+    constexpr uint32_t STAGE_BYTES = 2 * TC_BM * TC_BK * 4 + 2 * N * TC_BK * 4;
+    const int smem = (int)(TC_STAGES * STAGE_BYTES + 1024);
+    CUtensorMap mx, mwh, mwl;
+    const float *W = (const float *)P->tc_table;
+    if (!make_map(&mx, P->red, (uint64_t)P->B, K, TC_BM) || !make_map(&mwh, W, N, K, N) ||
+        !make_map(&mwl, W + (size_t)N * K, N, K, N)) {
+        set_error("cuTensorMapEncodeTiled unavailable or rejected the Helmholtz operands");
+        return P2P_ERR_CUDA;
+    }
+    P2P_CUDA_TRY(cudaFuncSetAttribute(k_helm_tc<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    P2P_LAUNCH(k_helm_tc<T>, div_up((uint64_t)P->B, TC_BM), TC_THREADS, smem, P->stream, mx, mwh, mwl, P->bstart,
+               P->perm, (uint32_t)P->B, (float2 *)y);
+    P2P_CUDA_TRY(cudaGetLastError());
+    return P2P_OK;
+}
+}  // namespace
+
+bool helmholtz_tc_supported(const p2p_plan *P) {
+    const int t = P->cfg.points_per_box;
+    return P->cfg.precision == P2P_FP32 && (t == 16 || t == 64) && encode_fn() != nullptr;
+}
+
+// W hi / lo (2 x [2t][18t] fp32, K-major) from the fp32 pattern table P[t][9t] (complex)
+p2p_status helmholtz_tc_table(p2p_plan *P, const float *Pf /* host, [t][9t] complex */) {
+    const int t = P->cfg.points_per_box, N = 2 * t, K = 18 * t;
+    std::vector<float> w((size_t)2 * N * K);
+    float *hi = w.data(), *lo = w.data() + (size_t)N * K;
+    auto split = [](float x, float &h, float &l) {
+        uint32_t u;
+        std::memcpy(&u, &x, 4);
+        u = (u + 0x1000u) & 0xFFFFE000u;  // nearest TF32 value (as tf32_rn on the device)
+        std::memcpy(&h, &u, 4);
+        l = x - h;  // exact
+    };
+    for (int i = 0; i < t; ++i)
+        for (int c = 0; c < 9 * t; ++c) {
+            const float pr = Pf[2 * ((size_t)i * 9 * t + c)], pi = Pf[2 * ((size_t)i * 9 * t + c) + 1];
+            const float v[4] = {pr, -pi, pi, pr};  // W[i][2c], W[i][2c+1], W[t+i][2c], W[t+i][2c+1]
+            const size_t q[4] = {(size_t)i * K + 2 * c, (size_t)i * K + 2 * c + 1, (size_t)(t + i) * K + 2 * c,
+                                 (size_t)(t + i) * K + 2 * c + 1};
+            for (int e = 0; e < 4; ++e) split(v[e], hi[q[e]], lo[q[e]]);
+        }
+    P2P_CUDA_TRY(dalloc(&P->tc_table, w.size() * 4, P->stream));
+    P2P_CUDA_TRY(cudaMemcpyAsync(P->tc_table, w.data(), w.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    P2P_CUDA_TRY(cudaStreamSynchronize(P->stream));
+    return P2P_OK;
+}
+
+p2p_status eval_helmholtz_tc(p2p_plan *P, void *y) {
+    if (P->B == 0) return P2P_OK;
+    return P->cfg.points_per_box == 16 ? launch_tc<16>(P, y) : launch_tc<64>(P, y);
+}
+
+}  // namespace p2p

@@ -14,6 +14,7 @@
 // slices.  REDUNDANT reads the im2col buffer Xg (restructure output); INDEXED gathers the same values from
 // the Morton-sorted unknowns through the 9-slot neighbour table on the fly (zero for missing neighbours).
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <vector>
 
@@ -315,6 +316,7 @@ p2p_status helmholtz_table(p2p_plan *P) {
         for (size_t q = 0; q < 2 * ne; ++q) f[q] = (float)tab[q];
         P2P_CUDA_TRY(cudaMemcpyAsync(P->table, f.data(), bytes, cudaMemcpyHostToDevice, P->stream));
         P2P_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        if (helmholtz_tc_supported(P)) return helmholtz_tc_table(P, f.data());
     }
     return P2P_OK;
 }
@@ -322,6 +324,13 @@ p2p_status helmholtz_table(p2p_plan *P) {
 p2p_status eval_helmholtz(p2p_plan *P, p2p_layout layout, void *y) {
     if (P->B == 0) return P2P_OK;
     const bool f64 = P->cfg.precision == P2P_FP64;
+    // REDUNDANT fp32 with t in {16, 64}: the tensor-core GEMM; P2P_HELM_SIMT=1 keeps the CUDA-core kernel
+    // (diagnostics / comparison only)
+    static const bool force_simt = [] {
+        const char *e = getenv("P2P_HELM_SIMT");
+        return e && e[0] == '1';
+    }();
+    if (layout == P2P_REDUNDANT && P->tc_table && !force_simt) return eval_helmholtz_tc(P, y);
     if (layout == P2P_REDUNDANT) return f64 ? launch_helm<double, P2P_REDUNDANT>(P, y) : launch_helm<float, P2P_REDUNDANT>(P, y);
     return f64 ? launch_helm<double, P2P_INDEXED>(P, y) : launch_helm<float, P2P_INDEXED>(P, y);
 }

@@ -97,9 +97,9 @@ static void free_plan_buffers(p2p_plan *P) {
     cudaStream_t st = P->stream;
     free_capacity(P);
     free_distributed(P);
-    void *bufs[] = {P->red, P->table, P->ctr, P->stage_in, P->stage_out};
+    void *bufs[] = {P->red, P->table, P->tc_table, P->ctr, P->stage_in, P->stage_out};
     for (void *b : bufs) dfree(b, st);
-    P->red = P->table = P->stage_in = P->stage_out = nullptr;
+    P->red = P->table = P->tc_table = P->stage_in = P->stage_out = nullptr;
     P->stage_in_cap = P->stage_out_cap = 0;
     P->ctr = nullptr;
 }

@@ -91,6 +91,7 @@ struct p2p_plan {
     p2p::Item *items = nullptr;
     void *red = nullptr;         // gravity red[R] records; helmholtz Xg[B][9][t]
     void *table = nullptr;       // helmholtz pattern table P[t][9t] complex
+    void *tc_table = nullptr;    // helmholtz tensor-core operand: real W hi / lo, 2 x [2t][18t] fp32 (k_helm_tc.cu)
     p2p::DevCounters *ctr = nullptr;
     // capacity-sized scratch, allocated once per plan (p2p_plan_update reuses it: no allocation, no sync)
     int64_t cap = 0, bcap = 0, red_cap = 0;
@@ -153,6 +154,10 @@ p2p_status eval_distributed(p2p_plan *P, p2p_layout layout, void *phi, void *fie
 void free_distributed(p2p_plan *P);
 p2p_status eval_helmholtz(p2p_plan *P, p2p_layout layout, void *y);
 p2p_status helmholtz_table(p2p_plan *P);
+// k_helm_tc.cu: a8 as one 3xTF32 tcgen05 GEMM (fp32, t in {16, 64})
+bool helmholtz_tc_supported(const p2p_plan *P);
+p2p_status helmholtz_tc_table(p2p_plan *P, const float *Pf);
+p2p_status eval_helmholtz_tc(p2p_plan *P, void *y);
 
 // allocation helpers (stream-ordered, pooled)
 cudaError_t dalloc(void **p, size_t bytes, cudaStream_t st);

@@ -1,5 +1,7 @@
 """GPU parity of the Helmholtz (DBIM-like) path (-m gpu): structures bit-exact, y within 1e-5 (complex64) /
-1e-12 (complex128) of the oracle, REDUNDANT (im2col Xg) == INDEXED bit for bit."""
+1e-12 (complex128) of the oracle.  The CUDA-core kernels give REDUNDANT (im2col Xg) == INDEXED bit for bit; the
+fp32 REDUNDANT path for t in {16, 64} is the 3xTF32 tensor-core GEMM (k_helm_tc.cu), held to the same tolerance
+and, tighter, to its own error budget (<= 5e-6 relative L2)."""
 import numpy as np
 import pytest
 
@@ -54,7 +56,31 @@ def test_helmholtz_parity(P, t, n, holes, f64):
     tol = 1e-12 if f64 else 1e-5
     assert oracle.rel_l2(y_red, ref) <= tol
     assert oracle.rel_l2(y_idx, ref) <= tol
-    assert np.array_equal(y_red, y_idx)
+    if tensor_core_path(t, f64):
+        assert oracle.rel_l2(y_red, ref) <= 5e-6
+    else:
+        assert np.array_equal(y_red, y_idx)
+
+
+def tensor_core_path(t, f64):
+    return (not f64) and t in (16, 64)
+
+
+@pytest.mark.parametrize("t,n,holes", [(16, 37, None), (64, 23, [(5, 7)]), (16, 12, [(0, 11), (11, 0)])])
+def test_helmholtz_tensor_core_ragged(P, t, n, holes):
+    """the tcgen05 GEMM on box counts that are not multiples of its 128-box tile (TMA zero-fill of the last
+    tile's rows, masked epilogue) and with missing neighbours (zero segments of Xg)"""
+    inp = G.dbim_lattice(n, t, seed=7 * n + t, holes=holes)
+    hp = oracle.HelmholtzPlan(inp)
+    ref = hp.eval_table()
+    with gpu_plan(P, inp) as plan:
+        plan.restructure()
+        y_red = to_c(plan.eval(P.P2P_REDUNDANT))
+        y_idx = to_c(plan.eval(P.P2P_INDEXED))
+    assert oracle.rel_l2(y_red, ref) <= 5e-6
+    assert oracle.rel_l2(y_idx, ref) <= 1e-5
+    # every output written (no stale values from a skipped tile row)
+    assert np.isfinite(y_red).all() and np.abs(y_red).min() > 0
 
 
 def test_irregular_rejected(P):
