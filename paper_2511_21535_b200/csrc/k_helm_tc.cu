@@ -16,9 +16,10 @@
 // Kernel: one CTA per 128 boxes (M = 128), all N = 2t outputs in one TMEM accumulator (N fp32 columns).
 //   warp 4, one lane      TMA producer: 2D tensor loads (128-byte swizzle) of the X tile and both W tiles of
 //                         each 32-float K slice into a 3-stage ring (mbarrier full / empty)
-//   warps 0..3            split X of the landed slice; thread 0 then issues 4 K-steps x 3 tcgen05.mma
-//                         (kind::tf32, M = 128, N = 2t, K = 8, both operands K-major from shared memory
-//                         descriptors) and commits them to the stage's empty barrier
+//   warps 0..3            split X of each landed slice (mbarrier split, 128 arrivals)
+//   warp 5, one lane      MMA issuer: 4 K-steps x 3 tcgen05.mma per slice (kind::tf32, M = 128, N = 2t, K = 8,
+//                         both operands K-major from shared memory descriptors), committed to the stage's empty
+//                         barrier (and, after the last slice, to the accumulator barrier)
 //   epilogue (warps 0-3)  tcgen05.ld of the accumulator rows (TMEM lane = box), scatter to input order
 #include <cuda.h>
 
@@ -33,7 +34,7 @@ namespace {
 constexpr int TC_BM = 128;        // boxes per CTA (MMA M, TMEM lanes)
 constexpr int TC_BK = 32;         // floats per K slice = one 128-byte swizzle row
 constexpr int TC_STAGES = 3;
-constexpr int TC_THREADS = 160;   // 4 compute warps + 1 producer warp
+constexpr int TC_THREADS = 192;   // 4 split / epilogue warps + 1 TMA producer warp + 1 MMA issuer warp
 // TMEM accumulators (K slices round-robin, summed in fp32 at the end): as many as fit the 512 TMEM columns, at
 // most 8 -- the tensor core's internal fp32 accumulation loses ~2^-23 of the running sum per step (measured: one
 // accumulator 7.8e-6, four 2.0e-6 relative L2 at t = 64 vs the fp64 oracle)
@@ -71,6 +72,10 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cvta_smem(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -111,7 +116,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     static_assert(K % TC_BK == 0 && N % 16 == 0 && N <= 256, "unsupported t");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], accum;
+    __shared__ __align__(8) uint64_t full[TC_STAGES], split[TC_STAGES], empty[TC_STAGES], accum;
     __shared__ uint32_t tmem_base;
     // 1024-byte alignment of the stage ring (128-byte swizzle atoms)
     const uint32_t ring = (cvta_smem(smem_raw) + 1023u) & ~1023u;
@@ -122,6 +127,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
             mbar_init(&full[s], 1);
+            mbar_init(&split[s], 128);
             mbar_init(&empty[s], 1);
         }
         mbar_init(&accum, 1);
@@ -151,12 +157,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 tma_load_2d(st + 2 * X_BYTES + W_BYTES, &tmWlo, kt * TC_BK, 0, cvta_smem(&full[s]));
             }
         }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer (one lane) ----------------
+        if (lane == 0) {
+            for (int kt = 0; kt < NKT; ++kt) {
+                const int s = kt % TC_STAGES;
+                mbar_wait(&split[s], (uint32_t)((kt / TC_STAGES) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t st = ring + s * STAGE_BYTES;
+                const uint32_t a_hi = st, a_lo = st + X_BYTES, b_hi = st + 2 * X_BYTES, b_lo = b_hi + W_BYTES;
+#pragma unroll
+                for (int k = 0; k < TC_BK / 8; ++k) {  // 4 K-steps of 8 TF32 (32 bytes) inside the swizzled row
+                    const uint32_t off = k * 32;
+                    const uint32_t d = tmem + (uint32_t)((kt % NACC) * (N < 32 ? 32 : N));
+                    const uint32_t acc0 = (kt >= NACC || k > 0) ? 1u : 0u;
+                    mma_tf32(d, sdesc_sw128(a_hi + off), sdesc_sw128(b_hi + off), IDESC, acc0);
+                    mma_tf32(d, sdesc_sw128(a_hi + off), sdesc_sw128(b_lo + off), IDESC, 1u);
+                    mma_tf32(d, sdesc_sw128(a_lo + off), sdesc_sw128(b_hi + off), IDESC, 1u);
+                }
+                mma_commit(cvta_smem(&empty[s]));  // the stage is free once these MMAs have read it
+            }
+            mma_commit(cvta_smem(&accum));
+        }
     } else {
-        // ---------------- split X, issue the MMAs ----------------
+        // ---------------- split X into TF32 hi / lo as each slice lands ----------------
         for (int kt = 0; kt < NKT; ++kt) {
             const int s = kt % TC_STAGES;
             mbar_wait(&full[s], (uint32_t)((kt / TC_STAGES) & 1));
-            const uint32_t st = ring + s * STAGE_BYTES;
             float4 *xh = reinterpret_cast<float4 *>(ring_gen + s * STAGE_BYTES);
             float4 *xl = reinterpret_cast<float4 *>(ring_gen + s * STAGE_BYTES + X_BYTES);
 #pragma unroll
@@ -174,24 +201,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 xh[i] = h;
                 xl[i] = l;
             }
-            // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
+            // generic-proxy shared-memory writes -> visible to the tensor core (async proxy), then signal
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (tid == 0) {
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a_hi = st, a_lo = st + X_BYTES, b_hi = st + 2 * X_BYTES, b_lo = b_hi + W_BYTES;
-#pragma unroll
-                for (int k = 0; k < TC_BK / 8; ++k) {  // 4 K-steps of 8 TF32 (32 bytes) inside the swizzled row
-                    const uint32_t off = k * 32;
-                    const uint32_t d = tmem + (uint32_t)((kt % NACC) * (N < 32 ? 32 : N));
-                    const uint32_t acc0 = (kt >= NACC || k > 0) ? 1u : 0u;
-                    mma_tf32(d, sdesc_sw128(a_hi + off), sdesc_sw128(b_hi + off), IDESC, acc0);
-                    mma_tf32(d, sdesc_sw128(a_hi + off), sdesc_sw128(b_lo + off), IDESC, 1u);
-                    mma_tf32(d, sdesc_sw128(a_lo + off), sdesc_sw128(b_hi + off), IDESC, 1u);
-                }
-                mma_commit(cvta_smem(&empty[s]));  // the stage is free once these MMAs have read it
-                if (kt == NKT - 1) mma_commit(cvta_smem(&accum));
-            }
+            mbar_arrive(&split[s]);
         }
         // ---------------- epilogue: TMEM -> registers -> y in input order ----------------
         mbar_wait(&accum, 0);
