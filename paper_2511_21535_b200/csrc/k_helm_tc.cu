@@ -33,13 +33,14 @@ namespace p2p {
 namespace {
 constexpr int TC_BM = 128;        // boxes per CTA (MMA M, TMEM lanes)
 constexpr int TC_BK = 32;         // floats per K slice = one 128-byte swizzle row
-constexpr int TC_STAGES = 3;
+constexpr int TC_STAGES = 4;      // smem ring of X + W hi + W lo slices (48 KB each at t = 64)
 constexpr int TC_THREADS = 192;   // 4 split / epilogue warps + 1 TMA producer warp + 1 MMA issuer warp
 // TMEM accumulators (K slices round-robin, summed in fp32 at the end): as many as fit the 512 TMEM columns, at
 // most 8 -- the tensor core's internal fp32 accumulation loses ~2^-23 of the running sum per step (measured: one
 // accumulator 7.8e-6, four 2.0e-6 relative L2 at t = 64 vs the fp64 oracle)
+// (the remaining columns hold >= 2 stages of the X hi / lo operand, 64 columns each)
 template <int N>
-constexpr int tc_nacc() { return (N < 32 ? 32 : N) * 8 <= 512 ? 8 : 512 / (N < 32 ? 32 : N); }
+constexpr int tc_nacc() { return (N < 32 ? 32 : N) * 8 <= 256 ? 8 : (512 - 128) / (N < 32 ? 32 : N); }
 
 __device__ __forceinline__ uint32_t cvta_smem(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -78,6 +79,28 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cvta_smem(bar)) : "memory");
 }
 
+// A from TMEM (X hi / lo written by the split warps), B from a shared-memory descriptor
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// 32 consecutive 32-bit TMEM columns of this thread's lane <- registers
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -105,18 +128,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const uint32_t *__restrict__ perm, uint32_t B, float2 *__restrict__ y) {
     constexpr int N = 2 * T, K = 18 * T, NKT = K / TC_BK;
     constexpr uint32_t X_BYTES = TC_BM * TC_BK * 4, W_BYTES = N * TC_BK * 4;
-    constexpr uint32_t STAGE_BYTES = 2 * X_BYTES + 2 * W_BYTES;  // X (hi in place), X lo, W hi, W lo
-    // NACC accumulators (K slices round-robin), summed in fp32 in the epilogue: the tensor core's fp32
-    // accumulation error grows with the number of accumulation steps into one accumulator
+    constexpr uint32_t STAGE_BYTES = X_BYTES + 2 * W_BYTES;  // X (raw fp32), W hi, W lo
+    constexpr uint32_t AST = N < 32 ? 32 : N;                 // TMEM columns per accumulator
     constexpr int NACC = tc_nacc<N>();
-    constexpr uint32_t TMEM_COLS = (N < 32 ? 32 : N) * NACC;
+    constexpr uint32_t ACOL = NACC * AST;                     // first TMEM column of the A stages
+    constexpr int ASTAGES = (int)((512 - ACOL) / (2 * TC_BK)); // X hi + X lo = 64 columns per stage
+    static_assert(ASTAGES >= 2, "TMEM budget");
     // instruction descriptor: D fp32, A/B TF32, both K-major, N >> 3, M >> 4
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)(TC_BM >> 4) << 24);
     static_assert(K % TC_BK == 0 && N % 16 == 0 && N <= 256, "unsupported t");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t full[TC_STAGES], split[TC_STAGES], empty[TC_STAGES], accum;
+    __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], tsplit[8], tfree[8], accum;
     __shared__ uint32_t tmem_base;
     // 1024-byte alignment of the stage ring (128-byte swizzle atoms)
     const uint32_t ring = (cvta_smem(smem_raw) + 1023u) & ~1023u;
@@ -127,15 +151,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&split[s], 128);
             mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < ASTAGES; ++a) {
+            mbar_init(&tsplit[a], 128);
+            mbar_init(&tfree[a], 1);
         }
         mbar_init(&accum, 1);
         fence_mbar_init();
     }
-    if (warp == 0) {  // TMEM accumulator: N fp32 columns x 128 lanes
+    if (warp == 0) {  // all 512 TMEM columns: NACC accumulators + ASTAGES (X hi, X lo) operand stages
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cvta_smem(&tmem_base)),
-                     "r"(TMEM_COLS)
+                     "r"(512)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -151,74 +178,78 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int s = kt % TC_STAGES;
                 if (kt >= TC_STAGES) mbar_wait(&empty[s], (uint32_t)((kt / TC_STAGES - 1) & 1));
                 const uint32_t st = ring + s * STAGE_BYTES;
-                mbar_arrive_expect_tx(&full[s], X_BYTES + 2 * W_BYTES);
+                mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
                 tma_load_2d(st, &tmX, kt * TC_BK, (int)m0, cvta_smem(&full[s]));
-                tma_load_2d(st + 2 * X_BYTES, &tmWhi, kt * TC_BK, 0, cvta_smem(&full[s]));
-                tma_load_2d(st + 2 * X_BYTES + W_BYTES, &tmWlo, kt * TC_BK, 0, cvta_smem(&full[s]));
+                tma_load_2d(st + X_BYTES, &tmWhi, kt * TC_BK, 0, cvta_smem(&full[s]));
+                tma_load_2d(st + X_BYTES + W_BYTES, &tmWlo, kt * TC_BK, 0, cvta_smem(&full[s]));
             }
         }
     } else if (warp == 5) {
-        // ---------------- MMA issuer (one lane) ----------------
+        // ---------------- MMA issuer (one lane): A = X hi / lo from TMEM, B = W hi / lo from shared memory ----
         if (lane == 0) {
             for (int kt = 0; kt < NKT; ++kt) {
-                const int s = kt % TC_STAGES;
-                mbar_wait(&split[s], (uint32_t)((kt / TC_STAGES) & 1));
+                const int s = kt % TC_STAGES, a = kt % ASTAGES;
+                mbar_wait(&full[s], (uint32_t)((kt / TC_STAGES) & 1));
+                mbar_wait(&tsplit[a], (uint32_t)((kt / ASTAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t st = ring + s * STAGE_BYTES;
-                const uint32_t a_hi = st, a_lo = st + X_BYTES, b_hi = st + 2 * X_BYTES, b_lo = b_hi + W_BYTES;
+                const uint32_t b_hi = st + X_BYTES, b_lo = b_hi + W_BYTES;
+                const uint32_t a_hi = tmem + ACOL + (uint32_t)a * (2 * TC_BK), a_lo = a_hi + TC_BK;
+                const uint32_t d = tmem + (uint32_t)((kt % NACC) * AST);
 #pragma unroll
-                for (int k = 0; k < TC_BK / 8; ++k) {  // 4 K-steps of 8 TF32 (32 bytes) inside the swizzled row
-                    const uint32_t off = k * 32;
-                    const uint32_t d = tmem + (uint32_t)((kt % NACC) * (N < 32 ? 32 : N));
+                for (int k = 0; k < TC_BK / 8; ++k) {  // 4 K-steps of 8 TF32: 8 TMEM columns / 32 smem bytes
                     const uint32_t acc0 = (kt >= NACC || k > 0) ? 1u : 0u;
-                    mma_tf32(d, sdesc_sw128(a_hi + off), sdesc_sw128(b_hi + off), IDESC, acc0);
-                    mma_tf32(d, sdesc_sw128(a_hi + off), sdesc_sw128(b_lo + off), IDESC, 1u);
-                    mma_tf32(d, sdesc_sw128(a_lo + off), sdesc_sw128(b_hi + off), IDESC, 1u);
+                    mma_tf32_ts(d, a_hi + 8 * k, sdesc_sw128(b_hi + 32 * k), IDESC, acc0);
+                    mma_tf32_ts(d, a_hi + 8 * k, sdesc_sw128(b_lo + 32 * k), IDESC, 1u);
+                    mma_tf32_ts(d, a_lo + 8 * k, sdesc_sw128(b_hi + 32 * k), IDESC, 1u);
                 }
-                mma_commit(cvta_smem(&empty[s]));  // the stage is free once these MMAs have read it
+                mma_commit(cvta_smem(&empty[s]));  // W of smem stage s consumed
+                mma_commit(cvta_smem(&tfree[a]));  // X hi / lo of TMEM stage a consumed
             }
             mma_commit(cvta_smem(&accum));
         }
     } else {
-        // ---------------- split X into TF32 hi / lo as each slice lands ----------------
+        // ---------------- split X rows into TF32 hi / lo, straight into TMEM ----------------
+        // thread = one X row (TMEM lane 32 warp + lane); its 128-byte row sits 16-byte-chunk-swizzled in smem
+        const uint32_t r = warp * 32 + lane;
+        const uint32_t lane_cols = (warp * 32u) << 16;
         for (int kt = 0; kt < NKT; ++kt) {
-            const int s = kt % TC_STAGES;
+            const int s = kt % TC_STAGES, a = kt % ASTAGES;
             mbar_wait(&full[s], (uint32_t)((kt / TC_STAGES) & 1));
-            float4 *xh = reinterpret_cast<float4 *>(ring_gen + s * STAGE_BYTES);
-            float4 *xl = reinterpret_cast<float4 *>(ring_gen + s * STAGE_BYTES + X_BYTES);
+            if (kt >= ASTAGES) mbar_wait(&tfree[a], (uint32_t)((kt / ASTAGES - 1) & 1));
+            const unsigned char *row = ring_gen + s * STAGE_BYTES + r * 128;
+            uint32_t hi[32], lo[32];
 #pragma unroll
-            for (int q = 0; q < (int)(X_BYTES / 16 / 128); ++q) {
-                const int i = (int)tid + 128 * q;
-                float4 v = xh[i], h, l;
-                h.x = tf32_rn(v.x);
-                h.y = tf32_rn(v.y);
-                h.z = tf32_rn(v.z);
-                h.w = tf32_rn(v.w);
-                l.x = __fsub_rn(v.x, h.x);
-                l.y = __fsub_rn(v.y, h.y);
-                l.z = __fsub_rn(v.z, h.z);
-                l.w = __fsub_rn(v.w, h.w);
-                xh[i] = h;
-                xl[i] = l;
+            for (int c = 0; c < 8; ++c) {
+                const float4 v = *reinterpret_cast<const float4 *>(row + ((c ^ (r & 7)) << 4));
+                const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float h = tf32_rn(e[q]);
+                    hi[4 * c + q] = __float_as_uint(h);
+                    lo[4 * c + q] = __float_as_uint(__fsub_rn(e[q], h));
+                }
             }
-            // generic-proxy shared-memory writes -> visible to the tensor core (async proxy), then signal
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&split[s]);
+            const uint32_t ta = tmem + lane_cols + ACOL + (uint32_t)a * (2 * TC_BK);
+            tmem_st32(ta, hi);
+            tmem_st32(ta + TC_BK, lo);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&tsplit[a]);
         }
         // ---------------- epilogue: TMEM -> registers -> y in input order ----------------
         mbar_wait(&accum, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t b = m0 + warp * 32 + lane;          // this thread's TMEM lane = box
-        const uint32_t lane_addr = tmem + ((warp * 32u) << 16);
+        const uint32_t b = m0 + r;  // this thread's TMEM lane = box
+        const uint32_t lane_addr = tmem + lane_cols;
         const uint32_t s0 = b < B ? bstart[b] : 0u;
-        constexpr uint32_t AST = N < 32 ? 32 : N;  // columns per accumulator
         if constexpr (T < 32) {  // t = 16: Re in columns 0..15, Im in 16..31 of one 32-column load
             float v[32];
             tmem_ld32(lane_addr, v);
 #pragma unroll
-            for (int a = 1; a < NACC; ++a) {
+            for (int ac = 1; ac < NACC; ++ac) {
                 float w[32];
-                tmem_ld32(lane_addr + a * AST, w);
+                tmem_ld32(lane_addr + ac * AST, w);
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] += w[i];
             }
@@ -233,12 +264,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 tmem_ld32(lane_addr + c0, re);
                 tmem_ld32(lane_addr + T + c0, im);
 #pragma unroll
-                for (int a = 1; a < NACC; ++a) {
+                for (int ac = 1; ac < NACC; ++ac) {
                     float w[32];
-                    tmem_ld32(lane_addr + a * AST + c0, w);
+                    tmem_ld32(lane_addr + ac * AST + c0, w);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) re[i] += w[i];
-                    tmem_ld32(lane_addr + a * AST + T + c0, w);
+                    tmem_ld32(lane_addr + ac * AST + T + c0, w);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) im[i] += w[i];
                 }
@@ -253,7 +284,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
     }
 }
 
@@ -290,7 +321,7 @@ bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, ui
 template <int T>
 p2p_status launch_tc(p2p_plan *P, void *y) {
     constexpr int N = 2 * T, K = 18 * T;
-    constexpr uint32_t STAGE_BYTES = 2 * TC_BM * TC_BK * 4 + 2 * N * TC_BK * 4;
+    constexpr uint32_t STAGE_BYTES = TC_BM * TC_BK * 4 + 2 * N * TC_BK * 4;
     const int smem = (int)(TC_STAGES * STAGE_BYTES + 1024);
     CUtensorMap mx, mwh, mwl;
     const float *W = (const float *)P->tc_table;
