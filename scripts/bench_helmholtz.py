@@ -1,6 +1,8 @@
 """Helmholtz (DBIM-like, BASELINE configs[1]) timing: plan (one-off geometry), restructure (im2col Xg), eval
-REDUNDANT / INDEXED, as pair-interactions (complex MACs) per second and the FP32-pipe roofline (4 FFMA per
-complex MAC: peak = n_SM * 128 * f_max / 4).  Prints one JSON line per workload.
+REDUNDANT / INDEXED, as pair-interactions (complex MACs) per second.  Rooflines: the CUDA-core kernels against the
+FP32 pipe (4 FFMA per complex MAC: peak = n_SM * 128 * f_max / 4); the fp32 REDUNDANT eval (t in {16, 64}) is the
+3xTF32 tensor-core GEMM (k_helm_tc.cu) -- 3 TF32 MMAs x 8 real flops per complex MAC against the TF32 dense peak
+(MEASURED_PEAKS bf16 x the nominal TF32 / BF16 ratio 1.1 / 2.25).  Prints one JSON line per workload.
 usage: python scripts/bench_helmholtz.py [c2a|c2b ...]"""
 import json
 import os
@@ -47,10 +49,16 @@ def main():
             info = plan.info
         I = int(info.n_pairs)
         peak = nsm * 128 * peaks["sm_max_mhz"] * 1e6 / 4
+        tf32_peak = peaks.get("bf16_tflops", 2250.0) * 1e12 * (1.1 / 2.25)
+        tc = inp.t in (16, 64) and os.environ.get("P2P_HELM_SIMT", "0") != "1"
         xg_bytes = int(info.n_red) * 8
         out = {"workload": wl, "N": inp.n, "t": inp.t, "boxes": int(info.n_boxes), "pairs": I,
                "restructure_ms": t_rest, "eval_redundant_ms": t_red, "eval_indexed_ms": t_idx,
                "eval_pairs_per_s": I / (t_red * 1e-3), "eval_frac_fp32": I / (t_red * 1e-3) / peak,
+               "eval_path": "tcgen05 3xTF32 GEMM" if tc else "CUDA-core FP32x2",
+               "eval_tensor_tflops": (24.0 * I / (t_red * 1e-3) / 1e12) if tc else None,
+               "eval_frac_tf32_peak": (24.0 * I / (t_red * 1e-3) / tf32_peak) if tc else None,
+               "indexed_frac_fp32": I / (t_idx * 1e-3) / peak,
                "restructure_plus_eval_pairs_per_s": I / ((t_rest + t_red) * 1e-3),
                "indexed_pairs_per_s": I / (t_idx * 1e-3),
                "restructure_hbm_frac": (xg_bytes + inp.n * 8) / (t_rest * 1e-3) / (peaks["hbm_gbs"] * 1e9),
