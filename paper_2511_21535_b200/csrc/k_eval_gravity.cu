@@ -92,16 +92,17 @@ struct Tgt;
 // fp32: K targets as K/2 packed pairs (float2 + the sm_100 packed intrinsics __fadd2_rn / __fmul2_rn /
 // __ffma2_rn -> SASS FADD2 / FMUL2 / FFMA2; the broadcast source component becomes a scalar operand)
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
-__device__ __forceinline__ float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
 
 template <int K>
 struct Tgt<float, K> {
     static constexpr int P = K / 2;
     float2 tx[P], ty[P], tz[P], ap[P], ax[P], ay[P], az[P];
+    // the targets are held NEGATED (-x, -y, -z): d = s + (-t) is then a plain FADD2 with no per-chunk negation
+    // prologue (exact: negation is exact, s + (-t) == s - t bit for bit)
     __device__ __forceinline__ void set(int k, float x, float y, float z) {
         const int p = k >> 1;
-        if (k & 1) { tx[p].y = x; ty[p].y = y; tz[p].y = z; }
-        else { tx[p].x = x; ty[p].x = y; tz[p].x = z; }
+        if (k & 1) { tx[p].y = -x; ty[p].y = -y; tz[p].y = -z; }
+        else { tx[p].x = -x; ty[p].x = -y; tz[p].x = -z; }
     }
     __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -110,9 +111,9 @@ struct Tgt<float, K> {
     __device__ __forceinline__ void interact(const float4 &s, float2 E) {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const float2 dx = __fadd2_rn(bc(s.x), neg2(tx[p]));
-            const float2 dy = __fadd2_rn(bc(s.y), neg2(ty[p]));
-            const float2 dz = __fadd2_rn(bc(s.z), neg2(tz[p]));
+            const float2 dx = __fadd2_rn(bc(s.x), tx[p]);
+            const float2 dy = __fadd2_rn(bc(s.y), ty[p]);
+            const float2 dz = __fadd2_rn(bc(s.z), tz[p]);
             float2 r2 = __ffma2_rn(dx, dx, E);
             r2 = __ffma2_rn(dy, dy, r2);
             r2 = __ffma2_rn(dz, dz, r2);
