@@ -7,7 +7,7 @@ TAG=${1:-r01}
 O=gpurun_out/$TAG
 mkdir -p $O
 ncu --set full --import-source on --clock-control none \
-    -k regex:"k_eval_gravity|k_restructure_gravity|k_nbr_count|k_nbr_fill|k_radix_pass|k_permute" -c 10 \
+    -k regex:"k_eval_gravity|k_restructure_gravity|k_nbr_build|k_radix_pass|k_permute" -c 9 \
     -o $O/full_c5w python scripts/profile_step.py c5w 1 redundant,indexed > $O/ncu_full.log 2>&1
 python - "$O" <<'PY'
 import csv, io, json, subprocess, sys
@@ -21,8 +21,11 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 for row in rows[2:]:
     if "k_eval_gravity<float, (int)0" in row[ki] or "k_eval_gravity<float, 0" in row[ki]:
         t = float(row[r]) * scale[units[r]] + float(row[w]) * scale[units[w]]
-        json.dump({"c5w": int(t)}, open("profiles/ncu_eval_traffic.json", "w"))
-        json.dump({"c5w": int(t)}, open(f"{o}/ncu_eval_traffic.json", "w"))
+        d = {"_source": "profiles/r01_ncu_full_c5w.txt: ncu --set full (scripts/round_profile.sh), "
+                        "k_eval_gravity<float,REDUNDANT,4> on the c5w tile, dram__bytes_read.sum + "
+                        "dram__bytes_write.sum per launch (bytes)", "c5w": int(t)}
+        json.dump(d, open("profiles/ncu_eval_traffic.json", "w"), indent=1)
+        json.dump(d, open(f"{o}/ncu_eval_traffic.json", "w"), indent=1)
         print("eval traffic", t)
         break
 PY
@@ -32,6 +35,8 @@ for w in c4-8 c4-16 c4-32 c4-64 c4-128 c3; do
 done
 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
 python scripts/bench_helmholtz.py c2a c2b > $O/bench_helmholtz.jsonl 2> $O/bench_helmholtz.err
+P2P_HELM_SIMT=1 python scripts/bench_helmholtz.py c2a c2b >> $O/bench_helmholtz.jsonl 2>> $O/bench_helmholtz.err
+for w in c5s c3dense; do python bench.py --workload $w --no-cpu-baseline --steps 5 > $O/bench_$w.json 2> $O/bench_$w.err; done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ncu_launches_bench.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_under_ncu.log 2>&1
 echo done
