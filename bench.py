@@ -392,13 +392,16 @@ def cpu_baseline(inp, budget_s: float = 12.0):
     gp.eval_indexed_boxes(sel)
     rate = pairs / (time.perf_counter() - t0)
     # scale the sample to about budget_s of CPU work, then time it
-    sel, pairs = _oracle_sample(gp, min(rate * budget_s, 0.5 * gp.I), seed=2)
+    sel, pairs = _oracle_sample(gp, min(rate * budget_s, float(gp.I)), seed=2)
     t0 = time.perf_counter()
     gp.eval_indexed_boxes(sel)
     dt = time.perf_counter() - t0
+    whole = len(sel) >= gp.B
+    what = "all" if whole else "seeded-random"
     return {"value": pairs / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"fp64 oracle mode (ii) over {len(sel)} seeded-random target boxes ({pairs} pairs, "
-                      f"{dt:.1f} s, OpenMP {os.cpu_count()} threads) of the same workload; structure build excluded"}
+            "sample": f"fp64 oracle mode (ii) over {what} {len(sel)} target boxes ({pairs} pairs, {dt:.1f} s wall, "
+                      f"OpenMP {os.cpu_count()} threads = {dt * os.cpu_count():.0f} core-s) of the same workload; "
+                      f"structure build excluded"}
 
 
 def reference_arm(args, rank, world):
