@@ -13,19 +13,24 @@
 //                        record, so the arithmetic and the outputs equal P2P_REDUNDANT bit for bit.
 //
 // B200 design (the paper's GTX 1050 thread-per-particle kernel is prior art, not the blueprint):
-//   * persistent CTAs (EV_WARPS warps each); every warp pulls work items (box, <= 32-target chunk) from a
-//     global atomic queue (index fetched one item ahead) and runs its own 2-stage producer/consumer pipeline:
-//     while it computes chunk c from one shared-memory stage, the bulk copies of chunk c+1 -- or of the next
-//     item's first chunk AND its targets -- land in the other stage (mbarrier + expect_tx completion).
+//   * persistent CTAs (EV_WARPS warps each); every warp pulls work items (box, <= 32-target chunk; a 32-byte
+//     record prefetched one item ahead) from a global atomic queue (two items per atomic) and runs its own
+//     2-stage producer/consumer pipeline: while it computes chunk c from one shared-memory stage, the bulk
+//     copies of chunk c+1 -- or of the next item's first chunk AND its targets (REDUNDANT: already rebased,
+//     from the box's own segment of its run) -- land in the other stage (mbarrier + expect_tx completion).
+//     Boxes with <= 8 targets and <= 128 sources take a thread-per-target-pair path instead (one warp per CTA
+//     starts with them, so their load latency hides behind the other warps' item work).
 //   * targets live in registers: lane (g, s) holds K targets (group g) and walks the staged sources
-//     j = s, s+S, ... (S source splits, G groups; S, G precomputed per item by k_nbr_fill), so boxes of any
-//     occupancy keep (almost) all 32 lanes busy; the S partial sums are combined by a fixed shuffle tree
+//     j = s, s+S, ... (S source splits, G groups; S, G precomputed per item by k_nbr_build), so boxes of any
+//     occupancy keep (almost) all 32 lanes busy; the S partial sums are combined by a fixed transpose-reduce
 //     (deterministic).
 //   * fp32: targets are paired and the pair math is issued as packed FP32x2 instructions (FADD2 / FMUL2 /
 //     FFMA2, sm_100a; the source component is a broadcast scalar operand), so the 13 FP32-pipe lane-ops of an
 //     interaction cost only 6.5 issue slots + 1 MUFU.RSQ: the kernel is bound by the FP32 pipe
 //     (128 lane-ops/clk/SM), not by instruction issue.  The rounding of every operation is the same as the
 //     scalar formula (fma.rn.f32x2 == two fma.rn.f32).
+//   * the hot loop is specialised on S (immediate-offset LDS, 4 sources per iteration, one ALU pointer add) and
+//     holds the targets negated (d = s + (-t): no per-chunk prologue); no IMAD runs on the FMA-heavy pipe.
 //   * the self pair (d = 0, r^2 = eps^2) is evaluated like any other and its potential term subtracted
 //     bit-exactly after the loop (DESIGN C3).
 #include <type_traits>
@@ -541,7 +546,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
             for (int d = 0; d < 3; ++d)
                 needs_fix |= ((a.g.periodic >> d) & 1u) && (cc[d] == 0 || (int)cc[d] == a.g.nbox[d] - 1);
         }
-        // lane layout (precomputed by k_nbr_fill): G groups of K targets x S source splits
+        // lane layout (precomputed by k_nbr_build): G groups of K targets x S source splits
         const uint32_t nt = c_meta & 0xffu, S = (c_meta >> 8) & 0xffu, G = (c_meta >> 16) & 0xffu;
         const uint32_t m20 = c_m20[S];
         const uint32_t g = (lane * m20) >> 20, sl = lane - g * S;

@@ -165,7 +165,7 @@ __global__ void k_eval_helm_generic(const typename C2T<T>::type *__restrict__ Pt
 // so the FP32 work issues in half the slots.  Shared tiles hold X as (c, d, d, c) and P as (a, a, -b, b) float4
 // so one LDS.128 yields both operand pairs.  Warp tile 32 boxes x 16 outputs, lane = (box group bg, output
 // group og), boxes bg + 8r / outputs og + 4r' interleaved (conflict-free LDS.128); CTA = 8 warps.
-// Rounding sequence per component identical to k_eval_helm_tiled (same two fmas in the same order).
+// Rounding sequence per component identical to k_eval_helm_tiled (fp64) (same two fmas in the same order).
 constexpr int HF_KT = 8;
 
 template <int LAYOUT, int TT>
