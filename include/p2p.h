@@ -191,7 +191,8 @@ void p2p_comm_destroy(p2p_comm *comm);
 /* Multi-GPU plan semantics (cfg->comm != NULL; gravity only).  Every rank calls p2p_plan_create / p2p_eval
  * collectively with ITS OWN input slice (any distribution).  The ranks repartition the particles into
  * contiguous Morton ranges of boxes, balanced by particle count on a coarse supercell histogram
- * (p2p_partition_splitters), exchange whole halo boxes, and each rank evaluates the targets of its range;
+ * (p2p_partition_splitters), route every particle to its owner and, as a halo source, to every other rank owning
+ * one of its box's 26 neighbours (one all-to-all-v), and each rank evaluates the targets of its range;
  * p2p_eval returns every result to the rank and input slot it came from.  Results are bitwise identical to a
  * 1-GPU plan over the rank-major concatenation of the slices.  p2p_get_info / p2p_copy_out describe the rank's
  * LOCAL plan (owned + halo particles; halo boxes have empty neighbour lists and runs).  p2p_plan_update is
@@ -205,6 +206,11 @@ void p2p_comm_destroy(p2p_comm *comm);
  *   hist: host, [nbins] u64;  splitters_out: host, [nranks + 1] u32 */
 p2p_status p2p_partition_splitters(const uint64_t *hist, int64_t nbins, int shift, int key_bits, int nranks,
                                    uint32_t *splitters_out);
+
+/* The splitters a collective plan's latest build derived ON THE DEVICE (k_splitters, from the all-reduced
+ * supercell histogram, sc_bits = min(key_bits, 18)); they must equal p2p_partition_splitters of the same
+ * histogram (tests).  splitters_out: host, [nranks + 1] u32.  INVALID_ARGUMENT for a 1-GPU plan or n != nranks+1. */
+p2p_status p2p_get_splitters(const p2p_plan *plan, uint32_t *splitters_out, int n);
 
 /* In-process "loopback" communicators: nranks emulated ranks = nranks host threads of ONE process sharing one
  * device; the collectives become device-to-device copies + a host barrier.  Used to run the whole multi-GPU

@@ -34,7 +34,7 @@ LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise"
 EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure", "p2p_eval",
             "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
-            "p2p_partition_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
+            "p2p_partition_splitters", "p2p_get_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
             "p2p_comm_create_loopback", "p2p_status_string", "p2p_last_error", "p2p_kernel_launch_count",
             "p2p_abi_version"]
 
@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
             "p2p_kernel_launch_count": (u64, []),
             "p2p_abi_version": (C.c_int, []),
             "p2p_partition_splitters": (C.c_int, [p, i64, C.c_int, C.c_int, C.c_int, p]),
+            "p2p_get_splitters": (C.c_int, [p, p, C.c_int]),
             "p2p_loopback_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
             "p2p_loopback_group_destroy": (None, [p]),
             "p2p_comm_create_loopback": (C.c_int, [p, C.c_int, C.POINTER(C.c_void_p)]),
@@ -197,6 +198,12 @@ def p2p_partition_splitters(hist: np.ndarray, shift: int, key_bits: int, nranks:
     out = np.zeros(nranks + 1, np.uint32)
     _check(lib().p2p_partition_splitters(h.ctypes.data_as(C.c_void_p), h.shape[0], int(shift), int(key_bits),
                                          int(nranks), out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def p2p_get_splitters(plan: int, nranks: int) -> np.ndarray:
+    out = np.zeros(nranks + 1, np.uint32)
+    _check(lib().p2p_get_splitters(plan, out.ctypes.data_as(C.c_void_p), int(nranks) + 1))
     return out
 
 

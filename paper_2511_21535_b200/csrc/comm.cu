@@ -36,6 +36,11 @@ struct NcclComm : CommBase {
         NCCL_TRY(ncclAllReduce(dev, dev, count, ncclUint64, ncclSum, comm, st));
         return P2P_OK;
     }
+    p2p_status allgather_u64(const unsigned long long *send, unsigned long long *recv, size_t count,
+                             cudaStream_t st) override {
+        NCCL_TRY(ncclAllGather(send, recv, count, ncclUint64, comm, st));
+        return P2P_OK;
+    }
     p2p_status alltoall_counts(const int64_t *send, int64_t *recv, cudaStream_t st) override {
         P2P_CUDA_TRY(cudaMemcpyAsync(dcnt, send, sizeof(long long) * nranks, cudaMemcpyHostToDevice, st));
         NCCL_TRY(ncclGroupStart());
@@ -72,6 +77,19 @@ struct LoopbackComm : CommBase {
             for (size_t i = 0; i < count; ++i) sum[i] += g->red_ptr[r][i];
         g->barrier();
         P2P_CUDA_TRY(cudaMemcpyAsync(dev, sum.data(), count * 8, cudaMemcpyHostToDevice, st));
+        P2P_CUDA_TRY(cudaStreamSynchronize(st));
+        return P2P_OK;
+    }
+    p2p_status allgather_u64(const unsigned long long *send, unsigned long long *recv, size_t count,
+                             cudaStream_t st) override {
+        std::vector<unsigned long long> mine(count), all(count * nranks);
+        P2P_CUDA_TRY(cudaMemcpyAsync(mine.data(), send, count * 8, cudaMemcpyDeviceToHost, st));
+        P2P_CUDA_TRY(cudaStreamSynchronize(st));
+        g->red_ptr[rank] = mine.data();
+        g->barrier();
+        for (int r = 0; r < nranks; ++r) std::memcpy(all.data() + r * count, g->red_ptr[r], count * 8);
+        g->barrier();
+        P2P_CUDA_TRY(cudaMemcpyAsync(recv, all.data(), count * 8 * nranks, cudaMemcpyHostToDevice, st));
         P2P_CUDA_TRY(cudaStreamSynchronize(st));
         return P2P_OK;
     }

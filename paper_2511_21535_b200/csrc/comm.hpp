@@ -1,5 +1,6 @@
 // comm.hpp -- the collectives the multi-GPU path needs, behind one small interface:
 //   allreduce_sum_u64  : the coarse supercell histogram (cost-balanced Morton splitters)
+//   allgather_u64      : every rank's route counts (one host read-back per plan build)
 //   alltoall_counts    : per-peer element counts before each all-to-all-v (host arrays)
 //   alltoallv          : repartition / halo / result return (device buffers, byte counts)
 // Two backends: NCCL (one process per GPU, NVLink/NVSwitch; grouped ncclSend/ncclRecv) and an in-process
@@ -22,6 +23,9 @@ struct CommBase {
     virtual ~CommBase() = default;
     // in-place sum over ranks of a device array of u64 (all ranks end with the same values)
     virtual p2p_status allreduce_sum_u64(unsigned long long *dev, size_t count, cudaStream_t st) = 0;
+    // recv[r * count + i] = send_i of rank r (device arrays; recv holds nranks * count values)
+    virtual p2p_status allgather_u64(const unsigned long long *send, unsigned long long *recv, size_t count,
+                                     cudaStream_t st) = 0;
     // send[r] = elements this rank sends to r; recv[r] = elements it receives from r (host arrays, blocking)
     virtual p2p_status alltoall_counts(const int64_t *send, int64_t *recv, cudaStream_t st) = 0;
     // device all-to-all-v of bytes: peer r gets send + soff[r] .. + scnt[r]; we receive rcnt[r] at recv + roff[r]

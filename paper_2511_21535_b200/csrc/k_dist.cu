@@ -1,21 +1,27 @@
 // k_dist.cu -- the multi-GPU path: Morton-range sharding with a halo exchange.
 //
-// Collective plan build on every rank (all steps stream-ordered; a few host syncs for exchange sizes):
-//   1. bin + key the rank's input particles (the same k_bin_gravity as the 1-GPU path);
-//   2. coarse histogram over 2^sc_bits Morton "supercells" (key >> shift), all-reduced (sum);
-//   3. identical count-balanced splitters on every rank: rank r owns keys [spl[r], spl[r+1]) -- contiguous
-//      Morton ranges aligned to supercells (C20);
-//   4. repartition: owner of every input particle, stable counting order by owner, all-to-all-v of
-//      {x,y,z,m} records -> the owned particles, arranged by (source rank, source input order);
-//   5. halo: every owned box whose 26-neighbourhood touches another rank's range is sent whole to that rank
-//      (box-level ownership makes the halo symmetric, so no request round is needed);
-//   6. the local plan = the ordinary a1..a5 over [owned ; halo] with target boxes restricted to the owned range
-//      (halo boxes are sources only).
-// Within every box the particles keep increasing GLOBAL input order (owned: rank-major concatenation; halo: the
-// owner's sorted order), so every target's redundant run -- records, order and rebased bits -- is identical to
-// the 1-GPU plan on the concatenated input: results are bitwise independent of the GPU count.
-// Eval: the local eval into owned-order buffers, then the reverse all-to-all-v returns each result to the rank
-// and input slot it came from.
+// Collective plan build on every rank (all steps stream-ordered; ONE host synchronisation for the exchange sizes):
+//   1. bin + key the rank's input particles (the binning arithmetic of k_bin_gravity, DESIGN C6);
+//   2. coarse histogram over 2^sc_bits Morton "supercells" (key >> shift), all-reduced (sum) on the device;
+//   3. k_splitters: identical count-balanced splitters on every rank, computed on the device from the reduced
+//      histogram (= p2p_partition_splitters, C20): rank r owns keys [spl[r], spl[r+1]), contiguous Morton ranges
+//      aligned to supercells;
+//   4. route: every input particle goes to its owner (as a target + source) and to every OTHER rank that owns a
+//      box of its 26-neighbourhood (as a halo source).  A particle whose 3x3x3 neighbourhood fits in one
+//      Morton-aligned cube lying inside one rank range needs no halo test (the common case: O(1) per particle);
+//      the rest test the 26 neighbour owners;
+//   5. the per-tile route counts are scanned per destination group (rank r, owned | halo) and all-gathered;
+//      ONE device->host read-back gives the splitters, every rank's send counts and the out-of-domain flag;
+//   6. a stable multi-split scatters {x,y,z,m} records straight from the caller's arrays into one send buffer
+//      laid out [to rank 0: owned ; halo][to rank 1: owned ; halo]...; ONE all-to-all-v delivers them;
+//   7. the local plan = the ordinary a1..a5 over the received records with target boxes restricted to the owned
+//      range (halo boxes are sources only).
+// Within every box the particles keep increasing GLOBAL input order (received runs are rank-major, each in its
+// sender's input order, and the local radix sort is stable), so every target's redundant run -- records, order and
+// rebased bits -- is identical to the 1-GPU plan on the concatenated input: results are bitwise independent of the
+// GPU count.
+// Eval: the local eval, then the reverse all-to-all-v returns the owned part of every received run to the rank and
+// input slot it came from.
 #include <algorithm>
 #include <vector>
 
@@ -29,16 +35,20 @@ template <typename T> struct V4T;
 template <> struct V4T<float> { using type = float4; };
 template <> struct V4T<double> { using type = double4; };
 
-// positions at pos[i*ps + d] (same binning arithmetic as k_structs.cu k_bin_gravity, DESIGN C6)
+constexpr int MAX_RANKS = 64;  // halo masks are u64
+constexpr int RT_THREADS = 256, RT_WARPS = RT_THREADS / 32, RT_ITEMS = 16, RT_TILE = RT_THREADS * RT_ITEMS;
+
+// positions at pos[i*3 + d] (same binning arithmetic as k_structs.cu k_bin_gravity, DESIGN C6); an out-of-domain
+// particle records its index in *err and gets box coordinate 0 in the offending dimension (a valid key)
 template <typename T>
-__global__ void k_keys(const T *__restrict__ pos, int ps, uint32_t n, Geom g, uint32_t *__restrict__ key,
-                       uint32_t *__restrict__ idx, unsigned long long *err) {
+__global__ void k_keys(const T *__restrict__ pos, uint32_t n, Geom g, uint32_t *__restrict__ key,
+                       unsigned long long *err) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         uint32_t c[3];
         bool bad = false;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            double f = floor(__ddiv_rn(__dsub_rn((double)pos[(size_t)ps * i + d], g.lo[d]), g.h));
+            double f = floor(__ddiv_rn(__dsub_rn((double)pos[(size_t)3 * i + d], g.lo[d]), g.h));
             if (!(f >= 0.0 && f < (double)g.nbox[d])) {
                 bad = true;
                 f = 0.0;
@@ -47,7 +57,6 @@ __global__ void k_keys(const T *__restrict__ pos, int ps, uint32_t n, Geom g, ui
         }
         if (bad) atomicMin(err, (unsigned long long)i);
         key[i] = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
-        idx[i] = i;
     }
 }
 
@@ -56,9 +65,66 @@ __global__ void k_sc_hist(const uint32_t *__restrict__ key, uint32_t n, int shif
         atomicAdd(&hist[key[i] >> shift], 1ull);
 }
 
-// hist[nbins] = 1 if this rank saw an out-of-domain input (summed over ranks by the all-reduce)
 __global__ void k_err_flag(const unsigned long long *err, unsigned long long *flag) {
     *flag = *err != ~0ull ? 1ull : 0ull;
+}
+
+// The splitters of compute_splitters (below) from the all-reduced device histogram, one block of 1024 threads:
+// spl[r] = (first supercell b with excl(b) * G >= r * total) << shift, where excl(b) = particles in supercells < b;
+// no such b < nbins -> nbins << shift.  Thread t owns bins [cs, ce) and resolves the crossings b in (cs, ce]
+// (excl is non-decreasing, so each crossing is found by exactly one thread).  Also copies the out-of-domain count
+// hist[nbins] and the splitters into the read-back words.
+constexpr int SPL_THREADS = 1024;
+__global__ void __launch_bounds__(SPL_THREADS) k_splitters(const unsigned long long *__restrict__ hist, uint32_t nbins,
+                                                           int shift, int key_bits, int G, uint32_t *__restrict__ spl,
+                                                           unsigned long long *__restrict__ xfer_spl,
+                                                           unsigned long long *__restrict__ xfer_err) {
+    __shared__ unsigned long long s_w[SPL_THREADS / 32];
+    __shared__ uint32_t s_spl[MAX_RANKS + 1];
+    const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
+    const uint32_t C = (nbins + SPL_THREADS - 1) / SPL_THREADS;
+    const uint32_t cs = min(nbins, t * C), ce = min(nbins, cs + C);
+    unsigned long long s = 0;
+    for (uint32_t b = cs; b < ce; ++b) s += hist[b];
+    // block exclusive scan of the chunk sums
+    unsigned long long x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) s_w[w] = x;
+    const uint32_t dflt = (uint32_t)min((unsigned long long)nbins << shift, 0xffffffffull);
+    if (t <= (unsigned)G) s_spl[t] = t == 0 ? 0u : (t == (unsigned)G ? (uint32_t)min(1ull << key_bits, 0xffffffffull) : dflt);
+    __syncthreads();
+    unsigned long long add = 0, total = 0;
+    for (int i = 0; i < SPL_THREADS / 32; ++i) {
+        add += i < (int)w ? s_w[i] : 0ull;
+        total += s_w[i];
+    }
+    const unsigned long long e = x - s + add;
+    if (total == 0) {
+        if (t > 0 && t < (unsigned)G) s_spl[t] = 0u;  // host loop: every r crosses at b = 0
+    } else {
+        for (int r = 1; r < G; ++r) {
+            const unsigned long long T = (unsigned long long)r * total;
+            if (!(e * (unsigned long long)G < T && T <= (e + s) * (unsigned long long)G)) continue;
+            unsigned long long xb = e;
+            for (uint32_t b = cs + 1; b <= ce; ++b) {
+                xb += hist[b - 1];
+                if (xb * (unsigned long long)G >= T) {
+                    s_spl[r] = b < nbins ? (uint32_t)(b << shift) : dflt;
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (t <= (unsigned)G) {
+        spl[t] = s_spl[t];
+        xfer_spl[t] = s_spl[t];
+    }
+    if (t == 0) *xfer_err = hist[nbins];
 }
 
 __device__ __forceinline__ int owner_of(uint32_t key, const uint32_t *spl, int G) {
@@ -70,48 +136,8 @@ __device__ __forceinline__ int owner_of(uint32_t key, const uint32_t *spl, int G
     return lo;
 }
 
-__global__ void k_dest(const uint32_t *__restrict__ key, uint32_t n, const uint32_t *__restrict__ spl, int G,
-                       uint32_t *__restrict__ dest, unsigned int *__restrict__ cnt) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int r = owner_of(key[i], spl, G);
-        dest[i] = (uint32_t)r;
-        atomicAdd(&cnt[r], 1u);
-    }
-}
-
-template <typename T, typename V4>
-__global__ void k_gather_rec(const T *__restrict__ pos, int ps, const T *__restrict__ q, int qs,
-                             const uint32_t *__restrict__ order, uint32_t n, V4 *__restrict__ out) {
-    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-        const uint32_t i = order[p];
-        V4 r;
-        r.x = pos[(size_t)ps * i + 0];
-        r.y = pos[(size_t)ps * i + 1];
-        r.z = pos[(size_t)ps * i + 2];
-        r.w = q[(size_t)qs * i];
-        out[p] = r;
-    }
-}
-
-struct HeadGetD {
-    const uint32_t *skey;
-    __device__ uint32_t operator()(uint64_t p) const { return (p == 0 || skey[p] != skey[p - 1]) ? 1u : 0u; }
-};
-struct HeadPutD {
-    const uint32_t *skey;
-    uint32_t *bkey, *bstart;
-    uint32_t n;
-    __device__ void operator()(uint64_t p, uint32_t e, uint32_t v) const {
-        if (v) {
-            bkey[e] = skey[p];
-            bstart[e] = (uint32_t)p;
-        }
-        if (p == n - 1) bstart[e + v] = n;
-    }
-};
-
-// ranks (other than `me`) that own a key of the box's 26-neighbourhood: they need this box as halo
-__device__ unsigned long long halo_mask(const Geom &g, uint32_t key, const uint32_t *spl, int G, int me) {
+// ranks other than `r0` that own a key of the box's 26-neighbourhood: they need the box's particles as halo
+__device__ unsigned long long halo_mask(const Geom &g, uint32_t key, const uint32_t *spl, int G, int r0) {
     const uint32_t c[3] = {compact3(key), compact3(key >> 1), compact3(key >> 2)};
     unsigned long long m = 0ull;
     for (int slot = 0; slot < 27; ++slot) {
@@ -130,40 +156,179 @@ __device__ unsigned long long halo_mask(const Geom &g, uint32_t key, const uint3
         }
         if (!ok) continue;
         const int r = owner_of(spread3(nc[0]) | (spread3(nc[1]) << 1) | (spread3(nc[2]) << 2), spl, G);
-        if (r != me) m |= 1ull << r;
+        if (r != r0) m |= 1ull << r;
     }
     return m;
 }
 
-__global__ void k_halo_count(Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
-                             const uint32_t *__restrict__ Bp, const uint32_t *__restrict__ spl, int G, int me,
-                             unsigned long long *__restrict__ mask, unsigned long long *__restrict__ cnt) {
-    const uint32_t B = *Bp;
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
-        const unsigned long long m = halo_mask(g, bkey[b], spl, G, me);
-        mask[b] = m;
-        const uint32_t nb = bstart[b + 1] - bstart[b];
-        for (unsigned long long mm = m; mm; mm &= mm - 1) atomicAdd(&cnt[__ffsll((long long)mm) - 1], (unsigned long long)nb);
+// halo_mask with an O(1) exit: if the box's 3x3x3 neighbourhood lies inside the Morton-aligned cube of side 2^l
+// (l = smallest level at which no coordinate sits on the cube's faces, i.e. its low l bits are neither all 0 nor
+// all 1) with no domain wrap, and both ends of that cube's key range belong to r0, every neighbour key is r0's
+// (rank ranges are contiguous in key order): no halo.
+__device__ __forceinline__ unsigned long long halo_of(const Geom &g, uint32_t key, const uint32_t *spl, int G,
+                                                      int r0) {
+    if (G == 1) return 0ull;
+    const uint32_t c[3] = {compact3(key), compact3(key >> 1), compact3(key >> 2)};
+    int l = 0;
+    bool fast = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        if (c[d] == 0u || c[d] + 1u >= (uint32_t)g.nbox[d]) fast = false;
+        const int tz = __ffs(c[d]) - 1, to = __ffs(~c[d]) - 1;  // trailing zeros / ones (c[d] != 0 if fast)
+        l = max(l, max(tz, to) + 1);
     }
+    if (fast && 3 * l < 32) {
+        const uint32_t span = (1u << (3 * l)) - 1u;
+        if (owner_of(key & ~span, spl, G) == r0 && owner_of(key | span, spl, G) == r0) return 0ull;
+    }
+    return halo_mask(g, key, spl, G, r0);
 }
 
-// warp per box: a box bound for rank r is copied whole (sorted order) to a slot reserved with one atomic
-template <typename V4>
-__global__ void k_halo_pack(const uint32_t *__restrict__ bstart, const uint32_t *__restrict__ Bp,
-                            const unsigned long long *__restrict__ mask, const V4 *__restrict__ sorted,
-                            const long long *__restrict__ base, unsigned long long *__restrict__ cursor,
-                            V4 *__restrict__ out) {
-    const uint32_t B = *Bp;
-    const unsigned lane = threadIdx.x & 31u;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nwarps) {
-        const uint32_t s0 = bstart[b], nb = bstart[b + 1] - s0;
-        for (unsigned long long mm = mask[b]; mm; mm &= mm - 1) {
-            const int r = __ffsll((long long)mm) - 1;
-            unsigned long long pos = 0;
-            if (lane == 0) pos = atomicAdd(&cursor[r], (unsigned long long)nb);
-            pos = __shfl_sync(0xffffffffu, pos, 0);
-            for (uint32_t j = lane; j < nb; j += 32) out[base[r] + pos + j] = sorted[s0 + j];
+// route, pass 1 (tile = 4096 input particles): owner + halo mask of every particle, and the tile's count per
+// destination group (group 2r = owned by rank r, 2r+1 = halo for rank r), column-major tcnt[group][tile]
+__global__ void __launch_bounds__(RT_THREADS) k_route_count(Geom g, const uint32_t *__restrict__ key, uint32_t n,
+                                                            const uint32_t *__restrict__ spl, int G,
+                                                            uint8_t *__restrict__ r0_out,
+                                                            unsigned long long *__restrict__ mask_out,
+                                                            uint32_t *__restrict__ tcnt, uint32_t ntiles) {
+    __shared__ uint32_t s_spl[MAX_RANKS + 1];
+    __shared__ uint32_t s_cnt[2 * MAX_RANKS];
+    const unsigned t = threadIdx.x;
+    if (t <= (unsigned)G) s_spl[t] = spl[t];
+    if (t < 2u * G) s_cnt[t] = 0u;
+    __syncthreads();
+    const uint32_t base = blockIdx.x * RT_TILE;
+#pragma unroll 4
+    for (int i = 0; i < RT_ITEMS; ++i) {
+        const uint32_t p = base + i * RT_THREADS + t;
+        if (p >= n) break;
+        const uint32_t k = key[p];
+        const int r0 = owner_of(k, s_spl, G);
+        const unsigned long long m = halo_of(g, k, s_spl, G, r0);
+        r0_out[p] = (uint8_t)r0;
+        mask_out[p] = m;
+        atomicAdd(&s_cnt[2 * r0], 1u);
+        for (unsigned long long mm = m; mm; mm &= mm - 1) atomicAdd(&s_cnt[2 * (__ffsll((long long)mm) - 1) + 1], 1u);
+    }
+    __syncthreads();
+    if (t < 2u * G) tcnt[(size_t)t * ntiles + blockIdx.x] = s_cnt[t];
+}
+
+// route, pass 2: block g scans column g of tcnt in place (exclusive tile offsets inside the group) and writes the
+// group total gtot[g]
+__global__ void __launch_bounds__(1024) k_route_scan(uint32_t *__restrict__ tcnt, uint32_t ntiles,
+                                                     unsigned long long *__restrict__ gtot) {
+    __shared__ uint32_t s_w[32];
+    const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
+    uint32_t *col = tcnt + (size_t)blockIdx.x * ntiles;
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < ntiles; b0 += 1024) {
+        const uint32_t i = b0 + t;
+        const uint32_t v = i < ntiles ? col[i] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (unsigned)o) x += y;
+        }
+        if (lane == 31) s_w[w] = x;
+        __syncthreads();
+        uint32_t add = 0, tot = 0;
+        for (int j = 0; j < 32; ++j) {
+            add += j < (int)w ? s_w[j] : 0u;
+            tot += s_w[j];
+        }
+        if (i < ntiles) col[i] = carry + x - v + add;
+        carry += tot;
+        __syncthreads();
+    }
+    if (t == 0) gtot[blockIdx.x] = carry;
+}
+
+// route, pass 3: stable multi-split.  The send buffer is laid out by group (to rank 0: owned, halo; to rank 1: ...),
+// each group in input order: tile offsets (pass 2) + per-warp offsets (pass A below) + the in-warp rank (match /
+// ballot, in input order).  Records {x,y,z,m} are read straight from the caller's arrays (coalesced) and written
+// to their send slot; perm_send[j] = input index of the j-th OWNED entry (rank-major), used by the result return.
+template <typename T, typename V4>
+__global__ void __launch_bounds__(RT_THREADS) k_route_scatter(const T *__restrict__ pos, const T *__restrict__ q,
+                                                              const uint8_t *__restrict__ r0_in,
+                                                              const unsigned long long *__restrict__ mask_in,
+                                                              uint32_t n, int G, const uint32_t *__restrict__ toff,
+                                                              uint32_t ntiles,
+                                                              const unsigned long long *__restrict__ gtot,
+                                                              V4 *__restrict__ send, uint32_t *__restrict__ perm_send) {
+    __shared__ unsigned long long s_gbase[2 * MAX_RANKS];
+    __shared__ uint32_t s_obase[MAX_RANKS];
+    __shared__ uint32_t s_w[RT_WARPS][2 * MAX_RANKS];
+    const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
+    const int NG = 2 * G;
+    if (t == 0) {
+        unsigned long long a = 0, o = 0;
+        for (int gi = 0; gi < NG; ++gi) {
+            s_gbase[gi] = a;
+            a += gtot[gi];
+            if (!(gi & 1)) {
+                s_obase[gi >> 1] = (uint32_t)o;
+                o += gtot[gi];
+            }
+        }
+    }
+    for (int i = t; i < RT_WARPS * NG; i += RT_THREADS) s_w[i / NG][i % NG] = 0u;
+    __syncthreads();
+    const uint32_t seg = blockIdx.x * RT_TILE + w * 32 * RT_ITEMS;
+    // pass A: per-warp counts per group
+    for (int i = 0; i < RT_ITEMS; ++i) {
+        const uint32_t p = seg + i * 32 + lane;
+        if (p >= n) break;
+        atomicAdd(&s_w[w][2 * r0_in[p]], 1u);
+        for (unsigned long long mm = mask_in[p]; mm; mm &= mm - 1)
+            atomicAdd(&s_w[w][2 * (__ffsll((long long)mm) - 1) + 1], 1u);
+    }
+    __syncthreads();
+    if (t < (unsigned)NG) {  // exclusive prefix over the warps + the tile's offset inside the group
+        uint32_t a = toff[(size_t)t * ntiles + blockIdx.x];
+        for (int ww = 0; ww < RT_WARPS; ++ww) {
+            const uint32_t c = s_w[ww][t];
+            s_w[ww][t] = a;
+            a += c;
+        }
+    }
+    __syncthreads();
+    // pass B: in input order, stable ranks inside the warp
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int i = 0; i < RT_ITEMS; ++i) {
+        const uint32_t p = seg + i * 32 + lane;
+        const bool ok = p < n;
+        const uint32_t act = __ballot_sync(0xffffffffu, ok);
+        if (!act) break;  // warp-uniform
+        const int r0 = ok ? (int)r0_in[p] : -1;
+        const unsigned long long m = ok ? mask_in[p] : 0ull;
+        V4 rec;
+        if (ok) {
+            rec.x = pos[(size_t)3 * p + 0];
+            rec.y = pos[(size_t)3 * p + 1];
+            rec.z = pos[(size_t)3 * p + 2];
+            rec.w = q[p];
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, r0);
+        uint32_t slot = 0;
+        if (ok) slot = s_w[w][2 * r0] + __popc(peers & lt);
+        __syncwarp();
+        if (ok) {
+            if (lane == (unsigned)(__ffs(peers) - 1)) s_w[w][2 * r0] += __popc(peers);
+            send[s_gbase[2 * r0] + slot] = rec;
+            perm_send[s_obase[r0] + slot] = p;
+        }
+        __syncwarp();
+        if (__ballot_sync(0xffffffffu, m != 0ull)) {
+            for (int r = 0; r < G; ++r) {
+                const uint32_t bm = __ballot_sync(0xffffffffu, (m >> r) & 1ull);
+                if (!bm) continue;
+                if ((m >> r) & 1ull) send[s_gbase[2 * r + 1] + s_w[w][2 * r + 1] + __popc(bm & lt)] = rec;
+                __syncwarp();
+                if (lane == 0) s_w[w][2 * r + 1] += __popc(bm);
+                __syncwarp();
+            }
         }
     }
 }
@@ -234,26 +399,37 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
     using V4 = typename V4T<T>::type;
     free_distributed(P);  // a previous build's exchange buffers (p2p_plan_update on a collective plan)
     CommBase *C = P->comm;
-    const int G = C->nranks, me = C->rank;
+    const int G = C->nranks, me = C->rank, NG = 2 * G;
+    if (G > MAX_RANKS) {
+        set_error("multi-GPU plans support at most 64 ranks (u64 halo masks)");
+        return P2P_ERR_UNSUPPORTED;
+    }
     cudaStream_t st = P->stream;
     const uint32_t n_in = (uint32_t)P->n_in;
     const T *pos = (const T *)pos_v, *q = (const T *)q_v;
     Tmp tmp{st, {}};
     const unsigned gb = grid1(std::max<uint32_t>(n_in, 1), P->num_sms);
-    // ---- 1. keys of the input particles ----
-    uint32_t *key = nullptr, *idx = nullptr, *kalt = nullptr, *valt = nullptr, *hist8 = nullptr, *status = nullptr;
-    unsigned long long *err = nullptr;
     const size_t nn = std::max<uint32_t>(n_in, 1);
+    const uint32_t ntiles = div_up(n_in, RT_TILE);
+    // read-back words: [G][NG] all-gathered group totals | [NG] this rank's totals | [G+1] splitters |
+    // out-of-domain count (all ranks) | this rank's first out-of-domain index
+    const size_t x_gall = 0, x_gtot = (size_t)G * NG, x_spl = x_gtot + NG, x_erra = x_spl + G + 1, x_erri = x_erra + 1;
+    const size_t xwords = x_erri + 1;
+    uint32_t *key = nullptr, *spl = nullptr, *tcnt = nullptr;
+    uint8_t *r0 = nullptr;
+    unsigned long long *err = nullptr, *hmask = nullptr, *xfer = nullptr;
     P2P_CUDA_TRY(tmp.get(&key, 4 * nn));
-    P2P_CUDA_TRY(tmp.get(&idx, 4 * nn));
-    P2P_CUDA_TRY(tmp.get(&kalt, 4 * nn));
-    P2P_CUDA_TRY(tmp.get(&valt, 4 * nn));
-    P2P_CUDA_TRY(tmp.get(&hist8, 4 * 4 * 256));
     P2P_CUDA_TRY(tmp.get(&err, 8));
+    P2P_CUDA_TRY(tmp.get(&xfer, 8 * xwords));
+    P2P_CUDA_TRY(tmp.get(&spl, 4 * (G + 1)));
+    P2P_CUDA_TRY(tmp.get(&r0, nn));
+    P2P_CUDA_TRY(tmp.get(&hmask, 8 * nn));
+    P2P_CUDA_TRY(tmp.get(&tcnt, 4 * (size_t)NG * std::max<uint32_t>(ntiles, 1)));
     P2P_CUDA_TRY(cudaMemsetAsync(err, 0xff, 8, st));
-    if (n_in) P2P_LAUNCH(k_keys<T>, gb, 256, 0, st, pos, 3, n_in, P->geom, key, idx, err);
+    // ---- 1. keys of the input particles ----
+    if (n_in) P2P_LAUNCH(k_keys<T>, gb, 256, 0, st, pos, n_in, P->geom, key, err);
     // ---- 2. supercell histogram (+ one extra bin: ranks with an out-of-domain input), all-reduced ----
-    const int sc_bits = std::min(P->key_bits, 20), shift = P->key_bits - sc_bits;
+    const int sc_bits = std::min(P->key_bits, 18), shift = P->key_bits - sc_bits;
     const size_t nbins = (size_t)1 << sc_bits;
     unsigned long long *hist = nullptr;
     P2P_CUDA_TRY(tmp.get(&hist, 8 * (nbins + 1)));
@@ -262,154 +438,80 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
     P2P_LAUNCH(k_err_flag, 1, 1, 0, st, err, hist + nbins);
     p2p_status s = C->allreduce_sum_u64(hist, nbins + 1, st);
     if (s != P2P_OK) return s;
-    std::vector<unsigned long long> h(nbins + 1);
-    unsigned long long herr = ~0ull;
-    P2P_CUDA_TRY(cudaMemcpyAsync(h.data(), hist, 8 * (nbins + 1), cudaMemcpyDeviceToHost, st));
-    P2P_CUDA_TRY(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, st));
-    P2P_CUDA_TRY(cudaStreamSynchronize(st));
-    if (h[nbins]) {  // every rank bails out consistently
-        if (herr != ~0ull) {
+    // ---- 3. count-balanced splitters on the device, identical on every rank (C20) ----
+    P2P_LAUNCH(k_splitters, 1, SPL_THREADS, 0, st, hist, (uint32_t)nbins, shift, P->key_bits, G, spl, xfer + x_spl,
+               xfer + x_erra);
+    // ---- 4./5. route counts per destination group, scanned and all-gathered ----
+    if (ntiles)
+        P2P_LAUNCH(k_route_count, ntiles, RT_THREADS, 0, st, P->geom, key, n_in, spl, G, r0, hmask, tcnt, ntiles);
+    P2P_LAUNCH(k_route_scan, NG, 1024, 0, st, tcnt, ntiles, xfer + x_gtot);
+    s = C->allgather_u64(xfer + x_gtot, xfer + x_gall, NG, st);
+    if (s != P2P_OK) return s;
+    P2P_CUDA_TRY(cudaMemcpyAsync(xfer + x_erri, err, 8, cudaMemcpyDeviceToDevice, st));
+    std::vector<unsigned long long> hx(xwords);
+    P2P_CUDA_TRY(cudaMemcpyAsync(hx.data(), xfer, 8 * xwords, cudaMemcpyDeviceToHost, st));
+    P2P_CUDA_TRY(cudaStreamSynchronize(st));  // the ONE host synchronisation of the collective build
+    if (hx[x_erra]) {  // every rank bails out consistently
+        if (hx[x_erri] != ~0ull) {
             char buf[160];
-            snprintf(buf, sizeof buf, "position of input particle %llu is outside the domain (C6)", herr);
+            snprintf(buf, sizeof buf, "position of input particle %llu is outside the domain (C6)", hx[x_erri]);
             set_error(buf);
         } else {
             set_error("another rank has a position outside the domain (C6)");
         }
         return P2P_ERR_OUT_OF_DOMAIN;
     }
-    // ---- 3. count-balanced splitters, identical on every rank (C20) ----
     P->splitters.assign(G + 1, 0u);
-    compute_splitters(h.data(), (int64_t)nbins, shift, P->key_bits, G, P->splitters.data());
+    for (int r = 0; r <= G; ++r) P->splitters[r] = (uint32_t)hx[x_spl + r];
     const uint32_t lo = P->splitters[me], hi = P->splitters[me + 1];
     P->geom.tkey_lo = lo;
     P->geom.tkey_hi = hi > lo ? hi - 1 : 0u;
     if (hi <= lo) P->geom.tkey_lo = 1;  // empty range: no target box
-    uint32_t *spl = nullptr;
-    P2P_CUDA_TRY(tmp.get(&spl, 4 * (G + 1)));
-    P2P_CUDA_TRY(cudaMemcpyAsync(spl, P->splitters.data(), 4 * (G + 1), cudaMemcpyHostToDevice, st));
-    // ---- 4. owners + stable order by owner (1-pass radix sort on the owner rank: stability keeps input order) ----
-    uint32_t *dest = nullptr;
-    unsigned int *dcnt = nullptr;
-    P2P_CUDA_TRY(tmp.get(&dest, 4 * nn));
-    P2P_CUDA_TRY(tmp.get(&dcnt, 4 * G));
-    P2P_CUDA_TRY(cudaMemsetAsync(dcnt, 0, 4 * G, st));
-    P2P_CUDA_TRY(tmp.get(&status, 4 * std::max<size_t>(1, radix_status_words(nn, 1))));
-    if (n_in) P2P_LAUNCH(k_dest, gb, 256, 0, st, key, n_in, spl, G, dest, dcnt);
-    uint32_t *sdest = nullptr, *order = nullptr;
-    P2P_CUDA_TRY(radix_sort_pairs(dest, idx, kalt, valt, n_in, 1, P->ctr, hist8, status, st, &sdest, &order));
-    P2P_CUDA_TRY(dalloc((void **)&P->perm_send, 4 * nn, st));
-    P2P_CUDA_TRY(cudaMemcpyAsync(P->perm_send, order, 4 * (size_t)n_in, cudaMemcpyDeviceToDevice, st));
-    std::vector<unsigned int> hc(G);
-    P2P_CUDA_TRY(cudaMemcpyAsync(hc.data(), dcnt, 4 * G, cudaMemcpyDeviceToHost, st));
-    P2P_CUDA_TRY(cudaStreamSynchronize(st));
+    // send: to rank r the run [owned by r ; halo for r]; receive from rank s: [owned from s ; halo from s]
+    // rp_scnt[r] / rp_soff[r]: owned entries sent to r and their offset among this rank's owned entries (result
+    // return); rp_rcnt[s] / rp_roff[s]: owned entries received from s and the offset of s's run in the local input
+    const unsigned long long *gme = &hx[x_gall + (size_t)me * NG];
     P->rp_scnt.assign(G, 0);
     P->rp_soff.assign(G, 0);
     P->rp_rcnt.assign(G, 0);
     P->rp_roff.assign(G, 0);
+    std::vector<int64_t> so(G), sc(G), ro(G), rc(G);
+    int64_t e_send = 0, n_loc = 0, n_own = 0, o_sent = 0;
     for (int r = 0; r < G; ++r) {
-        P->rp_scnt[r] = hc[r];
-        if (r) P->rp_soff[r] = P->rp_soff[r - 1] + P->rp_scnt[r - 1];
+        const unsigned long long *gr = &hx[x_gall + (size_t)r * NG];
+        P->rp_scnt[r] = (int64_t)gme[2 * r];
+        P->rp_soff[r] = o_sent;
+        o_sent += P->rp_scnt[r];
+        so[r] = e_send * (int64_t)sizeof(V4);
+        sc[r] = (int64_t)(gme[2 * r] + gme[2 * r + 1]) * (int64_t)sizeof(V4);
+        e_send += (int64_t)(gme[2 * r] + gme[2 * r + 1]);
+        P->rp_rcnt[r] = (int64_t)gr[2 * me];
+        P->rp_roff[r] = n_loc;
+        ro[r] = n_loc * (int64_t)sizeof(V4);
+        rc[r] = (int64_t)(gr[2 * me] + gr[2 * me + 1]) * (int64_t)sizeof(V4);
+        n_loc += (int64_t)(gr[2 * me] + gr[2 * me + 1]);
+        n_own += (int64_t)gr[2 * me];
     }
-    s = C->alltoall_counts(P->rp_scnt.data(), P->rp_rcnt.data(), st);
-    if (s != P2P_OK) return s;
-    int64_t n_own = 0;
-    for (int r = 0; r < G; ++r) {
-        P->rp_roff[r] = n_own;
-        n_own += P->rp_rcnt[r];
+    if (o_sent != (int64_t)n_in || n_loc >= ((int64_t)1 << 31)) {
+        set_error(o_sent != (int64_t)n_in ? "route: owned entries != input particles (internal)"
+                                          : "local plan over owned + halo particles would exceed 2^31");
+        return o_sent != (int64_t)n_in ? P2P_ERR_CUDA : P2P_ERR_UNSUPPORTED;
     }
     P->n_own = n_own;
-    // ---- 5. repartition: all-to-all-v of {x,y,z,m} records ----
-    V4 *send = nullptr, *own = nullptr;
-    P2P_CUDA_TRY(tmp.get(&send, sizeof(V4) * nn));
-    P2P_CUDA_TRY(tmp.get(&own, sizeof(V4) * std::max<int64_t>(n_own, 1)));
-    if (n_in) P2P_LAUNCH((k_gather_rec<T, V4>), gb, 256, 0, st, pos, 3, q, 1, order, n_in, send);
-    {
-        std::vector<int64_t> so(G), sc(G), ro(G), rc(G);
-        for (int r = 0; r < G; ++r) {
-            so[r] = P->rp_soff[r] * (int64_t)sizeof(V4);
-            sc[r] = P->rp_scnt[r] * (int64_t)sizeof(V4);
-            ro[r] = P->rp_roff[r] * (int64_t)sizeof(V4);
-            rc[r] = P->rp_rcnt[r] * (int64_t)sizeof(V4);
-        }
-        s = C->alltoallv(send, so.data(), sc.data(), own, ro.data(), rc.data(), st);
-        if (s != P2P_OK) return s;
-    }
-    // ---- 6. owned boxes (sorted), halo selection and exchange ----
-    const uint32_t no = (uint32_t)n_own;
-    const size_t nno = std::max<uint32_t>(no, 1);
-    uint32_t *okey = nullptr, *oidx = nullptr, *okalt = nullptr, *ovalt = nullptr, *ostatus = nullptr;
-    uint32_t *obkey = nullptr, *obstart = nullptr, *oB = nullptr;
-    void *opart = nullptr;
-    P2P_CUDA_TRY(tmp.get(&okey, 4 * nno));
-    P2P_CUDA_TRY(tmp.get(&oidx, 4 * nno));
-    P2P_CUDA_TRY(tmp.get(&okalt, 4 * nno));
-    P2P_CUDA_TRY(tmp.get(&ovalt, 4 * nno));
-    P2P_CUDA_TRY(tmp.get(&ostatus, 4 * std::max<size_t>(1, radix_status_words(nno, std::max(1, P->passes)))));
-    P2P_CUDA_TRY(tmp.get(&obkey, 4 * nno));
-    P2P_CUDA_TRY(tmp.get(&obstart, 4 * (nno + 1)));
-    P2P_CUDA_TRY(tmp.get(&oB, 4));
-    P2P_CUDA_TRY(tmp.get(&opart, scan_partials_bytes(nno)));
-    P2P_CUDA_TRY(cudaMemsetAsync(oB, 0, 4, st));
-    const unsigned gbo = grid1(nno, P->num_sms);
-    if (no) P2P_LAUNCH(k_keys<T>, gbo, 256, 0, st, (const T *)own, 4, no, P->geom, okey, oidx, err);
-    uint32_t *oskey = nullptr, *operm = nullptr;
-    P2P_CUDA_TRY(radix_sort_pairs(okey, oidx, okalt, ovalt, no, P->passes, P->ctr, hist8, ostatus, st, &oskey, &operm));
-    P2P_CUDA_TRY(device_scan<uint32_t>(HeadGetD{oskey}, HeadPutD{oskey, obkey, obstart, no}, nullptr, no, oB, opart,
-                                       st));
-    V4 *osorted = nullptr;
-    P2P_CUDA_TRY(tmp.get(&osorted, sizeof(V4) * nno));
-    if (no)
-        P2P_LAUNCH((k_gather_rec<T, V4>), gbo, 256, 0, st, (const T *)own, 4, (const T *)own + 3, 4, operm, no,
-                   osorted);
-    unsigned long long *omask = nullptr, *hcnt = nullptr, *cursor = nullptr;
-    long long *hbase = nullptr;
-    P2P_CUDA_TRY(tmp.get(&omask, 8 * nno));
-    P2P_CUDA_TRY(tmp.get(&hcnt, 8 * G));
-    P2P_CUDA_TRY(tmp.get(&cursor, 8 * G));
-    P2P_CUDA_TRY(tmp.get(&hbase, 8 * G));
-    P2P_CUDA_TRY(cudaMemsetAsync(hcnt, 0, 8 * G, st));
-    P2P_CUDA_TRY(cudaMemsetAsync(cursor, 0, 8 * G, st));
-    P2P_LAUNCH(k_halo_count, gbo, 256, 0, st, P->geom, obkey, obstart, oB, spl, G, me, omask, hcnt);
-    std::vector<unsigned long long> hh(G);
-    P2P_CUDA_TRY(cudaMemcpyAsync(hh.data(), hcnt, 8 * G, cudaMemcpyDeviceToHost, st));
-    P2P_CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<int64_t> hs(G), hso(G), hr(G), hro(G);
-    int64_t hsend = 0;
-    for (int r = 0; r < G; ++r) {
-        hs[r] = (int64_t)hh[r];
-        hso[r] = hsend;
-        hsend += hs[r];
-    }
-    P2P_CUDA_TRY(cudaMemcpyAsync(hbase, hso.data(), 8 * G, cudaMemcpyHostToDevice, st));
-    V4 *hsendbuf = nullptr;
-    P2P_CUDA_TRY(tmp.get(&hsendbuf, sizeof(V4) * std::max<int64_t>(hsend, 1)));
-    P2P_LAUNCH((k_halo_pack<V4>), gbo, 256, 0, st, obstart, oB, omask, osorted, hbase, cursor, hsendbuf);
-    s = C->alltoall_counts(hs.data(), hr.data(), st);
+    // ---- 6. stable multi-split of the records into the send buffer, ONE all-to-all-v ----
+    V4 *send = nullptr, *local = nullptr;
+    P2P_CUDA_TRY(tmp.get(&send, sizeof(V4) * std::max<int64_t>(e_send, 1)));
+    P2P_CUDA_TRY(tmp.get(&local, sizeof(V4) * std::max<int64_t>(n_loc, 1)));
+    P2P_CUDA_TRY(dalloc((void **)&P->perm_send, 4 * nn, st));
+    if (ntiles)
+        P2P_LAUNCH((k_route_scatter<T, V4>), ntiles, RT_THREADS, 0, st, pos, q, r0, hmask, n_in, G, tcnt, ntiles,
+                   xfer + x_gtot, send, P->perm_send);
+    s = C->alltoallv(send, so.data(), sc.data(), local, ro.data(), rc.data(), st);
     if (s != P2P_OK) return s;
-    int64_t n_halo = 0;
-    for (int r = 0; r < G; ++r) {
-        hro[r] = n_halo;
-        n_halo += hr[r];
-    }
-    // the local input = [owned (repartition order) ; halo]
-    V4 *local = nullptr;
-    P2P_CUDA_TRY(tmp.get(&local, sizeof(V4) * std::max<int64_t>(n_own + n_halo, 1)));
-    if (n_own) P2P_CUDA_TRY(cudaMemcpyAsync(local, own, sizeof(V4) * n_own, cudaMemcpyDeviceToDevice, st));
-    {
-        std::vector<int64_t> so(G), sc(G), ro(G), rc(G);
-        for (int r = 0; r < G; ++r) {
-            so[r] = hso[r] * (int64_t)sizeof(V4);
-            sc[r] = hs[r] * (int64_t)sizeof(V4);
-            ro[r] = (n_own + hro[r]) * (int64_t)sizeof(V4);
-            rc[r] = hr[r] * (int64_t)sizeof(V4);
-        }
-        s = C->alltoallv(hsendbuf, so.data(), sc.data(), local, ro.data(), rc.data(), st);
-        if (s != P2P_OK) return s;
-    }
-    // ---- 7. the local plan over [owned ; halo], targets = this rank's Morton range ----
+    // ---- 7. the local plan over the received records, targets = this rank's Morton range ----
     // capacity buffers persist across p2p_plan_update calls (grow only); the temporaries above are released
     // stream-ordered (cudaFreeAsync), after every collective that reads them has completed on this stream
-    P->n = n_own + n_halo;
+    P->n = n_loc;
     if (P->n == 0) return P2P_OK;
     if (P->n > P->cap) {
         free_capacity(P);
@@ -418,9 +520,10 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
     }
     s = build_gravity_structs(P, nullptr, nullptr, local);
     if (s != P2P_OK) return s;
-    P2P_CUDA_TRY(dalloc(&P->phi_loc, sizeof(T) * std::max<int64_t>(n_own, 1), st));
-    P2P_CUDA_TRY(dalloc(&P->field_loc, 3 * sizeof(T) * std::max<int64_t>(n_own, 1), st));
-    P2P_CUDA_TRY(dalloc(&P->res_own, sizeof(V4) * std::max<int64_t>(n_own, 1), st));
+    const size_t nl = (size_t)std::max<int64_t>(n_loc, 1);
+    P2P_CUDA_TRY(dalloc(&P->phi_loc, sizeof(T) * nl, st));
+    P2P_CUDA_TRY(dalloc(&P->field_loc, 3 * sizeof(T) * nl, st));
+    P2P_CUDA_TRY(dalloc(&P->res_own, sizeof(V4) * nl, st));
     P2P_CUDA_TRY(dalloc(&P->res_back, sizeof(V4) * nn, st));
     return P2P_OK;
 }
@@ -430,15 +533,16 @@ p2p_status eval_dist_t(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
     using V4 = typename V4T<T>::type;
     cudaStream_t st = P->stream;
     const int G = P->comm->nranks;
-    if (P->n > 0) {
+    const uint32_t nl = (uint32_t)P->n, ni = (uint32_t)P->n_in;
+    if (nl > 0) {
+        // results land at the local (received) positions; halo positions are not written and never sent back
         p2p_status s = eval_gravity(P, layout, P->phi_loc, P->field_loc);
         if (s != P2P_OK) return s;
+        P2P_LAUNCH((k_pack_results<T, V4>), grid1(nl, P->num_sms), 256, 0, st, (const T *)P->phi_loc,
+                   (const T *)P->field_loc, nl, (V4 *)P->res_own);
     }
-    const uint32_t no = (uint32_t)P->n_own, ni = (uint32_t)P->n_in;
-    if (no) P2P_LAUNCH((k_pack_results<T, V4>), grid1(no, P->num_sms), 256, 0, st, (const T *)P->phi_loc,
-                       (const T *)P->field_loc, no, (V4 *)P->res_own);
     std::vector<int64_t> so(G), sc(G), ro(G), rc(G);
-    for (int r = 0; r < G; ++r) {  // the reverse of the repartition
+    for (int r = 0; r < G; ++r) {  // the owned head of every received run goes back to its sender
         so[r] = P->rp_roff[r] * (int64_t)sizeof(V4);
         sc[r] = P->rp_rcnt[r] * (int64_t)sizeof(V4);
         ro[r] = P->rp_soff[r] * (int64_t)sizeof(V4);

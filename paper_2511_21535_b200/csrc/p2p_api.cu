@@ -522,6 +522,14 @@ p2p_status p2p_get_info(const p2p_plan *Pc, p2p_info *out) {
     return P2P_OK;
 }
 
+p2p_status p2p_get_splitters(const p2p_plan *P, uint32_t *out, int n) {
+    if (!P || !out) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!P->comm) return fail(P2P_ERR_INVALID_ARGUMENT, "not a multi-GPU plan");
+    if (n != (int)P->splitters.size()) return fail(P2P_ERR_INVALID_ARGUMENT, "n != nranks + 1");
+    std::copy(P->splitters.begin(), P->splitters.end(), out);
+    return P2P_OK;
+}
+
 p2p_status p2p_copy_out(const p2p_plan *Pc, p2p_array which, void *host_dst, size_t bytes) {
     if (!Pc || (!host_dst && bytes)) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
     p2p_plan *P = const_cast<p2p_plan *>(Pc);

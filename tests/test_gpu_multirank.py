@@ -1,7 +1,8 @@
 """Multi-GPU path on one GPU: G emulated ranks (host threads sharing the device, loopback
 communicators) run the full collective algorithm -- supercell histogram all-reduce, count-balanced Morton
-splitters, all-to-all-v repartition, halo exchange, local plan over [owned ; halo], reverse all-to-all-v of the
-results.  Each rank's outputs for its own input slice must equal, BIT FOR BIT, the 1-GPU plan over the rank-major
+splitters (computed on the device), one all-to-all-v routing every particle to its owner and as a halo source to
+every other rank owning one of its box's neighbours, local plan over the received records, reverse all-to-all-v of
+the results.  Each rank's outputs for its own input slice must equal, BIT FOR BIT, the 1-GPU plan over the rank-major
 concatenation of the slices (SURVEY §8e "bitwise identical to 1 GPU"), and match the fp64 oracle."""
 import threading
 
@@ -41,7 +42,7 @@ def run_ranks(P, inp, slices, layouts):
                 m = torch.from_numpy(np.ascontiguousarray(inp.mass[sl])).cuda()
                 plan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps,
                               stream=stream, comm=comms[r])
-                infos[r] = plan.info
+                infos[r] = (plan.info, P.p2p_get_splitters(plan.handle, nr))
                 plan.restructure()
                 res = {}
                 for lay in layouts:
@@ -77,7 +78,16 @@ def single(P, inp, layouts):
         return res, plan.info
 
 
-@pytest.mark.parametrize("case", ["plummer_g2", "plummer_g3", "uniform_g4", "open_g2", "skewed_g4", "fp64_g2"])
+def expected_splitters(P, cat, key_bits, nr):
+    """p2p_partition_splitters (host) of the global supercell histogram built from the oracle's keys"""
+    sc_bits = min(key_bits, 18)
+    shift = key_bits - sc_bits
+    hist = np.bincount(oracle.GravityPlan(cat, with_red=False).key >> shift, minlength=1 << sc_bits)
+    return P.p2p_partition_splitters(hist.astype(np.uint64), shift, key_bits, nr)
+
+
+@pytest.mark.parametrize("case", ["plummer_g2", "plummer_g3", "uniform_g4", "open_g2", "skewed_g4", "fp64_g2",
+                                  "plummer64_g8", "plummer128_g5", "uniform_g7"])
 def test_multirank_bitwise_equals_single_gpu(P, case):
     rng = np.random.default_rng(17)
     if case.startswith("plummer"):
@@ -88,6 +98,12 @@ def test_multirank_bitwise_equals_single_gpu(P, case):
         inp = G.random_gravity(5000, 0, seed=7, periodic=0, nbox=(7, 5, 6), h=0.15, lo=(-0.2, 0.1, 0.0))
     elif case == "fp64_g2":
         inp = G.plummer(8000, 8, seed=8, dtype=np.float64)
+    elif case == "plummer64_g8":
+        inp = G.plummer(60000, 64, seed=10)     # 18-bit keys: one supercell per box
+    elif case == "plummer128_g5":
+        inp = G.plummer(40000, 128, seed=11)    # 21-bit keys: supercells of 8 boxes
+    elif case == "uniform_g7":
+        inp = G.uniform_per_box(12, 2, seed=12)
     else:
         inp = G.plummer(20000, 16, seed=9)
     nr = int(case[-1])
@@ -105,7 +121,11 @@ def test_multirank_bitwise_equals_single_gpu(P, case):
     ref, rinfo = single(P, cat, lays)
     out, infos = run_ranks(P, cat, [np.arange(cuts[r], cuts[r + 1]) for r in range(nr)], lays)
     # every target box is owned by exactly one rank: pair counts add up to the 1-GPU plan's
-    assert sum(i.n_pairs for i in infos) == rinfo.n_pairs
+    assert sum(i.n_pairs for i, _ in infos) == rinfo.n_pairs
+    # the device-side splitters (k_splitters) equal the host function on the same global histogram, on every rank
+    want = expected_splitters(P, cat, rinfo.key_bits, nr)
+    for _, spl in infos:
+        assert np.array_equal(spl, want), (spl, want)
     for lay in lays:
         phi = np.concatenate([out[r][lay][0] for r in range(nr)])
         fld = np.concatenate([out[r][lay][1] for r in range(nr)])
