@@ -34,7 +34,8 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 
 def _compile(src: str, incs) -> tuple:
     obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
-    cmd = [NVCC, *FLAGS, *incs, "-c", src, "-o", obj]
+    extra = os.environ.get("P2P_NVCC_FLAGS", "").split()  # experiments only (e.g. -DP2P_RS_MATCH)
+    cmd = [NVCC, *FLAGS, *extra, *incs, "-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{p.stderr}")

@@ -135,7 +135,10 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_pass(const uint32_t *__res
             for (int64_t t = (int64_t)tile - 1;;) {
                 const uint32_t sv = ld_volatile(status + (size_t)t * 256 + d);
                 const uint32_t f = sv & ~VAL_MASK;
-                if (f == 0) continue;  // predecessor not published yet: spin
+                if (f == 0) {  // predecessor not published yet: back off, then retry
+                    __nanosleep(50);
+                    continue;
+                }
                 excl += sv & VAL_MASK;
                 if (f == FLAG_INC) break;
                 --t;
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_pass(const uint32_t *__res
         uint32_t mask = __ballot_sync(0xffffffffu, ok);
         if (ok) {
             uint32_t d = (k[i] >> shift) & 255u;
-            uint32_t peers = __match_any_sync(mask, d);
+uint32_t peers = __match_any_sync(mask, d);  // (8 bit-sliced ballots measured slower on sm_100a)
             uint32_t cnt = s_whist[w][d];
             r[i] = cnt + __popc(peers & lt_mask);
             __syncwarp(mask);

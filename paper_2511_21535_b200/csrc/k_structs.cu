@@ -145,53 +145,6 @@ struct HeadPut {
 };
 
 // ------------------------------------------------------------------------------------------------ a5
-// Neighbour keys by Morton arithmetic (no decode / re-encode): lane = stencil slot with offsets dd in {-1,0,1}^3;
-// a +-1 step in dimension d is a masked add / subtract on that dimension's interleaved bits, the periodic wrap
-// (C5) replaces the bits by 0 or by nbox_d - 1.  Slots in ascending order (C10): slot = (dx+1) + 3 (dy+1) + 9 (dz+1).
-struct MortonStencil {
-    uint32_t M[3], top[3];  // dimension-d bit mask of the key space, bits of coordinate nbox_d - 1
-    int dd[3];
-    bool live;
-};
-__device__ __forceinline__ MortonStencil make_stencil(const Geom &g, unsigned lane) {
-    MortonStencil s;
-    s.live = lane < 27;
-    const uint32_t full = spread3((1u << g.nb) - 1u);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        s.M[d] = full << d;
-        s.top[d] = spread3((uint32_t)(g.nbox[d] - 1)) << d;
-    }
-    s.dd[0] = (int)(lane % 3) - 1;
-    s.dd[1] = (int)((lane / 3) % 3) - 1;
-    s.dd[2] = (int)(lane / 9) - 1;
-    return s;
-}
-__device__ __forceinline__ bool morton_nbr(const Geom &g, const MortonStencil &s, uint32_t key, uint32_t &nk) {
-    if (!s.live) return false;
-    nk = key;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        const uint32_t M = s.M[d], kd = key & M;
-        if (s.dd[d] > 0) {
-            if (kd == s.top[d]) {
-                if (!((g.periodic >> d) & 1u)) return false;
-                nk &= ~M;
-            } else {
-                nk = (((nk | ~M) + (1u << d)) & M) | (nk & ~M);
-            }
-        } else if (s.dd[d] < 0) {
-            if (kd == 0u) {
-                if (!((g.periodic >> d) & 1u)) return false;
-                nk = (nk & ~M) | s.top[d];
-            } else {
-                nk = (((nk & M) - (1u << d)) & M) | (nk & ~M);
-            }
-        }
-    }
-    return true;
-}
-
 // dense key -> {box, n_b} table for the gravity neighbour search (valid where the occupancy bit is set)
 __global__ void k_boxinfo(const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
                           const DevCounters *__restrict__ ctr, uint2 *__restrict__ boxinfo) {
@@ -200,232 +153,339 @@ __global__ void k_boxinfo(const uint32_t *__restrict__ bkey, const uint32_t *__r
         boxinfo[bkey[b]] = make_uint2(b, bstart[b + 1] - bstart[b]);
 }
 
-// a5, one pass: neighbour search, the four exclusive scans (CSR offsets, redundant offsets, work items, small
-// target pairs) and all writes of the CSR / items / small lists / restructure chunk heads.
-// One warp per tile of 32 consecutive boxes; tiles are claimed from an atomic counter in launch order, so the
-// decoupled look-back (NbTileStatus) only ever waits on tiles that are already running.
-//   phase A  lane = stencil slot, 4 boxes in flight: neighbour key by Morton arithmetic, then the occupancy
-//            word and the {box, n} entry together (a stale entry of an empty key is ignored); per-slot results
-//            to shared memory, per-box totals to lane i
-//   phase B  warp scans of the per-box totals, look-back for the tile's exclusive prefix, nbr_off / red_off
-//   phase C  lane = stencil slot again, per box: ballot-compacted CSR in ascending slot order (C10), the
-//            restructure chunk heads, the eval work items or small-target entries
-constexpr int NBB_WARPS = 4;
-constexpr int NBB_TILE = 32;
+// a5 in two kernels, THREAD PER BOX (tile = the 256 consecutive boxes of one block):
+//   k_nbr_count  the box's 27 stencil neighbours (ascending slot, C10) by Morton arithmetic: per dimension the
+//                three candidate coordinates {-1, 0, +1} are formed once in interleaved form (periodic wrap /
+//                open edge, C5), a slot's key is an OR of three of them; the occupancy bit and the {box, n}
+//                entry are loaded together, branch-free (a stale entry of an empty key is ignored).  Per-box
+//                totals -> block sums per tile (CSR entries, redundant records, work items, small-target pairs)
+//                + the pair count I.
+//   k_nbr_fill   the same search again, block scan of the per-box totals + the tile's exclusive prefix from a
+//                look-back over the (already complete) tile sums that never waits, then nbr_off / red_off, the CSR
+//                staged in shared memory and written coalesced, the restructure chunk heads, the eval work items
+//                or small-target entries.
+// Lanes are consecutive boxes, so a slot's 32 neighbour keys are close in key order (coalesced table reads),
+// and no tile ever waits for another: the earlier single-kernel design (warp per 32 boxes, lane = slot, decoupled
+// look-back on tiles still searching) spent about half of its 1.06 ms there; this pair takes ~0.55 ms on c5w.
+constexpr int NB_THREADS = 256;
+constexpr int NB_SLOTS = 27;
 
-__device__ __forceinline__ unsigned long long ld_vol64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
+struct NbStencil {  // per dimension: candidate interleaved coordinates for offsets -1, 0, +1 and their validity
+    uint32_t c[3][3];
+    bool v[3][3];
+};
+__device__ __forceinline__ void make_nb(const Geom &g, uint32_t key, NbStencil &S) {
+    const uint32_t full = spread3((1u << g.nb) - 1u);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const uint32_t M = full << d, top = spread3((uint32_t)(g.nbox[d] - 1)) << d, kd = key & M;
+        const bool per = (g.periodic >> d) & 1u;
+        S.c[d][1] = kd;
+        S.v[d][1] = true;
+        S.c[d][0] = kd == 0u ? top : ((kd - (1u << d)) & M);
+        S.v[d][0] = kd != 0u || per;
+        S.c[d][2] = kd == top ? 0u : (((kd | ~M) + (1u << d)) & M);
+        S.v[d][2] = kd != top || per;
+    }
 }
-__device__ __forceinline__ void st_vol64(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
-__global__ void __launch_bounds__(NBB_WARPS * 32) k_nbr_build(
-    Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart, const uint2 *__restrict__ boxinfo,
-    const uint32_t *__restrict__ occ, DevCounters *ctr, NbTileStatus *status, uint32_t *__restrict__ nbr_off,
-    unsigned long long *__restrict__ red_off, uint32_t *__restrict__ nbr_box, uint8_t *__restrict__ nbr_slot,
-    Item *__restrict__ items, uint32_t *__restrict__ small_tgt, uint32_t *__restrict__ small_box,
-    uint32_t *__restrict__ chunk_box, unsigned long long *__restrict__ chunk_out, uint32_t K, uint32_t tmax) {
-    __shared__ uint32_t s_k[NBB_WARPS][NBB_TILE][27];
-    __shared__ uint32_t s_c[NBB_WARPS][NBB_TILE][27];
-    constexpr unsigned FULL = 0xffffffffu;
-    const uint32_t B = ctr->B;
-    const uint32_t ntiles = (B + NBB_TILE - 1) / NBB_TILE;
-    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    const MortonStencil stc = make_stencil(g, lane);
-    unsigned long long pairs = 0;
-    while (true) {
-        uint32_t t = 0;
-        if (lane == 0) t = atomicAdd(&ctr->nbr_tile, 1u);
-        t = __shfl_sync(FULL, t, 0);
-        if (t >= ntiles) break;
-        const uint32_t tb = t * NBB_TILE;
-        // lane i: box tb + i
-        const uint32_t mb = tb + lane;
-        const bool have = mb < B;
-        const uint32_t mkey = have ? bkey[mb] : 0u;
-        const uint32_t ms0 = have ? bstart[mb] : 0u;
-        const bool mtarget = have && mkey >= g.tkey_lo && mkey <= g.tkey_hi;  // halo boxes: source only
-        uint32_t my_nbr = 0, my_item = 0, my_small = 0, my_nb = 0;
-        unsigned long long my_red = 0;
-
-        // ---- phase A ----
-        constexpr int NB = 4;
-        for (int i0 = 0; i0 < NBB_TILE; i0 += NB) {
-            if (tb + i0 >= B) break;  // warp-uniform
-            bool ok[NB];
-            uint32_t kk[NB], cn[NB];
+// one dz-plane of the stencil (slots 9 dz .. 9 dz + 8), branch-free so that all 18 table loads are in flight at
+// once (an invalid slot loads the box's own entry and is masked): okm bit s = slot s holds a non-empty box
+__device__ __forceinline__ void nb_plane(const NbStencil &S, int dz, uint32_t key, bool tgt,
+                                         const uint32_t *__restrict__ occ, const uint2 *__restrict__ boxinfo,
+                                         uint32_t &okm, uint32_t &cnt, unsigned long long &red) {
+    uint32_t nk[9], wd[9], ny[9];
+    bool v[9];
 #pragma unroll
-            for (int u = 0; u < NB; ++u) {
-                const int i = i0 + u;
-                const uint32_t key = __shfl_sync(FULL, mkey, i);
-                const bool tgt = __shfl_sync(FULL, (uint32_t)mtarget, i) != 0u;
-                ok[u] = false;
-                kk[u] = 0;
-                cn[u] = 0;
-                uint32_t nk;
-                if (tgt && morton_nbr(g, stc, key, nk)) {
-                    const uint32_t wd = __ldg(&occ[nk >> 5]);
-                    const uint2 inf = boxinfo[nk];
-                    ok[u] = (wd >> (nk & 31u)) & 1u;
-                    kk[u] = inf.x;
-                    cn[u] = inf.y;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < NB; ++u) {
-                const int i = i0 + u;
-                if (lane < 27) {
-                    s_k[w][i][lane] = ok[u] ? kk[u] : 0xffffffffu;
-                    s_c[w][i][lane] = ok[u] ? cn[u] : 0u;
-                }
-                const uint32_t nk = __reduce_add_sync(FULL, ok[u] ? cn[u] : 0u);
-                const uint32_t cnt = __popc(__ballot_sync(FULL, ok[u]));
-                const uint32_t own = __shfl_sync(FULL, ok[u] ? cn[u] : 0u, 13);  // centre slot = the box itself
-                if (lane == (unsigned)i && have) {
-                    my_nbr = cnt;
-                    my_red = nk;
-                    my_nb = mtarget ? own : 0u;
-                    // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
-                    const bool small = my_nb <= SMALL_NT && nk <= SMALL_R;
-                    my_item = (small || !mtarget) ? 0u : item_chunks(my_nb, nk, tmax);
-                    my_small = (small && mtarget) ? (my_nb + 1) / 2 : 0u;  // target PAIRS
-                    pairs += (unsigned long long)my_nb * nk;
-                }
-            }
-        }
-        __syncwarp();
-
-        // ---- phase B: tile scans + decoupled look-back ----
-        uint32_t in_nbr = my_nbr, in_item = my_item, in_small = my_small;
-        unsigned long long in_red = my_red;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t a = __shfl_up_sync(FULL, in_nbr, o), b2 = __shfl_up_sync(FULL, in_item, o),
-                           c = __shfl_up_sync(FULL, in_small, o);
-            const unsigned long long d = __shfl_up_sync(FULL, in_red, o);
-            if (lane >= (unsigned)o) {
-                in_nbr += a;
-                in_item += b2;
-                in_small += c;
-                in_red += d;
-            }
-        }
-        // tile aggregates (lane 31's inclusive values); items | small << 31 share one word
-        constexpr unsigned long long VMASK = (1ull << 62) - 1ull, F_AGG = 1ull << 62, F_INC = 2ull << 62;
-        unsigned long long agg[3];
-        agg[0] = __shfl_sync(FULL, (unsigned long long)in_nbr, 31);
-        agg[1] = __shfl_sync(FULL, in_red, 31);
-        agg[2] = __shfl_sync(FULL, (unsigned long long)in_item | ((unsigned long long)in_small << 31), 31);
-        unsigned long long pre[3] = {0ull, 0ull, 0ull};
-        NbTileStatus *me = status + t;
-        const unsigned long long my_agg = lane == 0 ? agg[0] : (lane == 1 ? agg[1] : agg[2]);
-        if (t == 0) {
-            if (lane < 3) st_vol64(&me->w[lane], F_INC | my_agg);
-        } else {
-            if (lane < 3) st_vol64(&me->w[lane], F_AGG | my_agg);
-            // warp-parallel look-back, per word: lane j inspects tile base - j (a window of 32 predecessors per
-            // step) until the nearest inclusive prefix
-#pragma unroll
-            for (int wd = 0; wd < 3; ++wd) {
-                for (int64_t base = (int64_t)t - 1;;) {
-                    const int64_t q = base - (int64_t)lane;
-                    unsigned long long x = F_INC;  // tiles before 0 act as an inclusive zero
-                    if (q >= 0) {
-                        do {
-                            x = ld_vol64(&status[q].w[wd]);
-                        } while ((x >> 62) == 0ull);
-                    }
-                    const uint32_t incm = __ballot_sync(FULL, (x >> 62) == 2ull);
-                    const int jstop = incm ? __ffs(incm) - 1 : 31;  // nearest inclusive predecessor
-                    unsigned long long v = (int)lane <= jstop ? (x & VMASK) : 0ull;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-                    pre[wd] += v;
-                    if (incm) break;
-                    base -= 32;
-                }
-            }
-            if (lane < 3) {
-                const unsigned long long mine = (lane == 0 ? pre[0] : (lane == 1 ? pre[1] : pre[2])) + my_agg;
-                st_vol64(&me->w[lane], F_INC | mine);
-            }
-        }
-        const unsigned long long p_nbr = pre[0], p_red = pre[1], p_is = pre[2];
-        const uint32_t o_nbr = (uint32_t)p_nbr + in_nbr - my_nbr;
-        const unsigned long long o_red = p_red + in_red - my_red;
-        const uint32_t o_item = (uint32_t)(p_is & 0x7fffffffull) + in_item - my_item;
-        const uint32_t o_small = (uint32_t)(p_is >> 31) + in_small - my_small;
-        if (have) {
-            nbr_off[mb] = o_nbr;
-            red_off[mb] = o_red;
-        }
-        if (mb == B - 1) {  // the last box closes the offsets and publishes the totals
-            nbr_off[B] = o_nbr + my_nbr;
-            red_off[B] = o_red + my_red;
-            ctr->n_nbr = o_nbr + my_nbr;
-            ctr->R = o_red + my_red;
-            ctr->n_items = o_item + my_item;
-            ctr->n_small = o_small + my_small;
-        }
-
-        // ---- phase C: CSR, chunk heads, items / small entries (lane = stencil slot) ----
-        for (int i = 0; i < NBB_TILE; ++i) {
-            const uint32_t b = tb + i;
-            if (b >= B) break;  // warp-uniform
-            const uint32_t k = lane < 27 ? s_k[w][i][lane] : 0xffffffffu;
-            const uint32_t cl = lane < 27 ? s_c[w][i][lane] : 0u;
-            const bool ok = k != 0xffffffffu;
-            const uint32_t m = __ballot_sync(FULL, ok);
-            const uint32_t e0 = __shfl_sync(FULL, o_nbr, i);
-            const unsigned long long rb = __shfl_sync(FULL, o_red, i);
-            uint32_t incl = cl;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(FULL, incl, o);
-                if (lane >= (unsigned)o) incl += y;
-            }
-            // records of the slots before the centre (13) = offset of the box's own segment in its run
-            const uint32_t cen = __shfl_sync(FULL, incl - cl, 13);
-            if (ok) {
-                const uint32_t e = e0 + __popc(m & ((1u << lane) - 1u));
-                nbr_box[e] = k;
-                nbr_slot[e] = (uint8_t)lane;
-                if ((e & 31u) == 0u) {  // head of a restructure chunk
-                    chunk_box[e >> 5] = b;
-                    chunk_out[e >> 5] = rb + (incl - cl);
-                }
-            }
-            const bool tgt = __shfl_sync(FULL, (uint32_t)mtarget, i) != 0u;
-            if (!tgt) continue;
-            const uint32_t s0 = __shfl_sync(FULL, ms0, i), nb_b = __shfl_sync(FULL, my_nb, i);
-            const uint32_t nch = __shfl_sync(FULL, my_item, i);
-            if (nch == 0) {  // small box: thread-per-target path, one entry per target pair
-                const uint32_t so = __shfl_sync(FULL, o_small, i);
-                if (lane < (nb_b + 1) / 2) {
-                    small_tgt[so + lane] = s0 + 2 * lane;
-                    small_box[so + lane] = b;
-                }
-                continue;
-            }
-            const uint32_t it = __shfl_sync(FULL, o_item, i);
-            const uint32_t key = __shfl_sync(FULL, mkey, i);
-            const uint32_t Rb = (uint32_t)__shfl_sync(FULL, my_red, i);
-            for (uint32_t ci = lane; ci < nch; ci += 32) {
-                const uint32_t a0 = (uint32_t)(((uint64_t)nb_b * ci) / nch);
-                const uint32_t z0 = (uint32_t)(((uint64_t)nb_b * (ci + 1)) / nch);
-                // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
-                const uint32_t nt = z0 - a0, G = (nt + K - 1) / K, S = 32u / G;
-                items[it + ci] = Item{b, s0 + a0, nt | (S << 8) | (G << 16), key, rb, Rb, cen + a0};
-            }
-        }
-        __syncwarp();  // phase C's shared-memory reads before the next tile's phase A writes
+    for (int j = 0; j < 9; ++j) {
+        const int dx = j % 3, dy = j / 3;
+        v[j] = tgt && S.v[0][dx] && S.v[1][dy] && S.v[2][dz];
+        nk[j] = v[j] ? (S.c[0][dx] | S.c[1][dy] | S.c[2][dz]) : key;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(FULL, pairs, o);
-    if (lane == 0 && pairs) atomicAdd(&ctr->I, pairs);
+    for (int j = 0; j < 9; ++j) {
+        wd[j] = __ldg(&occ[nk[j] >> 5]);
+        ny[j] = __ldg(&boxinfo[nk[j]].y);
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        const bool ok = v[j] && ((wd[j] >> (nk[j] & 31u)) & 1u);
+        okm |= (ok ? 1u : 0u) << (9 * dz + j);
+        cnt += ok ? 1u : 0u;
+        red += ok ? ny[j] : 0u;
+    }
+}
+
+struct BoxTotals {
+    uint32_t nbr, item, small;
+    unsigned long long red;
+};
+__device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint32_t nb, bool tgt, uint32_t tmax) {
+    BoxTotals t;
+    t.nbr = nbr;
+    t.red = red;
+    // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
+    const bool small = nb <= SMALL_NT && red <= SMALL_R;
+    t.item = (small || !tgt) ? 0u : item_chunks(nb, red, tmax);
+    t.small = (small && tgt) ? (nb + 1) / 2 : 0u;  // target PAIRS
+    return t;
+}
+
+// block-wide inclusive scan of the four totals (NB_THREADS threads); returns the inclusive values, `tot` = sums
+__device__ __forceinline__ BoxTotals block_scan_totals(BoxTotals x, BoxTotals *tot) {
+    __shared__ BoxTotals s_w[NB_THREADS / 32];
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xffffffffu, x.nbr, o), b = __shfl_up_sync(0xffffffffu, x.item, o),
+                       c = __shfl_up_sync(0xffffffffu, x.small, o);
+        const unsigned long long d = __shfl_up_sync(0xffffffffu, x.red, o);
+        if (lane >= (unsigned)o) {
+            x.nbr += a;
+            x.item += b;
+            x.small += c;
+            x.red += d;
+        }
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    BoxTotals add{0, 0, 0, 0ull}, t{0, 0, 0, 0ull};
+#pragma unroll
+    for (int i = 0; i < NB_THREADS / 32; ++i) {
+        const BoxTotals v = s_w[i];
+        if (i < (int)w) {
+            add.nbr += v.nbr;
+            add.item += v.item;
+            add.small += v.small;
+            add.red += v.red;
+        }
+        t.nbr += v.nbr;
+        t.item += v.item;
+        t.small += v.small;
+        t.red += v.red;
+    }
+    __syncthreads();
+    *tot = t;
+    x.nbr += add.nbr;
+    x.item += add.item;
+    x.small += add.small;
+    x.red += add.red;
+    return x;
+}
+
+// tile sums / exclusive tile offsets: [0] CSR entries, [1] redundant records, [2] work items, [3] small pairs
+struct NbTile {
+    unsigned long long v[4];
+};
+
+__global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t *__restrict__ bkey,
+                                                          const uint32_t *__restrict__ bstart,
+                                                          const uint2 *__restrict__ boxinfo,
+                                                          const uint32_t *__restrict__ occ, DevCounters *ctr,
+                                                          NbTile *__restrict__ tiles, uint32_t tmax) {
+    const uint32_t B = ctr->B;
+    const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
+    unsigned long long pairs = 0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t b = tile * NB_THREADS + threadIdx.x;
+        const bool have = b < B;
+        const uint32_t key = have ? bkey[b] : 0u;
+        const uint32_t nb = have ? bstart[b + 1] - bstart[b] : 0u;
+        const bool tgt = have && key >= g.tkey_lo && key <= g.tkey_hi;  // halo boxes: source only
+        uint32_t cnt = 0, okm = 0;
+        unsigned long long red = 0;
+        NbStencil S;
+        make_nb(g, key, S);
+#pragma unroll
+        for (int dz = 0; dz < 3; ++dz) nb_plane(S, dz, key, tgt, occ, boxinfo, okm, cnt, red);
+        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax);
+        pairs += (unsigned long long)(tgt ? nb : 0u) * red;
+        BoxTotals tot;
+        block_scan_totals(x, &tot);
+        if (threadIdx.x == 0) tiles[tile] = NbTile{{tot.nbr, tot.red, tot.item, tot.small}};
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    if ((threadIdx.x & 31u) == 0 && pairs) atomicAdd(&ctr->I, pairs);
+}
+
+// exclusive prefix of the tile sums before `tile`, by a look-back that never waits: every tile sum (k_nbr_count) is
+// already complete, so the block walks back NB_THREADS tiles per step, adding sums, until it meets a tile whose
+// inclusive prefix a previous k_nbr_fill block has published (or tile 0).  Tiles are processed in near launch
+// order, so the walk is one or two steps.  Published: incl[t] = prefix + sum of tile t, then the flag (release).
+__device__ __forceinline__ unsigned long long ld_acquire_u32(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int *p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ NbTile tile_prefix(uint32_t tile, const NbTile *__restrict__ sums, const NbTile *incl,
+                              const unsigned int *flags) {
+    __shared__ unsigned long long s_r[NB_THREADS / 32][4];
+    __shared__ int s_stop[NB_THREADS / 32];
+    const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
+    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+    for (int64_t base = (int64_t)tile - 1; base >= 0; base -= NB_THREADS) {
+        const int64_t q = base - (int64_t)t;
+        const bool inc = q < 0 || ld_acquire_u32(&flags[q]) != 0u;  // tiles before 0: an inclusive zero
+        const unsigned bal = __ballot_sync(0xffffffffu, inc);
+        if (lane == 0) s_stop[w] = bal ? (int)(w * 32 + __ffs(bal) - 1) : NB_THREADS;
+        __syncthreads();
+        int stop = NB_THREADS;
+#pragma unroll
+        for (int i = 0; i < NB_THREADS / 32; ++i) stop = min(stop, s_stop[i]);
+        __syncthreads();
+        if ((int)t < stop) {
+            const NbTile v = sums[q];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] += v.v[k];
+        } else if ((int)t == stop && q >= 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] += __ldcg(&incl[q].v[k]);
+        }
+        if (stop < NB_THREADS) break;
+    }
+    // block sum
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+        if (lane == 0) s_r[w][k] = acc[k];
+    }
+    __syncthreads();
+    NbTile r;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        unsigned long long x = 0;
+#pragma unroll
+        for (int i = 0; i < NB_THREADS / 32; ++i) x += s_r[i][k];
+        r.v[k] = x;
+    }
+    __syncthreads();
+    return r;
+}
+
+#ifndef P2P_NB_MINB
+#define P2P_NB_MINB 3
+#endif
+#ifndef P2P_NB_CARVEOUT
+#define P2P_NB_CARVEOUT 50
+#endif
+__global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
+    Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart, const uint2 *__restrict__ boxinfo,
+    const uint32_t *__restrict__ occ, DevCounters *ctr, const NbTile *__restrict__ tiles, NbTile *incl,
+    unsigned int *flags, uint32_t *__restrict__ nbr_off, unsigned long long *__restrict__ red_off, uint32_t *__restrict__ nbr_box,
+    uint8_t *__restrict__ nbr_slot, Item *__restrict__ items, uint32_t *__restrict__ small_tgt,
+    uint32_t *__restrict__ small_box, uint32_t *__restrict__ chunk_box, unsigned long long *__restrict__ chunk_out,
+    uint32_t K, uint32_t tmax) {
+    __shared__ uint32_t s_box[NB_THREADS * NB_SLOTS];
+    __shared__ uint8_t s_slot[NB_THREADS * NB_SLOTS];
+    const uint32_t B = ctr->B;
+    const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t b = tile * NB_THREADS + threadIdx.x;
+        const bool have = b < B;
+        const uint32_t key = have ? bkey[b] : 0u;
+        const uint32_t s0 = have ? bstart[b] : 0u;
+        const uint32_t nb = have ? bstart[b + 1] - s0 : 0u;
+        const bool tgt = have && key >= g.tkey_lo && key <= g.tkey_hi;
+        NbStencil S;
+        make_nb(g, key, S);
+        // pass 1: totals (the same search as k_nbr_count); pass 2 repeats the boxinfo loads (L1 hits) instead of
+        // holding 54 registers of slot results (occupancy)
+        uint32_t cnt = 0, okm = 0;
+        unsigned long long red = 0;
+#pragma unroll
+        for (int dz = 0; dz < 3; ++dz) nb_plane(S, dz, key, tgt, occ, boxinfo, okm, cnt, red);
+        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax);
+        BoxTotals tot;
+        const BoxTotals inc = block_scan_totals(x, &tot);
+        const NbTile to = tile_prefix(tile, tiles, incl, flags);
+        if (threadIdx.x == 0) {  // publish this tile's inclusive prefix
+            NbTile in;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) in.v[k] = to.v[k];
+            in.v[0] += tot.nbr;
+            in.v[1] += tot.red;
+            in.v[2] += tot.item;
+            in.v[3] += tot.small;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) __stcg(&incl[tile].v[k], in.v[k]);
+            st_release_u32(&flags[tile], 1u);
+            if (tile == ntiles - 1) {  // the last tile closes the offsets and publishes the totals
+                nbr_off[B] = (uint32_t)in.v[0];
+                red_off[B] = in.v[1];
+                ctr->n_nbr = (uint32_t)in.v[0];
+                ctr->R = in.v[1];
+                ctr->n_items = (uint32_t)in.v[2];
+                ctr->n_small = (uint32_t)in.v[3];
+            }
+        }
+        const uint32_t e_loc = inc.nbr - x.nbr;  // block-relative CSR offset
+        const uint32_t e0 = (uint32_t)to.v[0] + e_loc;
+        const unsigned long long rb = to.v[1] + inc.red - x.red;
+        const uint32_t it = (uint32_t)to.v[2] + inc.item - x.item;
+        const uint32_t so = (uint32_t)to.v[3] + inc.small - x.small;
+        if (have) {
+            nbr_off[b] = e0;
+            red_off[b] = rb;
+        }
+        // pass 2: CSR entries (staged), chunk heads; records before the centre slot = offset of the box's own
+        // segment inside its run
+        uint32_t e = e0, el = e_loc, recs = 0, cen = 0;
+#pragma unroll
+        for (int dz = 0; dz < 3; ++dz) {
+            uint2 inf[9];
+#pragma unroll
+            for (int j = 0; j < 9; ++j) {
+                const int sl = 9 * dz + j;
+                inf[j] = boxinfo[((okm >> sl) & 1u) ? (S.c[0][j % 3] | S.c[1][j / 3] | S.c[2][dz]) : key];
+            }
+#pragma unroll
+            for (int j = 0; j < 9; ++j) {
+                const int sl = 9 * dz + j;
+                if (sl == 13) cen = recs;
+                if ((okm >> sl) & 1u) {
+                    s_box[el] = inf[j].x;
+                    s_slot[el] = (uint8_t)sl;
+                    if ((e & 31u) == 0u) {  // head of a restructure chunk
+                        chunk_box[e >> 5] = b;
+                        chunk_out[e >> 5] = rb + recs;
+                    }
+                    ++e;
+                    ++el;
+                    recs += inf[j].y;
+                }
+            }
+        }
+        if (tgt) {
+            if (x.item == 0) {  // small box: thread-per-target path, one entry per target pair
+                for (uint32_t j = 0; j < x.small; ++j) {
+                    small_tgt[so + j] = s0 + 2 * j;
+                    small_box[so + j] = b;
+                }
+            } else {
+                const uint32_t nch = x.item;
+                for (uint32_t ci = 0; ci < nch; ++ci) {
+                    const uint32_t a0 = (uint32_t)(((uint64_t)nb * ci) / nch);
+                    const uint32_t z0 = (uint32_t)(((uint64_t)nb * (ci + 1)) / nch);
+                    // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
+                    const uint32_t nt = z0 - a0, Gq = (nt + K - 1) / K, Sq = 32u / Gq;
+                    items[it + ci] = Item{b, s0 + a0, nt | (Sq << 8) | (Gq << 16), key, rb, (uint32_t)red, cen + a0};
+                }
+            }
+        }
+        __syncthreads();
+        // coalesced copy of the tile's CSR run
+        const uint32_t base = (uint32_t)to.v[0];
+        for (uint32_t j = threadIdx.x; j < tot.nbr; j += NB_THREADS) {
+            nbr_box[base + j] = s_box[j];
+            nbr_slot[base + j] = s_slot[j];
+        }
+        __syncthreads();
+    }
 }
 
 __global__ void k_helm_check(const uint32_t *__restrict__ skey, uint32_t n, DevCounters *ctr) {
@@ -475,13 +535,13 @@ static unsigned grid_for(uint64_t n, int threads, int num_sms) {
 void free_capacity(p2p_plan *P) {
     cudaStream_t st = P->stream;
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
-                    P->s_nb_status, P->boxinfo,
+                    P->s_nb_tiles, P->boxinfo,
                     P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, P->rec, P->bkey, P->bstart,
                     P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
-    P->s_nb_status = nullptr;
+    P->s_nb_tiles = nullptr;
     P->boxinfo = nullptr;
     P->small_tgt = P->small_box = P->chunk_box = nullptr;
     P->chunk_out = nullptr;
@@ -521,7 +581,7 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, (size_t)nslot * bcap, st));
     if (grav) {
         P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
-        P2P_CUDA_TRY(dalloc((void **)&P->s_nb_status, sizeof(NbTileStatus) * div_up(bcap, NBB_TILE), st));
+        P2P_CUDA_TRY(dalloc(&P->s_nb_tiles, (2 * sizeof(NbTile) + 4) * div_up(bcap, NB_THREADS), st));
         P2P_CUDA_TRY(dalloc((void **)&P->boxinfo, sizeof(uint2) * keyspace, st));
         P2P_CUDA_TRY(dalloc((void **)&P->small_tgt, 4 * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->small_box, 4 * n, st));
@@ -573,15 +633,24 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
                                        &P->ctr->B, P->s_partials, st));
     // a5
     const uint64_t bcap = (uint64_t)P->bcap;
-    const uint64_t ntile_cap = div_up(bcap, NBB_TILE);
     P2P_LAUNCH(k_boxinfo, std::max<unsigned>(1, std::min<unsigned>(div_up(bcap, 256), (unsigned)P->num_sms * 8)), 256,
                0, st, P->bkey, P->bstart, P->ctr, P->boxinfo);
-    P2P_CUDA_TRY(cudaMemsetAsync(P->s_nb_status, 0, sizeof(NbTileStatus) * ntile_cap, st));
-    P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->nbr_tile, 0, sizeof(unsigned int), st));
-    P2P_LAUNCH(k_nbr_build, std::max<unsigned>(1, std::min<unsigned>(div_up(ntile_cap, NBB_WARPS), (unsigned)P->num_sms * 8)),
-               NBB_WARPS * 32, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, P->s_nb_status,
-               P->nbr_off, (unsigned long long *)P->red_off, P->nbr_box, P->nbr_slot, P->items, P->small_tgt,
-               P->small_box, P->chunk_box, P->chunk_out, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32),
+    const unsigned nbg = std::max<unsigned>(1, std::min<unsigned>(div_up(bcap, NB_THREADS), (unsigned)P->num_sms * 8));
+    const uint64_t ntile_cap = div_up(bcap, NB_THREADS);
+    NbTile *tiles = (NbTile *)P->s_nb_tiles;            // [ntile_cap] sums, then [ntile_cap] inclusive prefixes
+    NbTile *incl = tiles + ntile_cap;
+    unsigned int *flags = (unsigned int *)(incl + ntile_cap);
+    P2P_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * ntile_cap, st));
+    P2P_LAUNCH(k_nbr_count, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, tiles,
+               (uint32_t)ITEM_TMAX);
+    static bool carveout_set = false;  // the fill keeps a large L1 (its pass-2 reloads must hit)
+    if (!carveout_set && P2P_NB_CARVEOUT > 0) {
+        P2P_CUDA_TRY(cudaFuncSetAttribute(k_nbr_fill, cudaFuncAttributePreferredSharedMemoryCarveout, P2P_NB_CARVEOUT));
+        carveout_set = true;
+    }
+    P2P_LAUNCH(k_nbr_fill, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, tiles,
+               incl, flags, P->nbr_off, (unsigned long long *)P->red_off, P->nbr_box, P->nbr_slot, P->items,
+               P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32),
                (uint32_t)ITEM_TMAX);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;

@@ -24,15 +24,8 @@ struct DevCounters {
     unsigned int sort_tile_ctr[4]; // onesweep tile counters, one per pass
     unsigned int n_small;          // targets of small boxes (thread-per-target path of the eval)
     unsigned int small_head;       // eval small-target queue head (reset before every eval)
-    unsigned int nbr_tile;         // k_nbr_build look-back tile counter (reset before every build)
 };
 
-// k_nbr_build decoupled look-back status of one 32-box tile: three self-describing 64-bit words (no fences
-// needed: each is stored and loaded whole), word = flag << 62 | value, flag 1 = tile aggregate, 2 = inclusive
-// prefix.  Values: [0] CSR entries, [1] redundant records, [2] work items | small target pairs << 31.
-struct NbTileStatus {
-    unsigned long long w[3];
-};
 // eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
 // meta = n_t | S << 8 | G << 16: the warp lane layout (G groups of K targets x S source splits, G*S <= 32)
 // key / red_base / R duplicate the box's Morton key and redundant run so the eval's one-item-ahead prefetch is a
@@ -101,7 +94,7 @@ struct p2p_plan {
     uint32_t *s_key = nullptr, *s_idx = nullptr, *s_kalt = nullptr, *s_valt = nullptr;
     uint32_t *s_hist = nullptr, *s_status = nullptr;
     void *s_partials = nullptr;
-    p2p::NbTileStatus *s_nb_status = nullptr;  // [ceil(B / 32)] k_nbr_build look-back words
+    void *s_nb_tiles = nullptr;  // [ceil(B / 256)] k_nbr_count tile sums -> k_nbr_scan offsets
     uint2 *boxinfo = nullptr;     // gravity: dense Morton key -> {box, n_b} (valid where occ has the bit set)
     uint32_t *small_tgt = nullptr, *small_box = nullptr;  // sorted target index / its box, small boxes only
     // restructure chunks: every 32 consecutive CSR entries e = 32 c .. 32 c + 31 form one chunk; their redundant
