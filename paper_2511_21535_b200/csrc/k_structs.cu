@@ -29,17 +29,21 @@ __device__ __forceinline__ uint32_t item_chunks(uint32_t nb_b, uint64_t nsrc, ui
 }
 
 // ------------------------------------------------------------------------------------------------ a1
-// positions at pos[i * ps + d] (ps = 3: the caller's [N][3] array; ps = 4: {x,y,z,m} records)
-template <typename T>
+// positions at pos[i * ps + d] (ps = 3: the caller's [N][3] array; ps = 4: {x,y,z,m} records).  With `aos` the
+// caller's SoA input is also packed into {x,y,z,m} records in input order (read sequentially here), so that the a3
+// gather touches ONE 16-byte record per particle instead of a position and a mass in two arrays (two DRAM bursts)
+template <typename T, typename V4>
 __global__ void k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geom g, uint32_t *__restrict__ key,
-                              uint32_t *__restrict__ idx, DevCounters *ctr) {
+                              uint32_t *__restrict__ idx, DevCounters *ctr, const T *__restrict__ q,
+                              V4 *__restrict__ aos) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         uint32_t c[3];
+        T xd[3];
         bool bad = false;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            double x = (double)pos[(size_t)ps * i + d];
-            double f = floor(__ddiv_rn(__dsub_rn(x, g.lo[d]), g.h));
+            xd[d] = pos[(size_t)ps * i + d];
+            double f = floor(__ddiv_rn(__dsub_rn((double)xd[d], g.lo[d]), g.h));
             if (!(f >= 0.0 && f < (double)g.nbox[d])) {
                 bad = true;
                 f = 0.0;
@@ -49,6 +53,14 @@ __global__ void k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geo
         if (bad) atomicMin(&ctr->err_index, (unsigned long long)i);
         key[i] = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
         idx[i] = i;
+        if (aos) {
+            V4 r;
+            r.x = xd[0];
+            r.y = xd[1];
+            r.z = xd[2];
+            r.w = q[i];
+            aos[i] = r;
+        }
     }
 }
 
@@ -85,11 +97,11 @@ __global__ void k_bin_helmholtz(const T *__restrict__ pos, uint32_t n, Geom g, i
 }
 
 // ------------------------------------------------------------------------------------------------ a3
-// random gather (input order is arbitrary): 4 particles per thread iteration, all loads issued before the
-// stores (memory-level parallelism for the latency-bound gather)
-template <typename T, typename V4>
-__global__ void k_permute_gravity(const T *__restrict__ pos, int ps, const T *__restrict__ q, int qs,
-                                  const uint32_t *__restrict__ perm, uint32_t n, V4 *__restrict__ rec) {
+// random gather (input order is arbitrary) of {x,y,z,m} records: one 16 B (fp64: 32 B) load per particle,
+// 4 particles per thread iteration, all loads issued before the stores (memory-level parallelism)
+template <typename V4>
+__global__ void k_permute_gravity(const V4 *__restrict__ src, const uint32_t *__restrict__ perm, uint32_t n,
+                                  V4 *__restrict__ rec) {
     constexpr int U = 4;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += U * stride) {
@@ -98,14 +110,8 @@ __global__ void k_permute_gravity(const T *__restrict__ pos, int ps, const T *__
         for (int u = 0; u < U; ++u) i[u] = p0 + u * stride < n ? perm[p0 + u * stride] : 0u;
         V4 r[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (p0 + u * stride < n) {
-                r[u].x = pos[(size_t)ps * i[u] + 0];
-                r[u].y = pos[(size_t)ps * i[u] + 1];
-                r[u].z = pos[(size_t)ps * i[u] + 2];
-                r[u].w = q[(size_t)qs * i[u]];
-            }
-        }
+        for (int u = 0; u < U; ++u)
+            if (p0 + u * stride < n) r[u] = src[i[u]];
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (p0 + u * stride < n) rec[p0 + u * stride] = r[u];
@@ -535,13 +541,14 @@ static unsigned grid_for(uint64_t n, int threads, int num_sms) {
 void free_capacity(p2p_plan *P) {
     cudaStream_t st = P->stream;
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
-                    P->s_nb_tiles, P->boxinfo,
+                    P->s_nb_tiles, P->s_aos, P->boxinfo,
                     P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, P->rec, P->bkey, P->bstart,
                     P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
     P->s_nb_tiles = nullptr;
+    P->s_aos = nullptr;
     P->boxinfo = nullptr;
     P->small_tgt = P->small_box = P->chunk_box = nullptr;
     P->chunk_out = nullptr;
@@ -581,6 +588,7 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     P2P_CUDA_TRY(dalloc((void **)&P->nbr_slot, (size_t)nslot * bcap, st));
     if (grav) {
         P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
+        P2P_CUDA_TRY(dalloc(&P->s_aos, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
         P2P_CUDA_TRY(dalloc(&P->s_nb_tiles, (2 * sizeof(NbTile) + 4) * div_up(bcap, NB_THREADS), st));
         P2P_CUDA_TRY(dalloc((void **)&P->boxinfo, sizeof(uint2) * keyspace, st));
         P2P_CUDA_TRY(dalloc((void **)&P->small_tgt, 4 * n, st));
@@ -608,23 +616,22 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
         pos = rec_in;
         q = (const char *)rec_in + 3 * tsz;
     }
-    // a1
+    // a1 (+ the SoA input packed into records, unless the input already is records)
+    void *aos = rec_in ? const_cast<void *>(rec_in) : P->s_aos;
     if (f64)
-        P2P_LAUNCH(k_bin_gravity<double>, gb, 256, 0, st, (const double *)pos, ps, n, P->geom, P->s_key, P->s_idx,
-                   P->ctr);
+        P2P_LAUNCH((k_bin_gravity<double, double4>), gb, 256, 0, st, (const double *)pos, ps, n, P->geom, P->s_key,
+                   P->s_idx, P->ctr, (const double *)q, rec_in ? (double4 *)nullptr : (double4 *)aos);
     else
-        P2P_LAUNCH(k_bin_gravity<float>, gb, 256, 0, st, (const float *)pos, ps, n, P->geom, P->s_key, P->s_idx,
-                   P->ctr);
+        P2P_LAUNCH((k_bin_gravity<float, float4>), gb, 256, 0, st, (const float *)pos, ps, n, P->geom, P->s_key,
+                   P->s_idx, P->ctr, (const float *)q, rec_in ? (float4 *)nullptr : (float4 *)aos);
     // a2
     P2P_CUDA_TRY(radix_sort_pairs(P->s_key, P->s_idx, P->s_kalt, P->s_valt, n, P->passes, P->ctr, P->s_hist,
                                   P->s_status, st, &P->skey, &P->perm));
     // a3
     if (f64)
-        P2P_LAUNCH((k_permute_gravity<double, double4>), gb, 256, 0, st, (const double *)pos, ps, (const double *)q,
-                   qs, P->perm, n, (double4 *)P->rec);
+        P2P_LAUNCH((k_permute_gravity<double4>), gb, 256, 0, st, (const double4 *)aos, P->perm, n, (double4 *)P->rec);
     else
-        P2P_LAUNCH((k_permute_gravity<float, float4>), gb, 256, 0, st, (const float *)pos, ps, (const float *)q, qs,
-                   P->perm, n, (float4 *)P->rec);
+        P2P_LAUNCH((k_permute_gravity<float4>), gb, 256, 0, st, (const float4 *)aos, P->perm, n, (float4 *)P->rec);
     // a4
     const uint64_t occ_words = std::max<uint64_t>(1, (1ull << P->key_bits) / 32);
     P2P_CUDA_TRY(cudaMemsetAsync(P->occ, 0, 4 * occ_words, st));

@@ -1,0 +1,123 @@
+"""the paper's locality model (§3.4, Eq 9-11) evaluated on B200 data.
+
+For each workload: the dispersion D (contiguous memory runs a work item = target box reads) and the volume V of
+the two layouts, the cache regime V <= C vs V > C (C = the 126 MB L2; and the per-SM shared memory a run is staged
+through), the model's predicted locality factor X_Locality (Eq 10: D' V' if V <= C; Eq 11: V'/D' if V > C, with
+D', V' = indexed / redundant), and the MEASURED kernel-only speedup t(INDEXED) / t(REDUNDANT) of the two eval
+kernels (CUDA events, L2 flushed before every launch, median of 7).  Then Pearson and Spearman correlations of
+predicted vs measured across the workloads, as the paper does for its own trend ("correlation ~94%",
+P:L433 "~92%").  A second predictor is reported beside it: the records streamed per pair (R / I), i.e. the memory
+traffic the redundant layout adds per unit of FP32 work -- what actually sets the trend on B200.
+
+Structures come from the product's copy-out (the oracle is test infrastructure and is not used here).
+usage: python scripts/locality_model.py [workloads...]  -> JSON lines on stdout"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import p2p_inputs as G  # noqa: E402
+import paper_2511_21535_b200 as P  # noqa: E402
+
+L2_BYTES = 126 * 2**20
+SMEM_BYTES = 228 * 1024
+WORKLOADS = sys.argv[1:] or ["c4-8", "c4-16", "c4-32", "c4-64", "c4-128", "c3", "c3dense", "c5w"]
+
+
+def make(name):
+    if name == "c5w":
+        return G.plummer_tiles(12_500_000, 256, 1, 0)
+    return G.config(name)
+
+
+def timed(fn, flush, reps=7):
+    ts = []
+    for _ in range(reps):
+        flush.add_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def rankdata(x):
+    order = np.argsort(x, kind="stable")
+    r = np.empty(len(x))
+    r[order] = np.arange(len(x))
+    return r
+
+
+def main():
+    flush = torch.empty(512 * 2**20 // 4, device="cuda")
+    rows = []
+    for name in WORKLOADS:
+        inp = make(name)
+        pos = torch.from_numpy(inp.pos).cuda()
+        m = torch.from_numpy(inp.mass).cuda()
+        phi = torch.empty(inp.n, device="cuda")
+        field = torch.empty((inp.n, 3), device="cuda")
+        with P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps) as plan:
+            plan.restructure()
+            info = plan.info
+            nbr_off = plan.copy_out(P.P2P_ARR_NBR_OFF).astype(np.int64)
+            nbr_box = plan.copy_out(P.P2P_ARR_NBR_BOX).astype(np.int64)
+            bstart = plan.copy_out(P.P2P_ARR_BOX_START).astype(np.int64)
+            plan.eval(P.P2P_REDUNDANT, phi, field)
+            plan.eval(P.P2P_INDEXED, phi, field)
+            t_red = timed(lambda: plan.eval(P.P2P_REDUNDANT, phi, field), flush)
+            t_idx = timed(lambda: plan.eval(P.P2P_INDEXED, phi, field), flush)
+        B = len(bstart) - 1
+        n_b = np.diff(bstart)
+        E = len(nbr_box)
+        # indexed dispersion: maximal runs of consecutive source boxes (records of box k and k+1 are adjacent)
+        owner = np.repeat(np.arange(B), np.diff(nbr_off))
+        new_run = np.ones(E, bool)
+        same_owner = owner[1:] == owner[:-1]
+        new_run[1:] = ~(same_owner & (nbr_box[1:] == nbr_box[:-1] + 1))
+        runs = np.bincount(owner[new_run], minlength=B)
+        R_b = np.bincount(owner, weights=n_b[nbr_box], minlength=B).astype(np.int64)
+        pairs_b = n_b * R_b
+        w = pairs_b / max(pairs_b.sum(), 1)
+        D_idx = float((runs * w).sum())           # pair-weighted mean runs per work item
+        D_red = 1.0                                # one contiguous run per target box
+        rec = 16
+        V_red = rec * int(info.n_red)              # the redundant buffer streamed by the REDUNDANT eval
+        V_idx = rec * int(info.n_local)            # the (unique) sorted records the INDEXED eval reads
+        Dp, Vp = D_idx / D_red, V_idx / V_red
+        # per work item: the run one target box stages (fits the 228 KB shared memory either way)
+        V_item = rec * float((R_b * w).sum())
+        fits = V_red <= L2_BYTES
+        x_loc = Dp * Vp if fits else Vp / Dp       # Eq 10 / Eq 11
+        row = {"workload": name, "N": int(info.n_local), "boxes": int(B), "pairs": int(info.n_pairs),
+               "R": int(info.n_red), "D_indexed_runs_per_item": D_idx, "D_redundant": D_red,
+               "V_redundant_bytes": V_red, "V_indexed_bytes": V_idx, "V_item_bytes": V_item,
+               "regime": "V<=C" if fits else "V>C", "C_bytes": L2_BYTES, "D_ratio": Dp, "V_ratio": Vp,
+               "X_locality_pred": x_loc, "records_per_pair": int(info.n_red) / max(int(info.n_pairs), 1),
+               "t_redundant_ms": t_red, "t_indexed_ms": t_idx, "X_measured": t_idx / t_red}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+        del pos, m, phi, field
+        torch.cuda.empty_cache()
+    xm = np.array([r["X_measured"] for r in rows])
+    out = {"summary": True, "n": len(rows)}
+    for key in ["X_locality_pred", "records_per_pair", "D_indexed_runs_per_item"]:
+        xp = np.array([r[key] for r in rows])
+        if len(rows) >= 3 and np.std(xp) > 0:
+            out[f"pearson_{key}"] = float(np.corrcoef(xp, xm)[0, 1])
+            out[f"spearman_{key}"] = float(np.corrcoef(rankdata(xp), rankdata(xm))[0, 1])
+        else:
+            out[f"pearson_{key}"] = None
+            out[f"spearman_{key}"] = None
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
