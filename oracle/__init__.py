@@ -59,6 +59,8 @@ def lib():
                 "orc_gravity_eval_indexed": (None, [i64, p, p, dbl, p, u32, p, p, p, p, p, p, dbl, p, p]),
                 "orc_gravity_eval_indexed_boxes": (None, [i64, p, p, p, dbl, p, u32, p, p, p, p, p, p, dbl, p, p]),
                 "orc_gravity_brute": (i64, [i64, p, p, dbl, p, p, u32, dbl, p, p]),
+                "orc_gravity_pairrec": (None, [i32, i64, p, p, dbl, p, p, u32, p, p, p, p, p, p, p, p]),
+                "orc_gravity_eval_pairrec": (None, [i32, i64, p, p, p, p, p, p, p, dbl, p, p, p]),
                 "orc_helm_weight": (None, [dbl, dbl, dbl, p, p]),
                 "orc_helm_table": (None, [i32, dbl, dbl, p]),
                 "orc_helm_structs": (i64, [i64, p, dbl, p, p, i32, p, p, p, p, p, p, p]),
@@ -201,6 +203,44 @@ class GravityPlan:
                                        _p(phi), _p(field))
         return phi, field
 
+
+    def build_pairrec(self, records: bool = True):
+        """SURVEY NEXT-4: the paper's thread-level pair records (P:L338), one per CSR entry: [targets of b ;
+        sources of k], rebased like red (C11).  Returns (pr_off[E+1], pr[P][4]) -- pr None if not records."""
+        off = np.zeros(self.n_nbr + 1, np.uint64)
+        L = lib()
+        L.orc_gravity_pairrec(self.prec, self.B, _p(self.pos), _p(self.mass), float(self.inp.h), _p(self.lo),
+                              _p(self.nbox), int(self.inp.periodic), _p(self.perm), _p(self.bkey), _p(self.bstart),
+                              _p(self.nbr_off), _p(self.nbr_box), _p(self.nbr_slot), _p(off), None)
+        pr = None
+        if records:
+            dt = np.float32 if self.prec == 0 else np.float64
+            pr = np.zeros((max(int(off[-1]), 1), 4), dt)
+            L.orc_gravity_pairrec(self.prec, self.B, _p(self.pos), _p(self.mass), float(self.inp.h), _p(self.lo),
+                                  _p(self.nbox), int(self.inp.periodic), _p(self.perm), _p(self.bkey),
+                                  _p(self.bstart), _p(self.nbr_off), _p(self.nbr_box), _p(self.nbr_slot), _p(off),
+                                  _p(pr))
+            pr = pr[:int(off[-1])]
+        self.pr_off, self.pr = off, pr
+        return off, pr
+
+    def eval_pairrec(self):
+        """per-(record, target) partials from the record bytes alone, then the deterministic update (ascending
+        record order per target).  Returns (phi, field, partial[T][4])."""
+        if getattr(self, "pr", None) is None:
+            self.build_pairrec()
+        n = self.pos.shape[0]
+        nb = np.diff(self.bstart.astype(np.int64))
+        T = int((np.diff(self.nbr_off.astype(np.int64)) * nb).sum())
+        partial = np.zeros((max(T, 1), 4))
+        phi = np.zeros(n)
+        field = np.zeros((n, 3))
+        pr = self.pr if self.pr.shape[0] > 0 else np.zeros((1, 4), self.pr.dtype)
+        lib().orc_gravity_eval_pairrec(self.prec, self.B, _p(self.perm), _p(self.bstart), _p(self.nbr_off),
+                                       _p(self.nbr_box), _p(self.nbr_slot), _p(self.pr_off),
+                                       _p(np.ascontiguousarray(pr)), float(self.inp.eps), _p(partial), _p(phi),
+                                       _p(field))
+        return phi, field, partial[:T]
 
     def eval_indexed_boxes(self, boxes):
         """plain definition (mode ii) for the targets of the listed boxes only; returns (phi, field) arrays of

@@ -397,6 +397,135 @@ void orc_gravity_eval_indexed_boxes(int64_t nsel, const uint32_t *sel, const dou
 }
 
 /* --------------------------------------------------------------------------------------------- */
+/* the paper's THREAD-level redundancy ("duplicating particle data for each     */
+/* interaction pair ... an Array-of-Structures (AoS) format, where each entry contains both source   */
+/* and target attributes"; S:L113-116 RedundantBuffers; partial results + reduction "through the     */
+/* update process").                                                             */
+/* One pair record per CSR entry e = (target box b, neighbour k, slot s), in CSR order:              */
+/*   [ the n_b targets of b : fl_p(((double)x_i + 0) - o_b), m_i ]  [ the n_k sources of k, rebased  */
+/*   exactly as in red (C11) ]                                                                      */
+/* pr_off[e] = first record of entry e (running count of n_b + n_k); the E+1'th value = total.       */
+/* --------------------------------------------------------------------------------------------- */
+static void put_rec(int prec, void *buf, uint64_t r, const double *v)
+{
+    if (prec == 0) {
+        float *f = (float *)buf + 4 * r;
+        for (int q = 0; q < 4; ++q) f[q] = (float)v[q];
+    } else {
+        double *g = (double *)buf + 4 * r;
+        for (int q = 0; q < 4; ++q) g[q] = v[q];
+    }
+}
+
+static void get_rec(int prec, const void *buf, uint64_t r, double *v)
+{
+    if (prec == 0)
+        for (int q = 0; q < 4; ++q) v[q] = (double)((const float *)buf)[4 * r + q];
+    else
+        for (int q = 0; q < 4; ++q) v[q] = ((const double *)buf)[4 * r + q];
+}
+
+/* offsets only (pr == NULL) or offsets + records */
+void orc_gravity_pairrec(int prec, int64_t B, const double *pos, const double *mass, double h, const double *lo,
+                         const int32_t *nbox, uint32_t periodic, const uint32_t *perm, const uint32_t *bkey,
+                         const uint32_t *bstart, const uint32_t *nbr_off, const uint32_t *nbr_box,
+                         const uint8_t *nbr_slot, uint64_t *pr_off, void *pr)
+{
+    int nb = orc_bits_per_dim(3, nbox);
+    uint64_t r = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        int32_t c[3];
+        double o[3];
+        orc_demorton(3, nb, bkey[b], c);
+        box_origin(c, h, lo, o);
+        for (uint32_t e = nbr_off[b]; e < nbr_off[b + 1]; ++e) {
+            pr_off[e] = r;
+            /* the target tuples of b */
+            for (uint32_t p = bstart[b]; p < bstart[b + 1]; ++p, ++r) {
+                if (!pr) continue;
+                uint32_t i = perm[p];
+                double v[4];
+                for (int d = 0; d < 3; ++d) v[d] = (pos[3 * (int64_t)i + d] + 0.0) - o[d];
+                v[3] = mass[i];
+                put_rec(prec, pr, r, v);
+            }
+            /* the source tuples of k, with the slot's periodic image */
+            double S[3];
+            slot_shift(nbr_slot[e], c, nbox, periodic, h, S);
+            uint32_t k = nbr_box[e];
+            for (uint32_t p = bstart[k]; p < bstart[k + 1]; ++p, ++r) {
+                if (!pr) continue;
+                uint32_t j = perm[p];
+                double v[4];
+                for (int d = 0; d < 3; ++d) v[d] = (pos[3 * (int64_t)j + d] + S[d]) - o[d];
+                v[3] = mass[j];
+                put_rec(prec, pr, r, v);
+            }
+        }
+    }
+    pr_off[nbr_off[B]] = r;
+}
+
+/* Eval over pair records: one logical thread per (record, target) computes a partial result from the
+ * record's bytes alone (the self pair -- slot 13, same sorted index -- excluded from phi, C3); then the
+ * update: every target sums its partials in ascending record order (deterministic).
+ * partial[4 * (slot)] = {phi, ax, ay, az}, slot = running count of targets over records (CSR order). */
+void orc_gravity_eval_pairrec(int prec, int64_t B, const uint32_t *perm, const uint32_t *bstart,
+                              const uint32_t *nbr_off, const uint32_t *nbr_box, const uint8_t *nbr_slot,
+                              const uint64_t *pr_off, const void *pr, double eps, double *partial, double *phi,
+                              double *field)
+{
+    double eps2 = eps * eps;
+    /* partial-slot base of every box: sum over earlier boxes of |N(b)| n_b */
+    uint64_t *pbase = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(B + 1));
+    pbase[0] = 0;
+    for (int64_t b = 0; b < B; ++b)
+        pbase[b + 1] = pbase[b] + (uint64_t)(nbr_off[b + 1] - nbr_off[b]) * (bstart[b + 1] - bstart[b]);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t b = 0; b < B; ++b) {
+        uint32_t nbb = bstart[b + 1] - bstart[b];
+        for (uint32_t e = nbr_off[b]; e < nbr_off[b + 1]; ++e) {
+            uint32_t nk = bstart[nbr_box[e] + 1] - bstart[nbr_box[e]];
+            uint64_t rt = pr_off[e], rs = pr_off[e] + nbb;
+            for (uint32_t j = 0; j < nbb; ++j) {
+                double t[4];
+                get_rec(prec, pr, rt + j, t);
+                double ph = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
+                for (uint32_t q = 0; q < nk; ++q) {
+                    double s[4];
+                    get_rec(prec, pr, rs + q, s);
+                    double dx = s[0] - t[0], dy = s[1] - t[1], dz = s[2] - t[2];
+                    double r2 = dx * dx + dy * dy + dz * dz + eps2;
+                    double rinv = 1.0 / sqrt(r2);
+                    double mr3 = s[3] * rinv * rinv * rinv;
+                    if (!(nbr_slot[e] == 13 && q == j)) ph -= s[3] * rinv;
+                    ax += mr3 * dx;
+                    ay += mr3 * dy;
+                    az += mr3 * dz;
+                }
+                double *o = partial + 4 * (pbase[b] + (uint64_t)(e - nbr_off[b]) * nbb + j);
+                o[0] = ph;
+                o[1] = ax;
+                o[2] = ay;
+                o[3] = az;
+            }
+        }
+        /* update: ascending record order per target */
+        for (uint32_t j = 0; j < nbb; ++j) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (uint32_t e = nbr_off[b]; e < nbr_off[b + 1]; ++e) {
+                const double *o = partial + 4 * (pbase[b] + (uint64_t)(e - nbr_off[b]) * nbb + j);
+                for (int q = 0; q < 4; ++q) acc[q] += o[q];
+            }
+            uint32_t i = perm[bstart[b] + j];
+            phi[i] = acc[0];
+            for (int d = 0; d < 3; ++d) field[3 * (int64_t)i + d] = acc[1 + d];
+        }
+    }
+    free(pbase);
+}
+
+/* --------------------------------------------------------------------------------------------- */
 /* Oracle mode (iii): O(N^2) brute force with the box-adjacency predicate, no lists at all.         */
 /* Per dimension: periodic -> (ib_j - ib_i) mod n in {-1,0,1}; open -> |ib_j - ib_i| <= 1.  The      */
 /* image is derived from the wrap: ib_j - ib_i == -(n-1) -> +L, == n-1 -> -L (needs n >= 3).         */
