@@ -79,8 +79,12 @@ typedef enum {
     P2P_INDEXED = 1,        /* non-redundant baseline (§5.2.1 "Particle indices are first loaded,
                                followed by data access"): neighbour segments of the Morton-sorted
                                records, located through the neighbour CSR, staged on the fly */
-    P2P_INDEXED_BITWISE = 2 /* test configuration of INDEXED: stages bit-identical copies of red[]
+    P2P_INDEXED_BITWISE = 2,/* test configuration of INDEXED: stages bit-identical copies of red[]
                                records, so its outputs equal P2P_REDUNDANT bit for bit */
+    P2P_PAIRREC = 3         /* SURVEY NEXT-4, the paper's THREAD-level redundancy (§5.2.1): one AoS
+                               pair record [targets of b ; sources of k] per neighbour pair (b, k), one
+                               partial result per (record, target), then the update sums them in record
+                               order (§1.1).  Gravity, single-GPU plans; needs p2p_restructure_pairs */
 } p2p_layout;
 
 typedef struct {
@@ -139,10 +143,21 @@ p2p_status p2p_eval_host(p2p_plan *plan, p2p_layout layout, void *potential_host
  * C11; helmholtz: Xg[B][9][t], zero segments for missing neighbours, C10).  Enqueue only. */
 p2p_status p2p_restructure(p2p_plan *plan);
 
+/* build the pair-record buffer of P2P_PAIRREC ("duplicating particle data for each
+ * interaction pair ... each entry contains both source and target attributes").  Record of CSR entry e =
+ * (b, k, slot): b's n_b target tuples rebased to o_b, then k's n_k source tuples rebased like red (C11) -- bit for
+ * bit b's own segment of red followed by e's segment.  Records in CSR order; 16 (T + R) bytes (fp64: 32), T =
+ * sum_b |N(b)| n_b (= R by neighbour symmetry), plus 16 T bytes of partial results.  Gravity, single-GPU plans
+ * (else P2P_ERR_UNSUPPORTED); synchronises the stream once (sizes).  Invalidated by update / set_charges. */
+p2p_status p2p_restructure_pairs(p2p_plan *plan);
+/* records (T + R) and partial-result slots (T) of the current pair-record buffer (BAD_STATE if not built) */
+p2p_status p2p_get_pairrec_size(const p2p_plan *plan, int64_t *records, int64_t *partials);
+
 /* a7/a8 + a9: evaluate every target and scatter to input order.
  *   potential : device, gravity [n_local] real; helmholtz [n_local] complex (re, im)
  *   field     : device, gravity [n_local][3] real (the acceleration, C1) or NULL; helmholtz: must be NULL
- * P2P_REDUNDANT requires a preceding p2p_restructure (else P2P_ERR_BAD_STATE).  Enqueue only. */
+ * P2P_REDUNDANT requires a preceding p2p_restructure, P2P_PAIRREC a preceding p2p_restructure_pairs (else
+ * P2P_ERR_BAD_STATE).  Enqueue only. */
 p2p_status p2p_eval(p2p_plan *plan, p2p_layout layout, void *potential, void *field);
 
 /* Replace the charges, keeping the geometry (DBIM reuses its geometry across iterations).
@@ -163,7 +178,8 @@ typedef enum {
     P2P_ARR_NBR_BOX = 5,     /* u32 [n_nbr]     neighbour box index (helmholtz: 0xffffffff = missing) */
     P2P_ARR_NBR_SLOT = 6,    /* u8  [n_nbr]     stencil slot 0..26 (2D 0..8), ascending per box */
     P2P_ARR_RED_OFF = 7,     /* u64 [n_boxes+1] first record of each box's redundant run */
-    P2P_ARR_RED = 8          /* gravity: [n_red][4] float/double; helmholtz: [n_boxes][9][t] complex */
+    P2P_ARR_RED = 8,         /* gravity: [n_red][4] float/double; helmholtz: [n_boxes][9][t] complex */
+    P2P_ARR_PAIRREC = 9      /* gravity pair records [T + R][4] float/double (p2p_restructure_pairs) */
 } p2p_array;
 
 typedef struct {

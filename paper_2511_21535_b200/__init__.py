@@ -25,13 +25,15 @@ P2P_OK, P2P_ERR_INVALID_ARGUMENT, P2P_ERR_OUT_OF_DOMAIN, P2P_ERR_OUT_OF_MEMORY, 
     P2P_ERR_BAD_STATE, P2P_ERR_UNSUPPORTED = range(8)
 P2P_GRAVITY, P2P_HELMHOLTZ2D = 0, 1
 P2P_FP32, P2P_FP64 = 0, 1
-P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE = 0, 1, 2
+P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE, P2P_PAIRREC = 0, 1, 2, 3
 (P2P_ARR_PERM, P2P_ARR_SORTED_KEYS, P2P_ARR_BOX_KEYS, P2P_ARR_BOX_START, P2P_ARR_NBR_OFF, P2P_ARR_NBR_BOX,
- P2P_ARR_NBR_SLOT, P2P_ARR_RED_OFF, P2P_ARR_RED) = range(9)
+ P2P_ARR_NBR_SLOT, P2P_ARR_RED_OFF, P2P_ARR_RED, P2P_ARR_PAIRREC) = range(10)
 
+# the layouts one p2p_restructure serves (P2P_PAIRREC needs p2p_restructure_pairs)
 LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise": P2P_INDEXED_BITWISE}
 
-EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure", "p2p_eval",
+EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure",
+            "p2p_restructure_pairs", "p2p_get_pairrec_size", "p2p_eval",
             "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
             "p2p_partition_splitters", "p2p_get_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
@@ -76,6 +78,8 @@ def lib() -> C.CDLL:
             "p2p_plan_update_host": (C.c_int, [p, i64, p, p]),
             "p2p_eval_host": (C.c_int, [p, C.c_int, p, p]),
             "p2p_restructure": (C.c_int, [p]),
+            "p2p_restructure_pairs": (C.c_int, [p]),
+            "p2p_get_pairrec_size": (C.c_int, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "p2p_eval": (C.c_int, [p, C.c_int, p, p]),
             "p2p_set_charges": (C.c_int, [p, p]),
             "p2p_destroy": (None, [p]),
@@ -152,6 +156,16 @@ def p2p_eval_host(plan: int, layout: int, potential_host: int, field_host: int |
 
 def p2p_restructure(plan: int):
     _check(lib().p2p_restructure(C.c_void_p(plan)))
+
+
+def p2p_restructure_pairs(plan: int):
+    _check(lib().p2p_restructure_pairs(C.c_void_p(plan)))
+
+
+def p2p_get_pairrec_size(plan: int) -> tuple:
+    r, t = C.c_int64(), C.c_int64()
+    _check(lib().p2p_get_pairrec_size(C.c_void_p(plan), C.byref(r), C.byref(t)))
+    return int(r.value), int(t.value)
 
 
 def p2p_eval(plan: int, layout: int, potential: int, field: int | None):
@@ -337,6 +351,10 @@ class Plan:
     def restructure(self):
         p2p_restructure(self.handle)
 
+    def restructure_pairs(self):
+        """the thread-level pair records of P2P_PAIRREC"""
+        p2p_restructure_pairs(self.handle)
+
     def set_charges(self, charges):
         p2p_set_charges(self.handle, charges.contiguous().data_ptr())
 
@@ -375,6 +393,9 @@ class Plan:
                 a = np.empty((i.n_red, 4), np.float64 if f64 else np.float32)
             else:
                 a = np.empty(i.n_red, np.complex128 if f64 else np.complex64)
+        elif which == P2P_ARR_PAIRREC:
+            nrec, _ = p2p_get_pairrec_size(self.handle)
+            a = np.empty((nrec, 4), np.float64 if f64 else np.float32)
         else:
             raise ValueError(which)
         if i.n_local == 0:

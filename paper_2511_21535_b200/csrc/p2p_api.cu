@@ -97,6 +97,7 @@ static void free_plan_buffers(p2p_plan *P) {
     cudaStream_t st = P->stream;
     free_capacity(P);
     free_distributed(P);
+    free_pairrec(P);
     void *bufs[] = {P->red, P->table, P->tc_table, P->ctr, P->stage_in, P->stage_out};
     for (void *b : bufs) dfree(b, st);
     P->red = P->table = P->tc_table = P->stage_in = P->stage_out = nullptr;
@@ -334,6 +335,7 @@ p2p_status p2p_plan_update(p2p_plan *P, int64_t n_local, const void *positions, 
         P->n_in = n_local;
         P->sizes_known = false;
         P->red_valid = false;
+        P->pr_valid = false;
         cudaMemsetAsync(P->ctr, 0, sizeof(DevCounters), st);
         cudaMemsetAsync(&P->ctr->err_index, 0xff, sizeof(unsigned long long), st);
         p2p_status bs = build_distributed(P, positions, charges);
@@ -379,6 +381,7 @@ p2p_status p2p_plan_update(p2p_plan *P, int64_t n_local, const void *positions, 
     P->n = n_local;
     P->sizes_known = false;
     P->red_valid = false;
+    P->pr_valid = false;
     cudaMemsetAsync(P->ctr, 0, sizeof(DevCounters), st);
     cudaMemsetAsync(&P->ctr->err_index, 0xff, sizeof(unsigned long long), st);
     if (n_local == 0) {
@@ -460,11 +463,39 @@ p2p_status p2p_restructure(p2p_plan *P) {
     return mark(P, s);
 }
 
+p2p_status p2p_restructure_pairs(p2p_plan *P) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (P->cfg.kernel != P2P_GRAVITY || P->comm)
+        return fail(P2P_ERR_UNSUPPORTED, "pair records are for single-GPU gravity plans");
+    s = resolve_sizes(P);
+    if (s != P2P_OK) return s;
+    return mark(P, restructure_pairs(P));
+}
+
+p2p_status p2p_get_pairrec_size(const p2p_plan *P, int64_t *records, int64_t *partials) {
+    if (!P || !records || !partials) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!P->pr_valid) return fail(P2P_ERR_BAD_STATE, "pair records are not built (call p2p_restructure_pairs)");
+    *records = P->pr_records;
+    *partials = P->pr_targets;
+    return P2P_OK;
+}
+
 p2p_status p2p_eval(p2p_plan *P, p2p_layout layout, void *potential, void *field) {
     p2p_status s = enter(P);
     if (s != P2P_OK) return s;
-    if (layout != P2P_REDUNDANT && layout != P2P_INDEXED && layout != P2P_INDEXED_BITWISE)
+    if (layout != P2P_REDUNDANT && layout != P2P_INDEXED && layout != P2P_INDEXED_BITWISE && layout != P2P_PAIRREC)
         return fail(P2P_ERR_INVALID_ARGUMENT, "unknown layout");
+    if (layout == P2P_PAIRREC) {
+        if (P->cfg.kernel != P2P_GRAVITY || P->comm)
+            return fail(P2P_ERR_UNSUPPORTED, "P2P_PAIRREC is for single-GPU gravity plans");
+        if (!P->pr_valid)
+            return fail(P2P_ERR_BAD_STATE, "eval(P2P_PAIRREC) needs p2p_restructure_pairs first (and after update)");
+        if (P->n == 0) return P2P_OK;
+        if (!is_device_ptr(potential)) return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
+        if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
+        return mark(P, eval_pairrec(P, potential, field));
+    }
     if (layout == P2P_REDUNDANT && !P->red_valid)
         return fail(P2P_ERR_BAD_STATE, "eval(P2P_REDUNDANT) needs p2p_restructure first (and after set_charges)");
     if (P->comm) {  // collective: every rank calls, even with no particles
@@ -490,6 +521,7 @@ p2p_status p2p_set_charges(p2p_plan *P, const void *charges) {
     if (P->n == 0) return P2P_OK;
     if (!is_device_ptr(charges)) return fail(P2P_ERR_INVALID_ARGUMENT, "charges must be a device pointer");
     P->red_valid = false;
+    P->pr_valid = false;
     s = P->cfg.kernel == P2P_GRAVITY ? set_charges_gravity(P, charges) : set_charges_helmholtz(P, charges);
     return mark(P, s);
 }
@@ -555,6 +587,11 @@ p2p_status p2p_copy_out(const p2p_plan *Pc, p2p_array which, void *host_dst, siz
         if (!P->red_valid) return fail(P2P_ERR_BAD_STATE, "the redundant buffer is not built (call p2p_restructure)");
         src = P->red;
         need = (size_t)P->R * (grav ? (f64 ? 32 : 16) : (f64 ? 16 : 8));
+        break;
+    case P2P_ARR_PAIRREC:
+        if (!P->pr_valid) return fail(P2P_ERR_BAD_STATE, "pair records are not built (call p2p_restructure_pairs)");
+        src = P->pr;
+        need = (size_t)P->pr_records * (f64 ? 32 : 16);
         break;
     default: return fail(P2P_ERR_INVALID_ARGUMENT, "unknown array");
     }

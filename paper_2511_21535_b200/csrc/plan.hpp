@@ -112,6 +112,11 @@ struct p2p_plan {
     std::vector<uint32_t> splitters;        // G + 1 key boundaries of the rank ranges
     void *phi_loc = nullptr, *field_loc = nullptr, *res_own = nullptr, *res_back = nullptr;
     bool red_valid = false;
+    // SURVEY NEXT-4 pair records (k_pairrec.cu): [T + R] records, [T] partial slots, t_off[B + 1] slot bases
+    void *pr = nullptr, *pr_partial = nullptr;
+    unsigned long long *pr_toff = nullptr;
+    int64_t pr_records = 0, pr_targets = 0;
+    bool pr_valid = false;
     p2p_status sticky = P2P_OK;
     int eval_blocks[3] = {0, 0, 0};
 };
@@ -152,6 +157,11 @@ p2p_status helmholtz_table(p2p_plan *P);
 bool helmholtz_tc_supported(const p2p_plan *P);
 p2p_status helmholtz_tc_table(p2p_plan *P, const float *Pf);
 p2p_status eval_helmholtz_tc(p2p_plan *P, void *y);
+
+// k_pairrec.cu: the thread-level pair-record layout (P2P_PAIRREC)
+p2p_status restructure_pairs(p2p_plan *P);
+p2p_status eval_pairrec(p2p_plan *P, void *phi, void *field);
+void free_pairrec(p2p_plan *P);
 
 // allocation helpers (stream-ordered, pooled)
 cudaError_t dalloc(void **p, size_t bytes, cudaStream_t st);
