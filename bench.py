@@ -67,6 +67,12 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a few hundred ms to start: wait for its first sample so that the timed region
+            # (which may last only ~0.2 s) is covered
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.n_before = len(self.samples)
         except OSError:
             self.proc = None
         return self
@@ -91,7 +97,8 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        load = [s for s in self.samples if not (s[3] & 0x1)] or self.samples
+        timed = self.samples[max(0, getattr(self, "n_before", 1) - 1):]  # the last pre-region sample onwards
+        load = [s for s in timed if not (s[3] & 0x1)] or timed
         reasons = set()
         for s in load:
             for bit, name in self.REASONS.items():

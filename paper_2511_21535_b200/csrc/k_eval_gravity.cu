@@ -21,7 +21,7 @@
 //     Boxes with <= 8 targets and <= 128 sources take a thread-per-target-pair path instead (one warp per CTA
 //     starts with them, so their load latency hides behind the other warps' item work).
 //   * targets live in registers: lane (g, s) holds K targets (group g) and walks the staged sources
-//     j = s, s+S, ... (S source splits, G groups; S, G precomputed per item by k_nbr_build), so boxes of any
+//     j = s, s+S, ... (S source splits, G groups; S, G precomputed per item by k_nbr_fill), so boxes of any
 //     occupancy keep (almost) all 32 lanes busy; the S partial sums are combined by a fixed transpose-reduce
 //     (deterministic).
 //   * fp32: targets are paired and the pair math is issued as packed FP32x2 instructions (FADD2 / FMUL2 /
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
             for (int d = 0; d < 3; ++d)
                 needs_fix |= ((a.g.periodic >> d) & 1u) && (cc[d] == 0 || (int)cc[d] == a.g.nbox[d] - 1);
         }
-        // lane layout (precomputed by k_nbr_build): G groups of K targets x S source splits
+        // lane layout (precomputed by k_nbr_fill): G groups of K targets x S source splits
         const uint32_t nt = c_meta & 0xffu, S = (c_meta >> 8) & 0xffu, G = (c_meta >> 16) & 0xffu;
         const uint32_t m20 = c_m20[S];
         const uint32_t g = (lane * m20) >> 20, sl = lane - g * S;

@@ -8,7 +8,7 @@
 //     red = { fl_p(((double)x_j + S_x) - o_bx), ..y.., ..z.., m_j },  o_bd = fma(ib_d, h, lo_d)
 // One warp per CHUNK of 32 consecutive CSR entries (not per box): the entries' segments are consecutive in
 // red[] (CSR order = run order, and runs of consecutive boxes are adjacent), so a chunk is one contiguous output
-// range even when it spans several small boxes.  k_nbr_build records each chunk's owner box and output start.
+// range even when it spans several small boxes.  k_nbr_fill records each chunk's owner box and output start.
 // Three dependent load levels per chunk (entry -> segment / owner box -> records) instead of four per box, and
 // no per-box idle lanes: the Plummer workloads' median box has R ~ 20 records.  The 32 lanes cover the range
 // contiguously (coalesced 16 B stores), each lane finding its segment from a ballot / OR-reduce over the

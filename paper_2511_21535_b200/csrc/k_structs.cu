@@ -166,7 +166,8 @@ __global__ void k_boxinfo(const uint32_t *__restrict__ bkey, const uint32_t *__r
 //                entry are loaded together, branch-free (a stale entry of an empty key is ignored).  Per-box
 //                totals -> block sums per tile (CSR entries, redundant records, work items, small-target pairs)
 //                + the pair count I.
-//   k_nbr_fill   the same search again, block scan of the per-box totals + the tile's exclusive prefix from a
+//   k_nbr_fill   the box's occupied-slot mask and record count (saved by k_nbr_count), block scan of the per-box
+//                totals + the tile's exclusive prefix from a
 //                look-back over the (already complete) tile sums that never waits, then nbr_off / red_off, the CSR
 //                staged in shared memory and written coalesced, the restructure chunk heads, the eval work items
 //                or small-target entries.
@@ -288,7 +289,8 @@ __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t
                                                           const uint32_t *__restrict__ bstart,
                                                           const uint2 *__restrict__ boxinfo,
                                                           const uint32_t *__restrict__ occ, DevCounters *ctr,
-                                                          NbTile *__restrict__ tiles, uint32_t tmax) {
+                                                          NbTile *__restrict__ tiles, uint2 *__restrict__ box_nbr,
+                                                          uint32_t tmax) {
     const uint32_t B = ctr->B;
     const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
     unsigned long long pairs = 0;
@@ -304,6 +306,7 @@ __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t
         make_nb(g, key, S);
 #pragma unroll
         for (int dz = 0; dz < 3; ++dz) nb_plane(S, dz, key, tgt, occ, boxinfo, okm, cnt, red);
+        if (have) box_nbr[b] = make_uint2(okm, (uint32_t)red);  // k_nbr_fill needs no occupancy search
         const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax);
         pairs += (unsigned long long)(tgt ? nb : 0u) * red;
         BoxTotals tot;
@@ -381,7 +384,7 @@ __device__ NbTile tile_prefix(uint32_t tile, const NbTile *__restrict__ sums, co
 #endif
 __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
     Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart, const uint2 *__restrict__ boxinfo,
-    const uint32_t *__restrict__ occ, DevCounters *ctr, const NbTile *__restrict__ tiles, NbTile *incl,
+    const uint2 *__restrict__ box_nbr, DevCounters *ctr, const NbTile *__restrict__ tiles, NbTile *incl,
     unsigned int *flags, uint32_t *__restrict__ nbr_off, unsigned long long *__restrict__ red_off, uint32_t *__restrict__ nbr_box,
     uint8_t *__restrict__ nbr_slot, Item *__restrict__ items, uint32_t *__restrict__ small_tgt,
     uint32_t *__restrict__ small_box, uint32_t *__restrict__ chunk_box, unsigned long long *__restrict__ chunk_out,
@@ -399,12 +402,10 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
         const bool tgt = have && key >= g.tkey_lo && key <= g.tkey_hi;
         NbStencil S;
         make_nb(g, key, S);
-        // pass 1: totals (the same search as k_nbr_count); pass 2 repeats the boxinfo loads (L1 hits) instead of
-        // holding 54 registers of slot results (occupancy)
-        uint32_t cnt = 0, okm = 0;
-        unsigned long long red = 0;
-#pragma unroll
-        for (int dz = 0; dz < 3; ++dz) nb_plane(S, dz, key, tgt, occ, boxinfo, okm, cnt, red);
+        // the occupied-slot mask and record count found by k_nbr_count
+        const uint2 bn = have ? box_nbr[b] : make_uint2(0u, 0u);
+        const uint32_t okm = bn.x, cnt = __popc(okm);
+        const unsigned long long red = bn.y;
         const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax);
         BoxTotals tot;
         const BoxTotals inc = block_scan_totals(x, &tot);
@@ -541,7 +542,7 @@ static unsigned grid_for(uint64_t n, int threads, int num_sms) {
 void free_capacity(p2p_plan *P) {
     cudaStream_t st = P->stream;
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
-                    P->s_nb_tiles, P->s_aos, P->boxinfo,
+                    P->s_nb_tiles, P->s_aos, P->s_box_nbr, P->boxinfo,
                     P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, P->rec, P->bkey, P->bstart,
                     P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
     for (void *b : bufs) dfree(b, st);
@@ -549,6 +550,7 @@ void free_capacity(p2p_plan *P) {
     P->s_partials = nullptr;
     P->s_nb_tiles = nullptr;
     P->s_aos = nullptr;
+    P->s_box_nbr = nullptr;
     P->boxinfo = nullptr;
     P->small_tgt = P->small_box = P->chunk_box = nullptr;
     P->chunk_out = nullptr;
@@ -589,6 +591,7 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     if (grav) {
         P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
         P2P_CUDA_TRY(dalloc(&P->s_aos, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
+        P2P_CUDA_TRY(dalloc((void **)&P->s_box_nbr, sizeof(uint2) * bcap, st));
         P2P_CUDA_TRY(dalloc(&P->s_nb_tiles, (2 * sizeof(NbTile) + 4) * div_up(bcap, NB_THREADS), st));
         P2P_CUDA_TRY(dalloc((void **)&P->boxinfo, sizeof(uint2) * keyspace, st));
         P2P_CUDA_TRY(dalloc((void **)&P->small_tgt, 4 * n, st));
@@ -649,13 +652,13 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     unsigned int *flags = (unsigned int *)(incl + ntile_cap);
     P2P_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * ntile_cap, st));
     P2P_LAUNCH(k_nbr_count, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, tiles,
-               (uint32_t)ITEM_TMAX);
+               P->s_box_nbr, (uint32_t)ITEM_TMAX);
     static bool carveout_set = false;  // the fill keeps a large L1 (its pass-2 reloads must hit)
     if (!carveout_set && P2P_NB_CARVEOUT > 0) {
         P2P_CUDA_TRY(cudaFuncSetAttribute(k_nbr_fill, cudaFuncAttributePreferredSharedMemoryCarveout, P2P_NB_CARVEOUT));
         carveout_set = true;
     }
-    P2P_LAUNCH(k_nbr_fill, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, tiles,
+    P2P_LAUNCH(k_nbr_fill, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->s_box_nbr, P->ctr, tiles,
                incl, flags, P->nbr_off, (unsigned long long *)P->red_off, P->nbr_box, P->nbr_slot, P->items,
                P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32),
                (uint32_t)ITEM_TMAX);

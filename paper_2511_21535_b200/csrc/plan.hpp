@@ -95,6 +95,7 @@ struct p2p_plan {
     uint32_t *s_hist = nullptr, *s_status = nullptr;
     void *s_partials = nullptr;
     void *s_aos = nullptr;       // gravity: the SoA input packed into {x,y,z,m} records (input order), a3's source
+    uint2 *s_box_nbr = nullptr;  // per box: occupied-slot mask, redundant records (k_nbr_count -> k_nbr_fill)
     void *s_nb_tiles = nullptr;  // [ceil(B / 256)] k_nbr_count tile sums -> k_nbr_scan offsets
     uint2 *boxinfo = nullptr;     // gravity: dense Morton key -> {box, n_b} (valid where occ has the bit set)
     uint32_t *small_tgt = nullptr, *small_box = nullptr;  // sorted target index / its box, small boxes only

@@ -7,7 +7,7 @@ TAG=${1:-r01}
 O=gpurun_out/$TAG
 mkdir -p $O
 ncu --set full --import-source on --clock-control none \
-    -k regex:"k_eval_gravity|k_restructure_gravity|k_nbr_build|k_radix_pass|k_permute" -c 9 \
+    -k regex:"k_eval_gravity|k_restructure_gravity|k_nbr_count|k_nbr_fill|k_radix_pass|k_permute|k_bin_gravity" -c 10 \
     -o $O/full_c5w python scripts/profile_step.py c5w 1 redundant,indexed > $O/ncu_full.log 2>&1
 python - "$O" <<'PY'
 import csv, io, json, subprocess, sys
@@ -40,3 +40,8 @@ for w in c5s c3dense; do python bench.py --workload $w --no-cpu-baseline --steps
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ncu_launches_bench.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_under_ncu.log 2>&1
 echo done
+python scripts/bench_pairrec.py > $O/bench_pairrec.jsonl 2> $O/bench_pairrec.err
+python scripts/locality_model.py > $O/locality.jsonl 2> $O/locality.err
+python scripts/dist_overhead.py > $O/dist_overhead.txt 2>&1
+python scripts/hbm_modes.py > $O/hbm_modes.json 2>&1
+python scripts/kprof.py c5w 5 > $O/kprof_c5w.txt 2>/dev/null
