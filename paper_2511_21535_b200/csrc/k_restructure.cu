@@ -20,183 +20,40 @@
 #include <cmath>
 
 #include "plan.hpp"
+#include "restructure.cuh"
 
 namespace p2p {
 
 namespace {
-template <typename T> struct V4T;
-template <> struct V4T<float> { using type = float4; };
-template <> struct V4T<double> { using type = double4; };
-
-// image shift of stencil slot `slot` seen from box c (DESIGN C5): +L past the upper face, -L past the lower
-__device__ __forceinline__ double slot_shift(const Geom &g, const uint32_t c[3], int slot, int d) {
-    const int dd = d == 0 ? slot % 3 - 1 : (d == 1 ? (slot / 3) % 3 - 1 : slot / 9 - 1);
-    const int v = (int)c[d] + dd;
-    if (v >= g.nbox[d]) return g.L[d];
-    if (v < 0) return -g.L[d];
-    return 0.0;
-}
-
 template <typename T, bool EXACT32>
-__global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const typename V4T<T>::type *__restrict__ rec,
-                                                             const uint32_t *__restrict__ bkey,
-                                                             const uint32_t *__restrict__ bstart,
-                                                             const uint32_t *__restrict__ nbr_off,
-                                                             const uint32_t *__restrict__ nbr_box,
-                                                             const uint8_t *__restrict__ nbr_slot,
-                                                             const uint32_t *__restrict__ chunk_box,
-                                                             const unsigned long long *__restrict__ chunk_out,
-                                                             const DevCounters *__restrict__ ctr,
-                                                             typename V4T<T>::type *__restrict__ red) {
-    using V4 = typename V4T<T>::type;
-    constexpr unsigned FULL = 0xffffffffu;
+__global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const rs::Ptrs<T> p,
+                                                             const DevCounters *__restrict__ ctr) {
     // device-side counts: no host sync needed after an asynchronous p2p_plan_update
     const uint32_t B = ctr->B, n_nbr = ctr->n_nbr;
     const uint32_t nchunk = (n_nbr + 31u) >> 5;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    const double L0 = g.L[0], L1 = g.L[1], L2 = g.L[2];
     // level 1 of a chunk: its head and lane e's CSR entry -- loaded one chunk ahead (software pipeline)
     uint32_t n_b0 = 0, n_k = 0, n_slot = 13;
     unsigned long long n_gout = 0;
     auto load1 = [&](uint32_t c) {
         if (c < nchunk) {
-            n_b0 = chunk_box[c];
-            n_gout = chunk_out[c];
+            n_b0 = p.chunk_box[c];
+            n_gout = p.chunk_out[c];
             const uint32_t ee = (c << 5) + lane;
             if (ee < n_nbr) {
-                n_k = nbr_box[ee];
-                n_slot = nbr_slot[ee];
+                n_k = p.nbr_box[ee];
+                n_slot = p.nbr_slot[ee];
             }
         }
     };
     uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     load1(ch);
     for (; ch < nchunk; ch += nw) {
-        const uint32_t e = (ch << 5) + lane;
-        const bool seg = e < n_nbr;
-        const uint32_t b0 = n_b0;
+        const uint32_t b0 = n_b0, k = n_k, slot = n_slot;
         const unsigned long long gout = n_gout;
-        const uint32_t k = seg ? n_k : 0u, slot = seg ? n_slot : 13u;
         load1(ch + nw);
-        // ---- level 2: boxes b0 .. b0 + 31 (CSR starts, keys) and lane e's source segment ----
-        const uint32_t bl = b0 + lane;
-        uint32_t boff = 0xffffffffu, keyl = 0;
-        if (bl < B) {
-            boff = nbr_off[bl];
-            keyl = bkey[bl];
-        }
-        uint32_t src = 0, cnt = 0;
-        if (seg) {
-            src = bstart[k];
-            cnt = bstart[k + 1] - src;
-        }
-        // owner of entry e: the largest i with nbr_off[b0 + i] <= e (non-decreasing in i; every target box owns
-        // >= 1 entry, so the chunk's <= 32 entries belong to boxes b0 .. b0 + 31)
-        uint32_t i = 0;
-#pragma unroll
-        for (uint32_t step = 16; step > 0; step >>= 1) {
-            const uint32_t t = __shfl_sync(FULL, boff, i + step);
-            if (t <= e) i += step;
-        }
-        const uint32_t key = __shfl_sync(FULL, keyl, i);
-        const uint32_t c[3] = {compact3(key), compact3(key >> 1), compact3(key >> 2)};
-        const double o0 = __fma_rn((double)c[0], g.h, g.lo[0]);
-        const double o1 = __fma_rn((double)c[1], g.h, g.lo[1]);
-        const double o2 = __fma_rn((double)c[2], g.h, g.lo[2]);
-        // image code of the entry's slot (2 bits per dim: 1 = +L, 2 = -L), once per segment
-        uint32_t code = 0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const double S = slot_shift(g, c, (int)slot, d);
-            code |= (S > 0.0 ? 1u : (S < 0.0 ? 2u : 0u)) << (2 * d);
-        }
-        // segments of consecutive CSR entries are consecutive in red[]: one contiguous output range per chunk
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= (unsigned)o) incl += y;
-        }
-        const uint32_t st = incl - cnt;
-        const uint32_t Rc = __shfl_sync(FULL, incl, 31);
-        V4 *__restrict__ out = red + gout;
-        const uint32_t le = lane == 31 ? FULL : ((2u << lane) - 1u);
-        // ---- level 3: UNR windows of 32 records per iteration, all loads issued before the first store ----
-        // chunks without any periodic image (all but the boundary layers) skip the shift selection: adding the
-        // +0.0 shift keeps the oracle's rounding sequence (and its -0 -> +0 behaviour) exactly
-        const bool wrap = __any_sync(FULL, seg && code != 0u);
-        // fp32 fast path (C11 unchanged bit for bit): with no periodic shift and every owner origin exactly an
-        // fp32 value, fl32(fl64(x + 0) - o) == fl32(fl32(x + 0) - o) -- a single subtraction of two fp32
-        // operands rounded through fp64 (53 >= 2*24 + 2 bits) rounds like the direct fp32 subtraction -- so the
-        // conversions and fp64 operations (6 F2F on the XU pipe per record) drop out
-        // (EXACT32: the host verified that every box origin of the grid is an fp32 value)
-        const float f0o = (float)o0, f1o = (float)o1, f2o = (float)o2;
-        const bool fast32 = EXACT32 && !wrap;
-        constexpr int UNR = 4;
-        for (uint32_t rb = 0; rb < Rc; rb += 32 * UNR) {
-            V4 x[UNR];
-            uint32_t xe[UNR];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const uint32_t r0 = rb + 32u * u;
-                if (r0 >= Rc) break;  // warp-uniform: short ranges skip the empty windows
-                // segment of record r0 + lane without a search (segments are non-empty and contiguous):
-                // segments starting before r0 (ballot) - 1 + segment starts in [r0, r0 + lane] (OR-reduced mask)
-                const uint32_t before = __popc(__ballot_sync(FULL, seg && st < r0));
-                const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
-                const uint32_t starts = __reduce_or_sync(FULL, in_win);
-                xe[u] = (before - 1u + __popc(starts & le)) & 31u;
-                const uint32_t e_src = __shfl_sync(FULL, src, xe[u]);
-                const uint32_t e_st = __shfl_sync(FULL, st, xe[u]);
-                const uint32_t r = r0 + lane;
-                if (r < Rc) x[u] = rec[e_src + (r - e_st)];
-            }
-            if (fast32) {
-#pragma unroll
-                for (int u = 0; u < UNR; ++u) {
-                    const uint32_t r0 = rb + 32u * u;
-                    if (r0 >= Rc) break;
-                    const float eo0 = __shfl_sync(FULL, f0o, xe[u]);
-                    const float eo1 = __shfl_sync(FULL, f1o, xe[u]);
-                    const float eo2 = __shfl_sync(FULL, f2o, xe[u]);
-                    const uint32_t r = r0 + lane;
-                    if (r < Rc) {
-                        V4 v;
-                        v.x = (T)__fsub_rn(__fadd_rn((float)x[u].x, 0.0f), eo0);
-                        v.y = (T)__fsub_rn(__fadd_rn((float)x[u].y, 0.0f), eo1);
-                        v.z = (T)__fsub_rn(__fadd_rn((float)x[u].z, 0.0f), eo2);
-                        v.w = x[u].w;
-                        out[r] = v;
-                    }
-                }
-                continue;
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const uint32_t r0 = rb + 32u * u;
-                if (r0 >= Rc) break;
-                const double eo0 = __shfl_sync(FULL, o0, xe[u]);
-                const double eo1 = __shfl_sync(FULL, o1, xe[u]);
-                const double eo2 = __shfl_sync(FULL, o2, xe[u]);
-                double S0 = 0.0, S1 = 0.0, S2 = 0.0;
-                if (wrap) {
-                    const uint32_t cd = __shfl_sync(FULL, code, xe[u]);
-                    S0 = (cd & 1u) ? L0 : ((cd & 2u) ? -L0 : 0.0);
-                    S1 = (cd & 4u) ? L1 : ((cd & 8u) ? -L1 : 0.0);
-                    S2 = (cd & 16u) ? L2 : ((cd & 32u) ? -L2 : 0.0);
-                }
-                const uint32_t r = r0 + lane;
-                if (r < Rc) {
-                    V4 v;
-                    v.x = (T)__dsub_rn(__dadd_rn((double)x[u].x, S0), eo0);
-                    v.y = (T)__dsub_rn(__dadd_rn((double)x[u].y, S1), eo1);
-                    v.z = (T)__dsub_rn(__dadd_rn((double)x[u].z, S2), eo2);
-                    v.w = x[u].w;
-                    out[r] = v;
-                }
-            }
-        }
+        rs::chunk<T, EXACT32>(g, p, B, n_nbr, ch, b0, gout, k, slot, lane);
     }
 }
 
@@ -219,7 +76,7 @@ __global__ void k_restructure_helmholtz(const C2 *__restrict__ xs, const uint32_
 }  // namespace
 
 // every box origin o_d = fma(c, h, lo_d), c < nbox_d, is exactly an fp32 value (the restructure's fp32 path)
-static bool origins_exact_fp32(const Geom &g) {
+bool origins_exact_fp32(const Geom &g) {
     for (int d = 0; d < 3; ++d)
         for (int c = 0; c < g.nbox[d]; ++c) {
             const double o = std::fma((double)c, g.h, g.lo[d]);
@@ -234,17 +91,11 @@ p2p_status restructure_gravity(p2p_plan *P) {
     const uint64_t nchunk = div_up(P->sizes_known ? (uint64_t)P->n_nbr : 27ull * (uint64_t)P->bcap, 32);
     const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(div_up(nchunk * 32, 256), (unsigned)P->num_sms * 16));
     if (P->cfg.precision == P2P_FP64)
-        P2P_LAUNCH((k_restructure_gravity<double, false>), grid, 256, 0, P->stream, P->geom, (const double4 *)P->rec,
-                   P->bkey, P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
-                   (double4 *)P->red);
+        P2P_LAUNCH((k_restructure_gravity<double, false>), grid, 256, 0, P->stream, P->geom, rs_ptrs<double>(P), P->ctr);
     else if (origins_exact_fp32(P->geom))
-        P2P_LAUNCH((k_restructure_gravity<float, true>), grid, 256, 0, P->stream, P->geom, (const float4 *)P->rec,
-                   P->bkey, P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
-                   (float4 *)P->red);
+        P2P_LAUNCH((k_restructure_gravity<float, true>), grid, 256, 0, P->stream, P->geom, rs_ptrs<float>(P), P->ctr);
     else
-        P2P_LAUNCH((k_restructure_gravity<float, false>), grid, 256, 0, P->stream, P->geom, (const float4 *)P->rec,
-                   P->bkey, P->bstart, P->nbr_off, P->nbr_box, P->nbr_slot, P->chunk_box, P->chunk_out, P->ctr,
-                   (float4 *)P->red);
+        P2P_LAUNCH((k_restructure_gravity<float, false>), grid, 256, 0, P->stream, P->geom, rs_ptrs<float>(P), P->ctr);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }
