@@ -127,9 +127,6 @@ def main():
     ap.add_argument("--workload", default="c5w")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--split", action="store_true",
-                    help="step = p2p_restructure then p2p_eval(REDUNDANT) as two launches (default: the overlapped "
-                         "p2p_restructure_eval, same results bit for bit)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -195,15 +192,10 @@ def ours(args, rank, world, local):
         plan = holder["plan"]
         if ev:
             ev[1].record(stream)
-        if args.split:
-            plan.restructure()
-            if ev:
-                ev[2].record(stream)
-            plan.eval(P.P2P_REDUNDANT, phi, field)
-        else:  # a6 + a7 + a9 overlapped in one kernel
-            if ev:
-                ev[2].record(stream)
-            plan.restructure_eval(phi, field)
+        plan.restructure()
+        if ev:
+            ev[2].record(stream)
+        plan.eval(P.P2P_REDUNDANT, phi, field)
         if ev:
             ev[3].record(stream)
 
@@ -265,7 +257,6 @@ def ours(args, rank, world, local):
     t_ev_red = timed(lambda: plan.eval(P.P2P_REDUNDANT, phi, field), reps)
     t_ev_idx = timed(lambda: plan.eval(P.P2P_INDEXED, phi, field), reps)
     t_restr = timed(lambda: plan.restructure(), reps)
-    t_fused = timed(lambda: plan.restructure_eval(phi, field), reps)
     R = int(plan.info.n_red)
     B = int(plan.info.n_boxes)
 
@@ -284,7 +275,7 @@ def ours(args, rank, world, local):
             traffic = None
     # restructure vs HBM: writes 16 R bytes + compulsory reads 16 N_src (= 16 N) bytes
     rest_bytes = 16 * R + 16 * N
-    rest_ms = float(np.mean(t_rest)) if args.split else t_restr[0]   # fused step: the standalone launch
+    rest_ms = float(np.mean(t_rest))
 
     out = {
         "metric": METRIC,
@@ -304,11 +295,8 @@ def ours(args, rank, world, local):
                                    f"repartition + halo exchange (one Plummer tile per GPU)") if world > 1
                    else "1 GPU",
                    "l2": "inputs+red buffer > L2 and 512 MB L2 flush between timed steps",
-                   "step": ("p2p_plan_update(a1-a5) + p2p_restructure(a6) + p2p_eval REDUNDANT(a7,a9)" if args.split
-                            else "p2p_plan_update(a1-a5) + p2p_restructure_eval (a6 + a7 + a9 overlapped in one "
-                                 "kernel)") + "; plan created once"},
-        "roofline": {"bound": "alu", "kernel": "k_eval_gravity<float,REDUNDANT,4>" if args.split else
-                     "k_eval_gravity<float,REDUNDANT,4,OVL> (restructure inside)", "achieved": achieved / 1e9,
+                   "step": "p2p_plan_update(a1-a5) + p2p_restructure(a6) + p2p_eval REDUNDANT(a7,a9); plan created once"},
+        "roofline": {"bound": "alu", "kernel": "k_eval_gravity<float,REDUNDANT,4>", "achieved": achieved / 1e9,
                      "peak": peak_pairs / 1e9, "unit": "Gpair/s (FP32 pipe: 13 instr/pair)",
                      "frac": achieved / peak_pairs, "traffic": traffic,
                      "peak_basis": f"{n_sm} SMs x 128 FP32 lanes x {pk['sm_max_mhz']:.0f} MHz ({pk['src']}) / 13"},
@@ -324,9 +312,6 @@ def ours(args, rank, world, local):
             "restructure_ms_median_min": t_restr,
             "redundant_e2e_vs_indexed": t_ev_idx[0] / (t_restr[0] + t_ev_red[0]),
             "redundant_kernel_vs_indexed": t_ev_idx[0] / t_ev_red[0],
-            "fused_restructure_eval_ms_median_min": t_fused,
-            "fused_restructure_eval_pairs_per_s": I / (t_fused[0] * 1e-3),
-            "fused_vs_indexed": t_ev_idx[0] / t_fused[0],
         },
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -343,15 +328,8 @@ def ours(args, rank, world, local):
 
             def e2e_call():
                 splan.update_host(pos_h, m_h)
-                if args.split:
-                    splan.restructure()
-                    splan.eval_host(P.P2P_REDUNDANT, phi_h, field_h)
-                else:
-                    splan.restructure_eval(phi, field)
-                    phi_h.copy_(phi, non_blocking=True)
-                    field_h.copy_(field, non_blocking=True)
-            if not args.split:
-                api = "Plan.update_host (p2p_plan_update_host, pinned H2D) + restructure_eval + D2H (pinned)"
+                splan.restructure()
+                splan.eval_host(P.P2P_REDUNDANT, phi_h, field_h)
         else:
             # collective plans have no host-buffer entry points: the same sequence with the copies done by torch
             # on the plan's stream (pinned buffers, non_blocking)
@@ -365,11 +343,8 @@ def ours(args, rank, world, local):
                 pos_e.copy_(pos_h, non_blocking=True)
                 m_e.copy_(m_h, non_blocking=True)
                 splan.update(pos_e, m_e)
-                if args.split:
-                    splan.restructure()
-                    splan.eval(P.P2P_REDUNDANT, phi, field)
-                else:
-                    splan.restructure_eval(phi, field)
+                splan.restructure()
+                splan.eval(P.P2P_REDUNDANT, phi, field)
                 phi_h.copy_(phi, non_blocking=True)
                 field_h.copy_(field, non_blocking=True)
 

@@ -143,18 +143,6 @@ p2p_status p2p_eval_host(p2p_plan *plan, p2p_layout layout, void *potential_host
  * C11; helmholtz: Xg[B][9][t], zero segments for missing neighbours, C10).  Enqueue only. */
 p2p_status p2p_restructure(p2p_plan *plan);
 
-/* a6 + a7 (+ a9) overlapped: builds red[] exactly as p2p_restructure and evaluates exactly as
- * p2p_eval(P2P_REDUNDANT) -- same red[] bytes, same outputs bit for bit -- in ONE kernel.  The restructure is
- * bound by HBM / memory latency and the eval by the FP32 pipe, so the two share the SMs: red[] is published in
- * groups of 2^16 records, an eval warp issues a box's run only once every record before its end is written, and
- * restructures chunks itself while it would otherwise wait (no dependence on co-scheduling).  The
- * paper's Eq 2 sums the phases and notes that restructuring "offsets the redundant kernel speedup"
- * (§5.2.3); this entry point hides most of it.  Arguments as p2p_eval (gravity: potential [n_local],
- * field [n_local][3] or NULL; helmholtz: potential = y [n_local] complex, field NULL -- DBIM runs the two steps
- * back to back).  Multi-GPU plans: collective, like p2p_eval.  Leaves red[] valid for later
- * p2p_eval(P2P_REDUNDANT) calls.  Enqueue only. */
-p2p_status p2p_restructure_eval(p2p_plan *plan, void *potential, void *field);
-
 /* build the pair-record buffer of P2P_PAIRREC ("duplicating particle data for each
  * interaction pair ... each entry contains both source and target attributes").  Record of CSR entry e =
  * (b, k, slot): b's n_b target tuples rebased to o_b, then k's n_k source tuples rebased like red (C11) -- bit for

@@ -32,7 +32,7 @@ P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE, P2P_PAIRREC = 0, 1, 2, 3
 # the layouts one p2p_restructure serves (P2P_PAIRREC needs p2p_restructure_pairs)
 LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise": P2P_INDEXED_BITWISE}
 
-EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure", "p2p_restructure_eval",
+EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure",
             "p2p_restructure_pairs", "p2p_get_pairrec_size", "p2p_eval",
             "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
@@ -78,7 +78,6 @@ def lib() -> C.CDLL:
             "p2p_plan_update_host": (C.c_int, [p, i64, p, p]),
             "p2p_eval_host": (C.c_int, [p, C.c_int, p, p]),
             "p2p_restructure": (C.c_int, [p]),
-            "p2p_restructure_eval": (C.c_int, [p, p, p]),
             "p2p_restructure_pairs": (C.c_int, [p]),
             "p2p_get_pairrec_size": (C.c_int, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "p2p_eval": (C.c_int, [p, C.c_int, p, p]),
@@ -157,10 +156,6 @@ def p2p_eval_host(plan: int, layout: int, potential_host: int, field_host: int |
 
 def p2p_restructure(plan: int):
     _check(lib().p2p_restructure(C.c_void_p(plan)))
-
-
-def p2p_restructure_eval(plan: int, potential: int, field: int | None):
-    _check(lib().p2p_restructure_eval(C.c_void_p(plan), C.c_void_p(potential), C.c_void_p(field or None)))
 
 
 def p2p_restructure_pairs(plan: int):
@@ -355,22 +350,6 @@ class Plan:
 
     def restructure(self):
         p2p_restructure(self.handle)
-
-    def restructure_eval(self, potential=None, field=None, want_field: bool = True):
-        """p2p_restructure_eval: restructure + eval(P2P_REDUNDANT) overlapped in one kernel (same results)"""
-        import torch
-        dev = torch.device("cuda", torch.cuda.current_device())
-        if self.kernel == P2P_GRAVITY:
-            if potential is None:
-                potential = torch.empty(self.n, dtype=self.dtype, device=dev)
-            if field is None and want_field:
-                field = torch.empty((self.n, 3), dtype=self.dtype, device=dev)
-            p2p_restructure_eval(self.handle, potential.data_ptr(), field.data_ptr() if field is not None else None)
-            return potential, field
-        if potential is None:
-            potential = torch.empty((self.n, 2), dtype=self.dtype, device=dev)
-        p2p_restructure_eval(self.handle, potential.data_ptr(), None)
-        return potential
 
     def restructure_pairs(self):
         """the thread-level pair records of P2P_PAIRREC"""

@@ -529,14 +529,14 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
 }
 
 template <typename T>
-p2p_status eval_dist_t(p2p_plan *P, p2p_layout layout, void *phi, void *field, bool fused) {
+p2p_status eval_dist_t(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
     using V4 = typename V4T<T>::type;
     cudaStream_t st = P->stream;
     const int G = P->comm->nranks;
     const uint32_t nl = (uint32_t)P->n, ni = (uint32_t)P->n_in;
     if (nl > 0) {
         // results land at the local (received) positions; halo positions are not written and never sent back
-        p2p_status s = eval_gravity(P, layout, P->phi_loc, P->field_loc, fused);
+        p2p_status s = eval_gravity(P, layout, P->phi_loc, P->field_loc);
         if (s != P2P_OK) return s;
         P2P_LAUNCH((k_pack_results<T, V4>), grid1(nl, P->num_sms), 256, 0, st, (const T *)P->phi_loc,
                    (const T *)P->field_loc, nl, (V4 *)P->res_own);
@@ -561,9 +561,9 @@ p2p_status build_distributed(p2p_plan *P, const void *pos, const void *q) {
     return P->cfg.precision == P2P_FP64 ? build_dist_t<double>(P, pos, q) : build_dist_t<float>(P, pos, q);
 }
 
-p2p_status eval_distributed(p2p_plan *P, p2p_layout layout, void *phi, void *field, bool fused) {
-    return P->cfg.precision == P2P_FP64 ? eval_dist_t<double>(P, layout, phi, field, fused)
-                                        : eval_dist_t<float>(P, layout, phi, field, fused);
+p2p_status eval_distributed(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
+    return P->cfg.precision == P2P_FP64 ? eval_dist_t<double>(P, layout, phi, field)
+                                        : eval_dist_t<float>(P, layout, phi, field);
 }
 
 }  // namespace p2p

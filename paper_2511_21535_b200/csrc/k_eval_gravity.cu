@@ -36,7 +36,6 @@
 #include <type_traits>
 
 #include "plan.hpp"
-#include "restructure.cuh"
 
 namespace p2p {
 
@@ -73,123 +72,7 @@ struct EvalArgs {
     const uint32_t *small_tgt, *small_box;
     T *phi;
     T *field;
-    // p2p_restructure_eval (OVL = true): the restructure runs inside the eval kernel (see ovl_help / ovl_wait)
-    rs::Ptrs<T> rsp;
-    const DevCounters *ctr;
-    uint32_t *rs_sync;        // [0] chunk queue head, [1] front, [2 + g] records written in group g
-    uint32_t exact32;         // restructure fp32 fast path allowed (origins_exact_fp32)
-    uint32_t ahead;           // groups the front should lead the item being issued by (helping is optional)
 };
-
-// ---- p2p_restructure_eval: restructure and eval in ONE kernel, overlapped --------------------------------
-// The restructure (a6) is HBM/latency bound and the eval (a7) FP32 bound, so on the same SMs they overlap:
-// red[] is cut into groups of 2^RS_GS records; a warp that restructures a chunk (rs::chunk, the same code as
-// the standalone kernel) release-adds its record counts to the groups it wrote (fire and forget).  The `front`
-// word is a monotone hint: every group below it is complete; readers that need more advance it themselves over
-// the complete groups that follow (acquire loads of 32 counters at a time, atomicMax).  An eval warp issues an
-// item's bulk copies only once the front covers the item's run; until then -- and whenever the front leads its
-// next item by fewer than `ahead` groups -- it restructures chunks itself (claimed in order from one queue), so
-// no progress depends on co-scheduling, and runs are consumed while still in L2.  Same red[] bytes, same
-// outputs as p2p_restructure + p2p_eval(P2P_REDUNDANT).
-// Visibility: a group counter reaches its size only after every record of the group was written and released
-// (red.release.gpu after the warp's stores); the eval's bulk copies read through L2 after a proxy fence.
-constexpr int RS_GS = 16;
-
-__device__ __forceinline__ uint32_t ld_vol(const uint32_t *p) { return *(const volatile uint32_t *)p; }
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void red_release_add(uint32_t *p, uint32_t v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t rs_need(uint64_t R, uint32_t g) {
-    const uint64_t left = R - ((uint64_t)g << RS_GS);
-    return left < (1ull << RS_GS) ? (uint32_t)left : (1u << RS_GS);
-}
-__device__ __forceinline__ bool rs_covered(uint32_t front, uint32_t ngroups, uint64_t end) {
-    return front >= ngroups || ((uint64_t)front << RS_GS) >= end;
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-// claim one restructure chunk (warp-collective) and write + publish it; false when every chunk is claimed
-template <typename T>
-__device__ __noinline__ bool ovl_help(const EvalArgs<T> &a, unsigned lane) {
-    constexpr unsigned FULL = 0xffffffffu;
-    const uint32_t n_nbr = a.ctr->n_nbr, B = a.ctr->B;
-    const uint32_t nchunk = (n_nbr + 31u) >> 5;
-    uint32_t ch = 0;
-    if (lane == 0) ch = atomicAdd(&a.rs_sync[0], 1u);
-    ch = __shfl_sync(FULL, ch, 0);
-    if (ch >= nchunk) return false;
-    const uint32_t b0 = a.rsp.chunk_box[ch];
-    const unsigned long long gout = a.rsp.chunk_out[ch];
-    const uint32_t e = (ch << 5) + lane;
-    uint32_t k = 0, slot = 13;
-    if (e < n_nbr) {
-        k = a.rsp.nbr_box[e];
-        slot = a.rsp.nbr_slot[e];
-    }
-    uint32_t Rc;
-    if constexpr (sizeof(T) == 4) {
-        if (a.exact32) Rc = rs::chunk<T, true>(a.g, a.rsp, B, n_nbr, ch, b0, gout, k, slot, lane);
-        else Rc = rs::chunk<T, false>(a.g, a.rsp, B, n_nbr, ch, b0, gout, k, slot, lane);
-    } else {
-        Rc = rs::chunk<T, false>(a.g, a.rsp, B, n_nbr, ch, b0, gout, k, slot, lane);
-    }
-    // publish: the warp's stores are ordered before the release-adds (bar.warp.sync orders the lanes' accesses;
-    // the release is cumulative over what the releasing lane has observed)
-    __syncwarp();
-    if (Rc == 0) return true;
-    const uint32_t g0 = (uint32_t)(gout >> RS_GS), g1 = (uint32_t)((gout + Rc - 1) >> RS_GS);
-    for (uint32_t g = g0 + lane; g <= g1; g += 32) {
-        const uint64_t glo = (uint64_t)g << RS_GS;
-        const uint64_t lo = gout > glo ? gout : glo;
-        const uint64_t hi = min(gout + Rc, glo + (1ull << RS_GS));
-        red_release_add(&a.rs_sync[2 + g], (uint32_t)(hi - lo));
-    }
-    return true;
-}
-
-// the current front, advanced over the complete groups that follow it (warp-collective)
-template <typename T>
-__device__ __forceinline__ uint32_t ovl_front(const EvalArgs<T> &a, unsigned lane, uint32_t ngroups, uint64_t R) {
-    constexpr unsigned FULL = 0xffffffffu;
-    uint32_t f = 0;
-    if (lane == 0) f = ld_acquire(&a.rs_sync[1]);
-    f = __shfl_sync(FULL, f, 0);
-    const uint32_t f0 = f;
-    while (f < ngroups) {
-        const uint32_t g = f + lane;
-        const bool done = g < ngroups && ld_acquire(&a.rs_sync[2 + g]) == rs_need(R, g);
-        const uint32_t m = __ballot_sync(FULL, done);
-        const uint32_t c = m == FULL ? 32u : (uint32_t)(__ffs(~m) - 1);
-        f += c;
-        if (c < 32u) break;
-    }
-    __syncwarp();
-    if (lane == 0 && f > f0) atomicMax(&a.rs_sync[1], f);
-    return f;
-}
-
-// wait until red[0, end) is written, restructuring chunks meanwhile (warp-collective); `front` caches the
-// last front value seen.  A bounded spin: a broken invariant traps instead of hanging the GPU.
-template <typename T>
-__device__ __forceinline__ void ovl_wait(const EvalArgs<T> &a, unsigned lane, uint64_t end, uint32_t ngroups,
-                                         uint64_t R, uint32_t &front) {
-    uint32_t spins = 0;
-    while (!rs_covered(front, ngroups, end)) {
-        front = ovl_front(a, lane, ngroups, R);
-        if (rs_covered(front, ngroups, end)) break;
-        if (!ovl_help(a, lane)) {
-            __nanosleep(100);
-            if (++spins > (1u << 25)) __trap();
-        }
-    }
-}
 
 // image shift of stencil slot seen from box c (DESIGN C5)
 __device__ __forceinline__ double slot_shift(const Geom &g, const uint32_t c[3], int slot, int d) {
@@ -427,22 +310,8 @@ __device__ __forceinline__ double4 ldro(const double4 *p) {
     return make_double4(a.x, a.y, b.x, b.y);
 }
 
-// red[] loads of the small path: the read-only (non-coherent) path, except while red[] is being written by
-// the same kernel (OVL: L2-coherent loads)
-template <bool OVL>
-__device__ __forceinline__ float4 ldred(const float4 *p) { return OVL ? __ldcg(p) : __ldg(p); }
-template <bool OVL>
-__device__ __forceinline__ double4 ldred(const double4 *p) {
-    if (OVL) {
-        const double2 a = __ldcg(reinterpret_cast<const double2 *>(p)), b = __ldcg(reinterpret_cast<const double2 *>(p) + 1);
-        return make_double4(a.x, a.y, b.x, b.y);
-    }
-    return ldro(p);
-}
-
-template <typename T, int LAYOUT, bool OVL>
-__device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane, uint32_t ngroups, uint64_t R_all,
-                                            uint32_t &front) {
+template <typename T, int LAYOUT>
+__device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane) {
     using V4 = typename V4T<T>::type;
     const uint32_t n_small = *a.n_small;
     const T eps2 = (T)a.g.eps2;
@@ -452,16 +321,6 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane,
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= n_small) break;
         const uint32_t i = base + lane;
-        if constexpr (OVL) {  // the batch's runs end at most at the last lane's box's run end
-            unsigned long long end = 0;
-            if (i < n_small) end = a.red_off[a.small_box[i] + 1];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long y = __shfl_xor_sync(0xffffffffu, end, o);
-                end = y > end ? y : end;
-            }
-            ovl_wait(a, lane, end, ngroups, R_all, front);
-        }
         if (i < n_small) {
         // lane = a PAIR of targets of one small box (the second may not exist: b_end), so the pair math is the
         // same packed FP32x2 code as the item path (Tgt<T,2>), one broadcast source per step
@@ -496,15 +355,14 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane,
             // four loads in flight per lane (the path is L1/L2-latency bound, not FP32 bound)
 #pragma unroll 1
             for (; j + 4 <= R; j += 4) {
-                const V4 s0 = ldred<OVL>(run + j), s1 = ldred<OVL>(run + j + 1), s2 = ldred<OVL>(run + j + 2),
-                         s3 = ldred<OVL>(run + j + 3);
+                const V4 s0 = ldro(run + j), s1 = ldro(run + j + 1), s2 = ldro(run + j + 2), s3 = ldro(run + j + 3);
                 tg.interact(s0, E);
                 tg.interact(s1, E);
                 tg.interact(s2, E);
                 tg.interact(s3, E);
             }
 #pragma unroll 1
-            for (; j < R; ++j) tg.interact(ldred<OVL>(run + j), E);
+            for (; j < R; ++j) tg.interact(ldro(run + j), E);
         } else {
             const uint32_t e0 = a.nbr_off[b], e1 = a.nbr_off[b + 1];
             for (uint32_t e = e0; e < e1; ++e) {
@@ -552,7 +410,7 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane,
     }
 }
 
-template <typename T, int LAYOUT, int K, bool OVL>
+template <typename T, int LAYOUT, int K>
 __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P_REDUNDANT ? 5 : 4) : 1) k_eval_gravity(const EvalArgs<T> a) {
     using V4 = typename V4T<T>::type;
     constexpr int CH = EV_STAGE_BYTES / (int)sizeof(V4);
@@ -575,13 +433,6 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     const T eps2 = (T)a.g.eps2;
     const auto E = Tgt<T, K>::eps_pack(eps2);
     const uint32_t n_items = *a.n_items;
-    // OVL: groups of red[], the last front value seen, and an asynchronous refresh of it (one item ahead)
-    uint32_t ngroups = 0, front = 0, fr_pend = 0;
-    uint64_t R_all = 0;
-    if constexpr (OVL) {
-        R_all = a.ctr->R;
-        ngroups = (uint32_t)((R_all + (1ull << RS_GS) - 1) >> RS_GS);
-    }
 
     // ---------------- producer state (item whose chunks are being copied in) ----------------
     uint32_t p_box = 0, p_t0 = 0, p_meta = 0, p_key = 0, p_R = 0, p_nch = 0, p_tofs = 0;
@@ -651,8 +502,6 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
             mbar_arrive_expect_tx(&bar[s], (cnt + (chunk == 0 ? nt : 0u)) * (uint32_t)sizeof(V4));
         }
         __syncwarp();
-        // OVL: red[] was written by other warps through the generic proxy (made visible by ovl_wait)
-        if (OVL && chunk == 0 && (lane == 0 || lane == 31)) fence_proxy_async_global();
         if (LAYOUT == P2P_REDUNDANT) {
             if (lane == 0) bulk_g2s(dst, a.red + p_base + c0, cnt * (uint32_t)sizeof(V4), &bar[s]);
         } else {
@@ -670,14 +519,11 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     // CTA, so their latency hides behind the FP32-bound item work of the CTA's other warps (run last by all
     // warps, they would form a latency-bound tail)
     const bool small_first = w == EV_WARPS - 1;
-    if (small_first) small_phase<T, LAYOUT, OVL>(a, lane, ngroups, R_all, front);
+    if (small_first) small_phase<T, LAYOUT>(a, lane);
     if (lane == 0) pend = atomicAdd(a.item_head, (uint32_t)EV_BATCH);
     const uint32_t first = next_index();
-    // end of the prefetched item's run in red[] (REDUNDANT Item: red_base | R)
-    auto q_end = [&]() -> unsigned long long { return ((uint64_t)q1.x | ((uint64_t)q1.y << 32)) + q1.z; };
     if (first < n_items) {
     prefetch(first);
-    if constexpr (OVL) ovl_wait(a, lane, q_end(), ngroups, R_all, front);
     load_item();
     issue(0, 0);
     uint32_t nxt = next_index();
@@ -705,19 +551,6 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
         const uint32_t m20 = c_m20[S];
         const uint32_t g = (lane * m20) >> 20, sl = lane - g * S;
         const bool active = g < G;
-
-        // OVL: the next item's run (issued during this item's last chunk) must be written by then -- wait / help
-        // here, where no accumulators are live; then keep the front `ahead` groups further when possible
-        if constexpr (OVL) {
-            if (nxt < n_items) {
-                const uint32_t fp = __shfl_sync(FULL, fr_pend, 0);
-                front = fp > front ? fp : front;
-                const unsigned long long qe = q_end();
-                ovl_wait(a, lane, qe, ngroups, R_all, front);
-                if (!rs_covered(front, ngroups, qe + ((unsigned long long)a.ahead << RS_GS))) ovl_help(a, lane);
-            }
-            if (lane == 0) fr_pend = ld_vol(&a.rs_sync[1]);
-        }
 
         Tgt<T, K> tg;
         tg.zero();
@@ -876,17 +709,13 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     }
     }
     // the remaining small boxes' targets, if any (fills the tail of the item queue)
-    if (!small_first) small_phase<T, LAYOUT, OVL>(a, lane, ngroups, R_all, front);
-    // OVL: every chunk is claimed (and so written) before the kernel ends, whatever the item mix
-    if constexpr (OVL)
-        while (ovl_help(a, lane)) {
-        }
+    if (!small_first) small_phase<T, LAYOUT>(a, lane);
 }
 
-template <typename T, int LAYOUT, int K, bool OVL = false>
+template <typename T, int LAYOUT, int K>
 p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
     using V4 = typename V4T<T>::type;
-    auto kern = k_eval_gravity<T, LAYOUT, K, OVL>;
+    auto kern = k_eval_gravity<T, LAYOUT, K>;
     const int smem = EV_WARPS * 2 * (EV_STAGE_BYTES + EV_TGT * (int)sizeof(V4));
     if (P->eval_blocks[slot] == 0) {
         P2P_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -914,23 +743,6 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
     a.small_box = P->small_box;
     a.phi = (T *)phi;
     a.field = (T *)field;
-    a.rsp = rs_ptrs<T>(P);
-    a.ctr = P->ctr;
-    a.rs_sync = P->rs_sync;
-    a.exact32 = sizeof(T) == 4 && origins_exact_fp32(P->geom);
-    a.ahead = P->ovl_ahead;
-    if (OVL) {  // zero the chunk queue, the front and the group counters (sized for the buffer capacity)
-        const uint64_t ng = ((uint64_t)std::max<int64_t>(P->red_cap, 1) + (1ull << RS_GS) - 1) >> RS_GS;
-        if ((int64_t)(ng + 2) > P->rs_sync_cap) {
-            dfree(P->rs_sync, P->stream);
-            P->rs_sync = nullptr;
-            P->rs_sync_cap = 0;
-            P2P_CUDA_TRY(dalloc((void **)&P->rs_sync, 4 * (ng + 2), P->stream));
-            P->rs_sync_cap = (int64_t)(ng + 2);
-        }
-        a.rs_sync = P->rs_sync;
-        P2P_CUDA_TRY(cudaMemsetAsync(P->rs_sync, 0, 4 * (ng + 2), P->stream));
-    }
     const int64_t nit = P->sizes_known ? P->n_items + (P->n + 31) / 32 : P->cap;
     const unsigned grid =
         (unsigned)std::min<int64_t>(P->eval_blocks[slot], std::max<int64_t>(1, (nit + EV_WARPS - 1) / EV_WARPS));
@@ -942,12 +754,9 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
 }
 }  // namespace
 
-p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field, bool fused) {
+p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
     if (P->sizes_known && P->n == 0) return P2P_OK;
     const bool f64 = P->cfg.precision == P2P_FP64;
-    if (fused)  // p2p_restructure_eval: a6 inside the REDUNDANT eval kernel
-        return f64 ? launch<double, P2P_REDUNDANT, EVAL_K_F64, true>(P, phi, field, 3)
-                   : launch<float, P2P_REDUNDANT, EVAL_K_F32, true>(P, phi, field, 3);
     switch (layout) {
     case P2P_REDUNDANT:
         return f64 ? launch<double, P2P_REDUNDANT, EVAL_K_F64>(P, phi, field, 0)

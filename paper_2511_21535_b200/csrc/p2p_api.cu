@@ -98,11 +98,9 @@ static void free_plan_buffers(p2p_plan *P) {
     free_capacity(P);
     free_distributed(P);
     free_pairrec(P);
-    void *bufs[] = {P->red, P->table, P->tc_table, P->ctr, P->stage_in, P->stage_out, P->rs_sync};
+    void *bufs[] = {P->red, P->table, P->tc_table, P->ctr, P->stage_in, P->stage_out};
     for (void *b : bufs) dfree(b, st);
     P->red = P->table = P->tc_table = P->stage_in = P->stage_out = nullptr;
-    P->rs_sync = nullptr;
-    P->rs_sync_cap = 0;
     P->stage_in_cap = P->stage_out_cap = 0;
     P->ctr = nullptr;
 }
@@ -200,7 +198,6 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
     P->stream = (cudaStream_t)cfg->stream;
     cudaGetDevice(&P->device);
     cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device);
-    if (const char *e = getenv("P2P_OVL_AHEAD")) P->ovl_ahead = (uint32_t)atoi(e);  // tuning experiments only
     P->n = n_local;
     // geometry
     Geom &g = P->geom;
@@ -462,40 +459,6 @@ p2p_status p2p_restructure(p2p_plan *P) {
         return P2P_OK;
     }
     s = P->cfg.kernel == P2P_GRAVITY ? restructure_gravity(P) : restructure_helmholtz(P);
-    if (s == P2P_OK) P->red_valid = true;
-    return mark(P, s);
-}
-
-p2p_status p2p_restructure_eval(p2p_plan *P, void *potential, void *field) {
-    p2p_status s = enter(P);
-    if (s != P2P_OK) return s;
-    if (P->cfg.kernel != P2P_GRAVITY) {  // DBIM: the im2col gather and the GEMM stay two launches
-        if (field) return fail(P2P_ERR_INVALID_ARGUMENT, "helmholtz has no field output (pass NULL)");
-        if (P->n == 0) {
-            P->red_valid = true;
-            return P2P_OK;
-        }
-        if (!is_device_ptr(potential)) return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
-        s = restructure_helmholtz(P);
-        if (s != P2P_OK) return mark(P, s);
-        P->red_valid = true;
-        return mark(P, eval_helmholtz(P, P2P_REDUNDANT, potential));
-    }
-    if (P->comm) {  // collective: every rank calls, even with no particles
-        if (P->n_in > 0 && !is_device_ptr(potential))
-            return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
-        if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
-        s = eval_distributed(P, P2P_REDUNDANT, potential, field, true);
-        if (s == P2P_OK) P->red_valid = true;
-        return mark(P, s);
-    }
-    if (P->n == 0) {
-        P->red_valid = true;
-        return P2P_OK;
-    }
-    if (!is_device_ptr(potential)) return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
-    if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
-    s = eval_gravity(P, P2P_REDUNDANT, potential, field, true);
     if (s == P2P_OK) P->red_valid = true;
     return mark(P, s);
 }

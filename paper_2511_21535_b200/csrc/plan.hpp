@@ -119,11 +119,7 @@ struct p2p_plan {
     int64_t pr_records = 0, pr_targets = 0;
     bool pr_valid = false;
     p2p_status sticky = P2P_OK;
-    int eval_blocks[4] = {0, 0, 0, 0};  // persistent eval grid per layout (+ [3] the fused restructure+eval)
-    // p2p_restructure_eval synchronisation words: chunk queue head, front, per-group record counters
-    uint32_t *rs_sync = nullptr;
-    int64_t rs_sync_cap = 0;
-    uint32_t ovl_ahead = 2;  // groups (2^16 records) the restructure front should lead the eval by
+    int eval_blocks[3] = {0, 0, 0};
 };
 
 namespace p2p {
@@ -151,12 +147,11 @@ bool origins_exact_fp32(const Geom &g);  // every box origin fma(c, h, lo_d) is 
 p2p_status restructure_helmholtz(p2p_plan *P);
 
 // k_eval_gravity.cu / k_helmholtz.cu
-// fused = true: p2p_restructure_eval (a6 inside the REDUNDANT eval kernel, overlapped; layout ignored)
-p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field, bool fused = false);
+p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field);
 
 // k_dist.cu: the distributed (multi-GPU) plan build and result return
 p2p_status build_distributed(p2p_plan *P, const void *pos, const void *q);
-p2p_status eval_distributed(p2p_plan *P, p2p_layout layout, void *phi, void *field, bool fused = false);
+p2p_status eval_distributed(p2p_plan *P, p2p_layout layout, void *phi, void *field);
 void free_distributed(p2p_plan *P);
 p2p_status eval_helmholtz(p2p_plan *P, p2p_layout layout, void *y);
 p2p_status helmholtz_table(p2p_plan *P);

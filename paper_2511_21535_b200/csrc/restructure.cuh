@@ -1,6 +1,6 @@
-// restructure.cuh -- the a6 per-chunk restructure body (§1.1, §5.2.1; DESIGN C11), shared by the
-// standalone k_restructure_gravity (k_restructure.cu) and the fused restructure+eval kernel
-// (k_eval_gravity.cu, p2p_restructure_eval), so both write red[] with the same code, bit for bit.
+// restructure.cuh -- the a6 per-chunk restructure body (§1.1, §5.2.1; DESIGN C11) of
+// k_restructure_gravity (k_restructure.cu), kept callable from other kernels (the round-1 fused
+// restructure+eval experiment, ran it inside the eval kernel).
 //
 // A chunk = 32 consecutive CSR entries e = 32 ch .. 32 ch + 31.  Their source segments are consecutive in red[]
 // (CSR order = run order, runs of consecutive boxes are adjacent): one contiguous output range starting at

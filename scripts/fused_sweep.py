@@ -1,6 +1,7 @@
 """Time p2p_restructure_eval against p2p_restructure + p2p_eval(REDUNDANT) and p2p_eval(INDEXED) on one
 workload, for several lookahead settings (P2P_OVL_AHEAD, groups of 2^16 records).  CUDA events on the plan
 stream, L2 flushed (512 MB write) before every launch, median of 7.  Prints one JSON line per setting.
+(needs the p2p_restructure_eval experiment of commit 95157da.)
 usage: python scripts/fused_sweep.py [workload] [ahead,ahead,...]"""
 import json
 import os
