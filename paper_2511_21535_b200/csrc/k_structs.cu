@@ -13,19 +13,24 @@
 namespace p2p {
 
 // ------------------------------------------------------------------------------------------------
-// eval work items: a box's targets are split into ceil(n_b / ITEM_TMAX) chunks, more if the chunk cost
-// n_t * R_b exceeds ITEM_COSTCAP interactions (bounds the tail of the dynamic work queue on clustered
-// inputs).  Chunks are balanced: chunk c = [n_b c / nch, n_b (c+1) / nch).
-// ITEM_TMAX (plan.hpp): at most 32 targets per item -> G <= 8 groups of K = 4 (fp32), >= 28 busy lanes
+// eval work items: a box's targets are split into chunks of at most ITEM_TMAX targets, more chunks if the chunk cost
+// n_t * R_b exceeds ITEM_COSTCAP interactions (bounds the tail of the dynamic work queue on clustered inputs).
+// Chunk sizes are chosen for the eval's lane layout (G = ceil(n_t / 4) groups of 4 targets x S = floor(32 / G)
+// source splits): every chunk but the box's last has ITEM_TMAX targets, or -- when the cost cap binds -- the
+// largest of 24, 20, 16, 12, 8, 4 targets not above the capped balanced size (G * S = 30 or 32 busy lanes); the
+// earlier balanced chunks (e.g. 25 + 25 targets: 28 lanes, 25 of 28 target slots) left up to 22% of the
+// lane-slots idle (c5w eval 6.60 -> 6.16 ms).
+// ITEM_TMAX (plan.hpp): at most 32 targets per item -> G <= 8 groups of K = 4 (fp32)
 constexpr uint64_t ITEM_COSTCAP = 1ull << 17;
 
-__device__ __forceinline__ uint32_t item_chunks(uint32_t nb_b, uint64_t nsrc, uint32_t tmax) {
-    uint64_t a = (nb_b + tmax - 1) / tmax;
-    uint64_t c = ((uint64_t)nb_b * nsrc + ITEM_COSTCAP - 1) / ITEM_COSTCAP;
-    uint64_t m = a > c ? a : c;
-    if (m > nb_b) m = nb_b;
-    if (m < 1) m = 1;
-    return (uint32_t)m;
+// targets per item of a box with nb_b targets and nsrc sources (its items: ceil(nb_b / size))
+__device__ __forceinline__ uint32_t item_size(uint32_t nb_b, uint64_t nsrc, uint32_t tmax) {
+    const uint64_t a = (nb_b + tmax - 1) / tmax;
+    const uint64_t c = ((uint64_t)nb_b * nsrc + ITEM_COSTCAP - 1) / ITEM_COSTCAP;
+    if (c <= a) return tmax;
+    const uint32_t ts = (uint32_t)(nb_b / c);  // balanced chunk size under the cap
+    if (ts < 4) return ts > 1 ? ts : 1u;
+    return ts >= 24 ? 24u : ts >= 20 ? 20u : ts >= 16 ? 16u : ts >= 12 ? 12u : ts >= 8 ? 8u : 4u;
 }
 
 // ------------------------------------------------------------------------------------------------ a1
@@ -233,7 +238,7 @@ __device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint
     t.red = red;
     // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
     const bool small = nb <= SMALL_NT && red <= SMALL_R;
-    t.item = (small || !tgt) ? 0u : item_chunks(nb, red, tmax);
+    t.item = (small || !tgt) ? 0u : (nb + item_size(nb, red, tmax) - 1) / item_size(nb, red, tmax);
     t.small = (small && tgt) ? (nb + 1) / 2 : 0u;  // target PAIRS
     return t;
 }
@@ -474,10 +479,9 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
                     small_box[so + j] = b;
                 }
             } else {
-                const uint32_t nch = x.item;
+                const uint32_t nch = x.item, sz = item_size(nb, red, tmax);
                 for (uint32_t ci = 0; ci < nch; ++ci) {
-                    const uint32_t a0 = (uint32_t)(((uint64_t)nb * ci) / nch);
-                    const uint32_t z0 = (uint32_t)(((uint64_t)nb * (ci + 1)) / nch);
+                    const uint32_t a0 = ci * sz, z0 = min(nb, (ci + 1) * sz);
                     // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
                     const uint32_t nt = z0 - a0, Gq = (nt + K - 1) / K, Sq = 32u / Gq;
                     items[it + ci] = Item{b, s0 + a0, nt | (Sq << 8) | (Gq << 16), key, rb, (uint32_t)red, cen + a0};
