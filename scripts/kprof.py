@@ -21,7 +21,9 @@ pos = torch.from_numpy(inp.pos).cuda()
 m = torch.from_numpy(inp.mass).cuda()
 phi = torch.empty(inp.n, device="cuda")
 field = torch.empty((inp.n, 3), device="cuda")
-plan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps)
+# P2P_KPROF_COMM=1: the collective (multi-GPU) plan path with a 1-rank NCCL communicator
+comm = P.p2p_comm_create(1, 0, P.p2p_comm_unique_id()) if os.environ.get("P2P_KPROF_COMM") else None
+plan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps, comm=comm)
 
 
 def step():
@@ -49,3 +51,5 @@ for name, v in acc.items():
     print(f"{per:9.1f} us/step  x{len(v) // K:<3d} {name}")
 print(f"{tot:9.1f} us/step  total ({wl}, {K} steps)")
 plan.close()
+if comm is not None:
+    P.p2p_comm_destroy(comm)

@@ -87,7 +87,7 @@ def expected_splitters(P, cat, key_bits, nr):
 
 
 @pytest.mark.parametrize("case", ["plummer_g2", "plummer_g3", "uniform_g4", "open_g2", "skewed_g4", "fp64_g2",
-                                  "plummer64_g8", "plummer128_g5", "uniform_g7"])
+                                  "plummer64_g8", "plummer128_g5", "uniform_g7", "clump_g6"])
 def test_multirank_bitwise_equals_single_gpu(P, case):
     rng = np.random.default_rng(17)
     if case.startswith("plummer"):
@@ -104,6 +104,11 @@ def test_multirank_bitwise_equals_single_gpu(P, case):
         inp = G.plummer(40000, 128, seed=11)    # 21-bit keys: supercells of 8 boxes
     elif case == "uniform_g7":
         inp = G.uniform_per_box(12, 2, seed=12)
+    elif case == "clump_g6":   # one box holds 90% of the particles: several splitters fall in one supercell
+        r2 = np.random.default_rng(13)
+        pts = np.concatenate([r2.random((400, 3)), 0.52 + 0.1 * r2.random((3600, 3))]).astype(np.float32)
+        inp = G.GravityInput(pts, (0.5 + r2.random(4000)).astype(np.float32) / 4000, (0.0, 0.0, 0.0), 0.125,
+                             (8, 8, 8), 0b111, 1e-3)
     else:
         inp = G.plummer(20000, 16, seed=9)
     nr = int(case[-1])
