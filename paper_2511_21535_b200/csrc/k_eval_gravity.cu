@@ -47,7 +47,10 @@ template <> struct V4T<double> { using type = double4; };
 constexpr int EV_WARPS = 4;              // warps per CTA
 constexpr int EV_STAGE_BYTES = 4096;     // source records per pipeline stage per warp (256 fp32 / 128 fp64)
 constexpr int EV_TGT = 32;               // max targets per item (ITEM_TMAX in k_structs.cu)
-constexpr int EV_BATCH = 2;              // work items claimed per queue atomic
+#ifndef P2P_EV_BATCH
+#define P2P_EV_BATCH 2
+#endif
+constexpr int EV_BATCH = P2P_EV_BATCH;   // work items claimed per queue atomic
 
 // ceil(2^20 / S) for S = 0..32: x / S == (x * M20[S]) >> 20 exactly for x < 2^11 (no integer division)
 __constant__ uint32_t c_m20[33] = {0,       1048576, 524288, 349526, 262144, 209716, 174763, 149797, 131072,
@@ -551,6 +554,11 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
         const uint32_t m20 = c_m20[S];
         const uint32_t g = (lane * m20) >> 20, sl = lane - g * S;
         const bool active = g < G;
+        // a9: the output slots of the lane's K targets, loaded now and used in the epilogue (the load latency
+        // was exposed there on small items: c4-8)
+        uint32_t pidx[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) pidx[k] = (active && g * K + k < nt) ? __ldg(a.perm + c_t0 + g * K + k) : 0u;
 
         Tgt<T, K> tg;
         tg.zero();
@@ -674,7 +682,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t f = f0 + j, q = f >> 2, k = f & 3u, ti = g * K + k;
                     if ((uint32_t)j < vcnt && ti < nt) {
-                        const uint32_t i = a.perm[c_t0 + ti];
+                        const uint32_t i = k == 0 ? pidx[0] : (k == 1 ? pidx[1] : (k == 2 ? pidx[2] : pidx[K - 1]));
                         if (q == 0) {
                             const T mk = k == 0 ? tm[0] : (k == 1 ? tm[1] : (k == 2 ? tm[2] : tm[3]));
                             a.phi[i] = -(v[j] - mk * rs);
@@ -692,7 +700,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
             for (int k = 0; k < K; ++k) {
                 const uint32_t ti = g * K + k;
                 if (ti < nt) {
-                    const uint32_t i = a.perm[c_t0 + ti];
+                    const uint32_t i = pidx[k];
                     T pot, fx, fy, fz;
                     tg.get(k, pot, fx, fy, fz);
                     a.phi[i] = -(pot - tm[k] * rs);
