@@ -46,8 +46,14 @@ constexpr int EVAL_K_F64 = 2;
 constexpr uint32_t ITEM_TMAX = 32;  // max targets per work item (lane utilisation)
 // boxes with <= SMALL_NT targets and <= SMALL_R sources take the eval's thread-per-target path (no work item):
 // their per-item overhead would exceed their work, and their runs are short enough for L1-latency-bound loads
-constexpr uint32_t SMALL_NT = 8;
-constexpr uint32_t SMALL_R = 128;
+#ifndef P2P_SMALL_NT
+#define P2P_SMALL_NT 8
+#endif
+#ifndef P2P_SMALL_R
+#define P2P_SMALL_R 128
+#endif
+constexpr uint32_t SMALL_NT = P2P_SMALL_NT;
+constexpr uint32_t SMALL_R = P2P_SMALL_R;
 
 // gravity geometry passed by value to kernels
 struct Geom {
