@@ -16,7 +16,7 @@
 // Bound: HBM -- writes 16 R bytes (fp32), reads 16 N_src bytes compulsory (repeats hit L2 in Morton order).
 //
 // Helmholtz: Xg[b][s][j] = xs[bstart[nbr9[b][s]] + j] or 0 (zero-padded im2col, DESIGN C10), one thread
-// per element, fully coalesced.
+// per 16-byte vector (per element when a row of t complex values is not a 16-byte multiple), fully coalesced.
 #include <cmath>
 
 #include "plan.hpp"
@@ -73,6 +73,25 @@ __global__ void k_restructure_helmholtz(const C2 *__restrict__ xs, const uint32_
         Xg[i] = v;
     }
 }
+
+// the same im2col with 16-byte vectors: thread per 16 B of Xg (rows of t complex values are 16-byte multiples when
+// t * sizeof(C2) is; the lattice is regular, so bstart[k] = k t and the source rows are 16-byte aligned too);
+// 32-bit indexing, a shift instead of the 64-bit division per element (c2b 0.142 -> 0.088 ms, c2a 0.044 -> 0.031)
+template <bool POW2>
+__global__ void __launch_bounds__(256) k_restructure_helmholtz_v(const uint4 *__restrict__ xs, uint32_t esz,
+                                                                 const uint32_t *__restrict__ bstart,
+                                                                 const uint32_t *__restrict__ nbr9, uint32_t rows,
+                                                                 uint32_t n16, uint32_t sh, uint4 *__restrict__ Xg) {
+    const uint32_t total = rows * n16;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < total; v += gridDim.x * blockDim.x) {
+        const uint32_t row = POW2 ? v >> sh : v / n16;
+        const uint32_t j = v - row * n16;
+        const uint32_t k = __ldg(nbr9 + row);
+        uint4 x = make_uint4(0u, 0u, 0u, 0u);  // missing neighbour: +0.0 real and imaginary (C10)
+        if (k != 0xffffffffu) x = __ldg(xs + (size_t)__ldg(bstart + k) * esz / 16u + j);
+        Xg[v] = x;
+    }
+}
 }  // namespace
 
 // every box origin o_d = fma(c, h, lo_d), c < nbox_d, is exactly an fp32 value (the restructure's fp32 path)
@@ -104,6 +123,22 @@ p2p_status restructure_helmholtz(p2p_plan *P) {
     if (P->B == 0) return P2P_OK;
     const uint32_t t = (uint32_t)P->cfg.points_per_box;
     const uint64_t total = (uint64_t)P->B * 9 * t;
+    const uint32_t esz = P->cfg.precision == P2P_FP64 ? 16u : 8u;
+    const uint64_t rows = (uint64_t)P->B * 9;
+    if ((t * esz) % 16 == 0 && rows * (t * esz / 16) < (1ull << 32)) {
+        const uint32_t n16 = t * esz / 16;
+        const bool pow2 = (n16 & (n16 - 1)) == 0;
+        const uint32_t sh = pow2 ? (uint32_t)__builtin_ctz(n16) : 0u;
+        const unsigned g16 = std::min<unsigned>(div_up(rows * n16, 256), (unsigned)P->num_sms * 16);
+        if (pow2)
+            P2P_LAUNCH(k_restructure_helmholtz_v<true>, g16, 256, 0, P->stream, (const uint4 *)P->rec, esz, P->bstart,
+                       P->nbr_box, (uint32_t)rows, n16, sh, (uint4 *)P->red);
+        else
+            P2P_LAUNCH(k_restructure_helmholtz_v<false>, g16, 256, 0, P->stream, (const uint4 *)P->rec, esz,
+                       P->bstart, P->nbr_box, (uint32_t)rows, n16, sh, (uint4 *)P->red);
+        P2P_CUDA_TRY(cudaGetLastError());
+        return P2P_OK;
+    }
     const unsigned grid = std::min<unsigned>(div_up(total, 256), (unsigned)P->num_sms * 16);
     if (P->cfg.precision == P2P_FP64)
         P2P_LAUNCH(k_restructure_helmholtz<double2>, grid, 256, 0, P->stream, (const double2 *)P->rec, P->bstart,
