@@ -75,6 +75,7 @@ struct EvalArgs {
     const uint32_t *small_tgt, *small_box;
     T *phi;
     T *field;
+    uint32_t zero;             // always 0 (see queue_claim)
 };
 
 // image shift of stencil slot seen from box c (DESIGN C5)
@@ -91,6 +92,17 @@ __device__ __forceinline__ double slot_shift(const Geom &g, const uint32_t c[3],
 // (Sterbenz), see DESIGN §5.
 __device__ __forceinline__ double frame_shift(const Geom &g, const uint32_t c[3], int d) {
     return (((g.periodic >> d) & 1u) && (int)c[d] == g.nbox[d] - 1) ? -g.L[d] : 0.0;
+}
+
+// one lane claims `n` work items.  ptxas turns an atomic on a warp-uniform address into a warp-aggregated one
+// whose result it broadcasts at once -- a wait for the atomic's round trip that the batch prefetch is meant to
+// hide.  The address is made lane-dependent for the compiler by a runtime zero (EvalArgs::zero = 0):
+// head + (laneid & zero) == head.
+__device__ __forceinline__ uint32_t queue_claim(unsigned int *head, uint32_t n, uint32_t zero) {
+    uint32_t lid, r;
+    asm("mov.u32 %0, %%laneid;" : "=r"(lid));
+    asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(head + (lid & zero)), "r"(n) : "memory");
+    return r;
 }
 
 // ---- per-lane target block + accumulators --------------------------------------------------------
@@ -452,17 +464,17 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
         if (nb_left == 0) {
             nb_idx = __shfl_sync(FULL, pend, 0);
             nb_left = EV_BATCH;
-            if (lane == 0) pend = atomicAdd(a.item_head, (uint32_t)EV_BATCH);
+            if (lane == 0) pend = queue_claim(a.item_head, (uint32_t)EV_BATCH, a.zero);
         }
         --nb_left;
         return nb_idx++;
     };
+    // unconditional (index clamped; only called with n_items >= 1): a predicated load made the compiler copy the
+    // prefetched registers right away (a predicated MOV on the load result), stalling on the load it was hiding
     auto prefetch = [&](uint32_t idx) {
-        if (idx < n_items) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(a.items + idx);
-            q0 = __ldg(src);
-            q1 = __ldg(src + 1);
-        }
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.items + min(idx, n_items - 1u));
+        q0 = __ldg(src);
+        q1 = __ldg(src + 1);
     };
     auto load_item = [&]() {
         p_box = q0.x;
@@ -523,7 +535,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     // warps, they would form a latency-bound tail)
     const bool small_first = w == EV_WARPS - 1;
     if (small_first) small_phase<T, LAYOUT>(a, lane);
-    if (lane == 0) pend = atomicAdd(a.item_head, (uint32_t)EV_BATCH);
+    if (lane == 0) pend = queue_claim(a.item_head, (uint32_t)EV_BATCH, a.zero);
     const uint32_t first = next_index();
     if (first < n_items) {
     prefetch(first);
@@ -751,6 +763,7 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
     a.small_box = P->small_box;
     a.phi = (T *)phi;
     a.field = (T *)field;
+    a.zero = 0u;
     const int64_t nit = P->sizes_known ? P->n_items + (P->n + 31) / 32 : P->cap;
     const unsigned grid =
         (unsigned)std::min<int64_t>(P->eval_blocks[slot], std::max<int64_t>(1, (nit + EV_WARPS - 1) / EV_WARPS));
