@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[EV_WARPS][2];
+    __shared__ __align__(16) uint4 qslot[EV_WARPS][2];  // the warp's next Item record (cp.async prefetch)
 
     const int w = threadIdx.x >> 5;
     const unsigned lane = threadIdx.x & 31u;
@@ -456,10 +457,12 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
 
     // work-queue pipeline: each atomicAdd claims EV_BATCH consecutive items (fewer atomics on the one queue
     // counter) and its result is consumed by shfl a whole batch later; item n+1's 32-byte Item record is already
-    // in registers when its first chunk is issued -- no dependent load on the per-item critical path (REDUNDANT)
+    // in shared memory when its first chunk is issued -- no dependent load on the per-item critical path
+    // (REDUNDANT).  Build option P2P_ITEM_SMEM: the record goes through cp.async into a per-warp shared slot instead
+    // of registers (the compiler copies the 128-bit register loads into the loop-carried registers at once, waiting
+    // for them): c4-8 eval -4.4%, c5w +0.5% (profiles/r01_item_prefetch.txt), so registers stay the default.
     uint32_t pend = 0;  // lane 0: result of the last issued atomicAdd
     uint32_t nb_idx = 0, nb_left = 0;
-    uint4 q0 = make_uint4(0, 0, 0, 0), q1 = make_uint4(0, 0, 0, 0);  // prefetched raw Item
     auto next_index = [&]() -> uint32_t {
         if (nb_left == 0) {
             nb_idx = __shfl_sync(FULL, pend, 0);
@@ -471,12 +474,27 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     };
     // unconditional (index clamped; only called with n_items >= 1): a predicated load made the compiler copy the
     // prefetched registers right away (a predicated MOV on the load result), stalling on the load it was hiding
+#ifndef P2P_ITEM_SMEM
+    uint4 q0 = make_uint4(0, 0, 0, 0), q1 = make_uint4(0, 0, 0, 0);
     auto prefetch = [&](uint32_t idx) {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.items + min(idx, n_items - 1u));
         q0 = __ldg(src);
         q1 = __ldg(src + 1);
     };
     auto load_item = [&]() {
+#else
+    auto prefetch = [&](uint32_t idx) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.items + min(idx, n_items - 1u));
+        if (lane < 2)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&qslot[w][lane])), "l"(src + lane)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto load_item = [&]() {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        const uint4 q0 = qslot[w][0], q1 = qslot[w][1];
+#endif
         p_box = q0.x;
         p_t0 = q0.y;
         p_meta = q0.z;
