@@ -153,6 +153,20 @@ p2p_status p2p_restructure_pairs(p2p_plan *plan);
 /* records (T + R) and partial-result slots (T) of the current pair-record buffer (BAD_STATE if not built) */
 p2p_status p2p_get_pairrec_size(const p2p_plan *plan, int64_t *records, int64_t *partials);
 
+/* SURVEY NEXT-1, first GPU step: the adaptive binary-tree leaves of the plan's particles (DESIGN C22; "an
+ * irregular binary MLFMA tree", P:L330 clustering threshold): longest-axis midpoint splits with ties z, y, x, so
+ * a cell is an l-bit prefix of the finest Morton key; a cell splits while it holds more than t particles or while
+ * l < min_bits (9 keeps periodic images unique for the adjacency of the next step); finest cells are leaves
+ * whatever their count.  Computed on the device from the sorted box table; leaves in Morton order, each one
+ * contiguous run of the sorted particles.
+ *   len_out[L], prefix_out[L], start_out[L] : host, u32 -- prefix length l, the l-bit prefix, the leaf's first
+ *                                              sorted particle (its count = next start or n_local minus start)
+ *   capacity : entries the outputs hold (n_boxes always suffices);  *n_leaves : L
+ * Gravity single-GPU plans on a periodic cube of 2^m boxes per dimension (else P2P_ERR_UNSUPPORTED); t >= 1.
+ * Synchronous (one stream synchronisation); the plan is unchanged. */
+p2p_status p2p_adaptive_leaves(p2p_plan *plan, int32_t t, int32_t min_bits, uint32_t *len_out, uint32_t *prefix_out,
+                               uint32_t *start_out, int64_t capacity, int64_t *n_leaves);
+
 /* a7/a8 + a9: evaluate every target and scatter to input order.
  *   potential : device, gravity [n_local] real; helmholtz [n_local] complex (re, im)
  *   field     : device, gravity [n_local][3] real (the acceleration, C1) or NULL; helmholtz: must be NULL

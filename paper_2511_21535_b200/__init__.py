@@ -33,7 +33,7 @@ P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE, P2P_PAIRREC = 0, 1, 2, 3
 LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise": P2P_INDEXED_BITWISE}
 
 EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure",
-            "p2p_restructure_pairs", "p2p_get_pairrec_size", "p2p_eval",
+            "p2p_restructure_pairs", "p2p_get_pairrec_size", "p2p_adaptive_leaves", "p2p_eval",
             "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
             "p2p_partition_splitters", "p2p_get_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
@@ -79,6 +79,7 @@ def lib() -> C.CDLL:
             "p2p_eval_host": (C.c_int, [p, C.c_int, p, p]),
             "p2p_restructure": (C.c_int, [p]),
             "p2p_restructure_pairs": (C.c_int, [p]),
+            "p2p_adaptive_leaves": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, C.POINTER(C.c_int64)]),
             "p2p_get_pairrec_size": (C.c_int, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "p2p_eval": (C.c_int, [p, C.c_int, p, p]),
             "p2p_set_charges": (C.c_int, [p, p]),
@@ -156,6 +157,18 @@ def p2p_eval_host(plan: int, layout: int, potential_host: int, field_host: int |
 
 def p2p_restructure(plan: int):
     _check(lib().p2p_restructure(C.c_void_p(plan)))
+
+
+def p2p_adaptive_leaves(plan: int, t: int, min_bits: int, capacity: int):
+    """(prefix length, prefix, first sorted particle) of every adaptive leaf, Morton order"""
+    cap = max(int(capacity), 1)
+    ln, px, st = np.empty(cap, np.uint32), np.empty(cap, np.uint32), np.empty(cap, np.uint32)
+    nl = C.c_int64()
+    _check(lib().p2p_adaptive_leaves(C.c_void_p(plan), int(t), int(min_bits), ln.ctypes.data_as(C.c_void_p),
+                                     px.ctypes.data_as(C.c_void_p), st.ctypes.data_as(C.c_void_p), cap,
+                                     C.byref(nl)))
+    n = int(nl.value)
+    return ln[:n].copy(), px[:n].copy(), st[:n].copy()
 
 
 def p2p_restructure_pairs(plan: int):

@@ -473,6 +473,22 @@ p2p_status p2p_restructure_pairs(p2p_plan *P) {
     return mark(P, restructure_pairs(P));
 }
 
+p2p_status p2p_adaptive_leaves(p2p_plan *P, int32_t t, int32_t min_bits, uint32_t *len_out, uint32_t *prefix_out,
+                               uint32_t *start_out, int64_t capacity, int64_t *n_leaves) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (!len_out || !prefix_out || !start_out || !n_leaves || t < 1 || min_bits < 0 || capacity < 0)
+        return fail(P2P_ERR_INVALID_ARGUMENT, "adaptive leaves: NULL output, t < 1, min_bits < 0 or capacity < 0");
+    if (P->cfg.kernel != P2P_GRAVITY || P->comm)
+        return fail(P2P_ERR_UNSUPPORTED, "adaptive leaves are for single-GPU gravity plans");
+    const int32_t n0 = P->cfg.nbox[0];
+    if (P->cfg.nbox[1] != n0 || P->cfg.nbox[2] != n0 || (n0 & (n0 - 1)) != 0 || P->cfg.periodic_mask != 7u)
+        return fail(P2P_ERR_UNSUPPORTED, "adaptive leaves need a periodic cube of 2^m boxes per dimension (C22)");
+    s = resolve_sizes(P);
+    if (s != P2P_OK) return s;
+    return mark(P, adaptive_leaves(P, (uint32_t)t, min_bits, len_out, prefix_out, start_out, capacity, n_leaves));
+}
+
 p2p_status p2p_get_pairrec_size(const p2p_plan *P, int64_t *records, int64_t *partials) {
     if (!P || !records || !partials) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
     if (!P->pr_valid) return fail(P2P_ERR_BAD_STATE, "pair records are not built (call p2p_restructure_pairs)");

@@ -112,7 +112,10 @@ __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint3
     const float f0o = (float)o0, f1o = (float)o1, f2o = (float)o2;
     const bool fast32 = EXACT32 && !wrap;
     const double L0 = g.L[0], L1 = g.L[1], L2 = g.L[2];
-    constexpr int UNR = 4;
+#ifndef P2P_RS_UNR
+#define P2P_RS_UNR 4
+#endif
+    constexpr int UNR = P2P_RS_UNR;
     for (uint32_t rb = 0; rb < Rc; rb += 32 * UNR) {
         V4 x[UNR];
         uint32_t xe[UNR];

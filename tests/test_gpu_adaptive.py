@@ -1,0 +1,66 @@
+"""SURVEY NEXT-1, first GPU step (-m gpu): the adaptive binary-tree leaves (DESIGN C22) computed on the device by
+p2p_adaptive_leaves equal the pinned oracle's (oracle/adaptive.py) bit for bit -- prefix length, prefix and the
+first sorted particle of every leaf, in Morton order -- on clustered and uniform inputs, for several clustering
+thresholds, after p2p_plan_update too; plans that are not a periodic 2^m cube are rejected."""
+import numpy as np
+import pytest
+
+import p2p_inputs as G
+from oracle import adaptive as A
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2511_21535_b200 as P
+    return P
+
+
+def _plan(P, inp):
+    pos = torch.from_numpy(inp.pos).cuda()
+    m = torch.from_numpy(inp.mass).cuda()
+    return P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps)
+
+
+def _check(P, plan, inp, t, min_bits=9):
+    ln, px, st = P.p2p_adaptive_leaves(plan.handle, t, min_bits, plan.info.n_boxes)
+    tr = A.AdaptiveTree(inp, t, min_bits)
+    want = np.array([(l, p, s) for l, p, s, _ in tr.leaves], dtype=np.int64).reshape(-1, 3)
+    got = np.stack([ln, px, st], axis=1).astype(np.int64)
+    assert got.shape == want.shape and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("t", [1, 4, 16, 64, 1000])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_plummer(P, t, dtype):
+    inp = G.plummer(20000, 32, seed=2, dtype=dtype)
+    with _plan(P, inp) as plan:
+        _check(P, plan, inp, t)
+
+
+def test_uniform_and_min_bits(P):
+    inp = G.uniform_per_box(16, 3, seed=4)
+    with _plan(P, inp) as plan:
+        _check(P, plan, inp, 3)              # every finest box its own leaf
+        _check(P, plan, inp, 24, 0)          # 8 boxes per leaf from the root down
+        _check(P, plan, inp, 10**6, 0)       # the root alone
+
+
+def test_after_update_and_large(P):
+    a = G.plummer(5000, 64, seed=5)
+    b = G.plummer(300000, 64, seed=6)
+    with _plan(P, a) as plan:
+        plan.update(torch.from_numpy(b.pos).cuda(), torch.from_numpy(b.mass).cuda())
+        plan.refresh_info()
+        _check(P, plan, b, 8)
+
+
+def test_rejects_non_cube(P):
+    inp = G.random_gravity(2000, 0, seed=1, periodic=0b111, nbox=(8, 8, 6), h=0.125)
+    with _plan(P, inp) as plan:
+        with pytest.raises(P.P2PError):
+            P.p2p_adaptive_leaves(plan.handle, 4, 9, plan.info.n_boxes)
