@@ -167,6 +167,17 @@ p2p_status p2p_get_pairrec_size(const p2p_plan *plan, int64_t *records, int64_t 
 p2p_status p2p_adaptive_leaves(p2p_plan *plan, int32_t t, int32_t min_bits, uint32_t *len_out, uint32_t *prefix_out,
                                uint32_t *start_out, int64_t capacity, int64_t *n_leaves);
 
+/* SURVEY NEXT-1, second GPU step: the closed neighbour lists of the adaptive leaves (DESIGN C23: B + S overlaps the
+ * target leaf dilated by its own extent, then symmetric closure), built on the device by range lookups in the
+ * Morton-ordered leaf table.  CSR over the leaves of p2p_adaptive_leaves(t, min_bits):
+ *   off_out[L + 1] (u32), nbr_out[E] (u32 leaf index), code_out[E] (u8 image code 9(s_z+1)+3(s_y+1)+(s_x+1),
+ *   S_d = +1 when the neighbour wraps past the upper face, C5); entries of a leaf in ascending (leaf, code) order.
+ * min_bits >= 9 (unique periodic images); a periodic cube of 2^m >= 8 boxes per dimension; capacities in entries
+ * (else P2P_ERR_INVALID_ARGUMENT, the counts are still returned).  Synchronous; the plan is unchanged. */
+p2p_status p2p_adaptive_neighbours(p2p_plan *plan, int32_t t, int32_t min_bits, uint32_t *off_out, uint32_t *nbr_out,
+                                   uint8_t *code_out, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
+                                   int64_t *n_entries);
+
 /* a7/a8 + a9: evaluate every target and scatter to input order.
  *   potential : device, gravity [n_local] real; helmholtz [n_local] complex (re, im)
  *   field     : device, gravity [n_local][3] real (the acceleration, C1) or NULL; helmholtz: must be NULL

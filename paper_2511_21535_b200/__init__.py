@@ -33,7 +33,8 @@ P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE, P2P_PAIRREC = 0, 1, 2, 3
 LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise": P2P_INDEXED_BITWISE}
 
 EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure",
-            "p2p_restructure_pairs", "p2p_get_pairrec_size", "p2p_adaptive_leaves", "p2p_eval",
+            "p2p_restructure_pairs", "p2p_get_pairrec_size", "p2p_adaptive_leaves", "p2p_adaptive_neighbours",
+            "p2p_eval",
             "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
             "p2p_partition_splitters", "p2p_get_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
@@ -80,6 +81,8 @@ def lib() -> C.CDLL:
             "p2p_restructure": (C.c_int, [p]),
             "p2p_restructure_pairs": (C.c_int, [p]),
             "p2p_adaptive_leaves": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, C.POINTER(C.c_int64)]),
+            "p2p_adaptive_neighbours": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, i64, C.POINTER(C.c_int64),
+                                                  C.POINTER(C.c_int64)]),
             "p2p_get_pairrec_size": (C.c_int, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "p2p_eval": (C.c_int, [p, C.c_int, p, p]),
             "p2p_set_charges": (C.c_int, [p, p]),
@@ -169,6 +172,19 @@ def p2p_adaptive_leaves(plan: int, t: int, min_bits: int, capacity: int):
                                      C.byref(nl)))
     n = int(nl.value)
     return ln[:n].copy(), px[:n].copy(), st[:n].copy()
+
+
+def p2p_adaptive_neighbours(plan: int, t: int, min_bits: int, cap_leaves: int, cap_entries: int):
+    """closed neighbour CSR of the adaptive leaves: (off[L + 1], leaf[E], image code[E])"""
+    off = np.empty(max(int(cap_leaves), 1), np.uint32)
+    nbr = np.empty(max(int(cap_entries), 1), np.uint32)
+    code = np.empty(max(int(cap_entries), 1), np.uint8)
+    nl, ne = C.c_int64(), C.c_int64()
+    _check(lib().p2p_adaptive_neighbours(C.c_void_p(plan), int(t), int(min_bits), off.ctypes.data_as(C.c_void_p),
+                                         nbr.ctypes.data_as(C.c_void_p), code.ctypes.data_as(C.c_void_p),
+                                         off.size, nbr.size, C.byref(nl), C.byref(ne)))
+    L, E = int(nl.value), int(ne.value)
+    return off[:L + 1].copy(), nbr[:E].copy(), code[:E].copy()
 
 
 def p2p_restructure_pairs(plan: int):

@@ -8,6 +8,8 @@
 // l >= min_bits whose cell holds <= t particles (counts are non-increasing in l: a binary search over l, each count
 // two binary searches over the box keys), and the leaves are the runs of consecutive boxes sharing (l, prefix):
 // a head-flag scan (scan.cuh) numbers them in Morton order.  Every leaf is one contiguous run of the sorted records.
+#include <vector>
+
 #include "plan.hpp"
 #include "scan.cuh"
 
@@ -73,6 +75,165 @@ struct LeafHeadPut {
         }
     }
 };
+
+// ---- C23 adjacency (dilation by the target leaf's extent + symmetric closure), the range construction pinned
+// ---- against the O(L^2) definition by tests/test_oracle_adaptive.py:
+//   nbr(B) = {leaves of prefix length >= l_B inside B's 27 same-shape cells}              (the dilation)
+//          u {leaves of length l < l_B that are one of the 27 cells around B's length-l ancestor}  (the closure)
+// Thread per leaf; the leaves are Morton-ordered by their cells' first keys (lkey), so the first set is, per
+// neighbour cell, the contiguous leaf range with first keys in the cell's key range (minus a coarser leaf starting
+// exactly at the cell), and the second set are exact-match lookups.  Entries in (leaf index, image code) order:
+// the 27 ranges are sorted by start and merged with the sorted closure lookups.  code = 9(s_z+1)+3(s_y+1)+(s_x+1),
+// image +1 when the neighbour cell wraps past the upper face (C5).
+constexpr int ADJ_MAX_CLOSURE = 96;  // closure entries per leaf (overflow -> error flag)
+
+__device__ __forceinline__ void halvings_of(int l, uint32_t sh[3]) {
+    sh[0] = (uint32_t)(l / 3);
+    sh[1] = (uint32_t)((l + 1) / 3);
+    sh[2] = (uint32_t)((l + 2) / 3);
+}
+// first finest key of the cell with coordinates c at halvings sh (m bits per dimension)
+__device__ __forceinline__ uint32_t cell_key(const uint32_t c[3], const uint32_t sh[3], int m) {
+    return spread3(c[0] << (m - sh[0])) | (spread3(c[1] << (m - sh[1])) << 1) | (spread3(c[2] << (m - sh[2])) << 2);
+}
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__ a, uint32_t n, uint32_t k) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < k) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+// neighbour cell of c (code) among cells[] per dimension, wrapped; returns the image code
+__device__ __forceinline__ uint32_t nbr_cell(const uint32_t c[3], const uint32_t sh[3], int code, uint32_t out[3]) {
+    const int dd[3] = {code % 3 - 1, (code / 3) % 3 - 1, code / 9 - 1};
+    int img[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const int cells = 1 << sh[d];
+        int v = (int)c[d] + dd[d];
+        img[d] = v < 0 ? -1 : (v >= cells ? 1 : 0);
+        out[d] = (uint32_t)(v - img[d] * cells);
+    }
+    return (uint32_t)(9 * (img[2] + 1) + 3 * (img[1] + 1) + (img[0] + 1));
+}
+
+template <bool FILL>
+__global__ void k_leaf_adj(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen, uint32_t L, int m,
+                           int min_bits, const uint32_t *__restrict__ off, uint32_t *__restrict__ cnt_or_nbr,
+                           uint8_t *__restrict__ code_out, unsigned int *err) {
+    const int bits = 3 * m;
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < L; b += gridDim.x * blockDim.x) {
+        const int lb = (int)llen[b];
+        uint32_t shb[3];
+        halvings_of(lb, shb);
+        const uint32_t k0 = lkey[b];
+        const uint32_t fc[3] = {compact3(k0), compact3(k0 >> 1), compact3(k0 >> 2)};   // finest coords
+        const uint32_t cb[3] = {fc[0] >> (m - shb[0]), fc[1] >> (m - shb[1]), fc[2] >> (m - shb[2])};
+        // the dilation: 27 leaf ranges [i0, i1) (a coarser leaf starting exactly at the cell is skipped)
+        uint32_t r0[27], r1[27], rc[27];
+        uint32_t total = 0;
+        for (int code = 0; code < 27; ++code) {
+            uint32_t cc[3];
+            const uint32_t ic = nbr_cell(cb, shb, code, cc);
+            const uint32_t lo = cell_key(cc, shb, m);
+            const uint64_t hi = (uint64_t)lo + (1ull << (bits - lb));
+            uint32_t i0 = lower_bound_u32(lkey, L, lo);
+            const uint32_t i1 = hi > 0xffffffffull ? L : lower_bound_u32(lkey, L, (uint32_t)hi);
+            if (i0 < i1 && (int)llen[i0] < lb) ++i0;
+            r0[code] = i0;
+            r1[code] = i1;
+            rc[code] = ic;
+            total += i1 - i0;
+        }
+        // the closure: coarser leaves among the 27 cells around each ancestor
+        uint32_t cl[ADJ_MAX_CLOSURE], cc_code[ADJ_MAX_CLOSURE];
+        int ncl = 0;
+        for (int la = min_bits; la < lb; ++la) {
+            uint32_t sha[3];
+            halvings_of(la, sha);
+            const uint32_t anc[3] = {cb[0] >> (shb[0] - sha[0]), cb[1] >> (shb[1] - sha[1]), cb[2] >> (shb[2] - sha[2])};
+            for (int code = 0; code < 27; ++code) {
+                uint32_t cc[3];
+                const uint32_t ic = nbr_cell(anc, sha, code, cc);
+                const uint32_t key = cell_key(cc, sha, m);
+                const uint32_t i = lower_bound_u32(lkey, L, key);
+                if (i < L && lkey[i] == key && (int)llen[i] == la) {
+                    if (ncl < ADJ_MAX_CLOSURE) {
+                        cl[ncl] = i;
+                        cc_code[ncl] = ic;
+                    }
+                    ++ncl;
+                }
+            }
+        }
+        if (ncl > ADJ_MAX_CLOSURE) {
+            atomicOr(err, 1u);
+            ncl = ADJ_MAX_CLOSURE;
+        }
+        total += (uint32_t)ncl;
+        if (!FILL) {
+            cnt_or_nbr[b] = total;
+            continue;
+        }
+        // merge: ranges by start (insertion sort), closure entries by leaf, then ascending leaf index
+        for (int i = 1; i < 27; ++i) {
+            const uint32_t a0 = r0[i], a1 = r1[i], ac = rc[i];
+            int j = i - 1;
+            while (j >= 0 && r0[j] > a0) {
+                r0[j + 1] = r0[j];
+                r1[j + 1] = r1[j];
+                rc[j + 1] = rc[j];
+                --j;
+            }
+            r0[j + 1] = a0;
+            r1[j + 1] = a1;
+            rc[j + 1] = ac;
+        }
+        for (int i = 1; i < ncl; ++i) {
+            const uint32_t a = cl[i], ac = cc_code[i];
+            int j = i - 1;
+            while (j >= 0 && cl[j] > a) {
+                cl[j + 1] = cl[j];
+                cc_code[j + 1] = cc_code[j];
+                --j;
+            }
+            cl[j + 1] = a;
+            cc_code[j + 1] = ac;
+        }
+        uint32_t o = off[b];
+        int ci = 0;
+        for (int r = 0; r < 27; ++r) {
+            for (uint32_t i = r0[r]; i < r1[r]; ++i) {
+                while (ci < ncl && cl[ci] < i) {
+                    cnt_or_nbr[o] = cl[ci];
+                    code_out[o++] = (uint8_t)cc_code[ci++];
+                }
+                cnt_or_nbr[o] = i;
+                code_out[o++] = (uint8_t)rc[r];
+            }
+        }
+        while (ci < ncl) {
+            cnt_or_nbr[o] = cl[ci];
+            code_out[o++] = (uint8_t)cc_code[ci++];
+        }
+    }
+}
+
+struct CntGet {
+    const uint32_t *cnt;
+    __device__ uint32_t operator()(uint64_t p) const { return cnt[p]; }
+};
+struct OffPut {
+    uint32_t *off;
+    __device__ void operator()(uint64_t p, uint32_t e, uint32_t) const { off[p] = e; }
+};
+__global__ void k_leaf_keys(const uint32_t *__restrict__ len, const uint32_t *__restrict__ prefix, uint32_t L,
+                            int bits, uint32_t *__restrict__ lkey) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
+        lkey[i] = (uint32_t)((uint64_t)prefix[i] << (bits - (int)len[i]));
+}
 }  // namespace
 
 p2p_status adaptive_leaves(p2p_plan *P, uint32_t t, int min_bits, uint32_t *len_h, uint32_t *prefix_h,
@@ -112,6 +273,80 @@ p2p_status adaptive_leaves(p2p_plan *P, uint32_t t, int min_bits, uint32_t *len_
     dfree(cnt, st);
     *n_leaves = L;
     return P2P_OK;
+}
+
+}  // namespace p2p
+
+namespace p2p {
+
+// leaves (as adaptive_leaves) and their closed neighbour CSR; host outputs, synchronous
+p2p_status adaptive_neighbours(p2p_plan *P, uint32_t t, int min_bits, uint32_t *off_h, uint32_t *nbr_h,
+                               uint8_t *code_h, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
+                               int64_t *n_entries) {
+    cudaStream_t st = P->stream;
+    const int bits = P->key_bits, m = bits / 3;
+    if (min_bits > bits) min_bits = bits;
+    *n_leaves = *n_entries = 0;
+    const int64_t B = P->B;
+    if (B == 0) return P2P_OK;
+    std::vector<uint32_t> ln((size_t)B), px((size_t)B), stt((size_t)B);
+    int64_t L = 0;
+    p2p_status s = adaptive_leaves(P, t, min_bits, ln.data(), px.data(), stt.data(), B, &L);
+    if (s != P2P_OK) return s;
+    if (L + 1 > cap_leaves) {
+        set_error("leaf capacity below the leaf count + 1");
+        return P2P_ERR_INVALID_ARGUMENT;
+    }
+    uint32_t *dlen = nullptr, *dpre = nullptr, *lkey = nullptr, *cnt = nullptr, *off = nullptr, *tot = nullptr;
+    unsigned int *err = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&dlen, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&dpre, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&lkey, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&cnt, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&off, 4 * (L + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&tot, 4, st));
+    P2P_CUDA_TRY(dalloc((void **)&err, 4, st));
+    P2P_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(dlen, ln.data(), 4 * L, cudaMemcpyHostToDevice, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(dpre, px.data(), 4 * L, cudaMemcpyHostToDevice, st));
+    const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(L, 128), (unsigned)P->num_sms * 8));
+    P2P_LAUNCH(k_leaf_keys, g, 128, 0, st, dlen, dpre, (uint32_t)L, bits, lkey);
+    P2P_LAUNCH(k_leaf_adj<false>, g, 128, 0, st, lkey, dlen, (uint32_t)L, m, min_bits, (const uint32_t *)nullptr,
+               cnt, (uint8_t *)nullptr, err);
+    void *scratch = nullptr;
+    P2P_CUDA_TRY(dalloc(&scratch, scan_partials_bytes(L), st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(CntGet{cnt}, OffPut{off}, nullptr, (uint64_t)L, tot, scratch, st));
+    uint32_t E = 0, e_err = 0;
+    P2P_CUDA_TRY(cudaMemcpyAsync(&E, tot, 4, cudaMemcpyDeviceToHost, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(off + L, tot, 4, cudaMemcpyDeviceToDevice, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(&e_err, err, 4, cudaMemcpyDeviceToHost, st));
+    P2P_CUDA_TRY(cudaStreamSynchronize(st));
+    p2p_status rs = P2P_OK;
+    if (e_err) {
+        set_error("a leaf has more closure neighbours than ADJ_MAX_CLOSURE (k_adaptive.cu)");
+        rs = P2P_ERR_UNSUPPORTED;
+    } else if ((int64_t)E > cap_entries) {
+        set_error("entry capacity below the neighbour-entry count");
+        rs = P2P_ERR_INVALID_ARGUMENT;
+    } else {
+        uint32_t *nbr = nullptr;
+        uint8_t *code = nullptr;
+        P2P_CUDA_TRY(dalloc((void **)&nbr, 4 * std::max<uint32_t>(E, 1), st));
+        P2P_CUDA_TRY(dalloc((void **)&code, std::max<uint32_t>(E, 1), st));
+        P2P_LAUNCH(k_leaf_adj<true>, g, 128, 0, st, lkey, dlen, (uint32_t)L, m, min_bits, (const uint32_t *)off, nbr,
+                   code, err);
+        P2P_CUDA_TRY(cudaMemcpyAsync(off_h, off, 4 * (L + 1), cudaMemcpyDeviceToHost, st));
+        P2P_CUDA_TRY(cudaMemcpyAsync(nbr_h, nbr, 4 * (size_t)E, cudaMemcpyDeviceToHost, st));
+        P2P_CUDA_TRY(cudaMemcpyAsync(code_h, code, (size_t)E, cudaMemcpyDeviceToHost, st));
+        P2P_CUDA_TRY(cudaStreamSynchronize(st));
+        dfree(nbr, st);
+        dfree(code, st);
+        *n_leaves = L;
+        *n_entries = E;
+    }
+    void *bufs[] = {dlen, dpre, lkey, cnt, off, tot, err, scratch};
+    for (void *p : bufs) dfree(p, st);
+    return rs;
 }
 
 }  // namespace p2p

@@ -489,6 +489,26 @@ p2p_status p2p_adaptive_leaves(p2p_plan *P, int32_t t, int32_t min_bits, uint32_
     return mark(P, adaptive_leaves(P, (uint32_t)t, min_bits, len_out, prefix_out, start_out, capacity, n_leaves));
 }
 
+p2p_status p2p_adaptive_neighbours(p2p_plan *P, int32_t t, int32_t min_bits, uint32_t *off_out, uint32_t *nbr_out,
+                                   uint8_t *code_out, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
+                                   int64_t *n_entries) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (!off_out || !nbr_out || !code_out || !n_leaves || !n_entries || t < 1 || min_bits < 9 || cap_leaves < 0 ||
+        cap_entries < 0)
+        return fail(P2P_ERR_INVALID_ARGUMENT,
+                    "adaptive neighbours: NULL output, t < 1, min_bits < 9 (unique images, C22) or capacity < 0");
+    if (P->cfg.kernel != P2P_GRAVITY || P->comm)
+        return fail(P2P_ERR_UNSUPPORTED, "adaptive leaves are for single-GPU gravity plans");
+    const int32_t n0 = P->cfg.nbox[0];
+    if (P->cfg.nbox[1] != n0 || P->cfg.nbox[2] != n0 || (n0 & (n0 - 1)) != 0 || n0 < 8 || P->cfg.periodic_mask != 7u)
+        return fail(P2P_ERR_UNSUPPORTED, "adaptive leaves need a periodic cube of 2^m >= 8 boxes per dimension (C22)");
+    s = resolve_sizes(P);
+    if (s != P2P_OK) return s;
+    return mark(P, adaptive_neighbours(P, (uint32_t)t, min_bits, off_out, nbr_out, code_out, cap_leaves, cap_entries,
+                                       n_leaves, n_entries));
+}
+
 p2p_status p2p_get_pairrec_size(const p2p_plan *P, int64_t *records, int64_t *partials) {
     if (!P || !records || !partials) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
     if (!P->pr_valid) return fail(P2P_ERR_BAD_STATE, "pair records are not built (call p2p_restructure_pairs)");

@@ -169,6 +169,9 @@ p2p_status eval_helmholtz_tc(p2p_plan *P, void *y);
 // k_adaptive.cu: SURVEY NEXT-1 adaptive binary-tree leaves (C22) from the box table; host outputs, synchronous
 p2p_status adaptive_leaves(p2p_plan *P, uint32_t t, int min_bits, uint32_t *len_h, uint32_t *prefix_h,
                            uint32_t *start_h, int64_t cap, int64_t *n_leaves);
+p2p_status adaptive_neighbours(p2p_plan *P, uint32_t t, int min_bits, uint32_t *off_h, uint32_t *nbr_h,
+                               uint8_t *code_h, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
+                               int64_t *n_entries);
 
 // k_pairrec.cu: the thread-level pair-record layout (P2P_PAIRREC)
 p2p_status restructure_pairs(p2p_plan *P);

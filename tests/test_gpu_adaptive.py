@@ -1,7 +1,8 @@
-"""SURVEY NEXT-1, first GPU step (-m gpu): the adaptive binary-tree leaves (DESIGN C22) computed on the device by
-p2p_adaptive_leaves equal the pinned oracle's (oracle/adaptive.py) bit for bit -- prefix length, prefix and the
-first sorted particle of every leaf, in Morton order -- on clustered and uniform inputs, for several clustering
-thresholds, after p2p_plan_update too; plans that are not a periodic 2^m cube are rejected."""
+"""SURVEY NEXT-1 on the GPU (-m gpu): the adaptive binary-tree leaves (DESIGN C22, p2p_adaptive_leaves) and their
+closed neighbour CSR (C23, p2p_adaptive_neighbours) equal the pinned oracle's (oracle/adaptive.py) bit for bit --
+prefix length, prefix and first sorted particle of every leaf in Morton order; every leaf's (neighbour leaf, image
+code) list in order -- on clustered and uniform inputs, for several clustering thresholds, after p2p_plan_update
+too; plans that are not a periodic 2^m cube are rejected."""
 import numpy as np
 import pytest
 
@@ -64,3 +65,29 @@ def test_rejects_non_cube(P):
     with _plan(P, inp) as plan:
         with pytest.raises(P.P2PError):
             P.p2p_adaptive_leaves(plan.handle, 4, 9, plan.info.n_boxes)
+
+
+def _check_csr(P, plan, inp, t, min_bits=9):
+    B = plan.info.n_boxes
+    off, nbr, code = P.p2p_adaptive_neighbours(plan.handle, t, min_bits, B + 1, 27 * 64 * B)
+    tr = A.AdaptiveTree(inp, t, min_bits)
+    want = tr.neighbours()
+    assert len(off) == tr.nleaf + 1 and off[0] == 0
+    for a in range(tr.nleaf):
+        got = list(zip(nbr[off[a]:off[a + 1]].tolist(), code[off[a]:off[a + 1]].tolist()))
+        assert got == want[a], a
+
+
+@pytest.mark.parametrize("seed,t", [(1, 8), (2, 16), (4, 3), (5, 64)])
+def test_neighbour_csr_plummer(P, seed, t):
+    inp = G.plummer(3000, 32, seed=seed)
+    with _plan(P, inp) as plan:
+        _check_csr(P, plan, inp, t)
+
+
+def test_neighbour_csr_uniform_is_the_stencil(P):
+    inp = G.uniform_per_box(8, 4, seed=5)
+    with _plan(P, inp) as plan:
+        off, nbr, code = P.p2p_adaptive_neighbours(plan.handle, 4, 9, 513, 27 * 512)
+        assert np.all(np.diff(off) == 27)
+        _check_csr(P, plan, inp, 4)
