@@ -178,6 +178,16 @@ p2p_status p2p_adaptive_neighbours(p2p_plan *plan, int32_t t, int32_t min_bits, 
                                    uint8_t *code_out, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
                                    int64_t *n_entries);
 
+/* SURVEY NEXT-1, a6 + a7 + a9 over the adaptive leaves: builds the leaves and closed lists as above, the redundant
+ * run of every target leaf (DESIGN C24: its entries' source runs in CSR order, rebased in fp64 to the target leaf's
+ * origin fma(c, w, lo) with the entry's image shift, one final rounding), and evaluates every target against its
+ * run with the REDUNDANT eval kernel (C1, C3; outputs in input order, overwritten).
+ *   potential, field : device, as p2p_eval (potential NULL: build only, e.g. to copy the runs out)
+ *   red_out : host or NULL, [cap_records][4] records of the plan's precision, leaves in order;  *n_records : R
+ * Same preconditions as p2p_adaptive_neighbours.  Synchronous (sizes are read back); the plan is unchanged. */
+p2p_status p2p_adaptive_eval(p2p_plan *plan, int32_t t, int32_t min_bits, void *potential, void *field, void *red_out,
+                             int64_t cap_records, int64_t *n_records);
+
 /* a7/a8 + a9: evaluate every target and scatter to input order.
  *   potential : device, gravity [n_local] real; helmholtz [n_local] complex (re, im)
  *   field     : device, gravity [n_local][3] real (the acceleration, C1) or NULL; helmholtz: must be NULL

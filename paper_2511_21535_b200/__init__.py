@@ -33,7 +33,7 @@ P2P_REDUNDANT, P2P_INDEXED, P2P_INDEXED_BITWISE, P2P_PAIRREC = 0, 1, 2, 3
 LAYOUTS = {"redundant": P2P_REDUNDANT, "indexed": P2P_INDEXED, "indexed_bitwise": P2P_INDEXED_BITWISE}
 
 EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_restructure",
-            "p2p_restructure_pairs", "p2p_get_pairrec_size", "p2p_adaptive_leaves", "p2p_adaptive_neighbours",
+            "p2p_restructure_pairs", "p2p_get_pairrec_size", "p2p_adaptive_leaves", "p2p_adaptive_neighbours", "p2p_adaptive_eval",
             "p2p_eval",
             "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
@@ -81,6 +81,7 @@ def lib() -> C.CDLL:
             "p2p_restructure": (C.c_int, [p]),
             "p2p_restructure_pairs": (C.c_int, [p]),
             "p2p_adaptive_leaves": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, C.POINTER(C.c_int64)]),
+            "p2p_adaptive_eval": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, C.POINTER(C.c_int64)]),
             "p2p_adaptive_neighbours": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, i64, C.POINTER(C.c_int64),
                                                   C.POINTER(C.c_int64)]),
             "p2p_get_pairrec_size": (C.c_int, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -185,6 +186,17 @@ def p2p_adaptive_neighbours(plan: int, t: int, min_bits: int, cap_leaves: int, c
                                          off.size, nbr.size, C.byref(nl), C.byref(ne)))
     L, E = int(nl.value), int(ne.value)
     return off[:L + 1].copy(), nbr[:E].copy(), code[:E].copy()
+
+
+def p2p_adaptive_eval(plan: int, t: int, min_bits: int, potential: int | None, field: int | None,
+                      red_out: np.ndarray | None = None) -> int:
+    """redundant runs + REDUNDANT eval over the adaptive leaves; returns the record count"""
+    nr = C.c_int64()
+    _check(lib().p2p_adaptive_eval(C.c_void_p(plan), int(t), int(min_bits), C.c_void_p(potential or None),
+                                   C.c_void_p(field or None),
+                                   red_out.ctypes.data_as(C.c_void_p) if red_out is not None else None,
+                                   int(red_out.shape[0]) if red_out is not None else 0, C.byref(nr)))
+    return int(nr.value)
 
 
 def p2p_restructure_pairs(plan: int):

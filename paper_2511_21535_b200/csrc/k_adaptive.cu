@@ -221,6 +221,90 @@ __global__ void k_leaf_adj(const uint32_t *__restrict__ lkey, const uint32_t *__
     }
 }
 
+// ---- C24: per target leaf, its run length, the offset of its own (self, image 0) segment, its work items ----
+__global__ void k_adapt_count(const uint32_t *__restrict__ off, const uint32_t *__restrict__ nbr,
+                              const uint8_t *__restrict__ code, const uint32_t *__restrict__ lstart, uint32_t L,
+                              unsigned long long *__restrict__ R, uint32_t *__restrict__ tself,
+                              uint32_t *__restrict__ nitems) {
+    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
+        unsigned long long sum = 0, ts = 0;
+        for (uint32_t e = off[a]; e < off[a + 1]; ++e) {
+            const uint32_t b = nbr[e];
+            if (b == a && code[e] == 13) ts = sum;
+            sum += lstart[b + 1] - lstart[b];
+        }
+        R[a] = sum;
+        tself[a] = (uint32_t)ts;
+        nitems[a] = (lstart[a + 1] - lstart[a] + ITEM_TMAX - 1) / ITEM_TMAX;
+    }
+}
+
+// eval work items of every leaf: full ITEM_TMAX-target items + a remainder (the eval's lane layout, K targets per
+// lane: G = ceil(n_t / K) groups x S = floor(32 / G) source splits); targets staged from the self segment
+__global__ void k_adapt_items(const uint32_t *__restrict__ lstart, const unsigned long long *__restrict__ red_off,
+                              const unsigned long long *__restrict__ R, const uint32_t *__restrict__ tself,
+                              const uint32_t *__restrict__ item_off, uint32_t L, uint32_t K, Item *__restrict__ items) {
+    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
+        const uint32_t nt_all = lstart[a + 1] - lstart[a];
+        uint32_t it = item_off[a];
+        for (uint32_t a0 = 0; a0 < nt_all; a0 += ITEM_TMAX, ++it) {
+            const uint32_t nt = min(ITEM_TMAX, nt_all - a0), G = (nt + K - 1) / K, S = 32u / G;
+            items[it] = Item{a, lstart[a] + a0, nt | (S << 8) | (G << 16), 0u, red_off[a], (uint32_t)R[a],
+                             tself[a] + a0};
+        }
+    }
+}
+
+// the redundant runs (C24): warp per target leaf, its entries' source runs in CSR order, rebased in fp64 to the
+// target leaf's origin o_d = fma(c_d, w_d, lo_d) (w_d = L / 2^s_d) with the entry's image shift, one final rounding
+template <typename T, typename V4>
+__global__ void k_adapt_restructure(const V4 *__restrict__ rec, const uint32_t *__restrict__ lkey,
+                                    const uint32_t *__restrict__ len, const uint32_t *__restrict__ lstart,
+                                    const uint32_t *__restrict__ off, const uint32_t *__restrict__ nbr,
+                                    const uint8_t *__restrict__ code, const unsigned long long *__restrict__ red_off,
+                                    uint32_t L, int m, double Lbox, double lo0, double lo1, double lo2,
+                                    V4 *__restrict__ red) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < L; a += nw) {
+        uint32_t sh[3];
+        halvings_of((int)len[a], sh);
+        const uint32_t k0 = lkey[a];
+        const uint32_t c0 = compact3(k0) >> (m - sh[0]), c1 = compact3(k0 >> 1) >> (m - sh[1]),
+                       c2 = compact3(k0 >> 2) >> (m - sh[2]);
+        const double o0 = __fma_rn((double)c0, ldexp(Lbox, -(int)sh[0]), lo0);
+        const double o1 = __fma_rn((double)c1, ldexp(Lbox, -(int)sh[1]), lo1);
+        const double o2 = __fma_rn((double)c2, ldexp(Lbox, -(int)sh[2]), lo2);
+        V4 *__restrict__ out = red + red_off[a];
+        uint32_t pos = 0;
+        for (uint32_t e = off[a]; e < off[a + 1]; ++e) {
+            const uint32_t b = nbr[e], cd = code[e];
+            const double S0 = (double)((int)(cd % 3) - 1) * Lbox, S1 = (double)((int)((cd / 3) % 3) - 1) * Lbox,
+                         S2 = (double)((int)(cd / 9) - 1) * Lbox;
+            const uint32_t s0 = lstart[b], n = lstart[b + 1] - s0;
+            for (uint32_t r = lane; r < n; r += 32) {
+                const V4 x = rec[s0 + r];
+                V4 v;
+                v.x = (T)__dsub_rn(__dadd_rn((double)x.x, S0), o0);
+                v.y = (T)__dsub_rn(__dadd_rn((double)x.y, S1), o1);
+                v.z = (T)__dsub_rn(__dadd_rn((double)x.z, S2), o2);
+                v.w = x.w;
+                out[pos + r] = v;
+            }
+            pos += n;
+        }
+    }
+}
+
+struct U64Get {
+    const unsigned long long *v;
+    __device__ unsigned long long operator()(uint64_t p) const { return v[p]; }
+};
+struct U64Put {
+    unsigned long long *off;
+    __device__ void operator()(uint64_t p, unsigned long long e, unsigned long long) const { off[p] = e; }
+};
+
 struct CntGet {
     const uint32_t *cnt;
     __device__ uint32_t operator()(uint64_t p) const { return cnt[p]; }
@@ -279,74 +363,176 @@ p2p_status adaptive_leaves(p2p_plan *P, uint32_t t, int min_bits, uint32_t *len_
 
 namespace p2p {
 
+// ---- the device-side adaptive structures: leaves (C22) + closed neighbour CSR (C23) ----
+struct AdaptiveDev {
+    int64_t L = 0, E = 0;
+    uint32_t *len = nullptr, *lkey = nullptr, *lstart = nullptr, *off = nullptr, *nbr = nullptr;
+    uint8_t *code = nullptr;
+    void release(cudaStream_t st) {
+        void *bufs[] = {len, lkey, lstart, off, nbr, code};
+        for (void *p : bufs) dfree(p, st);
+        len = lkey = lstart = off = nbr = nullptr;
+        code = nullptr;
+    }
+};
+
+static p2p_status build_adaptive(p2p_plan *P, uint32_t t, int min_bits, AdaptiveDev &A) {
+    cudaStream_t st = P->stream;
+    const int bits = P->key_bits, m = bits / 3;
+    if (min_bits > bits) min_bits = bits;
+    const int64_t B = P->B;
+    std::vector<uint32_t> ln((size_t)B + 1), px((size_t)B + 1), stt((size_t)B + 1);
+    int64_t L = 0;
+    p2p_status s = adaptive_leaves(P, t, min_bits, ln.data(), px.data(), stt.data(), B, &L);
+    if (s != P2P_OK || L == 0) return s;
+    stt[(size_t)L] = (uint32_t)P->n;
+    uint32_t *dpre = nullptr, *cnt = nullptr, *tot = nullptr;
+    unsigned int *err = nullptr;
+    void *scratch = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&A.len, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&dpre, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&A.lkey, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&A.lstart, 4 * (L + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&cnt, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&A.off, 4 * (L + 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&tot, 4, st));
+    P2P_CUDA_TRY(dalloc((void **)&err, 4, st));
+    P2P_CUDA_TRY(dalloc(&scratch, scan_partials_bytes(L), st));
+    P2P_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(A.len, ln.data(), 4 * L, cudaMemcpyHostToDevice, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(dpre, px.data(), 4 * L, cudaMemcpyHostToDevice, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(A.lstart, stt.data(), 4 * (L + 1), cudaMemcpyHostToDevice, st));
+    const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(L, 128), (unsigned)P->num_sms * 8));
+    P2P_LAUNCH(k_leaf_keys, g, 128, 0, st, A.len, dpre, (uint32_t)L, bits, A.lkey);
+    P2P_LAUNCH(k_leaf_adj<false>, g, 128, 0, st, A.lkey, A.len, (uint32_t)L, m, min_bits, (const uint32_t *)nullptr,
+               cnt, (uint8_t *)nullptr, err);
+    P2P_CUDA_TRY(device_scan<uint32_t>(CntGet{cnt}, OffPut{A.off}, nullptr, (uint64_t)L, tot, scratch, st));
+    uint32_t E = 0, e_err = 0;
+    P2P_CUDA_TRY(cudaMemcpyAsync(&E, tot, 4, cudaMemcpyDeviceToHost, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(A.off + L, tot, 4, cudaMemcpyDeviceToDevice, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(&e_err, err, 4, cudaMemcpyDeviceToHost, st));
+    P2P_CUDA_TRY(cudaStreamSynchronize(st));
+    A.L = L;
+    A.E = E;
+    if (!e_err) {
+        P2P_CUDA_TRY(dalloc((void **)&A.nbr, 4 * std::max<uint32_t>(E, 1), st));
+        P2P_CUDA_TRY(dalloc((void **)&A.code, std::max<uint32_t>(E, 1), st));
+        P2P_LAUNCH(k_leaf_adj<true>, g, 128, 0, st, A.lkey, A.len, (uint32_t)L, m, min_bits, (const uint32_t *)A.off,
+                   A.nbr, A.code, err);
+    }
+    void *bufs[] = {dpre, cnt, tot, err, scratch};
+    for (void *p : bufs) dfree(p, st);
+    if (e_err) {
+        set_error("a leaf has more closure neighbours than ADJ_MAX_CLOSURE (k_adaptive.cu)");
+        return P2P_ERR_UNSUPPORTED;
+    }
+    P2P_CUDA_TRY(cudaGetLastError());
+    return P2P_OK;
+}
+
 // leaves (as adaptive_leaves) and their closed neighbour CSR; host outputs, synchronous
 p2p_status adaptive_neighbours(p2p_plan *P, uint32_t t, int min_bits, uint32_t *off_h, uint32_t *nbr_h,
                                uint8_t *code_h, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
                                int64_t *n_entries) {
     cudaStream_t st = P->stream;
-    const int bits = P->key_bits, m = bits / 3;
-    if (min_bits > bits) min_bits = bits;
     *n_leaves = *n_entries = 0;
-    const int64_t B = P->B;
-    if (B == 0) return P2P_OK;
-    std::vector<uint32_t> ln((size_t)B), px((size_t)B), stt((size_t)B);
-    int64_t L = 0;
-    p2p_status s = adaptive_leaves(P, t, min_bits, ln.data(), px.data(), stt.data(), B, &L);
-    if (s != P2P_OK) return s;
-    if (L + 1 > cap_leaves) {
-        set_error("leaf capacity below the leaf count + 1");
-        return P2P_ERR_INVALID_ARGUMENT;
+    if (P->B == 0) return P2P_OK;
+    AdaptiveDev A;
+    p2p_status s = build_adaptive(P, t, min_bits, A);
+    if (s == P2P_OK) {
+        *n_leaves = A.L;
+        *n_entries = A.E;
+        if (A.L + 1 > cap_leaves || A.E > cap_entries) {
+            set_error("output capacity below the leaf / entry count");
+            s = P2P_ERR_INVALID_ARGUMENT;
+        } else if (A.L > 0) {
+            P2P_CUDA_TRY(cudaMemcpyAsync(off_h, A.off, 4 * (A.L + 1), cudaMemcpyDeviceToHost, st));
+            P2P_CUDA_TRY(cudaMemcpyAsync(nbr_h, A.nbr, 4 * (size_t)A.E, cudaMemcpyDeviceToHost, st));
+            P2P_CUDA_TRY(cudaMemcpyAsync(code_h, A.code, (size_t)A.E, cudaMemcpyDeviceToHost, st));
+            P2P_CUDA_TRY(cudaStreamSynchronize(st));
+        }
     }
-    uint32_t *dlen = nullptr, *dpre = nullptr, *lkey = nullptr, *cnt = nullptr, *off = nullptr, *tot = nullptr;
-    unsigned int *err = nullptr;
-    P2P_CUDA_TRY(dalloc((void **)&dlen, 4 * L, st));
-    P2P_CUDA_TRY(dalloc((void **)&dpre, 4 * L, st));
-    P2P_CUDA_TRY(dalloc((void **)&lkey, 4 * L, st));
-    P2P_CUDA_TRY(dalloc((void **)&cnt, 4 * L, st));
-    P2P_CUDA_TRY(dalloc((void **)&off, 4 * (L + 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&tot, 4, st));
-    P2P_CUDA_TRY(dalloc((void **)&err, 4, st));
-    P2P_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
-    P2P_CUDA_TRY(cudaMemcpyAsync(dlen, ln.data(), 4 * L, cudaMemcpyHostToDevice, st));
-    P2P_CUDA_TRY(cudaMemcpyAsync(dpre, px.data(), 4 * L, cudaMemcpyHostToDevice, st));
+    A.release(st);
+    return s;
+}
+
+}  // namespace p2p
+
+namespace p2p {
+
+// a6 + a7 + a9 over the adaptive leaves: leaves, CSR, redundant runs (optionally copied out), items, the REDUNDANT
+// eval over them; synchronous (sizes are read back)
+p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void *field, void *red_h, int64_t cap_red,
+                         int64_t *n_red) {
+    cudaStream_t st = P->stream;
+    const bool f64 = P->cfg.precision == P2P_FP64;
+    *n_red = 0;
+    if (P->B == 0) return P2P_OK;
+    AdaptiveDev A;
+    p2p_status s = build_adaptive(P, t, min_bits, A);
+    if (s != P2P_OK || A.L == 0) {
+        A.release(st);
+        return s;
+    }
+    const uint32_t L = (uint32_t)A.L;
+    unsigned long long *R = nullptr, *roff = nullptr, *rtot = nullptr;
+    uint32_t *tself = nullptr, *nit = nullptr, *ioff = nullptr, *itot = nullptr, *zero = nullptr;
+    void *scr = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&R, 8 * (size_t)L, st));
+    P2P_CUDA_TRY(dalloc((void **)&roff, 8 * (size_t)L, st));
+    P2P_CUDA_TRY(dalloc((void **)&rtot, 8, st));
+    P2P_CUDA_TRY(dalloc((void **)&tself, 4 * (size_t)L, st));
+    P2P_CUDA_TRY(dalloc((void **)&nit, 4 * (size_t)L, st));
+    P2P_CUDA_TRY(dalloc((void **)&ioff, 4 * (size_t)L, st));
+    P2P_CUDA_TRY(dalloc((void **)&itot, 4, st));
+    P2P_CUDA_TRY(dalloc((void **)&zero, 4, st));
+    P2P_CUDA_TRY(dalloc(&scr, scan_partials_bytes(L), st));
+    P2P_CUDA_TRY(cudaMemsetAsync(zero, 0, 4, st));
     const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(L, 128), (unsigned)P->num_sms * 8));
-    P2P_LAUNCH(k_leaf_keys, g, 128, 0, st, dlen, dpre, (uint32_t)L, bits, lkey);
-    P2P_LAUNCH(k_leaf_adj<false>, g, 128, 0, st, lkey, dlen, (uint32_t)L, m, min_bits, (const uint32_t *)nullptr,
-               cnt, (uint8_t *)nullptr, err);
-    void *scratch = nullptr;
-    P2P_CUDA_TRY(dalloc(&scratch, scan_partials_bytes(L), st));
-    P2P_CUDA_TRY(device_scan<uint32_t>(CntGet{cnt}, OffPut{off}, nullptr, (uint64_t)L, tot, scratch, st));
-    uint32_t E = 0, e_err = 0;
-    P2P_CUDA_TRY(cudaMemcpyAsync(&E, tot, 4, cudaMemcpyDeviceToHost, st));
-    P2P_CUDA_TRY(cudaMemcpyAsync(off + L, tot, 4, cudaMemcpyDeviceToDevice, st));
-    P2P_CUDA_TRY(cudaMemcpyAsync(&e_err, err, 4, cudaMemcpyDeviceToHost, st));
+    P2P_LAUNCH(k_adapt_count, g, 128, 0, st, A.off, A.nbr, A.code, A.lstart, L, R, tself, nit);
+    P2P_CUDA_TRY(device_scan<unsigned long long>(U64Get{R}, U64Put{roff}, nullptr, (uint64_t)L, rtot, scr, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(CntGet{nit}, OffPut{ioff}, nullptr, (uint64_t)L, itot, scr, st));
+    unsigned long long Rtot = 0;
+    uint32_t Itot = 0;
+    P2P_CUDA_TRY(cudaMemcpyAsync(&Rtot, rtot, 8, cudaMemcpyDeviceToHost, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(&Itot, itot, 4, cudaMemcpyDeviceToHost, st));
     P2P_CUDA_TRY(cudaStreamSynchronize(st));
-    p2p_status rs = P2P_OK;
-    if (e_err) {
-        set_error("a leaf has more closure neighbours than ADJ_MAX_CLOSURE (k_adaptive.cu)");
-        rs = P2P_ERR_UNSUPPORTED;
-    } else if ((int64_t)E > cap_entries) {
-        set_error("entry capacity below the neighbour-entry count");
-        rs = P2P_ERR_INVALID_ARGUMENT;
-    } else {
-        uint32_t *nbr = nullptr;
-        uint8_t *code = nullptr;
-        P2P_CUDA_TRY(dalloc((void **)&nbr, 4 * std::max<uint32_t>(E, 1), st));
-        P2P_CUDA_TRY(dalloc((void **)&code, std::max<uint32_t>(E, 1), st));
-        P2P_LAUNCH(k_leaf_adj<true>, g, 128, 0, st, lkey, dlen, (uint32_t)L, m, min_bits, (const uint32_t *)off, nbr,
-                   code, err);
-        P2P_CUDA_TRY(cudaMemcpyAsync(off_h, off, 4 * (L + 1), cudaMemcpyDeviceToHost, st));
-        P2P_CUDA_TRY(cudaMemcpyAsync(nbr_h, nbr, 4 * (size_t)E, cudaMemcpyDeviceToHost, st));
-        P2P_CUDA_TRY(cudaMemcpyAsync(code_h, code, (size_t)E, cudaMemcpyDeviceToHost, st));
-        P2P_CUDA_TRY(cudaStreamSynchronize(st));
-        dfree(nbr, st);
-        dfree(code, st);
-        *n_leaves = L;
-        *n_entries = E;
+    void *red = nullptr;
+    Item *items = nullptr;
+    const size_t rsz = f64 ? sizeof(double4) : sizeof(float4);
+    P2P_CUDA_TRY(dalloc(&red, rsz * std::max<unsigned long long>(Rtot, 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&items, sizeof(Item) * std::max<uint32_t>(Itot, 1), st));
+    const int m = P->key_bits / 3;
+    const unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up((uint64_t)L * 32, 256), (unsigned)P->num_sms * 16));
+    const Geom &G = P->geom;
+    if (f64)
+        P2P_LAUNCH((k_adapt_restructure<double, double4>), gw, 256, 0, st, (const double4 *)P->rec, A.lkey, A.len,
+                   A.lstart, A.off, A.nbr, A.code, roff, L, m, G.L[0], G.lo[0], G.lo[1], G.lo[2], (double4 *)red);
+    else
+        P2P_LAUNCH((k_adapt_restructure<float, float4>), gw, 256, 0, st, (const float4 *)P->rec, A.lkey, A.len,
+                   A.lstart, A.off, A.nbr, A.code, roff, L, m, G.L[0], G.lo[0], G.lo[1], G.lo[2], (float4 *)red);
+    P2P_LAUNCH(k_adapt_items, g, 128, 0, st, A.lstart, roff, R, tself, ioff, L,
+               (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32), items);
+    P2P_CUDA_TRY(cudaGetLastError());
+    s = P2P_OK;
+    if (phi) {
+        EvalItems it{items, itot, (int64_t)Itot, red, zero};
+        s = eval_gravity_items(P, it, phi, field);
     }
-    void *bufs[] = {dlen, dpre, lkey, cnt, off, tot, err, scratch};
+    *n_red = (int64_t)Rtot;
+    if (s == P2P_OK && red_h) {
+        if ((int64_t)Rtot > cap_red) {
+            set_error("red capacity below the record count");
+            s = P2P_ERR_INVALID_ARGUMENT;
+        } else {
+            P2P_CUDA_TRY(cudaMemcpyAsync(red_h, red, rsz * Rtot, cudaMemcpyDeviceToHost, st));
+        }
+    }
+    P2P_CUDA_TRY(cudaStreamSynchronize(st));
+    void *bufs[] = {R, roff, rtot, tself, nit, ioff, itot, zero, scr, red, items};
     for (void *p : bufs) dfree(p, st);
-    return rs;
+    A.release(st);
+    return s;
 }
 
 }  // namespace p2p

@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
 }
 
 template <typename T, int LAYOUT, int K>
-p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
+p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems *ov = nullptr) {
     using V4 = typename V4T<T>::type;
     auto kern = k_eval_gravity<T, LAYOUT, K>;
     const int smem = EV_WARPS * 2 * (EV_STAGE_BYTES + EV_TGT * (int)sizeof(V4));
@@ -782,7 +782,13 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
     a.phi = (T *)phi;
     a.field = (T *)field;
     a.zero = 0u;
-    const int64_t nit = P->sizes_known ? P->n_items + (P->n + 31) / 32 : P->cap;
+    if (ov) {  // an explicit item list over an explicit redundant buffer (adaptive leaves), no small-box path
+        a.red = (const V4 *)ov->red;
+        a.items = ov->items;
+        a.n_items = ov->n_items;
+        a.n_small = ov->zero;
+    }
+    const int64_t nit = ov ? ov->n_items_host : (P->sizes_known ? P->n_items + (P->n + 31) / 32 : P->cap);
     const unsigned grid =
         (unsigned)std::min<int64_t>(P->eval_blocks[slot], std::max<int64_t>(1, (nit + EV_WARPS - 1) / EV_WARPS));
     P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->item_head, 0, sizeof(unsigned int), P->stream));
@@ -792,6 +798,11 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot) {
     return P2P_OK;
 }
 }  // namespace
+
+p2p_status eval_gravity_items(p2p_plan *P, const EvalItems &it, void *phi, void *field) {
+    if (P->cfg.precision == P2P_FP64) return launch<double, P2P_REDUNDANT, EVAL_K_F64>(P, phi, field, 3, &it);
+    return launch<float, P2P_REDUNDANT, EVAL_K_F32>(P, phi, field, 3, &it);
+}
 
 p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
     if (P->sizes_known && P->n == 0) return P2P_OK;

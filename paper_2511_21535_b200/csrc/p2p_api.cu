@@ -509,6 +509,25 @@ p2p_status p2p_adaptive_neighbours(p2p_plan *P, int32_t t, int32_t min_bits, uin
                                        n_leaves, n_entries));
 }
 
+p2p_status p2p_adaptive_eval(p2p_plan *P, int32_t t, int32_t min_bits, void *potential, void *field, void *red_out,
+                             int64_t cap_records, int64_t *n_records) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (!n_records || t < 1 || min_bits < 9 || cap_records < 0)
+        return fail(P2P_ERR_INVALID_ARGUMENT, "adaptive eval: NULL n_records, t < 1, min_bits < 9 or capacity < 0");
+    if (P->cfg.kernel != P2P_GRAVITY || P->comm)
+        return fail(P2P_ERR_UNSUPPORTED, "adaptive leaves are for single-GPU gravity plans");
+    const int32_t n0 = P->cfg.nbox[0];
+    if (P->cfg.nbox[1] != n0 || P->cfg.nbox[2] != n0 || (n0 & (n0 - 1)) != 0 || n0 < 8 || P->cfg.periodic_mask != 7u)
+        return fail(P2P_ERR_UNSUPPORTED, "adaptive leaves need a periodic cube of 2^m >= 8 boxes per dimension (C22)");
+    if (potential && !is_device_ptr(potential)) return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
+    if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
+    if (field && !potential) return fail(P2P_ERR_INVALID_ARGUMENT, "field needs the potential buffer too");
+    s = resolve_sizes(P);
+    if (s != P2P_OK) return s;
+    return mark(P, adaptive_eval(P, (uint32_t)t, min_bits, potential, field, red_out, cap_records, n_records));
+}
+
 p2p_status p2p_get_pairrec_size(const p2p_plan *P, int64_t *records, int64_t *partials) {
     if (!P || !records || !partials) return fail(P2P_ERR_INVALID_ARGUMENT, "NULL argument");
     if (!P->pr_valid) return fail(P2P_ERR_BAD_STATE, "pair records are not built (call p2p_restructure_pairs)");

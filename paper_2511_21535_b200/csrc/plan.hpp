@@ -125,7 +125,7 @@ struct p2p_plan {
     int64_t pr_records = 0, pr_targets = 0;
     bool pr_valid = false;
     p2p_status sticky = P2P_OK;
-    int eval_blocks[3] = {0, 0, 0};
+    int eval_blocks[4] = {0, 0, 0, 0};  // persistent eval grid per layout (+ [3] the explicit-item REDUNDANT eval)
 };
 
 namespace p2p {
@@ -154,6 +154,15 @@ p2p_status restructure_helmholtz(p2p_plan *P);
 
 // k_eval_gravity.cu / k_helmholtz.cu
 p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field);
+// the REDUNDANT eval over an explicit item list and redundant buffer (adaptive leaves, k_adaptive.cu)
+struct EvalItems {
+    const Item *items;
+    const uint32_t *n_items;  // device
+    int64_t n_items_host;     // grid sizing
+    const void *red;
+    const uint32_t *zero;     // device 0 (no small-box path)
+};
+p2p_status eval_gravity_items(p2p_plan *P, const EvalItems &it, void *phi, void *field);
 
 // k_dist.cu: the distributed (multi-GPU) plan build and result return
 p2p_status build_distributed(p2p_plan *P, const void *pos, const void *q);
@@ -172,6 +181,8 @@ p2p_status adaptive_leaves(p2p_plan *P, uint32_t t, int min_bits, uint32_t *len_
 p2p_status adaptive_neighbours(p2p_plan *P, uint32_t t, int min_bits, uint32_t *off_h, uint32_t *nbr_h,
                                uint8_t *code_h, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
                                int64_t *n_entries);
+p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void *field, void *red_h, int64_t cap_red,
+                         int64_t *n_red);
 
 // k_pairrec.cu: the thread-level pair-record layout (P2P_PAIRREC)
 p2p_status restructure_pairs(p2p_plan *P);

@@ -6,6 +6,7 @@ too; plans that are not a periodic 2^m cube are rejected."""
 import numpy as np
 import pytest
 
+import oracle
 import p2p_inputs as G
 from oracle import adaptive as A
 
@@ -91,3 +92,38 @@ def test_neighbour_csr_uniform_is_the_stencil(P):
         off, nbr, code = P.p2p_adaptive_neighbours(plan.handle, 4, 9, 513, 27 * 512)
         assert np.all(np.diff(off) == 27)
         _check_csr(P, plan, inp, 4)
+
+
+@pytest.mark.parametrize("seed,t,dtype", [(1, 8, np.float32), (2, 16, np.float32), (3, 3, np.float32),
+                                          (4, 32, np.float64)])
+def test_adaptive_red_and_eval(P, seed, t, dtype):
+    """C24 runs bit-exact vs the oracle; potentials / fields vs the oracle's plain definition (1e-5 / 1e-12)"""
+    inp = G.plummer(3000, 32, seed=seed, dtype=dtype)
+    tr = A.AdaptiveTree(inp, t)
+    want_red = tr.red(dtype)
+    with _plan(P, inp) as plan:
+        red = np.empty((want_red.shape[0] + 1, 4), dtype)
+        n = P.p2p_adaptive_eval(plan.handle, t, 9, None, None, red)
+        assert n == want_red.shape[0]
+        assert red[:n].tobytes() == want_red.tobytes()
+        phi = torch.empty(inp.n, dtype=torch.from_numpy(np.zeros(1, dtype)).dtype, device="cuda")
+        fld = torch.empty((inp.n, 3), dtype=phi.dtype, device="cuda")
+        P.p2p_adaptive_eval(plan.handle, t, 9, phi.data_ptr(), fld.data_ptr())
+        torch.cuda.synchronize()
+        phi, fld = phi.cpu().numpy(), fld.cpu().numpy()
+    rphi, rf = tr.eval(inp.eps)
+    tol = 1e-5 if dtype == np.float32 else 1e-12
+    assert oracle.rel_l2(phi, rphi) <= tol and oracle.rel_l2(fld, rf) <= tol
+
+
+def test_adaptive_equal_leaves_match_the_grid_path(P):
+    """equal leaves: the adaptive path's outputs are the grid REDUNDANT path's, up to summation order"""
+    inp = G.uniform_per_box(16, 4, seed=8)
+    with _plan(P, inp) as plan:
+        plan.restructure()
+        gphi, gf = [x.cpu().numpy() for x in plan.eval(P.P2P_REDUNDANT)]
+        phi = torch.empty(inp.n, device="cuda")
+        fld = torch.empty((inp.n, 3), device="cuda")
+        P.p2p_adaptive_eval(plan.handle, 4, 9, phi.data_ptr(), fld.data_ptr())
+        torch.cuda.synchronize()
+    assert oracle.rel_l2(phi.cpu().numpy(), gphi) <= 1e-6 and oracle.rel_l2(fld.cpu().numpy(), gf) <= 1e-6
