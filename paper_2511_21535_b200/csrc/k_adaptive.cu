@@ -76,17 +76,15 @@ struct LeafHeadPut {
     }
 };
 
-// ---- C23 adjacency (dilation by the target leaf's extent + symmetric closure), the range construction pinned
-// ---- against the O(L^2) definition by tests/test_oracle_adaptive.py:
-//   nbr(B) = {leaves of prefix length >= l_B inside B's 27 same-shape cells}              (the dilation)
-//          u {leaves of length l < l_B that are one of the 27 cells around B's length-l ancestor}  (the closure)
-// Thread per leaf; the leaves are Morton-ordered by their cells' first keys (lkey), so the first set is, per
-// neighbour cell, the contiguous leaf range with first keys in the cell's key range (minus a coarser leaf starting
-// exactly at the cell), and the second set are exact-match lookups.  Entries in (leaf index, image code) order:
-// the 27 ranges are sorted by start and merged with the sorted closure lookups.  code = 9(s_z+1)+3(s_y+1)+(s_x+1),
-// image +1 when the neighbour cell wraps past the upper face (C5).
-constexpr int ADJ_MAX_CLOSURE = 96;  // closure entries per leaf (overflow -> error flag)
-
+// ---- C23 adjacency (dilation by the target leaf's extent + symmetric closure) ----
+// dil(A) = the leaves of prefix length >= l_A inside A's 27 same-shape cells: per neighbour cell the contiguous range
+// of the Morton-ordered leaf table whose cells start inside the cell's key range (minus a coarser leaf starting
+// exactly at it).  With aligned cells the closed list of B is dil(B) u {(A, -S) : (B, S) in dil(A), l_A < l_B}: a
+// coarser leaf overlapping D(B) contains one of B's 27 cells and so has B in its own dilation (the range
+// construction of oracle/adaptive.py, pinned against the O(L^2) definition).  So: dilation counts (+ per target the
+// number of transposed entries it receives), a scan, the dilation entries in order plus the transposed ones appended
+// by atomic cursors, then per leaf a sort of the (few) transposed entries merged with the sorted dilation run:
+// entries in (leaf, image code) order.  code = 9(s_z+1)+3(s_y+1)+(s_x+1), image +1 past the upper face (C5).
 __device__ __forceinline__ void halvings_of(int l, uint32_t sh[3]) {
     sh[0] = (uint32_t)(l / 3);
     sh[1] = (uint32_t)((l + 1) / 3);
@@ -105,7 +103,7 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__
     }
     return lo;
 }
-// neighbour cell of c (code) among cells[] per dimension, wrapped; returns the image code
+// neighbour cell of c (code), wrapped over 2^sh cells per dimension; returns the image code
 __device__ __forceinline__ uint32_t nbr_cell(const uint32_t c[3], const uint32_t sh[3], int code, uint32_t out[3]) {
     const int dd[3] = {code % 3 - 1, (code / 3) % 3 - 1, code / 9 - 1};
     int img[3];
@@ -119,104 +117,99 @@ __device__ __forceinline__ uint32_t nbr_cell(const uint32_t c[3], const uint32_t
     return (uint32_t)(9 * (img[2] + 1) + 3 * (img[1] + 1) + (img[0] + 1));
 }
 
-template <bool FILL>
-__global__ void k_leaf_adj(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen, uint32_t L, int m,
-                           int min_bits, const uint32_t *__restrict__ off, uint32_t *__restrict__ cnt_or_nbr,
-                           uint8_t *__restrict__ code_out, unsigned int *err) {
-    const int bits = 3 * m;
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < L; b += gridDim.x * blockDim.x) {
-        const int lb = (int)llen[b];
-        uint32_t shb[3];
-        halvings_of(lb, shb);
-        const uint32_t k0 = lkey[b];
-        const uint32_t fc[3] = {compact3(k0), compact3(k0 >> 1), compact3(k0 >> 2)};   // finest coords
-        const uint32_t cb[3] = {fc[0] >> (m - shb[0]), fc[1] >> (m - shb[1]), fc[2] >> (m - shb[2])};
-        // the dilation: 27 leaf ranges [i0, i1) (a coarser leaf starting exactly at the cell is skipped)
+// the 27 dilation ranges of leaf a, sorted by start
+__device__ __forceinline__ void dil_ranges(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen,
+                                           uint32_t L, int m, uint32_t a, uint32_t r0[27], uint32_t r1[27],
+                                           uint32_t rc[27]) {
+    const int bits = 3 * m, la = (int)llen[a];
+    uint32_t sh[3];
+    halvings_of(la, sh);
+    const uint32_t k0 = lkey[a];
+    const uint32_t c[3] = {compact3(k0) >> (m - sh[0]), compact3(k0 >> 1) >> (m - sh[1]), compact3(k0 >> 2) >> (m - sh[2])};
+    for (int code = 0; code < 27; ++code) {
+        uint32_t cc[3];
+        const uint32_t ic = nbr_cell(c, sh, code, cc);
+        const uint32_t lo = cell_key(cc, sh, m);
+        const uint64_t hi = (uint64_t)lo + (1ull << (bits - la));
+        uint32_t i0 = lower_bound_u32(lkey, L, lo);
+        const uint32_t i1 = hi > 0xffffffffull ? L : lower_bound_u32(lkey, L, (uint32_t)hi);
+        if (i0 < i1 && (int)llen[i0] < la) ++i0;
+        int j = code - 1;  // insertion by start
+        while (j >= 0 && r0[j] > i0) {
+            r0[j + 1] = r0[j];
+            r1[j + 1] = r1[j];
+            rc[j + 1] = rc[j];
+            --j;
+        }
+        r0[j + 1] = i0;
+        r1[j + 1] = i1;
+        rc[j + 1] = ic;
+    }
+}
+
+// pass 1: dilation counts; every finer target of a's dilation receives one transposed entry
+__global__ void k_dil_count(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen, uint32_t L, int m,
+                            uint32_t *__restrict__ dcnt, unsigned int *__restrict__ tcnt) {
+    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
         uint32_t r0[27], r1[27], rc[27];
-        uint32_t total = 0;
-        for (int code = 0; code < 27; ++code) {
-            uint32_t cc[3];
-            const uint32_t ic = nbr_cell(cb, shb, code, cc);
-            const uint32_t lo = cell_key(cc, shb, m);
-            const uint64_t hi = (uint64_t)lo + (1ull << (bits - lb));
-            uint32_t i0 = lower_bound_u32(lkey, L, lo);
-            const uint32_t i1 = hi > 0xffffffffull ? L : lower_bound_u32(lkey, L, (uint32_t)hi);
-            if (i0 < i1 && (int)llen[i0] < lb) ++i0;
-            r0[code] = i0;
-            r1[code] = i1;
-            rc[code] = ic;
-            total += i1 - i0;
-        }
-        // the closure: coarser leaves among the 27 cells around each ancestor
-        uint32_t cl[ADJ_MAX_CLOSURE], cc_code[ADJ_MAX_CLOSURE];
-        int ncl = 0;
-        for (int la = min_bits; la < lb; ++la) {
-            uint32_t sha[3];
-            halvings_of(la, sha);
-            const uint32_t anc[3] = {cb[0] >> (shb[0] - sha[0]), cb[1] >> (shb[1] - sha[1]), cb[2] >> (shb[2] - sha[2])};
-            for (int code = 0; code < 27; ++code) {
-                uint32_t cc[3];
-                const uint32_t ic = nbr_cell(anc, sha, code, cc);
-                const uint32_t key = cell_key(cc, sha, m);
-                const uint32_t i = lower_bound_u32(lkey, L, key);
-                if (i < L && lkey[i] == key && (int)llen[i] == la) {
-                    if (ncl < ADJ_MAX_CLOSURE) {
-                        cl[ncl] = i;
-                        cc_code[ncl] = ic;
-                    }
-                    ++ncl;
-                }
-            }
-        }
-        if (ncl > ADJ_MAX_CLOSURE) {
-            atomicOr(err, 1u);
-            ncl = ADJ_MAX_CLOSURE;
-        }
-        total += (uint32_t)ncl;
-        if (!FILL) {
-            cnt_or_nbr[b] = total;
-            continue;
-        }
-        // merge: ranges by start (insertion sort), closure entries by leaf, then ascending leaf index
-        for (int i = 1; i < 27; ++i) {
-            const uint32_t a0 = r0[i], a1 = r1[i], ac = rc[i];
-            int j = i - 1;
-            while (j >= 0 && r0[j] > a0) {
-                r0[j + 1] = r0[j];
-                r1[j + 1] = r1[j];
-                rc[j + 1] = rc[j];
-                --j;
-            }
-            r0[j + 1] = a0;
-            r1[j + 1] = a1;
-            rc[j + 1] = ac;
-        }
-        for (int i = 1; i < ncl; ++i) {
-            const uint32_t a = cl[i], ac = cc_code[i];
-            int j = i - 1;
-            while (j >= 0 && cl[j] > a) {
-                cl[j + 1] = cl[j];
-                cc_code[j + 1] = cc_code[j];
-                --j;
-            }
-            cl[j + 1] = a;
-            cc_code[j + 1] = ac;
-        }
-        uint32_t o = off[b];
-        int ci = 0;
+        dil_ranges(lkey, llen, L, m, a, r0, r1, rc);
+        const uint32_t la = llen[a];
+        uint32_t n = 0;
         for (int r = 0; r < 27; ++r) {
-            for (uint32_t i = r0[r]; i < r1[r]; ++i) {
-                while (ci < ncl && cl[ci] < i) {
-                    cnt_or_nbr[o] = cl[ci];
-                    code_out[o++] = (uint8_t)cc_code[ci++];
-                }
-                cnt_or_nbr[o] = i;
-                code_out[o++] = (uint8_t)rc[r];
-            }
+            n += r1[r] - r0[r];
+            for (uint32_t i = r0[r]; i < r1[r]; ++i)
+                if (llen[i] > la) atomicAdd(&tcnt[i], 1u);
         }
-        while (ci < ncl) {
-            cnt_or_nbr[o] = cl[ci];
-            code_out[o++] = (uint8_t)cc_code[ci++];
+        dcnt[a] = n;
+    }
+}
+
+// pass 2: the dilation entries in (leaf) order; the transposed ones appended to the finer leaves' lists
+__global__ void k_dil_fill(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen, uint32_t L, int m,
+                           const uint32_t *__restrict__ off, const uint32_t *__restrict__ dcnt,
+                           unsigned int *__restrict__ tcur, uint32_t *__restrict__ nbr, uint8_t *__restrict__ code) {
+    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
+        uint32_t r0[27], r1[27], rc[27];
+        dil_ranges(lkey, llen, L, m, a, r0, r1, rc);
+        const uint32_t la = llen[a];
+        uint32_t o = off[a];
+        for (int r = 0; r < 27; ++r)
+            for (uint32_t i = r0[r]; i < r1[r]; ++i) {
+                nbr[o] = i;
+                code[o++] = (uint8_t)rc[r];
+                if (llen[i] > la) {
+                    const uint32_t slot = off[i] + dcnt[i] + atomicAdd(&tcur[i], 1u);
+                    nbr[slot] = a;
+                    code[slot] = (uint8_t)(26u - rc[r]);
+                }
+            }
+    }
+}
+
+// pass 3: sort the transposed entries of each leaf by leaf index and merge them with its sorted dilation run
+__global__ void k_dil_merge(const uint32_t *__restrict__ off, const uint32_t *__restrict__ dcnt, uint32_t L,
+                            uint32_t *__restrict__ nbr, uint8_t *__restrict__ code, uint32_t *__restrict__ nbr_out,
+                            uint8_t *__restrict__ code_out) {
+    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
+        const uint32_t o = off[a], d = dcnt[a], e = off[a + 1];
+        for (uint32_t i = o + d + 1; i < e; ++i) {  // insertion sort of the transposed tail (few entries)
+            const uint32_t v = nbr[i];
+            const uint8_t c = code[i];
+            uint32_t j = i;
+            while (j > o + d && nbr[j - 1] > v) {
+                nbr[j] = nbr[j - 1];
+                code[j] = code[j - 1];
+                --j;
+            }
+            nbr[j] = v;
+            code[j] = c;
+        }
+        uint32_t p = o, q = o + d, w = o;
+        while (p < o + d || q < e) {
+            const bool takep = q >= e || (p < o + d && nbr[p] < nbr[q]);
+            const uint32_t s = takep ? p++ : q++;
+            nbr_out[w] = nbr[s];
+            code_out[w++] = code[s];
         }
     }
 }
@@ -305,6 +298,11 @@ struct U64Put {
     __device__ void operator()(uint64_t p, unsigned long long e, unsigned long long) const { off[p] = e; }
 };
 
+struct SumGet {
+    const uint32_t *a;
+    const unsigned int *b;
+    __device__ uint32_t operator()(uint64_t p) const { return a[p] + b[p]; }
+};
 struct CntGet {
     const uint32_t *cnt;
     __device__ uint32_t operator()(uint64_t p) const { return cnt[p]; }
@@ -386,46 +384,47 @@ static p2p_status build_adaptive(p2p_plan *P, uint32_t t, int min_bits, Adaptive
     p2p_status s = adaptive_leaves(P, t, min_bits, ln.data(), px.data(), stt.data(), B, &L);
     if (s != P2P_OK || L == 0) return s;
     stt[(size_t)L] = (uint32_t)P->n;
-    uint32_t *dpre = nullptr, *cnt = nullptr, *tot = nullptr;
-    unsigned int *err = nullptr;
+    uint32_t *dpre = nullptr, *dcnt = nullptr, *tot = nullptr;
+    unsigned int *tcnt = nullptr, *tcur = nullptr;
     void *scratch = nullptr;
     P2P_CUDA_TRY(dalloc((void **)&A.len, 4 * L, st));
     P2P_CUDA_TRY(dalloc((void **)&dpre, 4 * L, st));
     P2P_CUDA_TRY(dalloc((void **)&A.lkey, 4 * L, st));
     P2P_CUDA_TRY(dalloc((void **)&A.lstart, 4 * (L + 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&cnt, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&dcnt, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&tcnt, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&tcur, 4 * L, st));
     P2P_CUDA_TRY(dalloc((void **)&A.off, 4 * (L + 1), st));
     P2P_CUDA_TRY(dalloc((void **)&tot, 4, st));
-    P2P_CUDA_TRY(dalloc((void **)&err, 4, st));
     P2P_CUDA_TRY(dalloc(&scratch, scan_partials_bytes(L), st));
-    P2P_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+    P2P_CUDA_TRY(cudaMemsetAsync(tcnt, 0, 4 * L, st));
+    P2P_CUDA_TRY(cudaMemsetAsync(tcur, 0, 4 * L, st));
     P2P_CUDA_TRY(cudaMemcpyAsync(A.len, ln.data(), 4 * L, cudaMemcpyHostToDevice, st));
     P2P_CUDA_TRY(cudaMemcpyAsync(dpre, px.data(), 4 * L, cudaMemcpyHostToDevice, st));
     P2P_CUDA_TRY(cudaMemcpyAsync(A.lstart, stt.data(), 4 * (L + 1), cudaMemcpyHostToDevice, st));
     const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(L, 128), (unsigned)P->num_sms * 8));
     P2P_LAUNCH(k_leaf_keys, g, 128, 0, st, A.len, dpre, (uint32_t)L, bits, A.lkey);
-    P2P_LAUNCH(k_leaf_adj<false>, g, 128, 0, st, A.lkey, A.len, (uint32_t)L, m, min_bits, (const uint32_t *)nullptr,
-               cnt, (uint8_t *)nullptr, err);
-    P2P_CUDA_TRY(device_scan<uint32_t>(CntGet{cnt}, OffPut{A.off}, nullptr, (uint64_t)L, tot, scratch, st));
-    uint32_t E = 0, e_err = 0;
+    P2P_LAUNCH(k_dil_count, g, 128, 0, st, A.lkey, A.len, (uint32_t)L, m, dcnt, tcnt);
+    P2P_CUDA_TRY(device_scan<uint32_t>(SumGet{dcnt, tcnt}, OffPut{A.off}, nullptr, (uint64_t)L, tot, scratch, st));
+    uint32_t E = 0;
     P2P_CUDA_TRY(cudaMemcpyAsync(&E, tot, 4, cudaMemcpyDeviceToHost, st));
     P2P_CUDA_TRY(cudaMemcpyAsync(A.off + L, tot, 4, cudaMemcpyDeviceToDevice, st));
-    P2P_CUDA_TRY(cudaMemcpyAsync(&e_err, err, 4, cudaMemcpyDeviceToHost, st));
     P2P_CUDA_TRY(cudaStreamSynchronize(st));
     A.L = L;
     A.E = E;
-    if (!e_err) {
-        P2P_CUDA_TRY(dalloc((void **)&A.nbr, 4 * std::max<uint32_t>(E, 1), st));
-        P2P_CUDA_TRY(dalloc((void **)&A.code, std::max<uint32_t>(E, 1), st));
-        P2P_LAUNCH(k_leaf_adj<true>, g, 128, 0, st, A.lkey, A.len, (uint32_t)L, m, min_bits, (const uint32_t *)A.off,
-                   A.nbr, A.code, err);
-    }
-    void *bufs[] = {dpre, cnt, tot, err, scratch};
+    uint32_t *nbr_t = nullptr;
+    uint8_t *code_t = nullptr;
+    const size_t e1 = std::max<uint32_t>(E, 1);
+    P2P_CUDA_TRY(dalloc((void **)&A.nbr, 4 * e1, st));
+    P2P_CUDA_TRY(dalloc((void **)&A.code, e1, st));
+    P2P_CUDA_TRY(dalloc((void **)&nbr_t, 4 * e1, st));
+    P2P_CUDA_TRY(dalloc((void **)&code_t, e1, st));
+    P2P_LAUNCH(k_dil_fill, g, 128, 0, st, A.lkey, A.len, (uint32_t)L, m, (const uint32_t *)A.off,
+               (const uint32_t *)dcnt, tcur, nbr_t, code_t);
+    P2P_LAUNCH(k_dil_merge, g, 128, 0, st, (const uint32_t *)A.off, (const uint32_t *)dcnt, (uint32_t)L, nbr_t, code_t,
+               A.nbr, A.code);
+    void *bufs[] = {dpre, dcnt, tcnt, tcur, tot, scratch, nbr_t, code_t};
     for (void *p : bufs) dfree(p, st);
-    if (e_err) {
-        set_error("a leaf has more closure neighbours than ADJ_MAX_CLOSURE (k_adaptive.cu)");
-        return P2P_ERR_UNSUPPORTED;
-    }
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }
