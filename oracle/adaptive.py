@@ -128,7 +128,8 @@ class AdaptiveTree:
             self._nbr.append([(int(x), int(y)) for x, y in zip(b[o], c[o])])
         return self._nbr
 
-    # ---- the GPU-oriented construction (next round's kernels), to be pinned against the definition ----
+    # ---- a list construction by range lookups (the GPU's first version), pinned against the definition; the GPU now
+    # ---- builds the same lists as dilation + its transpose (k_adaptive.cu), tested against neighbours() directly ----
     def neighbours_by_ranges(self):
         """nbr(B) = {leaves of level >= l_B inside B's 27 same-shape cells} u {coarser leaves A with A one of the
         27 cells around B's level-l_A ancestor}; same order as neighbours()"""
@@ -251,6 +252,45 @@ def brute(tree: AdaptiveTree, eps: float):
         phi -= (tree.mass[None, :] * ri).sum(axis=1)
         field += ((tree.mass[None, :] * ri ** 3)[:, :, None] * d).sum(axis=1)
     return phi, field
+
+
+def neighbours_of(tree: AdaptiveTree, a: int):
+    """the closed list of ONE leaf straight from the definition (vectorised over the other leaves): for full-size
+    sampled checks where the all-pairs lists are out of reach"""
+    n = tree.n
+    lo, w = tree.lo_i, tree.w_i
+    out = []
+    for code in range(27):
+        S = np.array([code % 3 - 1, code // 3 % 3 - 1, code // 9 - 1], np.int64) * n
+        fwd = np.ones(tree.nleaf, bool)   # B + S overlaps D(a)
+        bwd = np.ones(tree.nleaf, bool)   # a - S overlaps D(B)
+        for d in range(3):
+            fwd &= (lo[:, d] + S[d] < lo[a, d] + 2 * w[a, d]) & (lo[:, d] + w[:, d] + S[d] > lo[a, d] - w[a, d])
+            bwd &= (lo[a, d] - S[d] < lo[:, d] + 2 * w[:, d]) & (lo[a, d] + w[a, d] - S[d] > lo[:, d] - w[:, d])
+        out += [(int(b), code) for b in np.nonzero(fwd | bwd)[0]]
+    return sorted(out)
+
+
+def eval_leaf(tree: AdaptiveTree, a: int, eps: float, nbr=None):
+    """phi, field of leaf a's targets (plain definition, fp64) from its closed list; returns (input indices, phi,
+    field)"""
+    nbr = neighbours_of(tree, a) if nbr is None else nbr
+    _, _, s, c = tree.leaves[a]
+    ti = tree.perm[s:s + c]
+    X, M, SELF = [], [], []
+    for b, code in nbr:
+        S = np.array([code % 3 - 1, code // 3 % 3 - 1, code // 9 - 1], np.float64) * tree.L
+        _, _, sb, cb = tree.leaves[b]
+        sj = tree.perm[sb:sb + cb]
+        X.append(tree.pos[sj] + S)
+        M.append(tree.mass[sj])
+        SELF.append(sj[None, :] == ti[:, None] if (b == a and code == 13) else np.zeros((len(ti), len(sj)), bool))
+    X, M, SELF = np.concatenate(X), np.concatenate(M), np.concatenate(SELF, axis=1)
+    d = X[None, :, :] - tree.pos[ti][:, None, :]
+    ri = 1.0 / np.sqrt((d * d).sum(axis=2) + eps * eps)
+    phi = -np.where(SELF, 0.0, M[None, :] * ri).sum(axis=1)
+    field = ((M[None, :] * ri ** 3)[:, :, None] * d).sum(axis=1)
+    return ti, phi, field
 
 
 def brute_pairs(tree: AdaptiveTree) -> int:

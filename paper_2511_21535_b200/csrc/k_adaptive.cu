@@ -1,5 +1,6 @@
-// k_adaptive.cu -- SURVEY §8f NEXT-1, first GPU step: the adaptive binary-tree leaves (DESIGN C22) of a gravity
-// plan's particles, computed on the device from the plan's Morton-sorted box table.
+// k_adaptive.cu -- SURVEY §8f NEXT-1 on the GPU: the adaptive binary-tree leaves (DESIGN C22), their closed
+// neighbour lists (C23) and the redundant runs + REDUNDANT eval over them (C24), from a gravity plan's Morton-sorted
+// box table and records.
 //
 // The paper's PhotoNs tree is "an irregular binary MLFMA tree" split by a clustering threshold t (P:L330,
 // Fig 8).  Reading C22: longest-axis MIDPOINT splits of the periodic cube with ties z, y, x, i.e. a cell is a prefix

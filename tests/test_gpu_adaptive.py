@@ -127,3 +127,30 @@ def test_adaptive_equal_leaves_match_the_grid_path(P):
         P.p2p_adaptive_eval(plan.handle, 4, 9, phi.data_ptr(), fld.data_ptr())
         torch.cuda.synchronize()
     assert oracle.rel_l2(phi.cpu().numpy(), gphi) <= 1e-6 and oracle.rel_l2(fld.cpu().numpy(), gf) <= 1e-6
+
+
+def test_full_size_sampled(P):
+    """BASELINE configs[2] (10^6 Plummer, 128^3 finest boxes), t = 16: the CSR rows and the potentials / fields of
+    120 seeded-random leaves (and the 10 largest) against the oracle's per-leaf definition"""
+    inp = G.config("c3")
+    t = 16
+    tr = A.AdaptiveTree(inp, t)
+    with _plan(P, inp) as plan:
+        B = plan.info.n_boxes
+        off, nbr, code = P.p2p_adaptive_neighbours(plan.handle, t, 9, B + 1, 40 * B)
+        phi = torch.empty(inp.n, device="cuda")
+        fld = torch.empty((inp.n, 3), device="cuda")
+        P.p2p_adaptive_eval(plan.handle, t, 9, phi.data_ptr(), fld.data_ptr())
+        torch.cuda.synchronize()
+        phi, fld = phi.cpu().numpy(), fld.cpu().numpy()
+    assert len(off) == tr.nleaf + 1
+    rng = np.random.default_rng(0)
+    cnt = np.array([c for _, _, _, c in tr.leaves])
+    pick = np.unique(np.concatenate([rng.choice(tr.nleaf, 120, replace=False), np.argsort(cnt)[-10:]]))
+    e = np.zeros(4)   # squared error / norm of phi, then of the field (one 3n vector)
+    for a in pick:
+        want = A.neighbours_of(tr, int(a))
+        assert list(zip(nbr[off[a]:off[a + 1]].tolist(), code[off[a]:off[a + 1]].tolist())) == want
+        ti, p, f = A.eval_leaf(tr, int(a), inp.eps, want)
+        e += [((phi[ti] - p) ** 2).sum(), (p ** 2).sum(), ((fld[ti] - f) ** 2).sum(), (f ** 2).sum()]
+    assert np.sqrt(e[0] / e[1]) <= 1e-5 and np.sqrt(e[2] / e[3]) <= 1e-5

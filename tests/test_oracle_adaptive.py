@@ -104,3 +104,15 @@ def test_eval_equals_brute_force_and_conserves_momentum():
     assert np.abs(mom).max() <= 1e-12 * np.abs(tr.mass[:, None] * f).sum()
     # interaction count (C19: i = j included) = the acting (i, j, S) triples of the predicate + the N self pairs
     assert tr.pair_count() == A.brute_pairs(tr) + len(tr.key)
+
+
+def test_single_leaf_lists_and_eval_match_the_all_pairs_ones():
+    # the per-leaf forms used for full-size sampled checks equal the all-pairs definition
+    inp = G.plummer(2500, 32, seed=9, dtype=np.float64)
+    tr = A.AdaptiveTree(inp, 8)
+    nbr = tr.neighbours()
+    phi, f = tr.eval(inp.eps)
+    for a in range(0, tr.nleaf, 37):
+        assert A.neighbours_of(tr, a) == nbr[a]
+        ti, p, ff = A.eval_leaf(tr, a, inp.eps)
+        assert np.allclose(p, phi[ti], rtol=1e-14, atol=0) and np.allclose(ff, f[ti], rtol=1e-13, atol=1e-300)
