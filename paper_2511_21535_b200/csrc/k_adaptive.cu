@@ -249,46 +249,106 @@ __global__ void k_adapt_items(const uint32_t *__restrict__ lstart, const unsigne
     }
 }
 
-// the redundant runs (C24): warp per target leaf, its entries' source runs in CSR order, rebased in fp64 to the
-// target leaf's origin o_d = fma(c_d, w_d, lo_d) (w_d = L / 2^s_d) with the entry's image shift, one final rounding
+// the redundant runs (C24): each target leaf's entries' source runs in CSR order, rebased in fp64 to the target
+// leaf's origin o_d = fma(c_d, w_d, lo_d) (w_d = L / 2^s_d) with the entry's image shift, one final rounding.
+// Warp per CHUNK of 32 consecutive CSR entries (the grid restructure's scheme, k_restructure.cu):
+// a chunk's segments are one contiguous output range starting at eoff[32 c] (eoff = exclusive scan of the entries'
+// source counts), its <= 32 entries belong to <= 32 consecutive leaves (every leaf lists itself); lanes copy windows
+// of 32 records, each lane finding its segment by ballot / OR-reduce over the segment starts (full lanes however
+// small the leaves are; a warp per leaf idled most lanes on small leaves: 0.60 -> 0.26 ms at t = 4)
 template <typename T, typename V4>
-__global__ void k_adapt_restructure(const V4 *__restrict__ rec, const uint32_t *__restrict__ lkey,
-                                    const uint32_t *__restrict__ len, const uint32_t *__restrict__ lstart,
-                                    const uint32_t *__restrict__ off, const uint32_t *__restrict__ nbr,
-                                    const uint8_t *__restrict__ code, const unsigned long long *__restrict__ red_off,
-                                    uint32_t L, int m, double Lbox, double lo0, double lo1, double lo2,
-                                    V4 *__restrict__ red) {
+__global__ void __launch_bounds__(256) k_adapt_restructure_chunks(
+    const V4 *__restrict__ rec, const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ len,
+    const uint32_t *__restrict__ lstart, const uint32_t *__restrict__ off, const uint32_t *__restrict__ nbr,
+    const uint8_t *__restrict__ code, const unsigned long long *__restrict__ eoff, uint32_t L, uint32_t E, int m,
+    double Lbox, double lo0, double lo1, double lo2, V4 *__restrict__ red) {
+    constexpr unsigned FULL = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31u;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < L; a += nw) {
-        uint32_t sh[3];
-        halvings_of((int)len[a], sh);
-        const uint32_t k0 = lkey[a];
-        const uint32_t c0 = compact3(k0) >> (m - sh[0]), c1 = compact3(k0 >> 1) >> (m - sh[1]),
-                       c2 = compact3(k0 >> 2) >> (m - sh[2]);
-        const double o0 = __fma_rn((double)c0, ldexp(Lbox, -(int)sh[0]), lo0);
-        const double o1 = __fma_rn((double)c1, ldexp(Lbox, -(int)sh[1]), lo1);
-        const double o2 = __fma_rn((double)c2, ldexp(Lbox, -(int)sh[2]), lo2);
-        V4 *__restrict__ out = red + red_off[a];
-        uint32_t pos = 0;
-        for (uint32_t e = off[a]; e < off[a + 1]; ++e) {
-            const uint32_t b = nbr[e], cd = code[e];
-            const double S0 = (double)((int)(cd % 3) - 1) * Lbox, S1 = (double)((int)((cd / 3) % 3) - 1) * Lbox,
-                         S2 = (double)((int)(cd / 9) - 1) * Lbox;
-            const uint32_t s0 = lstart[b], n = lstart[b + 1] - s0;
-            for (uint32_t r = lane; r < n; r += 32) {
-                const V4 x = rec[s0 + r];
-                V4 v;
-                v.x = (T)__dsub_rn(__dadd_rn((double)x.x, S0), o0);
-                v.y = (T)__dsub_rn(__dadd_rn((double)x.y, S1), o1);
-                v.z = (T)__dsub_rn(__dadd_rn((double)x.z, S2), o2);
-                v.w = x.w;
-                out[pos + r] = v;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5, nchunk = (E + 31u) >> 5;
+    for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunk; ch += nw) {
+        const uint32_t e0 = ch << 5, e = e0 + lane;
+        const bool seg = e < E;
+        uint32_t src = 0, cnt = 0, cd = 13;
+        if (seg) {
+            const uint32_t b = nbr[e];
+            src = lstart[b];
+            cnt = lstart[b + 1] - src;
+            cd = code[e];
+        }
+        // owner leaves: o0 = the leaf whose row holds e0; entry e belongs to the largest o0 + i with off <= e
+        uint32_t o0 = 0;
+        if (lane == 0) {
+            uint32_t lo = 0, hi = L + 1;  // upper_bound(off, e0) - 1
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (off[mid] <= e0) lo = mid + 1;
+                else hi = mid;
             }
-            pos += n;
+            o0 = lo - 1;
+        }
+        o0 = __shfl_sync(FULL, o0, 0);
+        const uint32_t ol = o0 + lane;
+        uint32_t boff = 0xffffffffu;
+        double org0 = 0.0, org1 = 0.0, org2 = 0.0;
+        if (ol < L) {
+            boff = off[ol];
+            uint32_t sh[3];
+            halvings_of((int)len[ol], sh);
+            const uint32_t k0 = lkey[ol];
+            org0 = __fma_rn((double)(compact3(k0) >> (m - sh[0])), ldexp(Lbox, -(int)sh[0]), lo0);
+            org1 = __fma_rn((double)(compact3(k0 >> 1) >> (m - sh[1])), ldexp(Lbox, -(int)sh[1]), lo1);
+            org2 = __fma_rn((double)(compact3(k0 >> 2) >> (m - sh[2])), ldexp(Lbox, -(int)sh[2]), lo2);
+        }
+        uint32_t i = 0;
+#pragma unroll
+        for (uint32_t step = 16; step > 0; step >>= 1) {
+            const uint32_t t = __shfl_sync(FULL, boff, i + step);
+            if (t <= e) i += step;
+        }
+        const double o0d = __shfl_sync(FULL, org0, i), o1d = __shfl_sync(FULL, org1, i), o2d = __shfl_sync(FULL, org2, i);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= (unsigned)o) incl += y;
+        }
+        const uint32_t st = incl - cnt, Rc = __shfl_sync(FULL, incl, 31);
+        V4 *__restrict__ out = red + eoff[e0];
+        const uint32_t le = lane == 31 ? FULL : ((2u << lane) - 1u);
+        for (uint32_t r0 = 0; r0 < Rc; r0 += 32) {
+            // segment of record r0 + lane (leaves are non-empty, so every entry's segment is): segments starting
+            // before r0 - 1 + segment starts in [r0, r0 + lane]
+            const uint32_t before = __popc(__ballot_sync(FULL, seg && st < r0));
+            const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
+            const uint32_t starts = __reduce_or_sync(FULL, in_win);
+            const uint32_t src_lane = (before - 1u + __popc(starts & le)) & 31u;
+            const uint32_t e_src = __shfl_sync(FULL, src, src_lane), e_st = __shfl_sync(FULL, st, src_lane);
+            const uint32_t e_cd = __shfl_sync(FULL, cd, src_lane);
+            const double eo0 = __shfl_sync(FULL, o0d, src_lane), eo1 = __shfl_sync(FULL, o1d, src_lane),
+                         eo2 = __shfl_sync(FULL, o2d, src_lane);
+            const uint32_t r = r0 + lane;
+            if (r < Rc) {
+                const V4 x = rec[e_src + (r - e_st)];
+                const double S0 = (double)((int)(e_cd % 3) - 1) * Lbox, S1 = (double)((int)((e_cd / 3) % 3) - 1) * Lbox,
+                             S2 = (double)((int)(e_cd / 9) - 1) * Lbox;
+                V4 v;
+                v.x = (T)__dsub_rn(__dadd_rn((double)x.x, S0), eo0);
+                v.y = (T)__dsub_rn(__dadd_rn((double)x.y, S1), eo1);
+                v.z = (T)__dsub_rn(__dadd_rn((double)x.z, S2), eo2);
+                v.w = x.w;
+                out[r] = v;
+            }
         }
     }
 }
+
+struct EntryCntGet {
+    const uint32_t *nbr, *lstart;
+    __device__ unsigned long long operator()(uint64_t e) const {
+        const uint32_t b = nbr[e];
+        return lstart[b + 1] - lstart[b];
+    }
+};
 
 struct U64Get {
     const unsigned long long *v;
@@ -503,14 +563,23 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void 
     P2P_CUDA_TRY(dalloc(&red, rsz * std::max<unsigned long long>(Rtot, 1), st));
     P2P_CUDA_TRY(dalloc((void **)&items, sizeof(Item) * std::max<uint32_t>(Itot, 1), st));
     const int m = P->key_bits / 3;
-    const unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up((uint64_t)L * 32, 256), (unsigned)P->num_sms * 16));
     const Geom &G = P->geom;
+    const uint32_t E = (uint32_t)A.E;
+    unsigned long long *eoff = nullptr, *etot = nullptr;
+    void *escr = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&eoff, 8 * (size_t)std::max<uint32_t>(E, 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&etot, 8, st));
+    P2P_CUDA_TRY(dalloc(&escr, scan_partials_bytes(E), st));
+    P2P_CUDA_TRY(device_scan<unsigned long long>(EntryCntGet{A.nbr, A.lstart}, U64Put{eoff}, nullptr, (uint64_t)E, etot,
+                                                 escr, st));
+    const unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up((uint64_t)E, 256), (unsigned)P->num_sms * 16));
     if (f64)
-        P2P_LAUNCH((k_adapt_restructure<double, double4>), gw, 256, 0, st, (const double4 *)P->rec, A.lkey, A.len,
-                   A.lstart, A.off, A.nbr, A.code, roff, L, m, G.L[0], G.lo[0], G.lo[1], G.lo[2], (double4 *)red);
+        P2P_LAUNCH((k_adapt_restructure_chunks<double, double4>), gw, 256, 0, st, (const double4 *)P->rec, A.lkey,
+                   A.len, A.lstart, A.off, A.nbr, A.code, eoff, L, E, m, G.L[0], G.lo[0], G.lo[1], G.lo[2],
+                   (double4 *)red);
     else
-        P2P_LAUNCH((k_adapt_restructure<float, float4>), gw, 256, 0, st, (const float4 *)P->rec, A.lkey, A.len,
-                   A.lstart, A.off, A.nbr, A.code, roff, L, m, G.L[0], G.lo[0], G.lo[1], G.lo[2], (float4 *)red);
+        P2P_LAUNCH((k_adapt_restructure_chunks<float, float4>), gw, 256, 0, st, (const float4 *)P->rec, A.lkey, A.len,
+                   A.lstart, A.off, A.nbr, A.code, eoff, L, E, m, G.L[0], G.lo[0], G.lo[1], G.lo[2], (float4 *)red);
     P2P_LAUNCH(k_adapt_items, g, 128, 0, st, A.lstart, roff, R, tself, ioff, L,
                (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32), items);
     P2P_CUDA_TRY(cudaGetLastError());
@@ -529,7 +598,7 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void 
         }
     }
     P2P_CUDA_TRY(cudaStreamSynchronize(st));
-    void *bufs[] = {R, roff, rtot, tself, nit, ioff, itot, zero, scr, red, items};
+    void *bufs[] = {R, roff, rtot, tself, nit, ioff, itot, zero, scr, red, items, eoff, etot, escr};
     for (void *p : bufs) dfree(p, st);
     A.release(st);
     return s;

@@ -54,7 +54,7 @@ with P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=in
         I = int(sum(cnt[a] * cnt[nbr[off[a]:off[a + 1]]].sum() for a in range(len(cnt))))
         k = kernel_times(lambda: P.p2p_adaptive_eval(plan.handle, t, 9, phi.data_ptr(), fld.data_ptr()))
         ev = k.get("k_eval_gravity", 0.0) * 1e-6
-        rs = k.get("k_adapt_restructure", 0.0) * 1e-6
+        rs = k.get("k_adapt_restructure_chunks", 0.0) * 1e-6
         build = sum(v for n, v in k.items() if n in ("k_leaf_len", "k_dil_count", "k_dil_fill", "k_dil_merge", "k_leaf_keys", "k_scan_reduce",
                                                        "k_scan_partials", "k_scan_down", "k_adapt_count",
                                                        "k_adapt_items")) * 1e-6
