@@ -118,60 +118,58 @@ __device__ __forceinline__ uint32_t nbr_cell(const uint32_t c[3], const uint32_t
     return (uint32_t)(9 * (img[2] + 1) + 3 * (img[1] + 1) + (img[0] + 1));
 }
 
-// the 27 dilation ranges of leaf a, sorted by start
-__device__ __forceinline__ void dil_ranges(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen,
-                                           uint32_t L, int m, uint32_t a, uint32_t r0[27], uint32_t r1[27],
-                                           uint32_t rc[27]) {
-    const int bits = 3 * m, la = (int)llen[a];
-    uint32_t sh[3];
-    halvings_of(la, sh);
-    const uint32_t k0 = lkey[a];
-    const uint32_t c[3] = {compact3(k0) >> (m - sh[0]), compact3(k0 >> 1) >> (m - sh[1]), compact3(k0 >> 2) >> (m - sh[2])};
-    for (int code = 0; code < 27; ++code) {
+// pass 1: thread per (leaf a, neighbour cell): the dilation range of the cell (two binary searches), its length
+// added to a's count, one transposed entry counted for every finer leaf in it
+__global__ void k_dil_ranges(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen, uint32_t L, int m,
+                             uint2 *__restrict__ rng, uint8_t *__restrict__ rcode, unsigned int *__restrict__ dcnt,
+                             unsigned int *__restrict__ tcnt) {
+    const int bits = 3 * m;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < 27ull * L;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = (uint32_t)(x / 27), code = (uint32_t)(x - 27ull * a);
+        const int la = (int)llen[a];
+        uint32_t sh[3];
+        halvings_of(la, sh);
+        const uint32_t k0 = lkey[a];
+        const uint32_t c[3] = {compact3(k0) >> (m - sh[0]), compact3(k0 >> 1) >> (m - sh[1]),
+                               compact3(k0 >> 2) >> (m - sh[2])};
         uint32_t cc[3];
-        const uint32_t ic = nbr_cell(c, sh, code, cc);
+        const uint32_t ic = nbr_cell(c, sh, (int)code, cc);
         const uint32_t lo = cell_key(cc, sh, m);
         const uint64_t hi = (uint64_t)lo + (1ull << (bits - la));
         uint32_t i0 = lower_bound_u32(lkey, L, lo);
         const uint32_t i1 = hi > 0xffffffffull ? L : lower_bound_u32(lkey, L, (uint32_t)hi);
         if (i0 < i1 && (int)llen[i0] < la) ++i0;
-        int j = code - 1;  // insertion by start
-        while (j >= 0 && r0[j] > i0) {
-            r0[j + 1] = r0[j];
-            r1[j + 1] = r1[j];
-            rc[j + 1] = rc[j];
-            --j;
-        }
-        r0[j + 1] = i0;
-        r1[j + 1] = i1;
-        rc[j + 1] = ic;
+        rng[x] = make_uint2(i0, i1);
+        rcode[x] = (uint8_t)ic;
+        if (i1 > i0) atomicAdd(&dcnt[a], i1 - i0);
+        for (uint32_t i = i0; i < i1; ++i)
+            if ((int)llen[i] > la) atomicAdd(&tcnt[i], 1u);
     }
 }
 
-// pass 1: dilation counts; every finer target of a's dilation receives one transposed entry
-__global__ void k_dil_count(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen, uint32_t L, int m,
-                            uint32_t *__restrict__ dcnt, unsigned int *__restrict__ tcnt) {
+// pass 2: thread per leaf: its 27 ranges sorted by start, the dilation entries in (leaf) order, the transposed ones
+// appended to the finer leaves' lists
+__global__ void k_dil_fill(const uint32_t *__restrict__ llen, uint32_t L, const uint2 *__restrict__ rng,
+                           const uint8_t *__restrict__ rcode, const uint32_t *__restrict__ off,
+                           const unsigned int *__restrict__ dcnt, unsigned int *__restrict__ tcur,
+                           uint32_t *__restrict__ nbr, uint8_t *__restrict__ code) {
     for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
         uint32_t r0[27], r1[27], rc[27];
-        dil_ranges(lkey, llen, L, m, a, r0, r1, rc);
-        const uint32_t la = llen[a];
-        uint32_t n = 0;
-        for (int r = 0; r < 27; ++r) {
-            n += r1[r] - r0[r];
-            for (uint32_t i = r0[r]; i < r1[r]; ++i)
-                if (llen[i] > la) atomicAdd(&tcnt[i], 1u);
+        for (int k = 0; k < 27; ++k) {  // insertion by start
+            const uint2 v = rng[27ull * a + k];
+            const uint32_t c = rcode[27ull * a + k];
+            int j = k - 1;
+            while (j >= 0 && r0[j] > v.x) {
+                r0[j + 1] = r0[j];
+                r1[j + 1] = r1[j];
+                rc[j + 1] = rc[j];
+                --j;
+            }
+            r0[j + 1] = v.x;
+            r1[j + 1] = v.y;
+            rc[j + 1] = c;
         }
-        dcnt[a] = n;
-    }
-}
-
-// pass 2: the dilation entries in (leaf) order; the transposed ones appended to the finer leaves' lists
-__global__ void k_dil_fill(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen, uint32_t L, int m,
-                           const uint32_t *__restrict__ off, const uint32_t *__restrict__ dcnt,
-                           unsigned int *__restrict__ tcur, uint32_t *__restrict__ nbr, uint8_t *__restrict__ code) {
-    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
-        uint32_t r0[27], r1[27], rc[27];
-        dil_ranges(lkey, llen, L, m, a, r0, r1, rc);
         const uint32_t la = llen[a];
         uint32_t o = off[a];
         for (int r = 0; r < 27; ++r)
@@ -188,7 +186,7 @@ __global__ void k_dil_fill(const uint32_t *__restrict__ lkey, const uint32_t *__
 }
 
 // pass 3: sort the transposed entries of each leaf by leaf index and merge them with its sorted dilation run
-__global__ void k_dil_merge(const uint32_t *__restrict__ off, const uint32_t *__restrict__ dcnt, uint32_t L,
+__global__ void k_dil_merge(const uint32_t *__restrict__ off, const unsigned int *__restrict__ dcnt, uint32_t L,
                             uint32_t *__restrict__ nbr, uint8_t *__restrict__ code, uint32_t *__restrict__ nbr_out,
                             uint8_t *__restrict__ code_out) {
     for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
@@ -360,7 +358,7 @@ struct U64Put {
 };
 
 struct SumGet {
-    const uint32_t *a;
+    const unsigned int *a;
     const unsigned int *b;
     __device__ uint32_t operator()(uint64_t p) const { return a[p] + b[p]; }
 };
@@ -445,8 +443,10 @@ static p2p_status build_adaptive(p2p_plan *P, uint32_t t, int min_bits, Adaptive
     p2p_status s = adaptive_leaves(P, t, min_bits, ln.data(), px.data(), stt.data(), B, &L);
     if (s != P2P_OK || L == 0) return s;
     stt[(size_t)L] = (uint32_t)P->n;
-    uint32_t *dpre = nullptr, *dcnt = nullptr, *tot = nullptr;
-    unsigned int *tcnt = nullptr, *tcur = nullptr;
+    uint32_t *dpre = nullptr, *tot = nullptr;
+    unsigned int *dcnt = nullptr, *tcnt = nullptr, *tcur = nullptr;
+    uint2 *rng = nullptr;
+    uint8_t *rcode = nullptr;
     void *scratch = nullptr;
     P2P_CUDA_TRY(dalloc((void **)&A.len, 4 * L, st));
     P2P_CUDA_TRY(dalloc((void **)&dpre, 4 * L, st));
@@ -455,17 +455,21 @@ static p2p_status build_adaptive(p2p_plan *P, uint32_t t, int min_bits, Adaptive
     P2P_CUDA_TRY(dalloc((void **)&dcnt, 4 * L, st));
     P2P_CUDA_TRY(dalloc((void **)&tcnt, 4 * L, st));
     P2P_CUDA_TRY(dalloc((void **)&tcur, 4 * L, st));
+    P2P_CUDA_TRY(dalloc((void **)&rng, 8 * 27 * (size_t)L, st));
+    P2P_CUDA_TRY(dalloc((void **)&rcode, 27 * (size_t)L, st));
     P2P_CUDA_TRY(dalloc((void **)&A.off, 4 * (L + 1), st));
     P2P_CUDA_TRY(dalloc((void **)&tot, 4, st));
     P2P_CUDA_TRY(dalloc(&scratch, scan_partials_bytes(L), st));
+    P2P_CUDA_TRY(cudaMemsetAsync(dcnt, 0, 4 * L, st));
     P2P_CUDA_TRY(cudaMemsetAsync(tcnt, 0, 4 * L, st));
     P2P_CUDA_TRY(cudaMemsetAsync(tcur, 0, 4 * L, st));
     P2P_CUDA_TRY(cudaMemcpyAsync(A.len, ln.data(), 4 * L, cudaMemcpyHostToDevice, st));
     P2P_CUDA_TRY(cudaMemcpyAsync(dpre, px.data(), 4 * L, cudaMemcpyHostToDevice, st));
     P2P_CUDA_TRY(cudaMemcpyAsync(A.lstart, stt.data(), 4 * (L + 1), cudaMemcpyHostToDevice, st));
     const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(L, 128), (unsigned)P->num_sms * 8));
+    const unsigned g27 = std::max<unsigned>(1, std::min<unsigned>(div_up(27 * (uint64_t)L, 256), (unsigned)P->num_sms * 16));
     P2P_LAUNCH(k_leaf_keys, g, 128, 0, st, A.len, dpre, (uint32_t)L, bits, A.lkey);
-    P2P_LAUNCH(k_dil_count, g, 128, 0, st, A.lkey, A.len, (uint32_t)L, m, dcnt, tcnt);
+    P2P_LAUNCH(k_dil_ranges, g27, 256, 0, st, A.lkey, A.len, (uint32_t)L, m, rng, rcode, dcnt, tcnt);
     P2P_CUDA_TRY(device_scan<uint32_t>(SumGet{dcnt, tcnt}, OffPut{A.off}, nullptr, (uint64_t)L, tot, scratch, st));
     uint32_t E = 0;
     P2P_CUDA_TRY(cudaMemcpyAsync(&E, tot, 4, cudaMemcpyDeviceToHost, st));
@@ -480,11 +484,11 @@ static p2p_status build_adaptive(p2p_plan *P, uint32_t t, int min_bits, Adaptive
     P2P_CUDA_TRY(dalloc((void **)&A.code, e1, st));
     P2P_CUDA_TRY(dalloc((void **)&nbr_t, 4 * e1, st));
     P2P_CUDA_TRY(dalloc((void **)&code_t, e1, st));
-    P2P_LAUNCH(k_dil_fill, g, 128, 0, st, A.lkey, A.len, (uint32_t)L, m, (const uint32_t *)A.off,
-               (const uint32_t *)dcnt, tcur, nbr_t, code_t);
-    P2P_LAUNCH(k_dil_merge, g, 128, 0, st, (const uint32_t *)A.off, (const uint32_t *)dcnt, (uint32_t)L, nbr_t, code_t,
-               A.nbr, A.code);
-    void *bufs[] = {dpre, dcnt, tcnt, tcur, tot, scratch, nbr_t, code_t};
+    P2P_LAUNCH(k_dil_fill, g, 128, 0, st, A.len, (uint32_t)L, rng, rcode, (const uint32_t *)A.off,
+               (const unsigned int *)dcnt, tcur, nbr_t, code_t);
+    P2P_LAUNCH(k_dil_merge, g, 128, 0, st, (const uint32_t *)A.off, (const unsigned int *)dcnt, (uint32_t)L, nbr_t,
+               code_t, A.nbr, A.code);
+    void *bufs[] = {dpre, dcnt, tcnt, tcur, rng, rcode, tot, scratch, nbr_t, code_t};
     for (void *p : bufs) dfree(p, st);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;

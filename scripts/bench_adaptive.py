@@ -55,7 +55,7 @@ with P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=in
         k = kernel_times(lambda: P.p2p_adaptive_eval(plan.handle, t, 9, phi.data_ptr(), fld.data_ptr()))
         ev = k.get("k_eval_gravity", 0.0) * 1e-6
         rs = k.get("k_adapt_restructure_chunks", 0.0) * 1e-6
-        build = sum(v for n, v in k.items() if n in ("k_leaf_len", "k_dil_count", "k_dil_fill", "k_dil_merge", "k_leaf_keys", "k_scan_reduce",
+        build = sum(v for n, v in k.items() if n in ("k_leaf_len", "k_dil_ranges", "k_dil_fill", "k_dil_merge", "k_leaf_keys", "k_scan_reduce",
                                                        "k_scan_partials", "k_scan_down", "k_adapt_count",
                                                        "k_adapt_items")) * 1e-6
         print(json.dumps({"workload": "c3 (10^6 Plummer, 128^3 finest boxes)", "t": t, "leaves": len(cnt),
