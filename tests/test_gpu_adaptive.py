@@ -154,3 +154,29 @@ def test_full_size_sampled(P):
         ti, p, f = A.eval_leaf(tr, int(a), inp.eps, want)
         e += [((phi[ti] - p) ** 2).sum(), (p ** 2).sum(), ((fld[ti] - f) ** 2).sum(), (f ** 2).sum()]
     assert np.sqrt(e[0] / e[1]) <= 1e-5 and np.sqrt(e[2] / e[3]) <= 1e-5
+
+
+def test_adaptive_errors_and_determinism(P):
+    inp = G.plummer(4000, 32, seed=11)
+    with _plan(P, inp) as plan:
+        B = plan.info.n_boxes
+        with pytest.raises(P.P2PError):           # min_bits < 9: periodic images not unique
+            P.p2p_adaptive_neighbours(plan.handle, 8, 6, B + 1, 64 * B)
+        with pytest.raises(P.P2PError):           # t < 1
+            P.p2p_adaptive_leaves(plan.handle, 0, 9, B)
+        with pytest.raises(P.P2PError):           # entry capacity too small
+            P.p2p_adaptive_neighbours(plan.handle, 8, 9, B + 1, 10)
+        runs = []
+        for _ in range(3):                       # the transposed entries are sorted: CSR and outputs are bitwise stable
+            off, nbr, code = P.p2p_adaptive_neighbours(plan.handle, 8, 9, B + 1, 64 * B)
+            phi = torch.empty(inp.n, device="cuda")
+            fld = torch.empty((inp.n, 3), device="cuda")
+            P.p2p_adaptive_eval(plan.handle, 8, 9, phi.data_ptr(), fld.data_ptr())
+            torch.cuda.synchronize()
+            runs.append((off.tobytes(), nbr.tobytes(), code.tobytes(), phi.cpu().numpy().tobytes(),
+                         fld.cpu().numpy().tobytes()))
+        assert runs[0] == runs[1] == runs[2]
+        # the plan itself is untouched: the grid path still evaluates as before
+        plan.restructure()
+        gphi, _ = plan.eval(P.P2P_REDUNDANT)
+        assert torch.isfinite(gphi).all()
