@@ -184,9 +184,11 @@ p2p_status p2p_adaptive_neighbours(p2p_plan *plan, int32_t t, int32_t min_bits, 
  * run with the REDUNDANT eval kernel (C1, C3; outputs in input order, overwritten).
  *   potential, field : device, as p2p_eval (potential NULL: build only, e.g. to copy the runs out)
  *   red_out : host or NULL, [cap_records][4] records of the plan's precision, leaves in order;  *n_records : R
+ *   layout : P2P_REDUNDANT (the runs above) or P2P_INDEXED (the non-redundant baseline: the same eval kernel stages the
+ *            leaves' neighbour segments of the sorted records, absolute coordinates, exact -L frames; no runs built)
  * Same preconditions as p2p_adaptive_neighbours.  Synchronous (sizes are read back); the plan is unchanged. */
-p2p_status p2p_adaptive_eval(p2p_plan *plan, int32_t t, int32_t min_bits, void *potential, void *field, void *red_out,
-                             int64_t cap_records, int64_t *n_records);
+p2p_status p2p_adaptive_eval(p2p_plan *plan, int32_t t, int32_t min_bits, p2p_layout layout, void *potential,
+                             void *field, void *red_out, int64_t cap_records, int64_t *n_records);
 
 /* a7/a8 + a9: evaluate every target and scatter to input order.
  *   potential : device, gravity [n_local] real; helmholtz [n_local] complex (re, im)

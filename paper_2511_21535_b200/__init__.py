@@ -81,7 +81,7 @@ def lib() -> C.CDLL:
             "p2p_restructure": (C.c_int, [p]),
             "p2p_restructure_pairs": (C.c_int, [p]),
             "p2p_adaptive_leaves": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, C.POINTER(C.c_int64)]),
-            "p2p_adaptive_eval": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, C.POINTER(C.c_int64)]),
+            "p2p_adaptive_eval": (C.c_int, [p, C.c_int32, C.c_int32, C.c_int, p, p, p, i64, C.POINTER(C.c_int64)]),
             "p2p_adaptive_neighbours": (C.c_int, [p, C.c_int32, C.c_int32, p, p, p, i64, i64, C.POINTER(C.c_int64),
                                                   C.POINTER(C.c_int64)]),
             "p2p_get_pairrec_size": (C.c_int, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -189,10 +189,11 @@ def p2p_adaptive_neighbours(plan: int, t: int, min_bits: int, cap_leaves: int, c
 
 
 def p2p_adaptive_eval(plan: int, t: int, min_bits: int, potential: int | None, field: int | None,
-                      red_out: np.ndarray | None = None) -> int:
-    """redundant runs + REDUNDANT eval over the adaptive leaves; returns the record count"""
+                      red_out: np.ndarray | None = None, layout: int = 0) -> int:
+    """redundant runs + REDUNDANT eval (or the INDEXED baseline) over the adaptive leaves; returns the
+    record count"""
     nr = C.c_int64()
-    _check(lib().p2p_adaptive_eval(C.c_void_p(plan), int(t), int(min_bits), C.c_void_p(potential or None),
+    _check(lib().p2p_adaptive_eval(C.c_void_p(plan), int(t), int(min_bits), int(layout), C.c_void_p(potential or None),
                                    C.c_void_p(field or None),
                                    red_out.ctypes.data_as(C.c_void_p) if red_out is not None else None,
                                    int(red_out.shape[0]) if red_out is not None else 0, C.byref(nr)))

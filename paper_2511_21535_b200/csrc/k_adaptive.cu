@@ -348,6 +348,24 @@ struct EntryCntGet {
     }
 };
 
+// INDEXED over the leaves: per leaf, bit d = its cell touches the upper face of dim d (frame -L), bit 3 + d the lower
+__global__ void k_leaf_frame(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ len, uint32_t L, int m,
+                             uint8_t *__restrict__ fr) {
+    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
+        uint32_t sh[3];
+        halvings_of((int)len[a], sh);
+        const uint32_t k0 = lkey[a];
+        uint32_t f = 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const uint32_t c = compact3(k0 >> d) >> (m - sh[d]);
+            if (c == (1u << sh[d]) - 1u) f |= 1u << d;
+            if (c == 0u) f |= 8u << d;
+        }
+        fr[a] = (uint8_t)f;
+    }
+}
+
 struct U64Get {
     const unsigned long long *v;
     __device__ unsigned long long operator()(uint64_t p) const { return v[p]; }
@@ -526,8 +544,8 @@ namespace p2p {
 
 // a6 + a7 + a9 over the adaptive leaves: leaves, CSR, redundant runs (optionally copied out), items, the REDUNDANT
 // eval over them; synchronous (sizes are read back)
-p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void *field, void *red_h, int64_t cap_red,
-                         int64_t *n_red) {
+p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, void *phi, void *field, void *red_h,
+                         int64_t cap_red, int64_t *n_red) {
     cudaStream_t st = P->stream;
     const bool f64 = P->cfg.precision == P2P_FP64;
     *n_red = 0;
@@ -577,7 +595,12 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void 
     P2P_CUDA_TRY(device_scan<unsigned long long>(EntryCntGet{A.nbr, A.lstart}, U64Put{eoff}, nullptr, (uint64_t)E, etot,
                                                  escr, st));
     const unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up((uint64_t)E, 256), (unsigned)P->num_sms * 16));
-    if (f64)
+    uint8_t *lframe = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&lframe, std::max<uint32_t>(L, 1), st));
+    P2P_LAUNCH(k_leaf_frame, g, 128, 0, st, A.lkey, A.len, L, m, lframe);
+    if (indexed) {
+        // the non-redundant baseline: no runs, the eval stages the neighbour segments of the sorted records
+    } else if (f64)
         P2P_LAUNCH((k_adapt_restructure_chunks<double, double4>), gw, 256, 0, st, (const double4 *)P->rec, A.lkey,
                    A.len, A.lstart, A.off, A.nbr, A.code, eoff, L, E, m, G.L[0], G.lo[0], G.lo[1], G.lo[2],
                    (double4 *)red);
@@ -590,10 +613,17 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void 
     s = P2P_OK;
     if (phi) {
         EvalItems it{items, itot, (int64_t)Itot, red, zero};
+        if (indexed) {
+            it.csr_off = A.off;
+            it.csr_nbr = A.nbr;
+            it.csr_code = A.code;
+            it.lstart = A.lstart;
+            it.lframe = lframe;
+        }
         s = eval_gravity_items(P, it, phi, field);
     }
     *n_red = (int64_t)Rtot;
-    if (s == P2P_OK && red_h) {
+    if (s == P2P_OK && red_h && !indexed) {
         if ((int64_t)Rtot > cap_red) {
             set_error("red capacity below the record count");
             s = P2P_ERR_INVALID_ARGUMENT;
@@ -602,7 +632,7 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void 
         }
     }
     P2P_CUDA_TRY(cudaStreamSynchronize(st));
-    void *bufs[] = {R, roff, rtot, tself, nit, ioff, itot, zero, scr, red, items, eoff, etot, escr};
+    void *bufs[] = {R, roff, rtot, tself, nit, ioff, itot, zero, scr, red, items, eoff, etot, escr, lframe};
     for (void *p : bufs) dfree(p, st);
     A.release(st);
     return s;

@@ -76,6 +76,7 @@ struct EvalArgs {
     T *phi;
     T *field;
     uint32_t zero;             // always 0 (see queue_claim)
+    const uint8_t *lframe;     // ADAPT: per leaf, bit d = touches the upper face of periodic dim d, bit 3 + d the lower
 };
 
 // image shift of stencil slot seen from box c (DESIGN C5)
@@ -425,7 +426,10 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
     }
 }
 
-template <typename T, int LAYOUT, int K>
+// ADAPT (P2P_INDEXED over adaptive leaves, k_adaptive.cu): the CSR's slot is the image code itself, a leaf's frame /
+// boundary flags come from a.lframe instead of the uniform grid's box coordinates, and a leaf may list more than 32
+// neighbour segments (the lane-per-segment registers then cover groups of 32, re-read from the CSR per chunk)
+template <typename T, int LAYOUT, int K, bool ADAPT = false>
 __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P_REDUNDANT ? 5 : 4) : 1) k_eval_gravity(const EvalArgs<T> a) {
     using V4 = typename V4T<T>::type;
     constexpr int CH = EV_STAGE_BYTES / (int)sizeof(V4);
@@ -454,6 +458,29 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     uint32_t p_box = 0, p_t0 = 0, p_meta = 0, p_key = 0, p_R = 0, p_nch = 0, p_tofs = 0;
     uint64_t p_base = 0;
     uint32_t p_src = 0, p_st = 0, p_cnt = 0, p_slot = 0, p_ne = 0;  // INDEXED: lane = segment
+    uint32_t p_e0 = 0;  // ADAPT: the item's first CSR entry
+    // ADAPT: segment group g0 .. g0 + 31 of the CSR row at e0 (ne entries), starts offset by `base`
+    auto seg_group = [&](uint32_t e0, uint32_t ne, uint32_t g0, uint32_t base, uint32_t &src, uint32_t &st,
+                         uint32_t &cntl, uint32_t &code, uint32_t &tot) {
+        const bool valid = g0 + lane < ne;
+        src = 0;
+        cntl = 0;
+        code = 13;
+        if (valid) {
+            const uint32_t k = a.nbr_box[e0 + g0 + lane];
+            src = a.bstart[k];
+            cntl = a.bstart[k + 1] - src;
+            code = a.nbr_slot[e0 + g0 + lane];
+        }
+        uint32_t incl = cntl;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += y;
+        }
+        st = base + incl - cntl;
+        tot = __shfl_sync(0xffffffffu, incl, 31);
+    };
 
     // work-queue pipeline: each atomicAdd claims EV_BATCH consecutive items (fewer atomics on the one queue
     // counter) and its result is consumed by shfl a whole batch later; item n+1's 32-byte Item record is already
@@ -521,6 +548,14 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
             }
             p_st = incl - p_cnt;
             p_R = __shfl_sync(FULL, incl, 31);
+            if constexpr (ADAPT) {
+                p_e0 = e0;
+                for (uint32_t g0 = 32; g0 < p_ne; g0 += 32) {  // rows longer than a warp: the remaining groups
+                    uint32_t src, st, cntl, code, tot;
+                    seg_group(e0, p_ne, g0, p_R, src, st, cntl, code, tot);
+                    p_R += tot;
+                }
+            }
         }
         p_nch = (p_R + CH - 1) / CH;
     };
@@ -541,6 +576,17 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
             const uint32_t ov0 = max(c0, p_st), ov1 = min(c0 + cnt, p_st + p_cnt);
             if (lane < p_ne && ov1 > ov0)
                 bulk_g2s(dst + (ov0 - c0), a.rec + p_src + (ov0 - p_st), (ov1 - ov0) * (uint32_t)sizeof(V4), &bar[s]);
+            if constexpr (ADAPT) {
+                uint32_t base = __shfl_sync(FULL, p_st + p_cnt, 31);
+                for (uint32_t g0 = 32; g0 < p_ne && base < c0 + cnt; g0 += 32) {
+                    uint32_t src, st, cntl, code, tot;
+                    seg_group(p_e0, p_ne, g0, base, src, st, cntl, code, tot);
+                    const uint32_t v0 = max(c0, st), v1 = min(c0 + cnt, st + cntl);
+                    if (v1 > v0)
+                        bulk_g2s(dst + (v0 - c0), a.rec + src + (v0 - st), (v1 - v0) * (uint32_t)sizeof(V4), &bar[s]);
+                    base += tot;
+                }
+            }
         }
         // targets: REDUNDANT takes them already rebased from the box's own segment of its run
         if (chunk == 0 && lane == 31)
@@ -567,17 +613,24 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     while (true) {
         // ---------------- adopt the producer's item as the current (consumer) item ----------------
         const uint32_t c_t0 = p_t0, c_meta = p_meta, c_R = p_R, c_nch = p_nch;
-        const uint32_t c_st = p_st, c_cnt = p_cnt, c_slot = p_slot, c_ne = p_ne;
+        const uint32_t c_st = p_st, c_cnt = p_cnt, c_slot = p_slot, c_ne = p_ne, c_e0 = p_e0;
         const uint32_t cc[3] = {compact3(p_key), compact3(p_key >> 1), compact3(p_key >> 2)};
         double org[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-            org[d] = (LAYOUT == P2P_INDEXED) ? frame_shift(a.g, cc, d) : __fma_rn((double)cc[d], a.g.h, a.g.lo[d]);
         bool needs_fix = false;
-        if (LAYOUT == P2P_INDEXED) {
+        if constexpr (ADAPT) {  // leaf frame: -L in the dims where the leaf touches the upper face (bits 0..2)
+            const uint32_t fr = a.lframe[p_box];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) org[d] = ((fr >> d) & 1u) ? -a.g.L[d] : 0.0;
+            needs_fix = fr != 0u;  // touches an upper (bits 0..2) or lower (bits 3..5) face
+        } else {
 #pragma unroll
             for (int d = 0; d < 3; ++d)
-                needs_fix |= ((a.g.periodic >> d) & 1u) && (cc[d] == 0 || (int)cc[d] == a.g.nbox[d] - 1);
+                org[d] = (LAYOUT == P2P_INDEXED) ? frame_shift(a.g, cc, d) : __fma_rn((double)cc[d], a.g.h, a.g.lo[d]);
+            if (LAYOUT == P2P_INDEXED) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                    needs_fix |= ((a.g.periodic >> d) & 1u) && (cc[d] == 0 || (int)cc[d] == a.g.nbox[d] - 1);
+            }
         }
         // lane layout (precomputed by k_nbr_fill): G groups of K targets x S source splits
         const uint32_t nt = c_meta & 0xffu, S = (c_meta >> 8) & 0xffu, G = (c_meta >> 16) & 0xffu;
@@ -642,13 +695,25 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
 
             // ---- layout fix-ups of the staged raw records (INDEXED variants only) ----
             if (LAYOUT == P2P_INDEXED_BITWISE || (LAYOUT == P2P_INDEXED && needs_fix)) {
-                for (uint32_t e = 0; e < c_ne; ++e) {
-                    const uint32_t est = __shfl_sync(FULL, c_st, e), ecnt = __shfl_sync(FULL, c_cnt, e);
-                    const int eslot = (int)__shfl_sync(FULL, c_slot, e);
+                // segment groups of 32 (one group unless ADAPT rows are longer than a warp)
+                uint32_t gbase = 0;
+                for (uint32_t g0 = 0; g0 < c_ne; g0 += 32) {
+                uint32_t g_st = c_st, g_cnt = c_cnt, g_slot = c_slot, g_tot = 0;
+                if (ADAPT && g0 > 0) {
+                    uint32_t src;
+                    seg_group(c_e0, c_ne, g0, gbase, src, g_st, g_cnt, g_slot, g_tot);
+                } else {
+                    g_tot = __shfl_sync(FULL, c_st + c_cnt, 31);
+                }
+                const uint32_t gne = min(32u, c_ne - g0);
+                for (uint32_t e = 0; e < gne; ++e) {
+                    const uint32_t est = __shfl_sync(FULL, g_st, e), ecnt = __shfl_sync(FULL, g_cnt, e);
+                    const int eslot = (int)__shfl_sync(FULL, g_slot, e);
                     const uint32_t ov0 = max(c0, est), ov1 = min(c0 + cnt, est + ecnt);
                     if (ov1 <= ov0) continue;
-                    const double S0 = slot_shift(a.g, cc, eslot, 0), S1 = slot_shift(a.g, cc, eslot, 1),
-                                 S2 = slot_shift(a.g, cc, eslot, 2);
+                    const double S0 = ADAPT ? (double)(eslot % 3 - 1) * a.g.L[0] : slot_shift(a.g, cc, eslot, 0);
+                    const double S1 = ADAPT ? (double)((eslot / 3) % 3 - 1) * a.g.L[1] : slot_shift(a.g, cc, eslot, 1);
+                    const double S2 = ADAPT ? (double)(eslot / 9 - 1) * a.g.L[2] : slot_shift(a.g, cc, eslot, 2);
                     if (LAYOUT == P2P_INDEXED) {
                         const T h0 = (T)(S0 + org[0]), h1 = (T)(S1 + org[1]), h2 = (T)(S2 + org[2]);
                         if (h0 == (T)0 && h1 == (T)0 && h2 == (T)0) continue;
@@ -666,6 +731,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
                             stg[j] = v;
                         }
                     }
+                }
+                gbase = (ADAPT && g0 > 0) ? gbase + g_tot : g_tot;
+                if (!ADAPT) break;
                 }
                 __syncwarp();
             }
@@ -750,10 +818,10 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     if (!small_first) small_phase<T, LAYOUT>(a, lane);
 }
 
-template <typename T, int LAYOUT, int K>
+template <typename T, int LAYOUT, int K, bool ADAPT = false>
 p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems *ov = nullptr) {
     using V4 = typename V4T<T>::type;
-    auto kern = k_eval_gravity<T, LAYOUT, K>;
+    auto kern = k_eval_gravity<T, LAYOUT, K, ADAPT>;
     const int smem = EV_WARPS * 2 * (EV_STAGE_BYTES + EV_TGT * (int)sizeof(V4));
     if (P->eval_blocks[slot] == 0) {
         P2P_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -782,11 +850,19 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems
     a.phi = (T *)phi;
     a.field = (T *)field;
     a.zero = 0u;
-    if (ov) {  // an explicit item list over an explicit redundant buffer (adaptive leaves), no small-box path
+    a.lframe = nullptr;
+    if (ov) {  // an explicit item list over an explicit redundant buffer / CSR (adaptive leaves), no small-box path
         a.red = (const V4 *)ov->red;
         a.items = ov->items;
         a.n_items = ov->n_items;
         a.n_small = ov->zero;
+        if (ov->csr_off) {
+            a.nbr_off = ov->csr_off;
+            a.nbr_box = ov->csr_nbr;
+            a.nbr_slot = ov->csr_code;
+            a.bstart = ov->lstart;
+            a.lframe = ov->lframe;
+        }
     }
     const int64_t nit = ov ? ov->n_items_host : (P->sizes_known ? P->n_items + (P->n + 31) / 32 : P->cap);
     const unsigned grid =
@@ -800,6 +876,10 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems
 }  // namespace
 
 p2p_status eval_gravity_items(p2p_plan *P, const EvalItems &it, void *phi, void *field) {
+    if (it.csr_off) {  // INDEXED over the adaptive leaves' CSR (the non-redundant baseline)
+        if (P->cfg.precision == P2P_FP64) return launch<double, P2P_INDEXED, EVAL_K_F64, true>(P, phi, field, 4, &it);
+        return launch<float, P2P_INDEXED, EVAL_K_F32, true>(P, phi, field, 4, &it);
+    }
     if (P->cfg.precision == P2P_FP64) return launch<double, P2P_REDUNDANT, EVAL_K_F64>(P, phi, field, 3, &it);
     return launch<float, P2P_REDUNDANT, EVAL_K_F32>(P, phi, field, 3, &it);
 }

@@ -509,12 +509,14 @@ p2p_status p2p_adaptive_neighbours(p2p_plan *P, int32_t t, int32_t min_bits, uin
                                        n_leaves, n_entries));
 }
 
-p2p_status p2p_adaptive_eval(p2p_plan *P, int32_t t, int32_t min_bits, void *potential, void *field, void *red_out,
-                             int64_t cap_records, int64_t *n_records) {
+p2p_status p2p_adaptive_eval(p2p_plan *P, int32_t t, int32_t min_bits, p2p_layout layout, void *potential, void *field,
+                             void *red_out, int64_t cap_records, int64_t *n_records) {
     p2p_status s = enter(P);
     if (s != P2P_OK) return s;
     if (!n_records || t < 1 || min_bits < 9 || cap_records < 0)
         return fail(P2P_ERR_INVALID_ARGUMENT, "adaptive eval: NULL n_records, t < 1, min_bits < 9 or capacity < 0");
+    if (layout != P2P_REDUNDANT && layout != P2P_INDEXED)
+        return fail(P2P_ERR_INVALID_ARGUMENT, "adaptive eval: layout must be P2P_REDUNDANT or P2P_INDEXED");
     if (P->cfg.kernel != P2P_GRAVITY || P->comm)
         return fail(P2P_ERR_UNSUPPORTED, "adaptive leaves are for single-GPU gravity plans");
     const int32_t n0 = P->cfg.nbox[0];
@@ -525,7 +527,8 @@ p2p_status p2p_adaptive_eval(p2p_plan *P, int32_t t, int32_t min_bits, void *pot
     if (field && !potential) return fail(P2P_ERR_INVALID_ARGUMENT, "field needs the potential buffer too");
     s = resolve_sizes(P);
     if (s != P2P_OK) return s;
-    return mark(P, adaptive_eval(P, (uint32_t)t, min_bits, potential, field, red_out, cap_records, n_records));
+    return mark(P, adaptive_eval(P, (uint32_t)t, min_bits, layout == P2P_INDEXED, potential, field, red_out, cap_records,
+                                 n_records));
 }
 
 p2p_status p2p_get_pairrec_size(const p2p_plan *P, int64_t *records, int64_t *partials) {

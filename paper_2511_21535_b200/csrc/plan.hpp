@@ -125,7 +125,7 @@ struct p2p_plan {
     int64_t pr_records = 0, pr_targets = 0;
     bool pr_valid = false;
     p2p_status sticky = P2P_OK;
-    int eval_blocks[4] = {0, 0, 0, 0};  // persistent eval grid per layout (+ [3] the explicit-item REDUNDANT eval)
+    int eval_blocks[5] = {0, 0, 0, 0, 0};  // persistent eval grid per layout (+ [3] / [4] the adaptive-leaf evals)
 };
 
 namespace p2p {
@@ -161,6 +161,10 @@ struct EvalItems {
     int64_t n_items_host;     // grid sizing
     const void *red;
     const uint32_t *zero;     // device 0 (no small-box path)
+    // INDEXED over adaptive leaves (csr_off != nullptr): the leaves' CSR, first sorted particle per leaf [L + 1],
+    // frame / boundary flags per leaf (bit d: touches the upper face of dim d, bit 3 + d: the lower face)
+    const uint32_t *csr_off = nullptr, *csr_nbr = nullptr, *lstart = nullptr;
+    const uint8_t *csr_code = nullptr, *lframe = nullptr;
 };
 p2p_status eval_gravity_items(p2p_plan *P, const EvalItems &it, void *phi, void *field);
 
@@ -181,8 +185,8 @@ p2p_status adaptive_leaves(p2p_plan *P, uint32_t t, int min_bits, uint32_t *len_
 p2p_status adaptive_neighbours(p2p_plan *P, uint32_t t, int min_bits, uint32_t *off_h, uint32_t *nbr_h,
                                uint8_t *code_h, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
                                int64_t *n_entries);
-p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, void *phi, void *field, void *red_h, int64_t cap_red,
-                         int64_t *n_red);
+p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, void *phi, void *field, void *red_h,
+                         int64_t cap_red, int64_t *n_red);
 
 // k_pairrec.cu: the thread-level pair-record layout (P2P_PAIRREC)
 p2p_status restructure_pairs(p2p_plan *P);

@@ -1,5 +1,5 @@
 """SURVEY NEXT-1 measurement: the adaptive-leaf path (p2p_adaptive_eval: leaves, closed lists, redundant runs,
-REDUNDANT eval) on BASELINE configs[2]'s clustered 10^6 Plummer input (128^3 finest boxes, periodic) for several
+REDUNDANT eval, and the INDEXED baseline on the same leaves) on BASELINE configs[2]'s clustered 10^6 Plummer input (128^3 finest boxes, periodic) for several
 clustering thresholds t, next to the uniform-grid path on the same plan.  Kernel times from CUPTI (torch.profiler,
 warm, no serialisation); pairs from the returned CSR.  Prints one JSON line per t.
 usage: python scripts/bench_adaptive.py [t,t,...]"""
@@ -53,6 +53,9 @@ with P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=in
         cnt = np.diff(np.append(st.astype(np.int64), inp.n))
         I = int(sum(cnt[a] * cnt[nbr[off[a]:off[a + 1]]].sum() for a in range(len(cnt))))
         k = kernel_times(lambda: P.p2p_adaptive_eval(plan.handle, t, 9, phi.data_ptr(), fld.data_ptr()))
+        ki = kernel_times(lambda: P.p2p_adaptive_eval(plan.handle, t, 9, phi.data_ptr(), fld.data_ptr(),
+                                                      layout=P.P2P_INDEXED))
+        ev_idx = ki.get("k_eval_gravity", 0.0) * 1e-6
         ev = k.get("k_eval_gravity", 0.0) * 1e-6
         rs = k.get("k_adapt_restructure_chunks", 0.0) * 1e-6
         build = sum(v for n, v in k.items() if n in ("k_leaf_len", "k_dil_ranges", "k_dil_fill", "k_dil_merge", "k_leaf_keys", "k_scan_reduce",
@@ -63,6 +66,8 @@ with P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=in
                           "eval_ms": ev * 1e3, "restructure_ms": rs * 1e3, "structure_kernels_ms": build * 1e3,
                           "eval_pairs_per_s": I / ev if ev else None, "eval_frac_fp32": I / ev / peak if ev else None,
                           "restr_plus_eval_pairs_per_s": I / (ev + rs) if ev else None,
+                          "indexed_eval_ms": ev_idx * 1e3, "redundant_kernel_vs_indexed": ev_idx / ev if ev else None,
+                          "redundant_e2e_vs_indexed": ev_idx / (ev + rs) if ev else None,
                           "grid_pairs": I_grid, "grid_eval_ms": grid.get("k_eval_gravity", 0) * 1e-3,
                           "grid_restructure_ms": grid.get("k_restructure_gravity", 0) * 1e-3,
                           "kernels_us": {n: round(v, 1) for n, v in k.items()}}), flush=True)

@@ -180,3 +180,25 @@ def test_adaptive_errors_and_determinism(P):
         plan.restructure()
         gphi, _ = plan.eval(P.P2P_REDUNDANT)
         assert torch.isfinite(gphi).all()
+
+
+@pytest.mark.parametrize("seed,t,dtype", [(1, 8, np.float32), (3, 3, np.float32), (4, 32, np.float64),
+                                          (6, 64, np.float32)])
+def test_adaptive_indexed_baseline(P, seed, t, dtype):
+    """the non-redundant baseline on the leaves (rows longer than a warp included) vs the oracle and vs REDUNDANT"""
+    inp = G.plummer(3000, 32, seed=seed, dtype=dtype)
+    tr = A.AdaptiveTree(inp, t)
+    assert max(len(x) for x in tr.neighbours()) > 32
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    out = {}
+    with _plan(P, inp) as plan:
+        for lay in (P.P2P_REDUNDANT, P.P2P_INDEXED):
+            phi = torch.empty(inp.n, dtype=tdt, device="cuda")
+            fld = torch.empty((inp.n, 3), dtype=tdt, device="cuda")
+            P.p2p_adaptive_eval(plan.handle, t, 9, phi.data_ptr(), fld.data_ptr(), layout=lay)
+            torch.cuda.synchronize()
+            out[lay] = (phi.cpu().numpy(), fld.cpu().numpy())
+    rphi, rf = tr.eval(inp.eps)
+    tol = 1e-5 if dtype == np.float32 else 1e-12
+    for lay, (phi, fld) in out.items():
+        assert oracle.rel_l2(phi, rphi) <= tol and oracle.rel_l2(fld, rf) <= tol, lay
