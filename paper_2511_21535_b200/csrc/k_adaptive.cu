@@ -148,67 +148,72 @@ __global__ void k_dil_ranges(const uint32_t *__restrict__ lkey, const uint32_t *
     }
 }
 
-// pass 2: thread per leaf: its 27 ranges sorted by start, the dilation entries in (leaf) order, the transposed ones
-// appended to the finer leaves' lists
+// pass 2: warp per leaf, lane per neighbour cell: a range's output position is the total length of the ranges that
+// start before it (the ranges are disjoint), so the dilation entries land in (leaf) order without sorting; the
+// transposed entries are appended to the finer leaves' lists (atomic cursors)
 __global__ void k_dil_fill(const uint32_t *__restrict__ llen, uint32_t L, const uint2 *__restrict__ rng,
                            const uint8_t *__restrict__ rcode, const uint32_t *__restrict__ off,
                            const unsigned int *__restrict__ dcnt, unsigned int *__restrict__ tcur,
                            uint32_t *__restrict__ nbr, uint8_t *__restrict__ code) {
-    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
-        uint32_t r0[27], r1[27], rc[27];
-        for (int k = 0; k < 27; ++k) {  // insertion by start
-            const uint2 v = rng[27ull * a + k];
-            const uint32_t c = rcode[27ull * a + k];
-            int j = k - 1;
-            while (j >= 0 && r0[j] > v.x) {
-                r0[j + 1] = r0[j];
-                r1[j + 1] = r1[j];
-                rc[j + 1] = rc[j];
-                --j;
-            }
-            r0[j + 1] = v.x;
-            r1[j + 1] = v.y;
-            rc[j + 1] = c;
+    constexpr unsigned FULL = 0xffffffffu;
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < L; a += nw) {
+        uint32_t i0 = 0, i1 = 0, c = 0;
+        if (lane < 27) {
+            const uint2 v = rng[27ull * a + lane];
+            i0 = v.x;
+            i1 = v.y;
+            c = rcode[27ull * a + lane];
+        }
+        const uint32_t n = i1 - i0;
+        uint32_t pos = 0;
+        for (int q = 0; q < 27; ++q) {
+            const uint32_t sq = __shfl_sync(FULL, i0, q), nq = __shfl_sync(FULL, n, q);
+            if (sq < i0) pos += nq;
         }
         const uint32_t la = llen[a];
-        uint32_t o = off[a];
-        for (int r = 0; r < 27; ++r)
-            for (uint32_t i = r0[r]; i < r1[r]; ++i) {
-                nbr[o] = i;
-                code[o++] = (uint8_t)rc[r];
-                if (llen[i] > la) {
-                    const uint32_t slot = off[i] + dcnt[i] + atomicAdd(&tcur[i], 1u);
-                    nbr[slot] = a;
-                    code[slot] = (uint8_t)(26u - rc[r]);
-                }
+        uint32_t o = off[a] + pos;
+        for (uint32_t i = i0; i < i1; ++i) {
+            nbr[o] = i;
+            code[o++] = (uint8_t)c;
+            if (llen[i] > la) {
+                const uint32_t slot = off[i] + dcnt[i] + atomicAdd(&tcur[i], 1u);
+                nbr[slot] = a;
+                code[slot] = (uint8_t)(26u - c);
             }
+        }
     }
 }
 
-// pass 3: sort the transposed entries of each leaf by leaf index and merge them with its sorted dilation run
+// pass 3: warp per leaf: the transposed tail (coarser leaves, distinct from the dilation's) merged into the sorted
+// dilation run -- every entry's final position is its rank among the tail plus its rank among the dilation run
 __global__ void k_dil_merge(const uint32_t *__restrict__ off, const unsigned int *__restrict__ dcnt, uint32_t L,
-                            uint32_t *__restrict__ nbr, uint8_t *__restrict__ code, uint32_t *__restrict__ nbr_out,
-                            uint8_t *__restrict__ code_out) {
-    for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
-        const uint32_t o = off[a], d = dcnt[a], e = off[a + 1];
-        for (uint32_t i = o + d + 1; i < e; ++i) {  // insertion sort of the transposed tail (few entries)
-            const uint32_t v = nbr[i];
-            const uint8_t c = code[i];
-            uint32_t j = i;
-            while (j > o + d && nbr[j - 1] > v) {
-                nbr[j] = nbr[j - 1];
-                code[j] = code[j - 1];
-                --j;
+                            const uint32_t *__restrict__ nbr, const uint8_t *__restrict__ code,
+                            uint32_t *__restrict__ nbr_out, uint8_t *__restrict__ code_out) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < L; a += nw) {
+        const uint32_t o = off[a], d = dcnt[a], e = off[a + 1], T = e - o - d;
+        for (uint32_t t = lane; t < T; t += 32) {
+            const uint32_t tv = nbr[o + d + t];
+            uint32_t rank = 0;  // tail entries below tv
+            for (uint32_t k = 0; k < T; ++k) rank += nbr[o + d + k] < tv ? 1u : 0u;
+            uint32_t lo = 0, hi = d;  // dilation entries below tv
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (nbr[o + mid] < tv) lo = mid + 1;
+                else hi = mid;
             }
-            nbr[j] = v;
-            code[j] = c;
+            nbr_out[o + rank + lo] = tv;
+            code_out[o + rank + lo] = code[o + d + t];
         }
-        uint32_t p = o, q = o + d, w = o;
-        while (p < o + d || q < e) {
-            const bool takep = q >= e || (p < o + d && nbr[p] < nbr[q]);
-            const uint32_t s = takep ? p++ : q++;
-            nbr_out[w] = nbr[s];
-            code_out[w++] = code[s];
+        for (uint32_t i = lane; i < d; i += 32) {
+            const uint32_t v = nbr[o + i];
+            uint32_t below = 0;  // tail entries below v
+            for (uint32_t k = 0; k < T; ++k) below += nbr[o + d + k] < v ? 1u : 0u;
+            nbr_out[o + i + below] = v;
+            code_out[o + i + below] = code[o + i];
         }
     }
 }
@@ -502,10 +507,11 @@ static p2p_status build_adaptive(p2p_plan *P, uint32_t t, int min_bits, Adaptive
     P2P_CUDA_TRY(dalloc((void **)&A.code, e1, st));
     P2P_CUDA_TRY(dalloc((void **)&nbr_t, 4 * e1, st));
     P2P_CUDA_TRY(dalloc((void **)&code_t, e1, st));
-    P2P_LAUNCH(k_dil_fill, g, 128, 0, st, A.len, (uint32_t)L, rng, rcode, (const uint32_t *)A.off,
+    const unsigned gwl = std::max<unsigned>(1, std::min<unsigned>(div_up(32 * (uint64_t)L, 256), (unsigned)P->num_sms * 16));
+    P2P_LAUNCH(k_dil_fill, gwl, 256, 0, st, A.len, (uint32_t)L, rng, rcode, (const uint32_t *)A.off,
                (const unsigned int *)dcnt, tcur, nbr_t, code_t);
-    P2P_LAUNCH(k_dil_merge, g, 128, 0, st, (const uint32_t *)A.off, (const unsigned int *)dcnt, (uint32_t)L, nbr_t,
-               code_t, A.nbr, A.code);
+    P2P_LAUNCH(k_dil_merge, gwl, 256, 0, st, (const uint32_t *)A.off, (const unsigned int *)dcnt, (uint32_t)L,
+               (const uint32_t *)nbr_t, (const uint8_t *)code_t, A.nbr, A.code);
     void *bufs[] = {dpre, dcnt, tcnt, tcur, rng, rcode, tot, scratch, nbr_t, code_t};
     for (void *p : bufs) dfree(p, st);
     P2P_CUDA_TRY(cudaGetLastError());
