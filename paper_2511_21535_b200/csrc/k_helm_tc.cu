@@ -23,6 +23,7 @@
 //   epilogue (warps 0-3)  tcgen05.ld of the accumulator rows (TMEM lane = box), scatter to input order
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -124,7 +125,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 template <int T>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_helm_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWhi,
-              const __grid_constant__ CUtensorMap tmWlo, const uint32_t *__restrict__ bstart,
+              const __grid_constant__ CUtensorMap tmWlo, uint32_t rf, const uint32_t *__restrict__ bstart,
               const uint32_t *__restrict__ perm, uint32_t B, float2 *__restrict__ y) {
     constexpr int N = 2 * T, K = 18 * T, NKT = K / TC_BK;
     constexpr uint32_t X_BYTES = TC_BM * TC_BK * 4, W_BYTES = N * TC_BK * 4;
@@ -180,8 +181,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const uint32_t st = ring + s * STAGE_BYTES;
                 mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
                 tma_load_2d(st, &tmX, kt * TC_BK, (int)m0, cvta_smem(&full[s]));
-                tma_load_2d(st + X_BYTES, &tmWhi, kt * TC_BK, 0, cvta_smem(&full[s]));
-                tma_load_2d(st + X_BYTES + W_BYTES, &tmWlo, kt * TC_BK, 0, cvta_smem(&full[s]));
+                // block-level redundancy (RF copies of the pattern table): CTA b reads copy b mod RF
+                const int wrow = (int)((blockIdx.x % rf) * N);
+                tma_load_2d(st + X_BYTES, &tmWhi, kt * TC_BK, wrow, cvta_smem(&full[s]));
+                tma_load_2d(st + X_BYTES + W_BYTES, &tmWlo, kt * TC_BK, wrow, cvta_smem(&full[s]));
             }
         }
     } else if (warp == 5) {
@@ -324,14 +327,15 @@ p2p_status launch_tc(p2p_plan *P, void *y) {
     constexpr uint32_t STAGE_BYTES = TC_BM * TC_BK * 4 + 2 * N * TC_BK * 4;
     const int smem = (int)(TC_STAGES * STAGE_BYTES + 1024);
     CUtensorMap mx, mwh, mwl;
-    const float *W = (const float *)P->tc_table;
-    if (!make_map(&mx, P->red, (uint64_t)P->B, K, TC_BM) || !make_map(&mwh, W, N, K, N) ||
-        !make_map(&mwl, W + (size_t)N * K, N, K, N)) {
+    const float *W = (const float *)P->tc_table;  // [RF] copies of W hi, then [RF] copies of W lo
+    const uint32_t rf = (uint32_t)P->tc_rf;
+    if (!make_map(&mx, P->red, (uint64_t)P->B, K, TC_BM) || !make_map(&mwh, W, (uint64_t)rf * N, K, N) ||
+        !make_map(&mwl, W + (size_t)rf * N * K, (uint64_t)rf * N, K, N)) {
         set_error("cuTensorMapEncodeTiled unavailable or rejected the Helmholtz operands");
         return P2P_ERR_CUDA;
     }
     P2P_CUDA_TRY(cudaFuncSetAttribute(k_helm_tc<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    P2P_LAUNCH(k_helm_tc<T>, div_up((uint64_t)P->B, TC_BM), TC_THREADS, smem, P->stream, mx, mwh, mwl, P->bstart,
+    P2P_LAUNCH(k_helm_tc<T>, div_up((uint64_t)P->B, TC_BM), TC_THREADS, smem, P->stream, mx, mwh, mwl, rf, P->bstart,
                P->perm, (uint32_t)P->B, (float2 *)y);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
@@ -363,8 +367,17 @@ p2p_status helmholtz_tc_table(p2p_plan *P, const float *Pf /* host, [t][9t] comp
                                  (size_t)(t + i) * K + 2 * c + 1};
             for (int e = 0; e < 4; ++e) split(v[e], hi[q[e]], lo[q[e]]);
         }
-    P2P_CUDA_TRY(dalloc(&P->tc_table, w.size() * 4, P->stream));
-    P2P_CUDA_TRY(cudaMemcpyAsync(P->tc_table, w.data(), w.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    // RF copies (P2P_HELM_RF, default 1: measured no gain): [RF] x W hi, then [RF] x W lo
+    const char *e = getenv("P2P_HELM_RF");
+    const int rf = e ? std::max(1, std::min(8, atoi(e))) : 1;
+    P->tc_rf = rf;
+    std::vector<float> wr((size_t)2 * rf * N * K);
+    for (int r = 0; r < rf; ++r) {
+        std::memcpy(wr.data() + (size_t)r * N * K, hi, sizeof(float) * N * K);
+        std::memcpy(wr.data() + (size_t)(rf + r) * N * K, lo, sizeof(float) * N * K);
+    }
+    P2P_CUDA_TRY(dalloc(&P->tc_table, wr.size() * 4, P->stream));
+    P2P_CUDA_TRY(cudaMemcpyAsync(P->tc_table, wr.data(), wr.size() * 4, cudaMemcpyHostToDevice, P->stream));
     P2P_CUDA_TRY(cudaStreamSynchronize(P->stream));
     return P2P_OK;
 }

@@ -91,6 +91,7 @@ struct p2p_plan {
     void *red = nullptr;         // gravity red[R] records; helmholtz Xg[B][9][t]
     void *table = nullptr;       // helmholtz pattern table P[t][9t] complex
     void *tc_table = nullptr;    // helmholtz tensor-core operand: real W hi / lo, 2 x [2t][18t] fp32 (k_helm_tc.cu)
+    int tc_rf = 1;               // copies of W (block-level redundancy factor RF)
     p2p::DevCounters *ctr = nullptr;
     // capacity-sized scratch, allocated once per plan (p2p_plan_update reuses it: no allocation, no sync)
     int64_t cap = 0, bcap = 0, red_cap = 0;
