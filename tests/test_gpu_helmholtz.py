@@ -106,3 +106,20 @@ def test_set_charges_dbim_iterations(P):
             ref = oracle.HelmholtzPlan(G.HelmholtzInput(inp.pos, x, inp.lo, inp.h, inp.nbox, inp.t, inp.delta,
                                                         inp.k)).eval_table()
             assert oracle.rel_l2(y, ref) < 1e-5
+
+
+def test_rf_copies_bitwise_equal(P, monkeypatch):
+    """NEXT-2 block-level redundancy: RF copies of the tensor-core operand W give the RF = 1 result bit for
+    bit (every CTA reads an identical copy)"""
+    import numpy as np
+    import p2p_inputs as G
+    h = G.dbim_lattice(32, 64, seed=3)
+    xr = torch.from_numpy(h.x.view(np.float32).reshape(-1, 2)).cuda()
+    pos = torch.from_numpy(h.pos).cuda()
+    out = []
+    for rf in ("1", "2", "4"):
+        monkeypatch.setenv("P2P_HELM_RF", rf)
+        with P.Plan(P.P2P_HELMHOLTZ2D, pos, xr, h.h, h.lo, h.nbox, 0, k=h.k, t=h.t) as plan:
+            plan.restructure()
+            out.append(plan.eval(P.P2P_REDUNDANT).cpu().numpy().tobytes())
+    assert out[0] == out[1] == out[2]
