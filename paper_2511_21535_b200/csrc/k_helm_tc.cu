@@ -122,8 +122,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// t = 16: half the TMEM (256 columns: 4 accumulators + 2 operand stages) and 96 KB of shared memory per CTA, so two
+// CTAs share an SM (the grid of 512 small tiles was 3.5 waves of one CTA per SM); t = 64: the whole TMEM
 template <int T>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+constexpr uint32_t tc_tcols() { return T == 16 ? 256u : 512u; }
+
+template <int T>
+__global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
     k_helm_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWhi,
               const __grid_constant__ CUtensorMap tmWlo, uint32_t rf, const uint32_t *__restrict__ bstart,
               const uint32_t *__restrict__ perm, uint32_t B, float2 *__restrict__ y) {
@@ -131,9 +136,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr uint32_t X_BYTES = TC_BM * TC_BK * 4, W_BYTES = N * TC_BK * 4;
     constexpr uint32_t STAGE_BYTES = X_BYTES + 2 * W_BYTES;  // X (raw fp32), W hi, W lo
     constexpr uint32_t AST = N < 32 ? 32 : N;                 // TMEM columns per accumulator
-    constexpr int NACC = tc_nacc<N>();
-    constexpr uint32_t ACOL = NACC * AST;                     // first TMEM column of the A stages
-    constexpr int ASTAGES = (int)((512 - ACOL) / (2 * TC_BK)); // X hi + X lo = 64 columns per stage
+    constexpr uint32_t TCOLS = tc_tcols<T>();
+    constexpr int NACC = T == 16 ? 4 : tc_nacc<N>();
+    constexpr uint32_t ACOL = NACC * AST;                       // first TMEM column of the A stages
+    constexpr int ASTAGES = (int)((TCOLS - ACOL) / (2 * TC_BK)); // X hi + X lo = 64 columns per stage
     static_assert(ASTAGES >= 2, "TMEM budget");
     // instruction descriptor: D fp32, A/B TF32, both K-major, N >> 3, M >> 4
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
@@ -161,9 +167,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_init(&accum, 1);
         fence_mbar_init();
     }
-    if (warp == 0) {  // all 512 TMEM columns: NACC accumulators + ASTAGES (X hi, X lo) operand stages
+    if (warp == 0) {  // TCOLS TMEM columns: NACC accumulators + ASTAGES (X hi, X lo) operand stages
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cvta_smem(&tmem_base)),
-                     "r"(512)
+                     "r"(TCOLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
     }
 }
 
