@@ -104,6 +104,21 @@ __global__ void k_bin_helmholtz(const T *__restrict__ pos, uint32_t n, Geom g, i
 // ------------------------------------------------------------------------------------------------ a3
 // random gather (input order is arbitrary) of {x,y,z,m} records: one 16 B (fp64: 32 B) load per particle,
 // 4 particles per thread iteration, all loads issued before the stores (memory-level parallelism)
+#ifndef P2P_PERMUTE_CS
+#define P2P_PERMUTE_CS 1
+#endif
+#if P2P_PERMUTE_CS  // streaming perm reads / record stores leave L2 to the gathered lines (8 records each): 231 -> 227 us
+#define P2P_PERM_LD(p) __ldcs(p)
+#define P2P_REC_ST(p, v) st_stream(p, v)
+#else
+#define P2P_PERM_LD(p) (*(p))
+#define P2P_REC_ST(p, v) (*(p) = (v))
+#endif
+__device__ __forceinline__ void st_stream(float4 *p, const float4 &v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double4 *p, const double4 &v) {
+    __stcs(reinterpret_cast<double2 *>(p), make_double2(v.x, v.y));
+    __stcs(reinterpret_cast<double2 *>(p) + 1, make_double2(v.z, v.w));
+}
 template <typename V4>
 __global__ void k_permute_gravity(const V4 *__restrict__ src, const uint32_t *__restrict__ perm, uint32_t n,
                                   V4 *__restrict__ rec) {
@@ -112,14 +127,14 @@ __global__ void k_permute_gravity(const V4 *__restrict__ src, const uint32_t *__
     for (uint32_t p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += U * stride) {
         uint32_t i[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) i[u] = p0 + u * stride < n ? perm[p0 + u * stride] : 0u;
+        for (int u = 0; u < U; ++u) i[u] = p0 + u * stride < n ? P2P_PERM_LD(perm + p0 + u * stride) : 0u;
         V4 r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (p0 + u * stride < n) r[u] = src[i[u]];
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (p0 + u * stride < n) rec[p0 + u * stride] = r[u];
+            if (p0 + u * stride < n) P2P_REC_ST(rec + p0 + u * stride, r[u]);
     }
 }
 
