@@ -64,7 +64,8 @@ typedef enum {
     P2P_ERR_BAD_STATE = 6,        /* eval(REDUNDANT) before restructure / after set_charges, ... */
     P2P_ERR_UNSUPPORTED = 7       /* key overflow (> 1024 boxes per dim in 3D, > 2^32 keys in 2D),
                                      Helmholtz input that is not a regular t-per-box lattice,
-                                     n_local >= 2^31 */
+                                     n_local >= 2^30 (u32 indices; the radix sort's look-back packs
+                                     per-digit prefixes into 30-bit fields) */
 } p2p_status;
 
 typedef enum { P2P_GRAVITY = 0, P2P_HELMHOLTZ2D = 1 } p2p_kernel;
@@ -202,7 +203,11 @@ p2p_status p2p_eval(p2p_plan *plan, p2p_layout layout, void *potential, void *fi
  * again before eval(REDUNDANT)).  Enqueue only. */
 p2p_status p2p_set_charges(p2p_plan *plan, const void *charges);
 
-/* Free every plan-owned buffer (stream-ordered).  NULL-safe. */
+/* Free every plan-owned buffer (stream-ordered).  NULL-safe.
+ * Memory: plan buffers come from a LIBRARY-OWNED stream-ordered pool per device (cudaMemPoolCreate; the device's
+ * default pool and PyTorch's caching allocator are untouched).  Freed blocks stay reserved in that pool while any
+ * plan on the device is alive (cheap regrowth inside a time-step loop); destroying the LAST live plan of a device
+ * synchronises the plan's stream and trims the pool to zero, returning the memory to the driver. */
 void p2p_destroy(p2p_plan *plan);
 
 /* ---- introspection for bit-exact parity (copy-out only; never hands out internal pointers) ---- */

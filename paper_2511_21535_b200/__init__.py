@@ -323,6 +323,27 @@ def _stream_handle(stream) -> int | None:
     return s.cuda_stream
 
 
+def _check_inputs(kernel: int, positions, charges, dtype=None, device=None):
+    """the C ABI cannot see dtypes or shapes: reject mismatches here (argument checking, no arithmetic)"""
+    import torch
+    dim = 3 if kernel == P2P_GRAVITY else 2
+    if positions.dtype not in (torch.float32, torch.float64):
+        raise P2PError(P2P_ERR_INVALID_ARGUMENT, f"positions must be float32 or float64, got {positions.dtype}")
+    if dtype is not None and positions.dtype != dtype:
+        raise P2PError(P2P_ERR_INVALID_ARGUMENT, f"positions dtype {positions.dtype} != the plan's {dtype}")
+    if charges.dtype != positions.dtype:
+        raise P2PError(P2P_ERR_INVALID_ARGUMENT,
+                       f"charges dtype {charges.dtype} != positions dtype {positions.dtype}")
+    if positions.dim() != 2 or positions.shape[1] != dim:
+        raise P2PError(P2P_ERR_INVALID_ARGUMENT, f"positions must be [N][{dim}], got {tuple(positions.shape)}")
+    n = positions.shape[0]
+    want = (n,) if kernel == P2P_GRAVITY else (n, 2)
+    if tuple(charges.shape) != want:
+        raise P2PError(P2P_ERR_INVALID_ARGUMENT, f"charges must be {list(want)}, got {tuple(charges.shape)}")
+    if positions.device != charges.device or (device is not None and positions.device.type != device):
+        raise P2PError(P2P_ERR_INVALID_ARGUMENT, "positions and charges must be on the same (expected) device")
+
+
 class Plan:
     """RAII wrapper of a p2p_plan over torch CUDA tensors (positions [N][dim], charges [N] real or [N][2] complex)."""
 
@@ -330,6 +351,7 @@ class Plan:
                  k: float = 0.0, t: int = 0, stream=None, comm: int | None = None):
         import torch
         assert positions.is_cuda and charges.is_cuda, "positions / charges must be CUDA tensors"
+        _check_inputs(kernel, positions, charges)
         positions = positions.contiguous()
         charges = charges.contiguous()
         prec = P2P_FP64 if positions.dtype == torch.float64 else P2P_FP32
@@ -358,6 +380,7 @@ class Plan:
     def update(self, positions, charges):
         """a PhotoNs-like time step: rebuild a1..a5 for moved particles, asynchronously (no host sync); the
         sizes in self.info refresh lazily (refresh_info() synchronises and reports input errors)."""
+        _check_inputs(self.kernel, positions, charges, self.dtype, "cuda")
         positions = positions.contiguous()
         charges = charges.contiguous()
         self.n = int(positions.shape[0])
@@ -371,6 +394,7 @@ class Plan:
         alive until the stream passes the copy."""
         positions = _host_array(positions, self.dtype)
         charges = _host_array(charges, self.dtype)
+        _check_inputs(self.kernel, positions, charges, self.dtype, "cpu")
         self.n = int(positions.shape[0])
         p2p_plan_update_host(self.handle, self.n, _host_ptr(positions), _host_ptr(charges))
         self._keep = (positions, charges)
@@ -398,6 +422,9 @@ class Plan:
         p2p_restructure_pairs(self.handle)
 
     def set_charges(self, charges):
+        want = (self.n,) if self.kernel == P2P_GRAVITY else (self.n, 2)
+        if charges.dtype != self.dtype or tuple(charges.shape) != want or not charges.is_cuda:
+            raise P2PError(P2P_ERR_INVALID_ARGUMENT, f"charges must be a CUDA {self.dtype} tensor of shape {want}")
         p2p_set_charges(self.handle, charges.contiguous().data_ptr())
 
     def eval(self, layout: int = P2P_REDUNDANT, potential=None, field=None, want_field: bool = True):

@@ -42,11 +42,20 @@ def _compile(src: str, incs) -> tuple:
     return obj, p.stderr
 
 
+STAMP = OUT + ".flags"  # the flag set libp2p.so was built with: a different P2P_NVCC_FLAGS forces a rebuild
+
+
+def _flag_stamp() -> str:
+    return " ".join([NVCC, *FLAGS, *os.environ.get("P2P_NVCC_FLAGS", "").split()])
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp")) + \
         [os.path.join(ROOT, "include", "p2p.h"), __file__]
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
+    stamp_ok = os.path.exists(STAMP) and open(STAMP).read() == _flag_stamp()
+    if not force and stamp_ok and os.path.exists(OUT) and \
+            os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
         return OUT
     os.makedirs(BUILD, exist_ok=True)
     nccl = _nccl_dir()
@@ -66,6 +75,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if p.returncode != 0:
         raise RuntimeError(f"link failed:\n{p.stderr}")
     os.replace(tmp, OUT)
+    with open(STAMP, "w") as f:
+        f.write(_flag_stamp())
     return OUT
 
 

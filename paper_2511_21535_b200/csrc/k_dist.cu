@@ -535,9 +535,9 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
         n_loc += (int64_t)(gr[2 * me] + gr[2 * me + 1]);
         n_own += (int64_t)gr[2 * me];
     }
-    if (o_sent != (int64_t)n_in || n_loc >= ((int64_t)1 << 31)) {
+    if (o_sent != (int64_t)n_in || n_loc >= ((int64_t)1 << 30)) {
         set_error(o_sent != (int64_t)n_in ? "route: owned entries != input particles (internal)"
-                                          : "local plan over owned + halo particles would exceed 2^31");
+                                          : "local plan over owned + halo particles would reach 2^30 (radix look-back 30-bit digit prefixes)");
         return o_sent != (int64_t)n_in ? P2P_ERR_CUDA : P2P_ERR_UNSUPPORTED;
     }
     P->n_own = n_own;

@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "plan.hpp"
@@ -17,8 +19,6 @@ static thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
 
 void set_error(const std::string &msg) { g_err = msg; }
-
-static bool g_pool_configured = false;
 
 // P2P_TRACE=1: host-side phase timestamps of p2p_plan_create on stderr (diagnostics only)
 static bool trace_on() {
@@ -38,20 +38,62 @@ struct Tracer {
     }
 };
 
+// Library-owned stream-ordered memory pool, one per device (the device's DEFAULT pool is never touched, so
+// other cudaMallocAsync users and PyTorch's caching allocator see no change).  Freed blocks stay in the pool while
+// a plan is alive on the device (time steps that grow / shrink plan buffers or create and destroy plans stay
+// cheap); when the last plan of the device is destroyed the pool is trimmed to zero and its memory returns to the
+// driver (p2p.h: p2p_destroy).
+static std::mutex g_pool_mu;
+static std::map<int, cudaMemPool_t> g_pools;
+static std::map<int, int> g_live_plans;
+
+static cudaMemPool_t lib_pool(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pools.find(dev);
+    if (it != g_pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    g_pools[dev] = pool;
+    return pool;
+}
+
+void plan_opened(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    ++g_live_plans[dev];
+}
+
+// called after the plan's frees were enqueued; trims the pool once no plan of the device is alive
+void plan_closed(int dev, cudaStream_t st) {
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (--g_live_plans[dev] > 0) return;
+        auto it = g_pools.find(dev);
+        if (it == g_pools.end()) return;
+        pool = it->second;
+    }
+    cudaStreamSynchronize(st);  // the stream-ordered frees must have executed before the trim can return them
+    cudaMemPoolTrimTo(pool, 0);
+}
+
 cudaError_t dalloc(void **p, size_t bytes, cudaStream_t st) {
     *p = nullptr;
     if (bytes == 0) bytes = 16;
-    if (!g_pool_configured) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;  // keep freed blocks for reuse: plan create/destroy per step stays cheap
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        g_pool_configured = true;
-    }
-    return cudaMallocAsync(p, bytes, st);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = lib_pool(dev);
+    if (!pool) return cudaMallocAsync(p, bytes, st);
+    return cudaMallocFromPoolAsync(p, bytes, pool, st);
 }
 
 void dfree(void *p, cudaStream_t st) {
@@ -164,7 +206,8 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
     *out = nullptr;
     if (!cfg) return fail(P2P_ERR_INVALID_ARGUMENT, "cfg is NULL");
     if (n_local < 0) return fail(P2P_ERR_INVALID_ARGUMENT, "n_local < 0");
-    if (n_local >= (int64_t)1 << 31) return fail(P2P_ERR_UNSUPPORTED, "n_local >= 2^31 (u32 indices)");
+    if (n_local >= (int64_t)1 << 30)
+        return fail(P2P_ERR_UNSUPPORTED, "n_local >= 2^30 (the radix look-back packs digit prefixes into 30 bits)");
     const bool grav = cfg->kernel == P2P_GRAVITY;
     if (!grav && cfg->kernel != P2P_HELMHOLTZ2D) return fail(P2P_ERR_INVALID_ARGUMENT, "unknown kernel");
     if (cfg->precision != P2P_FP32 && cfg->precision != P2P_FP64)
@@ -239,9 +282,11 @@ p2p_status p2p_plan_create(const p2p_config *cfg, int64_t n_local, const void *p
     P->passes = (P->key_bits + 7) / 8;
 
     cudaStream_t st = P->stream;
+    plan_opened(P->device);
     auto bail = [&](p2p_status s) {
         free_plan_buffers(P);
         cudaStreamSynchronize(st);
+        plan_closed(P->device, st);
         delete P;
         return s;
     };
@@ -325,7 +370,8 @@ p2p_status p2p_plan_update(p2p_plan *P, int64_t n_local, const void *positions, 
     if (P->cfg.kernel != P2P_GRAVITY)
         return fail(P2P_ERR_UNSUPPORTED, "p2p_plan_update is for gravity plans (DBIM geometry is fixed: use set_charges)");
     if (n_local < 0) return fail(P2P_ERR_INVALID_ARGUMENT, "n_local < 0");
-    if (n_local >= (int64_t)1 << 31) return fail(P2P_ERR_UNSUPPORTED, "n_local >= 2^31 (u32 indices)");
+    if (n_local >= (int64_t)1 << 30)
+        return fail(P2P_ERR_UNSUPPORTED, "n_local >= 2^30 (the radix look-back packs digit prefixes into 30 bits)");
     if (n_local > 0 && (!is_device_ptr(positions) || !is_device_ptr(charges)))
         return fail(P2P_ERR_INVALID_ARGUMENT, "positions / charges must be device pointers");
     cudaStream_t st = P->stream;
@@ -590,6 +636,7 @@ void p2p_destroy(p2p_plan *P) {
     cudaGetDevice(&dev);
     if (dev != P->device) cudaSetDevice(P->device);
     free_plan_buffers(P);
+    plan_closed(P->device, P->stream);
     delete P;
 }
 

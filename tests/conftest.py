@@ -4,6 +4,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+HERE = os.path.dirname(os.path.abspath(__file__))   # test helpers (p2p_bounds); a site-packages `tests` shadows
+if HERE not in sys.path:                              # the name `tests`, so helpers are imported by module name
+    sys.path.insert(0, HERE)
 
 
 def pytest_configure(config):

@@ -87,3 +87,38 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".hpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "p2p_oracle" not in txt, f
+
+
+def test_binding_rejects_dtype_and_shape_mismatch():
+    """the ABI cannot see dtypes, so the binding checks them (float64 masses with float32 positions
+    would otherwise be read as float32 and return P2P_OK with garbage)"""
+    import torch
+    import paper_2511_21535_b200 as P
+    pos = torch.zeros(8, 3, dtype=torch.float32)
+    with pytest.raises(P.P2PError):
+        P._check_inputs(P.P2P_GRAVITY, pos, torch.zeros(8, dtype=torch.float64))
+    with pytest.raises(P.P2PError):
+        P._check_inputs(P.P2P_GRAVITY, pos, torch.zeros(7, dtype=torch.float32))
+    with pytest.raises(P.P2PError):
+        P._check_inputs(P.P2P_GRAVITY, torch.zeros(8, 2), torch.zeros(8))
+    with pytest.raises(P.P2PError):
+        P._check_inputs(P.P2P_HELMHOLTZ2D, torch.zeros(8, 2), torch.zeros(8))
+    with pytest.raises(P.P2PError):
+        P._check_inputs(P.P2P_GRAVITY, pos, torch.zeros(8), dtype=torch.float64)
+    P._check_inputs(P.P2P_GRAVITY, pos, torch.zeros(8))
+    P._check_inputs(P.P2P_HELMHOLTZ2D, torch.zeros(8, 2, dtype=torch.float64), torch.zeros(8, 2, dtype=torch.float64))
+
+
+def test_build_stamp_records_the_flags(lib):
+    """libp2p.so built with experiment flags is rebuilt when P2P_NVCC_FLAGS changes"""
+    from paper_2511_21535_b200 import build as B
+    assert os.path.exists(B.STAMP) and open(B.STAMP).read() == B._flag_stamp()
+    old = os.environ.get("P2P_NVCC_FLAGS")
+    os.environ["P2P_NVCC_FLAGS"] = "-DP2P_SOME_EXPERIMENT"
+    try:
+        assert B._flag_stamp() != open(B.STAMP).read()
+    finally:
+        if old is None:
+            del os.environ["P2P_NVCC_FLAGS"]
+        else:
+            os.environ["P2P_NVCC_FLAGS"] = old

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
+import p2p_bounds as bounds
 import p2p_inputs as G
 from oracle import adaptive as A
 
@@ -113,7 +114,7 @@ def test_adaptive_red_and_eval(P, seed, t, dtype):
         phi, fld = phi.cpu().numpy(), fld.cpu().numpy()
     rphi, rf = tr.eval(inp.eps)
     tol = 1e-5 if dtype == np.float32 else 1e-12
-    assert oracle.rel_l2(phi, rphi) <= tol and oracle.rel_l2(fld, rf) <= tol
+    assert bounds.close(phi, rphi, tol) and bounds.close(fld, rf, tol)
 
 
 def test_adaptive_equal_leaves_match_the_grid_path(P):
@@ -126,7 +127,7 @@ def test_adaptive_equal_leaves_match_the_grid_path(P):
         fld = torch.empty((inp.n, 3), device="cuda")
         P.p2p_adaptive_eval(plan.handle, 4, 9, phi.data_ptr(), fld.data_ptr())
         torch.cuda.synchronize()
-    assert oracle.rel_l2(phi.cpu().numpy(), gphi) <= 1e-6 and oracle.rel_l2(fld.cpu().numpy(), gf) <= 1e-6
+    assert bounds.close(phi.cpu().numpy(), gphi, 1e-6) and bounds.close(fld.cpu().numpy(), gf, 1e-6)
 
 
 def test_full_size_sampled(P):
@@ -201,4 +202,4 @@ def test_adaptive_indexed_baseline(P, seed, t, dtype):
     rphi, rf = tr.eval(inp.eps)
     tol = 1e-5 if dtype == np.float32 else 1e-12
     for lay, (phi, fld) in out.items():
-        assert oracle.rel_l2(phi, rphi) <= tol and oracle.rel_l2(fld, rf) <= tol, lay
+        assert bounds.close(phi, rphi, tol) and bounds.close(fld, rf, tol), lay

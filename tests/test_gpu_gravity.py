@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
+import p2p_bounds as bounds
 import p2p_inputs as G
 
 torch = pytest.importorskip("torch")
@@ -64,8 +65,8 @@ def check_case(P, inp, structs=True):
             red = plan.copy_out(P.P2P_ARR_RED)
             assert red.tobytes() == gp.red.tobytes()     # bit-exact redundant buffer
     for name, (phi, f) in out.items():
-        assert oracle.rel_l2(phi, ref_phi) <= TOL[dt], name
-        assert oracle.rel_l2(f, ref_f) <= TOL[dt], name
+        assert bounds.close(phi, ref_phi, TOL[dt]), name
+        assert bounds.close(f, ref_f, TOL[dt]), name
     # REDUNDANT and INDEXED_BITWISE stage identical bits -> identical outputs
     assert out["redundant"][0].tobytes() == out["indexed_bitwise"][0].tobytes()
     assert out["redundant"][1].tobytes() == out["indexed_bitwise"][1].tobytes()
@@ -154,8 +155,8 @@ def test_set_charges_reuses_geometry(P):
         plan.restructure()
         for lay in P.LAYOUTS.values():
             phi, f = plan.eval(lay)
-            assert oracle.rel_l2(phi.cpu().numpy(), rphi) < 1e-5
-            assert oracle.rel_l2(f.cpu().numpy(), rf) < 1e-5
+            assert bounds.close(phi.cpu().numpy(), rphi, 1e-5)
+            assert bounds.close(f.cpu().numpy(), rf, 1e-5)
 
 
 def test_determinism(P):
@@ -175,7 +176,7 @@ def test_nearfield_host_api(P):
                          inp.nbox, inp.periodic, eps=inp.eps)
     assert not phi.is_cuda
     rphi, rf = oracle.GravityPlan(inp).eval_indexed()
-    assert oracle.rel_l2(phi.numpy(), rphi) < 1e-5 and oracle.rel_l2(f.numpy(), rf) < 1e-5
+    assert bounds.close(phi.numpy(), rphi, 1e-5) and bounds.close(f.numpy(), rf, 1e-5)
 
 
 def test_plan_update_time_steps(P):
@@ -192,9 +193,9 @@ def test_plan_update_time_steps(P):
             check_structs(P, plan, gp)
             assert plan.copy_out(P.P2P_ARR_RED).tobytes() == gp.red.tobytes()
             rphi, rf = gp.eval_indexed()
-            assert oracle.rel_l2(phi.cpu().numpy(), rphi) < 1e-5 and oracle.rel_l2(f.cpu().numpy(), rf) < 1e-5
+            assert bounds.close(phi.cpu().numpy(), rphi, 1e-5) and bounds.close(f.cpu().numpy(), rf, 1e-5)
             phi2, f2 = plan.eval(P.P2P_INDEXED)
-            assert oracle.rel_l2(phi2.cpu().numpy(), rphi) < 1e-5 and oracle.rel_l2(f2.cpu().numpy(), rf) < 1e-5
+            assert bounds.close(phi2.cpu().numpy(), rphi, 1e-5) and bounds.close(f2.cpu().numpy(), rf, 1e-5)
 
 
 def test_plan_update_reports_out_of_domain(P):
@@ -230,7 +231,7 @@ def test_host_buffer_entry_points(P):
             assert phi_h.numpy().tobytes() == phi_d.cpu().numpy().tobytes()
             assert f_h.numpy().tobytes() == f_d.cpu().numpy().tobytes()
             rphi, rf = oracle.GravityPlan(inp).eval_indexed()
-            assert oracle.rel_l2(phi_h.numpy(), rphi) < 1e-5 and oracle.rel_l2(f_h.numpy(), rf) < 1e-5
+            assert bounds.close(phi_h.numpy(), rphi, 1e-5) and bounds.close(f_h.numpy(), rf, 1e-5)
             # numpy inputs (pageable) work too; device pointers are rejected
             plan.update_host(inp.pos, inp.mass)
             plan.restructure()

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
+import p2p_bounds as bounds
 import p2p_inputs as G
 
 torch = pytest.importorskip("torch")
@@ -139,7 +140,7 @@ def test_multirank_bitwise_equals_single_gpu(P, case):
     tol = 1e-12 if inp.pos.dtype == np.float64 else 1e-5
     rphi, rf = oracle.GravityPlan(cat, with_red=False).eval_indexed()
     phi = np.concatenate([out[r][P.P2P_REDUNDANT][0] for r in range(nr)])
-    assert oracle.rel_l2(phi, rphi) <= tol
+    assert bounds.close(phi, rphi, tol)
 
 
 def test_nccl_communicator_single_rank(P):

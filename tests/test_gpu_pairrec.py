@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
+import p2p_bounds as bounds
 import p2p_inputs as G
 
 torch = pytest.importorskip("torch")
@@ -66,11 +67,11 @@ def test_pairrec_records_and_values(P, case):
         torch.cuda.synchronize()
         phi, f, phi2, f2 = (x.cpu().numpy() for x in (phi, f, phi2, f2))
     assert phi.tobytes() == phi2.tobytes() and f.tobytes() == f2.tobytes()   # deterministic update
-    assert oracle.rel_l2(phi, ref_phi) <= TOL[dt], case
-    assert oracle.rel_l2(f, ref_f) <= TOL[dt], case
+    assert bounds.close(phi, ref_phi, TOL[dt]), case
+    assert bounds.close(f, ref_f, TOL[dt]), case
     if dt == np.float64:   # fp64: also within 1e-12 of the oracle's own pair-record evaluation
         p3, f3, _ = gp.eval_pairrec()
-        assert oracle.rel_l2(phi, p3) <= 1e-12 and oracle.rel_l2(f, f3) <= 1e-12
+        assert bounds.close(phi, p3, 1e-12) and bounds.close(f, f3, 1e-12)
 
 
 def test_pairrec_plummer_1e6_sampled(P):
@@ -85,8 +86,8 @@ def test_pairrec_plummer_1e6_sampled(P):
         plan.restructure_pairs()
         phi, f = plan.eval(P.P2P_PAIRREC)
         phi, f = phi.cpu().numpy(), f.cpu().numpy()
-    assert oracle.rel_l2(phi[mask], rphi[mask]) <= 1e-5
-    assert oracle.rel_l2(f[mask], rf[mask]) <= 1e-5
+    assert bounds.close(phi[mask], rphi[mask], 1e-5)
+    assert bounds.close(f[mask], rf[mask], 1e-5)
 
 
 def test_pairrec_state_errors(P):
@@ -104,7 +105,7 @@ def test_pairrec_state_errors(P):
         plan.restructure_pairs()                                   # rebuilt after the update
         phi, _ = plan.eval(P.P2P_PAIRREC)
         ref, _ = oracle.GravityPlan(inp, with_red=False).eval_indexed()
-        assert oracle.rel_l2(phi.cpu().numpy(), ref) <= 1e-5
+        assert bounds.close(phi.cpu().numpy(), ref, 1e-5)
     h = G.dbim_lattice(4, 4, seed=0)
     xr = torch.from_numpy(h.x.view(np.float32).reshape(-1, 2)).cuda()
     with P.Plan(P.P2P_HELMHOLTZ2D, torch.from_numpy(h.pos).cuda(), xr, h.h, h.lo, h.nbox, 0, k=h.k, t=h.t) as plan:

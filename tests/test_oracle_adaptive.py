@@ -116,3 +116,61 @@ def test_single_leaf_lists_and_eval_match_the_all_pairs_ones():
         assert A.neighbours_of(tr, a) == nbr[a]
         ti, p, ff = A.eval_leaf(tr, a, inp.eps)
         assert np.allclose(p, phi[ti], rtol=1e-14, atol=0) and np.allclose(ff, f[ti], rtol=1e-13, atol=1e-300)
+
+
+@pytest.mark.parametrize("seed,t,lo", [(11, 3, (-0.3, 0.7, 1.1)), (12, 8, (0.0, 0.0, 0.0)), (13, 20, (2.5, -1.25, 0.6))])
+def test_red_round_trip_unequal_leaves(seed, t, lo):
+    """C24 pinned from outside for UNEQUAL leaves and lo != 0 (value checks cannot catch a wrong
+    origin because it cancels in d = s - t): for every target leaf a, with a's origin and width recomputed here
+    from its (level, prefix) pair by plain arithmetic, every record of a's run moved back by that origin and its
+    entry's image S is its source particle (unique mass), the source lies inside leaf b's own cell, the pair is
+    adjacent in the closed sense (b + S overlaps a dilated by a's width, or a - S overlaps b dilated by b's), and
+    dilation entries (b no coarser than a) lie in [-w_a, 2 w_a) of a's origin."""
+    base = G.plummer(2500, 16, seed=seed, dtype=np.float64)
+    pos = np.ascontiguousarray(base.pos + np.array(lo))
+    inp = G.GravityInput(pos, base.mass, lo, base.h, base.nbox, base.periodic, base.eps)
+    assert len(np.unique(inp.mass)) == inp.n
+    tr = A.AdaptiveTree(inp, t)
+    n = tr.n
+    L = float(n * inp.h)
+    levels = {l for l, _, _, _ in tr.leaves}
+    assert len(levels) >= 3                                   # genuinely unequal leaves
+    nbr = tr.neighbours()
+    red = tr.red(np.float64)
+    by_mass = {float(m): j for j, m in enumerate(inp.mass)}
+
+    def cell(leaf):
+        l, p, _, _ = tr.leaves[leaf]
+        sx, sy, sz = l // 3, (l + 1) // 3, (l + 2) // 3       # halvings per dimension (z first)
+        c = [0, 0, 0]
+        key = p << (3 * tr.m - l)                             # the cell's first finest key
+        for k in range(tr.m):
+            for d in range(3):
+                c[d] |= ((key >> (3 * k + d)) & 1) << k
+        sh = np.array([sx, sy, sz])
+        w = L / (1 << sh).astype(np.float64)
+        cc = np.array(c) >> (tr.m - sh)                       # cell index at this level
+        return np.array(lo) + cc * w, w
+
+    off = 0
+    for a in range(tr.nleaf):
+        oa, wa = cell(a)
+        la = tr.leaves[a][0]
+        for b, code in nbr[a]:
+            ob, wb = cell(b)
+            lb, _, sb, cb = tr.leaves[b]
+            S = np.array([code % 3 - 1, code // 3 % 3 - 1, code // 9 - 1], np.float64) * L
+            seg = red[off:off + cb]
+            off += cb
+            # adjacency (closed): b + S overlaps D(a) or a - S overlaps D(b), positive volume
+            def overlap(x0, w0, y0, wy):
+                return np.all(np.minimum(x0 + w0, y0 + 2 * wy) - np.maximum(x0, y0 - wy) > 1e-12 * L)
+            assert overlap(ob + S, wb, oa, wa) or overlap(oa - S, wa, ob, wb)
+            for rec in seg:
+                j = by_mass[float(rec[3])]
+                back = rec[:3] + oa - S
+                assert np.all(np.abs(back - inp.pos[j]) <= 1e-12 * (L + np.abs(oa)))
+                assert np.all(inp.pos[j] >= ob - 1e-12 * L) and np.all(inp.pos[j] < ob + wb + 1e-12 * L)
+                if lb >= la:
+                    assert np.all(rec[:3] >= -wa * (1 + 1e-9)) and np.all(rec[:3] < 2 * wa * (1 + 1e-9))
+    assert off == len(red)

@@ -298,3 +298,35 @@ def test_empty_and_single():
     inp = _single([[0.1, 0.2, 0.3]], [2.0], dtype=np.float64)
     for phi, field in _all_modes(inp):
         assert phi[0] == 0.0 and np.all(field == 0.0)
+
+
+@pytest.mark.parametrize("dt,per", [(np.float64, 0b111), (np.float32, 0b101), (np.float64, 0b000)])
+def test_red_round_trip_coordinates_nonzero_lo(dt, per):
+    """C11 pinned from outside with lo != 0: every record of box b's run, moved back by b's
+    origin lo + c_b h (computed here from the box key by plain arithmetic, not by the oracle's fma), is its source
+    particle (identified by its unique mass) up to ONE periodic image S_d in {-L_d, 0, +L_d} (0 if open), that
+    image is the box-level one (the source box, shifted by S, is a stencil neighbour of b), and the record lies
+    in [-h, 2h) of b's origin.  A wrong origin, a wrong image sign or a transposed component fails here."""
+    lo, h, nbox = (-0.4, 0.25, 2.0), 0.13, (5, 4, 6)
+    inp = G.random_gravity(1500, 0, seed=31, dtype=dt, periodic=per, nbox=nbox, h=h, lo=lo)
+    assert len(np.unique(inp.mass)) == inp.n
+    gp = oracle.GravityPlan(inp)
+    nb = oracle.bits_per_dim(nbox)
+    ib = oracle.bin_positions(inp.pos, h, lo, nbox)
+    L = np.array(nbox, np.float64) * h
+    by_mass = {float(m): j for j, m in enumerate(inp.mass)}
+    ulp = np.finfo(dt).eps
+    for b in range(gp.B):
+        cb = np.array(oracle.demorton(3, nb, int(gp.bkey[b])), np.float64)
+        o = np.array(lo) + cb * h
+        run = gp.red[gp.red_off[b]:gp.red_off[b + 1]].astype(np.float64)
+        for rec in run:
+            j = by_mass[float(dt(rec[3]))]
+            S = rec[:3] + o - inp.pos[j].astype(np.float64)
+            img = np.rint(S / L)
+            assert np.all(np.abs(S - img * L) <= 8 * ulp * (np.abs(o) + 2 * h + L))
+            for d in range(3):
+                assert img[d] in (-1, 0, 1) and (img[d] == 0 or (per >> d) & 1)
+            delta = ib[j] + img * np.array(nbox) - cb
+            assert np.all(np.abs(delta) <= 1)
+            assert np.all(rec[:3] >= -h * (1 + 1e-6)) and np.all(rec[:3] < 2 * h * (1 + 1e-6))
