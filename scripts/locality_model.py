@@ -48,6 +48,30 @@ def timed(fn, flush, reps=7):
     return float(np.median(ts))
 
 
+def dispersion_per_thread(nbr_off, nbr_box, bstart):
+    """P:L165 (§3.4, Proposed Definition 1): "For a thread, let D be the number of non-adjacent memory blocks
+    accessed".  The paper's kernels run one thread per TARGET particle; a target thread of box b reads the
+    sources of b's neighbour segments [bstart[k], bstart[k+1]) (INDEXED) -- D_indexed(thread) = the number of
+    maximal contiguous blocks of the UNION of those segments in the sorted array (segments adjacent in memory merge
+    whatever their order in the list) -- or its box's one contiguous run (REDUNDANT, D = 1).  Returns
+    (D_box[B] for each target box, threads_per_box[B]); a thread-weighted mean is sum(D_box * n_b) / N."""
+    nbr_off = np.asarray(nbr_off, np.int64)
+    nbr_box = np.asarray(nbr_box, np.int64)
+    bstart = np.asarray(bstart, np.int64)
+    B = len(bstart) - 1
+    owner = np.repeat(np.arange(B), np.diff(nbr_off))
+    s0, s1 = bstart[nbr_box], bstart[nbr_box + 1]
+    order = np.lexsort((s0, owner))                 # segments of each box by start address
+    o, a, e = owner[order], s0[order], s1[order]
+    new_blk = np.ones(len(o), bool)
+    if len(o) > 1:
+        # a block continues when the next segment (same box) starts where the running block ends; segments of one
+        # box never overlap (distinct source boxes), so the running end is the previous segment's end
+        new_blk[1:] = ~((o[1:] == o[:-1]) & (a[1:] == e[:-1]))
+    D_box = np.bincount(o[new_blk], minlength=B)
+    return D_box, np.diff(bstart)
+
+
 def rankdata(x):
     order = np.argsort(x, kind="stable")
     r = np.empty(len(x))
@@ -77,7 +101,8 @@ def main():
         B = len(bstart) - 1
         n_b = np.diff(bstart)
         E = len(nbr_box)
-        # indexed dispersion: maximal runs of consecutive source boxes (records of box k and k+1 are adjacent)
+        # indexed dispersion: maximal runs of consecutive source boxes in CSR order (records of box k and k+1 are
+        # adjacent) -- the per-work-item variant (a warp's item reads its box's list in CSR order)
         owner = np.repeat(np.arange(B), np.diff(nbr_off))
         new_run = np.ones(E, bool)
         same_owner = owner[1:] == owner[:-1]
@@ -87,6 +112,11 @@ def main():
         pairs_b = n_b * R_b
         w = pairs_b / max(pairs_b.sum(), 1)
         D_idx = float((runs * w).sum())           # pair-weighted mean runs per work item
+        # P:L165's per-THREAD dispersion (one thread per target particle): union-of-segments blocks,
+        # averaged over the threads (targets); volume per thread = the 16 R_b bytes it reads (both layouts)
+        D_box, thr = dispersion_per_thread(nbr_off, nbr_box, bstart)
+        D_thread = float((D_box * thr).sum() / max(thr.sum(), 1))
+        V_thread = float((16 * R_b * thr).sum() / max(thr.sum(), 1))
         D_red = 1.0                                # one contiguous run per target box
         rec = 16
         V_red = rec * int(info.n_red)              # the redundant buffer streamed by the REDUNDANT eval
@@ -100,6 +130,8 @@ def main():
                "R": int(info.n_red), "D_indexed_runs_per_item": D_idx, "D_redundant": D_red,
                "V_redundant_bytes": V_red, "V_indexed_bytes": V_idx, "V_item_bytes": V_item,
                "regime": "V<=C" if fits else "V>C", "C_bytes": L2_BYTES, "D_ratio": Dp, "V_ratio": Vp,
+               "D_indexed_per_thread": D_thread, "D_redundant_per_thread": 1.0, "V_per_thread_bytes": V_thread,
+               "X_locality_pred_thread": D_thread,   # Eq 10 per thread: V_thread <= C (smem / L1), V' = 1
                "X_locality_pred": x_loc, "records_per_pair": int(info.n_red) / max(int(info.n_pairs), 1),
                "t_redundant_ms": t_red, "t_indexed_ms": t_idx, "X_measured": t_idx / t_red}
         rows.append(row)
@@ -108,7 +140,7 @@ def main():
         torch.cuda.empty_cache()
     xm = np.array([r["X_measured"] for r in rows])
     out = {"summary": True, "n": len(rows)}
-    for key in ["X_locality_pred", "records_per_pair", "D_indexed_runs_per_item"]:
+    for key in ["X_locality_pred", "records_per_pair", "D_indexed_runs_per_item", "X_locality_pred_thread"]:
         xp = np.array([r[key] for r in rows])
         if len(rows) >= 3 and np.std(xp) > 0:
             out[f"pearson_{key}"] = float(np.corrcoef(xp, xm)[0, 1])
