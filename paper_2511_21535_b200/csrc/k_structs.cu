@@ -613,6 +613,9 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
         P2P_CUDA_TRY(dalloc((void **)&P->s_box_nbr, sizeof(uint2) * bcap, st));
         P2P_CUDA_TRY(dalloc(&P->s_nb_tiles, (2 * sizeof(NbTile) + 4) * div_up(bcap, NB_THREADS), st));
         P2P_CUDA_TRY(dalloc((void **)&P->boxinfo, sizeof(uint2) * keyspace, st));
+        // defined contents once per allocation: nb_plane's branch-free lookups load (and then mask) the entry of
+        // keys whose occupancy bit is clear; entries are never cleared afterwards (stale ones are masked too)
+        P2P_CUDA_TRY(cudaMemsetAsync(P->boxinfo, 0, sizeof(uint2) * keyspace, st));
         P2P_CUDA_TRY(dalloc((void **)&P->small_tgt, 4 * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->small_box, 4 * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->red_off, 8 * (bcap + 1), st));
