@@ -373,9 +373,12 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_scatter(const T *__restric
     }
 }
 
+// packs the results of local positions [i0, i0 + n): the owned head of one received run (halo positions are
+// source-only, never written by the eval and never sent back)
 template <typename T, typename V4>
-__global__ void k_pack_results(const T *__restrict__ phi, const T *__restrict__ field, uint32_t n, V4 *__restrict__ res) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+__global__ void k_pack_results(const T *__restrict__ phi, const T *__restrict__ field, uint32_t i0, uint32_t n,
+                               V4 *__restrict__ res) {
+    for (uint32_t i = i0 + blockIdx.x * blockDim.x + threadIdx.x; i < i0 + n; i += gridDim.x * blockDim.x) {
         V4 r;
         r.x = phi[i];
         r.y = field[3 * (size_t)i + 0];
@@ -581,8 +584,11 @@ p2p_status eval_dist_t(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
         // results land at the local (received) positions; halo positions are not written and never sent back
         p2p_status s = eval_gravity(P, layout, P->phi_loc, P->field_loc);
         if (s != P2P_OK) return s;
-        P2P_LAUNCH((k_pack_results<T, V4>), grid1(nl, P->num_sms), 256, 0, st, (const T *)P->phi_loc,
-                   (const T *)P->field_loc, nl, (V4 *)P->res_own);
+        for (int r = 0; r < G; ++r)
+            if (P->rp_rcnt[r] > 0)
+                P2P_LAUNCH((k_pack_results<T, V4>), grid1((uint64_t)P->rp_rcnt[r], P->num_sms), 256, 0, st,
+                           (const T *)P->phi_loc, (const T *)P->field_loc, (uint32_t)P->rp_roff[r],
+                           (uint32_t)P->rp_rcnt[r], (V4 *)P->res_own);
     }
     std::vector<int64_t> so(G), sc(G), ro(G), rc(G);
     for (int r = 0; r < G; ++r) {  // the owned head of every received run goes back to its sender

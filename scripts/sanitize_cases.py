@@ -99,6 +99,11 @@ def main(case):
         assert not errs, errs
     else:
         raise SystemExit(f"unknown case {case}")
+    # free every tensor before exit (memcheck's leak check would report torch's still-referenced blocks)
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     print(f"case {case} done")
 
 

@@ -35,8 +35,8 @@ struct Mix {
 template <int MODE>
 __global__ void __launch_bounds__(128) k_mix(const float4 *gsrc, float *out, long long *cyc, int iters, float one,
                                               float nzero) {
-    __shared__ float4 src[1024];
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) src[i] = gsrc[i];
+    __shared__ float4 src[1024 + 64];  // 64 records of slack: a 4-source step at the wrap point reads past 1024
+    for (int i = threadIdx.x; i < 1024 + 64; i += blockDim.x) src[i] = gsrc[i & 1023];
     __syncthreads();
     Mix<MODE> M;
     M.one = bc(one);
@@ -105,7 +105,11 @@ void run(int ctas_per_sm, int sms, const float4 *src, float *out, long long *cyc
     cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
-    cudaMemcpy(hcyc, cyc, sizeof(long long) * grid, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(hcyc, cyc, sizeof(long long) * grid, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        printf("mode %d: %s\n", MODE, cudaGetErrorString(e));
+        return;
+    }
     long long mx = 0;
     for (int i = 0; i < grid; ++i) mx = hcyc[i] > mx ? hcyc[i] : mx;
     // lane-ops per SM: ctas * 128 threads * iters * 4 sources * 4 targets * 13
@@ -115,18 +119,30 @@ void run(int ctas_per_sm, int sms, const float4 *src, float *out, long long *cyc
            MODE, ctas_per_sm, ms, pairs / (ms * 1e-3), ops_sm / mx, ops_sm / mx / 128.0, mx / (ms * 1e-3) / 1e6);
 }
 
+#define CK(x)                                                                                      \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess) {                                                                   \
+            printf("%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_));               \
+            fflush(stdout);                                                                        \
+            return 1;                                                                              \
+        }                                                                                          \
+    } while (0)
+
 int main() {
-    int sms;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    float4 h[1024];
+    setvbuf(stdout, nullptr, _IONBF, 0);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    printf("SMs %d\n", sms);
+    static float4 h[1024];
     for (int i = 0; i < 1024; ++i) h[i] = make_float4(0.001f * i, 0.002f * (i % 37), 0.003f * (i % 11), 1.0f + i);
     float4 *src;
     float *out;
     long long *cyc, *hcyc = new long long[sms * 16];
-    cudaMalloc(&src, sizeof(h));
-    cudaMemcpy(src, h, sizeof(h), cudaMemcpyHostToDevice);
-    cudaMalloc(&out, sizeof(float) * sms * 16 * 128);
-    cudaMalloc(&cyc, sizeof(long long) * sms * 16);
+    CK(cudaMalloc(&src, sizeof(h)));
+    CK(cudaMemcpy(src, h, sizeof(h), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&out, sizeof(float) * sms * 16 * 128));
+    CK(cudaMalloc(&cyc, sizeof(long long) * sms * 16));
     for (int c : {4, 5, 6, 8}) {
         run<0>(c, sms, src, out, cyc, hcyc);
         run<1>(c, sms, src, out, cyc, hcyc);

@@ -95,10 +95,10 @@ def test_faces_bit_exact(P, gi, dt):
         # field by up to 5.6e-4 (oracle mode (i) vs (ii), geometry 1) -- a property of the layout, not of the
         # kernel -- so the kernel is checked against the oracle evaluated over the SAME bit-exact records (mode i).
         # INDEXED works on the input coordinates with -L frame shifts that are exact only when x - L is (lo = 0
-        # with a power-of-two L, or no periodic dimension): it is checked against the plain definition (mode ii)
-        # there and in fp64.
+        # with a representable L, or no periodic dimension): it is checked against the plain definition (mode ii)
+        # there (fp32 and fp64 alike: geometries 1 and 2 round x - L in fp64 too, 1.4e-12 / 7.9e-12).
         pr, fr = gp.eval_redundant()
-        frames_exact = dt == np.float64 or _frames_exact(inp)
+        frames_exact = _frames_exact(inp)
         for name, lay in P.LAYOUTS.items():
             phi, f = plan.eval(lay)
             if lay == P.P2P_INDEXED:
@@ -113,19 +113,22 @@ def test_faces_bit_exact(P, gi, dt):
 
 
 def _frames_exact(inp):
-    """True iff the INDEXED frame arithmetic is exact on this input: in every periodic dimension d, fl32(L_d) == L_d
-    and fl32(x - L_d) == x - L_d for every coordinate x in the top two box layers (the only values the -L frame /
-    image shifts are applied to: DESIGN §6, k_eval_gravity.cu frame_shift)"""
+    """True iff the INDEXED frame arithmetic is exact on this input, in the working precision p: in every periodic
+    dimension d, fl_p(L_d) == L_d and fl_p(x - L_d) == x - L_d for every coordinate x in the top two box layers
+    (the only values the -L frame / image shifts are applied to: DESIGN §6, k_eval_gravity.cu frame_shift).
+    Exactness is decided with rationals."""
+    from fractions import Fraction
+    dt = inp.pos.dtype.type
     for d in range(3):
         if not (inp.periodic >> d) & 1:
             continue
         n = int(inp.nbox[d])
         L = np.float64(n) * np.float64(inp.h)
-        if np.float64(np.float32(L)) != L:
+        if np.float64(dt(L)) != L:
             return False
-        x = inp.pos[:, d].astype(np.float32)
+        x = inp.pos[:, d]
         ib = np.floor((x.astype(np.float64) - np.float64(inp.lo[d])) / np.float64(inp.h))
-        x = x[ib >= n - 2]
-        if not np.array_equal((x - np.float32(L)).astype(np.float64), x.astype(np.float64) - L):
-            return False
+        for v in x[ib >= n - 2]:
+            if Fraction(float(v - dt(L))) != Fraction(float(v)) - Fraction(float(L)):
+                return False
     return True
