@@ -47,6 +47,11 @@ template <> struct V4T<double> { using type = double4; };
 constexpr int EV_WARPS = 4;              // warps per CTA
 constexpr int EV_STAGE_BYTES = 4096;     // source records per pipeline stage per warp (256 fp32 / 128 fp64)
 constexpr int EV_TGT = 32;               // max targets per item (ITEM_TMAX in k_structs.cu)
+// work-item records are prefetched through cp.async into a per-warp shared slot (P2P_ITEM_REGS: into registers,
+// the round-1 default): c4-8 eval 1.515 -> 1.463 ms, c5w / c3 unchanged (profiles/r02_eval_options.txt)
+#if !defined(P2P_ITEM_REGS) && !defined(P2P_ITEM_SMEM)
+#define P2P_ITEM_SMEM
+#endif
 #ifndef P2P_EV_BATCH
 #define P2P_EV_BATCH 2
 #endif
@@ -147,15 +152,17 @@ struct Tgt<float, K> {
             az[p] = __ffma2_rn(m3, dz, az[p]);
         }
     }
-    // Transpose-reduce of the S source splits of a group (K = 4: 16 values per lane, f = 4 q + k with q = 0
-    // potential, 1..3 field, k = target): each level exchanges HALF of the remaining values with the partner
-    // split and keeps the other half, so log2(S) levels cost 8 + 4 + 2 + 1 shuffles instead of 16 per level.
-    // A non-power-of-two S first folds its tail splits [Sp, S) onto [0, S - Sp).  Afterwards split sl < Sp
-    // (lg = log2 Sp, Lh = min(lg, 4)) holds the cnt = 16 >> Lh consecutive values f0 .. f0 + cnt - 1 in v[],
-    // f0 = (sl >> (lg - Lh)) * cnt; for lg = 5 only the even splits' values are unique.  Fixed exchange pattern
-    // -> deterministic.
+    // Transpose-reduce of the S source splits of a group: every lane holds V = 4K values (f = K q + k with q = 0
+    // potential, 1..3 field, k = target) as NW = 2K packed pairs.  Each level exchanges HALF of the remaining
+    // values with the partner split and keeps the other half, so log2(S) levels cost NW/2 + NW/4 + ... shuffles
+    // of pairs instead of NW per level.  A non-power-of-two S first folds its tail splits [Sp, S) onto [0, S - Sp).
+    // Afterwards split sl < Sp (lg = log2 Sp, Lh = min(lg, log2 V)) holds the cnt = V >> Lh consecutive values
+    // f0 .. f0 + cnt - 1 in v[], f0 = (sl >> (lg - Lh)) * cnt; when lg > log2 V only the splits whose low
+    // lg - Lh bits are 0 hold unique values.  Fixed exchange pattern -> deterministic.
+    static constexpr int NW = 2 * K;
+    static constexpr int LOGV = K == 4 ? 4 : 5;  // log2(4K)
     template <int H>
-    static __device__ __forceinline__ void tr_level(float2 (&w)[8], uint32_t sl, uint32_t gbase, uint32_t o) {
+    static __device__ __forceinline__ void tr_level(float2 (&w)[NW], uint32_t sl, uint32_t gbase, uint32_t o) {
         const bool up = (sl & o) != 0u;
         const uint32_t src = (gbase + (sl ^ o)) & 31u;
 #pragma unroll
@@ -167,31 +174,43 @@ struct Tgt<float, K> {
         }
     }
     __device__ __forceinline__ void treduce(uint32_t S, uint32_t sl, uint32_t gbase, float (&v)[4]) const {
-        static_assert(K == 4, "transpose-reduce is written for K = 4");
-        float2 w[8] = {ap[0], ap[1], ax[0], ax[1], ay[0], ay[1], az[0], az[1]};
+        static_assert(K == 4 || K == 8, "transpose-reduce is written for K = 4 or 8");
+        float2 w[NW];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            w[p] = ap[p];
+            w[P + p] = ax[p];
+            w[2 * P + p] = ay[p];
+            w[3 * P + p] = az[p];
+        }
         uint32_t Sp = S;
         if (S & (S - 1u)) {
             Sp = 1u << (31 - __clz(S));
             const uint32_t src = (gbase + sl + Sp) & 31u;
             const bool take = sl + Sp < S;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < NW; ++i) {
                 const float2 r = make_float2(__shfl_sync(0xffffffffu, w[i].x, src),
                                              __shfl_sync(0xffffffffu, w[i].y, src));
                 if (take) w[i] = __fadd2_rn(w[i], r);
             }
         }
-        const uint32_t lg = 31u - __clz(Sp);  // S >= 4 (G <= 8) -> lg in 2..5
-        tr_level<4>(w, sl, gbase, Sp >> 1);
-        tr_level<2>(w, sl, gbase, Sp >> 2);
-        if (lg >= 3) tr_level<1>(w, sl, gbase, Sp >> 3);
-        if (lg >= 4) {
-            const uint32_t o = Sp >> 4;
+        const uint32_t lg = 31u - __clz(Sp);  // S >= 4 -> lg in 2..5
+        // packed levels: keep NW/2, NW/4, ..., 1 pairs (level l runs when lg > l)
+        if (lg >= 1) tr_level<NW / 2>(w, sl, gbase, Sp >> 1);
+        if (lg >= 2) tr_level<NW / 4>(w, sl, gbase, Sp >> 2);
+        if (lg >= 3) tr_level<NW / 8>(w, sl, gbase, Sp >> 3);
+        if constexpr (NW >= 16) {
+            if (lg >= 4) tr_level<NW / 16>(w, sl, gbase, Sp >> 4);
+        }
+        constexpr int LP = NW == 8 ? 3 : 4;  // packed levels available (log2 NW)
+        if (lg >= (uint32_t)LP + 1u) {  // scalar level: split the last pair
+            const uint32_t o = Sp >> (LP + 1);
             const bool up = (sl & o) != 0u;
             const float snd = up ? w[0].x : w[0].y, kp = up ? w[0].y : w[0].x;
             w[0].x = kp + __shfl_sync(0xffffffffu, snd, (gbase + (sl ^ o)) & 31u);
         }
-        if (lg == 5) w[0].x += __shfl_xor_sync(0xffffffffu, w[0].x, 1);
+        if (lg >= (uint32_t)LOGV + 1u) w[0].x += __shfl_xor_sync(0xffffffffu, w[0].x, 1);  // K = 4, S = 32 only
         v[0] = w[0].x;
         v[1] = w[0].y;
         v[2] = w[1].x;
@@ -430,7 +449,7 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
 // boundary flags come from a.lframe instead of the uniform grid's box coordinates, and a leaf may list more than 32
 // neighbour segments (the lane-per-segment registers then cover groups of 32, re-read from the CSR per chunk)
 template <typename T, int LAYOUT, int K, bool ADAPT = false>
-__global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P_REDUNDANT ? 5 : 4) : 1) k_eval_gravity(const EvalArgs<T> a) {
+__global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : (LAYOUT == P2P_REDUNDANT ? 5 : 4)) : 1) k_eval_gravity(const EvalArgs<T> a) {
     using V4 = typename V4T<T>::type;
     constexpr int CH = EV_STAGE_BYTES / (int)sizeof(V4);
     constexpr int STAGE_RECS = CH + EV_TGT;  // source chunk + the item's targets
@@ -485,9 +504,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
     // work-queue pipeline: each atomicAdd claims EV_BATCH consecutive items (fewer atomics on the one queue
     // counter) and its result is consumed by shfl a whole batch later; item n+1's 32-byte Item record is already
     // in shared memory when its first chunk is issued -- no dependent load on the per-item critical path
-    // (REDUNDANT).  Build option P2P_ITEM_SMEM: the record goes through cp.async into a per-warp shared slot instead
-    // of registers (the compiler copies the 128-bit register loads into the loop-carried registers at once, waiting
-    // for them): c4-8 eval -4.4%, c5w +0.5% (profiles/r01_item_prefetch.txt), so registers stay the default.
+    // (REDUNDANT).  Default P2P_ITEM_SMEM: the record goes through cp.async into a per-warp shared slot instead of
+    // registers (with registers the compiler copies the 128-bit loads into the loop-carried registers at once,
+    // waiting for them): c4-8 eval -3.4%, c5w / c3 unchanged (profiles/r02_eval_options.txt).
     uint32_t pend = 0;  // lane 0: result of the last issued atomicAdd
     uint32_t nb_idx = 0, nb_left = 0;
     auto next_index = [&]() -> uint32_t {
@@ -566,7 +585,13 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
         const uint32_t nt = p_meta & 0xffu;
         V4 *dst = stage_base + s * STAGE_RECS;
         if (lane == 0) {
-            fence_proxy_async_smem();  // order earlier generic smem accesses of this stage before the async write
+            // the INDEXED variants WRITE the staged records (frame fix-ups, rebase): order those generic writes
+            // before the next async (TMA) write of the stage.  REDUNDANT only reads the stage, and every read has
+            // retired into the registers the hot loop consumed before the __syncwarp that precedes this issue
+#ifndef P2P_EV_FENCE_ALL
+            if (LAYOUT != P2P_REDUNDANT)
+#endif
+                fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[s], (cnt + (chunk == 0 ? nt : 0u)) * (uint32_t)sizeof(V4));
         }
         __syncwarp();
@@ -637,15 +662,14 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
         const uint32_t m20 = c_m20[S];
         const uint32_t g = (lane * m20) >> 20, sl = lane - g * S;
         const bool active = g < G;
-        // a9: the output slots of the lane's K targets, loaded now and used in the epilogue (the load latency
-        // was exposed there on small items: c4-8)
-        uint32_t pidx[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) pidx[k] = (active && g * K + k < nt) ? __ldg(a.perm + c_t0 + g * K + k) : 0u;
+        // a9: the output slot of target `lane` of the item (one coalesced load, issued now and used in the
+        // epilogue -- the load latency was exposed there on small items: c4-8); the epilogue fetches target ti's
+        // slot and mass from lane ti by shuffle (2 registers instead of 2 K)
+        const uint32_t my_slot = lane < nt ? __ldg(a.perm + c_t0 + lane) : 0u;
+        T my_m = 0;
 
         Tgt<T, K> tg;
         tg.zero();
-        T tm[K];
 
         bool have_next = true;
         for (uint32_t c = 0; c < c_nch; ++c) {
@@ -667,13 +691,13 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
             const uint32_t cnt = min((uint32_t)CH, c_R - c0);
 
             if (c == 0) {  // targets landed with the first chunk
+                if (lane < nt) my_m = stg[CH + lane].w;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const uint32_t ti = g * K + k;
-                    T x = 0, y = 0, z = 0, m = 0;
+                    T x = 0, y = 0, z = 0;
                     if (active && ti < nt) {
                         const V4 r = stg[CH + ti];
-                        m = r.w;
                         if (LAYOUT == P2P_INDEXED) {
                             x = r.x + (T)org[0];
                             y = r.y + (T)org[1];
@@ -689,7 +713,6 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
                         }
                     }
                     tg.set(k, x, y, z);
-                    tm[k] = m;
                 }
             }
 
@@ -770,38 +793,38 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (LAYOUT == P2P
         if constexpr (sizeof(T) == 4) {
             float v[4];
             tg.treduce(S, sl, g * S, v);
-            // the lane's values after the transpose-reduce (see Tgt::treduce): f0 .. f0 + vcnt - 1
+            // the lane's values after the transpose-reduce (see Tgt::treduce): f0 .. f0 + vcnt - 1 (vcnt <= 4:
+            // S >= 4 for K = 4, S >= 8 for K = 8, as ITEM_TMAX = 32 bounds G)
+            constexpr uint32_t LOGV = Tgt<T, K>::LOGV, LOGK = K == 4 ? 2u : 3u;
             const uint32_t lg = 31u - __clz(S);  // log2 of the power-of-two part of S
-            const uint32_t Lh = lg < 4u ? lg : 4u, vcnt = 16u >> Lh, f0 = (sl >> (lg - Lh)) * vcnt;
-            const bool own = sl < (1u << lg) && (lg < 5u || (sl & 1u) == 0u);
-            if (active && own) {
-                const T rs = Tgt<T, K>::self_rinv(eps2);
+            const uint32_t Lh = lg < LOGV ? lg : LOGV, vcnt = (1u << LOGV) >> Lh, f0 = (sl >> (lg - Lh)) * vcnt;
+            const bool own = active && sl < (1u << lg) && (lg <= LOGV || (sl & 1u) == 0u);
+            const T rs = Tgt<T, K>::self_rinv(eps2);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t f = f0 + j, q = f >> 2, k = f & 3u, ti = g * K + k;
-                    if ((uint32_t)j < vcnt && ti < nt) {
-                        const uint32_t i = k == 0 ? pidx[0] : (k == 1 ? pidx[1] : (k == 2 ? pidx[2] : pidx[K - 1]));
-                        if (q == 0) {
-                            const T mk = k == 0 ? tm[0] : (k == 1 ? tm[1] : (k == 2 ? tm[2] : tm[3]));
-                            a.phi[i] = -(v[j] - mk * rs);
-                        } else if (a.field) {
-                            a.field[3 * (size_t)i + (q - 1)] = v[j];
-                        }
-                    }
+            for (int j = 0; j < 4; ++j) {  // all lanes run the shuffles (no divergence around them)
+                const uint32_t f = f0 + j, q = f >> LOGK, k = f & (K - 1u), ti = g * K + k;
+                const uint32_t i = __shfl_sync(FULL, my_slot, ti & 31u);
+                const T mk = __shfl_sync(FULL, my_m, ti & 31u);
+                if ((uint32_t)j < vcnt && own && ti < nt) {
+                    if (q == 0)
+                        a.phi[i] = -(v[j] - mk * rs);
+                    else if (a.field)
+                        a.field[3 * (size_t)i + (q - 1)] = v[j];
                 }
             }
         } else {
         tg.reduce(S, sl);
-        if (active && sl == 0) {
+        {
             const T rs = Tgt<T, K>::self_rinv(eps2);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const uint32_t ti = g * K + k;
-                if (ti < nt) {
-                    const uint32_t i = pidx[k];
+                const uint32_t i = __shfl_sync(FULL, my_slot, ti & 31u);
+                const T mk = __shfl_sync(FULL, my_m, ti & 31u);
+                if (active && sl == 0 && ti < nt) {
                     T pot, fx, fy, fz;
                     tg.get(k, pot, fx, fy, fz);
-                    a.phi[i] = -(pot - tm[k] * rs);
+                    a.phi[i] = -(pot - mk * rs);
                     if (a.field) {
                         a.field[3 * (size_t)i + 0] = fx;
                         a.field[3 * (size_t)i + 1] = fy;

@@ -24,12 +24,14 @@ namespace p2p {
 constexpr uint64_t ITEM_COSTCAP = 1ull << 17;
 
 // targets per item of a box with nb_b targets and nsrc sources (its items: ceil(nb_b / size))
-__device__ __forceinline__ uint32_t item_size(uint32_t nb_b, uint64_t nsrc, uint32_t tmax) {
+// K = targets per lane of the eval (the capped sizes are multiples of K: every group of K target slots full)
+__device__ __forceinline__ uint32_t item_size(uint32_t nb_b, uint64_t nsrc, uint32_t tmax, uint32_t K) {
     const uint64_t a = (nb_b + tmax - 1) / tmax;
     const uint64_t c = ((uint64_t)nb_b * nsrc + ITEM_COSTCAP - 1) / ITEM_COSTCAP;
     if (c <= a) return tmax;
     const uint32_t ts = (uint32_t)(nb_b / c);  // balanced chunk size under the cap
-    if (ts < 4) return ts > 1 ? ts : 1u;
+    if (ts < K) return ts > 1 ? ts : 1u;
+    if (K == 8) return ts >= 24 ? 24u : ts >= 16 ? 16u : 8u;
     return ts >= 24 ? 24u : ts >= 20 ? 20u : ts >= 16 ? 16u : ts >= 12 ? 12u : ts >= 8 ? 8u : 4u;
 }
 
@@ -247,13 +249,14 @@ struct BoxTotals {
     uint32_t nbr, item, small;
     unsigned long long red;
 };
-__device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint32_t nb, bool tgt, uint32_t tmax) {
+__device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint32_t nb, bool tgt, uint32_t tmax,
+                                                 uint32_t K) {
     BoxTotals t;
     t.nbr = nbr;
     t.red = red;
     // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
     const bool small = nb <= SMALL_NT && red <= SMALL_R;
-    t.item = (small || !tgt) ? 0u : (nb + item_size(nb, red, tmax) - 1) / item_size(nb, red, tmax);
+    t.item = (small || !tgt) ? 0u : (nb + item_size(nb, red, tmax, K) - 1) / item_size(nb, red, tmax, K);
     t.small = (small && tgt) ? (nb + 1) / 2 : 0u;  // target PAIRS
     return t;
 }
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t
                                                           const uint2 *__restrict__ boxinfo,
                                                           const uint32_t *__restrict__ occ, DevCounters *ctr,
                                                           NbTile *__restrict__ tiles, uint2 *__restrict__ box_nbr,
-                                                          uint32_t tmax) {
+                                                          uint32_t tmax, uint32_t K) {
     const uint32_t B = ctr->B;
     const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
     unsigned long long pairs = 0;
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t
 #pragma unroll
         for (int dz = 0; dz < 3; ++dz) nb_plane(S, dz, key, tgt, occ, boxinfo, okm, cnt, red);
         if (have) box_nbr[b] = make_uint2(okm, (uint32_t)red);  // k_nbr_fill needs no occupancy search
-        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax);
+        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K);
         pairs += (unsigned long long)(tgt ? nb : 0u) * red;
         BoxTotals tot;
         block_scan_totals(x, &tot);
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
         const uint2 bn = have ? box_nbr[b] : make_uint2(0u, 0u);
         const uint32_t okm = bn.x, cnt = __popc(okm);
         const unsigned long long red = bn.y;
-        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax);
+        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K);
         BoxTotals tot;
         const BoxTotals inc = block_scan_totals(x, &tot);
         const NbTile to = tile_prefix(tile, tiles, incl, flags);
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
                     small_box[so + j] = b;
                 }
             } else {
-                const uint32_t nch = x.item, sz = item_size(nb, red, tmax);
+                const uint32_t nch = x.item, sz = item_size(nb, red, tmax, K);
                 for (uint32_t ci = 0; ci < nch; ++ci) {
                     const uint32_t a0 = ci * sz, z0 = min(nb, (ci + 1) * sz);
                     // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
@@ -674,7 +677,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     unsigned int *flags = (unsigned int *)(incl + ntile_cap);
     P2P_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * ntile_cap, st));
     P2P_LAUNCH(k_nbr_count, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, tiles,
-               P->s_box_nbr, (uint32_t)ITEM_TMAX);
+               P->s_box_nbr, (uint32_t)ITEM_TMAX, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));
     static bool carveout_set = false;  // the fill keeps a large L1 (its pass-2 reloads must hit)
     if (!carveout_set && P2P_NB_CARVEOUT > 0) {
         P2P_CUDA_TRY(cudaFuncSetAttribute(k_nbr_fill, cudaFuncAttributePreferredSharedMemoryCarveout, P2P_NB_CARVEOUT));

@@ -41,7 +41,14 @@ struct __align__(16) Item {
     uint32_t R;
     uint32_t tofs;
 };
-constexpr int EVAL_K_F32 = 4;    // targets per lane in k_eval_gravity (fp32: two packed FP32x2 pairs)
+#ifndef P2P_EVAL_K
+#define P2P_EVAL_K 4
+#endif
+// targets per lane in k_eval_gravity (fp32: K/2 packed FP32x2 pairs).  K = 4 or 8 (build option).  The hot
+// loop alone reaches 0.83 (K = 4) / 0.86 (K = 8) of the FP32 lane-op peak (scripts/ubench_evalmix.cu,
+// profiles/r02_ubench_evalmix.txt), but K = 8 needs 128 registers (16 warps per SM): c5w eval 6.00 -> 6.43 ms,
+// c4-8 1.60 -> 1.78, c4-128 15.3 -> 15.6, so K = 4 stays
+constexpr int EVAL_K_F32 = P2P_EVAL_K;
 constexpr int EVAL_K_F64 = 2;
 constexpr uint32_t ITEM_TMAX = 32;  // max targets per work item (lane utilisation)
 // boxes with <= SMALL_NT targets and <= SMALL_R sources take the eval's thread-per-target path (no work item):

@@ -1,6 +1,6 @@
 """Per-kernel device times of warm bench steps (CUPTI via torch.profiler: no serialisation, no clock lock).
 One step = p2p_plan_update + p2p_restructure + p2p_eval(REDUNDANT) on a persistent plan, like bench.py.
-usage: python scripts/kprof.py [workload] [steps]"""
+usage: python scripts/kprof.py [workload] [steps] [layouts, e.g. redundant,indexed]"""
 import collections
 import os
 import sys
@@ -16,6 +16,7 @@ import paper_2511_21535_b200 as P  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "c5w"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+LAYS = sys.argv[3].split(",") if len(sys.argv) > 3 else ["redundant"]
 inp = G.plummer_tiles(12_500_000, 256, 1, 0) if wl == "c5w" else G.config(wl)
 pos = torch.from_numpy(inp.pos).cuda()
 m = torch.from_numpy(inp.mass).cuda()
@@ -29,7 +30,8 @@ plan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=
 def step():
     plan.update(pos, m)
     plan.restructure()
-    plan.eval(P.P2P_REDUNDANT, phi, field)
+    for lay in LAYS:
+        plan.eval(P.LAYOUTS[lay], phi, field)
 
 
 for _ in range(3):

@@ -32,20 +32,24 @@ struct Mix {
     }
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(128) k_mix(const float4 *gsrc, float *out, long long *cyc, int iters, float one,
-                                              float nzero) {
+template <int MODE, int K = 4, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) k_mix(const float4 *gsrc, float *out, long long *cyc, int iters, float one,
+                                                    float nzero) {
+    constexpr int NP = K / 2;
     __shared__ float4 src[1024 + 64];  // 64 records of slack: a 4-source step at the wrap point reads past 1024
     for (int i = threadIdx.x; i < 1024 + 64; i += blockDim.x) src[i] = gsrc[i & 1023];
     __syncthreads();
     Mix<MODE> M;
     M.one = bc(one);
     M.nz = bc(nzero);
-    float2 tx[2], ty[2], tz[2], ap[2], ax[2], ay[2], az[2];
-    for (int p = 0; p < 2; ++p) {
-        tx[p] = make_float2(-0.1f * threadIdx.x, -0.2f * p);
-        ty[p] = make_float2(-0.3f, -0.01f * threadIdx.x);
-        tz[p] = make_float2(-0.5f, -0.7f);
+    float2 tx[NP], ty[NP], tz[NP], ap[NP], ax[NP], ay[NP], az[NP];
+    for (int p = 0; p < NP; ++p) {
+        // every target coordinate distinct and runtime-dependent (constant or repeated targets let ptxas share
+        // the d = s - t of equal targets across pairs -- the first version of this benchmark did, and over-reported)
+        const float u = (float)(threadIdx.x + 1) * one;
+        tx[p] = make_float2(-0.011f * u - 0.13f * p, -0.017f * u - 0.29f * p - 0.07f);
+        ty[p] = make_float2(-0.023f * u - 0.31f * p - 0.05f, -0.019f * u - 0.37f * p - 0.11f);
+        tz[p] = make_float2(-0.029f * u - 0.41f * p - 0.03f, -0.013f * u - 0.43f * p - 0.17f);
         ap[p] = ax[p] = ay[p] = az[p] = make_float2(0.f, 0.f);
     }
     const float2 E = bc(1e-6f);
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(128) k_mix(const float4 *gsrc, float *out, lon
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
 #pragma unroll
-            for (int p = 0; p < 2; ++p) {
+            for (int p = 0; p < NP; ++p) {
                 const float2 dx = M.add(bc(s[q].x), tx[p]);
                 const float2 dy = M.add(bc(s[q].y), ty[p]);
                 const float2 dz = M.add(bc(s[q].z), tz[p]);
@@ -86,21 +90,23 @@ __global__ void __launch_bounds__(128) k_mix(const float4 *gsrc, float *out, lon
     }
     long long t1 = clock64();
     float acc = 0.f;
-    for (int p = 0; p < 2; ++p) acc += ap[p].x + ap[p].y + ax[p].x + ax[p].y + ay[p].x + ay[p].y + az[p].x + az[p].y;
+    for (int p = 0; p < NP; ++p) acc += ap[p].x + ap[p].y + ax[p].x + ax[p].y + ay[p].x + ay[p].y + az[p].x + az[p].y;
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int MODE>
+template <int MODE, int K = 4, int MINB = 1>
 void run(int ctas_per_sm, int sms, const float4 *src, float *out, long long *cyc, long long *hcyc) {
-    const int iters = 4000;
+    const int iters = 4000 * 4 / K;
     const int grid = sms * ctas_per_sm;
-    k_mix<MODE><<<grid, 128>>>(src, out, cyc, iters, 1.0f, -0.0f);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_mix<MODE, K, MINB>);
+    k_mix<MODE, K, MINB><<<grid, 128>>>(src, out, cyc, iters, 1.0f, -0.0f);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    k_mix<MODE><<<grid, 128>>>(src, out, cyc, iters, 1.0f, -0.0f);
+    k_mix<MODE, K, MINB><<<grid, 128>>>(src, out, cyc, iters, 1.0f, -0.0f);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
@@ -113,10 +119,11 @@ void run(int ctas_per_sm, int sms, const float4 *src, float *out, long long *cyc
     long long mx = 0;
     for (int i = 0; i < grid; ++i) mx = hcyc[i] > mx ? hcyc[i] : mx;
     // lane-ops per SM: ctas * 128 threads * iters * 4 sources * 4 targets * 13
-    const double ops_sm = (double)ctas_per_sm * 128 * iters * 16 * 13;
-    const double pairs = (double)grid * 128 * iters * 16;
-    printf("mode %d ctas/SM %d: %.3f ms, %.3e pairs/s, %.1f lane-ops/clk/SM (frac of 128: %.3f), f_eff %.0f MHz\n",
-           MODE, ctas_per_sm, ms, pairs / (ms * 1e-3), ops_sm / mx, ops_sm / mx / 128.0, mx / (ms * 1e-3) / 1e6);
+    const double ops_sm = (double)ctas_per_sm * 128 * iters * 4 * K * 13;
+    const double pairs = (double)grid * 128 * iters * 4 * K;
+    printf("mode %d K %d regs %3d ctas/SM %d: %.3f ms, %.3e pairs/s, %.1f lane-ops/clk/SM (frac of 128: %.3f), "
+           "f_eff %.0f MHz\n", MODE, K, fa.numRegs, ctas_per_sm, ms, pairs / (ms * 1e-3), ops_sm / mx, ops_sm / mx / 128.0,
+           mx / (ms * 1e-3) / 1e6);
 }
 
 #define CK(x)                                                                                      \
@@ -143,12 +150,13 @@ int main() {
     CK(cudaMemcpy(src, h, sizeof(h), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&out, sizeof(float) * sms * 16 * 128));
     CK(cudaMalloc(&cyc, sizeof(long long) * sms * 16));
-    for (int c : {4, 5, 6, 8}) {
-        run<0>(c, sms, src, out, cyc, hcyc);
-        run<1>(c, sms, src, out, cyc, hcyc);
-        run<2>(c, sms, src, out, cyc, hcyc);
-        run<3>(c, sms, src, out, cyc, hcyc);
-        run<4>(c, sms, src, out, cyc, hcyc);
+    for (int c : {3, 4, 5, 6, 8}) {
+        run<0, 4>(c, sms, src, out, cyc, hcyc);
+        run<2, 4>(c, sms, src, out, cyc, hcyc);
+        run<0, 8>(c, sms, src, out, cyc, hcyc);
+        run<2, 8>(c, sms, src, out, cyc, hcyc);
+        run<0, 6>(c, sms, src, out, cyc, hcyc);
+        run<2, 6>(c, sms, src, out, cyc, hcyc);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("CUDA error %s\n", cudaGetErrorString(e));
