@@ -34,6 +34,10 @@ BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
 UNIT = "pair-interactions/s"
 FP32_INSTR_PER_PAIR = 13           # SURVEY §8d, verified from SASS
+FP64_INSTR_PER_PAIR = 26           # fp64 hot loop SASS per pair: 3 DADD + 3 DFMA (r^2) + 8 (correctly rounded sqrt:
+                                   # MUFU.RSQ64H seed + DMUL/DFMA Newton) + 5 DFMA (correctly rounded 1/x, C14) + 3 DMUL
+                                   # + 1 DADD + 3 DFMA
+FP64_LANES_PER_SM = 64             # DFMA lane-ops per clock per SM, measured (profiles/r02_ubench_fp64.txt)
 SM_COUNT_NOMINAL = 148
 LANES_PER_SM = 128
 
@@ -109,13 +113,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------ workload
-def make_workload(name: str, rank: int, world: int, seed: int = 0):
+def make_workload(name: str, rank: int, world: int, seed: int = 0, dtype=np.float32):
     import p2p_inputs as G
     if name == "c5w":
         # rank r owns tile r of the G-tile domain (Morton octant == tile for 2x2x2)
-        inp = G.plummer_tiles(12_500_000, 256, world, seed, tile_index=rank)
+        inp = G.plummer_tiles(12_500_000, 256, world, seed, dtype=dtype, tile_index=rank)
         return inp, f"c5w: Plummer tile (a=0.1 tile) 12.5M particles/GPU, 256^3 boxes/tile, {world} tile(s)"
-    return G.config(name, seed), name
+    return G.config(name, seed, dtype), name
 
 
 def main():
@@ -125,6 +129,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5w")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"],
+                    help="fp64: the same workload in double precision end to end (P:L258's 8-byte fields)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -152,7 +158,9 @@ def ours(args, rank, world, local):
     W = max(3, args.warmup)
     K = max(1, args.steps)
 
-    inp, wdesc = make_workload(args.workload, rank, world)
+    f64 = args.precision == "fp64"
+    fdt = torch.float64 if f64 else torch.float32
+    inp, wdesc = make_workload(args.workload, rank, world, dtype=np.float64 if f64 else np.float32)
     pos_h = torch.from_numpy(inp.pos).pin_memory()
     m_h = torch.from_numpy(inp.mass).pin_memory()
     pos = pos_h.to(dev)
@@ -164,8 +172,8 @@ def ours(args, rank, world, local):
     def l2_flush():
         flush.add_(1.0)
 
-    phi = torch.empty(N, dtype=torch.float32, device=dev)
-    field = torch.empty((N, 3), dtype=torch.float32, device=dev)
+    phi = torch.empty(N, dtype=fdt, device=dev)
+    field = torch.empty((N, 3), dtype=fdt, device=dev)
 
     comm = None
     if world > 1:
@@ -261,11 +269,15 @@ def ours(args, rank, world, local):
     B = int(plan.info.n_boxes)
 
     pk = peaks()
-    # roofline of the dominant kernel (eval): FP32-pipe bound, 13 FP32 instructions per pair
+    # roofline of the dominant kernel (eval): FP32-pipe bound, 13 FP32 instructions per pair;
+    # fp64: FP64-pipe bound, 26 FP64-pipe instructions per pair (SASS hot loop) at the measured DFMA rate per SM
+    # (scripts/ubench_fp64.cu, profiles/r02_ubench_fp64.txt)
     eval_ms_in_step = float(np.mean(t_eval))
     achieved = I / (eval_ms_in_step * 1e-3)
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak_pairs = n_sm * LANES_PER_SM * pk["sm_max_mhz"] * 1e6 / FP32_INSTR_PER_PAIR
+    lanes = FP64_LANES_PER_SM if f64 else LANES_PER_SM
+    ipp = FP64_INSTR_PER_PAIR if f64 else FP32_INSTR_PER_PAIR
+    peak_pairs = n_sm * lanes * pk["sm_max_mhz"] * 1e6 / ipp
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_eval_traffic.json")
     if os.path.exists(prof):
@@ -274,8 +286,12 @@ def ours(args, rank, world, local):
         except (ValueError, OSError):
             traffic = None
     # restructure vs HBM: writes 16 R bytes + compulsory reads 16 N_src (= 16 N) bytes
-    rest_bytes = 16 * R + 16 * N
+    rb = 32 if f64 else 16   # record bytes (float4 / double4)
+    rest_bytes = rb * R + rb * N
     rest_ms = float(np.mean(t_rest))
+    # SURVEY §8d end-to-end roofline: the FP32-bound eval time + the HBM-bound restructure time over the measured
+    # restructure + eval time of the step
+    t_roof = (I / peak_pairs + rest_bytes / (pk["hbm_gbs"] * 1e9)) * 1e3
 
     out = {
         "metric": METRIC,
@@ -288,7 +304,7 @@ def ours(args, rank, world, local):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32",
+        "dtype": "f64" if f64 else "f32",
         "data": "synthetic (seeded numpy PCG64 Plummer tiles; BASELINE configs[4] per-GPU tile)",
         "config": {"workload": wdesc, "N_per_gpu": N, "boxes_per_gpu": B, "pairs_per_gpu_per_step": I,
                    "red_records_per_gpu": R, "parallelism": (f"morton-range sharding over {world} GPUs: NCCL histogram all-reduce + all-to-all-v "
@@ -296,11 +312,19 @@ def ours(args, rank, world, local):
                    else "1 GPU",
                    "l2": "inputs+red buffer > L2 and 512 MB L2 flush between timed steps",
                    "step": "p2p_plan_update(a1-a5) + p2p_restructure(a6) + p2p_eval REDUNDANT(a7,a9); plan created once"},
-        "roofline": {"bound": "alu", "kernel": "k_eval_gravity<float,REDUNDANT,4>", "achieved": achieved / 1e9,
-                     "peak": peak_pairs / 1e9, "unit": "Gpair/s (FP32 pipe: 13 instr/pair)",
-                     "frac": achieved / peak_pairs, "traffic": traffic,
-                     "peak_basis": f"{n_sm} SMs x 128 FP32 lanes x {pk['sm_max_mhz']:.0f} MHz ({pk['src']}) / 13"},
-        "roofline_hbm": {"kernel": "k_restructure_gravity<float>", "bound": "hbm", "unit": "GB/s",
+        "roofline": {"bound": "alu", "kernel": f"k_eval_gravity<{'double' if f64 else 'float'},REDUNDANT,"
+                                                     f"{2 if f64 else 4}>", "achieved": achieved / 1e9,
+                     "peak": peak_pairs / 1e9,
+                     "unit": f"Gpair/s ({'FP64' if f64 else 'FP32'} pipe: {ipp} instr/pair)",
+                     "frac": achieved / peak_pairs, "traffic": traffic if not f64 else None,
+                     "peak_basis": f"{n_sm} SMs x {lanes} {'FP64 (measured DFMA rate)' if f64 else 'FP32'} lanes x "
+                                   f"{pk['sm_max_mhz']:.0f} MHz ({pk['src']}) / {ipp}"},
+        "roofline_e2e": {"frac": t_roof / (rest_ms + eval_ms_in_step), "t_roofline_ms": t_roof,
+                         "t_measured_ms": rest_ms + eval_ms_in_step,
+                         "formula": "SURVEY 8d: (ipp I / (n_SM lanes f) + (rb R + rb N) / BW_hbm) / (t_restructure + "
+                                    "t_eval), ipp = pipe instructions per pair, rb = record bytes"},
+        "roofline_hbm": {"kernel": f"k_restructure_gravity<{'double' if f64 else 'float'}>", "bound": "hbm",
+                         "unit": "GB/s",
                          "achieved": rest_bytes / (rest_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
                          "frac": rest_bytes / (rest_ms * 1e-3) / 1e9 / pk["hbm_gbs"], "bytes": rest_bytes},
         "phases": {
@@ -322,8 +346,8 @@ def ours(args, rank, world, local):
         if comm is None:
             # the time-stepping user's call sequence on the persistent plan, through the host-buffer ABI:
             # H2D of the step's inputs (pinned) + a1..a5, a6, a7+a9 + D2H of phi and field, every step
-            phi_h = torch.empty(N, dtype=torch.float32, pin_memory=True)
-            field_h = torch.empty((N, 3), dtype=torch.float32, pin_memory=True)
+            phi_h = torch.empty(N, dtype=fdt, pin_memory=True)
+            field_h = torch.empty((N, 3), dtype=fdt, pin_memory=True)
             api = "Plan.update_host + restructure + eval_host (p2p_plan_update_host / p2p_eval_host, pinned)"
 
             def e2e_call():
@@ -333,8 +357,8 @@ def ours(args, rank, world, local):
         else:
             # collective plans have no host-buffer entry points: the same sequence with the copies done by torch
             # on the plan's stream (pinned buffers, non_blocking)
-            phi_h = torch.empty(N, dtype=torch.float32, pin_memory=True)
-            field_h = torch.empty((N, 3), dtype=torch.float32, pin_memory=True)
+            phi_h = torch.empty(N, dtype=fdt, pin_memory=True)
+            field_h = torch.empty((N, 3), dtype=fdt, pin_memory=True)
             pos_e = torch.empty_like(pos)
             m_e = torch.empty_like(m)
             api = "H2D (pinned) + collective Plan.update + restructure + eval + D2H (persistent plan)"
@@ -362,8 +386,8 @@ def ours(args, rank, world, local):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         out["e2e"] = {"value": I_all / (te * 1e-3), "unit": UNIT, "ms_per_step": te,
-                      "h2d_bytes_per_step": int(pos_h.numel() * 4 + m_h.numel() * 4),
-                      "d2h_bytes_per_step": int(N * 4 + N * 12), "api": api}
+                      "h2d_bytes_per_step": int((pos_h.numel() + m_h.numel()) * pos_h.element_size()),
+                      "d2h_bytes_per_step": int(N * 4 * phi_h.element_size()), "api": api}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(inp, budget_s=12.0)
@@ -391,24 +415,47 @@ def _oracle_sample(gp, target_pairs: float, seed: int = 1):
     return sel, int((nb[sel] * nsrc[sel]).sum())
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(inp, budget_s: float = 12.0):
+    """the fp64 oracle (mode ii) on seeded-random target-box samples of the workload: all host cores (the
+    reported value) and 1 core (SURVEY §8d asks for both)"""
     import oracle
     gp = oracle.GravityPlan(inp, with_red=False)
-    sel, pairs = _oracle_sample(gp, 5e7)
-    t0 = time.perf_counter()
-    gp.eval_indexed_boxes(sel)
-    rate = pairs / (time.perf_counter() - t0)
-    # scale the sample to about budget_s of CPU work, then time it
-    sel, pairs = _oracle_sample(gp, min(rate * budget_s, float(gp.I)), seed=2)
-    t0 = time.perf_counter()
-    gp.eval_indexed_boxes(sel)
-    dt = time.perf_counter() - t0
-    whole = len(sel) >= gp.B
-    what = "all" if whole else "seeded-random"
-    return {"value": pairs / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+    ncpu = os.cpu_count()
+
+    def run(threads, budget):
+        used = oracle.set_threads(threads)
+        sel, pairs = _oracle_sample(gp, 5e7 / max(1, ncpu // threads))
+        t0 = time.perf_counter()
+        gp.eval_indexed_boxes(sel)
+        rate = pairs / (time.perf_counter() - t0)
+        # scale the sample to about `budget` s of wall time, then time it
+        sel, pairs = _oracle_sample(gp, min(rate * budget, float(gp.I)), seed=2)
+        t0 = time.perf_counter()
+        gp.eval_indexed_boxes(sel)
+        dt = time.perf_counter() - t0
+        return used, sel, pairs, dt
+
+    used1, sel1, pairs1, dt1 = run(1, budget_s / 2)
+    used, sel, pairs, dt = run(ncpu, budget_s)
+    oracle.set_threads(ncpu)
+    what = "all" if len(sel) >= gp.B else "seeded-random"
+    return {"value": pairs / dt, "unit": UNIT, "cores": used, "kind": "oracle",
+            "cpu": cpu_model(),
+            "one_core": {"value": pairs1 / dt1, "cores": used1,
+                         "sample": f"{len(sel1)} seeded-random target boxes ({pairs1} pairs, {dt1:.1f} s)"},
             "sample": f"fp64 oracle mode (ii) over {what} {len(sel)} target boxes ({pairs} pairs, {dt:.1f} s wall, "
-                      f"OpenMP {os.cpu_count()} threads = {dt * os.cpu_count():.0f} core-s) of the same workload; "
-                      f"structure build excluded"}
+                      f"OpenMP {used} threads = {dt * used:.0f} core-s) of the same workload; "
+                      f"structure build excluded; one_core = the same oracle on 1 thread"}
 
 
 def reference_arm(args, rank, world):
@@ -432,7 +479,7 @@ def reference_arm(args, rank, world):
            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": wdesc, "sample_pairs_per_step": pairs, "sample_boxes": int(len(sel))},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "cpu": cpu_model(),
                             "sample": f"{len(sel)} seeded-random target boxes ({pairs} pairs) per step, fp64 mode ii"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

@@ -66,6 +66,7 @@ def lib():
                 "orc_helm_structs": (i64, [i64, p, dbl, p, p, i32, p, p, p, p, p, p, p]),
                 "orc_helm_eval_table": (None, [i64, i32, p, p, p, p, p, p]),
                 "orc_helm_dense": (i64, [i64, p, p, dbl, p, p, dbl, dbl, p]),
+                "orc_set_threads": (i32, [i32]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -365,3 +366,8 @@ def rel_l2(a, b) -> float:
     b = np.asarray(b, dtype=a.dtype).ravel()
     nb = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads of the following oracle calls (timing harness only); returns the count in effect."""
+    return int(lib().orc_set_threads(int(n)))

@@ -733,3 +733,18 @@ int64_t orc_helm_dense(int64_t n, const double *pos, const double *x, double h, 
     free(ib);
     return -1;
 }
+
+/* Host-thread control for the timing harness (bench.py cpu_baseline at 1 core and at all cores); no arithmetic.
+ * Returns the thread count the following parallel regions use. */
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+int orc_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}

@@ -16,6 +16,7 @@ import torch  # noqa: E402
 
 import p2p_inputs as G  # noqa: E402
 import paper_2511_21535_b200 as P  # noqa: E402
+from bench import ClockSampler  # noqa: E402  (nvidia-smi clocks + throttle reasons during the timed region)
 
 
 def timed(fn, stream, reps=10):
@@ -43,9 +44,11 @@ def main():
         pos = torch.from_numpy(inp.pos).cuda()
         y = torch.empty((inp.n, 2), dtype=torch.float32, device="cuda")
         with P.Plan(P.P2P_HELMHOLTZ2D, pos, xr, inp.h, inp.lo, inp.nbox, 0, k=inp.k, t=inp.t) as plan:
-            t_rest = timed(plan.restructure, stream)
-            t_red = timed(lambda: plan.eval(P.P2P_REDUNDANT, y), stream)
-            t_idx = timed(lambda: plan.eval(P.P2P_INDEXED, y), stream)
+            with ClockSampler(0) as clk:
+                # enough repetitions that the 50 ms clock sampler sees the timed region
+                t_rest = timed(plan.restructure, stream, reps=200)
+                t_red = timed(lambda: plan.eval(P.P2P_REDUNDANT, y), stream, reps=200)
+                t_idx = timed(lambda: plan.eval(P.P2P_INDEXED, y), stream, reps=200)
             info = plan.info
         I = int(info.n_pairs)
         peak = nsm * 128 * peaks["sm_max_mhz"] * 1e6 / 4
@@ -62,7 +65,8 @@ def main():
                "restructure_plus_eval_pairs_per_s": I / ((t_rest + t_red) * 1e-3),
                "indexed_pairs_per_s": I / (t_idx * 1e-3),
                "restructure_hbm_frac": (xg_bytes + inp.n * 8) / (t_rest * 1e-3) / (peaks["hbm_gbs"] * 1e9),
-               "peak_basis": f"{nsm} SM x 128 FP32 lanes x {peaks['sm_max_mhz']} MHz / 4 FFMA per complex MAC"}
+               "peak_basis": f"{nsm} SM x 128 FP32 lanes x {peaks['sm_max_mhz']} MHz / 4 FFMA per complex MAC",
+               "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
 
 
