@@ -131,6 +131,9 @@ def main():
     ap.add_argument("--workload", default="c5w")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"],
                     help="fp64: the same workload in double precision end to end (P:L258's 8-byte fields)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "ipc"],
+                    help="N > 1: the NCCL communicator (one process per GPU) or the CUDA-IPC peer-memory one "
+                         "(p2p_comm_create_ipc; also runs N processes on ONE GPU -- not a scaling measurement)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -149,12 +152,20 @@ def ours(args, rank, world, local):
     import paper_2511_21535_b200 as P
 
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    ipc = args.comm == "ipc" and world > 1
+    ndev = torch.cuda.device_count()
+    if ipc:
+        local = local % ndev   # IPC ranks may share a device (more processes than GPUs)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ipc:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if ipc else dev   # where the timing reductions run (gloo: host tensors)
     W = max(3, args.warmup)
     K = max(1, args.steps)
 
@@ -176,7 +187,13 @@ def ours(args, rank, world, local):
     field = torch.empty((N, 3), dtype=fdt, device=dev)
 
     comm = None
-    if world > 1:
+    if world > 1 and ipc:
+        # CUDA-IPC communicator: rank 0 draws the rendezvous token, broadcast over the gloo group
+        import secrets
+        tok = [("p2pbench_" + secrets.token_hex(8)) if rank == 0 else None]
+        dist.broadcast_object_list(tok, 0)
+        comm = P.p2p_comm_create_ipc(world, rank, tok[0])
+    elif world > 1:
         # NCCL communicator owned by libp2p; rank 0's unique id is broadcast over the torch process group
         idt = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
@@ -235,10 +252,10 @@ def ours(args, rank, world, local):
     t_step = [e[0].elapsed_time(e[3]) for e in evs]
     ms_step = float(np.mean(t_step))
     if dist:
-        t = torch.tensor([ms_step], device=dev)
+        t = torch.tensor([ms_step], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-        tot = torch.tensor([float(I)], device=dev, dtype=torch.float64)
+        tot = torch.tensor([float(I)], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tot)
         I_all = int(tot.item())
     else:
@@ -308,8 +325,11 @@ def ours(args, rank, world, local):
         "data": "synthetic (seeded numpy PCG64 Plummer tiles; BASELINE configs[4] per-GPU tile)",
         "config": {"workload": wdesc, "N_per_gpu": N, "boxes_per_gpu": B, "pairs_per_gpu_per_step": I,
                    "red_records_per_gpu": R, "parallelism": (f"morton-range sharding over {world} GPUs: NCCL histogram all-reduce + all-to-all-v "
-                                   f"repartition + halo exchange (one Plummer tile per GPU)") if world > 1
-                   else "1 GPU",
+                                   f"repartition + halo exchange (one Plummer tile per GPU)") if world > 1 and not ipc
+                   else (f"morton-range sharding over {world} processes on {min(world, ndev)} GPU(s) through the "
+                         f"CUDA-IPC peer-memory communicator" + (" -- several ranks share a GPU: NOT a scaling "
+                                                                   "measurement" if world > ndev else ""))
+                   if ipc else "1 GPU",
                    "l2": "inputs+red buffer > L2 and 512 MB L2 flush between timed steps",
                    "step": "p2p_plan_update(a1-a5) + p2p_restructure(a6) + p2p_eval REDUNDANT(a7,a9); plan created once"},
         "roofline": {"bound": "alu", "kernel": f"k_eval_gravity<{'double' if f64 else 'float'},REDUNDANT,"
@@ -382,7 +402,7 @@ def ours(args, rank, world, local):
         e2e_once()
         te = float(np.median([e2e_once() for _ in range(max(2, min(K, 5)))]))
         if dist:
-            t = torch.tensor([te], device=dev)
+            t = torch.tensor([te], device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         out["e2e"] = {"value": I_all / (te * 1e-3), "unit": UNIT, "ms_per_step": te,

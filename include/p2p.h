@@ -278,6 +278,16 @@ p2p_status p2p_loopback_group_create(int nranks, p2p_loopback_group **out);
 void p2p_loopback_group_destroy(p2p_loopback_group *group);
 p2p_status p2p_comm_create_loopback(p2p_loopback_group *group, int rank, p2p_comm **out);
 
+/* Multi-PROCESS communicator over CUDA IPC peer memory (SURVEY §8e "B200-native option"): one process per rank
+ * on one node -- one GPU each (peer copies over NVLink / NVSwitch) or several processes sharing one GPU (NCCL
+ * allows one rank per device).  Each rank exports a cudaMalloc'd device arena; the collectives stage into the
+ * own arena and pull from the peers' (comm_ipc.cu).  `name` (no '/') names the POSIX shared-memory rendezvous
+ * segment: rank 0 creates it (INVALID_ARGUMENT if the name exists), the others wait up to 120 s for it; use a
+ * fresh random token per communicator (rank 0 draws it, the caller broadcasts it, e.g. over torch.distributed).
+ * Collective over all nranks ranks; the segment name is unlinked once every rank attached.
+ *   name: host NUL-terminated string;  out: receives the communicator (free with p2p_comm_destroy). */
+p2p_status p2p_comm_create_ipc(int nranks, int rank, const char *name, p2p_comm **out);
+
 /* ---- diagnostics ---- */
 const char *p2p_status_string(p2p_status s);
 const char *p2p_last_error(void);        /* thread-local detail of the last failing call on this thread */

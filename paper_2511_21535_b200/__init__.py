@@ -38,7 +38,7 @@ EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_r
             "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
             "p2p_partition_splitters", "p2p_get_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
-            "p2p_comm_create_loopback", "p2p_status_string", "p2p_last_error", "p2p_kernel_launch_count",
+            "p2p_comm_create_loopback", "p2p_comm_create_ipc", "p2p_status_string", "p2p_last_error", "p2p_kernel_launch_count",
             "p2p_abi_version"]
 
 
@@ -102,6 +102,7 @@ def lib() -> C.CDLL:
             "p2p_loopback_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
             "p2p_loopback_group_destroy": (None, [p]),
             "p2p_comm_create_loopback": (C.c_int, [p, C.c_int, C.POINTER(C.c_void_p)]),
+            "p2p_comm_create_ipc": (C.c_int, [C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -271,6 +272,14 @@ def p2p_loopback_group_create(nranks: int) -> int:
 
 def p2p_loopback_group_destroy(group: int):
     lib().p2p_loopback_group_destroy(C.c_void_p(group))
+
+
+def p2p_comm_create_ipc(nranks: int, rank: int, name: str) -> int:
+    """multi-process communicator over CUDA IPC peer memory (include/p2p.h); `name` = a fresh token shared by all
+    ranks (rank 0 draws it, the caller broadcasts it)"""
+    out = C.c_void_p()
+    _check(lib().p2p_comm_create_ipc(int(nranks), int(rank), name.encode(), C.byref(out)))
+    return out.value
 
 
 def p2p_comm_create_loopback(group: int, rank: int) -> int:

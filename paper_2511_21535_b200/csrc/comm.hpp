@@ -60,6 +60,7 @@ struct LoopbackGroup {
 
 CommBase *make_nccl_comm(int nranks, int rank, const void *id, p2p_status *st);
 CommBase *make_loopback_comm(LoopbackGroup *grp, int rank);
+CommBase *make_ipc_comm(int nranks, int rank, const char *name, p2p_status *st);
 
 }  // namespace p2p
 
