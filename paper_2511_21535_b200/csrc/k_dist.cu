@@ -565,7 +565,12 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
     P2P_CUDA_TRY(dalloc(&P->field_loc, 3 * sizeof(T) * nl, st));
     P2P_CUDA_TRY(dalloc(&P->res_own, sizeof(V4) * nl, st));
     P2P_CUDA_TRY(dalloc(&P->res_back, sizeof(V4) * nn, st));
-    if (P->n == 0) return P2P_OK;
+    if (P->n == 0) {
+        // no local particle, but the build's collectives (the item cost cap's all-reduce, k_structs.cu) still
+        // need this rank's (zero) contribution
+        P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->sum_nb2, 0, sizeof(unsigned long long), st));
+        return P->comm->allreduce_sum_u64(&P->ctr->sum_nb2, 1, st);
+    }
     if (P->n > P->cap) {
         free_capacity(P);
         s = alloc_capacity(P, P->n);

@@ -21,13 +21,32 @@ namespace p2p {
 // earlier balanced chunks (e.g. 25 + 25 targets: 28 lanes, 25 of 28 target slots) left up to 22% of the
 // lane-slots idle (c5w eval 6.60 -> 6.16 ms).
 // ITEM_TMAX (plan.hpp): at most 32 targets per item -> G <= 8 groups of K = 4 (fp32)
-constexpr uint64_t ITEM_COSTCAP = 1ull << 17;
+// The cap scales with the work: the dynamic queue's tail is bounded by its largest item, so a fixed 2^17-pair cap
+// left a 1e6-particle Plummer eval (c3, 6e8 pairs: 2e5 pairs per warp) waiting on single 2^17-pair items (SMs
+// active 81% of the kernel).  cap = pow2floor(I_est / (8 W)) clamped to [2^13, 2^17], I_est = 27 sum_b n_b^2 (the
+// pair count of a uniform periodic grid; ~25 sum n_b^2 on the Plummer inputs) over the TARGET boxes, W = a fixed
+// nominal eval warp count (148 SMs x 20) -- sum_nb2 is all-reduced over ranks, so every rank and a 1-GPU plan
+// derive the same cap and the same items (bitwise results independent of the GPU count).  c3 479 -> ~390 us;
+// c5w, c3dense, c4-k unchanged (their cap stays 2^17) (profiles/r02_eval_options.txt).
+#ifndef P2P_ITEM_COSTCAP
+#define P2P_ITEM_COSTCAP (1ull << 17)
+#endif
+constexpr uint64_t ITEM_COSTCAP = P2P_ITEM_COSTCAP;  // upper bound of the cap
+constexpr uint64_t ITEM_COSTCAP_MIN = 1ull << 13;
+constexpr uint64_t EVAL_WARPS_NOMINAL = 148 * 20;
+
+__device__ __forceinline__ uint64_t item_costcap(const DevCounters *ctr) {
+    const uint64_t est = 27ull * ctr->sum_nb2 / (8ull * EVAL_WARPS_NOMINAL);
+    if (est >= ITEM_COSTCAP) return ITEM_COSTCAP;
+    if (est <= ITEM_COSTCAP_MIN) return ITEM_COSTCAP_MIN;
+    return 1ull << (63 - __clzll((long long)est));
+}
 
 // targets per item of a box with nb_b targets and nsrc sources (its items: ceil(nb_b / size))
 // K = targets per lane of the eval (the capped sizes are multiples of K: every group of K target slots full)
-__device__ __forceinline__ uint32_t item_size(uint32_t nb_b, uint64_t nsrc, uint32_t tmax, uint32_t K) {
+__device__ __forceinline__ uint32_t item_size(uint32_t nb_b, uint64_t nsrc, uint32_t tmax, uint32_t K, uint64_t cap) {
     const uint64_t a = (nb_b + tmax - 1) / tmax;
-    const uint64_t c = ((uint64_t)nb_b * nsrc + ITEM_COSTCAP - 1) / ITEM_COSTCAP;
+    const uint64_t c = ((uint64_t)nb_b * nsrc + cap - 1) / cap;
     if (c <= a) return tmax;
     const uint32_t ts = (uint32_t)(nb_b / c);  // balanced chunk size under the cap
     if (ts < K) return ts > 1 ? ts : 1u;
@@ -174,11 +193,20 @@ struct HeadPut {
 
 // ------------------------------------------------------------------------------------------------ a5
 // dense key -> {box, n_b} table for the gravity neighbour search (valid where the occupancy bit is set)
+// + sum over the target boxes of n_b^2 (the item cost cap's work estimate; integer atomics: order-independent)
 __global__ void k_boxinfo(const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
-                          const DevCounters *__restrict__ ctr, uint2 *__restrict__ boxinfo) {
+                          DevCounters *__restrict__ ctr, uint2 *__restrict__ boxinfo, uint32_t tkey_lo,
+                          uint32_t tkey_hi) {
     const uint32_t B = ctr->B;
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x)
-        boxinfo[bkey[b]] = make_uint2(b, bstart[b + 1] - bstart[b]);
+    unsigned long long s2 = 0;
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+        const uint32_t key = bkey[b], nb = bstart[b + 1] - bstart[b];
+        boxinfo[key] = make_uint2(b, nb);
+        if (key >= tkey_lo && key <= tkey_hi) s2 += (unsigned long long)nb * nb;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if ((threadIdx.x & 31u) == 0 && s2) atomicAdd(&ctr->sum_nb2, s2);
 }
 
 // a5 in two kernels, THREAD PER BOX (tile = the 256 consecutive boxes of one block):
@@ -250,13 +278,13 @@ struct BoxTotals {
     unsigned long long red;
 };
 __device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint32_t nb, bool tgt, uint32_t tmax,
-                                                 uint32_t K) {
+                                                 uint32_t K, uint64_t cap) {
     BoxTotals t;
     t.nbr = nbr;
     t.red = red;
     // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
     const bool small = nb <= SMALL_NT && red <= SMALL_R;
-    t.item = (small || !tgt) ? 0u : (nb + item_size(nb, red, tmax, K) - 1) / item_size(nb, red, tmax, K);
+    t.item = (small || !tgt) ? 0u : (nb + item_size(nb, red, tmax, K, cap) - 1) / item_size(nb, red, tmax, K, cap);
     t.small = (small && tgt) ? (nb + 1) / 2 : 0u;  // target PAIRS
     return t;
 }
@@ -316,6 +344,7 @@ __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t
                                                           uint32_t tmax, uint32_t K) {
     const uint32_t B = ctr->B;
     const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
+    const uint64_t cap = item_costcap(ctr);
     unsigned long long pairs = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t b = tile * NB_THREADS + threadIdx.x;
@@ -330,7 +359,7 @@ __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t
 #pragma unroll
         for (int dz = 0; dz < 3; ++dz) nb_plane(S, dz, key, tgt, occ, boxinfo, okm, cnt, red);
         if (have) box_nbr[b] = make_uint2(okm, (uint32_t)red);  // k_nbr_fill needs no occupancy search
-        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K);
+        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K, cap);
         pairs += (unsigned long long)(tgt ? nb : 0u) * red;
         BoxTotals tot;
         block_scan_totals(x, &tot);
@@ -416,6 +445,7 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
     __shared__ uint8_t s_slot[NB_THREADS * NB_SLOTS];
     const uint32_t B = ctr->B;
     const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
+    const uint64_t cap = item_costcap(ctr);
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t b = tile * NB_THREADS + threadIdx.x;
         const bool have = b < B;
@@ -429,7 +459,7 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
         const uint2 bn = have ? box_nbr[b] : make_uint2(0u, 0u);
         const uint32_t okm = bn.x, cnt = __popc(okm);
         const unsigned long long red = bn.y;
-        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K);
+        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K, cap);
         BoxTotals tot;
         const BoxTotals inc = block_scan_totals(x, &tot);
         const NbTile to = tile_prefix(tile, tiles, incl, flags);
@@ -497,7 +527,7 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
                     small_box[so + j] = b;
                 }
             } else {
-                const uint32_t nch = x.item, sz = item_size(nb, red, tmax, K);
+                const uint32_t nch = x.item, sz = item_size(nb, red, tmax, K, cap);
                 for (uint32_t ci = 0; ci < nch; ++ci) {
                     const uint32_t a0 = ci * sz, z0 = min(nb, (ci + 1) * sz);
                     // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
@@ -668,8 +698,13 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
                                        &P->ctr->B, P->s_partials, st));
     // a5
     const uint64_t bcap = (uint64_t)P->bcap;
+    P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->sum_nb2, 0, sizeof(unsigned long long), st));
     P2P_LAUNCH(k_boxinfo, std::max<unsigned>(1, std::min<unsigned>(div_up(bcap, 256), (unsigned)P->num_sms * 8)), 256,
-               0, st, P->bkey, P->bstart, P->ctr, P->boxinfo);
+               0, st, P->bkey, P->bstart, P->ctr, P->boxinfo, P->geom.tkey_lo, P->geom.tkey_hi);
+    if (P->comm) {  // the cap's work estimate over ALL ranks' target boxes (= the 1-GPU value)
+        p2p_status cs = P->comm->allreduce_sum_u64(&P->ctr->sum_nb2, 1, st);
+        if (cs != P2P_OK) return cs;
+    }
     const unsigned nbg = std::max<unsigned>(1, std::min<unsigned>(div_up(bcap, NB_THREADS), (unsigned)P->num_sms * 8));
     const uint64_t ntile_cap = div_up(bcap, NB_THREADS);
     NbTile *tiles = (NbTile *)P->s_nb_tiles;            // [ntile_cap] sums, then [ntile_cap] inclusive prefixes

@@ -24,6 +24,7 @@ struct DevCounters {
     unsigned int sort_tile_ctr[4]; // onesweep tile counters, one per pass
     unsigned int n_small;          // targets of small boxes (thread-per-target path of the eval)
     unsigned int small_head;       // eval small-target queue head (reset before every eval)
+    unsigned long long sum_nb2;    // sum over target boxes of n_b^2 (k_boxinfo; all-reduced over ranks): item cost cap
 };
 
 // eval work item: a chunk [t0, t0 + nt) of the sorted targets of box `box`
