@@ -472,7 +472,9 @@ p2p_status build_dist_t(p2p_plan *P, const void *pos_v, const void *q_v) {
     // ---- 1. keys of the input particles ----
     if (n_in) P2P_LAUNCH(k_keys<T>, gb, 256, 0, st, pos, n_in, P->geom, key, err);
     // ---- 2. supercell histogram (+ one extra bin: ranks with an out-of-domain input), all-reduced ----
-    const int sc_bits = std::min(P->key_bits, 18), shift = P->key_bits - sc_bits;
+    // supercells span >= 4 keys (shift >= 2): the splitters are multiples of 4 keys, so an aligned key block -- a
+    // multi-box quad of the REDUNDANT eval (k_structs.cu mb_role) -- never straddles two ranks
+    const int sc_bits = std::max(0, std::min(P->key_bits - 2, 18)), shift = P->key_bits - sc_bits;
     const size_t nbins = (size_t)1 << sc_bits;
     unsigned long long *hist = nullptr;
     unsigned int *hist32 = nullptr;

@@ -478,6 +478,11 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
     uint64_t p_base = 0;
     uint32_t p_src = 0, p_st = 0, p_cnt = 0, p_slot = 0, p_ne = 0;  // INDEXED: lane = segment
     uint32_t p_e0 = 0;  // ADAPT: the item's first CSR entry
+    // multi-box items (k_structs.cu mb_quad; REDUNDANT fp32): 4 boxes, 8 lanes each, runs staged in lockstep
+    constexpr bool MBK = LAYOUT == P2P_REDUNDANT && sizeof(T) == 4 && K == 4 && !ADAPT;
+    constexpr uint32_t MBP = 64;  // records of each box's run per stage (4 x 64 = CH)
+    bool p_mb = false;
+    uint32_t p_mbnt = 0, p_R01 = 0, p_R23 = 0, p_tofs01 = 0, p_tofs23 = 0;
     // ADAPT: segment group g0 .. g0 + 31 of the CSR row at e0 (ne entries), starts offset by `base`
     auto seg_group = [&](uint32_t e0, uint32_t ne, uint32_t g0, uint32_t base, uint32_t &src, uint32_t &st,
                          uint32_t &cntl, uint32_t &code, uint32_t &tot) {
@@ -549,6 +554,18 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
             p_base = (uint64_t)q1.x | ((uint64_t)q1.y << 32);
             p_R = q1.z;
             p_tofs = q1.w;
+            if constexpr (MBK) {
+                p_mb = (q0.x >> 31) != 0u;
+                if (p_mb) {
+                    p_mbnt = q0.x & 0xffffu;
+                    p_R01 = q0.z;
+                    p_R23 = q0.w;
+                    p_tofs01 = q1.z;
+                    p_tofs23 = q1.w;
+                    p_meta = 32u | (4u << 8) | (8u << 16);  // G = 8 groups (2 per box) x S = 4 splits
+                    p_R = max(max(p_R01 & 0xffffu, p_R01 >> 16), max(p_R23 & 0xffffu, p_R23 >> 16));
+                }
+            }
         } else {
             const uint32_t e0 = a.nbr_off[p_box];
             p_ne = a.nbr_off[p_box + 1] - e0;
@@ -576,10 +593,34 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                 }
             }
         }
-        p_nch = (p_R + CH - 1) / CH;
+        p_nch = (MBK && p_mb) ? (p_R + MBP - 1) / MBP : (p_R + CH - 1) / CH;
     };
     // copy chunk `chunk` of the producer item into stage s (+ the item's targets when chunk == 0)
     auto issue = [&](uint32_t chunk, int s) {
+        if constexpr (MBK) {
+            if (p_mb) {  // box j = lane & 3: piece `chunk` of its run (lanes 0..3), its targets (lanes 4..7)
+                V4 *dst = stage_base + s * STAGE_RECS;
+                const uint32_t j = lane & 3u;
+                const uint32_t R0 = p_R01 & 0xffffu, R1 = p_R01 >> 16, R2 = p_R23 & 0xffffu, R3 = p_R23 >> 16;
+                const uint32_t Rj = j == 0 ? R0 : (j == 1 ? R1 : (j == 2 ? R2 : R3));
+                const uint32_t pre = (j > 0 ? R0 : 0u) + (j > 1 ? R1 : 0u) + (j > 2 ? R2 : 0u);
+                const uint32_t ntj = (p_mbnt >> (4 * j)) & 0xfu;
+                const uint32_t tofj = j < 2 ? (j == 0 ? p_tofs01 & 0xffffu : p_tofs01 >> 16)
+                                            : (j == 2 ? p_tofs23 & 0xffffu : p_tofs23 >> 16);
+                const uint32_t c0 = chunk * MBP;
+                const uint32_t cntj = Rj > c0 ? min(MBP, Rj - c0) : 0u;
+                uint32_t bytes = (lane < 4u ? cntj : 0u) + ((chunk == 0 && lane >= 4u && lane < 8u) ? ntj : 0u);
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
+                if (lane == 0) mbar_arrive_expect_tx(&bar[s], bytes * (uint32_t)sizeof(V4));
+                __syncwarp();
+                if (lane < 4u && cntj > 0u)
+                    bulk_g2s(dst + MBP * j, a.red + p_base + pre + c0, cntj * (uint32_t)sizeof(V4), &bar[s]);
+                if (chunk == 0 && lane >= 4u && lane < 8u && ntj > 0u)
+                    bulk_g2s(dst + CH + 8u * j, a.red + p_base + pre + tofj, ntj * (uint32_t)sizeof(V4), &bar[s]);
+                return;
+            }
+        }
         const uint32_t c0 = chunk * CH;
         const uint32_t cnt = min((uint32_t)CH, p_R - c0);
         const uint32_t nt = p_meta & 0xffu;
@@ -639,6 +680,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
         // ---------------- adopt the producer's item as the current (consumer) item ----------------
         const uint32_t c_t0 = p_t0, c_meta = p_meta, c_R = p_R, c_nch = p_nch;
         const uint32_t c_st = p_st, c_cnt = p_cnt, c_slot = p_slot, c_ne = p_ne, c_e0 = p_e0;
+        const bool c_mb = MBK && p_mb;
+        const uint32_t c_mbnt = p_mbnt, c_R01 = p_R01, c_R23 = p_R23;
         const uint32_t cc[3] = {compact3(p_key), compact3(p_key >> 1), compact3(p_key >> 2)};
         double org[3];
         bool needs_fix = false;
@@ -658,14 +701,34 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
             }
         }
         // lane layout (precomputed by k_nbr_fill): G groups of K targets x S source splits
-        const uint32_t nt = c_meta & 0xffu, S = (c_meta >> 8) & 0xffu, G = (c_meta >> 16) & 0xffu;
+        uint32_t S = (c_meta >> 8) & 0xffu, G = (c_meta >> 16) & 0xffu;
+        const uint32_t nt = c_meta & 0xffu;
+        if (LAYOUT == P2P_INDEXED_BITWISE && sizeof(T) == 4 && ((c_meta >> 24) & 1u)) {
+            S = 4u;  // a multi-box-quad member: the REDUNDANT eval's lane layout (G <= 2 groups x 4 splits)
+            G = (nt + K - 1) / K;
+        }
         const uint32_t m20 = c_m20[S];
         const uint32_t g = (lane * m20) >> 20, sl = lane - g * S;
         const bool active = g < G;
         // a9: the output slot of target `lane` of the item (one coalesced load, issued now and used in the
         // epilogue -- the load latency was exposed there on small items: c4-8); the epilogue fetches target ti's
         // slot and mass from lane ti by shuffle (2 registers instead of 2 K)
-        const uint32_t my_slot = lane < nt ? __ldg(a.perm + c_t0 + lane) : 0u;
+        // target slot ti holds a real target iff bit ti of vmask (multi-box items: slot 8 j + l = target l of box j)
+        uint32_t vmask = nt >= 32u ? 0xffffffffu : ((1u << nt) - 1u);
+        uint32_t my_t = c_t0 + lane;
+        if (c_mb) {
+            vmask = 0u;
+            uint32_t pre = 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t ntj = (c_mbnt >> (4 * j)) & 0xfu;
+                vmask |= ((1u << ntj) - 1u) << (8 * j);
+                if ((lane >> 3) == (uint32_t)j) my_t = c_t0 + pre + (lane & 7u);
+                pre += ntj;
+            }
+        }
+        const bool my_valid = (vmask >> lane) & 1u;
+        const uint32_t my_slot = my_valid ? __ldg(a.perm + my_t) : 0u;
         T my_m = 0;
 
         Tgt<T, K> tg;
@@ -691,12 +754,12 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
             const uint32_t cnt = min((uint32_t)CH, c_R - c0);
 
             if (c == 0) {  // targets landed with the first chunk
-                if (lane < nt) my_m = stg[CH + lane].w;
+                if (my_valid) my_m = stg[CH + lane].w;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const uint32_t ti = g * K + k;
                     T x = 0, y = 0, z = 0;
-                    if (active && ti < nt) {
+                    if (active && ((vmask >> ti) & 1u)) {
                         const V4 r = stg[CH + ti];
                         if (LAYOUT == P2P_INDEXED) {
                             x = r.x + (T)org[0];
@@ -762,7 +825,15 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
             }
 
             // ---- the hot loop: staged sources x register targets ----
-            if (active && sl < cnt) {
+            if (c_mb) {  // group g = box g / 2's targets over its own piece of this stage (S = 4)
+                const uint32_t j = g >> 1;
+                const uint32_t Rj = (j < 2 ? c_R01 : c_R23) >> (16 * (j & 1u)) & 0xffffu;
+                const uint32_t cj = c * MBP, cntj = Rj > cj ? min(MBP, Rj - cj) : 0u;
+                if (sl < cntj) {
+                    if constexpr (sizeof(T) == 4)
+                        hot_loop<T, K, 4>(tg, smem_u32(stg + MBP * j + sl), ((cntj - 1u - sl) >> 2) + 1u, E);
+                }
+            } else if (active && sl < cnt) {
                 // two sources per iteration with one remainder step: the accumulators stay in the same
                 // registers (no IMAD.MOV copies, which would occupy the FMA-heavy pipe the FFMA2s run on), and
                 // the addresses advance by pointer increments (ALU pipe) instead of IMAD
@@ -805,7 +876,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                 const uint32_t f = f0 + j, q = f >> LOGK, k = f & (K - 1u), ti = g * K + k;
                 const uint32_t i = __shfl_sync(FULL, my_slot, ti & 31u);
                 const T mk = __shfl_sync(FULL, my_m, ti & 31u);
-                if ((uint32_t)j < vcnt && own && ti < nt) {
+                if ((uint32_t)j < vcnt && own && ((vmask >> ti) & 1u)) {
                     if (q == 0)
                         a.phi[i] = -(v[j] - mk * rs);
                     else if (a.field)
@@ -821,7 +892,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                 const uint32_t ti = g * K + k;
                 const uint32_t i = __shfl_sync(FULL, my_slot, ti & 31u);
                 const T mk = __shfl_sync(FULL, my_m, ti & 31u);
-                if (active && sl == 0 && ti < nt) {
+                if (active && sl == 0 && ((vmask >> ti) & 1u)) {
                     T pot, fx, fy, fz;
                     tg.get(k, pot, fx, fy, fz);
                     a.phi[i] = -(pot - mk * rs);
@@ -865,6 +936,12 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems
     a.perm = P->perm;
     a.items = P->items;
     a.n_items = &P->ctr->n_items;
+    if constexpr (LAYOUT == P2P_REDUNDANT && sizeof(T) == 4 && K == 4 && !ADAPT) {
+        if (P->items_red) {  // the REDUNDANT item list with multi-box quads (k_structs.cu mb_quad)
+            a.items = P->items_red;
+            a.n_items = &P->ctr->n_items_red;
+        }
+    }
     a.item_head = &P->ctr->item_head;
     a.n_small = &P->ctr->n_small;
     a.small_head = &P->ctr->small_head;

@@ -7,6 +7,8 @@
 // a rounding.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "plan.hpp"
 #include "scan.cuh"
 
@@ -250,7 +252,8 @@ __device__ __forceinline__ void make_nb(const Geom &g, uint32_t key, NbStencil &
 // once (an invalid slot loads the box's own entry and is masked): okm bit s = slot s holds a non-empty box
 __device__ __forceinline__ void nb_plane(const NbStencil &S, int dz, uint32_t key, bool tgt,
                                          const uint32_t *__restrict__ occ, const uint2 *__restrict__ boxinfo,
-                                         uint32_t &okm, uint32_t &cnt, unsigned long long &red) {
+                                         uint32_t &okm, uint32_t &cnt, unsigned long long &red,
+                                         unsigned long long &part4) {
     uint32_t nk[9], wd[9], ny[9];
     bool v[9];
 #pragma unroll
@@ -270,11 +273,12 @@ __device__ __forceinline__ void nb_plane(const NbStencil &S, int dz, uint32_t ke
         okm |= (ok ? 1u : 0u) << (9 * dz + j);
         cnt += ok ? 1u : 0u;
         red += ok ? ny[j] : 0u;
+        if (j < 4) part4 += ok ? ny[j] : 0u;
     }
 }
 
 struct BoxTotals {
-    uint32_t nbr, item, small;
+    uint32_t nbr, item, small, item_red;  // item_red: the REDUNDANT eval's items (multi-box quads, see mb_role)
     unsigned long long red;
 };
 __device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint32_t nb, bool tgt, uint32_t tmax,
@@ -286,7 +290,41 @@ __device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint
     const bool small = nb <= SMALL_NT && red <= SMALL_R;
     t.item = (small || !tgt) ? 0u : (nb + item_size(nb, red, tmax, K, cap) - 1) / item_size(nb, red, tmax, K, cap);
     t.small = (small && tgt) ? (nb + 1) / 2 : 0u;  // target PAIRS
+    t.item_red = t.item;
     return t;
+}
+
+// Multi-box work items of the REDUNDANT eval (fp32): the 4 boxes of an aligned Morton key block (keys 4c .. 4c + 3, a
+// 2 x 2 x 1 block of boxes) that are all non-empty target boxes with <= 8 targets each (item path, not the small-box
+// path) and <= 65535 sources become ONE work item: box j owns lanes 8j .. 8j + 7 (2 groups of 4 targets x 4 source
+// splits, the standard G = 8 / S = 4 layout) and the 4 runs are staged in lockstep, 64 records of each per stage (4
+// bulk copies) -- possible only because every box's sources are ONE contiguous run (the redundant layout).  The
+// per-item overhead (record fetch, staging, transpose-reduce, epilogue) is paid once per 4 boxes: on 8-per-box
+// inputs it was half of the eval's instructions.  The grouping depends only on keys and per-box data, and the
+// multi-GPU splitters are multiples of 4 keys (k_dist.cu), so a block never straddles ranks: the items, and the
+// bits, are the same on any number of GPUs.
+constexpr uint32_t MB_NT = 8, MB_R = 65535;
+constexpr uint32_t MB_ELIG = 1u << 31;  // box_nbr[b].x flag (okm uses bits 0..26): the box may join a quad
+// cost <= cap / 4: a quad item (8 lanes per box) then takes no longer than a capped single-box item (32 lanes)
+__device__ __forceinline__ bool mb_eligible(bool enabled, bool tgt, uint32_t items, uint32_t nb, uint64_t red,
+                                            uint64_t cap) {
+    return enabled && tgt && items == 1u && nb >= 1u && nb <= MB_NT && red <= MB_R && (uint64_t)nb * red * 4 <= cap;
+}
+// 0: no quad, 1: leader (key % 4 == 0), 2: member of the quad led by box b - (key & 3)
+__device__ __forceinline__ int mb_role(uint32_t b, uint32_t key, uint32_t B, const uint32_t *__restrict__ bkey,
+                                       const uint2 *__restrict__ box_nbr) {
+    const uint32_t j = key & 3u;
+    if (b < j || b - j + 3u >= B) return 0;
+    const uint32_t lead = b - j, k0 = key - j;
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) {
+        if (i == j) {
+            if (!(box_nbr[b].x & MB_ELIG)) return 0;
+            continue;
+        }
+        if (bkey[lead + i] != k0 + i || !(box_nbr[lead + i].x & MB_ELIG)) return 0;
+    }
+    return j == 0 ? 1 : 2;
 }
 
 // block-wide inclusive scan of the four totals (NB_THREADS threads); returns the inclusive values, `tot` = sums
@@ -296,18 +334,19 @@ __device__ __forceinline__ BoxTotals block_scan_totals(BoxTotals x, BoxTotals *t
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t a = __shfl_up_sync(0xffffffffu, x.nbr, o), b = __shfl_up_sync(0xffffffffu, x.item, o),
-                       c = __shfl_up_sync(0xffffffffu, x.small, o);
+                       c = __shfl_up_sync(0xffffffffu, x.small, o), ir = __shfl_up_sync(0xffffffffu, x.item_red, o);
         const unsigned long long d = __shfl_up_sync(0xffffffffu, x.red, o);
         if (lane >= (unsigned)o) {
             x.nbr += a;
             x.item += b;
             x.small += c;
+            x.item_red += ir;
             x.red += d;
         }
     }
     if (lane == 31) s_w[w] = x;
     __syncthreads();
-    BoxTotals add{0, 0, 0, 0ull}, t{0, 0, 0, 0ull};
+    BoxTotals add{0, 0, 0, 0, 0ull}, t{0, 0, 0, 0, 0ull};
 #pragma unroll
     for (int i = 0; i < NB_THREADS / 32; ++i) {
         const BoxTotals v = s_w[i];
@@ -315,11 +354,13 @@ __device__ __forceinline__ BoxTotals block_scan_totals(BoxTotals x, BoxTotals *t
             add.nbr += v.nbr;
             add.item += v.item;
             add.small += v.small;
+            add.item_red += v.item_red;
             add.red += v.red;
         }
         t.nbr += v.nbr;
         t.item += v.item;
         t.small += v.small;
+        t.item_red += v.item_red;
         t.red += v.red;
     }
     __syncthreads();
@@ -327,13 +368,16 @@ __device__ __forceinline__ BoxTotals block_scan_totals(BoxTotals x, BoxTotals *t
     x.nbr += add.nbr;
     x.item += add.item;
     x.small += add.small;
+    x.item_red += add.item_red;
     x.red += add.red;
     return x;
 }
 
-// tile sums / exclusive tile offsets: [0] CSR entries, [1] redundant records, [2] work items, [3] small pairs
+// tile sums / exclusive tile offsets: [0] CSR entries, [1] redundant records, [2] work items, [3] small pairs,
+// [4] REDUNDANT-eval work items (multi-box quads)
+constexpr int NB_TOT = 5;
 struct NbTile {
-    unsigned long long v[4];
+    unsigned long long v[NB_TOT];
 };
 
 __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t *__restrict__ bkey,
@@ -341,7 +385,8 @@ __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t
                                                           const uint2 *__restrict__ boxinfo,
                                                           const uint32_t *__restrict__ occ, DevCounters *ctr,
                                                           NbTile *__restrict__ tiles, uint2 *__restrict__ box_nbr,
-                                                          uint32_t tmax, uint32_t K) {
+                                                          uint32_t tmax, uint32_t K, bool mb,
+                                                          uint32_t *__restrict__ mb_cen) {
     const uint32_t B = ctr->B;
     const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
     const uint64_t cap = item_costcap(ctr);
@@ -357,17 +402,51 @@ __global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t
         NbStencil S;
         make_nb(g, key, S);
 #pragma unroll
-        for (int dz = 0; dz < 3; ++dz) nb_plane(S, dz, key, tgt, occ, boxinfo, okm, cnt, red);
-        if (have) box_nbr[b] = make_uint2(okm, (uint32_t)red);  // k_nbr_fill needs no occupancy search
-        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K, cap);
+        unsigned long long part4 = 0, red0 = 0;
+#pragma unroll
+        for (int dz = 0; dz < 3; ++dz) {
+            unsigned long long p4 = 0;
+            nb_plane(S, dz, key, tgt, occ, boxinfo, okm, cnt, red, p4);
+            if (dz == 0) red0 = red;
+            if (dz == 1) part4 = p4;
+        }
+        BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K, cap);
+        const bool elig = mb_eligible(mb, tgt, x.item, nb, red, cap);
+        // k_nbr_fill needs no occupancy search; the eligibility flag and (eligible boxes) the offset of the box's
+        // own segment inside its run feed the quad items
+        if (have) box_nbr[b] = make_uint2(okm | (elig ? MB_ELIG : 0u), (uint32_t)red);
+        if (elig) mb_cen[b] = (uint32_t)(red0 + part4);
         pairs += (unsigned long long)(tgt ? nb : 0u) * red;
         BoxTotals tot;
         block_scan_totals(x, &tot);
-        if (threadIdx.x == 0) tiles[tile] = NbTile{{tot.nbr, tot.red, tot.item, tot.small}};
+        if (threadIdx.x == 0) tiles[tile] = NbTile{{tot.nbr, tot.red, tot.item, tot.small, 0ull}};
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
     if ((threadIdx.x & 31u) == 0 && pairs) atomicAdd(&ctr->I, pairs);
+}
+
+// the REDUNDANT list's item count per tile = work items - quad members (every eligible box has exactly one item)
+__global__ void __launch_bounds__(NB_THREADS) k_mb_tiles(const uint32_t *__restrict__ bkey,
+                                                         const uint2 *__restrict__ box_nbr, const DevCounters *ctr,
+                                                         NbTile *__restrict__ tiles) {
+    __shared__ uint32_t s_m[NB_THREADS / 32];
+    const uint32_t B = ctr->B;
+    const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t b = tile * NB_THREADS + threadIdx.x;
+        const bool member = b < B && mb_role(b, bkey[b], B, bkey, box_nbr) == 2;
+        const uint32_t m = __popc(__ballot_sync(0xffffffffu, member));
+        if ((threadIdx.x & 31u) == 0) s_m[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int i = 0; i < NB_THREADS / 32; ++i) t += s_m[i];
+            tiles[tile].v[4] = tiles[tile].v[2] - t;
+        }
+        __syncthreads();
+    }
 }
 
 // exclusive prefix of the tile sums before `tile`, by a look-back that never waits: every tile sum (k_nbr_count) is
@@ -384,10 +463,10 @@ __device__ __forceinline__ void st_release_u32(unsigned int *p, unsigned int v) 
 }
 __device__ NbTile tile_prefix(uint32_t tile, const NbTile *__restrict__ sums, const NbTile *incl,
                               const unsigned int *flags) {
-    __shared__ unsigned long long s_r[NB_THREADS / 32][4];
+    __shared__ unsigned long long s_r[NB_THREADS / 32][NB_TOT];
     __shared__ int s_stop[NB_THREADS / 32];
     const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
-    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+    unsigned long long acc[NB_TOT] = {0ull, 0ull, 0ull, 0ull, 0ull};
     for (int64_t base = (int64_t)tile - 1; base >= 0; base -= NB_THREADS) {
         const int64_t q = base - (int64_t)t;
         const bool inc = q < 0 || ld_acquire_u32(&flags[q]) != 0u;  // tiles before 0: an inclusive zero
@@ -401,16 +480,16 @@ __device__ NbTile tile_prefix(uint32_t tile, const NbTile *__restrict__ sums, co
         if ((int)t < stop) {
             const NbTile v = sums[q];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] += v.v[k];
+            for (int k = 0; k < NB_TOT; ++k) acc[k] += v.v[k];
         } else if ((int)t == stop && q >= 0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] += __ldcg(&incl[q].v[k]);
+            for (int k = 0; k < NB_TOT; ++k) acc[k] += __ldcg(&incl[q].v[k]);
         }
         if (stop < NB_THREADS) break;
     }
     // block sum
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < NB_TOT; ++k) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
         if (lane == 0) s_r[w][k] = acc[k];
@@ -418,7 +497,7 @@ __device__ NbTile tile_prefix(uint32_t tile, const NbTile *__restrict__ sums, co
     __syncthreads();
     NbTile r;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < NB_TOT; ++k) {
         unsigned long long x = 0;
 #pragma unroll
         for (int i = 0; i < NB_THREADS / 32; ++i) x += s_r[i][k];
@@ -440,7 +519,7 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
     unsigned int *flags, uint32_t *__restrict__ nbr_off, unsigned long long *__restrict__ red_off, uint32_t *__restrict__ nbr_box,
     uint8_t *__restrict__ nbr_slot, Item *__restrict__ items, uint32_t *__restrict__ small_tgt,
     uint32_t *__restrict__ small_box, uint32_t *__restrict__ chunk_box, unsigned long long *__restrict__ chunk_out,
-    uint32_t K, uint32_t tmax) {
+    uint32_t K, uint32_t tmax, Item *__restrict__ items_red, const uint32_t *__restrict__ mb_cen) {
     __shared__ uint32_t s_box[NB_THREADS * NB_SLOTS];
     __shared__ uint8_t s_slot[NB_THREADS * NB_SLOTS];
     const uint32_t B = ctr->B;
@@ -457,22 +536,26 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
         make_nb(g, key, S);
         // the occupied-slot mask and record count found by k_nbr_count
         const uint2 bn = have ? box_nbr[b] : make_uint2(0u, 0u);
-        const uint32_t okm = bn.x, cnt = __popc(okm);
+        const uint32_t okm = bn.x & ~MB_ELIG, cnt = __popc(okm);
         const unsigned long long red = bn.y;
-        const BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K, cap);
+        BoxTotals x = box_totals(cnt, red, tgt ? nb : 0u, tgt, tmax, K, cap);
+        const int role = (items_red != nullptr && have) ? mb_role(b, key, B, bkey, box_nbr) : 0;
+        const bool quad = role != 0;
+        if (role == 2) x.item_red = 0u;
         BoxTotals tot;
         const BoxTotals inc = block_scan_totals(x, &tot);
         const NbTile to = tile_prefix(tile, tiles, incl, flags);
         if (threadIdx.x == 0) {  // publish this tile's inclusive prefix
             NbTile in;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) in.v[k] = to.v[k];
+            for (int k = 0; k < NB_TOT; ++k) in.v[k] = to.v[k];
             in.v[0] += tot.nbr;
             in.v[1] += tot.red;
             in.v[2] += tot.item;
             in.v[3] += tot.small;
+            in.v[4] += tot.item_red;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) __stcg(&incl[tile].v[k], in.v[k]);
+            for (int k = 0; k < NB_TOT; ++k) __stcg(&incl[tile].v[k], in.v[k]);
             st_release_u32(&flags[tile], 1u);
             if (tile == ntiles - 1) {  // the last tile closes the offsets and publishes the totals
                 nbr_off[B] = (uint32_t)in.v[0];
@@ -481,6 +564,7 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
                 ctr->R = in.v[1];
                 ctr->n_items = (uint32_t)in.v[2];
                 ctr->n_small = (uint32_t)in.v[3];
+                ctr->n_items_red = (uint32_t)in.v[4];
             }
         }
         const uint32_t e_loc = inc.nbr - x.nbr;  // block-relative CSR offset
@@ -488,6 +572,7 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
         const unsigned long long rb = to.v[1] + inc.red - x.red;
         const uint32_t it = (uint32_t)to.v[2] + inc.item - x.item;
         const uint32_t so = (uint32_t)to.v[3] + inc.small - x.small;
+        const uint32_t itr = (uint32_t)to.v[4] + inc.item_red - x.item_red;
         if (have) {
             nbr_off[b] = e0;
             red_off[b] = rb;
@@ -520,6 +605,30 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
                 }
             }
         }
+        if (role == 1) {
+            // the quad leader packs the 4 boxes' item data (members' from global: count finished):
+            // q0 = {flag | nt_0..3 (4 bits each), t0 of box 0, R_0 | R_1 << 16, R_2 | R_3 << 16},
+            // q1 = {red_base lo, hi, tofs_0 | tofs_1 << 16, tofs_2 | tofs_3 << 16}  (eval: k_eval_gravity.cu)
+            uint32_t q_nt[4], q_R[4], q_tofs[4];
+            q_nt[0] = nb;
+            q_R[0] = (uint32_t)red;
+            q_tofs[0] = cen;
+#pragma unroll
+            for (int j = 1; j < 4; ++j) {
+                q_nt[j] = bstart[b + j + 1] - bstart[b + j];
+                q_R[j] = box_nbr[b + j].y;
+                q_tofs[j] = mb_cen[b + j];
+            }
+            Item mi;
+            mi.box = 0x80000000u | q_nt[0] | (q_nt[1] << 4) | (q_nt[2] << 8) | (q_nt[3] << 12);
+            mi.t0 = s0;
+            mi.meta = q_R[0] | (q_R[1] << 16);
+            mi.key = q_R[2] | (q_R[3] << 16);
+            mi.red_base = rb;
+            mi.R = q_tofs[0] | (q_tofs[1] << 16);
+            mi.tofs = q_tofs[2] | (q_tofs[3] << 16);
+            items_red[itr] = mi;
+        }
         if (tgt) {
             if (x.item == 0) {  // small box: thread-per-target path, one entry per target pair
                 for (uint32_t j = 0; j < x.small; ++j) {
@@ -532,7 +641,12 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
                     const uint32_t a0 = ci * sz, z0 = min(nb, (ci + 1) * sz);
                     // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
                     const uint32_t nt = z0 - a0, Gq = (nt + K - 1) / K, Sq = 32u / Gq;
-                    items[it + ci] = Item{b, s0 + a0, nt | (Sq << 8) | (Gq << 16), key, rb, (uint32_t)red, cen + a0};
+                    // bit 24: the box belongs to a multi-box quad of the REDUNDANT list -- P2P_INDEXED_BITWISE then
+                    // evaluates it with the quad's S = 4 splits, so its bits still equal the REDUNDANT eval's
+                    const Item itm{b, s0 + a0, nt | (Sq << 8) | (Gq << 16) | (quad ? 1u << 24 : 0u), key, rb,
+                                   (uint32_t)red, cen + a0};
+                    items[it + ci] = itm;
+                    if (items_red != nullptr && !quad) items_red[itr + ci] = itm;
                 }
             }
         }
@@ -596,7 +710,7 @@ void free_capacity(p2p_plan *P) {
     void *bufs[] = {P->s_key, P->s_idx, P->s_kalt, P->s_valt, P->s_hist, P->s_status, P->s_partials,
                     P->s_nb_tiles, P->s_aos, P->s_box_nbr, P->boxinfo,
                     P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, P->rec, P->bkey, P->bstart,
-                    P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->occ};
+                    P->nbr_off, P->nbr_box, P->nbr_slot, P->red_off, P->box_of, P->items, P->items_red, P->s_mb_cen, P->occ};
     for (void *b : bufs) dfree(b, st);
     P->s_key = P->s_idx = P->s_kalt = P->s_valt = P->s_hist = P->s_status = nullptr;
     P->s_partials = nullptr;
@@ -610,7 +724,8 @@ void free_capacity(p2p_plan *P) {
     P->bkey = P->bstart = P->nbr_off = P->nbr_box = P->box_of = P->occ = nullptr;
     P->nbr_slot = nullptr;
     P->red_off = nullptr;
-    P->items = nullptr;
+    P->items = P->items_red = nullptr;
+    P->s_mb_cen = nullptr;
     P->skey = P->perm = nullptr;
     P->cap = P->bcap = 0;
 }
@@ -653,6 +768,13 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
         P2P_CUDA_TRY(dalloc((void **)&P->small_box, 4 * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->red_off, 8 * (bcap + 1), st));
         P2P_CUDA_TRY(dalloc((void **)&P->items, sizeof(Item) * n, st));
+        // the REDUNDANT eval's own item list with multi-box quads (fp32 only: the eval's K = 4 lane layout)
+        // (P2P_NO_MB=1 at plan creation: no quads, for the measurements in profiles/r02_eval_options.txt)
+        const char *nomb = getenv("P2P_NO_MB");
+        if (!f64 && EVAL_K_F32 == 4 && !(nomb && nomb[0] == '1')) {
+            P2P_CUDA_TRY(dalloc((void **)&P->items_red, sizeof(Item) * n, st));
+            P2P_CUDA_TRY(dalloc((void **)&P->s_mb_cen, 4 * bcap, st));
+        }
         const uint64_t nchunk = div_up((uint64_t)nslot * bcap, 32) + 1;
         P2P_CUDA_TRY(dalloc((void **)&P->chunk_box, 4 * nchunk, st));
         P2P_CUDA_TRY(dalloc((void **)&P->chunk_out, 8 * nchunk, st));
@@ -712,7 +834,10 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     unsigned int *flags = (unsigned int *)(incl + ntile_cap);
     P2P_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * ntile_cap, st));
     P2P_LAUNCH(k_nbr_count, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, tiles,
-               P->s_box_nbr, (uint32_t)ITEM_TMAX, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32));
+               P->s_box_nbr, (uint32_t)ITEM_TMAX, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32), P->items_red != nullptr,
+               P->s_mb_cen);
+    if (P->items_red)
+        P2P_LAUNCH(k_mb_tiles, nbg, NB_THREADS, 0, st, P->bkey, P->s_box_nbr, P->ctr, tiles);
     static bool carveout_set = false;  // the fill keeps a large L1 (its pass-2 reloads must hit)
     if (!carveout_set && P2P_NB_CARVEOUT > 0) {
         P2P_CUDA_TRY(cudaFuncSetAttribute(k_nbr_fill, cudaFuncAttributePreferredSharedMemoryCarveout, P2P_NB_CARVEOUT));
@@ -721,7 +846,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     P2P_LAUNCH(k_nbr_fill, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->s_box_nbr, P->ctr, tiles,
                incl, flags, P->nbr_off, (unsigned long long *)P->red_off, P->nbr_box, P->nbr_slot, P->items,
                P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32),
-               (uint32_t)ITEM_TMAX);
+               (uint32_t)ITEM_TMAX, P->items_red, P->s_mb_cen);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }

@@ -24,6 +24,7 @@ struct DevCounters {
     unsigned int sort_tile_ctr[4]; // onesweep tile counters, one per pass
     unsigned int n_small;          // targets of small boxes (thread-per-target path of the eval)
     unsigned int small_head;       // eval small-target queue head (reset before every eval)
+    unsigned int n_items_red;      // REDUNDANT-eval work items (items_red)
     unsigned long long sum_nb2;    // sum over target boxes of n_b^2 (k_boxinfo; all-reduced over ranks): item cost cap
 };
 
@@ -96,6 +97,8 @@ struct p2p_plan {
     uint32_t *box_of = nullptr;  // Helmholtz: dense Morton-key -> box lookup
     uint32_t *occ = nullptr;     // gravity: occupancy bitmap of the key space (cleared every build)
     p2p::Item *items = nullptr;
+    p2p::Item *items_red = nullptr;
+    uint32_t *s_mb_cen = nullptr;    // per eligible box: offset of its own segment in its run (quad items)  // the REDUNDANT eval's items: multi-box quads + the other boxes' items (fp32)
     void *red = nullptr;         // gravity red[R] records; helmholtz Xg[B][9][t]
     void *table = nullptr;       // helmholtz pattern table P[t][9t] complex
     void *tc_table = nullptr;    // helmholtz tensor-core operand: real W hi / lo, 2 x [2t][18t] fp32 (k_helm_tc.cu)

@@ -81,7 +81,7 @@ def single(P, inp, layouts):
 
 def expected_splitters(P, cat, key_bits, nr):
     """p2p_partition_splitters (host) of the global supercell histogram built from the oracle's keys"""
-    sc_bits = min(key_bits, 18)
+    sc_bits = max(0, min(key_bits - 2, 18))  # supercells >= 4 keys (k_dist.cu)
     shift = key_bits - sc_bits
     hist = np.bincount(oracle.GravityPlan(cat, with_red=False).key >> shift, minlength=1 << sc_bits)
     return P.p2p_partition_splitters(hist.astype(np.uint64), shift, key_bits, nr)
