@@ -21,6 +21,13 @@
 //                         both operands K-major from shared memory descriptors), committed to the stage's empty
 //                         barrier (and, after the last slice, to the accumulator barrier)
 //   epilogue (warps 0-3)  tcgen05.ld of the accumulator rows (TMEM lane = box), scatter to input order
+//
+// GATHER = true is the non-redundant (INDEXED) layout on the same tensor cores -- the like-for-like DBIM comparison
+// of the paper's block-level redundancy (§5.1.2): no Xg; each split thread gathers its box row's K slice
+// straight from the Morton-sorted unknowns, xs[t * nbr9[b][s] ..] (slot s = the slice's stencil segment, a missing
+// neighbour zero-filled), by cp.async 16-byte copies into its own row of the stage, D = TC_STAGES - 1 slices ahead
+// (private rows: no barrier), then splits as above.  Only W goes through TMA.  Same A values, same MMA sequence:
+// the outputs equal the REDUNDANT tensor-core path bit for bit.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -127,11 +134,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 template <int T>
 constexpr uint32_t tc_tcols() { return T == 16 ? 256u : 512u; }
 
-template <int T>
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+template <int T, bool GATHER = false>
 __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
     k_helm_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWhi,
               const __grid_constant__ CUtensorMap tmWlo, uint32_t rf, const uint32_t *__restrict__ bstart,
-              const uint32_t *__restrict__ perm, uint32_t B, float2 *__restrict__ y) {
+              const uint32_t *__restrict__ perm, uint32_t B, float2 *__restrict__ y,
+              const float *__restrict__ xs, const uint32_t *__restrict__ nbr9) {
     constexpr int N = 2 * T, K = 18 * T, NKT = K / TC_BK;
     constexpr uint32_t X_BYTES = TC_BM * TC_BK * 4, W_BYTES = N * TC_BK * 4;
     constexpr uint32_t STAGE_BYTES = X_BYTES + 2 * W_BYTES;  // X (raw fp32), W hi, W lo
@@ -185,8 +197,8 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
                 const int s = kt % TC_STAGES;
                 if (kt >= TC_STAGES) mbar_wait(&empty[s], (uint32_t)((kt / TC_STAGES - 1) & 1));
                 const uint32_t st = ring + s * STAGE_BYTES;
-                mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-                tma_load_2d(st, &tmX, kt * TC_BK, (int)m0, cvta_smem(&full[s]));
+                mbar_arrive_expect_tx(&full[s], GATHER ? 2 * W_BYTES : STAGE_BYTES);
+                if (!GATHER) tma_load_2d(st, &tmX, kt * TC_BK, (int)m0, cvta_smem(&full[s]));
                 // block-level redundancy (RF copies of the pattern table): CTA b reads copy b mod RF
                 const int wrow = (int)((blockIdx.x % rf) * N);
                 tma_load_2d(st + X_BYTES, &tmWhi, kt * TC_BK, wrow, cvta_smem(&full[s]));
@@ -222,15 +234,41 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
         // thread = one X row (TMEM lane 32 warp + lane); its 128-byte row sits 16-byte-chunk-swizzled in smem
         const uint32_t r = warp * 32 + lane;
         const uint32_t lane_cols = (warp * 32u) << 16;
+        // GATHER: this row's K slice kt = 32 floats of stencil segment s = 32 kt / 2t (2t is a multiple of 32)
+        constexpr int GD = TC_STAGES - 1;  // slices gathered ahead
+        const uint32_t gb = m0 + r;
+        auto gather = [&](int kt) {
+            const uint32_t f0 = (uint32_t)kt * TC_BK, slot = f0 / (2 * T), off = f0 - slot * 2 * T;
+            const uint32_t k = gb < B ? __ldg(nbr9 + (size_t)gb * 9 + slot) : 0xffffffffu;
+            const bool ok = k != 0xffffffffu;
+            const float *src = xs + (ok ? (size_t)k * 2 * T + off : 0);
+            const uint32_t dst = ring + (uint32_t)(kt % TC_STAGES) * STAGE_BYTES + r * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) cp_async16_zfill(dst + 16 * c, src + 4 * c, ok ? 16u : 0u);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if constexpr (GATHER) {
+            for (int kt = 0; kt < GD; ++kt) {
+                if (kt < NKT) gather(kt);
+                else asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+        }
         for (int kt = 0; kt < NKT; ++kt) {
             const int s = kt % TC_STAGES, a = kt % ASTAGES;
-            mbar_wait(&full[s], (uint32_t)((kt / TC_STAGES) & 1));
+            if constexpr (GATHER) {
+                // stage (kt + GD) % TC_STAGES was last read by this thread at slice kt - 1 (its own row)
+                if (kt + GD < NKT) gather(kt + GD);
+                else asm volatile("cp.async.commit_group;" ::: "memory");
+                asm volatile("cp.async.wait_group %0;" ::"n"(GD) : "memory");
+            } else {
+                mbar_wait(&full[s], (uint32_t)((kt / TC_STAGES) & 1));
+            }
             if (kt >= ASTAGES) mbar_wait(&tfree[a], (uint32_t)((kt / ASTAGES - 1) & 1));
             const unsigned char *row = ring_gen + s * STAGE_BYTES + r * 128;
             uint32_t hi[32], lo[32];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                const float4 v = *reinterpret_cast<const float4 *>(row + ((c ^ (r & 7)) << 4));
+                const float4 v = *reinterpret_cast<const float4 *>(row + ((GATHER ? c : (c ^ (r & 7))) << 4));
                 const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -327,7 +365,7 @@ bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, ui
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int T>
+template <int T, bool GATHER>
 p2p_status launch_tc(p2p_plan *P, void *y) {
     constexpr int N = 2 * T, K = 18 * T;
     constexpr uint32_t STAGE_BYTES = TC_BM * TC_BK * 4 + 2 * N * TC_BK * 4;
@@ -335,14 +373,15 @@ p2p_status launch_tc(p2p_plan *P, void *y) {
     CUtensorMap mx, mwh, mwl;
     const float *W = (const float *)P->tc_table;  // [RF] copies of W hi, then [RF] copies of W lo
     const uint32_t rf = (uint32_t)P->tc_rf;
-    if (!make_map(&mx, P->red, (uint64_t)P->B, K, TC_BM) || !make_map(&mwh, W, (uint64_t)rf * N, K, N) ||
+    if (!make_map(&mx, GATHER ? (const void *)W : P->red, GATHER ? (uint64_t)rf * N : (uint64_t)P->B, K,
+                  GATHER ? N : TC_BM) || !make_map(&mwh, W, (uint64_t)rf * N, K, N) ||
         !make_map(&mwl, W + (size_t)rf * N * K, (uint64_t)rf * N, K, N)) {
         set_error("cuTensorMapEncodeTiled unavailable or rejected the Helmholtz operands");
         return P2P_ERR_CUDA;
     }
-    P2P_CUDA_TRY(cudaFuncSetAttribute(k_helm_tc<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    P2P_LAUNCH(k_helm_tc<T>, div_up((uint64_t)P->B, TC_BM), TC_THREADS, smem, P->stream, mx, mwh, mwl, rf, P->bstart,
-               P->perm, (uint32_t)P->B, (float2 *)y);
+    P2P_CUDA_TRY(cudaFuncSetAttribute(k_helm_tc<T, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    P2P_LAUNCH((k_helm_tc<T, GATHER>), div_up((uint64_t)P->B, TC_BM), TC_THREADS, smem, P->stream, mx, mwh, mwl, rf,
+               P->bstart, P->perm, (uint32_t)P->B, (float2 *)y, (const float *)P->rec, P->nbr_box);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }
@@ -388,9 +427,10 @@ p2p_status helmholtz_tc_table(p2p_plan *P, const float *Pf /* host, [t][9t] comp
     return P2P_OK;
 }
 
-p2p_status eval_helmholtz_tc(p2p_plan *P, void *y) {
+p2p_status eval_helmholtz_tc(p2p_plan *P, void *y, bool gather) {
     if (P->B == 0) return P2P_OK;
-    return P->cfg.points_per_box == 16 ? launch_tc<16>(P, y) : launch_tc<64>(P, y);
+    if (gather) return P->cfg.points_per_box == 16 ? launch_tc<16, true>(P, y) : launch_tc<64, true>(P, y);
+    return P->cfg.points_per_box == 16 ? launch_tc<16, false>(P, y) : launch_tc<64, false>(P, y);
 }
 
 }  // namespace p2p

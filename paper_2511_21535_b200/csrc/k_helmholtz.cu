@@ -330,7 +330,11 @@ p2p_status eval_helmholtz(p2p_plan *P, p2p_layout layout, void *y) {
         const char *e = getenv("P2P_HELM_SIMT");
         return e && e[0] == '1';
     }();
-    if (layout == P2P_REDUNDANT && P->tc_table && !force_simt) return eval_helmholtz_tc(P, y);
+    // fp32 t in {16, 64}: BOTH layouts on the tensor cores (the like-for-like DBIM comparison): REDUNDANT streams Xg
+    // by TMA, INDEXED gathers the neighbour segments of xs by cp.async (k_helm_tc.cu GATHER); P2P_HELM_SIMT=1 runs
+    // both on the CUDA cores instead
+    if ((layout == P2P_REDUNDANT || layout == P2P_INDEXED) && P->tc_table && !force_simt)
+        return eval_helmholtz_tc(P, y, layout == P2P_INDEXED);
     if (layout == P2P_REDUNDANT) return f64 ? launch_helm<double, P2P_REDUNDANT>(P, y) : launch_helm<float, P2P_REDUNDANT>(P, y);
     return f64 ? launch_helm<double, P2P_INDEXED>(P, y) : launch_helm<float, P2P_INDEXED>(P, y);
 }

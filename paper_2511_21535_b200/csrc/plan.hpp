@@ -189,7 +189,7 @@ p2p_status helmholtz_table(p2p_plan *P);
 // k_helm_tc.cu: a8 as one 3xTF32 tcgen05 GEMM (fp32, t in {16, 64})
 bool helmholtz_tc_supported(const p2p_plan *P);
 p2p_status helmholtz_tc_table(p2p_plan *P, const float *Pf);
-p2p_status eval_helmholtz_tc(p2p_plan *P, void *y);
+p2p_status eval_helmholtz_tc(p2p_plan *P, void *y, bool gather);  // gather: the INDEXED layout
 
 // k_adaptive.cu: SURVEY NEXT-1 adaptive binary-tree leaves (C22) from the box table; host outputs, synchronous
 p2p_status adaptive_leaves(p2p_plan *P, uint32_t t, int min_bits, uint32_t *len_h, uint32_t *prefix_h,
