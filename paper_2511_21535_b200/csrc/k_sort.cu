@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_radix_pass(const uint32_t *__
                                                            const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
                                                            uint32_t *__restrict__ vout, uint32_t n, int shift,
                                                            const uint32_t *__restrict__ digit_off,
-                                                           uint32_t *status, uint32_t *tile_ctr) {
+                                                           uint32_t *status, uint32_t *tile_ctr, bool iota) {
     __shared__ uint32_t s_whist[RS_WARPS][256];
     __shared__ uint32_t s_tdig[256];
     __shared__ uint32_t s_goff[256];
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_radix_pass(const uint32_t *__
         uint32_t idx = seg + i * 32 + lane;
         bool ok = idx < n;
         k[i] = ok ? kin[idx] : 0u;
-        v[i] = ok ? vin[idx] : 0u;
+        v[i] = iota ? idx : (ok ? vin[idx] : 0u);  // iota: the first pass's values are the input positions
     }
     // the tile's digit counts first (shared-memory atomics), published as the tile aggregate BEFORE the
     // ranking: successors looking back find it early, and this tile's own look-back (after the ranking) mostly
@@ -213,6 +213,10 @@ uint32_t peers = __match_any_sync(mask, d);  // (8 bit-sliced ballots measured s
     }
 }
 
+__global__ void k_iota_u32(uint32_t *__restrict__ v, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+
 __global__ void k_copy_u32(const uint32_t *__restrict__ a, uint32_t *__restrict__ b, uint32_t n) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = a[i];
 }
@@ -222,21 +226,27 @@ size_t radix_status_words(uint64_t n, int passes) { return (size_t)passes * div_
 
 cudaError_t radix_sort_pairs(uint32_t *kin, uint32_t *vin, uint32_t *kalt, uint32_t *valt, uint32_t n, int passes,
                              DevCounters *ctr, uint32_t *hist, uint32_t *status, cudaStream_t st, uint32_t **kout,
-                             uint32_t **vout) {
+                             uint32_t **vout, bool iota_values, bool hist_ready) {
     *kout = kin;
     *vout = vin;
-    if (n == 0 || passes == 0) return cudaSuccess;
+    if (n == 0) return cudaSuccess;
+    if (passes == 0) {  // one box: the order is the input order
+        if (iota_values) P2P_LAUNCH(k_iota_u32, std::min<unsigned>(div_up(n, 256), 148 * 8), 256, 0, st, vin, n);
+        return cudaGetLastError();
+    }
     const uint32_t ntiles = div_up(n, RS_TILE);
-    cudaMemsetAsync(hist, 0, (size_t)passes * 256 * sizeof(uint32_t), st);
     cudaMemsetAsync(status, 0, radix_status_words(n, passes) * sizeof(uint32_t), st);
     cudaMemsetAsync(ctr->sort_tile_ctr, 0, sizeof(ctr->sort_tile_ctr), st);
-    unsigned hg = std::min<unsigned>(div_up(n, 256 * 8), 148 * 8);
-    P2P_LAUNCH(k_radix_hist, hg, 256, 0, st, kin, n, passes, hist);
+    if (!hist_ready) {  // else the caller's key kernel built the digit histograms (k_bin_gravity)
+        cudaMemsetAsync(hist, 0, (size_t)passes * 256 * sizeof(uint32_t), st);
+        unsigned hg = std::min<unsigned>(div_up(n, 256 * 8), 148 * 8);
+        P2P_LAUNCH(k_radix_hist, hg, 256, 0, st, kin, n, passes, hist);
+    }
     P2P_LAUNCH(k_radix_hist_scan, passes, 256, 0, st, hist);
     uint32_t *a_k = kin, *a_v = vin, *b_k = kalt, *b_v = valt;
     for (int p = 0; p < passes; ++p) {
         P2P_LAUNCH(k_radix_pass, ntiles, RS_THREADS, 0, st, a_k, a_v, b_k, b_v, n, 8 * p, hist + 256 * p,
-                   status + (size_t)p * ntiles * 256, &ctr->sort_tile_ctr[p]);
+                   status + (size_t)p * ntiles * 256, &ctr->sort_tile_ctr[p], iota_values && p == 0);
         std::swap(a_k, b_k);
         std::swap(a_v, b_v);
     }

@@ -60,10 +60,16 @@ __device__ __forceinline__ uint32_t item_size(uint32_t nb_b, uint64_t nsrc, uint
 // positions at pos[i * ps + d] (ps = 3: the caller's [N][3] array; ps = 4: {x,y,z,m} records).  With `aos` the
 // caller's SoA input is also packed into {x,y,z,m} records in input order (read sequentially here), so that the a3
 // gather touches ONE 16-byte record per particle instead of a position and a mass in two arrays (two DRAM bursts)
+// The a2 sort's digit histograms are built here too (the keys are in registers; the sort's own histogram pass
+// re-read 50 MB at c5w), and its first pass takes the input positions as values (no iota array written / read).
 template <typename T, typename V4>
-__global__ void k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geom g, uint32_t *__restrict__ key,
-                              uint32_t *__restrict__ idx, DevCounters *ctr, const T *__restrict__ q,
-                              V4 *__restrict__ aos) {
+__global__ void __launch_bounds__(256) k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geom g,
+                                                     uint32_t *__restrict__ key, DevCounters *ctr,
+                                                     const T *__restrict__ q, V4 *__restrict__ aos, int passes,
+                                                     uint32_t *__restrict__ hist) {
+    __shared__ uint32_t sh[4][256];
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         uint32_t c[3];
         T xd[3];
@@ -79,8 +85,9 @@ __global__ void k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geo
             c[d] = (uint32_t)f;
         }
         if (bad) atomicMin(&ctr->err_index, (unsigned long long)i);
-        key[i] = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
-        idx[i] = i;
+        const uint32_t k = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
+        key[i] = k;
+        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
         if (aos) {
             V4 r;
             r.x = xd[0];
@@ -89,6 +96,11 @@ __global__ void k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geo
             r.w = q[i];
             aos[i] = r;
         }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+        const uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
     }
 }
 
@@ -313,15 +325,13 @@ __device__ __forceinline__ bool mb_eligible(bool enabled, bool tgt, uint32_t ite
 // 0: no quad, 1: leader (key % 4 == 0), 2: member of the quad led by box b - (key & 3)
 __device__ __forceinline__ int mb_role(uint32_t b, uint32_t key, uint32_t B, const uint32_t *__restrict__ bkey,
                                        const uint2 *__restrict__ box_nbr) {
+    if (!(box_nbr[b].x & MB_ELIG)) return 0;  // most boxes of clustered inputs: one load
     const uint32_t j = key & 3u;
     if (b < j || b - j + 3u >= B) return 0;
     const uint32_t lead = b - j, k0 = key - j;
 #pragma unroll
     for (uint32_t i = 0; i < 4; ++i) {
-        if (i == j) {
-            if (!(box_nbr[b].x & MB_ELIG)) return 0;
-            continue;
-        }
+        if (i == j) continue;
         if (bkey[lead + i] != k0 + i || !(box_nbr[lead + i].x & MB_ELIG)) return 0;
     }
     return j == 0 ? 1 : 2;
@@ -435,7 +445,7 @@ __global__ void __launch_bounds__(NB_THREADS) k_mb_tiles(const uint32_t *__restr
     const uint32_t ntiles = (B + NB_THREADS - 1) / NB_THREADS;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t b = tile * NB_THREADS + threadIdx.x;
-        const bool member = b < B && mb_role(b, bkey[b], B, bkey, box_nbr) == 2;
+        const bool member = b < B && (box_nbr[b].x & MB_ELIG) && mb_role(b, bkey[b], B, bkey, box_nbr) == 2;
         const uint32_t m = __popc(__ballot_sync(0xffffffffu, member));
         if ((threadIdx.x & 31u) == 0) s_m[threadIdx.x >> 5] = m;
         __syncthreads();
@@ -798,15 +808,16 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     }
     // a1 (+ the SoA input packed into records, unless the input already is records)
     void *aos = rec_in ? const_cast<void *>(rec_in) : P->s_aos;
+    P2P_CUDA_TRY(cudaMemsetAsync(P->s_hist, 0, (size_t)4 * 256 * sizeof(uint32_t), st));
     if (f64)
         P2P_LAUNCH((k_bin_gravity<double, double4>), gb, 256, 0, st, (const double *)pos, ps, n, P->geom, P->s_key,
-                   P->s_idx, P->ctr, (const double *)q, rec_in ? (double4 *)nullptr : (double4 *)aos);
+                   P->ctr, (const double *)q, rec_in ? (double4 *)nullptr : (double4 *)aos, P->passes, P->s_hist);
     else
         P2P_LAUNCH((k_bin_gravity<float, float4>), gb, 256, 0, st, (const float *)pos, ps, n, P->geom, P->s_key,
-                   P->s_idx, P->ctr, (const float *)q, rec_in ? (float4 *)nullptr : (float4 *)aos);
-    // a2
+                   P->ctr, (const float *)q, rec_in ? (float4 *)nullptr : (float4 *)aos, P->passes, P->s_hist);
+    // a2 (digit histograms from a1; first-pass values = input positions)
     P2P_CUDA_TRY(radix_sort_pairs(P->s_key, P->s_idx, P->s_kalt, P->s_valt, n, P->passes, P->ctr, P->s_hist,
-                                  P->s_status, st, &P->skey, &P->perm));
+                                  P->s_status, st, &P->skey, &P->perm, true, true));
     // a3
     if (f64)
         P2P_LAUNCH((k_permute_gravity<double4>), gb, 256, 0, st, (const double4 *)aos, P->perm, n, (double4 *)P->rec);

@@ -147,7 +147,7 @@ namespace p2p {
 // hist: [4][256] u32, status: [passes][ceil(n/4096)][256] u32 scratch (plan-owned)
 cudaError_t radix_sort_pairs(uint32_t *kin, uint32_t *vin, uint32_t *kalt, uint32_t *valt, uint32_t n, int passes,
                              DevCounters *ctr, uint32_t *hist, uint32_t *status, cudaStream_t st, uint32_t **kout,
-                             uint32_t **vout);
+                             uint32_t **vout, bool iota_values = false, bool hist_ready = false);
 size_t radix_status_words(uint64_t n, int passes);
 
 // k_structs.cu
