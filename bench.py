@@ -115,6 +115,10 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------ workload
 def make_workload(name: str, rank: int, world: int, seed: int = 0, dtype=np.float32):
     import p2p_inputs as G
+    if "-adaptive-t" in name:  # e.g. c3-adaptive-t16: the base workload on adaptive leaves of threshold t (NEXT-1)
+        base, t = name.split("-adaptive-t")
+        inp, desc = make_workload(base, rank, world, seed, dtype)
+        return inp, f"{desc} on adaptive binary-tree leaves, clustering threshold t = {int(t)} (p2p_adaptive_enable)"
     if name == "c5w":
         # rank r owns tile r of the G-tile domain (Morton octant == tile for 2x2x2)
         inp = G.plummer_tiles(12_500_000, 256, world, seed, dtype=dtype, tile_index=rank)
@@ -207,6 +211,9 @@ def ours(args, rank, world, local):
     # sizes need host syncs, then a1..a5 on the plan's buffers), a6, a7+a9 and the reverse all-to-all-v.
     splan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps, stream=stream,
                    comm=comm)
+    if "-adaptive-t" in args.workload:
+        # adaptive-leaf mode: the same step over the leaves, asynchronous (measured once here)
+        splan.enable_adaptive(int(args.workload.split("-adaptive-t")[1]))
     holder = {"plan": splan}
 
     def step(events=None):

@@ -38,7 +38,8 @@ EXPORTED = ["p2p_plan_create", "p2p_plan_update", "p2p_plan_update_host", "p2p_r
             "p2p_eval_host", "p2p_set_charges", "p2p_destroy",
             "p2p_get_info", "p2p_copy_out", "p2p_comm_unique_id", "p2p_comm_create", "p2p_comm_destroy",
             "p2p_partition_splitters", "p2p_get_splitters", "p2p_loopback_group_create", "p2p_loopback_group_destroy",
-            "p2p_comm_create_loopback", "p2p_comm_create_ipc", "p2p_status_string", "p2p_last_error", "p2p_kernel_launch_count",
+            "p2p_comm_create_loopback", "p2p_comm_create_ipc", "p2p_adaptive_enable", "p2p_adaptive_disable",
+            "p2p_status_string", "p2p_last_error", "p2p_kernel_launch_count",
             "p2p_abi_version"]
 
 
@@ -103,6 +104,8 @@ def lib() -> C.CDLL:
             "p2p_loopback_group_destroy": (None, [p]),
             "p2p_comm_create_loopback": (C.c_int, [p, C.c_int, C.POINTER(C.c_void_p)]),
             "p2p_comm_create_ipc": (C.c_int, [C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]),
+            "p2p_adaptive_enable": (C.c_int, [p, C.c_int, C.c_int]),
+            "p2p_adaptive_disable": (C.c_int, [p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -282,6 +285,14 @@ def p2p_comm_create_ipc(nranks: int, rank: int, name: str) -> int:
     return out.value
 
 
+def p2p_adaptive_enable(plan: int, t: int, min_bits: int = 9):
+    _check(lib().p2p_adaptive_enable(plan, int(t), int(min_bits)))
+
+
+def p2p_adaptive_disable(plan: int):
+    _check(lib().p2p_adaptive_disable(plan))
+
+
 def p2p_comm_create_loopback(group: int, rank: int) -> int:
     out = C.c_void_p()
     _check(lib().p2p_comm_create_loopback(C.c_void_p(group), int(rank), C.byref(out)))
@@ -425,6 +436,20 @@ class Plan:
 
     def restructure(self):
         p2p_restructure(self.handle)
+        if getattr(self, "adaptive", None):
+            self._info = None  # adaptive mode: records / pairs are counted by the restructure
+
+    def enable_adaptive(self, t: int, min_bits: int = 9):
+        """SURVEY NEXT-1 on the per-step path: run update / restructure / eval over adaptive leaves with threshold t
+        (p2p_adaptive_enable; measures the current input once, then every step is asynchronous)"""
+        _check(lib().p2p_adaptive_enable(self.handle, int(t), int(min_bits)))
+        self.adaptive = (int(t), int(min_bits))
+        self._info = None
+
+    def disable_adaptive(self):
+        _check(lib().p2p_adaptive_disable(self.handle))
+        self.adaptive = None
+        self._info = None
 
     def restructure_pairs(self):
         """the thread-level pair records of P2P_PAIRREC"""

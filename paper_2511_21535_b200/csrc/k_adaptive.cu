@@ -16,6 +16,15 @@
 
 namespace p2p {
 
+// device-side sizes of the persistent (asynchronous) adaptive path: kernels read the leaf / entry counts from device
+// memory (no host sync) and do nothing after a capacity overflow (null pointers: the synchronous entry points)
+struct DevN {
+    const uint32_t *L = nullptr, *E = nullptr, *ovf = nullptr;
+    __device__ __forceinline__ bool stop() const { return ovf && *ovf; }
+    __device__ __forceinline__ uint32_t l(uint32_t v) const { return L ? *L : v; }
+    __device__ __forceinline__ uint32_t e(uint32_t v) const { return E ? *E : v; }
+};
+
 namespace {
 // first box whose key is >= k (B boxes, ascending keys)
 __device__ __forceinline__ uint32_t lower_bound_key(const uint32_t *__restrict__ bkey, uint32_t B, uint64_t k) {
@@ -122,7 +131,9 @@ __device__ __forceinline__ uint32_t nbr_cell(const uint32_t c[3], const uint32_t
 // added to a's count, one transposed entry counted for every finer leaf in it
 __global__ void k_dil_ranges(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ llen, uint32_t L, int m,
                              uint2 *__restrict__ rng, uint8_t *__restrict__ rcode, unsigned int *__restrict__ dcnt,
-                             unsigned int *__restrict__ tcnt) {
+                             unsigned int *__restrict__ tcnt, DevN dn = DevN()) {
+    if (dn.stop()) return;
+    L = dn.l(L);
     const int bits = 3 * m;
     for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < 27ull * L;
          x += (uint64_t)gridDim.x * blockDim.x) {
@@ -154,7 +165,9 @@ __global__ void k_dil_ranges(const uint32_t *__restrict__ lkey, const uint32_t *
 __global__ void k_dil_fill(const uint32_t *__restrict__ llen, uint32_t L, const uint2 *__restrict__ rng,
                            const uint8_t *__restrict__ rcode, const uint32_t *__restrict__ off,
                            const unsigned int *__restrict__ dcnt, unsigned int *__restrict__ tcur,
-                           uint32_t *__restrict__ nbr, uint8_t *__restrict__ code) {
+                           uint32_t *__restrict__ nbr, uint8_t *__restrict__ code, DevN dn = DevN()) {
+    if (dn.stop()) return;
+    L = dn.l(L);
     constexpr unsigned FULL = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -190,7 +203,9 @@ __global__ void k_dil_fill(const uint32_t *__restrict__ llen, uint32_t L, const 
 // dilation run -- every entry's final position is its rank among the tail plus its rank among the dilation run
 __global__ void k_dil_merge(const uint32_t *__restrict__ off, const unsigned int *__restrict__ dcnt, uint32_t L,
                             const uint32_t *__restrict__ nbr, const uint8_t *__restrict__ code,
-                            uint32_t *__restrict__ nbr_out, uint8_t *__restrict__ code_out) {
+                            uint32_t *__restrict__ nbr_out, uint8_t *__restrict__ code_out, DevN dn = DevN()) {
+    if (dn.stop()) return;
+    L = dn.l(L);
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < L; a += nw) {
@@ -222,7 +237,11 @@ __global__ void k_dil_merge(const uint32_t *__restrict__ off, const unsigned int
 __global__ void k_adapt_count(const uint32_t *__restrict__ off, const uint32_t *__restrict__ nbr,
                               const uint8_t *__restrict__ code, const uint32_t *__restrict__ lstart, uint32_t L,
                               unsigned long long *__restrict__ R, uint32_t *__restrict__ tself,
-                              uint32_t *__restrict__ nitems) {
+                              uint32_t *__restrict__ nitems, DevN dn = DevN(),
+                              unsigned long long *__restrict__ pairs = nullptr) {
+    if (dn.stop()) return;
+    L = dn.l(L);
+    unsigned long long ip = 0;
     for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
         unsigned long long sum = 0, ts = 0;
         for (uint32_t e = off[a]; e < off[a + 1]; ++e) {
@@ -233,6 +252,12 @@ __global__ void k_adapt_count(const uint32_t *__restrict__ off, const uint32_t *
         R[a] = sum;
         tself[a] = (uint32_t)ts;
         nitems[a] = (lstart[a + 1] - lstart[a] + ITEM_TMAX - 1) / ITEM_TMAX;
+        ip += sum * (lstart[a + 1] - lstart[a]);
+    }
+    if (pairs) {  // I = sum over leaves of n_targets x run length (the pair count of the step)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ip += __shfl_xor_sync(0xffffffffu, ip, o);
+        if ((threadIdx.x & 31u) == 0 && ip) atomicAdd(pairs, ip);
     }
 }
 
@@ -240,7 +265,10 @@ __global__ void k_adapt_count(const uint32_t *__restrict__ off, const uint32_t *
 // lane: G = ceil(n_t / K) groups x S = floor(32 / G) source splits); targets staged from the self segment
 __global__ void k_adapt_items(const uint32_t *__restrict__ lstart, const unsigned long long *__restrict__ red_off,
                               const unsigned long long *__restrict__ R, const uint32_t *__restrict__ tself,
-                              const uint32_t *__restrict__ item_off, uint32_t L, uint32_t K, Item *__restrict__ items) {
+                              const uint32_t *__restrict__ item_off, uint32_t L, uint32_t K, Item *__restrict__ items,
+                              DevN dn = DevN()) {
+    if (dn.stop()) return;
+    L = dn.l(L);
     for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
         const uint32_t nt_all = lstart[a + 1] - lstart[a];
         uint32_t it = item_off[a];
@@ -264,7 +292,10 @@ __global__ void __launch_bounds__(256) k_adapt_restructure_chunks(
     const V4 *__restrict__ rec, const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ len,
     const uint32_t *__restrict__ lstart, const uint32_t *__restrict__ off, const uint32_t *__restrict__ nbr,
     const uint8_t *__restrict__ code, const unsigned long long *__restrict__ eoff, uint32_t L, uint32_t E, int m,
-    double Lbox, double lo0, double lo1, double lo2, V4 *__restrict__ red) {
+    double Lbox, double lo0, double lo1, double lo2, V4 *__restrict__ red, DevN dn = DevN()) {
+    if (dn.stop()) return;
+    L = dn.l(L);
+    E = dn.e(E);
     constexpr unsigned FULL = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5, nchunk = (E + 31u) >> 5;
@@ -355,7 +386,9 @@ struct EntryCntGet {
 
 // INDEXED over the leaves: per leaf, bit d = its cell touches the upper face of dim d (frame -L), bit 3 + d the lower
 __global__ void k_leaf_frame(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ len, uint32_t L, int m,
-                             uint8_t *__restrict__ fr) {
+                             uint8_t *__restrict__ fr, DevN dn = DevN()) {
+    if (dn.stop()) return;
+    L = dn.l(L);
     for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
         uint32_t sh[3];
         halvings_of((int)len[a], sh);
@@ -394,7 +427,8 @@ struct OffPut {
     __device__ void operator()(uint64_t p, uint32_t e, uint32_t) const { off[p] = e; }
 };
 __global__ void k_leaf_keys(const uint32_t *__restrict__ len, const uint32_t *__restrict__ prefix, uint32_t L,
-                            int bits, uint32_t *__restrict__ lkey) {
+                            int bits, uint32_t *__restrict__ lkey, DevN dn = DevN()) {
+    L = dn.l(L);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
         lkey[i] = (uint32_t)((uint64_t)prefix[i] << (bits - (int)len[i]));
 }
@@ -642,6 +676,205 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, vo
     for (void *p : bufs) dfree(p, st);
     A.release(st);
     return s;
+}
+
+}  // namespace p2p
+
+// ======================================================================================================================
+// The persistent, asynchronous adaptive path (SURVEY NEXT-1 on the per-step path; "p2p_plan_update
+// builds adaptive leaves, CSR, runs and items in place, with no host sync").  p2p_adaptive_enable measures the
+// current input once (synchronous, like p2p_plan_create) and allocates capacities with headroom: leaves <= boxes,
+// entries <= ecap = 2 E, records <= rcap = 2 R, items <= boxes + N / 32.  Every later p2p_plan_update runs a1-a4
+// and the leaves + closed CSR with all counts device-side (the kernels read L / E from device memory); p2p_restructure
+// builds the runs and items, p2p_eval runs the unchanged eval over them.  A step that exceeds a capacity sets a
+// device overflow flag: its kernels do nothing and p2p_get_info reports P2P_ERR_OUT_OF_MEMORY (call
+// p2p_adaptive_enable again to re-measure).
+namespace p2p {
+
+namespace {
+__global__ void k_adapt_tail(AdaptCtr *ac, uint32_t *__restrict__ lstart, uint32_t n) { lstart[ac->L] = n; }
+// after the entry scan: off[L] = E and the entry capacity check
+__global__ void k_adapt_check_e(AdaptCtr *ac, uint32_t *__restrict__ off, uint64_t ecap) {
+    if (ac->E > ecap) ac->overflow = 1u;
+    off[ac->L] = ac->E;
+}
+__global__ void k_adapt_check_r(AdaptCtr *ac, uint64_t rcap, uint64_t icap) {
+    if (ac->R > rcap || ac->n_items > icap) ac->overflow = 1u;
+    if (ac->overflow) ac->n_items = 0;  // the eval then does nothing (its items were not built)
+}
+}  // namespace
+
+void adaptive_free(p2p_plan *P) {
+    AdaptState *A = P->ad;
+    if (!A) return;
+    cudaStream_t st = P->stream;
+    void *bufs[] = {A->ac,    A->len8, A->rcode, A->code, A->code_t, A->lframe, A->llen, A->lprefix, A->lstart,
+                    A->lkey,  A->off,  A->nbr,   A->nbr_t, A->tself, A->nit,    A->ioff, A->zero,    A->dcnt,
+                    A->tcnt,  A->tcur, A->rng,   A->R,    A->roff,   A->eoff,   A->red,  A->scr,     A->items};
+    for (void *b : bufs) dfree(b, st);
+    delete A;
+    P->ad = nullptr;
+}
+
+p2p_status adaptive_enable(p2p_plan *P, uint32_t t, int min_bits) {
+    cudaStream_t st = P->stream;
+    adaptive_free(P);
+    // measure the current input (synchronous, once): entries and records of its leaves
+    int64_t E = 0, R = 0;
+    if (P->B > 0) {
+        AdaptiveDev D;
+        p2p_status s = build_adaptive(P, t, min_bits, D);
+        E = D.E;
+        D.release(st);
+        if (s != P2P_OK) return s;
+        s = adaptive_eval(P, t, min_bits, false, nullptr, nullptr, nullptr, 0, &R);
+        if (s != P2P_OK) return s;
+    }
+    AdaptState *A = new AdaptState();
+    P->ad = A;
+    A->t = t;
+    A->min_bits = std::min(min_bits, P->key_bits);
+    A->bcap = std::max<int64_t>(P->bcap, 1);
+    A->ecap = std::max<int64_t>(2 * E, 64);
+    A->rcap = std::max<int64_t>(2 * R, std::max<int64_t>(P->cap, 1));
+    A->icap = A->bcap + P->cap / 32 + 1;
+    const int64_t L = A->bcap, Ec = A->ecap;
+    const size_t rsz = P->cfg.precision == P2P_FP64 ? sizeof(double4) : sizeof(float4);
+#define ADA(ptr, bytes)                                                                   \
+    do {                                                                                  \
+        if (dalloc((void **)&(ptr), (size_t)(bytes), st) != cudaSuccess) {             \
+            adaptive_free(P);                                                             \
+            set_error("cannot allocate the adaptive-leaf buffers");                       \
+            return P2P_ERR_OUT_OF_MEMORY;                                                 \
+        }                                                                                 \
+    } while (0)
+    ADA(A->ac, sizeof(AdaptCtr));
+    ADA(A->len8, L);
+    ADA(A->llen, 4 * L);
+    ADA(A->lprefix, 4 * L);
+    ADA(A->lstart, 4 * (L + 1));
+    ADA(A->lkey, 4 * L);
+    ADA(A->dcnt, 4 * L);
+    ADA(A->tcnt, 4 * L);
+    ADA(A->tcur, 4 * L);
+    ADA(A->rng, 8 * 27 * L);
+    ADA(A->rcode, 27 * L);
+    ADA(A->off, 4 * (L + 1));
+    ADA(A->nbr, 4 * Ec);
+    ADA(A->code, Ec);
+    ADA(A->nbr_t, 4 * Ec);
+    ADA(A->code_t, Ec);
+    ADA(A->R, 8 * L);
+    ADA(A->roff, 8 * L);
+    ADA(A->tself, 4 * L);
+    ADA(A->nit, 4 * L);
+    ADA(A->ioff, 4 * L);
+    ADA(A->eoff, 8 * Ec);
+    ADA(A->lframe, L);
+    ADA(A->zero, 4);
+    ADA(A->red, rsz * A->rcap);
+    ADA(A->items, sizeof(Item) * A->icap);
+    ADA(A->scr, std::max(scan_partials_bytes(L), scan_partials_bytes(Ec)));
+#undef ADA
+    P2P_CUDA_TRY(cudaMemsetAsync(A->zero, 0, 4, st));
+    return adaptive_build_async(P);
+}
+
+// a5 of adaptive mode: leaves (C22) + closed CSR (C23) of the current sorted boxes, all counts device-side
+p2p_status adaptive_build_async(p2p_plan *P) {
+    AdaptState *A = P->ad;
+    cudaStream_t st = P->stream;
+    A->built = true;
+    A->runs_valid = false;
+    P2P_CUDA_TRY(cudaMemsetAsync(A->ac, 0, sizeof(AdaptCtr), st));
+    if (P->n == 0) return P2P_OK;
+    const int bits = P->key_bits, m = bits / 3;
+    const uint32_t Lc = (uint32_t)A->bcap;
+    const DevN dn{&A->ac->L, &A->ac->E, &A->ac->overflow};
+    const unsigned gb = std::max<unsigned>(1, std::min<unsigned>(div_up(Lc, 256), (unsigned)P->num_sms * 8));
+    const unsigned g27 = std::max<unsigned>(1, std::min<unsigned>(div_up(27ull * Lc, 256), (unsigned)P->num_sms * 16));
+    const unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up(32ull * Lc, 256), (unsigned)P->num_sms * 16));
+    // leaves: length per box, head-flag scan -> Morton-ordered leaf table (device L)
+    P2P_LAUNCH(k_leaf_len, gb, 256, 0, st, P->bkey, P->bstart, P->ctr, bits, A->t, A->min_bits, A->len8);
+    P2P_CUDA_TRY(device_scan<uint32_t>(LeafHeadGet{P->bkey, A->len8, bits},
+                                       LeafHeadPut{P->bkey, P->bstart, A->len8, bits, A->llen, A->lprefix, A->lstart},
+                                       &P->ctr->B, Lc, &A->ac->L, A->scr, st));
+    P2P_LAUNCH(k_adapt_tail, 1, 1, 0, st, A->ac, A->lstart, (uint32_t)P->n);
+    P2P_LAUNCH(k_leaf_keys, gb, 256, 0, st, A->llen, A->lprefix, Lc, bits, A->lkey, dn);
+    // closed neighbour CSR: dilation ranges, counts, scan (device E), fill, merge
+    P2P_CUDA_TRY(cudaMemsetAsync(A->dcnt, 0, 4 * (size_t)Lc, st));
+    P2P_CUDA_TRY(cudaMemsetAsync(A->tcnt, 0, 4 * (size_t)Lc, st));
+    P2P_CUDA_TRY(cudaMemsetAsync(A->tcur, 0, 4 * (size_t)Lc, st));
+    P2P_LAUNCH(k_dil_ranges, g27, 256, 0, st, A->lkey, A->llen, Lc, m, A->rng, A->rcode, A->dcnt, A->tcnt, dn);
+    P2P_CUDA_TRY(device_scan<uint32_t>(SumGet{A->dcnt, A->tcnt}, OffPut{A->off}, &A->ac->L, Lc, &A->ac->E, A->scr, st));
+    P2P_LAUNCH(k_adapt_check_e, 1, 1, 0, st, A->ac, A->off, (uint64_t)A->ecap);
+    P2P_LAUNCH(k_dil_fill, gw, 256, 0, st, A->llen, Lc, A->rng, A->rcode, (const uint32_t *)A->off,
+               (const unsigned int *)A->dcnt, A->tcur, A->nbr_t, A->code_t, dn);
+    P2P_LAUNCH(k_dil_merge, gw, 256, 0, st, (const uint32_t *)A->off, (const unsigned int *)A->dcnt, Lc,
+               (const uint32_t *)A->nbr_t, (const uint8_t *)A->code_t, A->nbr, A->code, dn);
+    P2P_CUDA_TRY(cudaGetLastError());
+    return P2P_OK;
+}
+
+// a6 of adaptive mode: per-leaf run lengths / self offsets / items (scans: device R, items), entry offsets, the
+// redundant runs (C24), the work items and (INDEXED) the leaf frames
+p2p_status adaptive_restructure_async(p2p_plan *P) {
+    AdaptState *A = P->ad;
+    cudaStream_t st = P->stream;
+    if (P->n == 0) {
+        A->runs_valid = true;
+        return P2P_OK;
+    }
+    const bool f64 = P->cfg.precision == P2P_FP64;
+    const int m = P->key_bits / 3;
+    const uint32_t Lc = (uint32_t)A->bcap;
+    const DevN dn{&A->ac->L, &A->ac->E, &A->ac->overflow};
+    const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(Lc, 128), (unsigned)P->num_sms * 8));
+    P2P_CUDA_TRY(cudaMemsetAsync(&A->ac->I, 0, sizeof(unsigned long long), st));
+    P2P_LAUNCH(k_adapt_count, g, 128, 0, st, A->off, A->nbr, A->code, A->lstart, Lc, A->R, A->tself, A->nit, dn,
+               &A->ac->I);
+    P2P_CUDA_TRY(device_scan<unsigned long long>(U64Get{A->R}, U64Put{A->roff}, &A->ac->L, Lc, &A->ac->R, A->scr, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(CntGet{A->nit}, OffPut{A->ioff}, &A->ac->L, Lc, &A->ac->n_items, A->scr, st));
+    P2P_LAUNCH(k_adapt_check_r, 1, 1, 0, st, A->ac, (uint64_t)A->rcap, (uint64_t)A->icap);
+    P2P_CUDA_TRY(device_scan<unsigned long long>(EntryCntGet{A->nbr, A->lstart}, U64Put{A->eoff}, &A->ac->E,
+                                                 (uint64_t)A->ecap, (unsigned long long *)nullptr, A->scr, st));
+    P2P_LAUNCH(k_leaf_frame, g, 128, 0, st, A->lkey, A->llen, Lc, m, A->lframe, dn);
+    const unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up((uint64_t)A->ecap, 256), (unsigned)P->num_sms * 16));
+    const Geom &G = P->geom;
+    if (f64)
+        P2P_LAUNCH((k_adapt_restructure_chunks<double, double4>), gw, 256, 0, st, (const double4 *)P->rec, A->lkey,
+                   A->llen, A->lstart, A->off, A->nbr, A->code, A->eoff, Lc, (uint32_t)A->ecap, m, G.L[0], G.lo[0],
+                   G.lo[1], G.lo[2], (double4 *)A->red, dn);
+    else
+        P2P_LAUNCH((k_adapt_restructure_chunks<float, float4>), gw, 256, 0, st, (const float4 *)P->rec, A->lkey,
+                   A->llen, A->lstart, A->off, A->nbr, A->code, A->eoff, Lc, (uint32_t)A->ecap, m, G.L[0], G.lo[0],
+                   G.lo[1], G.lo[2], (float4 *)A->red, dn);
+    P2P_LAUNCH(k_adapt_items, g, 128, 0, st, A->lstart, A->roff, A->R, A->tself, A->ioff, Lc,
+               (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32), A->items, dn);
+    P2P_CUDA_TRY(cudaGetLastError());
+    A->runs_valid = true;
+    return P2P_OK;
+}
+
+// a7 + a9 of adaptive mode: REDUNDANT over the runs, or INDEXED over the leaves' CSR segments (the baseline)
+p2p_status adaptive_eval_async(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
+    AdaptState *A = P->ad;
+    if (P->n == 0) return P2P_OK;
+    EvalItems it{A->items, &A->ac->n_items, A->icap, A->red, A->zero};
+    if (layout == P2P_INDEXED) {
+        it.csr_off = A->off;
+        it.csr_nbr = A->nbr;
+        it.csr_code = A->code;
+        it.lstart = A->lstart;
+        it.lframe = A->lframe;
+    }
+    return eval_gravity_items(P, it, phi, field);  // after an overflow n_items = 0: nothing is evaluated
+}
+
+p2p_status adaptive_info(p2p_plan *P, AdaptCtr *out) {
+    P2P_CUDA_TRY(cudaMemcpyAsync(out, P->ad->ac, sizeof(AdaptCtr), cudaMemcpyDeviceToHost, P->stream));
+    P2P_CUDA_TRY(cudaStreamSynchronize(P->stream));
+    return P2P_OK;
 }
 
 }  // namespace p2p

@@ -794,7 +794,7 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     return P2P_OK;
 }
 
-p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, const void *rec_in) {
+p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, const void *rec_in, bool grid_a5) {
     cudaStream_t st = P->stream;
     const uint32_t n = (uint32_t)P->n;
     const bool f64 = P->cfg.precision == P2P_FP64;
@@ -829,6 +829,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, 1u},
                                        HeadPut{P->skey, 1u, P->bkey, P->bstart, nullptr, n, P->occ}, nullptr, n,
                                        &P->ctr->B, P->s_partials, st));
+    if (!grid_a5) return cudaGetLastError() == cudaSuccess ? P2P_OK : P2P_ERR_CUDA;  // adaptive mode: its own a5
     // a5
     const uint64_t bcap = (uint64_t)P->bcap;
     P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->sum_nb2, 0, sizeof(unsigned long long), st));

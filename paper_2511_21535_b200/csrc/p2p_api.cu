@@ -137,6 +137,7 @@ static p2p_status mark(p2p_plan *P, p2p_status s) {
 
 static void free_plan_buffers(p2p_plan *P) {
     cudaStream_t st = P->stream;
+    adaptive_free(P);
     free_capacity(P);
     free_distributed(P);
     free_pairrec(P);
@@ -430,11 +431,25 @@ p2p_status p2p_plan_update(p2p_plan *P, int64_t n_local, const void *positions, 
     P->pr_valid = false;
     cudaMemsetAsync(P->ctr, 0, sizeof(DevCounters), st);
     cudaMemsetAsync(&P->ctr->err_index, 0xff, sizeof(unsigned long long), st);
+    if (P->ad) P->ad->runs_valid = false;
     if (n_local == 0) {
         P->sizes_known = true;
         P->B = P->n_nbr = P->R = P->I = P->n_items = 0;
+        if (P->ad) return mark(P, adaptive_build_async(P));
+        P->grid_stale = false;
         return P2P_OK;
     }
+    if (P->ad) {  // adaptive-leaf mode: a1-a4 as always, then the leaves + closed CSR (no grid a5), asynchronous
+        s = build_gravity_structs(P, positions, charges, nullptr, false);
+        if (s != P2P_OK) return mark(P, s);
+        if (P->bcap > P->ad->bcap) {  // the box capacity grew (rare): re-measure and re-allocate (synchronous)
+            s = resolve_sizes(P);
+            if (s != P2P_OK) return s;
+            return mark(P, adaptive_enable(P, P->ad->t, P->ad->min_bits));
+        }
+        return mark(P, adaptive_build_async(P));
+    }
+    P->grid_stale = false;
     return mark(P, build_gravity_structs(P, positions, charges));
 }
 
@@ -504,6 +519,8 @@ p2p_status p2p_restructure(p2p_plan *P) {
         P->red_valid = true;
         return P2P_OK;
     }
+    if (P->ad) return mark(P, adaptive_restructure_async(P));  // adaptive mode: the leaves' runs + items
+    if (P->grid_stale) return fail(P2P_ERR_BAD_STATE, "after p2p_adaptive_disable: call p2p_plan_update first");
     s = P->cfg.kernel == P2P_GRAVITY ? restructure_gravity(P) : restructure_helmholtz(P);
     if (s == P2P_OK) P->red_valid = true;
     return mark(P, s);
@@ -600,6 +617,17 @@ p2p_status p2p_eval(p2p_plan *P, p2p_layout layout, void *potential, void *field
         if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
         return mark(P, eval_pairrec(P, potential, field));
     }
+    if (P->ad) {  // adaptive-leaf mode
+        if (layout != P2P_REDUNDANT && layout != P2P_INDEXED)
+            return fail(P2P_ERR_UNSUPPORTED, "adaptive mode evaluates P2P_REDUNDANT or P2P_INDEXED");
+        if (!P->ad->runs_valid)
+            return fail(P2P_ERR_BAD_STATE, "eval needs p2p_restructure first in adaptive mode (and after update)");
+        if (P->n == 0) return P2P_OK;
+        if (!is_device_ptr(potential)) return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
+        if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
+        return mark(P, adaptive_eval_async(P, layout, potential, field));
+    }
+    if (P->grid_stale) return fail(P2P_ERR_BAD_STATE, "after p2p_adaptive_disable: call p2p_plan_update first");
     if (layout == P2P_REDUNDANT && !P->red_valid)
         return fail(P2P_ERR_BAD_STATE, "eval(P2P_REDUNDANT) needs p2p_restructure first (and after set_charges)");
     if (P->comm) {  // collective: every rank calls, even with no particles
@@ -626,6 +654,7 @@ p2p_status p2p_set_charges(p2p_plan *P, const void *charges) {
     if (!is_device_ptr(charges)) return fail(P2P_ERR_INVALID_ARGUMENT, "charges must be a device pointer");
     P->red_valid = false;
     P->pr_valid = false;
+    if (P->ad) P->ad->runs_valid = false;
     s = P->cfg.kernel == P2P_GRAVITY ? set_charges_gravity(P, charges) : set_charges_helmholtz(P, charges);
     return mark(P, s);
 }
@@ -656,6 +685,45 @@ p2p_status p2p_get_info(const p2p_plan *Pc, p2p_info *out) {
     out->n_items = P->n_items;
     out->key_bits = P->key_bits;
     out->sort_passes = P->passes;
+    if (P->ad) {  // adaptive mode: the leaves' counts (pairs / records after p2p_restructure)
+        AdaptCtr h;
+        rs = adaptive_info(P, &h);
+        if (rs != P2P_OK) return rs;
+        if (h.overflow)
+            return fail(P2P_ERR_OUT_OF_MEMORY, "adaptive capacities exceeded by the last update (entries / records / "
+                                               "items above 2x the measured input): call p2p_adaptive_enable again");
+        out->n_boxes = h.L;
+        out->n_nbr = h.E;
+        out->n_red = (int64_t)h.R;
+        out->n_pairs = (int64_t)h.I;
+        out->n_items = h.n_items;
+    }
+    return P2P_OK;
+}
+
+p2p_status p2p_adaptive_enable(p2p_plan *P, int32_t t, int32_t min_bits) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (t < 1 || min_bits < 9) return fail(P2P_ERR_INVALID_ARGUMENT, "adaptive mode: t < 1 or min_bits < 9 (C22)");
+    if (P->cfg.kernel != P2P_GRAVITY || P->comm)
+        return fail(P2P_ERR_UNSUPPORTED, "adaptive mode is for single-GPU gravity plans");
+    const int32_t n0 = P->cfg.nbox[0];
+    if (P->cfg.nbox[1] != n0 || P->cfg.nbox[2] != n0 || (n0 & (n0 - 1)) != 0 || n0 < 8 || P->cfg.periodic_mask != 7u)
+        return fail(P2P_ERR_UNSUPPORTED, "adaptive mode needs a periodic cube of 2^m >= 8 boxes per dimension (C22)");
+    s = resolve_sizes(P);
+    if (s != P2P_OK) return s;
+    return mark(P, adaptive_enable(P, (uint32_t)t, min_bits));
+}
+
+p2p_status p2p_adaptive_disable(p2p_plan *P) {
+    p2p_status s = enter(P);
+    if (s != P2P_OK) return s;
+    if (!P->ad) return P2P_OK;
+    adaptive_free(P);
+    // the grid a5 structures (neighbour CSR, items) are not built in adaptive mode: the next grid restructure / eval
+    // needs a p2p_plan_update first
+    P->grid_stale = true;
+    P->red_valid = false;
     return P2P_OK;
 }
 

@@ -78,6 +78,31 @@ struct Geom {
 
 }  // namespace p2p
 
+namespace p2p {
+// the persistent adaptive-leaf state (SURVEY NEXT-1 on the per-step path, k_adaptive.cu): capacities fixed at
+// p2p_adaptive_enable, every count device-side, no host sync per step
+struct AdaptCtr {
+    uint32_t L, E, n_items, overflow;
+    unsigned long long R, I;
+};
+struct AdaptState {
+    uint32_t t = 0;
+    int min_bits = 9;
+    int64_t bcap = 0, ecap = 0, rcap = 0, icap = 0;
+    AdaptCtr *ac = nullptr;
+    uint8_t *len8 = nullptr, *rcode = nullptr, *code = nullptr, *code_t = nullptr, *lframe = nullptr;
+    uint32_t *llen = nullptr, *lprefix = nullptr, *lstart = nullptr, *lkey = nullptr, *off = nullptr, *nbr = nullptr,
+             *nbr_t = nullptr, *tself = nullptr, *nit = nullptr, *ioff = nullptr, *zero = nullptr;
+    unsigned int *dcnt = nullptr, *tcnt = nullptr, *tcur = nullptr;
+    uint2 *rng = nullptr;
+    unsigned long long *R = nullptr, *roff = nullptr, *eoff = nullptr;
+    void *red = nullptr, *scr = nullptr;
+    Item *items = nullptr;
+    bool built = false;     // leaves + CSR of the current positions
+    bool runs_valid = false;
+};
+}  // namespace p2p
+
 struct p2p_plan {
     p2p_config cfg;
     cudaStream_t stream = nullptr;
@@ -131,6 +156,8 @@ struct p2p_plan {
     std::vector<uint32_t> splitters;        // G + 1 key boundaries of the rank ranges
     void *phi_loc = nullptr, *field_loc = nullptr, *res_own = nullptr, *res_back = nullptr;
     bool red_valid = false;
+    p2p::AdaptState *ad = nullptr;  // adaptive-leaf mode (p2p_adaptive_enable)
+    bool grid_stale = false;        // grid a5 not built (after adaptive-mode updates) until the next p2p_plan_update
     // SURVEY NEXT-4 pair records (k_pairrec.cu): [T + R] records, [T] partial slots, t_off[B + 1] slot bases
     void *pr = nullptr, *pr_partial = nullptr;
     unsigned long long *pr_toff = nullptr;
@@ -154,7 +181,8 @@ size_t radix_status_words(uint64_t n, int passes);
 p2p_status alloc_capacity(p2p_plan *P, int64_t cap);   // all N-/B-sized buffers + scratch
 void free_capacity(p2p_plan *P);
 // pos/q: SoA caller arrays; or, if rec_in != nullptr, AoS {x,y,z,m} records (multi-GPU local plans)
-p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, const void *rec_in = nullptr);
+p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, const void *rec_in = nullptr,
+                                 bool grid_a5 = true);
 p2p_status build_helmholtz_structs(p2p_plan *P, const void *pos, const void *q);
 p2p_status set_charges_gravity(p2p_plan *P, const void *q);
 p2p_status set_charges_helmholtz(p2p_plan *P, const void *q);
@@ -197,6 +225,13 @@ p2p_status adaptive_leaves(p2p_plan *P, uint32_t t, int min_bits, uint32_t *len_
 p2p_status adaptive_neighbours(p2p_plan *P, uint32_t t, int min_bits, uint32_t *off_h, uint32_t *nbr_h,
                                uint8_t *code_h, int64_t cap_leaves, int64_t cap_entries, int64_t *n_leaves,
                                int64_t *n_entries);
+// the persistent asynchronous adaptive path (p2p_adaptive_enable / update / restructure / eval in adaptive mode)
+p2p_status adaptive_enable(p2p_plan *P, uint32_t t, int min_bits);
+void adaptive_free(p2p_plan *P);
+p2p_status adaptive_build_async(p2p_plan *P);
+p2p_status adaptive_restructure_async(p2p_plan *P);
+p2p_status adaptive_eval_async(p2p_plan *P, p2p_layout layout, void *phi, void *field);
+p2p_status adaptive_info(p2p_plan *P, AdaptCtr *out);  // synchronises
 p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, void *phi, void *field, void *red_h,
                          int64_t cap_red, int64_t *n_red);
 

@@ -45,7 +45,7 @@ __device__ __forceinline__ T block_excl_scan(T v, T *total) {
 template <typename T, typename Get>
 __global__ void __launch_bounds__(SC_THREADS) k_scan_reduce(Get get, const uint32_t *nptr, uint64_t ncap,
                                                             T *partials) {
-    const uint64_t n = nptr ? (uint64_t)*nptr : ncap;
+    const uint64_t n = nptr ? min((uint64_t)*nptr, ncap) : ncap;  // a device count never exceeds the capacity
     const uint64_t base = (uint64_t)blockIdx.x * SC_TILE;
     T s = 0;
     if (base < n) {
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_partials(T *partials, uint3
 template <typename T, typename Get, typename Put>
 __global__ void __launch_bounds__(SC_THREADS) k_scan_down(Get get, Put put, const uint32_t *nptr, uint64_t ncap,
                                                           const T *partials) {
-    const uint64_t n = nptr ? (uint64_t)*nptr : ncap;
+    const uint64_t n = nptr ? min((uint64_t)*nptr, ncap) : ncap;  // a device count never exceeds the capacity
     const uint64_t base = (uint64_t)blockIdx.x * SC_TILE;
     if (base >= n) return;  // whole block beyond n: uniform exit (no barrier below is skipped partially)
     // thread-contiguous items: thread t owns [base + t*ITEMS, base + (t+1)*ITEMS)
