@@ -36,7 +36,8 @@ def main(d):
     for f in sorted(glob.glob(os.path.join(d, "*.log"))):
         tool, case = os.path.basename(f)[:-4].split("_", 1)
         text = open(f, errors="replace").read()
-        summ = re.findall(r"ERROR SUMMARY: (\d+) error", text)
+        summ = re.findall(r"ERROR SUMMARY: (\d+) error", text) or \
+            re.findall(r"RACECHECK SUMMARY: (\d+) hazard", text)
         total = int(summ[-1]) if summ else -1
         rc = re.findall(r"^rc=(\d+)", text, re.M)
         done = f"case {case} done" in text
