@@ -57,6 +57,18 @@ __device__ __forceinline__ uint32_t item_size(uint32_t nb_b, uint64_t nsrc, uint
 }
 
 // ------------------------------------------------------------------------------------------------ a1
+// floor(fl(a / h)) (C6: the IEEE fp64 division, then floor) without the division in the common case: q = fl(a *
+// fl(1/h)) is within 2^-52 |q| (1 + 2^-52) of a/h and fl(a/h) within 2^-53 of it, so floor(q) == floor(fl(a/h))
+// whenever q is farther than 2^-50 |q| from an integer (q - f and f + 1 - q are exact: Sterbenz); otherwise -- a
+// point within a few ulp of a box face -- the division decides, exactly as the oracle (face tests pin both paths)
+__device__ __forceinline__ double floor_div_exact(double a, double h, double inv_h) {
+    const double q = a * inv_h;
+    const double f = floor(q);
+    const double margin = fabs(q) * 0x1p-50;
+    if (q - f > margin && (f + 1.0) - q > margin) return f;
+    return floor(__ddiv_rn(a, h));
+}
+
 // positions at pos[i * ps + d] (ps = 3: the caller's [N][3] array; ps = 4: {x,y,z,m} records).  With `aos` the
 // caller's SoA input is also packed into {x,y,z,m} records in input order (read sequentially here), so that the a3
 // gather touches ONE 16-byte record per particle instead of a position and a mass in two arrays (two DRAM bursts)
@@ -70,6 +82,7 @@ __global__ void __launch_bounds__(256) k_bin_gravity(const T *__restrict__ pos, 
     __shared__ uint32_t sh[4][256];
     for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
     __syncthreads();
+    const double inv_h = 1.0 / g.h;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         uint32_t c[3];
         T xd[3];
@@ -77,7 +90,7 @@ __global__ void __launch_bounds__(256) k_bin_gravity(const T *__restrict__ pos, 
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             xd[d] = pos[(size_t)ps * i + d];
-            double f = floor(__ddiv_rn(__dsub_rn((double)xd[d], g.lo[d]), g.h));
+            double f = floor_div_exact(__dsub_rn((double)xd[d], g.lo[d]), g.h, inv_h);
             if (!(f >= 0.0 && f < (double)g.nbox[d])) {
                 bad = true;
                 f = 0.0;
@@ -186,6 +199,10 @@ struct HeadGet {
     __device__ uint32_t operator()(uint64_t p) const {
         return (p == 0 || skey[p] / div != skey[p - 1] / div) ? 1u : 0u;
     }
+};
+struct HeadGet1 {  // gravity: the box key is the sorted key itself (no division)
+    const uint32_t *skey;
+    __device__ uint32_t operator()(uint64_t p) const { return (p == 0 || skey[p] != skey[p - 1]) ? 1u : 0u; }
 };
 struct HeadPut {
     const uint32_t *skey;
@@ -756,7 +773,8 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
     P2P_CUDA_TRY(dalloc((void **)&P->s_kalt, 4 * n, st));
     P2P_CUDA_TRY(dalloc((void **)&P->s_valt, 4 * n, st));
     P2P_CUDA_TRY(dalloc((void **)&P->s_hist, 4 * 4 * 256, st));
-    P2P_CUDA_TRY(dalloc((void **)&P->s_status, 4 * std::max<size_t>(1, radix_status_words(n, std::max(1, P->passes))), st));
+    P2P_CUDA_TRY(dalloc((void **)&P->s_status, 4 * std::max<size_t>(scan_lb_status_words(n),
+                                                                    radix_status_words(n, std::max(1, P->passes))), st));
     P2P_CUDA_TRY(dalloc(&P->s_partials, scan_partials_bytes(std::max(n, bcap)), st));
     P2P_CUDA_TRY(dalloc((void **)&P->bkey, 4 * bcap, st));
     P2P_CUDA_TRY(dalloc((void **)&P->bstart, 4 * (bcap + 1), st));
@@ -826,7 +844,9 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     // a4
     const uint64_t occ_words = std::max<uint64_t>(1, (1ull << P->key_bits) / 32);
     P2P_CUDA_TRY(cudaMemsetAsync(P->occ, 0, 4 * occ_words, st));
-    P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet{P->skey, 1u},
+    // (a single-pass look-back variant, scan.cuh device_scan_lb, measured 124 vs 99 us on c5w: the 3052 tiles'
+    // walks back over unpublished prefixes cost more than the second read of the keys)
+    P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet1{P->skey},
                                        HeadPut{P->skey, 1u, P->bkey, P->bstart, nullptr, n, P->occ}, nullptr, n,
                                        &P->ctr->B, P->s_partials, st));
     if (!grid_a5) return cudaGetLastError() == cudaSuccess ? P2P_OK : P2P_ERR_CUDA;  // adaptive mode: its own a5

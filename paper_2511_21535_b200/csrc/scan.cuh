@@ -119,4 +119,89 @@ cudaError_t device_scan(Get get, Put put, const uint32_t *nptr, uint64_t ncap, T
     return cudaGetLastError();
 }
 
+// ---- single-pass scan (u32 values < 2^30) with decoupled look-back: reads the input ONCE (the 3-phase scan
+// above reads it twice and launches three kernels).  Tiles are claimed in launch order through `tile_ctr`, so every
+// predecessor of a tile is already running; a tile publishes its aggregate, then a warp walks back 32 predecessors
+// per step to the nearest inclusive prefix.  `status` holds >= ceil(ncap / SCL_TILE) words, zeroed before the
+// launch together with *tile_ctr.
+constexpr int SCL_ITEMS = 16;
+constexpr int SCL_TILE = SC_THREADS * SCL_ITEMS;
+constexpr uint32_t SCL_AGG = 1u << 30, SCL_INC = 2u << 30, SCL_VAL = (1u << 30) - 1u;
+
+template <typename Get, typename Put>
+__global__ void __launch_bounds__(SC_THREADS) k_scan_lb(Get get, Put put, const uint32_t *nptr, uint64_t ncap,
+                                                        uint32_t *status, uint32_t *tile_ctr, uint32_t *total_out) {
+    __shared__ uint32_t s_tile, s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t n = nptr ? min((uint64_t)*nptr, ncap) : ncap;
+    const uint64_t base = (uint64_t)tile * SCL_TILE;
+    if (base >= n) return;  // no successor of this tile holds elements either
+    uint32_t vals[SCL_ITEMS];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < SCL_ITEMS; ++i) {
+        const uint64_t idx = base + (uint64_t)threadIdx.x * SCL_ITEMS + i;
+        vals[i] = idx < n ? get(idx) : 0u;
+        sum += vals[i];
+    }
+    uint32_t tot;
+    const uint32_t bex = block_excl_scan<uint32_t>(sum, &tot);
+    if (threadIdx.x < 32) {
+        const unsigned lane = threadIdx.x;
+        volatile uint32_t *vs = status;
+        uint32_t excl = 0;
+        if (tile == 0) {
+            if (lane == 0) vs[0] = SCL_INC | tot;
+        } else {
+            if (lane == 0) vs[tile] = SCL_AGG | tot;
+            for (int64_t t = (int64_t)tile - 1;; t -= 32) {
+                const int64_t q = t - (int64_t)lane;
+                uint32_t v = SCL_INC;  // before tile 0: an inclusive zero
+                if (q >= 0)
+                    do {
+                        v = vs[q];
+                    } while ((v & ~SCL_VAL) == 0u);
+                const uint32_t inc = __ballot_sync(0xffffffffu, (v & ~SCL_VAL) == SCL_INC);
+                const int first = inc ? __ffs(inc) - 1 : 32;  // nearest predecessor with an inclusive prefix
+                uint32_t part = (int)lane <= first ? (v & SCL_VAL) : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                excl += part;
+                if (inc) break;
+            }
+            __threadfence();
+            if (lane == 0) vs[tile] = SCL_INC | (excl + tot);
+        }
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    uint32_t e = s_excl + bex;
+#pragma unroll
+    for (int i = 0; i < SCL_ITEMS; ++i) {
+        const uint64_t idx = base + (uint64_t)threadIdx.x * SCL_ITEMS + i;
+        if (idx < n) put(idx, e, vals[i]);
+        e += vals[i];
+    }
+    if (total_out && base + SCL_TILE >= n && threadIdx.x == 0) *total_out = s_excl + tot;  // the last tile
+}
+
+static inline size_t scan_lb_status_words(uint64_t ncap) { return div_up(ncap, SCL_TILE) + 1; }
+
+template <typename Get, typename Put>
+cudaError_t device_scan_lb(Get get, Put put, const uint32_t *nptr, uint64_t ncap, uint32_t *total_out,
+                           uint32_t *status, uint32_t *tile_ctr, cudaStream_t st) {
+    if (ncap == 0) {
+        if (total_out) cudaMemsetAsync(total_out, 0, sizeof(uint32_t), st);
+        return cudaGetLastError();
+    }
+    const unsigned ntiles = div_up(ncap, SCL_TILE);
+    cudaMemsetAsync(status, 0, sizeof(uint32_t) * ntiles, st);
+    cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
+    if (total_out) cudaMemsetAsync(total_out, 0, sizeof(uint32_t), st);
+    P2P_LAUNCH((k_scan_lb<Get, Put>), ntiles, SC_THREADS, 0, st, get, put, nptr, ncap, status, tile_ctr, total_out);
+    return cudaGetLastError();
+}
+
 }  // namespace p2p
