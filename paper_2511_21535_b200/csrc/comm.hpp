@@ -31,6 +31,16 @@ struct CommBase {
     // device all-to-all-v of bytes: peer r gets send + soff[r] .. + scnt[r]; we receive rcnt[r] at recv + roff[r]
     virtual p2p_status alltoallv(const void *send, const int64_t *soff, const int64_t *scnt, void *recv,
                                  const int64_t *roff, const int64_t *rcnt, cudaStream_t st) = 0;
+    // Peer-memory result return (the a7 + a9 eval fused with the reverse all-to-all-v: the eval epilogue stores every
+    // owned target's result straight into its origin rank's receive buffer).  Collective.  begin: this rank's
+    // receive buffer holds recv_bytes; my_off[r] = where rank r's results land in it (elements); returns dst[r] =
+    // rank r's receive buffer (device address usable here) and dst_off[r] = where MY results land in it
+    // (elements), and *recv = my receive buffer.  end: after the eval kernel -- every rank's stores have landed.
+    virtual bool has_peer_results() const { return false; }
+    virtual p2p_status peer_results_begin(uint64_t, const int64_t *, char **, int64_t *, char **, cudaStream_t) {
+        return P2P_ERR_UNSUPPORTED;
+    }
+    virtual p2p_status peer_results_end(cudaStream_t) { return P2P_ERR_UNSUPPORTED; }
 };
 
 // shared state of an in-process loopback group (G emulated ranks, one per host thread)

@@ -53,6 +53,7 @@ struct IpcShared {
     int64_t counts[IPC_MAX_RANKS][IPC_MAX_RANKS];  // counts[src][dst] (alltoall_counts)
     int64_t soff[IPC_MAX_RANKS][IPC_MAX_RANKS];    // soff[src][dst]: byte offset of src's block for dst (alltoallv)
     int32_t dev[IPC_MAX_RANKS];                    // CUDA device ordinal of every rank (diagnostics)
+    int64_t res_off[IPC_MAX_RANKS][IPC_MAX_RANKS]; // res_off[dst][src]: where src's results land in dst's buffer
 };
 
 __global__ void k_sum_ranks(const unsigned long long *__restrict__ all, int nranks, size_t count,
@@ -179,6 +180,32 @@ struct IpcComm : CommBase {
         p2p_status s = gather_all(send, count, st);
         if (s != P2P_OK) return s;
         if (count) P2P_CUDA_TRY(cudaMemcpyAsync(recv, scratch, count * 8 * nranks, cudaMemcpyDeviceToDevice, st));
+        return P2P_OK;
+    }
+    bool has_peer_results() const override { return true; }
+    // the receive buffer of the fused result return is the rank's own arena: peers store into it directly
+    p2p_status peer_results_begin(uint64_t recv_bytes, const int64_t *my_off, char **dst, int64_t *dst_off,
+                                  char **recv, cudaStream_t st) override {
+        P2P_CUDA_TRY(cudaStreamSynchronize(st));  // every earlier read of the arena (stream-ordered) is done
+        barrier();                                // ... on every rank
+        p2p_status s = reserve(recv_bytes);
+        if (s != P2P_OK) return s;
+        for (int r = 0; r < nranks; ++r) sh->res_off[rank][r] = my_off[r];
+        std::atomic_thread_fence(std::memory_order_release);
+        barrier();
+        s = refresh_peers();
+        if (s != P2P_OK) return s;
+        std::atomic_thread_fence(std::memory_order_acquire);
+        for (int r = 0; r < nranks; ++r) {
+            dst[r] = peer[r];
+            dst_off[r] = sh->res_off[r][rank];
+        }
+        *recv = arena;
+        return P2P_OK;
+    }
+    p2p_status peer_results_end(cudaStream_t st) override {
+        P2P_CUDA_TRY(cudaStreamSynchronize(st));  // this rank's eval (and its stores into peers) finished
+        barrier();                                // ... on every rank: my buffer is complete
         return P2P_OK;
     }
     p2p_status alltoall_counts(const int64_t *send, int64_t *recv, cudaStream_t) override {

@@ -25,6 +25,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstdlib>
+
 #include "plan.hpp"
 #include "scan.cuh"
 
@@ -587,6 +589,40 @@ p2p_status eval_dist_t(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
     cudaStream_t st = P->stream;
     const int G = P->comm->nranks;
     const uint32_t nl = (uint32_t)P->n, ni = (uint32_t)P->n_in;
+    static const bool peer_ok = [] {
+        const char *e = getenv("P2P_PEER_RESULTS");  // 0: the pack + all-to-all-v + unpack path on any communicator
+        return !(e && e[0] == '0');
+    }();
+    if (peer_ok && P->comm->has_peer_results() && G <= PEER_MAX) {
+        // a7 + a9 fused with the reverse all-to-all-v over peer memory: the eval epilogue stores every owned target's
+        // {phi, fx, fy, fz} straight into its origin rank's receive buffer (comm_ipc.cu), laid out like res_back
+        std::vector<char *> dst(G);
+        std::vector<int64_t> dst_off(G), my_off(G);
+        for (int r = 0; r < G; ++r) my_off[r] = P->rp_soff[r];
+        char *recv = nullptr;
+        p2p_status s = P->comm->peer_results_begin((uint64_t)std::max<uint32_t>(ni, 1) * sizeof(V4), my_off.data(),
+                                                   dst.data(), dst_off.data(), &recv, st);
+        if (s != P2P_OK) return s;
+        if (nl > 0) {
+            PeerRes h{};
+            h.G = G;
+            for (int r = 0; r < G; ++r) {
+                h.lo[r] = (uint32_t)P->rp_roff[r];
+                h.dst[r] = dst[r];
+                h.off[r] = dst_off[r];
+            }
+            if (!P->peer_tab) P2P_CUDA_TRY(cudaMalloc(&P->peer_tab, sizeof(PeerRes)));
+            P2P_CUDA_TRY(cudaMemcpy(P->peer_tab, &h, sizeof(PeerRes), cudaMemcpyHostToDevice));
+            s = eval_gravity(P, layout, nullptr, nullptr, (const PeerRes *)P->peer_tab);
+            if (s != P2P_OK) return s;
+        }
+        s = P->comm->peer_results_end(st);
+        if (s != P2P_OK) return s;
+        if (ni) P2P_LAUNCH((k_unpack_results<T, V4>), grid1(ni, P->num_sms), 256, 0, st, (const V4 *)recv,
+                           P->perm_send, ni, (T *)phi, (T *)field);
+        P2P_CUDA_TRY(cudaGetLastError());
+        return P2P_OK;
+    }
     if (nl > 0) {
         // results land at the local (received) positions; halo positions are not written and never sent back
         p2p_status s = eval_gravity(P, layout, P->phi_loc, P->field_loc);
@@ -642,6 +678,8 @@ void free_distributed(p2p_plan *P) {
     for (void *b : bufs) dfree(b, P->stream);
     P->perm_send = nullptr;
     P->phi_loc = P->field_loc = P->res_own = P->res_back = nullptr;
+    if (P->peer_tab) cudaFree(P->peer_tab);
+    P->peer_tab = nullptr;
 }
 
 }  // namespace p2p

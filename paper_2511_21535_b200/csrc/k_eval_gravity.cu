@@ -82,7 +82,31 @@ struct EvalArgs {
     T *field;
     uint32_t zero;             // always 0 (see queue_claim)
     const uint8_t *lframe;     // ADAPT: per leaf, bit d = touches the upper face of periodic dim d, bit 3 + d the lower
+    const PeerRes *pr;         // multi-GPU over peer memory: results stored straight into the origin ranks' buffers
 };
+
+// a9: one result value (q = 0 potential, 1..3 field component) of local target slot i -- into the caller's arrays,
+// or (multi-GPU, peer memory) into its origin rank's receive buffer: rank r = the run holding i (runs are rank-major,
+// lo[] ascending), element (off[r] + i - lo[r]) of {phi, fx, fy, fz} records -- the reverse all-to-all-v of the
+// results fused into the eval's epilogue
+template <typename T>
+__device__ __forceinline__ void put_result(const EvalArgs<T> &a, uint32_t i, int q, T v) {
+    if (a.pr) {
+        const PeerRes *pr = a.pr;
+        int lo = 0, hi = pr->G - 1;  // the largest r with lo[r] <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pr->lo[mid] <= i) lo = mid;
+            else hi = mid - 1;
+        }
+        T *d = reinterpret_cast<T *>(pr->dst[lo]) + (size_t)(pr->off[lo] + (int64_t)(i - pr->lo[lo])) * 4 + q;
+        *d = v;
+    } else if (q == 0) {
+        a.phi[i] = v;
+    } else if (a.field) {
+        a.field[3 * (size_t)i + (q - 1)] = v;
+    }
+}
 
 // image shift of stencil slot seen from box c (DESIGN C5)
 __device__ __forceinline__ double slot_shift(const Geom &g, const uint32_t c[3], int slot, int d) {
@@ -434,12 +458,10 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
             T pot, fx, fy, fz;
             tg.get(k, pot, fx, fy, fz);
             const uint32_t idx = a.perm[p + k];
-            a.phi[idx] = -(pot - tm[k] * rs);
-            if (a.field) {
-                a.field[3 * (size_t)idx + 0] = fx;
-                a.field[3 * (size_t)idx + 1] = fy;
-                a.field[3 * (size_t)idx + 2] = fz;
-            }
+            put_result(a, idx, 0, -(pot - tm[k] * rs));
+            put_result(a, idx, 1, fx);
+            put_result(a, idx, 2, fy);
+            put_result(a, idx, 3, fz);
         }
         }
     }
@@ -876,12 +898,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                 const uint32_t f = f0 + j, q = f >> LOGK, k = f & (K - 1u), ti = g * K + k;
                 const uint32_t i = __shfl_sync(FULL, my_slot, ti & 31u);
                 const T mk = __shfl_sync(FULL, my_m, ti & 31u);
-                if ((uint32_t)j < vcnt && own && ((vmask >> ti) & 1u)) {
-                    if (q == 0)
-                        a.phi[i] = -(v[j] - mk * rs);
-                    else if (a.field)
-                        a.field[3 * (size_t)i + (q - 1)] = v[j];
-                }
+                if ((uint32_t)j < vcnt && own && ((vmask >> ti) & 1u))
+                    put_result(a, i, (int)q, q == 0 ? -(v[j] - mk * rs) : v[j]);
             }
         } else {
         tg.reduce(S, sl);
@@ -895,12 +913,10 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                 if (active && sl == 0 && ((vmask >> ti) & 1u)) {
                     T pot, fx, fy, fz;
                     tg.get(k, pot, fx, fy, fz);
-                    a.phi[i] = -(pot - mk * rs);
-                    if (a.field) {
-                        a.field[3 * (size_t)i + 0] = fx;
-                        a.field[3 * (size_t)i + 1] = fy;
-                        a.field[3 * (size_t)i + 2] = fz;
-                    }
+                    put_result(a, i, 0, -(pot - mk * rs));
+                    put_result(a, i, 1, fx);
+                    put_result(a, i, 2, fy);
+                    put_result(a, i, 3, fz);
                 }
             }
         }
@@ -913,7 +929,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
 }
 
 template <typename T, int LAYOUT, int K, bool ADAPT = false>
-p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems *ov = nullptr) {
+p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems *ov = nullptr,
+                  const PeerRes *pr = nullptr) {
     using V4 = typename V4T<T>::type;
     auto kern = k_eval_gravity<T, LAYOUT, K, ADAPT>;
     const int smem = EV_WARPS * 2 * (EV_STAGE_BYTES + EV_TGT * (int)sizeof(V4));
@@ -951,6 +968,7 @@ p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems
     a.field = (T *)field;
     a.zero = 0u;
     a.lframe = nullptr;
+    a.pr = pr;
     if (ov) {  // an explicit item list over an explicit redundant buffer / CSR (adaptive leaves), no small-box path
         a.red = (const V4 *)ov->red;
         a.items = ov->items;
@@ -984,19 +1002,19 @@ p2p_status eval_gravity_items(p2p_plan *P, const EvalItems &it, void *phi, void 
     return launch<float, P2P_REDUNDANT, EVAL_K_F32>(P, phi, field, 3, &it);
 }
 
-p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
+p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field, const PeerRes *pr) {
     if (P->sizes_known && P->n == 0) return P2P_OK;
     const bool f64 = P->cfg.precision == P2P_FP64;
     switch (layout) {
     case P2P_REDUNDANT:
-        return f64 ? launch<double, P2P_REDUNDANT, EVAL_K_F64>(P, phi, field, 0)
-                   : launch<float, P2P_REDUNDANT, EVAL_K_F32>(P, phi, field, 0);
+        return f64 ? launch<double, P2P_REDUNDANT, EVAL_K_F64>(P, phi, field, 0, nullptr, pr)
+                   : launch<float, P2P_REDUNDANT, EVAL_K_F32>(P, phi, field, 0, nullptr, pr);
     case P2P_INDEXED:
-        return f64 ? launch<double, P2P_INDEXED, EVAL_K_F64>(P, phi, field, 1)
-                   : launch<float, P2P_INDEXED, EVAL_K_F32>(P, phi, field, 1);
+        return f64 ? launch<double, P2P_INDEXED, EVAL_K_F64>(P, phi, field, 1, nullptr, pr)
+                   : launch<float, P2P_INDEXED, EVAL_K_F32>(P, phi, field, 1, nullptr, pr);
     case P2P_INDEXED_BITWISE:
-        return f64 ? launch<double, P2P_INDEXED_BITWISE, EVAL_K_F64>(P, phi, field, 2)
-                   : launch<float, P2P_INDEXED_BITWISE, EVAL_K_F32>(P, phi, field, 2);
+        return f64 ? launch<double, P2P_INDEXED_BITWISE, EVAL_K_F64>(P, phi, field, 2, nullptr, pr)
+                   : launch<float, P2P_INDEXED_BITWISE, EVAL_K_F32>(P, phi, field, 2, nullptr, pr);
     }
     return P2P_ERR_INVALID_ARGUMENT;
 }

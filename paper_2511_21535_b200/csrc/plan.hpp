@@ -156,6 +156,7 @@ struct p2p_plan {
     std::vector<int64_t> rp_scnt, rp_soff, rp_rcnt, rp_roff;  // repartition counts / offsets (elements)
     std::vector<uint32_t> splitters;        // G + 1 key boundaries of the rank ranges
     void *phi_loc = nullptr, *field_loc = nullptr, *res_own = nullptr, *res_back = nullptr;
+    void *peer_tab = nullptr;  // device PeerRes of the fused peer-memory result return (cudaMalloc)
     bool red_valid = false;
     p2p::AdaptState *ad = nullptr;  // adaptive-leaf mode (p2p_adaptive_enable)
     bool grid_stale = false;        // grid a5 not built (after adaptive-mode updates) until the next p2p_plan_update
@@ -194,7 +195,6 @@ bool origins_exact_fp32(const Geom &g);  // every box origin fma(c, h, lo_d) is 
 p2p_status restructure_helmholtz(p2p_plan *P);
 
 // k_eval_gravity.cu / k_helmholtz.cu
-p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field);
 // the REDUNDANT eval over an explicit item list and redundant buffer (adaptive leaves, k_adaptive.cu)
 struct EvalItems {
     const Item *items;
@@ -208,6 +208,16 @@ struct EvalItems {
     const uint8_t *csr_code = nullptr, *lframe = nullptr;
 };
 p2p_status eval_gravity_items(p2p_plan *P, const EvalItems &it, void *phi, void *field);
+// multi-GPU over peer memory (comm_ipc.cu): the eval stores each owned target's {phi, fx, fy, fz} into its origin
+// rank's receive buffer (device table, k_dist.cu)
+constexpr int PEER_MAX = 64;
+struct PeerRes {
+    int G;
+    uint32_t lo[PEER_MAX];   // first local slot of the run received from rank r (owned head first)
+    char *dst[PEER_MAX];     // rank r's receive buffer
+    int64_t off[PEER_MAX];   // where this rank's results land in it (records)
+};
+p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field, const PeerRes *pr = nullptr);
 
 // k_dist.cu: the distributed (multi-GPU) plan build and result return
 p2p_status build_distributed(p2p_plan *P, const void *pos, const void *q);
