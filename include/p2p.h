@@ -193,14 +193,16 @@ p2p_status p2p_adaptive_eval(p2p_plan *plan, int32_t t, int32_t min_bits, p2p_la
 
 /* SURVEY NEXT-1 on the per-step path: ADAPTIVE-LEAF MODE of a gravity plan.  After
  * p2p_adaptive_enable(plan, t, min_bits) the plan's steps run over the adaptive leaves (C22-C24) instead of the grid
- * boxes: p2p_plan_update = a1-a4 + the leaves + their closed neighbour CSR; p2p_restructure = the leaves' redundant
- * runs + work items; p2p_eval(P2P_REDUNDANT | P2P_INDEXED) = the eval over them (other layouts: UNSUPPORTED).  All
+ * boxes: p2p_plan_update = a1-a4 + the leaves + their closed neighbour CSR + run lengths, work items and chunk heads
+ * (what both layouts need, like the grid's a5); p2p_restructure = the leaves' redundant runs;
+ * p2p_eval(P2P_REDUNDANT | P2P_INDEXED) = the eval over them (other layouts: UNSUPPORTED; P2P_REDUNDANT needs the
+ * restructure of the current update, P2P_INDEXED only the update).  All
  * of it is ASYNCHRONOUS with every count on the device (no host sync, no allocation per step): enable measures the
  * current input once (synchronous, like p2p_plan_create) and sizes the buffers with headroom (neighbour entries and
  * redundant records 2x the measured, leaves <= boxes).  An update exceeding them sets a device flag: its
  * restructure / eval do nothing and p2p_get_info reports P2P_ERR_OUT_OF_MEMORY (call p2p_adaptive_enable again).
- * p2p_get_info in adaptive mode describes the leaves (n_boxes = leaves, n_nbr = entries, n_red / n_pairs after
- * p2p_restructure).  Same preconditions as p2p_adaptive_neighbours (single-GPU periodic cube of 2^m >= 8 boxes).
+ * p2p_get_info in adaptive mode describes the leaves (n_boxes = leaves, n_nbr = entries, n_red = records,
+ * n_pairs, n_items).  Same preconditions as p2p_adaptive_neighbours (single-GPU periodic cube of 2^m >= 8 boxes).
  * p2p_adaptive_disable returns to grid mode (the next restructure / eval needs a p2p_plan_update first). */
 p2p_status p2p_adaptive_enable(p2p_plan *plan, int32_t t, int32_t min_bits);
 p2p_status p2p_adaptive_disable(p2p_plan *plan);

@@ -436,8 +436,6 @@ class Plan:
 
     def restructure(self):
         p2p_restructure(self.handle)
-        if getattr(self, "adaptive", None):
-            self._info = None  # adaptive mode: records / pairs are counted by the restructure
 
     def enable_adaptive(self, t: int, min_bits: int = 9):
         """SURVEY NEXT-1 on the per-step path: run update / restructure / eval over adaptive leaves with threshold t

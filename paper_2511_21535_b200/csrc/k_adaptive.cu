@@ -11,7 +11,9 @@
 // a head-flag scan (scan.cuh) numbers them in Morton order.  Every leaf is one contiguous run of the sorted records.
 #include <vector>
 
+#include "items.cuh"
 #include "plan.hpp"
+#include "restructure.cuh"
 #include "scan.cuh"
 
 namespace p2p {
@@ -236,9 +238,9 @@ __global__ void k_dil_merge(const uint32_t *__restrict__ off, const unsigned int
 // ---- C24: per target leaf, its run length, the offset of its own (self, image 0) segment, its work items ----
 __global__ void k_adapt_count(const uint32_t *__restrict__ off, const uint32_t *__restrict__ nbr,
                               const uint8_t *__restrict__ code, const uint32_t *__restrict__ lstart, uint32_t L,
-                              unsigned long long *__restrict__ R, uint32_t *__restrict__ tself,
-                              uint32_t *__restrict__ nitems, DevN dn = DevN(),
-                              unsigned long long *__restrict__ pairs = nullptr) {
+                              unsigned long long *__restrict__ R, uint32_t *__restrict__ tself, DevN dn,
+                              unsigned long long *__restrict__ pairs, uint32_t *__restrict__ ch_leaf = nullptr,
+                              unsigned long long *__restrict__ ch_rel = nullptr) {
     if (dn.stop()) return;
     L = dn.l(L);
     unsigned long long ip = 0;
@@ -246,100 +248,219 @@ __global__ void k_adapt_count(const uint32_t *__restrict__ off, const uint32_t *
         unsigned long long sum = 0, ts = 0;
         for (uint32_t e = off[a]; e < off[a + 1]; ++e) {
             const uint32_t b = nbr[e];
+            if ((e & 31u) == 0u) {  // head of restructure chunk e / 32: its owner leaf and offset inside the run
+                ch_leaf[e >> 5] = a;
+                ch_rel[e >> 5] = sum;
+            }
             if (b == a && code[e] == 13) ts = sum;
             sum += lstart[b + 1] - lstart[b];
         }
         R[a] = sum;
         tself[a] = (uint32_t)ts;
-        nitems[a] = (lstart[a + 1] - lstart[a] + ITEM_TMAX - 1) / ITEM_TMAX;
         ip += sum * (lstart[a + 1] - lstart[a]);
     }
-    if (pairs) {  // I = sum over leaves of n_targets x run length (the pair count of the step)
+    {  // I = sum over leaves of n_targets x run length (the pair count of the step; it sizes the work items)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ip += __shfl_xor_sync(0xffffffffu, ip, o);
         if ((threadIdx.x & 31u) == 0 && ip) atomicAdd(pairs, ip);
     }
 }
 
+// Multi-leaf quad items of the REDUNDANT eval (fp32): the grid path's multi-box quads (k_structs.cu mb_role) over
+// leaves.  The 4 leaves of an aligned leaf-index block 4q .. 4q + 3 that each hold 1 .. 8 targets and <= 65535 run
+// records become ONE work item: leaf j owns lanes 8j .. 8j + 7 (2 groups of 4 targets x 4 source splits) and the 4
+// runs -- adjacent in red[], like their targets in the sorted records -- are staged in lockstep, so the per-item
+// cost (fetch, staging, transpose-reduce, epilogue) is paid once per 4 small leaves.  Leaves are Morton-ordered: a
+// block is 4 neighbouring cells; adaptive mode is single-GPU, no rank boundary constrains the blocks.
+constexpr uint32_t AQ_NT = 8, AQ_R = 65535;
+// the leaf's work items: ITEM_TMAX targets each, fewer when n_t x R exceeds the work-scaled cost cap (items.cuh,
+// the grid path's rule with the exact pair count I)
+__device__ __forceinline__ uint32_t adapt_nitems(uint32_t nt, uint64_t R, uint32_t K, uint64_t cap) {
+    const uint32_t sz = item_size(nt, R, ITEM_TMAX, K, cap);
+    return (nt + sz - 1) / sz;
+}
+// a quad member: one item, <= 8 targets, a 16-bit run, and cost <= cap / 4 (a quad item -- 8 lanes per leaf -- then
+// takes no longer than a capped single-leaf item: k_structs.cu mb_eligible)
+__device__ __forceinline__ bool aq_elig(const uint32_t *__restrict__ lstart, const unsigned long long *__restrict__ R,
+                                        uint32_t a, uint32_t K, uint64_t cap) {
+    const uint32_t nt = lstart[a + 1] - lstart[a];
+    const uint64_t r = R[a];
+    return nt >= 1u && nt <= AQ_NT && r <= AQ_R && (uint64_t)nt * r * 4 <= cap && adapt_nitems(nt, r, K, cap) == 1u;
+}
+// 0: no quad, 1: leader (a % 4 == 0), 2: member
+__device__ __forceinline__ int aq_role(const uint32_t *__restrict__ lstart, const unsigned long long *__restrict__ R,
+                                       uint32_t a, uint32_t L, uint32_t K, uint64_t cap) {
+    const uint32_t q = a & ~3u;
+    if (q + 3u >= L) return 0;
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i)
+        if (!aq_elig(lstart, R, q + i, K, cap)) return 0;
+    return a == q ? 1 : 2;
+}
+// the cost cap from the device pair count; I == nullptr: uncapped (ITEM_TMAX-target items)
+__device__ __forceinline__ uint64_t adapt_cap(const unsigned long long *I) { return I ? item_costcap_of(*I) : ~0ull; }
+// per leaf: its work items (INDEXED list) / its items in the REDUNDANT list (quad leader 1, member 0, else its own);
+// L and the pair count I from the device
+struct ItemCntGet {
+    const uint32_t *lstart;
+    const unsigned long long *R, *I;
+    uint32_t K;
+    __device__ uint32_t operator()(uint64_t p) const {
+        const uint32_t a = (uint32_t)p;
+        return adapt_nitems(lstart[a + 1] - lstart[a], R[a], K, adapt_cap(I));
+    }
+};
+struct RedCntGet {
+    const uint32_t *lstart;
+    const unsigned long long *R, *I;
+    const uint32_t *Lp;
+    uint32_t Lh, K;
+    bool quads;
+    __device__ uint32_t operator()(uint64_t p) const {
+        const uint32_t a = (uint32_t)p;
+        const uint64_t cap = adapt_cap(I);
+        const int role = quads ? aq_role(lstart, R, a, Lp ? *Lp : Lh, K, cap) : 0;
+        return role == 0 ? adapt_nitems(lstart[a + 1] - lstart[a], R[a], K, cap) : (role == 1 ? 1u : 0u);
+    }
+};
+
 // eval work items of every leaf: full ITEM_TMAX-target items + a remainder (the eval's lane layout, K targets per
-// lane: G = ceil(n_t / K) groups x S = floor(32 / G) source splits); targets staged from the self segment
+// lane: G = ceil(n_t / K) groups x S = floor(32 / G) source splits); targets staged from the self segment.
+// items_red (optional): the REDUNDANT list at ioff_red -- a quad leader's multi-leaf item (packed like the grid's:
+// k_structs.cu k_nbr_fill), nothing for a member, the leaf's own items otherwise
 __global__ void k_adapt_items(const uint32_t *__restrict__ lstart, const unsigned long long *__restrict__ red_off,
                               const unsigned long long *__restrict__ R, const uint32_t *__restrict__ tself,
-                              const uint32_t *__restrict__ item_off, uint32_t L, uint32_t K, Item *__restrict__ items,
-                              DevN dn = DevN()) {
+                              const uint32_t *__restrict__ item_off, uint32_t L, uint32_t K,
+                              const unsigned long long *__restrict__ I_idx, Item *__restrict__ items, DevN dn = DevN(),
+                              Item *__restrict__ items_red = nullptr, const uint32_t *__restrict__ ioff_red = nullptr,
+                              const unsigned long long *__restrict__ I_red = nullptr, bool quads = false) {
     if (dn.stop()) return;
     L = dn.l(L);
+    const uint64_t cap_i = adapt_cap(I_idx), cap_r = adapt_cap(I_red);
     for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
         const uint32_t nt_all = lstart[a + 1] - lstart[a];
-        uint32_t it = item_off[a];
-        for (uint32_t a0 = 0; a0 < nt_all; a0 += ITEM_TMAX, ++it) {
-            const uint32_t nt = min(ITEM_TMAX, nt_all - a0), G = (nt + K - 1) / K, S = 32u / G;
-            items[it] = Item{a, lstart[a] + a0, nt | (S << 8) | (G << 16), 0u, red_off[a], (uint32_t)R[a],
-                             tself[a] + a0};
+        for (int list = 0; list < (items_red ? 2 : 1); ++list) {
+            const uint64_t cap = list ? cap_r : cap_i;
+            if (list && quads && aq_role(lstart, R, a, L, K, cap) != 0) continue;  // written by the quad's leader
+            const uint32_t sz = item_size(nt_all, R[a], ITEM_TMAX, K, cap);
+            uint32_t it = list ? ioff_red[a] : item_off[a];
+            for (uint32_t a0 = 0; a0 < nt_all; a0 += sz, ++it) {
+                const uint32_t nt = min(sz, nt_all - a0), G = (nt + K - 1) / K, S = 32u / G;
+                (list ? items_red : items)[it] = Item{a, lstart[a] + a0, nt | (S << 8) | (G << 16), 0u, red_off[a],
+                                                      (uint32_t)R[a], tself[a] + a0};
+            }
+        }
+        const int role = (items_red && quads) ? aq_role(lstart, R, a, L, K, cap_r) : 0;
+        if (role == 1) {
+            uint32_t q_nt[4], q_R[4], q_tofs[4];
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                q_nt[j] = lstart[a + j + 1] - lstart[a + j];
+                q_R[j] = (uint32_t)R[a + j];
+                q_tofs[j] = tself[a + j];
+            }
+            Item mi;
+            mi.box = 0x80000000u | q_nt[0] | (q_nt[1] << 4) | (q_nt[2] << 8) | (q_nt[3] << 12);
+            mi.t0 = lstart[a];
+            mi.meta = q_R[0] | (q_R[1] << 16);
+            mi.key = q_R[2] | (q_R[3] << 16);
+            mi.red_base = red_off[a];
+            mi.R = q_tofs[0] | (q_tofs[1] << 16);
+            mi.tofs = q_tofs[2] | (q_tofs[3] << 16);
+            items_red[ioff_red[a]] = mi;
         }
     }
 }
 
+// Item sizes per layout, each its measured best (profiles/r02_adaptive_items.txt, c3): the REDUNDANT list is
+// cost-capped like the grid's (items.cuh: the dynamic queue's tail; t = 4 / 16 / 64: -5% / -7% / -1.5% eval), the
+// INDEXED list is not (its per-item CSR setup makes smaller items cost more: +6% / +7% / 0).  P2P_ADAPT_CAP=0:
+// REDUNDANT uncapped too.
+static bool adapt_capped() {
+    const char *e = getenv("P2P_ADAPT_CAP");
+    return !(e && e[0] == '0');
+}
+// multi-leaf quads: OPT-IN (P2P_ADAPT_QUADS=1), fp32 only.  Measured on c3 (profiles/r02_adaptive_items.txt): on
+// the adaptive leaves they do not pay -- t = 4: +7% REDUNDANT eval (most quad leaves hold <= 4 targets, so half of
+// every leaf's 8 lanes idle), t = 16 / 64: within noise -- unlike the grid's 8-per-box c4-8
+static bool adapt_quads(const p2p_plan *P) {
+    const char *e = getenv("P2P_ADAPT_QUADS");
+    return P->cfg.precision != P2P_FP64 && e && e[0] == '1';
+}
+
 // the redundant runs (C24): each target leaf's entries' source runs in CSR order, rebased in fp64 to the target
-// leaf's origin o_d = fma(c_d, w_d, lo_d) (w_d = L / 2^s_d) with the entry's image shift, one final rounding.
-// Warp per CHUNK of 32 consecutive CSR entries (the grid restructure's scheme, k_restructure.cu):
-// a chunk's segments are one contiguous output range starting at eoff[32 c] (eoff = exclusive scan of the entries'
-// source counts), its <= 32 entries belong to <= 32 consecutive leaves (every leaf lists itself); lanes copy windows
-// of 32 records, each lane finding its segment by ballot / OR-reduce over the segment starts (full lanes however
-// small the leaves are; a warp per leaf idled most lanes on small leaves: 0.60 -> 0.26 ms at t = 4)
-template <typename T, typename V4>
+// leaf's origin o_d = fma(c_d, w_d, lo_d) (w_d = L / 2^s_d) with the entry's image shift, one final rounding:
+//     red = { fl_p(((double)x_j + S_d) - o_d), .., m_j },  S_d = (image digit d - 1) L   (C24, P:L197 + C11)
+// Warp per CHUNK of 32 consecutive CSR entries (the grid restructure's scheme, restructure.cuh): a chunk's segments
+// are one contiguous output range starting at roff[owner of its first entry] + ch_rel (both recorded by
+// k_adapt_count: no entry-offset scan, no owner search), its <= 32 entries belong to <= 32 consecutive leaves (every
+// leaf lists itself).  The chunk's level-1 values are loaded one chunk ahead; lanes copy windows of 32 records,
+// UNR windows with all loads in flight before the first store, each lane finding its segment by ballot / OR-reduce
+// over the segment starts; streaming stores (the runs are read back by the next kernel only).
+// EXACT32 (host-checked: every cell origin of the 2^m lattice is an fp32 value, so every leaf origin -- a lattice
+// cell origin -- is too): chunks without an image shift take the fp32 subtraction, which rounds like the fp64
+// sequence (restructure.cuh).
+template <typename T, typename V4, bool EXACT32>
 __global__ void __launch_bounds__(256) k_adapt_restructure_chunks(
     const V4 *__restrict__ rec, const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ len,
     const uint32_t *__restrict__ lstart, const uint32_t *__restrict__ off, const uint32_t *__restrict__ nbr,
-    const uint8_t *__restrict__ code, const unsigned long long *__restrict__ eoff, uint32_t L, uint32_t E, int m,
-    double Lbox, double lo0, double lo1, double lo2, V4 *__restrict__ red, DevN dn = DevN()) {
+    const uint8_t *__restrict__ code, const uint32_t *__restrict__ ch_leaf,
+    const unsigned long long *__restrict__ ch_rel, const unsigned long long *__restrict__ roff, uint32_t L, uint32_t E,
+    int m, double Lbox, double lo0, double lo1, double lo2, V4 *__restrict__ red, DevN dn = DevN()) {
     if (dn.stop()) return;
     L = dn.l(L);
     E = dn.e(E);
     constexpr unsigned FULL = 0xffffffffu;
+    constexpr int UNR = 4;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5, nchunk = (E + 31u) >> 5;
-    for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunk; ch += nw) {
-        const uint32_t e0 = ch << 5, e = e0 + lane;
+    uint32_t n_o0 = 0, n_b = 0, n_cd = 13;
+    unsigned long long n_rel = 0;
+    auto load1 = [&](uint32_t c) {
+        if (c < nchunk) {
+            n_o0 = ch_leaf[c];
+            n_rel = ch_rel[c];
+            const uint32_t ee = (c << 5) + lane;
+            if (ee < E) {
+                n_b = nbr[ee];
+                n_cd = code[ee];
+            }
+        }
+    };
+    uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    load1(ch);
+    for (; ch < nchunk; ch += nw) {
+        const uint32_t o0 = n_o0, b = n_b, cd = n_cd;
+        const unsigned long long rel = n_rel;
+        load1(ch + nw);
+        const uint32_t e = (ch << 5) + lane;
         const bool seg = e < E;
-        uint32_t src = 0, cnt = 0, cd = 13;
+        uint32_t src = 0, cnt = 0;
         if (seg) {
-            const uint32_t b = nbr[e];
             src = lstart[b];
             cnt = lstart[b + 1] - src;
-            cd = code[e];
         }
-        // owner leaves: o0 = the leaf whose row holds e0; entry e belongs to the largest o0 + i with off <= e
-        uint32_t o0 = 0;
-        if (lane == 0) {
-            uint32_t lo = 0, hi = L + 1;  // upper_bound(off, e0) - 1
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (off[mid] <= e0) lo = mid + 1;
-                else hi = mid;
-            }
-            o0 = lo - 1;
-        }
-        o0 = __shfl_sync(FULL, o0, 0);
         const uint32_t ol = o0 + lane;
-        uint32_t boff = 0xffffffffu;
-        double org0 = 0.0, org1 = 0.0, org2 = 0.0;
+        uint32_t boff = FULL, keyl = 0, lenl = 0;
         if (ol < L) {
             boff = off[ol];
-            uint32_t sh[3];
-            halvings_of((int)len[ol], sh);
-            const uint32_t k0 = lkey[ol];
-            org0 = __fma_rn((double)(compact3(k0) >> (m - sh[0])), ldexp(Lbox, -(int)sh[0]), lo0);
-            org1 = __fma_rn((double)(compact3(k0 >> 1) >> (m - sh[1])), ldexp(Lbox, -(int)sh[1]), lo1);
-            org2 = __fma_rn((double)(compact3(k0 >> 2) >> (m - sh[2])), ldexp(Lbox, -(int)sh[2]), lo2);
+            keyl = lkey[ol];
+            lenl = len[ol];
         }
+        V4 *__restrict__ out = red + (roff[o0] + rel);
+        // owner of entry e: the largest i with off[o0 + i] <= e
         uint32_t i = 0;
 #pragma unroll
         for (uint32_t step = 16; step > 0; step >>= 1) {
             const uint32_t t = __shfl_sync(FULL, boff, i + step);
             if (t <= e) i += step;
         }
-        const double o0d = __shfl_sync(FULL, org0, i), o1d = __shfl_sync(FULL, org1, i), o2d = __shfl_sync(FULL, org2, i);
+        const uint32_t k0 = __shfl_sync(FULL, keyl, i), ln = __shfl_sync(FULL, lenl, i);
+        uint32_t sh[3];
+        halvings_of((int)ln, sh);
+        const double o0d = __fma_rn((double)(compact3(k0) >> (m - sh[0])), ldexp(Lbox, -(int)sh[0]), lo0);
+        const double o1d = __fma_rn((double)(compact3(k0 >> 1) >> (m - sh[1])), ldexp(Lbox, -(int)sh[1]), lo1);
+        const double o2d = __fma_rn((double)(compact3(k0 >> 2) >> (m - sh[2])), ldexp(Lbox, -(int)sh[2]), lo2);
         uint32_t incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -347,42 +468,69 @@ __global__ void __launch_bounds__(256) k_adapt_restructure_chunks(
             if (lane >= (unsigned)o) incl += y;
         }
         const uint32_t st = incl - cnt, Rc = __shfl_sync(FULL, incl, 31);
-        V4 *__restrict__ out = red + eoff[e0];
         const uint32_t le = lane == 31 ? FULL : ((2u << lane) - 1u);
-        for (uint32_t r0 = 0; r0 < Rc; r0 += 32) {
-            // segment of record r0 + lane (leaves are non-empty, so every entry's segment is): segments starting
-            // before r0 - 1 + segment starts in [r0, r0 + lane]
-            const uint32_t before = __popc(__ballot_sync(FULL, seg && st < r0));
-            const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
-            const uint32_t starts = __reduce_or_sync(FULL, in_win);
-            const uint32_t src_lane = (before - 1u + __popc(starts & le)) & 31u;
-            const uint32_t e_src = __shfl_sync(FULL, src, src_lane), e_st = __shfl_sync(FULL, st, src_lane);
-            const uint32_t e_cd = __shfl_sync(FULL, cd, src_lane);
-            const double eo0 = __shfl_sync(FULL, o0d, src_lane), eo1 = __shfl_sync(FULL, o1d, src_lane),
-                         eo2 = __shfl_sync(FULL, o2d, src_lane);
-            const uint32_t r = r0 + lane;
-            if (r < Rc) {
-                const V4 x = rec[e_src + (r - e_st)];
-                const double S0 = (double)((int)(e_cd % 3) - 1) * Lbox, S1 = (double)((int)((e_cd / 3) % 3) - 1) * Lbox,
-                             S2 = (double)((int)(e_cd / 9) - 1) * Lbox;
-                V4 v;
-                v.x = (T)__dsub_rn(__dadd_rn((double)x.x, S0), eo0);
-                v.y = (T)__dsub_rn(__dadd_rn((double)x.y, S1), eo1);
-                v.z = (T)__dsub_rn(__dadd_rn((double)x.z, S2), eo2);
-                v.w = x.w;
-                out[r] = v;
+        const bool wrap = __any_sync(FULL, seg && cd != 13u);
+        const bool fast32 = EXACT32 && !wrap;
+        const float f0o = (float)o0d, f1o = (float)o1d, f2o = (float)o2d;
+        for (uint32_t rb = 0; rb < Rc; rb += 32 * UNR) {
+            V4 x[UNR];
+            uint32_t xe[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t r0 = rb + 32u * u;
+                if (r0 >= Rc) break;  // warp-uniform
+                // segment of record r0 + lane: segments starting before r0 - 1 + segment starts in [r0, r0 + lane]
+                const uint32_t before = __popc(__ballot_sync(FULL, seg && st < r0));
+                const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
+                const uint32_t starts = __reduce_or_sync(FULL, in_win);
+                xe[u] = (before - 1u + __popc(starts & le)) & 31u;
+                const uint32_t e_src = __shfl_sync(FULL, src, xe[u]), e_st = __shfl_sync(FULL, st, xe[u]);
+                const uint32_t r = r0 + lane;
+                if (r < Rc) x[u] = rec[e_src + (r - e_st)];
+            }
+            if (fast32) {
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const uint32_t r0 = rb + 32u * u;
+                    if (r0 >= Rc) break;
+                    const float eo0 = __shfl_sync(FULL, f0o, xe[u]), eo1 = __shfl_sync(FULL, f1o, xe[u]),
+                                eo2 = __shfl_sync(FULL, f2o, xe[u]);
+                    const uint32_t r = r0 + lane;
+                    if (r < Rc) {
+                        V4 v;
+                        v.x = (T)__fsub_rn(__fadd_rn((float)x[u].x, 0.0f), eo0);
+                        v.y = (T)__fsub_rn(__fadd_rn((float)x[u].y, 0.0f), eo1);
+                        v.z = (T)__fsub_rn(__fadd_rn((float)x[u].z, 0.0f), eo2);
+                        v.w = x[u].w;
+                        rs::st_cs(out + r, v);
+                    }
+                }
+                continue;
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t r0 = rb + 32u * u;
+                if (r0 >= Rc) break;
+                const uint32_t e_cd = __shfl_sync(FULL, cd, xe[u]);
+                const double eo0 = __shfl_sync(FULL, o0d, xe[u]), eo1 = __shfl_sync(FULL, o1d, xe[u]),
+                             eo2 = __shfl_sync(FULL, o2d, xe[u]);
+                const uint32_t r = r0 + lane;
+                if (r < Rc) {
+                    const double S0 = (double)((int)(e_cd % 3) - 1) * Lbox,
+                                 S1 = (double)((int)((e_cd / 3) % 3) - 1) * Lbox,
+                                 S2 = (double)((int)(e_cd / 9) - 1) * Lbox;
+                    V4 v;
+                    v.x = (T)__dsub_rn(__dadd_rn((double)x[u].x, S0), eo0);
+                    v.y = (T)__dsub_rn(__dadd_rn((double)x[u].y, S1), eo1);
+                    v.z = (T)__dsub_rn(__dadd_rn((double)x[u].z, S2), eo2);
+                    v.w = x[u].w;
+                    rs::st_cs(out + r, v);
+                }
             }
         }
     }
 }
 
-struct EntryCntGet {
-    const uint32_t *nbr, *lstart;
-    __device__ unsigned long long operator()(uint64_t e) const {
-        const uint32_t b = nbr[e];
-        return lstart[b + 1] - lstart[b];
-    }
-};
 
 // INDEXED over the leaves: per leaf, bit d = its cell touches the upper face of dim d (frame -L), bit 3 + d the lower
 __global__ void k_leaf_frame(const uint32_t *__restrict__ lkey, const uint32_t *__restrict__ len, uint32_t L, int m,
@@ -402,6 +550,46 @@ __global__ void k_leaf_frame(const uint32_t *__restrict__ lkey, const uint32_t *
         }
         fr[a] = (uint8_t)f;
     }
+}
+
+// every cell origin fma(c, L 2^-m, lo_d), c < 2^m, of the leaves' lattice is an fp32 value -- then so is every
+// leaf origin fma(c_l, L 2^-s, lo_d): the same real number as the origin of the leaf's first cell, one rounding
+static bool adapt_origins_exact_fp32(const Geom &G, int m) {
+    const double w = std::ldexp(G.L[0], -m);
+    for (int d = 0; d < 3; ++d)
+        for (int c = 0; c < (1 << m); ++c) {
+            const double o = std::fma((double)c, w, G.lo[d]);
+            if ((double)(float)o != o) return false;
+        }
+    return true;
+}
+
+// a6 over the leaves: the chunk kernel in the plan's precision (EXACT32 when the lattice allows it)
+static p2p_status launch_adapt_runs(p2p_plan *P, const uint32_t *lkey, const uint32_t *len, const uint32_t *lstart,
+                                    const uint32_t *off, const uint32_t *nbr, const uint8_t *code,
+                                    const uint32_t *ch_leaf, const unsigned long long *ch_rel,
+                                    const unsigned long long *roff, uint32_t L, uint32_t E, uint64_t egrid, void *red,
+                                    DevN dn) {
+    const int m = P->key_bits / 3;
+    const Geom &G = P->geom;
+    cudaStream_t st = P->stream;
+    unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up(egrid, 256), (unsigned)P->num_sms * 16));
+    // P2P_RS_MAXGRID=<blocks> (tests): fewer warps than chunks, so that every warp walks several chunks
+    if (const char *e = getenv("P2P_RS_MAXGRID")) gw = std::max(1u, std::min(gw, (unsigned)atoi(e)));
+    if (P->cfg.precision == P2P_FP64)
+        P2P_LAUNCH((k_adapt_restructure_chunks<double, double4, false>), gw, 256, 0, st, (const double4 *)P->rec, lkey,
+                   len, lstart, off, nbr, code, ch_leaf, ch_rel, roff, L, E, m, G.L[0], G.lo[0], G.lo[1], G.lo[2],
+                   (double4 *)red, dn);
+    else if (adapt_origins_exact_fp32(G, m))
+        P2P_LAUNCH((k_adapt_restructure_chunks<float, float4, true>), gw, 256, 0, st, (const float4 *)P->rec, lkey,
+                   len, lstart, off, nbr, code, ch_leaf, ch_rel, roff, L, E, m, G.L[0], G.lo[0], G.lo[1], G.lo[2],
+                   (float4 *)red, dn);
+    else
+        P2P_LAUNCH((k_adapt_restructure_chunks<float, float4, false>), gw, 256, 0, st, (const float4 *)P->rec, lkey,
+                   len, lstart, off, nbr, code, ch_leaf, ch_rel, roff, L, E, m, G.L[0], G.lo[0], G.lo[1], G.lo[2],
+                   (float4 *)red, dn);
+    P2P_CUDA_TRY(cudaGetLastError());
+    return P2P_OK;
 }
 
 struct U64Get {
@@ -585,7 +773,7 @@ namespace p2p {
 // a6 + a7 + a9 over the adaptive leaves: leaves, CSR, redundant runs (optionally copied out), items, the REDUNDANT
 // eval over them; synchronous (sizes are read back)
 p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, void *phi, void *field, void *red_h,
-                         int64_t cap_red, int64_t *n_red) {
+                         int64_t cap_red, int64_t *n_red, int64_t *n_items) {
     cudaStream_t st = P->stream;
     const bool f64 = P->cfg.precision == P2P_FP64;
     *n_red = 0;
@@ -598,61 +786,68 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, vo
     }
     const uint32_t L = (uint32_t)A.L;
     unsigned long long *R = nullptr, *roff = nullptr, *rtot = nullptr;
-    uint32_t *tself = nullptr, *nit = nullptr, *ioff = nullptr, *itot = nullptr, *zero = nullptr;
+    uint32_t *tself = nullptr, *ioff = nullptr, *itot = nullptr, *zero = nullptr;
+    unsigned long long *ptot = nullptr;  // the pair count I (sizes the work items)
     void *scr = nullptr;
     P2P_CUDA_TRY(dalloc((void **)&R, 8 * (size_t)L, st));
     P2P_CUDA_TRY(dalloc((void **)&roff, 8 * (size_t)L, st));
     P2P_CUDA_TRY(dalloc((void **)&rtot, 8, st));
     P2P_CUDA_TRY(dalloc((void **)&tself, 4 * (size_t)L, st));
-    P2P_CUDA_TRY(dalloc((void **)&nit, 4 * (size_t)L, st));
+    P2P_CUDA_TRY(dalloc((void **)&ptot, 8, st));
+    P2P_CUDA_TRY(cudaMemsetAsync(ptot, 0, 8, st));
     P2P_CUDA_TRY(dalloc((void **)&ioff, 4 * (size_t)L, st));
     P2P_CUDA_TRY(dalloc((void **)&itot, 4, st));
     P2P_CUDA_TRY(dalloc((void **)&zero, 4, st));
     P2P_CUDA_TRY(dalloc(&scr, scan_partials_bytes(L), st));
+    const uint32_t E = (uint32_t)A.E, nch = (E + 31u) / 32u + 1u;
+    uint32_t *ch_leaf = nullptr;
+    unsigned long long *ch_rel = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&ch_leaf, 4 * (size_t)nch, st));
+    P2P_CUDA_TRY(dalloc((void **)&ch_rel, 8 * (size_t)nch, st));
     P2P_CUDA_TRY(cudaMemsetAsync(zero, 0, 4, st));
     const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(L, 128), (unsigned)P->num_sms * 8));
-    P2P_LAUNCH(k_adapt_count, g, 128, 0, st, A.off, A.nbr, A.code, A.lstart, L, R, tself, nit);
+    P2P_LAUNCH(k_adapt_count, g, 128, 0, st, A.off, A.nbr, A.code, A.lstart, L, R, tself, DevN(), ptot,
+               ch_leaf, ch_rel);
     P2P_CUDA_TRY(device_scan<unsigned long long>(U64Get{R}, U64Put{roff}, nullptr, (uint64_t)L, rtot, scr, st));
-    P2P_CUDA_TRY(device_scan<uint32_t>(CntGet{nit}, OffPut{ioff}, nullptr, (uint64_t)L, itot, scr, st));
+    const uint32_t K = (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32);
+    P2P_CUDA_TRY(device_scan<uint32_t>(ItemCntGet{A.lstart, R, nullptr, K}, OffPut{ioff}, nullptr, (uint64_t)L, itot, scr,
+                                       st));
+    // the REDUNDANT list (multi-leaf quads) -- built whatever the layout, so both paths' items are the same
+    const bool quads = adapt_quads(P);
+    uint32_t *ioff_red = nullptr, *itot_red = nullptr;
+    P2P_CUDA_TRY(dalloc((void **)&ioff_red, 4 * (size_t)L, st));
+    P2P_CUDA_TRY(dalloc((void **)&itot_red, 4, st));
+    P2P_CUDA_TRY(device_scan<uint32_t>(RedCntGet{A.lstart, R, adapt_capped() ? ptot : nullptr, nullptr, L, K, quads}, OffPut{ioff_red}, nullptr,
+                                       (uint64_t)L, itot_red, scr, st));
     unsigned long long Rtot = 0;
-    uint32_t Itot = 0;
+    uint32_t Itot = 0, Itot_red = 0;
     P2P_CUDA_TRY(cudaMemcpyAsync(&Rtot, rtot, 8, cudaMemcpyDeviceToHost, st));
     P2P_CUDA_TRY(cudaMemcpyAsync(&Itot, itot, 4, cudaMemcpyDeviceToHost, st));
+    P2P_CUDA_TRY(cudaMemcpyAsync(&Itot_red, itot_red, 4, cudaMemcpyDeviceToHost, st));
     P2P_CUDA_TRY(cudaStreamSynchronize(st));
     void *red = nullptr;
-    Item *items = nullptr;
+    Item *items = nullptr, *items_red = nullptr;
     const size_t rsz = f64 ? sizeof(double4) : sizeof(float4);
     P2P_CUDA_TRY(dalloc(&red, rsz * std::max<unsigned long long>(Rtot, 1), st));
     P2P_CUDA_TRY(dalloc((void **)&items, sizeof(Item) * std::max<uint32_t>(Itot, 1), st));
+    P2P_CUDA_TRY(dalloc((void **)&items_red, sizeof(Item) * std::max<uint32_t>(Itot_red, 1), st));
     const int m = P->key_bits / 3;
-    const Geom &G = P->geom;
-    const uint32_t E = (uint32_t)A.E;
-    unsigned long long *eoff = nullptr, *etot = nullptr;
-    void *escr = nullptr;
-    P2P_CUDA_TRY(dalloc((void **)&eoff, 8 * (size_t)std::max<uint32_t>(E, 1), st));
-    P2P_CUDA_TRY(dalloc((void **)&etot, 8, st));
-    P2P_CUDA_TRY(dalloc(&escr, scan_partials_bytes(E), st));
-    P2P_CUDA_TRY(device_scan<unsigned long long>(EntryCntGet{A.nbr, A.lstart}, U64Put{eoff}, nullptr, (uint64_t)E, etot,
-                                                 escr, st));
-    const unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up((uint64_t)E, 256), (unsigned)P->num_sms * 16));
     uint8_t *lframe = nullptr;
     P2P_CUDA_TRY(dalloc((void **)&lframe, std::max<uint32_t>(L, 1), st));
     P2P_LAUNCH(k_leaf_frame, g, 128, 0, st, A.lkey, A.len, L, m, lframe);
-    if (indexed) {
-        // the non-redundant baseline: no runs, the eval stages the neighbour segments of the sorted records
-    } else if (f64)
-        P2P_LAUNCH((k_adapt_restructure_chunks<double, double4>), gw, 256, 0, st, (const double4 *)P->rec, A.lkey,
-                   A.len, A.lstart, A.off, A.nbr, A.code, eoff, L, E, m, G.L[0], G.lo[0], G.lo[1], G.lo[2],
-                   (double4 *)red);
-    else
-        P2P_LAUNCH((k_adapt_restructure_chunks<float, float4>), gw, 256, 0, st, (const float4 *)P->rec, A.lkey, A.len,
-                   A.lstart, A.off, A.nbr, A.code, eoff, L, E, m, G.L[0], G.lo[0], G.lo[1], G.lo[2], (float4 *)red);
-    P2P_LAUNCH(k_adapt_items, g, 128, 0, st, A.lstart, roff, R, tself, ioff, L,
-               (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32), items);
+    // INDEXED: the non-redundant baseline, no runs (the eval stages the neighbour segments of the sorted records)
+    if (!indexed) {
+        s = launch_adapt_runs(P, A.lkey, A.len, A.lstart, A.off, A.nbr, A.code, ch_leaf, ch_rel, roff, L, E, E, red,
+                              DevN());
+        if (s != P2P_OK) return s;
+    }
+    P2P_LAUNCH(k_adapt_items, g, 128, 0, st, A.lstart, roff, R, tself, ioff, L, K, nullptr, items, DevN(), items_red,
+               ioff_red, adapt_capped() ? ptot : nullptr, quads);
     P2P_CUDA_TRY(cudaGetLastError());
     s = P2P_OK;
     if (phi) {
-        EvalItems it{items, itot, (int64_t)Itot, red, zero};
+        EvalItems it = indexed ? EvalItems{items, itot, (int64_t)Itot, red, zero}
+                               : EvalItems{items_red, itot_red, (int64_t)Itot_red, red, zero};
         if (indexed) {
             it.csr_off = A.off;
             it.csr_nbr = A.nbr;
@@ -663,6 +858,7 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, vo
         s = eval_gravity_items(P, it, phi, field);
     }
     *n_red = (int64_t)Rtot;
+    if (n_items) *n_items = (int64_t)std::max(Itot, Itot_red);
     if (s == P2P_OK && red_h && !indexed) {
         if ((int64_t)Rtot > cap_red) {
             set_error("red capacity below the record count");
@@ -672,7 +868,8 @@ p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, vo
         }
     }
     P2P_CUDA_TRY(cudaStreamSynchronize(st));
-    void *bufs[] = {R, roff, rtot, tself, nit, ioff, itot, zero, scr, red, items, eoff, etot, escr, lframe};
+    void *bufs[] = {R,   roff,  rtot,    tself,  ptot,     ioff,     itot,     zero,     scr,
+                    red, items, ch_leaf, ch_rel, lframe, ioff_red, itot_red, items_red};
     for (void *p : bufs) dfree(p, st);
     A.release(st);
     return s;
@@ -699,8 +896,8 @@ __global__ void k_adapt_check_e(AdaptCtr *ac, uint32_t *__restrict__ off, uint64
     off[ac->L] = ac->E;
 }
 __global__ void k_adapt_check_r(AdaptCtr *ac, uint64_t rcap, uint64_t icap) {
-    if (ac->R > rcap || ac->n_items > icap) ac->overflow = 1u;
-    if (ac->overflow) ac->n_items = 0;  // the eval then does nothing (its items were not built)
+    if (ac->R > rcap || ac->n_items > icap || ac->n_items_red > icap) ac->overflow = 1u;
+    if (ac->overflow) ac->n_items = ac->n_items_red = 0;  // the eval then does nothing (its items were not built)
 }
 }  // namespace
 
@@ -709,8 +906,9 @@ void adaptive_free(p2p_plan *P) {
     if (!A) return;
     cudaStream_t st = P->stream;
     void *bufs[] = {A->ac,    A->len8, A->rcode, A->code, A->code_t, A->lframe, A->llen, A->lprefix, A->lstart,
-                    A->lkey,  A->off,  A->nbr,   A->nbr_t, A->tself, A->nit,    A->ioff, A->zero,    A->dcnt,
-                    A->tcnt,  A->tcur, A->rng,   A->R,    A->roff,   A->eoff,   A->red,  A->scr,     A->items};
+                    A->lkey,  A->off,  A->nbr,   A->nbr_t, A->tself, A->ioff, A->zero,    A->dcnt,
+                    A->tcnt,  A->tcur, A->rng,   A->R,    A->roff,   A->ch_rel, A->red,  A->scr,     A->items,
+                    A->ch_leaf, A->items_red, A->ioff_red};
     for (void *b : bufs) dfree(b, st);
     delete A;
     P->ad = nullptr;
@@ -720,14 +918,14 @@ p2p_status adaptive_enable(p2p_plan *P, uint32_t t, int min_bits) {
     cudaStream_t st = P->stream;
     adaptive_free(P);
     // measure the current input (synchronous, once): entries and records of its leaves
-    int64_t E = 0, R = 0;
+    int64_t E = 0, R = 0, I = 0;
     if (P->B > 0) {
         AdaptiveDev D;
         p2p_status s = build_adaptive(P, t, min_bits, D);
         E = D.E;
         D.release(st);
         if (s != P2P_OK) return s;
-        s = adaptive_eval(P, t, min_bits, false, nullptr, nullptr, nullptr, 0, &R);
+        s = adaptive_eval(P, t, min_bits, false, nullptr, nullptr, nullptr, 0, &R, &I);
         if (s != P2P_OK) return s;
     }
     AdaptState *A = new AdaptState();
@@ -737,7 +935,7 @@ p2p_status adaptive_enable(p2p_plan *P, uint32_t t, int min_bits) {
     A->bcap = std::max<int64_t>(P->bcap, 1);
     A->ecap = std::max<int64_t>(2 * E, 64);
     A->rcap = std::max<int64_t>(2 * R, std::max<int64_t>(P->cap, 1));
-    A->icap = A->bcap + P->cap / 32 + 1;
+    A->icap = std::max<int64_t>(2 * I, A->bcap + P->cap / 32 + 1);  // cost-capped items: measured, with headroom
     const int64_t L = A->bcap, Ec = A->ecap;
     const size_t rsz = P->cfg.precision == P2P_FP64 ? sizeof(double4) : sizeof(float4);
 #define ADA(ptr, bytes)                                                                   \
@@ -767,13 +965,15 @@ p2p_status adaptive_enable(p2p_plan *P, uint32_t t, int min_bits) {
     ADA(A->R, 8 * L);
     ADA(A->roff, 8 * L);
     ADA(A->tself, 4 * L);
-    ADA(A->nit, 4 * L);
     ADA(A->ioff, 4 * L);
-    ADA(A->eoff, 8 * Ec);
+    ADA(A->ch_leaf, 4 * (Ec / 32 + 1));
+    ADA(A->ch_rel, 8 * (Ec / 32 + 1));
     ADA(A->lframe, L);
     ADA(A->zero, 4);
     ADA(A->red, rsz * A->rcap);
     ADA(A->items, sizeof(Item) * A->icap);
+    ADA(A->items_red, sizeof(Item) * A->icap);
+    ADA(A->ioff_red, 4 * L);
     ADA(A->scr, std::max(scan_partials_bytes(L), scan_partials_bytes(Ec)));
 #undef ADA
     P2P_CUDA_TRY(cudaMemsetAsync(A->zero, 0, 4, st));
@@ -812,56 +1012,50 @@ p2p_status adaptive_build_async(p2p_plan *P) {
                (const unsigned int *)A->dcnt, A->tcur, A->nbr_t, A->code_t, dn);
     P2P_LAUNCH(k_dil_merge, gw, 256, 0, st, (const uint32_t *)A->off, (const unsigned int *)A->dcnt, Lc,
                (const uint32_t *)A->nbr_t, (const uint8_t *)A->code_t, A->nbr, A->code, dn);
+    // per leaf: run length, self offset, items (scans: device R, items) + the restructure chunk heads, the leaf
+    // frames and the work items -- what BOTH layouts' evals need (the grid path's a5 builds the same), so that
+    // p2p_restructure is the redundant runs alone
+    const bool f64 = P->cfg.precision == P2P_FP64;
+    const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(Lc, 128), (unsigned)P->num_sms * 8));
+    P2P_LAUNCH(k_adapt_count, g, 128, 0, st, A->off, A->nbr, A->code, A->lstart, Lc, A->R, A->tself, dn,
+               &A->ac->I, A->ch_leaf, A->ch_rel);
+    P2P_CUDA_TRY(device_scan<unsigned long long>(U64Get{A->R}, U64Put{A->roff}, &A->ac->L, Lc, &A->ac->R, A->scr, st));
+    const uint32_t K = (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32);
+    P2P_CUDA_TRY(device_scan<uint32_t>(ItemCntGet{A->lstart, A->R, nullptr, K}, OffPut{A->ioff}, &A->ac->L, Lc,
+                                       &A->ac->n_items, A->scr, st));
+    const bool quads = adapt_quads(P);
+    P2P_CUDA_TRY(device_scan<uint32_t>(RedCntGet{A->lstart, A->R, adapt_capped() ? &A->ac->I : nullptr, &A->ac->L, 0u, K, quads}, OffPut{A->ioff_red},
+                                       &A->ac->L, Lc, &A->ac->n_items_red, A->scr, st));
+    P2P_LAUNCH(k_adapt_check_r, 1, 1, 0, st, A->ac, (uint64_t)A->rcap, (uint64_t)A->icap);
+    P2P_LAUNCH(k_leaf_frame, g, 128, 0, st, A->lkey, A->llen, Lc, m, A->lframe, dn);
+    P2P_LAUNCH(k_adapt_items, g, 128, 0, st, A->lstart, A->roff, A->R, A->tself, A->ioff, Lc, K, nullptr, A->items,
+               dn, A->items_red, A->ioff_red, adapt_capped() ? &A->ac->I : nullptr, quads);
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }
 
-// a6 of adaptive mode: per-leaf run lengths / self offsets / items (scans: device R, items), entry offsets, the
-// redundant runs (C24), the work items and (INDEXED) the leaf frames
+// a6 of adaptive mode: the redundant runs (C24) over the chunk heads the update recorded
 p2p_status adaptive_restructure_async(p2p_plan *P) {
     AdaptState *A = P->ad;
-    cudaStream_t st = P->stream;
     if (P->n == 0) {
         A->runs_valid = true;
         return P2P_OK;
     }
-    const bool f64 = P->cfg.precision == P2P_FP64;
-    const int m = P->key_bits / 3;
-    const uint32_t Lc = (uint32_t)A->bcap;
     const DevN dn{&A->ac->L, &A->ac->E, &A->ac->overflow};
-    const unsigned g = std::max<unsigned>(1, std::min<unsigned>(div_up(Lc, 128), (unsigned)P->num_sms * 8));
-    P2P_CUDA_TRY(cudaMemsetAsync(&A->ac->I, 0, sizeof(unsigned long long), st));
-    P2P_LAUNCH(k_adapt_count, g, 128, 0, st, A->off, A->nbr, A->code, A->lstart, Lc, A->R, A->tself, A->nit, dn,
-               &A->ac->I);
-    P2P_CUDA_TRY(device_scan<unsigned long long>(U64Get{A->R}, U64Put{A->roff}, &A->ac->L, Lc, &A->ac->R, A->scr, st));
-    P2P_CUDA_TRY(device_scan<uint32_t>(CntGet{A->nit}, OffPut{A->ioff}, &A->ac->L, Lc, &A->ac->n_items, A->scr, st));
-    P2P_LAUNCH(k_adapt_check_r, 1, 1, 0, st, A->ac, (uint64_t)A->rcap, (uint64_t)A->icap);
-    P2P_CUDA_TRY(device_scan<unsigned long long>(EntryCntGet{A->nbr, A->lstart}, U64Put{A->eoff}, &A->ac->E,
-                                                 (uint64_t)A->ecap, (unsigned long long *)nullptr, A->scr, st));
-    P2P_LAUNCH(k_leaf_frame, g, 128, 0, st, A->lkey, A->llen, Lc, m, A->lframe, dn);
-    const unsigned gw = std::max<unsigned>(1, std::min<unsigned>(div_up((uint64_t)A->ecap, 256), (unsigned)P->num_sms * 16));
-    const Geom &G = P->geom;
-    if (f64)
-        P2P_LAUNCH((k_adapt_restructure_chunks<double, double4>), gw, 256, 0, st, (const double4 *)P->rec, A->lkey,
-                   A->llen, A->lstart, A->off, A->nbr, A->code, A->eoff, Lc, (uint32_t)A->ecap, m, G.L[0], G.lo[0],
-                   G.lo[1], G.lo[2], (double4 *)A->red, dn);
-    else
-        P2P_LAUNCH((k_adapt_restructure_chunks<float, float4>), gw, 256, 0, st, (const float4 *)P->rec, A->lkey,
-                   A->llen, A->lstart, A->off, A->nbr, A->code, A->eoff, Lc, (uint32_t)A->ecap, m, G.L[0], G.lo[0],
-                   G.lo[1], G.lo[2], (float4 *)A->red, dn);
-    P2P_LAUNCH(k_adapt_items, g, 128, 0, st, A->lstart, A->roff, A->R, A->tself, A->ioff, Lc,
-               (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32), A->items, dn);
-    P2P_CUDA_TRY(cudaGetLastError());
-    A->runs_valid = true;
-    return P2P_OK;
+    p2p_status s = launch_adapt_runs(P, A->lkey, A->llen, A->lstart, A->off, A->nbr, A->code, A->ch_leaf, A->ch_rel,
+                                     A->roff, (uint32_t)A->bcap, (uint32_t)A->ecap, (uint64_t)A->ecap, A->red, dn);
+    if (s == P2P_OK) A->runs_valid = true;
+    return s;
 }
 
 // a7 + a9 of adaptive mode: REDUNDANT over the runs, or INDEXED over the leaves' CSR segments (the baseline)
 p2p_status adaptive_eval_async(p2p_plan *P, p2p_layout layout, void *phi, void *field) {
     AdaptState *A = P->ad;
     if (P->n == 0) return P2P_OK;
-    EvalItems it{A->items, &A->ac->n_items, A->icap, A->red, A->zero};
+    EvalItems it{A->items_red, &A->ac->n_items_red, A->icap, A->red, A->zero};
     if (layout == P2P_INDEXED) {
+        it.items = A->items;
+        it.n_items = &A->ac->n_items;
         it.csr_off = A->off;
         it.csr_nbr = A->nbr;
         it.csr_code = A->code;

@@ -620,8 +620,9 @@ p2p_status p2p_eval(p2p_plan *P, p2p_layout layout, void *potential, void *field
     if (P->ad) {  // adaptive-leaf mode
         if (layout != P2P_REDUNDANT && layout != P2P_INDEXED)
             return fail(P2P_ERR_UNSUPPORTED, "adaptive mode evaluates P2P_REDUNDANT or P2P_INDEXED");
-        if (!P->ad->runs_valid)
-            return fail(P2P_ERR_BAD_STATE, "eval needs p2p_restructure first in adaptive mode (and after update)");
+        if (layout == P2P_REDUNDANT && !P->ad->runs_valid)
+            return fail(P2P_ERR_BAD_STATE,
+                        "eval(P2P_REDUNDANT) needs p2p_restructure first in adaptive mode (and after update)");
         if (P->n == 0) return P2P_OK;
         if (!is_device_ptr(potential)) return fail(P2P_ERR_INVALID_ARGUMENT, "potential must be a device pointer");
         if (field && !is_device_ptr(field)) return fail(P2P_ERR_INVALID_ARGUMENT, "field must be a device pointer");
@@ -685,7 +686,7 @@ p2p_status p2p_get_info(const p2p_plan *Pc, p2p_info *out) {
     out->n_items = P->n_items;
     out->key_bits = P->key_bits;
     out->sort_passes = P->passes;
-    if (P->ad) {  // adaptive mode: the leaves' counts (pairs / records after p2p_restructure)
+    if (P->ad) {  // adaptive mode: the leaves' counts
         AdaptCtr h;
         rs = adaptive_info(P, &h);
         if (rs != P2P_OK) return rs;

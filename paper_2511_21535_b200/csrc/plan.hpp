@@ -85,6 +85,7 @@ namespace p2p {
 struct AdaptCtr {
     uint32_t L, E, n_items, overflow;
     unsigned long long R, I;
+    uint32_t n_items_red, pad;  // the REDUNDANT eval's items (multi-leaf quads, fp32)
 };
 struct AdaptState {
     uint32_t t = 0;
@@ -93,12 +94,15 @@ struct AdaptState {
     AdaptCtr *ac = nullptr;
     uint8_t *len8 = nullptr, *rcode = nullptr, *code = nullptr, *code_t = nullptr, *lframe = nullptr;
     uint32_t *llen = nullptr, *lprefix = nullptr, *lstart = nullptr, *lkey = nullptr, *off = nullptr, *nbr = nullptr,
-             *nbr_t = nullptr, *tself = nullptr, *nit = nullptr, *ioff = nullptr, *zero = nullptr;
+             *nbr_t = nullptr, *tself = nullptr, *ioff = nullptr, *zero = nullptr;
     unsigned int *dcnt = nullptr, *tcnt = nullptr, *tcur = nullptr;
     uint2 *rng = nullptr;
-    unsigned long long *R = nullptr, *roff = nullptr, *eoff = nullptr;
+    unsigned long long *R = nullptr, *roff = nullptr, *ch_rel = nullptr;  // ch_*: per restructure chunk (32 entries)
+    uint32_t *ch_leaf = nullptr;
     void *red = nullptr, *scr = nullptr;
     Item *items = nullptr;
+    Item *items_red = nullptr;  // REDUNDANT list: multi-leaf quads + the other leaves' items
+    uint32_t *ioff_red = nullptr;
     bool built = false;     // leaves + CSR of the current positions
     bool runs_valid = false;
 };
@@ -244,7 +248,7 @@ p2p_status adaptive_restructure_async(p2p_plan *P);
 p2p_status adaptive_eval_async(p2p_plan *P, p2p_layout layout, void *phi, void *field);
 p2p_status adaptive_info(p2p_plan *P, AdaptCtr *out);  // synchronises
 p2p_status adaptive_eval(p2p_plan *P, uint32_t t, int min_bits, bool indexed, void *phi, void *field, void *red_h,
-                         int64_t cap_red, int64_t *n_red);
+                         int64_t cap_red, int64_t *n_red, int64_t *n_items = nullptr);
 
 // k_pairrec.cu: the thread-level pair-record layout (P2P_PAIRREC)
 p2p_status restructure_pairs(p2p_plan *P);

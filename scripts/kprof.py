@@ -17,7 +17,8 @@ import paper_2511_21535_b200 as P  # noqa: E402
 wl = sys.argv[1] if len(sys.argv) > 1 else "c5w"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 LAYS = sys.argv[3].split(",") if len(sys.argv) > 3 else ["redundant"]
-inp = G.plummer_tiles(12_500_000, 256, 1, 0) if wl == "c5w" else G.config(wl)
+base, _, t_ad = wl.partition("-adaptive-t")  # e.g. c3-adaptive-t4: adaptive leaves of threshold t (bench.py)
+inp = G.plummer_tiles(12_500_000, 256, 1, 0) if base == "c5w" else G.config(base)
 pos = torch.from_numpy(inp.pos).cuda()
 m = torch.from_numpy(inp.mass).cuda()
 phi = torch.empty(inp.n, device="cuda")
@@ -25,6 +26,8 @@ field = torch.empty((inp.n, 3), device="cuda")
 # P2P_KPROF_COMM=1: the collective (multi-GPU) plan path with a 1-rank NCCL communicator
 comm = P.p2p_comm_create(1, 0, P.p2p_comm_unique_id()) if os.environ.get("P2P_KPROF_COMM") else None
 plan = P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps, comm=comm)
+if t_ad:
+    plan.enable_adaptive(int(t_ad))
 
 
 def step():

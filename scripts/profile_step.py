@@ -14,12 +14,15 @@ import paper_2511_21535_b200 as P  # noqa: E402
 wl = sys.argv[1] if len(sys.argv) > 1 else "c5w"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 layouts = sys.argv[3].split(",") if len(sys.argv) > 3 else ["redundant"]
-inp = G.plummer_tiles(12_500_000, 256, 1, 0) if wl == "c5w" else G.config(wl)
+base, _, t_ad = wl.partition("-adaptive-t")  # e.g. c3-adaptive-t4: adaptive leaves of threshold t
+inp = G.plummer_tiles(12_500_000, 256, 1, 0) if base == "c5w" else G.config(base)
 pos = torch.from_numpy(inp.pos).cuda()
 m = torch.from_numpy(inp.mass).cuda()
 if inp.pos.ndim == 2 and inp.pos.shape[1] == 3:
     for _ in range(steps):
         with P.Plan(P.P2P_GRAVITY, pos, m, inp.h, inp.lo, inp.nbox, inp.periodic, eps=inp.eps) as plan:
+            if t_ad:
+                plan.enable_adaptive(int(t_ad))
             plan.restructure()
             for lay in layouts:
                 plan.eval(P.LAYOUTS[lay])

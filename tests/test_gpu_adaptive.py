@@ -203,3 +203,71 @@ def test_adaptive_indexed_baseline(P, seed, t, dtype):
     tol = 1e-5 if dtype == np.float32 else 1e-12
     for lay, (phi, fld) in out.items():
         assert bounds.close(phi, rphi, tol) and bounds.close(fld, rf, tol), lay
+
+
+def _shifted(inp, lo):
+    """the same clustered particles in a domain at origin lo (positions moved in fp64, rounded once)"""
+    import dataclasses
+    pos = (inp.pos.astype(np.float64) + np.asarray(lo)).astype(inp.pos.dtype)
+    return dataclasses.replace(inp, pos=np.ascontiguousarray(pos), lo=tuple(lo), name=inp.name + f" lo={lo}")
+
+
+@pytest.mark.parametrize("lo,t,maxgrid", [((0.1, -0.37, 0.55), 8, None),     # leaf origins not fp32 values: fp64
+                                          ((0.25, 0.5, -0.75), 16, None),    # fp32-exact origins: fp32 fast path
+                                          ((0.0, 0.0, 0.0), 4, "2"),         # 16 warps walk every chunk
+                                          ((0.1, -0.37, 0.55), 32, "3")])
+def test_adaptive_runs_origin_and_chunk_walk(P, lo, t, maxgrid, monkeypatch):
+    """C24 runs bit-exact vs the oracle with the domain off the origin -- both rounding paths of the chunk
+    restructure (the fp64 sequence, and the fp32 subtraction taken when every lattice origin is an fp32 value) --
+    and with the grid capped so that each warp walks many chunks (its one-chunk-ahead loads)"""
+    if maxgrid:
+        monkeypatch.setenv("P2P_RS_MAXGRID", maxgrid)
+    inp = _shifted(G.plummer(6000, 32, seed=31), lo)
+    tr = A.AdaptiveTree(inp, t)
+    want_red = tr.red(np.float32)
+    with _plan(P, inp) as plan:
+        red = np.empty((want_red.shape[0] + 1, 4), np.float32)
+        n = P.p2p_adaptive_eval(plan.handle, t, 9, None, None, red)
+        assert n == want_red.shape[0]
+        assert red[:n].tobytes() == want_red.tobytes()
+        # the asynchronous mode builds the same runs (its eval equals the synchronous one bit for bit)
+        plan.enable_adaptive(t)
+        phi, fld = [x.cpu().numpy() for x in plan.eval(P.P2P_INDEXED)]  # INDEXED needs the update only
+        with pytest.raises(P.P2PError) as e:
+            plan.eval(P.P2P_REDUNDANT)
+        assert e.value.status == P.P2P_ERR_BAD_STATE
+        info = plan.refresh_info()  # counts are the update's: known before the restructure
+        assert info.n_red == n
+        plan.restructure()
+        mphi, mfld = [x.cpu().numpy() for x in plan.eval(P.P2P_REDUNDANT)]
+    sphi = torch.empty(inp.n, device="cuda")
+    sfld = torch.empty((inp.n, 3), device="cuda")
+    with _plan(P, inp) as plan:
+        P.p2p_adaptive_eval(plan.handle, t, 9, sphi.data_ptr(), sfld.data_ptr())
+        torch.cuda.synchronize()
+    assert mphi.tobytes() == sphi.cpu().numpy().tobytes() and mfld.tobytes() == sfld.cpu().numpy().tobytes()
+    rphi, rf = tr.eval(inp.eps)
+    assert bounds.close(mphi, rphi, 1e-5) and bounds.close(mfld, rf, 1e-5)
+    assert np.isfinite(phi).all()
+
+
+@pytest.mark.parametrize("t,cap", [(2, "1"), (4, "1"), (8, "1"), (4, "0")])
+def test_adaptive_quads(P, t, cap, monkeypatch):
+    """multi-leaf quad items (REDUNDANT, fp32; opt-in P2P_ADAPT_QUADS=1): within tolerance of the oracle with and
+    without them, and actually taken (the 8-lane split of a quad leaf sums in another order than its own item)"""
+    monkeypatch.setenv("P2P_ADAPT_CAP", cap)  # "0": uncapped REDUNDANT items, quads limited by 8 targets / 16 bits
+    inp = G.plummer(8000, 32, seed=40 + t)
+    tr = A.AdaptiveTree(inp, t)
+    rphi, rf = tr.eval(inp.eps)
+    out = []
+    for quads in ("1", "0"):
+        monkeypatch.setenv("P2P_ADAPT_QUADS", quads)
+        phi = torch.empty(inp.n, device="cuda")
+        fld = torch.empty((inp.n, 3), device="cuda")
+        with _plan(P, inp) as plan:
+            P.p2p_adaptive_eval(plan.handle, t, 9, phi.data_ptr(), fld.data_ptr())
+            torch.cuda.synchronize()
+        phi, fld = phi.cpu().numpy(), fld.cpu().numpy()
+        assert bounds.close(phi, rphi, 1e-5) and bounds.close(fld, rf, 1e-5)
+        out.append(phi.tobytes() + fld.tobytes())
+    assert out[0] != out[1]
