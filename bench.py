@@ -34,9 +34,9 @@ BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
 UNIT = "pair-interactions/s"
 FP32_INSTR_PER_PAIR = 13           # SURVEY §8d, verified from SASS
-FP64_INSTR_PER_PAIR = 26           # fp64 hot loop SASS per pair: 3 DADD + 3 DFMA (r^2) + 8 (correctly rounded sqrt:
-                                   # MUFU.RSQ64H seed + DMUL/DFMA Newton) + 5 DFMA (correctly rounded 1/x, C14) + 3 DMUL
-                                   # + 1 DADD + 3 DFMA
+FP64_INSTR_PER_PAIR = 18           # fp64 hot loop SASS per pair: 3 DADD + 3 DFMA (r^2) + 5 (rsqrt, C14: MUFU.RSQ64H
+                                   # seed + DMUL/DFMA second-order Newton step) + 3 DMUL + 1 DADD + 3 DFMA (
+                                   # 26 with the correctly rounded 1/sqrt of round 2's first fp64 line)
 FP64_LANES_PER_SM = 64             # DFMA lane-ops per clock per SM, measured (profiles/r02_ubench_fp64.txt)
 SM_COUNT_NOMINAL = 148
 LANES_PER_SM = 128
@@ -294,7 +294,7 @@ def ours(args, rank, world, local):
 
     pk = peaks()
     # roofline of the dominant kernel (eval): FP32-pipe bound, 13 FP32 instructions per pair;
-    # fp64: FP64-pipe bound, 26 FP64-pipe instructions per pair (SASS hot loop) at the measured DFMA rate per SM
+    # fp64: FP64-pipe bound, FP64_INSTR_PER_PAIR FP64-pipe instructions per pair (SASS hot loop) at the measured DFMA rate per SM
     # (scripts/ubench_fp64.cu, profiles/r02_ubench_fp64.txt)
     eval_ms_in_step = float(np.mean(t_eval))
     achieved = I / (eval_ms_in_step * 1e-3)

@@ -271,7 +271,7 @@ struct Tgt<double, K> {
             double r2 = __fma_rn(dx, dx, E);
             r2 = __fma_rn(dy, dy, r2);
             r2 = __fma_rn(dz, dz, r2);
-            const double ri = 1.0 / sqrt(r2);
+            const double ri = rsqrt(r2);  // C14: MUFU.RSQ64H seed + one 2nd-order Newton step (<= 1 ulp)
             const double mri = s.w * ri;
             ap[k] += mri;
             const double m3 = mri * (ri * ri);
@@ -294,7 +294,7 @@ struct Tgt<double, K> {
     __device__ __forceinline__ void get(int k, double &p_, double &x, double &y, double &z) const {
         p_ = ap[k]; x = ax[k]; y = ay[k]; z = az[k];
     }
-    static __device__ __forceinline__ double self_rinv(double eps2) { return 1.0 / sqrt(__fma_rn(0.0, 0.0, eps2)); }
+    static __device__ __forceinline__ double self_rinv(double eps2) { return rsqrt(__fma_rn(0.0, 0.0, eps2)); }
     static __device__ __forceinline__ double eps_pack(double e2) { return e2; }
 };
 

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_restructure_pairs(
 }
 
 __device__ __forceinline__ float rinv_of(float r2) { return rsqrt_ftz(r2); }  // C14
-__device__ __forceinline__ double rinv_of(double r2) { return 1.0 / sqrt(r2); }
+__device__ __forceinline__ double rinv_of(double r2) { return rsqrt(r2); }  // C14
 
 // warp per target box; lane = one (record, target) slot of the box's ne x n_b partial slots (the paper's thread
 // per target per pair record): the lane reads its target tuple and its record's sources -- nothing else -- and
