@@ -40,10 +40,12 @@ __device__ __forceinline__ uint64_t item_costcap(const DevCounters *ctr) { retur
 // targets per item of a box with nb_b targets and nsrc sources (its items: ceil(nb_b / size))
 // K = targets per lane of the eval (the capped sizes are multiples of K: every group of K target slots full)
 __device__ __forceinline__ uint32_t item_size(uint32_t nb_b, uint64_t nsrc, uint32_t tmax, uint32_t K, uint64_t cap) {
-    const uint64_t a = (nb_b + tmax - 1) / tmax;
-    const uint64_t c = ((uint64_t)nb_b * nsrc + cap - 1) / cap;
+    const uint32_t a = (nb_b + tmax - 1) / tmax;
+    // the cap is a power of two (item_costcap_of): a shift instead of a 64-bit division (a5 runs this per box)
+    const uint64_t num = (uint64_t)nb_b * nsrc + cap - 1;
+    const uint64_t c = (cap & (cap - 1)) == 0 ? num >> (__ffsll((long long)cap) - 1) : num / cap;
     if (c <= a) return tmax;
-    const uint32_t ts = (uint32_t)(nb_b / c);  // balanced chunk size under the cap
+    const uint32_t ts = c > nb_b ? 0u : nb_b / (uint32_t)c;  // balanced chunk size under the cap
     if (ts < K) return ts > 1 ? ts : 1u;
     if (K == 8) return ts >= 24 ? 24u : ts >= 16 ? 16u : 8u;
     return ts >= 24 ? 24u : ts >= 20 ? 20u : ts >= 16 ? 16u : ts >= 12 ? 12u : ts >= 8 ? 8u : 4u;

@@ -89,9 +89,12 @@ struct EvalArgs {
 // or (multi-GPU, peer memory) into its origin rank's receive buffer: rank r = the run holding i (runs are rank-major,
 // lo[] ascending), element (off[r] + i - lo[r]) of {phi, fx, fy, fz} records -- the reverse all-to-all-v of the
 // results fused into the eval's epilogue
-template <typename T>
+// PEER is a template parameter (only the multi-GPU peer-memory launch instantiates it): with the destination
+// search compiled into every kernel the REDUNDANT eval grew from 3864 to 4672 SASS instructions and ran 5% slower
+// (c5w 5.96 -> 6.26 ms on one box)
+template <bool PEER, typename T>
 __device__ __forceinline__ void put_result(const EvalArgs<T> &a, uint32_t i, int q, T v) {
-    if (a.pr) {
+    if constexpr (PEER) {
         const PeerRes *pr = a.pr;
         int lo = 0, hi = pr->G - 1;  // the largest r with lo[r] <= i
         while (lo < hi) {
@@ -369,7 +372,7 @@ __device__ __forceinline__ double4 ldro(const double4 *p) {
     return make_double4(a.x, a.y, b.x, b.y);
 }
 
-template <typename T, int LAYOUT>
+template <typename T, int LAYOUT, bool PEER>
 __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane) {
     using V4 = typename V4T<T>::type;
     const uint32_t n_small = *a.n_small;
@@ -458,10 +461,10 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
             T pot, fx, fy, fz;
             tg.get(k, pot, fx, fy, fz);
             const uint32_t idx = a.perm[p + k];
-            put_result(a, idx, 0, -(pot - tm[k] * rs));
-            put_result(a, idx, 1, fx);
-            put_result(a, idx, 2, fy);
-            put_result(a, idx, 3, fz);
+            put_result<PEER>(a, idx, 0, -(pot - tm[k] * rs));
+            put_result<PEER>(a, idx, 1, fx);
+            put_result<PEER>(a, idx, 2, fy);
+            put_result<PEER>(a, idx, 3, fz);
         }
         }
     }
@@ -470,7 +473,7 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
 // ADAPT (P2P_INDEXED over adaptive leaves, k_adaptive.cu): the CSR's slot is the image code itself, a leaf's frame /
 // boundary flags come from a.lframe instead of the uniform grid's box coordinates, and a leaf may list more than 32
 // neighbour segments (the lane-per-segment registers then cover groups of 32, re-read from the CSR per chunk)
-template <typename T, int LAYOUT, int K, bool ADAPT = false>
+template <typename T, int LAYOUT, int K, bool ADAPT = false, bool PEER = false>
 __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : (LAYOUT == P2P_REDUNDANT ? 5 : 4)) : 1) k_eval_gravity(const EvalArgs<T> a) {
     using V4 = typename V4T<T>::type;
     constexpr int CH = EV_STAGE_BYTES / (int)sizeof(V4);
@@ -686,7 +689,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
     // CTA, so their latency hides behind the FP32-bound item work of the CTA's other warps (run last by all
     // warps, they would form a latency-bound tail)
     const bool small_first = w == EV_WARPS - 1;
-    if (small_first) small_phase<T, LAYOUT>(a, lane);
+    if (small_first) small_phase<T, LAYOUT, PEER>(a, lane);
     if (lane == 0) pend = queue_claim(a.item_head, (uint32_t)EV_BATCH, a.zero);
     const uint32_t first = next_index();
     if (first < n_items) {
@@ -899,7 +902,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                 const uint32_t i = __shfl_sync(FULL, my_slot, ti & 31u);
                 const T mk = __shfl_sync(FULL, my_m, ti & 31u);
                 if ((uint32_t)j < vcnt && own && ((vmask >> ti) & 1u))
-                    put_result(a, i, (int)q, q == 0 ? -(v[j] - mk * rs) : v[j]);
+                    put_result<PEER>(a, i, (int)q, q == 0 ? -(v[j] - mk * rs) : v[j]);
             }
         } else {
         tg.reduce(S, sl);
@@ -913,10 +916,10 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                 if (active && sl == 0 && ((vmask >> ti) & 1u)) {
                     T pot, fx, fy, fz;
                     tg.get(k, pot, fx, fy, fz);
-                    put_result(a, i, 0, -(pot - mk * rs));
-                    put_result(a, i, 1, fx);
-                    put_result(a, i, 2, fy);
-                    put_result(a, i, 3, fz);
+                    put_result<PEER>(a, i, 0, -(pot - mk * rs));
+                    put_result<PEER>(a, i, 1, fx);
+                    put_result<PEER>(a, i, 2, fy);
+                    put_result<PEER>(a, i, 3, fz);
                 }
             }
         }
@@ -925,15 +928,16 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
     }
     }
     // the remaining small boxes' targets, if any (fills the tail of the item queue)
-    if (!small_first) small_phase<T, LAYOUT>(a, lane);
+    if (!small_first) small_phase<T, LAYOUT, PEER>(a, lane);
 }
 
-template <typename T, int LAYOUT, int K, bool ADAPT = false>
+template <typename T, int LAYOUT, int K, bool ADAPT = false, bool PEER = false>
 p2p_status launch(p2p_plan *P, void *phi, void *field, int slot, const EvalItems *ov = nullptr,
                   const PeerRes *pr = nullptr) {
     using V4 = typename V4T<T>::type;
-    auto kern = k_eval_gravity<T, LAYOUT, K, ADAPT>;
+    auto kern = k_eval_gravity<T, LAYOUT, K, ADAPT, PEER>;
     const int smem = EV_WARPS * 2 * (EV_STAGE_BYTES + EV_TGT * (int)sizeof(V4));
+    if (PEER) slot += 5;  // own occupancy record
     if (P->eval_blocks[slot] == 0) {
         P2P_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int per_sm = 0;
@@ -1005,16 +1009,30 @@ p2p_status eval_gravity_items(p2p_plan *P, const EvalItems &it, void *phi, void 
 p2p_status eval_gravity(p2p_plan *P, p2p_layout layout, void *phi, void *field, const PeerRes *pr) {
     if (P->sizes_known && P->n == 0) return P2P_OK;
     const bool f64 = P->cfg.precision == P2P_FP64;
+    if (pr) {  // multi-GPU over peer memory: results stored into the origin ranks' buffers
+        switch (layout) {
+        case P2P_REDUNDANT:
+            return f64 ? launch<double, P2P_REDUNDANT, EVAL_K_F64, false, true>(P, phi, field, 0, nullptr, pr)
+                       : launch<float, P2P_REDUNDANT, EVAL_K_F32, false, true>(P, phi, field, 0, nullptr, pr);
+        case P2P_INDEXED:
+            return f64 ? launch<double, P2P_INDEXED, EVAL_K_F64, false, true>(P, phi, field, 1, nullptr, pr)
+                       : launch<float, P2P_INDEXED, EVAL_K_F32, false, true>(P, phi, field, 1, nullptr, pr);
+        case P2P_INDEXED_BITWISE:
+            return f64 ? launch<double, P2P_INDEXED_BITWISE, EVAL_K_F64, false, true>(P, phi, field, 2, nullptr, pr)
+                       : launch<float, P2P_INDEXED_BITWISE, EVAL_K_F32, false, true>(P, phi, field, 2, nullptr, pr);
+        }
+        return P2P_ERR_INVALID_ARGUMENT;
+    }
     switch (layout) {
     case P2P_REDUNDANT:
-        return f64 ? launch<double, P2P_REDUNDANT, EVAL_K_F64>(P, phi, field, 0, nullptr, pr)
-                   : launch<float, P2P_REDUNDANT, EVAL_K_F32>(P, phi, field, 0, nullptr, pr);
+        return f64 ? launch<double, P2P_REDUNDANT, EVAL_K_F64>(P, phi, field, 0)
+                   : launch<float, P2P_REDUNDANT, EVAL_K_F32>(P, phi, field, 0);
     case P2P_INDEXED:
-        return f64 ? launch<double, P2P_INDEXED, EVAL_K_F64>(P, phi, field, 1, nullptr, pr)
-                   : launch<float, P2P_INDEXED, EVAL_K_F32>(P, phi, field, 1, nullptr, pr);
+        return f64 ? launch<double, P2P_INDEXED, EVAL_K_F64>(P, phi, field, 1)
+                   : launch<float, P2P_INDEXED, EVAL_K_F32>(P, phi, field, 1);
     case P2P_INDEXED_BITWISE:
-        return f64 ? launch<double, P2P_INDEXED_BITWISE, EVAL_K_F64>(P, phi, field, 2, nullptr, pr)
-                   : launch<float, P2P_INDEXED_BITWISE, EVAL_K_F32>(P, phi, field, 2, nullptr, pr);
+        return f64 ? launch<double, P2P_INDEXED_BITWISE, EVAL_K_F64>(P, phi, field, 2)
+                   : launch<float, P2P_INDEXED_BITWISE, EVAL_K_F32>(P, phi, field, 2);
     }
     return P2P_ERR_INVALID_ARGUMENT;
 }

@@ -8,7 +8,7 @@
 //                     counter in launch order, so look-back never waits on an unscheduled tile), counts its
 //                     digits, publishes them and resolves its exclusive prefix by decoupled look-back over
 //                     earlier tiles (before the ranking: the inclusive prefixes propagate at look-back speed),
-//                     ranks its keys stably with warp-level match (__match_any_sync) in input order,
+//                     ranks its keys stably in input order (8 bit-sliced ballots per key: digit_peers),
 //                     stages the tile in shared memory in digit order and writes each digit run
 //                     contiguously (coalesced) to its global position.
 // Stability: within a tile keys are ranked in (warp, item, lane) order, which is input order; tiles are
@@ -71,6 +71,24 @@ __global__ void __launch_bounds__(256) k_radix_hist_scan(uint32_t *hist) {
     uint32_t v = h[threadIdx.x];
     uint32_t e = block_excl_scan256(v, wt, nullptr);
     h[threadIdx.x] = e;
+}
+
+// lanes of `mask` whose 8-bit digit equals this lane's: bit-sliced, 8 ballots (default).  __match_any_sync
+// (P2P_SORT_MATCH=1) costs one pass per DISTINCT value in the warp on sm_100a: ~28 on uniform digits, so the
+// histogram kernel ran at 0.55 TB/s on passes 0-1 and 1.0 TB/s on the skewed top digit (ncu, gpurun_out/sort)
+__device__ __forceinline__ uint32_t digit_peers(uint32_t mask, uint32_t d) {
+#if defined(P2P_SORT_MATCH) && P2P_SORT_MATCH
+    return __match_any_sync(mask, d);
+#else
+    uint32_t peers = mask;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const bool one = (d >> b) & 1u;
+        const uint32_t bb = __ballot_sync(mask, one);
+        peers &= one ? bb : ~bb;
+    }
+    return peers;
+#endif
 }
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
@@ -169,7 +187,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_radix_pass(const uint32_t *__
         uint32_t mask = __ballot_sync(0xffffffffu, ok);
         if (ok) {
             uint32_t d = (k[i] >> shift) & 255u;
-uint32_t peers = __match_any_sync(mask, d);  // (8 bit-sliced ballots measured slower on sm_100a)
+            const uint32_t peers = digit_peers(mask, d);
             uint32_t cnt = s_whist[w][d];
             r[i] = cnt + __popc(peers & lt_mask);
             __syncwarp(mask);

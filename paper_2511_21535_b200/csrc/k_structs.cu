@@ -42,31 +42,47 @@ __global__ void __launch_bounds__(256) k_bin_gravity(const T *__restrict__ pos, 
     for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
     __syncthreads();
     const double inv_h = 1.0 / g.h;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        uint32_t c[3];
-        T xd[3];
-        bool bad = false;
+    // BIN_U particles per thread per iteration, every load issued before the first use (memory-level parallelism:
+    // one particle per iteration left the kernel at 0.55 of HBM with 67% warps active)
+    constexpr int BIN_U = 4;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x * BIN_U + threadIdx.x; i0 < n; i0 += stride * BIN_U) {
+        T xd[BIN_U][3], qm[BIN_U];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            xd[d] = pos[(size_t)ps * i + d];
-            double f = floor_div_exact(__dsub_rn((double)xd[d], g.lo[d]), g.h, inv_h);
-            if (!(f >= 0.0 && f < (double)g.nbox[d])) {
-                bad = true;
-                f = 0.0;
-            }
-            c[d] = (uint32_t)f;
+        for (int u = 0; u < BIN_U; ++u) {
+            const uint32_t i = i0 + u * blockDim.x;
+            const bool ok = i < n;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) xd[u][d] = ok ? pos[(size_t)ps * i + d] : (T)g.lo[d];
+            qm[u] = (ok && aos) ? q[i] : (T)0;
         }
-        if (bad) atomicMin(&ctr->err_index, (unsigned long long)i);
-        const uint32_t k = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
-        key[i] = k;
-        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
-        if (aos) {
-            V4 r;
-            r.x = xd[0];
-            r.y = xd[1];
-            r.z = xd[2];
-            r.w = q[i];
-            aos[i] = r;
+#pragma unroll
+        for (int u = 0; u < BIN_U; ++u) {
+            const uint32_t i = i0 + u * blockDim.x;
+            if (i >= n) break;
+            uint32_t c[3];
+            bool bad = false;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                double f = floor_div_exact(__dsub_rn((double)xd[u][d], g.lo[d]), g.h, inv_h);
+                if (!(f >= 0.0 && f < (double)g.nbox[d])) {
+                    bad = true;
+                    f = 0.0;
+                }
+                c[d] = (uint32_t)f;
+            }
+            if (bad) atomicMin(&ctr->err_index, (unsigned long long)i);
+            const uint32_t k = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
+            key[i] = k;
+            for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+            if (aos) {
+                V4 r;
+                r.x = xd[u][0];
+                r.y = xd[u][1];
+                r.z = xd[u][2];
+                r.w = qm[u];
+                aos[i] = r;
+            }
         }
     }
     __syncthreads();

@@ -170,7 +170,7 @@ struct p2p_plan {
     int64_t pr_records = 0, pr_targets = 0;
     bool pr_valid = false;
     p2p_status sticky = P2P_OK;
-    int eval_blocks[5] = {0, 0, 0, 0, 0};  // persistent eval grid per layout (+ [3] / [4] the adaptive-leaf evals)
+    int eval_blocks[10] = {};  // persistent eval grid per layout (+ [3] / [4] the adaptive-leaf evals; +5: peer-result kernels)
 };
 
 namespace p2p {
