@@ -222,14 +222,14 @@ __global__ void k_boxinfo(const uint32_t *__restrict__ bkey, const uint32_t *__r
 //                entry are loaded together, branch-free (a stale entry of an empty key is ignored).  Per-box
 //                totals -> block sums per tile (CSR entries, redundant records, work items, small-target pairs)
 //                + the pair count I.
+//   k_tile_scan  exclusive prefixes of the tile sums (chunks of 1024 tiles per CTA + the chunk totals)
 //   k_nbr_fill   the box's occupied-slot mask and record count (saved by k_nbr_count), block scan of the per-box
-//                totals + the tile's exclusive prefix from a
-//                look-back over the (already complete) tile sums that never waits, then nbr_off / red_off, the CSR
-//                staged in shared memory and written coalesced, the restructure chunk heads, the eval work items
-//                or small-target entries.
+//                totals + the tile's exclusive prefix (k_tile_scan), then nbr_off / red_off, the CSR staged in
+//                shared memory and written coalesced, the restructure chunk heads, the eval work items or
+//                small-target entries.
 // Lanes are consecutive boxes, so a slot's 32 neighbour keys are close in key order (coalesced table reads),
 // and no tile ever waits for another: the earlier single-kernel design (warp per 32 boxes, lane = slot, decoupled
-// look-back on tiles still searching) spent about half of its 1.06 ms there; this pair takes ~0.55 ms on c5w.
+// look-back on tiles still searching) spent about half of its 1.06 ms there; these take 0.14 + 0.006 + 0.25 ms on c5w.
 constexpr int NB_THREADS = 256;
 constexpr int NB_SLOTS = 27;
 
@@ -451,62 +451,52 @@ __global__ void __launch_bounds__(NB_THREADS) k_mb_tiles(const uint32_t *__restr
     }
 }
 
-// exclusive prefix of the tile sums before `tile`, by a look-back that never waits: every tile sum (k_nbr_count) is
-// already complete, so the block walks back NB_THREADS tiles per step, adding sums, until it meets a tile whose
-// inclusive prefix a previous k_nbr_fill block has published (or tile 0).  Tiles are processed in near launch
-// order, so the walk is one or two steps.  Published: incl[t] = prefix + sum of tile t, then the flag (release).
-__device__ __forceinline__ unsigned long long ld_acquire_u32(const unsigned int *p) {
-    unsigned int v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned int *p, unsigned int v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ NbTile tile_prefix(uint32_t tile, const NbTile *__restrict__ sums, const NbTile *incl,
-                              const unsigned int *flags) {
-    __shared__ unsigned long long s_r[NB_THREADS / 32][NB_TOT];
-    __shared__ int s_stop[NB_THREADS / 32];
+// exclusive prefix of the per-256-box tile sums (k_nbr_count / k_mb_tiles) for k_nbr_fill: CTA c scans tiles
+// 1024 c .. 1024 c + 1023 (in-chunk exclusive prefixes) and writes the chunk's total; the fill adds the totals of
+// the earlier chunks (<= 11 on c5w).  The fill used to resolve its prefix itself by a look-back over the tile sums
+// (ld.acquire + 3 barriers + a 5-value block reduction per tile): c5w fill 305 -> 237 us
+constexpr int TS_THREADS = 1024;
+__global__ void __launch_bounds__(TS_THREADS) k_tile_scan(const NbTile *__restrict__ sums, NbTile *__restrict__ excl,
+                                                        NbTile *__restrict__ ctot, const DevCounters *ctr) {
+    __shared__ unsigned long long s_w[TS_THREADS / 32][NB_TOT];
+    const uint32_t ntiles = (ctr->B + NB_THREADS - 1) / NB_THREADS;
+    const uint32_t t0 = blockIdx.x * TS_THREADS;
+    if (t0 >= ntiles) return;
     const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
-    unsigned long long acc[NB_TOT] = {0ull, 0ull, 0ull, 0ull, 0ull};
-    for (int64_t base = (int64_t)tile - 1; base >= 0; base -= NB_THREADS) {
-        const int64_t q = base - (int64_t)t;
-        const bool inc = q < 0 || ld_acquire_u32(&flags[q]) != 0u;  // tiles before 0: an inclusive zero
-        const unsigned bal = __ballot_sync(0xffffffffu, inc);
-        if (lane == 0) s_stop[w] = bal ? (int)(w * 32 + __ffs(bal) - 1) : NB_THREADS;
-        __syncthreads();
-        int stop = NB_THREADS;
+    const uint32_t q = t0 + t;
+    unsigned long long v[NB_TOT], x[NB_TOT];
+    const NbTile sv = q < ntiles ? sums[q] : NbTile{{0ull, 0ull, 0ull, 0ull, 0ull}};
 #pragma unroll
-        for (int i = 0; i < NB_THREADS / 32; ++i) stop = min(stop, s_stop[i]);
-        __syncthreads();
-        if ((int)t < stop) {
-            const NbTile v = sums[q];
+    for (int k = 0; k < NB_TOT; ++k) {
+        v[k] = sv.v[k];
+        x[k] = v[k];
 #pragma unroll
-            for (int k = 0; k < NB_TOT; ++k) acc[k] += v.v[k];
-        } else if ((int)t == stop && q >= 0) {
-#pragma unroll
-            for (int k = 0; k < NB_TOT; ++k) acc[k] += __ldcg(&incl[q].v[k]);
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x[k], o);
+            if (lane >= (unsigned)o) x[k] += y;
         }
-        if (stop < NB_THREADS) break;
-    }
-    // block sum
-#pragma unroll
-    for (int k = 0; k < NB_TOT; ++k) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-        if (lane == 0) s_r[w][k] = acc[k];
+        if (lane == 31) s_w[w][k] = x[k];
     }
     __syncthreads();
-    NbTile r;
+    if (w == 0) {  // warp 0: exclusive scan of the 32 warp totals (per value), the chunk total
 #pragma unroll
-    for (int k = 0; k < NB_TOT; ++k) {
-        unsigned long long x = 0;
+        for (int k = 0; k < NB_TOT; ++k) {
+            const unsigned long long y0 = s_w[lane][k];
+            unsigned long long y = y0;
 #pragma unroll
-        for (int i = 0; i < NB_THREADS / 32; ++i) x += s_r[i][k];
-        r.v[k] = x;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= (unsigned)o) y += z;
+            }
+            if (lane == 31) ctot[blockIdx.x].v[k] = y;
+            s_w[lane][k] = y - y0;
+        }
     }
     __syncthreads();
-    return r;
+    NbTile e;
+#pragma unroll
+    for (int k = 0; k < NB_TOT; ++k) e.v[k] = x[k] - v[k] + s_w[w][k];
+    if (q < ntiles) excl[q] = e;
 }
 
 #ifndef P2P_NB_MINB
@@ -517,8 +507,8 @@ __device__ NbTile tile_prefix(uint32_t tile, const NbTile *__restrict__ sums, co
 #endif
 __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
     Geom g, const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart, const uint2 *__restrict__ boxinfo,
-    const uint2 *__restrict__ box_nbr, DevCounters *ctr, const NbTile *__restrict__ tiles, NbTile *incl,
-    unsigned int *flags, uint32_t *__restrict__ nbr_off, unsigned long long *__restrict__ red_off, uint32_t *__restrict__ nbr_box,
+    const uint2 *__restrict__ box_nbr, DevCounters *ctr, const NbTile *__restrict__ incl,
+    const NbTile *__restrict__ ctot, uint32_t *__restrict__ nbr_off, unsigned long long *__restrict__ red_off, uint32_t *__restrict__ nbr_box,
     uint8_t *__restrict__ nbr_slot, Item *__restrict__ items, uint32_t *__restrict__ small_tgt,
     uint32_t *__restrict__ small_box, uint32_t *__restrict__ chunk_box, unsigned long long *__restrict__ chunk_out,
     uint32_t K, uint32_t tmax, Item *__restrict__ items_red, const uint32_t *__restrict__ mb_cen) {
@@ -546,28 +536,20 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
         if (role == 2) x.item_red = 0u;
         BoxTotals tot;
         const BoxTotals inc = block_scan_totals(x, &tot);
-        const NbTile to = tile_prefix(tile, tiles, incl, flags);
-        if (threadIdx.x == 0) {  // publish this tile's inclusive prefix
-            NbTile in;
+        NbTile to = incl[tile];  // exclusive prefix inside the tile's chunk (k_tile_scan) + the earlier chunks
+        for (uint32_t c = 0; c < tile / TS_THREADS; ++c) {
 #pragma unroll
-            for (int k = 0; k < NB_TOT; ++k) in.v[k] = to.v[k];
-            in.v[0] += tot.nbr;
-            in.v[1] += tot.red;
-            in.v[2] += tot.item;
-            in.v[3] += tot.small;
-            in.v[4] += tot.item_red;
-#pragma unroll
-            for (int k = 0; k < NB_TOT; ++k) __stcg(&incl[tile].v[k], in.v[k]);
-            st_release_u32(&flags[tile], 1u);
-            if (tile == ntiles - 1) {  // the last tile closes the offsets and publishes the totals
-                nbr_off[B] = (uint32_t)in.v[0];
-                red_off[B] = in.v[1];
-                ctr->n_nbr = (uint32_t)in.v[0];
-                ctr->R = in.v[1];
-                ctr->n_items = (uint32_t)in.v[2];
-                ctr->n_small = (uint32_t)in.v[3];
-                ctr->n_items_red = (uint32_t)in.v[4];
-            }
+            for (int k = 0; k < NB_TOT; ++k) to.v[k] += ctot[c].v[k];
+        }
+        if (threadIdx.x == 0 && tile == ntiles - 1) {  // the last tile closes the offsets and publishes the totals
+            const unsigned long long t0 = to.v[0] + tot.nbr, t1 = to.v[1] + tot.red;
+            nbr_off[B] = (uint32_t)t0;
+            red_off[B] = t1;
+            ctr->n_nbr = (uint32_t)t0;
+            ctr->R = t1;
+            ctr->n_items = (uint32_t)(to.v[2] + tot.item);
+            ctr->n_small = (uint32_t)(to.v[3] + tot.small);
+            ctr->n_items_red = (uint32_t)(to.v[4] + tot.item_red);
         }
         const uint32_t e_loc = inc.nbr - x.nbr;  // block-relative CSR offset
         const uint32_t e0 = (uint32_t)to.v[0] + e_loc;
@@ -762,7 +744,8 @@ p2p_status alloc_capacity(p2p_plan *P, int64_t cap) {
         P2P_CUDA_TRY(dalloc(&P->rec, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
         P2P_CUDA_TRY(dalloc(&P->s_aos, (f64 ? sizeof(double4) : sizeof(float4)) * n, st));
         P2P_CUDA_TRY(dalloc((void **)&P->s_box_nbr, sizeof(uint2) * bcap, st));
-        P2P_CUDA_TRY(dalloc(&P->s_nb_tiles, (2 * sizeof(NbTile) + 4) * div_up(bcap, NB_THREADS), st));
+        const uint64_t ntc = div_up(bcap, NB_THREADS);  // tile sums, exclusive prefixes, per-1024-tile chunk totals
+        P2P_CUDA_TRY(dalloc(&P->s_nb_tiles, sizeof(NbTile) * (2 * ntc + div_up(ntc, 1024) + 1), st));
         P2P_CUDA_TRY(dalloc((void **)&P->boxinfo, sizeof(uint2) * keyspace, st));
         // defined contents once per allocation: nb_plane's branch-free lookups load (and then mask) the entry of
         // keys whose occupancy bit is clear; entries are never cleared afterwards (stale ones are masked too)
@@ -837,9 +820,7 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     const unsigned nbg = std::max<unsigned>(1, std::min<unsigned>(div_up(bcap, NB_THREADS), (unsigned)P->num_sms * 8));
     const uint64_t ntile_cap = div_up(bcap, NB_THREADS);
     NbTile *tiles = (NbTile *)P->s_nb_tiles;            // [ntile_cap] sums, then [ntile_cap] inclusive prefixes
-    NbTile *incl = tiles + ntile_cap;
-    unsigned int *flags = (unsigned int *)(incl + ntile_cap);
-    P2P_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * ntile_cap, st));
+    NbTile *incl = tiles + ntile_cap;  // exclusive tile prefixes (k_tile_scan)
     P2P_LAUNCH(k_nbr_count, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->occ, P->ctr, tiles,
                P->s_box_nbr, (uint32_t)ITEM_TMAX, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32), P->items_red != nullptr,
                P->s_mb_cen);
@@ -850,8 +831,11 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
         P2P_CUDA_TRY(cudaFuncSetAttribute(k_nbr_fill, cudaFuncAttributePreferredSharedMemoryCarveout, P2P_NB_CARVEOUT));
         carveout_set = true;
     }
-    P2P_LAUNCH(k_nbr_fill, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->s_box_nbr, P->ctr, tiles,
-               incl, flags, P->nbr_off, (unsigned long long *)P->red_off, P->nbr_box, P->nbr_slot, P->items,
+    NbTile *ctot = incl + ntile_cap;  // per 1024-tile chunk totals (fits the s_nb_tiles tail: 4 B per tile)
+    P2P_LAUNCH(k_tile_scan, (unsigned)std::max<uint64_t>(1, div_up(ntile_cap, TS_THREADS)), TS_THREADS, 0, st, tiles,
+               incl, ctot, P->ctr);
+    P2P_LAUNCH(k_nbr_fill, nbg, NB_THREADS, 0, st, P->geom, P->bkey, P->bstart, P->boxinfo, P->s_box_nbr, P->ctr,
+               incl, ctot, P->nbr_off, (unsigned long long *)P->red_off, P->nbr_box, P->nbr_slot, P->items,
                P->small_tgt, P->small_box, P->chunk_box, P->chunk_out, (uint32_t)(f64 ? EVAL_K_F64 : EVAL_K_F32),
                (uint32_t)ITEM_TMAX, P->items_red, P->s_mb_cen);
     P2P_CUDA_TRY(cudaGetLastError());
