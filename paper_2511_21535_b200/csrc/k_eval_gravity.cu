@@ -353,6 +353,26 @@ __device__ __forceinline__ void hot_loop(TG &tg, uint32_t sa, uint32_t nj, const
 #pragma unroll 1
     for (uint32_t r = nj & 3u; r; --r, sa += ST) tg.interact(lds_rec<float4>(sa), E);
 }
+// the same loop with the split stride in a register (one loop body for every S): the S-specialised copies are 7 x
+// 2 KB of hot code, and when a CTA's warps run different S the instruction cache misses (c3 ncu: 13% of the stall
+// samples "no instruction"); this costs 3 more ALU adds per 4 sources on the otherwise FMA-bound loop
+template <int K, typename TG, typename EP>
+__device__ __forceinline__ void hot_loop_rt4(TG &tg, uint32_t sa, uint32_t nj, uint32_t stride, const EP &E) {
+    uint32_t a1 = sa + stride, a2 = sa + 2 * stride, a3 = sa + 3 * stride;
+    const uint32_t st4 = 4 * stride;
+    const uint32_t end4 = sa + (nj & ~3u) * stride;
+#pragma unroll 1
+    for (; sa != end4; sa += st4, a1 += st4, a2 += st4, a3 += st4) {
+        const float4 s0 = lds_rec<float4>(sa), s1 = lds_rec<float4>(a1), s2 = lds_rec<float4>(a2),
+                     s3 = lds_rec<float4>(a3);
+        tg.interact(s0, E);
+        tg.interact(s1, E);
+        tg.interact(s2, E);
+        tg.interact(s3, E);
+    }
+#pragma unroll 1
+    for (uint32_t r = nj & 3u; r; --r, sa += stride) tg.interact(lds_rec<float4>(sa), E);
+}
 template <typename T, int K, typename TG, typename EP>
 __device__ __forceinline__ void hot_loop_rt(TG &tg, uint32_t sa, uint32_t nj, uint32_t stride, const EP &E) {
     using V4 = typename V4T<T>::type;
@@ -867,6 +887,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                 // the split stride S as a compile-time constant: the second source of an iteration is an
                 // immediate-offset LDS and the pointer advances once per two sources
                 if constexpr (sizeof(T) == 4) {
+#ifdef P2P_EV_HOT_RT
+                    hot_loop_rt4<K>(tg, sa, nj, S * 16u, E);
+#else
                     switch (S) {
                     case 32: hot_loop<T, K, 32>(tg, sa, nj, E); break;
                     case 16: hot_loop<T, K, 16>(tg, sa, nj, E); break;
@@ -876,6 +899,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : 
                     case 5: hot_loop<T, K, 5>(tg, sa, nj, E); break;
                     default: hot_loop<T, K, 4>(tg, sa, nj, E); break;  // S >= 4 always (G <= 8)
                     }
+#endif
                 } else {
                     hot_loop_rt<T, K>(tg, sa, nj, S * (uint32_t)sizeof(V4), E);
                 }
