@@ -30,6 +30,10 @@ ncu --set full --import-source on --clock-control none -k regex:"k_helm_tc" -c 2
     -o $O/full_helm_tc python scripts/helm_prof.py c2b > $O/ncu_helm.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ncu_launches_bench.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_under_ncu.log 2>&1
-SAN_TIMEOUT=500 bash scripts/sanitize.sh > $O/sanitize_run.txt 2>&1
-cp -r gpurun_out/sanitize $O/
+# compute-sanitizer: closed on the GPU pool since late round 2 (runs refused); profiles/r02_sanitize_summary.txt is
+# the earlier clean run -- re-enable with RUN_SANITIZE=1 where the tool is available
+if [ "${RUN_SANITIZE:-0}" = 1 ]; then
+  SAN_TIMEOUT=500 bash scripts/sanitize.sh > $O/sanitize_run.txt 2>&1
+  cp -r gpurun_out/sanitize $O/
+fi
 echo done
