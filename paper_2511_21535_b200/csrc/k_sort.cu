@@ -18,9 +18,21 @@
 namespace p2p {
 
 namespace {
-constexpr int RS_THREADS = 256;
+#ifndef P2P_RS_THREADS
+#define P2P_RS_THREADS 256
+#endif
+#ifndef P2P_RS_ITEMS
+#define P2P_RS_ITEMS 16
+#endif
+#ifndef P2P_RS_MINB
+#define P2P_RS_MINB 3
+#endif
+#ifndef P2P_RS_LB
+#define P2P_RS_LB 8
+#endif
+constexpr int RS_THREADS = P2P_RS_THREADS;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 16;
+constexpr int RS_ITEMS = P2P_RS_ITEMS;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys per tile
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_INC = 2u << 30;
@@ -101,7 +113,7 @@ __device__ __forceinline__ void st_volatile(uint32_t *p, uint32_t v) {
 }
 
 // 3 resident CTAs per SM (<= 85 registers): measured 377 us per c5w sort vs 438 at 2 CTAs and 390 at 4 (spills)
-__global__ void __launch_bounds__(RS_THREADS, 3) k_radix_pass(const uint32_t *__restrict__ kin,
+__global__ void __launch_bounds__(RS_THREADS, P2P_RS_MINB) k_radix_pass(const uint32_t *__restrict__ kin,
                                                            const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
                                                            uint32_t *__restrict__ vout, uint32_t n, int shift,
                                                            const uint32_t *__restrict__ digit_off,
@@ -109,8 +121,8 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_radix_pass(const uint32_t *__
     __shared__ uint32_t s_whist[RS_WARPS][256];
     __shared__ uint32_t s_tdig[256];
     __shared__ uint32_t s_goff[256];
-    __shared__ uint32_t s_keys[RS_TILE];
-    __shared__ uint32_t s_vals[RS_TILE];
+    extern __shared__ uint32_t s_dyn[];  // the tile staged in digit order: keys, then values (dynamic: > 48 KB tiles)
+    uint32_t *s_keys = s_dyn, *s_vals = s_dyn + RS_TILE;
     __shared__ uint32_t s_wt[RS_WARPS];
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_thist[256];
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_radix_pass(const uint32_t *__
             // walk back LB predecessors per step (independent loads in flight; tile 0 is always inclusive, so
             // the walk never passes it): a chain of one dependent load per predecessor made the look-back the
             // pass's critical path
-            constexpr int LB = 8;
+            constexpr int LB = P2P_RS_LB;
             for (int64_t t = (int64_t)tile - 1;;) {
                 uint32_t sv[LB];
 #pragma unroll
@@ -261,9 +273,14 @@ cudaError_t radix_sort_pairs(uint32_t *kin, uint32_t *vin, uint32_t *kalt, uint3
         P2P_LAUNCH(k_radix_hist, hg, 256, 0, st, kin, n, passes, hist);
     }
     P2P_LAUNCH(k_radix_hist_scan, passes, 256, 0, st, hist);
+    static bool smem_set = false;
+    if (!smem_set) {  // static (12 KB) + dynamic staging may exceed the 48 KB default
+        cudaFuncSetAttribute(k_radix_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * RS_TILE);
+        smem_set = true;
+    }
     uint32_t *a_k = kin, *a_v = vin, *b_k = kalt, *b_v = valt;
     for (int p = 0; p < passes; ++p) {
-        P2P_LAUNCH(k_radix_pass, ntiles, RS_THREADS, 0, st, a_k, a_v, b_k, b_v, n, 8 * p, hist + 256 * p,
+        P2P_LAUNCH(k_radix_pass, ntiles, RS_THREADS, 8 * RS_TILE, st, a_k, a_v, b_k, b_v, n, 8 * p, hist + 256 * p,
                    status + (size_t)p * ntiles * 256, &ctr->sort_tile_ctr[p], iota_values && p == 0);
         std::swap(a_k, b_k);
         std::swap(a_v, b_v);
