@@ -200,15 +200,34 @@ struct HeadPut {
 // ------------------------------------------------------------------------------------------------ a5
 // dense key -> {box, n_b} table for the gravity neighbour search (valid where the occupancy bit is set)
 // + sum over the target boxes of n_b^2 (the item cost cap's work estimate; integer atomics: order-independent)
+// + the occupancy bitmap: lanes are consecutive boxes (ascending keys), so the lanes sharing a 32-key occupancy word
+// are contiguous; a segmented OR over them leaves ONE atomicOr per word and warp (the run-head scan's per-box
+// atomicOr serialised on the shared words)
 __global__ void k_boxinfo(const uint32_t *__restrict__ bkey, const uint32_t *__restrict__ bstart,
-                          DevCounters *__restrict__ ctr, uint2 *__restrict__ boxinfo, uint32_t tkey_lo,
-                          uint32_t tkey_hi) {
+                          DevCounters *__restrict__ ctr, uint2 *__restrict__ boxinfo, uint32_t *__restrict__ occ,
+                          uint32_t tkey_lo, uint32_t tkey_hi) {
     const uint32_t B = ctr->B;
+    const unsigned lane = threadIdx.x & 31u;
     unsigned long long s2 = 0;
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
-        const uint32_t key = bkey[b], nb = bstart[b + 1] - bstart[b];
-        boxinfo[key] = make_uint2(b, nb);
-        if (key >= tkey_lo && key <= tkey_hi) s2 += (unsigned long long)nb * nb;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < B; b0 += stride) {  // warp-uniform trip count
+        const uint32_t b = b0 + threadIdx.x;
+        const bool have = b < B;
+        const uint32_t key = have ? bkey[b] : 0xffffffffu;
+        if (have) {
+            const uint32_t nb = bstart[b + 1] - bstart[b];
+            boxinfo[key] = make_uint2(b, nb);
+            if (key >= tkey_lo && key <= tkey_hi) s2 += (unsigned long long)nb * nb;
+        }
+        const uint32_t wd = key >> 5;
+        uint32_t bits = have ? 1u << (key & 31u) : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ob = __shfl_down_sync(0xffffffffu, bits, o), ow = __shfl_down_sync(0xffffffffu, wd, o);
+            if (lane + o < 32u && ow == wd) bits |= ob;
+        }
+        const uint32_t pw = __shfl_up_sync(0xffffffffu, wd, 1);
+        if (have && (lane == 0u || pw != wd)) atomicOr(&occ[wd], bits);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
@@ -805,14 +824,14 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     // (a single-pass look-back variant, scan.cuh device_scan_lb, measured 124 vs 99 us on c5w: the 3052 tiles'
     // walks back over unpublished prefixes cost more than the second read of the keys)
     P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet1{P->skey},
-                                       HeadPut{P->skey, 1u, P->bkey, P->bstart, nullptr, n, P->occ}, nullptr, n,
+                                       HeadPut{P->skey, 1u, P->bkey, P->bstart, nullptr, n}, nullptr, n,
                                        &P->ctr->B, P->s_partials, st));
     if (!grid_a5) return cudaGetLastError() == cudaSuccess ? P2P_OK : P2P_ERR_CUDA;  // adaptive mode: its own a5
     // a5
     const uint64_t bcap = (uint64_t)P->bcap;
     P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->sum_nb2, 0, sizeof(unsigned long long), st));
     P2P_LAUNCH(k_boxinfo, std::max<unsigned>(1, std::min<unsigned>(div_up(bcap, 256), (unsigned)P->num_sms * 8)), 256,
-               0, st, P->bkey, P->bstart, P->ctr, P->boxinfo, P->geom.tkey_lo, P->geom.tkey_hi);
+               0, st, P->bkey, P->bstart, P->ctr, P->boxinfo, P->occ, P->geom.tkey_lo, P->geom.tkey_hi);
     if (P->comm) {  // the cap's work estimate over ALL ranks' target boxes (= the 1-GPU value)
         p2p_status cs = P->comm->allreduce_sum_u64(&P->ctr->sum_nb2, 1, st);
         if (cs != P2P_OK) return cs;
