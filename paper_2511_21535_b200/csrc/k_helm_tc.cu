@@ -74,6 +74,29 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
+// the same 2D load delivered to every CTA of `mask` in the cluster (same shared offset, each CTA's own mbarrier)
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar,
+                                               uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                     "r"(bar), "h"(mask)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
     asm volatile(
@@ -138,13 +161,23 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 
-template <int T, bool GATHER = false>
+// NSPLIT = 2 (t = 64, P2P_HELM_NSPLIT): the N = 2t outputs of a 128-box tile are split over two CTAs (half 0: the
+// Re y columns, 1: the Im y columns; each loads X and its half of W; the two are adjacent in launch order, so the
+// second X read hits L2): 1024 units of work instead of 512, so the last of the 148-SM waves is nearly full (512
+// tiles were 3.46 waves of one CTA per SM: 13.5% idle)
+// CL > 1 (P2P_HELM_CLUSTER): clusters of CL CTAs share every W slice through TMA MULTICAST ("RF copies
+// of the pattern table ... as B200 cluster TMA multicast"): CTA r of the cluster loads rows [r N/CL, (r+1) N/CL) of
+// the W hi / lo slice into the same shared offset of all CL CTAs, so each W byte crosses L2 -> SM once per cluster
+// instead of once per CTA (W was 2/3 of the kernel's 48 KB per slice of TMA traffic).  A stage is refilled only
+// after all CL MMA issuers released it: their commits arrive on every CTA's `empty` barrier (multicast commit).
+template <int T, bool GATHER = false, int NSPLIT = 1, int CL = 1>
 __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
     k_helm_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWhi,
               const __grid_constant__ CUtensorMap tmWlo, uint32_t rf, const uint32_t *__restrict__ bstart,
               const uint32_t *__restrict__ perm, uint32_t B, float2 *__restrict__ y,
               const float *__restrict__ xs, const uint32_t *__restrict__ nbr9) {
-    constexpr int N = 2 * T, K = 18 * T, NKT = K / TC_BK;
+    constexpr int NF = 2 * T, N = NF / NSPLIT, K = 18 * T, NKT = K / TC_BK;  // NF: all outputs, N: this CTA's
+    static_assert(NSPLIT == 1 || (NSPLIT == 2 && T >= 32), "split into the Re / Im halves only");
     constexpr uint32_t X_BYTES = TC_BM * TC_BK * 4, W_BYTES = N * TC_BK * 4;
     constexpr uint32_t STAGE_BYTES = X_BYTES + 2 * W_BYTES;  // X (raw fp32), W hi, W lo
     constexpr uint32_t AST = N < 32 ? 32 : N;                 // TMEM columns per accumulator
@@ -166,11 +199,12 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
     unsigned char *ring_gen = smem_raw + (ring - cvta_smem(smem_raw));
 
     const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-    const uint32_t m0 = blockIdx.x * TC_BM;
+    const uint32_t half = NSPLIT == 2 ? (blockIdx.x & 1u) : 0u, tile = NSPLIT == 2 ? (blockIdx.x >> 1) : blockIdx.x;
+    const uint32_t m0 = tile * TC_BM;
     if (tid == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], CL);  // one commit from each MMA issuer of the cluster
         }
         for (int a = 0; a < ASTAGES; ++a) {
             mbar_init(&tsplit[a], 128);
@@ -187,8 +221,11 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync();  // every CTA's barriers initialised before any multicast lands
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_base;
+    const uint32_t crank = CL > 1 ? cluster_rank() : 0u;
+    constexpr uint16_t CMASK = (uint16_t)((1u << CL) - 1u);
 
     if (warp == 4) {
         // ---------------- TMA producer ----------------
@@ -200,9 +237,19 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
                 mbar_arrive_expect_tx(&full[s], GATHER ? 2 * W_BYTES : STAGE_BYTES);
                 if (!GATHER) tma_load_2d(st, &tmX, kt * TC_BK, (int)m0, cvta_smem(&full[s]));
                 // block-level redundancy (RF copies of the pattern table): CTA b reads copy b mod RF
-                const int wrow = (int)((blockIdx.x % rf) * N);
-                tma_load_2d(st + X_BYTES, &tmWhi, kt * TC_BK, wrow, cvta_smem(&full[s]));
-                tma_load_2d(st + X_BYTES + W_BYTES, &tmWlo, kt * TC_BK, wrow, cvta_smem(&full[s]));
+                // (clusters: the cluster's index mod RF -- its CTAs share one copy)
+                const int wrow = (int)(((CL > 1 ? tile / CL : tile) % rf) * NF + half * N);
+                if constexpr (CL > 1) {
+                    constexpr int RP = N / CL;  // W rows this CTA multicasts (a multiple of 8: whole swizzle atoms)
+                    const uint32_t off = crank * RP * (TC_BK * 4);
+                    tma_load_2d_mc(st + X_BYTES + off, &tmWhi, kt * TC_BK, wrow + (int)(crank * RP),
+                                   cvta_smem(&full[s]), CMASK);
+                    tma_load_2d_mc(st + X_BYTES + W_BYTES + off, &tmWlo, kt * TC_BK, wrow + (int)(crank * RP),
+                                   cvta_smem(&full[s]), CMASK);
+                } else {
+                    tma_load_2d(st + X_BYTES, &tmWhi, kt * TC_BK, wrow, cvta_smem(&full[s]));
+                    tma_load_2d(st + X_BYTES + W_BYTES, &tmWlo, kt * TC_BK, wrow, cvta_smem(&full[s]));
+                }
             }
         }
     } else if (warp == 5) {
@@ -224,7 +271,10 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
                     mma_tf32_ts(d, a_hi + 8 * k, sdesc_sw128(b_lo + 32 * k), IDESC, 1u);
                     mma_tf32_ts(d, a_lo + 8 * k, sdesc_sw128(b_hi + 32 * k), IDESC, 1u);
                 }
-                mma_commit(cvta_smem(&empty[s]));  // W of smem stage s consumed
+                if constexpr (CL > 1)
+                    mma_commit_mc(cvta_smem(&empty[s]), CMASK);  // stage s consumed: tell every producer of the cluster
+                else
+                    mma_commit(cvta_smem(&empty[s]));  // W of smem stage s consumed
                 mma_commit(cvta_smem(&tfree[a]));  // X hi / lo of TMEM stage a consumed
             }
             mma_commit(cvta_smem(&accum));
@@ -304,6 +354,24 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
 #pragma unroll
                 for (int i = 0; i < T; ++i) y[perm[s0 + i]] = make_float2(v[i], v[T + i]);
             }
+        } else if constexpr (NSPLIT == 2) {  // this CTA's half: Re (half 0) or Im (1) of outputs 0 .. t-1
+            float *yf = reinterpret_cast<float *>(y) + half;
+#pragma unroll
+            for (int c0 = 0; c0 < T; c0 += 32) {
+                float v[32];
+                tmem_ld32(lane_addr + c0, v);
+#pragma unroll
+                for (int ac = 1; ac < NACC; ++ac) {
+                    float w[32];
+                    tmem_ld32(lane_addr + ac * AST + c0, w);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] += w[i];
+                }
+                if (b < B) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) yf[2 * (size_t)perm[s0 + c0 + i]] = v[i];
+                }
+            }
         } else {
 #pragma unroll
             for (int c0 = 0; c0 < T; c0 += 32) {  // outputs c0 .. c0 + 31
@@ -329,6 +397,7 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     }
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync();  // no CTA exits while a cluster peer may still multicast into it
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
@@ -365,23 +434,45 @@ bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, ui
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int T, bool GATHER>
+template <int T, bool GATHER, int NSPLIT = 1, int CL = 1>
 p2p_status launch_tc(p2p_plan *P, void *y) {
-    constexpr int N = 2 * T, K = 18 * T;
-    constexpr uint32_t STAGE_BYTES = TC_BM * TC_BK * 4 + 2 * N * TC_BK * 4;
+    constexpr int N = 2 * T, K = 18 * T, NC = N / NSPLIT;
+    constexpr uint32_t STAGE_BYTES = TC_BM * TC_BK * 4 + 2 * NC * TC_BK * 4;
     const int smem = (int)(TC_STAGES * STAGE_BYTES + 1024);
     CUtensorMap mx, mwh, mwl;
     const float *W = (const float *)P->tc_table;  // [RF] copies of W hi, then [RF] copies of W lo
     const uint32_t rf = (uint32_t)P->tc_rf;
     if (!make_map(&mx, GATHER ? (const void *)W : P->red, GATHER ? (uint64_t)rf * N : (uint64_t)P->B, K,
-                  GATHER ? N : TC_BM) || !make_map(&mwh, W, (uint64_t)rf * N, K, N) ||
-        !make_map(&mwl, W + (size_t)rf * N * K, (uint64_t)rf * N, K, N)) {
+                  GATHER ? NC : TC_BM) || !make_map(&mwh, W, (uint64_t)rf * N, K, NC / CL) ||
+        !make_map(&mwl, W + (size_t)rf * N * K, (uint64_t)rf * N, K, NC / CL)) {
         set_error("cuTensorMapEncodeTiled unavailable or rejected the Helmholtz operands");
         return P2P_ERR_CUDA;
     }
-    P2P_CUDA_TRY(cudaFuncSetAttribute(k_helm_tc<T, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    P2P_LAUNCH((k_helm_tc<T, GATHER>), div_up((uint64_t)P->B, TC_BM), TC_THREADS, smem, P->stream, mx, mwh, mwl, rf,
-               P->bstart, P->perm, (uint32_t)P->B, (float2 *)y, (const float *)P->rec, P->nbr_box);
+    auto kern = k_helm_tc<T, GATHER, NSPLIT, CL>;
+    P2P_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const unsigned tiles = (unsigned)div_up((uint64_t)P->B, TC_BM);
+    const unsigned grid = div_up(tiles, CL) * CL * NSPLIT;  // whole clusters (CTAs past B load zeros, store nothing)
+    if constexpr (CL > 1) {
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(TC_THREADS);
+        lc.dynamicSmemBytes = (size_t)smem;
+        lc.stream = P->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        P2P_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, mx, mwh, mwl, rf, (const uint32_t *)P->bstart,
+                                        (const uint32_t *)P->perm, (uint32_t)P->B, (float2 *)y,
+                                        (const float *)P->rec, (const uint32_t *)P->nbr_box));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    } else {
+        P2P_LAUNCH(kern, grid, TC_THREADS, smem, P->stream, mx, mwh, mwl, rf, P->bstart, P->perm, (uint32_t)P->B,
+                   (float2 *)y, (const float *)P->rec, P->nbr_box);
+    }
     P2P_CUDA_TRY(cudaGetLastError());
     return P2P_OK;
 }
@@ -429,8 +520,26 @@ p2p_status helmholtz_tc_table(p2p_plan *P, const float *Pf /* host, [t][9t] comp
 
 p2p_status eval_helmholtz_tc(p2p_plan *P, void *y, bool gather) {
     if (P->B == 0) return P2P_OK;
-    if (gather) return P->cfg.points_per_box == 16 ? launch_tc<16, true>(P, y) : launch_tc<64, true>(P, y);
-    return P->cfg.points_per_box == 16 ? launch_tc<16, false>(P, y) : launch_tc<64, false>(P, y);
+    // measured options (profiles/r02_helm_tc_variants.txt), both bit-identical to the default and slower on B200:
+    //   P2P_HELM_NSPLIT=2     t = 64 outputs split over two CTAs per 128-box tile (better wave fill, 2x the X split)
+    //   P2P_HELM_CLUSTER=2|4  W slices multicast over clusters of 2 / 4 CTAs (W's L2 -> SM traffic / CL)
+    static int nsplit = -1, cl = -1;
+    if (nsplit < 0) {
+        const char *e = getenv("P2P_HELM_NSPLIT");
+        nsplit = (e && atoi(e) == 2) ? 2 : 1;
+        const char *c = getenv("P2P_HELM_CLUSTER");
+        cl = c ? atoi(c) : 1;
+        if (cl != 1 && cl != 2 && cl != 4) cl = 1;
+    }
+    if (P->cfg.points_per_box == 16) {
+        if (cl == 4) return gather ? launch_tc<16, true, 1, 4>(P, y) : launch_tc<16, false, 1, 4>(P, y);
+        if (cl == 2) return gather ? launch_tc<16, true, 1, 2>(P, y) : launch_tc<16, false, 1, 2>(P, y);
+        return gather ? launch_tc<16, true>(P, y) : launch_tc<16, false>(P, y);
+    }
+    if (nsplit == 2) return gather ? launch_tc<64, true, 2>(P, y) : launch_tc<64, false, 2>(P, y);
+    if (cl == 4) return gather ? launch_tc<64, true, 1, 4>(P, y) : launch_tc<64, false, 1, 4>(P, y);
+    if (cl == 2) return gather ? launch_tc<64, true, 1, 2>(P, y) : launch_tc<64, false, 1, 2>(P, y);
+    return gather ? launch_tc<64, true>(P, y) : launch_tc<64, false>(P, y);
 }
 
 }  // namespace p2p
