@@ -523,14 +523,11 @@ p2p_status eval_helmholtz_tc(p2p_plan *P, void *y, bool gather) {
     // measured options (profiles/r02_helm_tc_variants.txt), both bit-identical to the default and slower on B200:
     //   P2P_HELM_NSPLIT=2     t = 64 outputs split over two CTAs per 128-box tile (better wave fill, 2x the X split)
     //   P2P_HELM_CLUSTER=2|4  W slices multicast over clusters of 2 / 4 CTAs (W's L2 -> SM traffic / CL)
-    static int nsplit = -1, cl = -1;
-    if (nsplit < 0) {
-        const char *e = getenv("P2P_HELM_NSPLIT");
-        nsplit = (e && atoi(e) == 2) ? 2 : 1;
-        const char *c = getenv("P2P_HELM_CLUSTER");
-        cl = c ? atoi(c) : 1;
-        if (cl != 1 && cl != 2 && cl != 4) cl = 1;
-    }
+    const char *e = getenv("P2P_HELM_NSPLIT");  // read per call (tests switch them within one process)
+    const int nsplit = (e && atoi(e) == 2) ? 2 : 1;
+    const char *c = getenv("P2P_HELM_CLUSTER");
+    int cl = c ? atoi(c) : 1;
+    if (cl != 1 && cl != 2 && cl != 4) cl = 1;
     if (P->cfg.points_per_box == 16) {
         if (cl == 4) return gather ? launch_tc<16, true, 1, 4>(P, y) : launch_tc<16, false, 1, 4>(P, y);
         if (cl == 2) return gather ? launch_tc<16, true, 1, 2>(P, y) : launch_tc<16, false, 1, 2>(P, y);

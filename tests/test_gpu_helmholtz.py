@@ -125,3 +125,29 @@ def test_rf_copies_bitwise_equal(P, monkeypatch):
             plan.restructure()
             out.append(plan.eval(P.P2P_REDUNDANT).cpu().numpy().tobytes())
     assert out[0] == out[1] == out[2]
+
+
+@pytest.mark.parametrize("t", [16, 64])
+def test_tc_multicast_and_split(P, monkeypatch, t):
+    """NEXT-2 on B200 clusters: the W operand multicast over clusters of 2 / 4 CTAs (TMA .multicast::cluster, multicast
+    tcgen05.commit) stages the same operands and issues the same MMA sequence, so it gives the default's bits; the
+    t = 64 output split over two CTAs accumulates its K slices over 6 instead of 3 TMEM accumulators (other rounding):
+    REDUNDANT == INDEXED bitwise within it and the oracle bound.  A ragged box count (not a multiple of the 128-box
+    tile, nor of the cluster) exercises the padding CTAs of the last cluster"""
+    h = G.dbim_lattice(21, t, seed=5)  # 441 boxes: 3.4 tiles
+    xr = torch.from_numpy(h.x.view(np.float32).reshape(-1, 2)).cuda()
+    pos = torch.from_numpy(h.pos).cuda()
+    out = {}
+    with P.Plan(P.P2P_HELMHOLTZ2D, pos, xr, h.h, h.lo, h.nbox, 0, k=h.k, t=h.t) as plan:
+        plan.restructure()
+        for cl, ns in [("1", "1"), ("2", "1"), ("4", "1")] + ([("1", "2"), ("2", "2")] if t == 64 else []):
+            monkeypatch.setenv("P2P_HELM_CLUSTER", cl)
+            monkeypatch.setenv("P2P_HELM_NSPLIT", ns)
+            for lay in ("redundant", "indexed"):
+                out[(cl, ns, lay)] = plan.eval(P.LAYOUTS[lay]).cpu().numpy()
+    for (cl, ns, lay), v in out.items():  # bitwise within each output split, for every cluster size and layout
+        assert v.tobytes() == out[("1", ns, "redundant")].tobytes(), (cl, ns, lay)
+    if t == 64:
+        ref = oracle.HelmholtzPlan(h).eval_table()
+        y = out[("1", "2", "redundant")]
+        assert bounds.close(y[:, 0] + 1j * y[:, 1], ref, 5e-6)
