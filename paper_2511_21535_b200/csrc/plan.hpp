@@ -23,6 +23,7 @@ struct DevCounters {
     unsigned int item_head;        // eval work queue head (reset before every eval)
     unsigned int sort_tile_ctr[4]; // onesweep tile counters, one per pass
     unsigned int scan_tile_ctr;    // single-pass box-table scan (scan.cuh k_scan_lb)
+    unsigned int rs_head;          // restructure chunk queue (P2P_RS_BATCH)
     unsigned int n_small;          // targets of small boxes (thread-per-target path of the eval)
     unsigned int small_head;       // eval small-target queue head (reset before every eval)
     unsigned int n_items_red;      // REDUNDANT-eval work items (items_red)
