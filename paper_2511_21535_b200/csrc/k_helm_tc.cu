@@ -43,6 +43,15 @@ constexpr int TC_BM = 128;        // boxes per CTA (MMA M, TMEM lanes)
 constexpr int TC_BK = 32;         // floats per K slice = one 128-byte swizzle row
 constexpr int TC_STAGES = 4;      // smem ring of X + W hi + W lo slices (48 KB each at t = 64)
 constexpr int TC_THREADS = 192;   // 4 split / epilogue warps + 1 TMA producer warp + 1 MMA issuer warp
+// split warps per CTA (P2P_HELM_SPLITW, t = 64): the X split into TF32 hi / lo (smem -> registers -> tcgen05.st) paces
+// the kernel, so at t = 64 (one CTA per SM) 8 warps split, two per TMEM lane quarter, 16 of a slice's 32 columns each
+#ifndef P2P_HELM_SPLITW
+#define P2P_HELM_SPLITW 8
+#endif
+template <int T>
+constexpr int tc_splitw() { return T == 64 ? P2P_HELM_SPLITW : 4; }
+template <int T>
+constexpr int tc_threads() { return 32 * (tc_splitw<T>() + 2); }
 // TMEM accumulators (K slices round-robin, summed in fp32 at the end): as many as fit the 512 TMEM columns, at
 // most 8 -- the tensor core's internal fp32 accumulation loses ~2^-23 of the running sum per step (measured: one
 // accumulator 7.8e-6, four 2.0e-6 relative L2 at t = 64 vs the fp64 oracle)
@@ -132,6 +141,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         : "memory");
 }
 
+// 16 consecutive 32-bit TMEM columns of this thread's lane <- registers
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -171,7 +190,7 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, 
 // instead of once per CTA (W was 2/3 of the kernel's 48 KB per slice of TMA traffic).  A stage is refilled only
 // after all CL MMA issuers released it: their commits arrive on every CTA's `empty` barrier (multicast commit).
 template <int T, bool GATHER = false, int NSPLIT = 1, int CL = 1>
-__global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
+__global__ void __launch_bounds__(tc_threads<T>(), T == 16 ? 2 : 1)
     k_helm_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWhi,
               const __grid_constant__ CUtensorMap tmWlo, uint32_t rf, const uint32_t *__restrict__ bstart,
               const uint32_t *__restrict__ perm, uint32_t B, float2 *__restrict__ y,
@@ -190,6 +209,9 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)(TC_BM >> 4) << 24);
     static_assert(K % TC_BK == 0 && N % 16 == 0 && N <= 256, "unsupported t");
+    constexpr int SW = tc_splitw<T>();           // split warps: 4 or 8 (two per TMEM lane quarter)
+    constexpr int NCH = 8 / (SW / 4);            // 16-byte chunks of a 128-byte row per split thread
+    static_assert(SW == 4 || SW == 8, "4 or 8 split warps");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], tsplit[8], tfree[8], accum;
@@ -207,7 +229,7 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
             mbar_init(&empty[s], CL);  // one commit from each MMA issuer of the cluster
         }
         for (int a = 0; a < ASTAGES; ++a) {
-            mbar_init(&tsplit[a], 128);
+            mbar_init(&tsplit[a], 32 * SW);
             mbar_init(&tfree[a], 1);
         }
         mbar_init(&accum, 1);
@@ -227,7 +249,7 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
     const uint32_t crank = CL > 1 ? cluster_rank() : 0u;
     constexpr uint16_t CMASK = (uint16_t)((1u << CL) - 1u);
 
-    if (warp == 4) {
+    if (warp == SW) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
             for (int kt = 0; kt < NKT; ++kt) {
@@ -252,7 +274,7 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
                 }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == SW + 1) {
         // ---------------- MMA issuer (one lane): A = X hi / lo from TMEM, B = W hi / lo from shared memory ----
         if (lane == 0) {
             for (int kt = 0; kt < NKT; ++kt) {
@@ -282,8 +304,10 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
     } else {
         // ---------------- split X rows into TF32 hi / lo, straight into TMEM ----------------
         // thread = one X row (TMEM lane 32 warp + lane); its 128-byte row sits 16-byte-chunk-swizzled in smem
-        const uint32_t r = warp * 32 + lane;
-        const uint32_t lane_cols = (warp * 32u) << 16;
+        const uint32_t rq = warp & 3u, hh = warp >> 2;  // TMEM lane quarter; which NCH chunks of the row
+        const uint32_t r = rq * 32 + lane;
+        const uint32_t lane_cols = (rq * 32u) << 16;
+        const uint32_t c0 = hh * NCH;
         // GATHER: this row's K slice kt = 32 floats of stencil segment s = 32 kt / 2t (2t is a multiple of 32)
         constexpr int GD = TC_STAGES - 1;  // slices gathered ahead
         const uint32_t gb = m0 + r;
@@ -294,7 +318,7 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
             const float *src = xs + (ok ? (size_t)k * 2 * T + off : 0);
             const uint32_t dst = ring + (uint32_t)(kt % TC_STAGES) * STAGE_BYTES + r * 128;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) cp_async16_zfill(dst + 16 * c, src + 4 * c, ok ? 16u : 0u);
+            for (int c = (int)c0; c < (int)c0 + NCH; ++c) cp_async16_zfill(dst + 16 * c, src + 4 * c, ok ? 16u : 0u);
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
         if constexpr (GATHER) {
@@ -315,26 +339,33 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
             }
             if (kt >= ASTAGES) mbar_wait(&tfree[a], (uint32_t)((kt / ASTAGES - 1) & 1));
             const unsigned char *row = ring_gen + s * STAGE_BYTES + r * 128;
-            uint32_t hi[32], lo[32];
+            uint32_t hi[4 * NCH], lo[4 * NCH];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
+            for (int j = 0; j < NCH; ++j) {
+                const uint32_t c = c0 + (uint32_t)j;
                 const float4 v = *reinterpret_cast<const float4 *>(row + ((GATHER ? c : (c ^ (r & 7))) << 4));
                 const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const float h = tf32_rn(e[q]);
-                    hi[4 * c + q] = __float_as_uint(h);
-                    lo[4 * c + q] = __float_as_uint(__fsub_rn(e[q], h));
+                    hi[4 * j + q] = __float_as_uint(h);
+                    lo[4 * j + q] = __float_as_uint(__fsub_rn(e[q], h));
                 }
             }
-            const uint32_t ta = tmem + lane_cols + ACOL + (uint32_t)a * (2 * TC_BK);
-            tmem_st32(ta, hi);
-            tmem_st32(ta + TC_BK, lo);
+            const uint32_t ta = tmem + lane_cols + ACOL + (uint32_t)a * (2 * TC_BK) + 4 * c0;
+            if constexpr (NCH == 8) {
+                tmem_st32(ta, hi);
+                tmem_st32(ta + TC_BK, lo);
+            } else {
+                tmem_st16(ta, hi);
+                tmem_st16(ta + TC_BK, lo);
+            }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(&tsplit[a]);
         }
-        // ---------------- epilogue: TMEM -> registers -> y in input order ----------------
+        // ---------------- epilogue: TMEM -> registers -> y in input order (lane quarters: warps 0..3) ----------------
+        if (hh == 0) {
         mbar_wait(&accum, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t b = m0 + r;  // this thread's TMEM lane = box
@@ -393,6 +424,7 @@ __global__ void __launch_bounds__(TC_THREADS, T == 16 ? 2 : 1)
                     for (int i = 0; i < 32; ++i) y[perm[s0 + c0 + i]] = make_float2(re[i], im[i]);
                 }
             }
+        }
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     }
@@ -455,7 +487,7 @@ p2p_status launch_tc(p2p_plan *P, void *y) {
     if constexpr (CL > 1) {
         cudaLaunchConfig_t lc{};
         lc.gridDim = dim3(grid);
-        lc.blockDim = dim3(TC_THREADS);
+        lc.blockDim = dim3(tc_threads<T>());
         lc.dynamicSmemBytes = (size_t)smem;
         lc.stream = P->stream;
         cudaLaunchAttribute at[1];
@@ -470,7 +502,7 @@ p2p_status launch_tc(p2p_plan *P, void *y) {
                                         (const float *)P->rec, (const uint32_t *)P->nbr_box));
         g_launches.fetch_add(1, std::memory_order_relaxed);
     } else {
-        P2P_LAUNCH(kern, grid, TC_THREADS, smem, P->stream, mx, mwh, mwl, rf, P->bstart, P->perm, (uint32_t)P->B,
+        P2P_LAUNCH(kern, grid, tc_threads<T>(), smem, P->stream, mx, mwh, mwl, rf, P->bstart, P->perm, (uint32_t)P->B,
                    (float2 *)y, (const float *)P->rec, P->nbr_box);
     }
     P2P_CUDA_TRY(cudaGetLastError());
