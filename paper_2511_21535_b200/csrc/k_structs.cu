@@ -401,7 +401,10 @@ struct NbTile {
     unsigned long long v[NB_TOT];
 };
 
-__global__ void __launch_bounds__(NB_THREADS) k_nbr_count(Geom g, const uint32_t *__restrict__ bkey,
+#ifndef P2P_NC_MINB
+#define P2P_NC_MINB 4  // (an explicit 1 let ptxas take 90 registers: 237 vs 136 us on c5w)
+#endif
+__global__ void __launch_bounds__(NB_THREADS, P2P_NC_MINB) k_nbr_count(Geom g, const uint32_t *__restrict__ bkey,
                                                           const uint32_t *__restrict__ bstart,
                                                           const uint2 *__restrict__ boxinfo,
                                                           const uint32_t *__restrict__ occ, DevCounters *ctr,
