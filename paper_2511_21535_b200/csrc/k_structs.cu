@@ -33,8 +33,11 @@ __device__ __forceinline__ double floor_div_exact(double a, double h, double inv
 // gather touches ONE 16-byte record per particle instead of a position and a mass in two arrays (two DRAM bursts)
 // The a2 sort's digit histograms are built here too (the keys are in registers; the sort's own histogram pass
 // re-read 50 MB at c5w), and its first pass takes the input positions as values (no iota array written / read).
+#ifndef P2P_BIN_MINB
+#define P2P_BIN_MINB 0  // 0: no register cap
+#endif
 template <typename T, typename V4>
-__global__ void __launch_bounds__(256) k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geom g,
+__global__ void __launch_bounds__(256, P2P_BIN_MINB) k_bin_gravity(const T *__restrict__ pos, int ps, uint32_t n, Geom g,
                                                      uint32_t *__restrict__ key, DevCounters *ctr,
                                                      const T *__restrict__ q, V4 *__restrict__ aos, int passes,
                                                      uint32_t *__restrict__ hist) {
