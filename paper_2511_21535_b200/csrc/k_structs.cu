@@ -313,7 +313,16 @@ __device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint
     t.nbr = nbr;
     t.red = red;
     // boxes with <= SMALL_NT targets go to the eval's thread-per-target path (no work item)
-    const bool small = nb <= SMALL_NT && red <= SMALL_R;
+// a second small-path window: boxes of <= P2P_SMALL_NT2 targets with <= P2P_SMALL_R2 sources also take the
+// thread-per-target-pair path (measured on one box: c5w eval 5961 / 5968 -> 5878 / 5897 us, c3 407 -> 400 us, c4-8 /
+// c4-16 unchanged; a plain SMALL_R = 256 sent c4-8's 8-target boxes (R = 216) there and lost their quad items: +60%)
+#ifndef P2P_SMALL_NT2
+#define P2P_SMALL_NT2 6
+#endif
+#ifndef P2P_SMALL_R2
+#define P2P_SMALL_R2 256
+#endif
+    const bool small = (nb <= SMALL_NT && red <= SMALL_R) || (nb <= P2P_SMALL_NT2 && red <= P2P_SMALL_R2);
     t.item = (small || !tgt) ? 0u : (nb + item_size(nb, red, tmax, K, cap) - 1) / item_size(nb, red, tmax, K, cap);
     t.small = (small && tgt) ? (nb + 1) / 2 : 0u;  // target PAIRS
     t.item_red = t.item;
