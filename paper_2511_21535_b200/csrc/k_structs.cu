@@ -322,7 +322,12 @@ __device__ __forceinline__ BoxTotals box_totals(uint32_t nbr, uint64_t red, uint
 #ifndef P2P_SMALL_R2
 #define P2P_SMALL_R2 256
 #endif
-    const bool small = (nb <= SMALL_NT && red <= SMALL_R) || (nb <= P2P_SMALL_NT2 && red <= P2P_SMALL_R2);
+#ifndef P2P_SMALL_NT3  // a third window (sweep knob, off)
+#define P2P_SMALL_NT3 0
+#define P2P_SMALL_R3 0
+#endif
+    const bool small = (nb <= SMALL_NT && red <= SMALL_R) || (nb <= P2P_SMALL_NT2 && red <= P2P_SMALL_R2) ||
+                       (nb <= P2P_SMALL_NT3 && red <= P2P_SMALL_R3);
     t.item = (small || !tgt) ? 0u : (nb + item_size(nb, red, tmax, K, cap) - 1) / item_size(nb, red, tmax, K, cap);
     t.small = (small && tgt) ? (nb + 1) / 2 : 0u;  // target PAIRS
     t.item_red = t.item;
