@@ -406,7 +406,11 @@ p2p_status restructure_gravity(p2p_plan *P) {
     if (P->sizes_known && (P->B == 0 || P->n_nbr == 0)) return P2P_OK;
     // one warp per chunk of 32 CSR entries; the chunk count is device-side after an asynchronous update
     const uint64_t nchunk = div_up(P->sizes_known ? (uint64_t)P->n_nbr : 27ull * (uint64_t)P->bcap, 32);
-    const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(div_up(nchunk * 32, 256), (unsigned)P->num_sms * 16));
+#ifndef P2P_RS_CTAS_PER_SM
+#define P2P_RS_CTAS_PER_SM 16
+#endif
+    const unsigned grid =
+        std::max<unsigned>(1, std::min<unsigned>(div_up(nchunk * 32, 256), (unsigned)P->num_sms * P2P_RS_CTAS_PER_SM));
     static const bool legacy = [] {
         // the pipelined kernel (rsp::k_restructure_pipe) measured SLOWER than the chunk kernel on every workload
         // (c5w 1.38 vs 1.18 ms, c4-8 1.23 vs 1.11, c3 0.126 vs 0.097: ncu -- long-scoreboard stalls 46% -> 13%,
