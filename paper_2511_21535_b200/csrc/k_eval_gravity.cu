@@ -18,7 +18,7 @@
 //     2-stage producer/consumer pipeline: while it computes chunk c from one shared-memory stage, the bulk
 //     copies of chunk c+1 -- or of the next item's first chunk AND its targets (REDUNDANT: already rebased,
 //     from the box's own segment of its run) -- land in the other stage (mbarrier + expect_tx completion).
-//     Boxes with <= 8 targets and <= 128 sources take a thread-per-target-pair path instead (one warp per CTA
+//     Boxes with <= 8 targets and <= 128 sources (or <= 6 and <= 256) take a thread-per-target-pair path instead (one warp per CTA
 //     starts with them, so their load latency hides behind the other warps' item work).
 //   * targets live in registers: lane (g, s) holds K targets (group g) and walks the staged sources
 //     j = s, s+S, ... (S source splits, G groups; S, G precomputed per item by k_nbr_fill), so boxes of any
