@@ -14,10 +14,10 @@
 // in shared memory after each TMA load (hi in place, lo into a second buffer with the same swizzled offsets).
 //
 // Kernel: one CTA per 128 boxes (M = 128), all N = 2t outputs in one TMEM accumulator (N fp32 columns).
-//   warp 4, one lane      TMA producer: 2D tensor loads (128-byte swizzle) of the X tile and both W tiles of
+//   warp SW, one lane     TMA producer: 2D tensor loads (128-byte swizzle) of the X tile and both W tiles of
 //                         each 32-float K slice into a 3-stage ring (mbarrier full / empty)
-//   warps 0..3            split X of each landed slice (mbarrier split, 128 arrivals)
-//   warp 5, one lane      MMA issuer: 4 K-steps x 3 tcgen05.mma per slice (kind::tf32, M = 128, N = 2t, K = 8,
+//   warps 0..SW-1         split X of each landed slice (mbarrier split, 32 SW arrivals; SW = 4, or 8 at t = 64)
+//   warp SW+1, one lane   MMA issuer: 4 K-steps x 3 tcgen05.mma per slice (kind::tf32, M = 128, N = 2t, K = 8,
 //                         both operands K-major from shared memory descriptors), committed to the stage's empty
 //                         barrier (and, after the last slice, to the accumulator barrier)
 //   epilogue (warps 0-3)  tcgen05.ld of the accumulator rows (TMEM lane = box), scatter to input order
@@ -42,7 +42,7 @@ namespace {
 constexpr int TC_BM = 128;        // boxes per CTA (MMA M, TMEM lanes)
 constexpr int TC_BK = 32;         // floats per K slice = one 128-byte swizzle row
 constexpr int TC_STAGES = 4;      // smem ring of X + W hi + W lo slices (48 KB each at t = 64)
-constexpr int TC_THREADS = 192;   // 4 split / epilogue warps + 1 TMA producer warp + 1 MMA issuer warp
+// threads per CTA: split / epilogue warps (4 at t = 16, 8 at t = 64) + 1 TMA producer warp + 1 MMA issuer warp
 // split warps per CTA (P2P_HELM_SPLITW, t = 64): the X split into TF32 hi / lo (smem -> registers -> tcgen05.st) paces
 // the kernel, so at t = 64 (one CTA per SM) 8 warps split, two per TMEM lane quarter, 16 of a slice's 32 columns each
 #ifndef P2P_HELM_SPLITW
