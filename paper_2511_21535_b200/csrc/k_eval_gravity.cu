@@ -44,7 +44,10 @@ template <typename T> struct V4T;
 template <> struct V4T<float> { using type = float4; };
 template <> struct V4T<double> { using type = double4; };
 
-constexpr int EV_WARPS = 4;              // warps per CTA
+#ifndef P2P_EV_WARPS
+#define P2P_EV_WARPS 4
+#endif
+constexpr int EV_WARPS = P2P_EV_WARPS;   // warps per CTA (x 5 CTAs per SM for the fp32 REDUNDANT kernel: 20 warps)
 constexpr int EV_STAGE_BYTES = 4096;     // source records per pipeline stage per warp (256 fp32 / 128 fp64)
 constexpr int EV_TGT = 32;               // max targets per item (ITEM_TMAX in k_structs.cu)
 // work-item records are prefetched through cp.async into a per-warp shared slot (P2P_ITEM_REGS: into registers,
@@ -494,7 +497,7 @@ __device__ __forceinline__ void small_phase(const EvalArgs<T> &a, unsigned lane)
 // boundary flags come from a.lframe instead of the uniform grid's box coordinates, and a leaf may list more than 32
 // neighbour segments (the lane-per-segment registers then cover groups of 32, re-read from the CSR per chunk)
 template <typename T, int LAYOUT, int K, bool ADAPT = false, bool PEER = false>
-__global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 4 : (LAYOUT == P2P_REDUNDANT ? 5 : 4)) : 1) k_eval_gravity(const EvalArgs<T> a) {
+__global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 16 : (LAYOUT == P2P_REDUNDANT ? 20 : 16)) / EV_WARPS : 1) k_eval_gravity(const EvalArgs<T> a) {
     using V4 = typename V4T<T>::type;
     constexpr int CH = EV_STAGE_BYTES / (int)sizeof(V4);
     constexpr int STAGE_RECS = CH + EV_TGT;  // source chunk + the item's targets
