@@ -47,7 +47,10 @@ __global__ void __launch_bounds__(256, P2P_BIN_MINB) k_bin_gravity(const T *__re
     const double inv_h = 1.0 / g.h;
     // BIN_U particles per thread per iteration, every load issued before the first use (memory-level parallelism:
     // one particle per iteration left the kernel at 0.55 of HBM with 67% warps active)
-    constexpr int BIN_U = 4;
+#ifndef P2P_BIN_U
+#define P2P_BIN_U 4
+#endif
+    constexpr int BIN_U = P2P_BIN_U;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t i0 = blockIdx.x * blockDim.x * BIN_U + threadIdx.x; i0 < n; i0 += stride * BIN_U) {
         T xd[BIN_U][3], qm[BIN_U];
@@ -145,10 +148,13 @@ __device__ __forceinline__ void st_stream(double4 *p, const double4 &v) {
     __stcs(reinterpret_cast<double2 *>(p), make_double2(v.x, v.y));
     __stcs(reinterpret_cast<double2 *>(p) + 1, make_double2(v.z, v.w));
 }
+#ifndef P2P_PERM_U
+#define P2P_PERM_U 4
+#endif
 template <typename V4>
 __global__ void k_permute_gravity(const V4 *__restrict__ src, const uint32_t *__restrict__ perm, uint32_t n,
                                   V4 *__restrict__ rec) {
-    constexpr int U = 4;
+    constexpr int U = P2P_PERM_U;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += U * stride) {
         uint32_t i[U];
