@@ -49,6 +49,9 @@ __device__ __forceinline__ void st_cs(double4 *p, const double4 &v) {
     __stcs(reinterpret_cast<double2 *>(p) + 1, make_double2(v.z, v.w));
 }
 
+#ifndef P2P_RS_PACKED
+#define P2P_RS_PACKED 1
+#endif
 template <typename T, bool EXACT32>
 __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint32_t B, uint32_t n_nbr, uint32_t ch,
                                           uint32_t b0, unsigned long long gout, uint32_t n_k, uint32_t n_slot,
@@ -145,8 +148,17 @@ __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint3
                 const uint32_t r = r0 + lane;
                 if (r < Rc) {
                     V4 v;
+#if P2P_RS_PACKED
+                    // x, y as one FP32x2 pair (FADD2): fl(fl(x + 0) + (-o)) == fl(fl(x + 0) - o) bit for bit
+                    const float2 xy = __fadd2_rn(__fadd2_rn(make_float2((float)x[u].x, (float)x[u].y),
+                                                            make_float2(0.0f, 0.0f)),
+                                                 make_float2(-eo0, -eo1));
+                    v.x = (T)xy.x;
+                    v.y = (T)xy.y;
+#else
                     v.x = (T)__fsub_rn(__fadd_rn((float)x[u].x, 0.0f), eo0);
                     v.y = (T)__fsub_rn(__fadd_rn((float)x[u].y, 0.0f), eo1);
+#endif
                     v.z = (T)__fsub_rn(__fadd_rn((float)x[u].z, 0.0f), eo2);
                     v.w = x[u].w;
                     st_cs(out + r, v);
