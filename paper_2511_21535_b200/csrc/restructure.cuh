@@ -52,6 +52,9 @@ __device__ __forceinline__ void st_cs(double4 *p, const double4 &v) {
 #ifndef P2P_RS_PACKED
 #define P2P_RS_PACKED 1
 #endif
+#ifndef P2P_RS_ONESHFL
+#define P2P_RS_ONESHFL 1
+#endif
 template <typename T, bool EXACT32>
 __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint32_t B, uint32_t n_nbr, uint32_t ch,
                                           uint32_t b0, unsigned long long gout, uint32_t n_k, uint32_t n_slot,
@@ -101,6 +104,7 @@ __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint3
         if (lane >= (unsigned)o) incl += y;
     }
     const uint32_t st = incl - cnt;
+    const uint32_t src_m_st = src - st;
     const uint32_t Rc = __shfl_sync(FULL, incl, 31);
     V4 *__restrict__ out = p.red + gout;
     const uint32_t le = lane == 31 ? FULL : ((2u << lane) - 1u);
@@ -132,10 +136,15 @@ __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint3
             const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
             const uint32_t starts = __reduce_or_sync(FULL, in_win);
             xe[u] = (before - 1u + __popc(starts & le)) & 31u;
-            const uint32_t e_src = __shfl_sync(FULL, src, xe[u]);
-            const uint32_t e_st = __shfl_sync(FULL, st, xe[u]);
+            // one shuffle: the entry's (source start - run offset), so record r of the window is rec[sd + r]
+            // (mod 2^32 arithmetic: sd may wrap, the sum never exceeds the record count)
+#if P2P_RS_ONESHFL
+            const uint32_t sd = __shfl_sync(FULL, src_m_st, xe[u]);
+#else
+            const uint32_t sd = __shfl_sync(FULL, src, xe[u]) - __shfl_sync(FULL, st, xe[u]);
+#endif
             const uint32_t r = r0 + lane;
-            if (r < Rc) x[u] = p.rec[e_src + (r - e_st)];
+            if (r < Rc) x[u] = p.rec[sd + r];
         }
         if (fast32) {
 #pragma unroll
