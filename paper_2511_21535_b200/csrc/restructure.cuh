@@ -55,6 +55,9 @@ __device__ __forceinline__ void st_cs(double4 *p, const double4 &v) {
 #ifndef P2P_RS_ONESHFL
 #define P2P_RS_ONESHFL 1
 #endif
+#ifndef P2P_RS_SENT
+#define P2P_RS_SENT 1
+#endif
 template <typename T, bool EXACT32>
 __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint32_t B, uint32_t n_nbr, uint32_t ch,
                                           uint32_t b0, unsigned long long gout, uint32_t n_k, uint32_t n_slot,
@@ -105,6 +108,7 @@ __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint3
     }
     const uint32_t st = incl - cnt;
     const uint32_t src_m_st = src - st;
+    const uint32_t stS = seg ? st : 0xffffffffu;
     const uint32_t Rc = __shfl_sync(FULL, incl, 31);
     V4 *__restrict__ out = p.red + gout;
     const uint32_t le = lane == 31 ? FULL : ((2u << lane) - 1u);
@@ -132,10 +136,20 @@ __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint3
             if (r0 >= Rc) break;  // warp-uniform: short ranges skip the empty windows
             // segment of record r0 + lane without a search (segments are non-empty and contiguous):
             // segments starting before r0 (ballot) - 1 + segment starts in [r0, r0 + lane] (OR-reduced mask)
+#if P2P_RS_SENT
+            // stS = st, or ~0 for lanes past the CSR end: no per-window "seg &&"; the entry index is always in
+            // [0, 31] (segments are contiguous from record 0), so no mask either
+            const uint32_t before = __popc(__ballot_sync(FULL, stS < r0));
+            const uint32_t d0 = stS - r0;
+            const uint32_t in_win = d0 < 32u ? (1u << d0) : 0u;
+            const uint32_t starts = __reduce_or_sync(FULL, in_win);
+            xe[u] = before - 1u + __popc(starts & le);
+#else
             const uint32_t before = __popc(__ballot_sync(FULL, seg && st < r0));
             const uint32_t in_win = (seg && st >= r0 && st < r0 + 32) ? (1u << (st - r0)) : 0u;
             const uint32_t starts = __reduce_or_sync(FULL, in_win);
             xe[u] = (before - 1u + __popc(starts & le)) & 31u;
+#endif
             // one shuffle: the entry's (source start - run offset), so record r of the window is rec[sd + r]
             // (mod 2^32 arithmetic: sd may wrap, the sum never exceeds the record count)
 #if P2P_RS_ONESHFL
