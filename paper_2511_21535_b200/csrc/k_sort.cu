@@ -88,9 +88,24 @@ __global__ void __launch_bounds__(256) k_radix_hist_scan(uint32_t *hist) {
 // lanes of `mask` whose 8-bit digit equals this lane's: bit-sliced, 8 ballots (default).  __match_any_sync
 // (P2P_SORT_MATCH=1) costs one pass per DISTINCT value in the warp on sm_100a: ~28 on uniform digits, so the
 // histogram kernel ran at 0.55 TB/s on passes 0-1 and 1.0 TB/s on the skewed top digit (ncu, gpurun_out/sort)
+#ifndef P2P_SORT_XORPEERS
+#define P2P_SORT_XORPEERS 1
+#endif
 __device__ __forceinline__ uint32_t digit_peers(uint32_t mask, uint32_t d) {
 #if defined(P2P_SORT_MATCH) && P2P_SORT_MATCH
     return __match_any_sync(mask, d);
+#else
+#if P2P_SORT_XORPEERS
+    // lanes whose digit differs from this lane's in any bit: OR over the bits of (ballot XOR my-bit-broadcast);
+    // the bit sits in the sign of (d << (31 - b)), which gives both the ballot predicate and the broadcast mask
+    uint32_t diff = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const int32_t sb = (int32_t)(d << (31 - b));
+        const uint32_t bb = __ballot_sync(mask, sb < 0);
+        diff |= bb ^ (uint32_t)(sb >> 31);
+    }
+    return mask & ~diff;
 #else
     uint32_t peers = mask;
 #pragma unroll
@@ -100,6 +115,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t mask, uint32_t d) {
         peers &= one ? bb : ~bb;
     }
     return peers;
+#endif
 #endif
 }
 
