@@ -417,6 +417,36 @@ __device__ __forceinline__ BoxTotals block_scan_totals(BoxTotals x, BoxTotals *t
     return x;
 }
 
+// block-wide sums of the totals (k_nbr_count needs only the tile sums, not the per-box prefixes): warp reductions
+// (REDUX for the 32-bit fields), then warp 0
+__device__ __forceinline__ BoxTotals block_sum_totals(const BoxTotals &x) {
+    __shared__ BoxTotals s_w[NB_THREADS / 32];
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    BoxTotals r;
+    r.nbr = __reduce_add_sync(0xffffffffu, x.nbr);
+    r.item = __reduce_add_sync(0xffffffffu, x.item);
+    r.small = __reduce_add_sync(0xffffffffu, x.small);
+    r.item_red = __reduce_add_sync(0xffffffffu, x.item_red);
+    unsigned long long red = x.red;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) red += __shfl_xor_sync(0xffffffffu, red, o);
+    r.red = red;
+    if (lane == 0) s_w[w] = r;
+    __syncthreads();
+    BoxTotals t{0, 0, 0, 0, 0ull};
+#pragma unroll
+    for (int i = 0; i < NB_THREADS / 32; ++i) {
+        const BoxTotals v = s_w[i];
+        t.nbr += v.nbr;
+        t.item += v.item;
+        t.small += v.small;
+        t.item_red += v.item_red;
+        t.red += v.red;
+    }
+    __syncthreads();
+    return t;
+}
+
 // tile sums / exclusive tile offsets: [0] CSR entries, [1] redundant records, [2] work items, [3] small pairs,
 // [4] REDUNDANT-eval work items (multi-box quads)
 constexpr int NB_TOT = 5;
@@ -464,8 +494,15 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NC_MINB) k_nbr_count(Geom g, c
         if (have) box_nbr[b] = make_uint2(okm | (elig ? MB_ELIG : 0u), (uint32_t)red);
         if (elig) mb_cen[b] = (uint32_t)(red0 + part4);
         pairs += (unsigned long long)(tgt ? nb : 0u) * red;
+#ifndef P2P_NC_REDUCE
+#define P2P_NC_REDUCE 1
+#endif
+#if P2P_NC_REDUCE
+        const BoxTotals tot = block_sum_totals(x);
+#else
         BoxTotals tot;
         block_scan_totals(x, &tot);
+#endif
         if (threadIdx.x == 0) tiles[tile] = NbTile{{tot.nbr, tot.red, tot.item, tot.small, 0ull}};
     }
 #pragma unroll
