@@ -309,6 +309,9 @@ __device__ __forceinline__ void nb_plane(const NbStencil &S, int dz, uint32_t ke
     }
 }
 
+__constant__ uint8_t c_div32[33] = {0,  32, 16, 10, 8, 6, 5, 4, 4, 3, 3, 2, 2, 2, 2, 2, 2,
+                                     1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};  // 32 / g
+
 struct BoxTotals {
     uint32_t nbr, item, small, item_red;  // item_red: the REDUNDANT eval's items (multi-box quads, see mb_role)
     unsigned long long red;
@@ -706,7 +709,8 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
                 for (uint32_t ci = 0; ci < nch; ++ci) {
                     const uint32_t a0 = ci * sz, z0 = min(nb, (ci + 1) * sz);
                     // eval lane layout: G = ceil(n_t / K) groups of K targets, S = floor(32 / G) source splits
-                    const uint32_t nt = z0 - a0, Gq = (nt + K - 1) / K, Sq = 32u / Gq;
+                    // K is a power of two; Gq <= 32 / K: 32 / Gq from a table (no integer divisions per item)
+                    const uint32_t nt = z0 - a0, Gq = (nt + K - 1) >> (__ffs(K) - 1), Sq = c_div32[Gq];
                     // bit 24: the box belongs to a multi-box quad of the REDUNDANT list -- P2P_INDEXED_BITWISE then
                     // evaluates it with the quad's S = 4 splits, so its bits still equal the REDUNDANT eval's
                     const Item itm{b, s0 + a0, nt | (Sq << 8) | (Gq << 16) | (quad ? 1u << 24 : 0u), key, rb,
