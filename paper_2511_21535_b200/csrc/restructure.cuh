@@ -58,6 +58,9 @@ __device__ __forceinline__ void st_cs(double4 *p, const double4 &v) {
 #ifndef P2P_RS_SENT
 #define P2P_RS_SENT 1
 #endif
+#ifndef P2P_RS_ICODE
+#define P2P_RS_ICODE 1
+#endif
 template <typename T, bool EXACT32>
 __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint32_t B, uint32_t n_nbr, uint32_t ch,
                                           uint32_t b0, unsigned long long gout, uint32_t n_k, uint32_t n_slot,
@@ -94,11 +97,22 @@ __device__ __forceinline__ uint32_t chunk(const Geom &g, const Ptrs<T> &p, uint3
     const double o2 = __fma_rn((double)c[2], g.h, g.lo[2]);
     // image code of the entry's slot (2 bits per dim: 1 = +L, 2 = -L), once per segment
     uint32_t code = 0;
+#if P2P_RS_ICODE
+    {  // integer form of slot_shift's sign (L > 0): +L past the upper face, -L past the lower
+        const int so[3] = {(int)(slot % 3u) - 1, (int)((slot / 3u) % 3u) - 1, (int)(slot / 9u) - 1};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const int v = (int)c[d] + so[d];
+            code |= (v >= g.nbox[d] ? 1u : (v < 0 ? 2u : 0u)) << (2 * d);
+        }
+    }
+#else
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         const double S = slot_shift(g, c, (int)slot, d);
         code |= (S > 0.0 ? 1u : (S < 0.0 ? 2u : 0u)) << (2 * d);
     }
+#endif
     // segments of consecutive CSR entries are consecutive in red[]: one contiguous output range per chunk
     uint32_t incl = cnt;
 #pragma unroll
