@@ -584,6 +584,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_tile_scan(const NbTile *__restri
     if (q < ntiles) excl[q] = e;
 }
 
+#ifndef P2P_NB_SLOT4
+#define P2P_NB_SLOT4 1
+#endif
 #ifndef P2P_NB_MINB
 #define P2P_NB_MINB 3
 #endif
@@ -723,10 +726,24 @@ __global__ void __launch_bounds__(NB_THREADS, P2P_NB_MINB) k_nbr_fill(
         __syncthreads();
         // coalesced copy of the tile's CSR run
         const uint32_t base = (uint32_t)to.v[0];
-        for (uint32_t j = threadIdx.x; j < tot.nbr; j += NB_THREADS) {
-            nbr_box[base + j] = s_box[j];
-            nbr_slot[base + j] = s_slot[j];
+        for (uint32_t j = threadIdx.x; j < tot.nbr; j += NB_THREADS) nbr_box[base + j] = s_box[j];
+#if P2P_NB_SLOT4
+        {  // the slot bytes four at a time (32-bit stores from the first 4-byte boundary; byte stores at the ends)
+            const uint32_t head = min(tot.nbr, (4u - (base & 3u)) & 3u);
+            if (threadIdx.x < head) nbr_slot[base + threadIdx.x] = s_slot[threadIdx.x];
+            const uint32_t nw = (tot.nbr - head) >> 2;
+            uint32_t *dst = reinterpret_cast<uint32_t *>(nbr_slot + base + head);
+            for (uint32_t q = threadIdx.x; q < nw; q += NB_THREADS) {
+                const uint32_t j = head + 4 * q;
+                dst[q] = (uint32_t)s_slot[j] | ((uint32_t)s_slot[j + 1] << 8) | ((uint32_t)s_slot[j + 2] << 16) |
+                         ((uint32_t)s_slot[j + 3] << 24);
+            }
+            const uint32_t tail0 = head + 4 * nw;
+            if (tail0 + threadIdx.x < tot.nbr) nbr_slot[base + tail0 + threadIdx.x] = s_slot[tail0 + threadIdx.x];
         }
+#else
+        for (uint32_t j = threadIdx.x; j < tot.nbr; j += NB_THREADS) nbr_slot[base + j] = s_slot[j];
+#endif
         __syncthreads();
     }
 }
