@@ -206,6 +206,56 @@ struct HeadPut {
     }
 };
 
+// gravity run heads with vectorised key loads: thread t holds keys i0 .. i0 + 7 (i0 = tile + 8 t) in registers from two
+// 16-byte loads plus its predecessor, instead of the generic scan's two scalar loads per element (HeadGet1)
+__device__ __forceinline__ uint32_t head_bits(const uint32_t *__restrict__ skey, uint32_t n, uint64_t i0,
+                                              uint32_t (&k)[8]) {
+    if (i0 + 8 <= n) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(skey + i0), b = *reinterpret_cast<const uint4 *>(skey + i0 + 4);
+        k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w; k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) k[i] = i0 + i < n ? skey[i0 + i] : 0u;
+    }
+    uint32_t prev = i0 > 0 && i0 < n ? skey[i0 - 1] : ~k[0];
+    uint32_t h = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (i0 + i < n && k[i] != prev) h |= 1u << i;
+        prev = k[i];
+    }
+    return h;
+}
+__global__ void __launch_bounds__(SC_THREADS) k_head_reduce(const uint32_t *__restrict__ skey, uint32_t n,
+                                                           uint32_t *__restrict__ partials) {
+    const uint64_t i0 = (uint64_t)blockIdx.x * SC_TILE + (uint64_t)threadIdx.x * SC_ITEMS;
+    uint32_t k[8];
+    const uint32_t h = i0 < n ? head_bits(skey, n, i0, k) : 0u;
+    uint32_t tot;
+    block_excl_scan<uint32_t>((uint32_t)__popc(h), &tot);
+    if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(SC_THREADS) k_head_down(const uint32_t *__restrict__ skey, uint32_t n,
+                                                         const uint32_t *__restrict__ partials,
+                                                         uint32_t *__restrict__ bkey, uint32_t *__restrict__ bstart) {
+    const uint64_t base = (uint64_t)blockIdx.x * SC_TILE;
+    if (base >= n) return;  // whole block beyond n: uniform exit
+    const uint64_t i0 = base + (uint64_t)threadIdx.x * SC_ITEMS;
+    uint32_t k[8];
+    const uint32_t h = i0 < n ? head_bits(skey, n, i0, k) : 0u;
+    uint32_t tot;
+    uint32_t e = block_excl_scan<uint32_t>((uint32_t)__popc(h), &tot) + partials[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if ((h >> i) & 1u) {
+            bkey[e] = k[i];
+            bstart[e] = (uint32_t)(i0 + i);
+            ++e;
+        }
+    }
+    if (i0 < n && i0 + 8 >= n) bstart[e] = n;  // the thread of the last element closes the table
+}
+
 // ------------------------------------------------------------------------------------------------ a5
 // dense key -> {box, n_b} table for the gravity neighbour search (valid where the occupancy bit is set)
 // + sum over the target boxes of n_b^2 (the item cost cap's work estimate; integer atomics: order-independent)
@@ -584,6 +634,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_tile_scan(const NbTile *__restri
     if (q < ntiles) excl[q] = e;
 }
 
+#ifndef P2P_HEADVEC
+#define P2P_HEADVEC 1
+#endif
 #ifndef P2P_NB_SLOT4
 #define P2P_NB_SLOT4 1
 #endif
@@ -907,9 +960,21 @@ p2p_status build_gravity_structs(p2p_plan *P, const void *pos, const void *q, co
     P2P_CUDA_TRY(cudaMemsetAsync(P->occ, 0, 4 * occ_words, st));
     // (a single-pass look-back variant, scan.cuh device_scan_lb, measured 124 vs 99 us on c5w: the 3052 tiles'
     // walks back over unpublished prefixes cost more than the second read of the keys)
+#if P2P_HEADVEC
+    if (n > 0) {
+        const unsigned nblk = div_up(n, SC_TILE);
+        uint32_t *parts = (uint32_t *)P->s_partials;
+        P2P_LAUNCH(k_head_reduce, nblk, SC_THREADS, 0, st, P->skey, n, parts);
+        P2P_LAUNCH((k_scan_partials<uint32_t>), 1, SC_THREADS, 0, st, parts, nblk, &P->ctr->B);
+        P2P_LAUNCH(k_head_down, nblk, SC_THREADS, 0, st, P->skey, n, parts, P->bkey, P->bstart);
+    } else {
+        P2P_CUDA_TRY(cudaMemsetAsync(&P->ctr->B, 0, sizeof(unsigned int), st));
+    }
+#else
     P2P_CUDA_TRY(device_scan<uint32_t>(HeadGet1{P->skey},
                                        HeadPut{P->skey, 1u, P->bkey, P->bstart, nullptr, n}, nullptr, n,
                                        &P->ctr->B, P->s_partials, st));
+#endif
     if (!grid_a5) return cudaGetLastError() == cudaSuccess ? P2P_OK : P2P_ERR_CUDA;  // adaptive mode: its own a5
     // a5
     const uint64_t bcap = (uint64_t)P->bcap;
