@@ -281,8 +281,16 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_restructure_pipe(const Geom g
 #ifndef P2P_RS_BATCH
 #define P2P_RS_BATCH 0
 #endif
+#ifndef P2P_RS_MINB
+#define P2P_RS_MINB 0  // 0: no register cap (ptxas picks 62)
+#endif
+#if P2P_RS_MINB > 0
+#define P2P_RS_LB __launch_bounds__(256, P2P_RS_MINB)
+#else
+#define P2P_RS_LB __launch_bounds__(256)
+#endif
 template <typename T, bool EXACT32>
-__global__ void __launch_bounds__(256) k_restructure_gravity(const Geom g, const rs::Ptrs<T> p,
+__global__ void P2P_RS_LB k_restructure_gravity(const Geom g, const rs::Ptrs<T> p,
                                                              const DevCounters *__restrict__ ctr) {
     // device-side counts: no host sync needed after an asynchronous p2p_plan_update
     const uint32_t B = ctr->B, n_nbr = ctr->n_nbr;
