@@ -56,7 +56,7 @@ constexpr int EV_TGT = 32;               // max targets per item (ITEM_TMAX in k
 #define P2P_ITEM_SMEM
 #endif
 #ifndef P2P_EV_BATCH
-#define P2P_EV_BATCH 2
+#define P2P_EV_BATCH 1  // 1 vs 2 vs 3 per atomic (profiles/r02_eval_options.txt): c4-8 -1.3%, c5w / c3 equal
 #endif
 constexpr int EV_BATCH = P2P_EV_BATCH;   // work items claimed per queue atomic
 
