@@ -711,7 +711,10 @@ __global__ void __launch_bounds__(EV_WARPS * 32, sizeof(T) == 4 ? (K == 8 ? 16 :
     // the small boxes' targets (thread per target, L1/L2-latency bound) are taken first by one warp of every
     // CTA, so their latency hides behind the FP32-bound item work of the CTA's other warps (run last by all
     // warps, they would form a latency-bound tail)
-    const bool small_first = w == EV_WARPS - 1;
+#ifndef P2P_SMALL_WARPS
+#define P2P_SMALL_WARPS 1  // warps per CTA that start on the small boxes
+#endif
+    const bool small_first = w >= EV_WARPS - P2P_SMALL_WARPS;
     if (small_first) small_phase<T, LAYOUT, PEER>(a, lane);
     if (lane == 0) pend = queue_claim(a.item_head, (uint32_t)EV_BATCH, a.zero);
     const uint32_t first = next_index();
