@@ -14,7 +14,7 @@
 //
 // B200 design (the paper's GTX 1050 thread-per-particle kernel is prior art, not the blueprint):
 //   * persistent CTAs (EV_WARPS warps each); every warp pulls work items (box, <= 32-target chunk; a 32-byte
-//     record prefetched one item ahead) from a global atomic queue (two items per atomic) and runs its own
+//     record prefetched one item ahead) from a global atomic queue (EV_BATCH = 1 item per atomic, claimed one item ahead) and runs its own
 //     2-stage producer/consumer pipeline: while it computes chunk c from one shared-memory stage, the bulk
 //     copies of chunk c+1 -- or of the next item's first chunk AND its targets (REDUNDANT: already rebased,
 //     from the box's own segment of its run) -- land in the other stage (mbarrier + expect_tx completion).
