@@ -15,7 +15,7 @@ namespace p2p {
 // ITEM_TMAX (plan.hpp): at most 32 targets per item -> G <= 8 groups of K = 4 (fp32)
 // The cap scales with the work: the dynamic queue's tail is bounded by its largest item, so a fixed 2^17-pair cap
 // left a 1e6-particle Plummer eval (c3, 6e8 pairs: 2e5 pairs per warp) waiting on single 2^17-pair items (SMs
-// active 81% of the kernel).  cap = pow2floor(I_est / (8 W)) clamped to [2^13, 2^17], I_est = 27 sum_b n_b^2 (the
+// active 81% of the kernel).  cap = pow2floor(I_est / (4 W)) clamped to [2^13, 2^17], I_est = 27 sum_b n_b^2 (the
 // pair count of a uniform periodic grid; ~25 sum n_b^2 on the Plummer inputs) over the TARGET boxes, W = a fixed
 // nominal eval warp count (148 SMs x 20) -- sum_nb2 is all-reduced over ranks, so every rank and a 1-GPU plan
 // derive the same cap and the same items (bitwise results independent of the GPU count).  c3 479 -> ~390 us;
@@ -27,9 +27,12 @@ constexpr uint64_t ITEM_COSTCAP = P2P_ITEM_COSTCAP;  // upper bound of the cap
 constexpr uint64_t ITEM_COSTCAP_MIN = 1ull << 13;
 constexpr uint64_t EVAL_WARPS_NOMINAL = 148 * 20;
 
-// cap = pow2floor(pairs / (8 W)) clamped to [ITEM_COSTCAP_MIN, ITEM_COSTCAP]
+// cap = pow2floor(pairs / (P2P_CAP_DIV W)) clamped to [ITEM_COSTCAP_MIN, ITEM_COSTCAP]
 __device__ __forceinline__ uint64_t item_costcap_of(uint64_t pairs) {
-    const uint64_t est = pairs / (8ull * EVAL_WARPS_NOMINAL);
+#ifndef P2P_CAP_DIV
+#define P2P_CAP_DIV 4  // items per nominal eval warp the cap aims at (8 / 2 / 1 / 16 measured: r02_eval_options.txt)
+#endif
+    const uint64_t est = pairs / ((uint64_t)P2P_CAP_DIV * EVAL_WARPS_NOMINAL);
     if (est >= ITEM_COSTCAP) return ITEM_COSTCAP;
     if (est <= ITEM_COSTCAP_MIN) return ITEM_COSTCAP_MIN;
     return 1ull << (63 - __clzll((long long)est));
